@@ -1,0 +1,283 @@
+"""Pins P7, P9-P17 for the oracle's IETI-DP solver.
+
+Independent references: the monolithic glued direct solve (P11, a plain LU of the
+same discrete system), the block 3x3 Euler system residual (P12), gauge invariance
+of curl-related quantities (P13), closed-form degenerate cases (P14), a manufactured
+exact discrete solution (P15) and manufactured-solution convergence rates of the
+paper's error measures (P16)."""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import workloads
+from oracle import assembly
+from oracle.ietidp import Oracle
+from oracle.monolithic import Monolithic
+from oracle.gauge import CLS_P, CLS_R
+
+SMALL = [
+    workloads.cfg1(),
+    workloads.custom((2, 2, 2), 2, (2, 2, 2), [0, 0, 0, 0, 0, 0, 0, 10.0], [1, 2, 3, 4, 5, 6, 7, 8], name="corner-conductor"),
+    workloads.custom((3, 3, 3), 1, (2, 2, 2), [1.0 if s == 13 else 0.0 for s in range(27)],
+                     np.linspace(0.5, 1.5, 27), name="floating-centre"),
+    workloads.custom((3, 2, 2), 2, (1, 2, 1), [1e3 if s % 3 == 0 else 0.0 for s in range(12)], [1.0], name="aniso"),
+    workloads.custom((2, 2, 1), 3, (2, 2, 2), [1e6, 0, 1e6, 0], [1e-3, 1, 1, 1e-2], name="contrast"),
+]
+
+
+def _o(pr, **kw):
+    for k, v in kw.items():
+        setattr(pr, k, v)
+    return Oracle(pr)
+
+
+@pytest.mark.parametrize("pr", SMALL, ids=lambda p: p.name)
+def test_spd_local_and_coarse(pr):
+    """P7: Cholesky of every W_rr, W_ii and S_pp succeeds (Oracle raises NotSPD otherwise)."""
+    o = _o(pr)
+    for s in range(pr.n_patches):
+        if o.Wrr_cf[s] is not None:
+            assert np.all(np.diag(o.Wrr_cf[s][0]) > 0)
+    if o.Spp_cf is not None:
+        assert np.all(np.diag(o.Spp_cf[0]) > 0)
+
+
+@pytest.mark.parametrize("scaling", [0, 1])
+def test_F_and_preconditioner_spd(scaling):
+    """P9 on cfg1 (112 x 112): F and M^-1 symmetric and positive definite; the
+    preconditioner improves the spectral condition number."""
+    o = _o(workloads.cfg1(), scaling=scaling)
+    F = o.dense_F()
+    Mi = o.dense_precond()
+    assert np.max(np.abs(F - F.T)) <= 1e-12 * np.max(np.abs(F))
+    assert np.max(np.abs(Mi - Mi.T)) <= 1e-12 * np.max(np.abs(Mi))
+    evF = np.linalg.eigvalsh(F)
+    assert evF.min() > 0
+    assert np.linalg.eigvalsh(Mi).min() > 0
+    ev = np.real(sla.eigvals(Mi @ F))
+    assert ev.min() > 0
+    assert ev.max() / ev.min() < evF.max() / evF.min()
+
+
+@pytest.mark.parametrize("pr", SMALL[:3], ids=lambda p: p.name)
+def test_local_solve_residual(pr):
+    """P10: W_rr block solves have residual <= 1e-12 on random right-hand sides."""
+    o = _o(pr)
+    rng = np.random.default_rng(5)
+    for s in range(pr.n_patches):
+        r = o.part.r_order(s)
+        Wrr = o.W(s)[np.ix_(r, r)]
+        b = rng.standard_normal(len(r))
+        x = sla.cho_solve(o.Wrr_cf[s], b)
+        assert np.linalg.norm(Wrr @ x - b) <= 1e-12 * np.linalg.norm(Wrr, 2) * np.linalg.norm(x)
+
+
+@pytest.mark.parametrize("pr", SMALL, ids=lambda p: p.name)
+def test_monolithic_agreement(pr):
+    """P11: every step, IETI-DP at rtol 1e-12 equals the glued direct solve to 1e-10
+    (1e-8, the BJ.ns parity bar, for the 1e6/1e-3 contrast case whose glued matrix
+    has condition number ~1e10)."""
+    pr.n_steps = 4
+    o = _o(pr, rtol=1e-12)
+    mono = Monolithic(o)
+    for _ in range(pr.n_steps):
+        o.step()
+        mono.step()
+        a, ref = o.coefficients(1), mono.coefficients()
+        tol = 1e-8 if pr.name == "contrast" else 1e-10
+        assert np.linalg.norm(a - ref) <= tol * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("pr", SMALL[:3], ids=lambda p: p.name)
+def test_euler_system_residual(pr):
+    """P12: after each step the torn 3x3 system holds: patch r-rows,
+    assembled primal rows and the jump B a_r = 0, relative residual <= 1e-8."""
+    pr.n_steps = 3
+    o = _o(pr)
+    pt = o.part
+    for _ in range(pr.n_steps):
+        a_old = [a.copy() for a in o.a]
+        o.step()
+        t = o.ell * o.dt
+        v = o.Bt(o.lam)
+        res_r, scale = 0.0, 0.0
+        prim = np.zeros(pt.nc)
+        for s in range(pr.n_patches):
+            f = o.M[s] @ a_old[s] / o.dt + o.source_factor(s, t) * o.jS[s]
+            W = o.W(s)
+            r, pl = pt.r_order(s), pt.p_loc[s]
+            rr = W[np.ix_(r, r)] @ o.a[s][r] + W[np.ix_(r, pl)] @ o.a[s][pl] + v[s] - f[r]
+            res_r = max(res_r, np.max(np.abs(rr), initial=0))
+            scale = max(scale, np.max(np.abs(f)))
+            np.add.at(prim, pt.p_grp[s], W[np.ix_(pl, r)] @ o.a[s][r] + W[np.ix_(pl, pl)] @ o.a[s][pl] - f[pl])
+        jump = o.Bj([o.a[s][pt.r_order(s)] for s in range(pr.n_patches)])
+        amax = max(np.max(np.abs(a)) for a in o.a)
+        assert res_r <= 1e-8 * scale
+        assert np.max(np.abs(prim), initial=0) <= 1e-8 * scale
+        assert np.max(np.abs(jump), initial=0) <= 1e-8 * amax
+
+
+@pytest.mark.parametrize("pr", SMALL[:4], ids=lambda p: p.name)
+def test_gauge_invariance(pr):
+    """P13: the two tie-break orders give different trees, identical conductor
+    coefficients and identical K_s a_s (curl-curl is blind to gradients), while the
+    gauged insulator coefficients differ (P:L49 gradient freedom).
+    The load is the discretely divergence-free j_s = K_s c_s (G^T j = 0 exactly); with
+    the quadrature load of the BJ source G^T j is only ~1e-5 relative (R18),
+    and the gauges then differ at that level (checked below with a loose bound)."""
+    import copy
+    pr.n_steps = 3
+    pr1 = copy.deepcopy(pr)
+    o0 = _o(pr, tree_order=0, rtol=1e-12)
+    o1 = _o(pr1, tree_order=1, rtol=1e-12)
+    assert not np.array_equal(o0.tree, o1.tree)
+    rng = np.random.default_rng(3)
+    c = rng.standard_normal(o0.topo.nedges)
+    c[o0.topo.cls == 0] = 0.0
+    load = [o0.K[s] @ c[o0.topo.l2g[s]] for s in range(pr.n_patches)]
+    for _ in range(pr.n_steps):
+        o0.step(load=load)
+        o1.step(load=load)
+    differ = False
+    for s in range(pr.n_patches):
+        Ka0, Ka1 = o0.K[s] @ o0.a[s], o1.K[s] @ o1.a[s]
+        assert np.linalg.norm(Ka0 - Ka1) <= 1e-9 * np.linalg.norm(Ka0)
+        if pr.sigma[s] > 0:
+            assert np.linalg.norm(o0.a[s] - o1.a[s]) <= 1e-9 * np.linalg.norm(o0.a[s])
+        elif np.linalg.norm(o0.a[s] - o1.a[s]) > 1e-3 * np.linalg.norm(o0.a[s]):
+            differ = True
+    assert differ
+    # BJ source: invariance only up to the discrete incompatibility of the quadrature load
+    b0 = _o(copy.deepcopy(pr), tree_order=0, rtol=1e-12).run()
+    b1 = _o(copy.deepcopy(pr), tree_order=1, rtol=1e-12).run()
+    Ka0 = np.concatenate([b0.K[s] @ b0.a[s] for s in range(pr.n_patches)])
+    Ka1 = np.concatenate([b1.K[s] @ b1.a[s] for s in range(pr.n_patches)])
+    assert np.linalg.norm(Ka0 - Ka1) <= 1e-3 * np.linalg.norm(Ka0)
+
+
+def test_single_conductor_patch_is_direct_euler():
+    """P14: one conductor patch -> no multipliers, 0 PCG iterations, and the result
+    is plain implicit Euler on the Dirichlet-reduced system."""
+    pr = workloads.custom((1, 1, 1), 2, (2, 2, 2), [5.0], [0.5], n_steps=3)
+    o = _o(pr).run()
+    assert o.iters == [0, 0, 0] and o.part.m == 0 and o.part.nc == 0
+    keep = o.part.r_order(0)
+    W = o.W(0)[np.ix_(keep, keep)]
+    a = np.zeros(o.topo.l2g.shape[1])
+    for ell in range(3):
+        t = (ell + 1) * o.dt
+        f = o.M[0] @ a / o.dt + math.sin(2 * math.pi * t) * o.jS[0]
+        a = np.zeros_like(a)
+        a[keep] = np.linalg.solve(W, f[keep])
+    assert np.linalg.norm(o.a[0] - a) <= 1e-12 * np.linalg.norm(a)
+
+
+def test_zero_source_and_linearity():
+    """P14: J = 0 -> zero solution with 0 iterations; doubling the load doubles A."""
+    pr = workloads.cfg1()
+    pr.n_steps = 2
+    pr.source = workloads.SOURCE_NONE
+    o = _o(pr).run()
+    assert o.iters == [0, 0] and not any(a.any() for a in o.a)
+    pr2 = workloads.cfg1()
+    o1 = _o(pr2)
+    o2 = Oracle(workloads.cfg1())
+    o1.step()
+    o2.step(load=[2.0 * o2.source_factor(s, o2.dt) * o2.jS[s] for s in range(8)])
+    a1, a2 = o1.coefficients(1), o2.coefficients(1)
+    assert np.linalg.norm(a2 - 2 * a1) <= 1e-9 * np.linalg.norm(a2)
+
+
+@pytest.mark.parametrize("pr", SMALL, ids=lambda p: p.name)
+def test_exact_discrete_solution(pr):
+    """P15: for a random glued c (zero on E), the load j := W^ c (one step from a=0)
+    makes c the exact discrete solution; IETI-DP must return it (no monolithic solve)."""
+    o = _o(pr, rtol=1e-12)
+    rng = np.random.default_rng(11)
+    c = rng.standard_normal(o.topo.nedges)
+    c[~np.isin(o.part.part, (CLS_R, CLS_P))] = 0.0
+    load = [o.W(s) @ c[o.topo.l2g[s]] for s in range(pr.n_patches)]
+    o.step(load=load)
+    got = o.coefficients(1)
+    assert np.linalg.norm(got - c) <= 1e-8 * np.linalg.norm(c)
+
+
+def test_determinism():
+    """P17: two runs are bitwise identical."""
+    a = _o(workloads.cfg1()).run(3)
+    b = _o(workloads.cfg1()).run(3)
+    assert np.array_equal(a.coefficients(0), b.coefficients(0)) and a.iters == b.iters
+
+
+# ---- P16: manufactured solution rates -------------------------------
+
+def _curlS(X, Y, Z):
+    pi = math.pi
+    sx, sy, sz = np.sin(pi * X), np.sin(pi * Y), np.sin(pi * Z)
+    cx, cy, cz = np.cos(pi * X), np.cos(pi * Y), np.cos(pi * Z)
+    return np.stack([pi * sx * (cy - cz), pi * sy * (cz - cx), pi * sz * (cx - cy)], 1)
+
+
+def _S(X, Y, Z):
+    pi = math.pi
+    return np.stack([np.sin(pi * Y) * np.sin(pi * Z), np.sin(pi * X) * np.sin(pi * Z), np.sin(pi * X) * np.sin(pi * Y)], 1)
+
+
+def _spaces(o, extra=3):
+    pr = o.prob
+    return [assembly.PatchSpace(pr.p, pr.elems, *o.patch_box(s), nq=pr.p + extra) for s in range(pr.n_patches)]
+
+
+def _err_B(o, sps, t):
+    """Relative ||B(t) - curl A_h||_{L2(Omega)} with B = (1-e^-t) curl S."""
+    e2 = n2 = 0.0
+    for s, sp in enumerate(sps):
+        for el in sp.elements():
+            ids, val, cur, (X, Y, Z), W = sp.element_values(*el)
+            Bh = np.einsum("a,qac->qc", o.a[s][ids], cur)
+            Be = (1 - math.exp(-t)) * _curlS(X, Y, Z)
+            e2 += np.sum(W[:, None] * (Bh - Be) ** 2)
+            n2 += np.sum(W[:, None] * Be ** 2)
+    return math.sqrt(e2 / n2)
+
+
+@pytest.mark.parametrize("p,expect", [(1, 1.0), (2, 2.0)])
+def test_mms_space_rate(p, expect):
+    """epsilon_B = O(h^p): two-subdomain cube (C: x<0.5), one short step so
+    the time error is negligible; observed order within 0.3 of p."""
+    errs = []
+    for d in (1, 2, 4):
+        pr = workloads.custom((2, 1, 1), p, (d, 2 * d, 2 * d), [1.0, 0.0], [1.0, 1.0], n_steps=1, T=0.01,
+                              source=workloads.SOURCE_MMS)
+        o = Oracle(pr).run()
+        errs.append(_err_B(o, _spaces(o), pr.T))
+    rates = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert abs(rates[-1] - expect) <= 0.3, (errs, rates)
+
+
+def test_mms_time_rate():
+    """epsilon_E = O(n_t^-1) with the paper's backward-difference measure on
+    Omega_C; p=3, fine space; observed order in n_t within 0.15 of 1."""
+    errs = []
+    for nt in (4, 8, 16):
+        pr = workloads.custom((2, 1, 1), 3, (1, 2, 2), [1.0, 0.0], [1.0, 1.0], n_steps=nt, T=1.0,
+                              source=workloads.SOURCE_MMS)
+        o = Oracle(pr)
+        sps = _spaces(o)
+        tot = 0.0
+        for _ in range(nt):
+            old = [a.copy() for a in o.a]
+            o.step()
+            t = o.ell * o.dt
+            for s in range(pr.n_patches):
+                if pr.sigma[s] == 0:
+                    continue
+                for el in sps[s].elements():
+                    ids, val, cur, (X, Y, Z), W = sps[s].element_values(*el)
+                    dA = np.einsum("a,qac->qc", (o.a[s][ids] - old[s][ids]) / o.dt, val)
+                    tot += o.dt * np.sum(W[:, None] * (-math.exp(-t) * _S(X, Y, Z) + dA) ** 2)
+        errs.append(math.sqrt(tot))
+    rates = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert all(abs(r - 1.0) <= 0.15 for r in rates), (errs, rates)
