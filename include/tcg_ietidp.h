@@ -1,0 +1,164 @@
+/*
+ * tcg_ietidp.h — C ABI of the B200-native tree-cotree IETI-DP time stepper.
+ *
+ * Method: Mally, Vazquez, Schoeps, "Tree-Cotree-Based IETI-DP for Eddy Current
+ * Problems in Time-Domain", arXiv 2510.23446 (cited P:Lnnn = line of PAPER.md).
+ *   PDE            curl(nu curl A) + sigma dA/dt = J, A x n = 0 on dOmega    (eq. formA*)
+ *   discretisation spline edge elements (degrees (p-1,p,p) cyclic) per box patch,
+ *                  conforming interfaces, Boolean multiplier coupling
+ *   time stepping  implicit Euler [W dtB^T; dtB 0][a;m] = [f;0]             (eq. euler)
+ *   solver         tree-cotree gauge + IETI-DP (e/p/r splitting, primal coarse
+ *                  problem, PCG on the multipliers, Dirichlet preconditioner)
+ * Readings of passages the paper leaves open are listed in DESIGN.md §3 (R1..R18).
+ *
+ * Conventions
+ *   patch id      s = ix + Px*(iy + Py*iz)
+ *   local DOFs    per patch: component-major (x, y, z); within a component k slowest,
+ *                 then j, then i fastest; component c has (n_c - 1) indices along c and
+ *                 n_d = elems_d + p along the other directions d.
+ *   glued edges   the glued control grid has N_d = P_d (n_d - 1) + 1 vertices per
+ *                 direction; edge (c,i,j,k) joins vertex (i,j,k) to its +1 neighbour
+ *                 along c; ids are component-major with i fastest (R3).
+ *   precision     IEEE FP64 throughout (R14).
+ *
+ * Ownership: the caller owns every input array (copied during the call) and every
+ * output buffer (written during the call; a too-short `len` returns TCG_EINVAL and
+ * the required length in tcg_last_error). The library owns all device memory,
+ * streams and, for world > 1, its NCCL communicator.
+ *
+ * State machine: create -> set_* (any order, all required except source/solver)
+ *                -> [plan] -> setup -> step* -> get_* -> destroy.
+ *   set_* after plan/setup -> TCG_ESTATE.  After TCG_ENOTSPD only get_* / destroy.
+ * Errors: every call returns a tcg_status; tcg_last_error(h) holds a message with
+ *   the details (ENOTSPD: patch id or "coarse", pivot index, pivot value;
+ *   ENOCONV: step, iterations, relative residual).
+ * Threading: one handle per host thread; calls on one handle are not thread-safe.
+ */
+#ifndef TCG_IETIDP_H
+#define TCG_IETIDP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tcg_ctx* tcg_handle;
+
+typedef enum {
+  TCG_OK = 0,
+  TCG_EINVAL = -1,   /* invalid argument (p<1, counts<1, nu<=0, sigma<0, short buffer ...) */
+  TCG_ESTATE = -2,   /* call not allowed in the current state                               */
+  TCG_ENOTSPD = -3,  /* a Cholesky pivot <= 0 (gauging bug)                    */
+  TCG_ENOCONV = -4,  /* PCG hit max_iter                                           */
+  TCG_ECUDA = -5,    /* CUDA runtime error, or no usable sm_100 device                      */
+  TCG_ENCCL = -6,    /* NCCL error                                                          */
+  TCG_ENOMEM = -7    /* device allocation failed                                            */
+} tcg_status;
+
+/* source kinds: J = phi_s(t) S(x) */
+#define TCG_SOURCE_NONE 0
+#define TCG_SOURCE_CURL_PSI 1 /* S = curl(0,0,sin(pi x)sin(pi y)sin(pi z)), phi = sin(2 pi t)  (BASELINE.json configs) */
+#define TCG_SOURCE_MMS 2      /* S = (sin pi y sin pi z, sin pi x sin pi z, sin pi x sin pi y),
+                                 phi_s = 2 pi^2 nu_s (1-e^-t) + sigma_s e^-t  (manufactured, R16) */
+
+/* preconditioner scaling (P:L170 uses none; BASELINE.json north_star says "scaled") */
+#define TCG_SCALING_NONE 0
+#define TCG_SCALING_RHO 1     /* rho_s = diagonal of W^_s at the interface DOF (R5) */
+
+/* plan arrays for tcg_get_plan (host-side tree-cotree results, integer) */
+#define TCG_PLAN_EDGE_CLASS 0  /* per glued edge: 0 D, 1 WB, 2 F, 3 I                          */
+#define TCG_PLAN_EDGE_REGION 1 /* per glued edge: bit0 = has a conductor owner, bit1 = has an insulator owner */
+#define TCG_PLAN_TREE 2        /* per glued edge: 1 if in the spanning tree                     */
+#define TCG_PLAN_PART 3        /* per glued edge: 0 GAUGE(e), 1 primal, 2 remaining, 3 Dirichlet(e) */
+#define TCG_PLAN_PATCH_COUNTS 4 /* per patch: n_i, n_b, n_p (3 values each)                     */
+#define TCG_PLAN_LAMBDA 5      /* per multiplier k: glued edge id, patch(+1), patch(-1)          */
+#define TCG_PLAN_PRIMAL 6      /* per primal group: glued edge id                               */
+#define TCG_PLAN_RANK_OF_PATCH 7 /* per patch: owning rank (x-slab sharding)                     */
+
+typedef struct tcg_info {
+  int64_t n_patches, n_local, n_edges, n_verts;
+  int64_t m;            /* number of multipliers (lambda)                                */
+  int64_t n_c;          /* number of primal groups (coarse size)                         */
+  int64_t n_gauge, n_dirichlet, n_primal_local_total;
+  int64_t nr_min, nr_max, nb_min, nb_max, np_min, np_max;
+  int64_t steps_done, total_iters;
+  int64_t device_bytes; /* bytes of device memory held by the handle                      */
+  int64_t kernel_launches; /* kernels launched by the last tcg_step call                 */
+  double bytes_fapply;  /* algorithmic HBM bytes of one F-apply (all patches + coarse)    */
+  double bytes_precond; /* algorithmic HBM bytes of one preconditioner apply             */
+  double bytes_step_fixed; /* algorithmic HBM bytes of one step outside the PCG loop     */
+  double flops_factor;  /* local + coarse factorisation flops                            */
+  double ms_plan, ms_assembly, ms_factor, ms_coarse, ms_steps; /* device-event timings     */
+  double ms_pcg_last_step;
+  int32_t rank, world;
+  int32_t pad_;
+} tcg_info;
+
+/* Create a handle. device: CUDA ordinal used by setup; rank/world: this process's place
+ * in the job (world=1 for one GPU); nccl_id: 128-byte ncclUniqueId when world > 1
+ * (NULL iff world == 1); cuda_stream: cudaStream_t to use, or NULL for an owned stream.
+ * No CUDA call is made before tcg_setup. */
+tcg_status tcg_create(tcg_handle* out, int device, int rank, int world,
+                      const unsigned char* nccl_id, void* cuda_stream);
+
+/* Uniform box grid of npatch[0] x npatch[1] x npatch[2] patches on [lo,hi], spline degree
+ * p >= 1 and elems[d] >= 1 elements per patch per direction. */
+tcg_status tcg_set_patches(tcg_handle h, const int npatch[3], const double lo[3], const double hi[3],
+                           int degree_p, const int elems[3]);
+
+/* Per-patch conductivity sigma >= 0 (0 = insulator) and reluctivity nu > 0, n = #patches
+ * (sigma = 0 in Omega_I, nu bounded away from 0). */
+tcg_status tcg_set_materials(tcg_handle h, const double* sigma, const double* nu, size_t n);
+
+/* Source kind (TCG_SOURCE_*). Default TCG_SOURCE_CURL_PSI. */
+tcg_status tcg_set_source(tcg_handle h, int kind);
+
+/* Time interval (0,T], n_steps implicit-Euler steps, dt = T/n_steps, A(0) = 0. */
+tcg_status tcg_set_time(tcg_handle h, double T, int n_steps);
+
+/* PCG stopping rule sqrt(r^T z) <= rtol sqrt(r0^T z0), max_iter (ENOCONV beyond);
+ * scaling TCG_SCALING_*; tree_order 0: ascending edge ids within a Kruskal rank,
+ * 1: descending (gauge-invariance test). Defaults 1e-10, 5000, RHO, 0. */
+tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, int tree_order);
+
+/* Host-only planning (no CUDA): topology, ranked-Kruskal tree, e/p/r partition,
+ * multiplier and primal numbering, patch->rank sharding. Idempotent. */
+tcg_status tcg_plan(tcg_handle h);
+
+/* Copy a plan array (TCG_PLAN_*) into out[len] (int64). Requires tcg_plan. */
+tcg_status tcg_get_plan(tcg_handle h, int what, int64_t* out, size_t len);
+
+/* Collective: plan (if needed), device assembly of W^_s = nu_s K_s + sigma_s/dt M_s,
+ * batched FP64 Cholesky, coarse problem assembly and factorisation. */
+tcg_status tcg_setup(tcg_handle h);
+
+/* Collective: n implicit-Euler steps (each: rhs, PCG on lambda, recovery). */
+tcg_status tcg_step(tcg_handle h, int n);
+
+/* Coefficients of A after the last step. layout 0: per-patch local vectors concatenated
+ * (n_patches * n_local; eliminated DOFs 0); layout 1: one value per glued edge taken
+ * from the lowest-id owning patch (n_edges). */
+tcg_status tcg_get_coefficients(tcg_handle h, int layout, double* out, size_t len);
+
+/* Per-step PCG iteration counts iters[nsteps] and final relative residuals
+ * final_relres[nsteps] (either may be NULL); if relres_hist != NULL, the concatenated
+ * per-step histories sqrt(r_k^T z_k / r_0^T z_0), k = 0..iters (sum(iters+1) values). */
+tcg_status tcg_get_history(tcg_handle h, int* iters, double* final_relres, size_t nsteps,
+                           double* relres_hist, size_t hist_len);
+
+tcg_status tcg_get_info(tcg_handle h, tcg_info* out);
+
+/* Benchmark hook: `n` applications of the dual operator F (the exact per-iteration
+ * sequence forward solve -> coarse -> backward solve -> jump) on a fixed vector;
+ * returns the device time in *ms. Requires setup. */
+tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms);
+
+const char* tcg_last_error(tcg_handle h);
+void tcg_destroy(tcg_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCG_IETIDP_H */

@@ -67,11 +67,29 @@ def source_field(kind: int, x, y, z):
     return (0.0 * x, 0.0 * x, 0.0 * x)
 
 
+def sinpi(x: float) -> float:
+    """sin(pi x) with exact argument reduction (R19): x mod 2 and the
+    reflections r -> r-1, r -> 1-r are exact in binary floating point (Sterbenz), so
+    sin(pi x) is exactly 0 at integers and +-1 at half-integers, as the definition is.
+    math.sin(math.pi * x) instead rounds pi*x first (sin(2 pi * 1.0) = -2.4e-16)."""
+    r = math.fmod(x, 2.0)
+    if r < 0.0:
+        r += 2.0
+    sign = 1.0
+    if r >= 1.0:
+        r -= 1.0
+        sign = -1.0
+    if r > 0.5:
+        r = 1.0 - r
+    return sign * math.sin(math.pi * r)
+
+
 def source_time_factor(kind: int, t: float, nu: float, sigma: float) -> float:
     """phi_s(t) with J = phi_s(t) S(x) on patch s.
-    kind 1: sin(2 pi t).  kind 2: 2 pi^2 nu (1-e^-t) + sigma e^-t  (curl curl S = 2 pi^2 S)."""
+    kind 1: sin(2 pi t) (evaluated as sinpi(2t)).  kind 2: 2 pi^2 nu (1-e^-t) + sigma e^-t
+    (curl curl S = 2 pi^2 S)."""
     if kind == 1:
-        return math.sin(2.0 * math.pi * t)
+        return sinpi(2.0 * t)
     if kind == 2:
         return 2.0 * math.pi ** 2 * nu * (1.0 - math.exp(-t)) + sigma * math.exp(-t)
     return 0.0

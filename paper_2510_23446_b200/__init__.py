@@ -1,0 +1,183 @@
+"""paper_2510_23446_b200 — B200-native tree-cotree IETI-DP time stepper (arXiv 2510.23446).
+
+Thin ctypes binding over the C ABI declared in include/tcg_ietidp.h (argument
+marshalling only: topology/tree/partition run in the library's C++ host code, every
+arithmetic step of the method runs in its sm_100a CUDA kernels). There is no CPU
+fallback: if libtcg_ietidp.so is missing or cannot be loaded, importing `lib()` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIBPATH = os.path.join(HERE, "libtcg_ietidp.so")
+
+TCG_OK, TCG_EINVAL, TCG_ESTATE, TCG_ENOTSPD, TCG_ENOCONV, TCG_ECUDA, TCG_ENCCL, TCG_ENOMEM = 0, -1, -2, -3, -4, -5, -6, -7
+STATUS_NAMES = {0: "TCG_OK", -1: "TCG_EINVAL", -2: "TCG_ESTATE", -3: "TCG_ENOTSPD", -4: "TCG_ENOCONV",
+                -5: "TCG_ECUDA", -6: "TCG_ENCCL", -7: "TCG_ENOMEM"}
+PLAN_EDGE_CLASS, PLAN_EDGE_REGION, PLAN_TREE, PLAN_PART, PLAN_PATCH_COUNTS, PLAN_LAMBDA, PLAN_PRIMAL, PLAN_RANK_OF_PATCH = range(8)
+
+EXPORTS = ["tcg_create", "tcg_set_patches", "tcg_set_materials", "tcg_set_source", "tcg_set_time", "tcg_set_solver",
+           "tcg_plan", "tcg_get_plan", "tcg_setup", "tcg_step", "tcg_get_coefficients", "tcg_get_history",
+           "tcg_get_info", "tcg_bench_fapply", "tcg_last_error", "tcg_destroy"]
+
+
+class TcgInfo(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in (
+        "n_patches", "n_local", "n_edges", "n_verts", "m", "n_c", "n_gauge", "n_dirichlet", "n_primal_local_total",
+        "nr_min", "nr_max", "nb_min", "nb_max", "np_min", "np_max", "steps_done", "total_iters", "device_bytes",
+        "kernel_launches")] + [(n, C.c_double) for n in (
+        "bytes_fapply", "bytes_precond", "bytes_step_fixed", "flops_factor", "ms_plan", "ms_assembly", "ms_factor",
+        "ms_coarse", "ms_steps", "ms_pcg_last_step")] + [("rank", C.c_int32), ("world", C.c_int32),
+                                                         ("pad_", C.c_int32)]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_ if n != "pad_"}
+
+
+class TcgError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_LIB = None
+
+
+def lib():
+    """Load the in-tree C-ABI library (raises if it is missing: no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIBPATH):
+        raise ImportError(f"{LIBPATH} not built: run `python -m paper_2510_23446_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = C.CDLL(LIBPATH)
+    vp, dp, ip, i64p = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int64)
+    L.tcg_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, C.c_char_p, vp]
+    L.tcg_set_patches.argtypes = [vp, ip, dp, dp, C.c_int, ip]
+    L.tcg_set_materials.argtypes = [vp, dp, dp, C.c_size_t]
+    L.tcg_set_source.argtypes = [vp, C.c_int]
+    L.tcg_set_time.argtypes = [vp, C.c_double, C.c_int]
+    L.tcg_set_solver.argtypes = [vp, C.c_double, C.c_int, C.c_int, C.c_int]
+    L.tcg_plan.argtypes = [vp]
+    L.tcg_get_plan.argtypes = [vp, C.c_int, i64p, C.c_size_t]
+    L.tcg_setup.argtypes = [vp]
+    L.tcg_step.argtypes = [vp, C.c_int]
+    L.tcg_get_coefficients.argtypes = [vp, C.c_int, dp, C.c_size_t]
+    L.tcg_get_history.argtypes = [vp, ip, dp, C.c_size_t, dp, C.c_size_t]
+    L.tcg_get_info.argtypes = [vp, C.POINTER(TcgInfo)]
+    L.tcg_bench_fapply.argtypes = [vp, C.c_int, dp]
+    L.tcg_last_error.argtypes = [vp]
+    L.tcg_last_error.restype = C.c_char_p
+    L.tcg_destroy.argtypes = [vp]
+    L.tcg_destroy.restype = None
+    for n in EXPORTS:
+        if n not in ("tcg_last_error", "tcg_destroy"):
+            getattr(L, n).restype = C.c_int
+    _LIB = L
+    return L
+
+
+def _dptr(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Solver:
+    """One handle of the C ABI. Arguments mirror include/tcg_ietidp.h."""
+
+    def __init__(self, device=0, rank=0, world=1, nccl_id=None, stream=None):
+        self.L = lib()
+        self.h = C.c_void_p()
+        st = self.L.tcg_create(C.byref(self.h), device, rank, world, nccl_id, stream)
+        if st != TCG_OK:
+            msg = self.L.tcg_last_error(self.h).decode() if self.h else "tcg_create failed"
+            raise TcgError(st, msg)
+
+    def _ck(self, st):
+        if st != TCG_OK:
+            raise TcgError(st, self.L.tcg_last_error(self.h).decode())
+
+    def set_patches(self, npatch, lo, hi, p, elems):
+        self._ck(self.L.tcg_set_patches(self.h, (C.c_int * 3)(*npatch), (C.c_double * 3)(*lo),
+                                        (C.c_double * 3)(*hi), int(p), (C.c_int * 3)(*elems)))
+
+    def set_materials(self, sigma, nu):
+        s = np.ascontiguousarray(sigma, dtype=np.float64)
+        n = np.ascontiguousarray(nu, dtype=np.float64)
+        self._ck(self.L.tcg_set_materials(self.h, _dptr(s), _dptr(n), len(s)))
+
+    def set_source(self, kind):
+        self._ck(self.L.tcg_set_source(self.h, int(kind)))
+
+    def set_time(self, T, n_steps):
+        self._ck(self.L.tcg_set_time(self.h, float(T), int(n_steps)))
+
+    def set_solver(self, rtol=1e-10, max_iter=5000, scaling=1, tree_order=0):
+        self._ck(self.L.tcg_set_solver(self.h, float(rtol), int(max_iter), int(scaling), int(tree_order)))
+
+    def configure(self, prob):
+        """Set everything from a problem description with the fields of workloads.Problem."""
+        self.set_patches(prob.npatch, prob.lo, prob.hi, prob.p, prob.elems)
+        self.set_materials(prob.sigma, prob.nu)
+        self.set_source(prob.source)
+        self.set_time(prob.T, prob.n_steps)
+        self.set_solver(prob.rtol, prob.max_iter, prob.scaling, prob.tree_order)
+        return self
+
+    def plan(self):
+        self._ck(self.L.tcg_plan(self.h))
+
+    def plan_array(self, what, n):
+        out = np.zeros(n, dtype=np.int64)
+        self._ck(self.L.tcg_get_plan(self.h, int(what), out.ctypes.data_as(C.POINTER(C.c_int64)), n))
+        return out
+
+    def setup(self):
+        self._ck(self.L.tcg_setup(self.h))
+
+    def step(self, n=1):
+        self._ck(self.L.tcg_step(self.h, int(n)))
+
+    def info(self):
+        inf = TcgInfo()
+        self._ck(self.L.tcg_get_info(self.h, C.byref(inf)))
+        return inf.as_dict()
+
+    def coefficients(self, layout=1, out=None):
+        inf = self.info()
+        n = inf["n_edges"] if layout == 1 else inf["n_patches"] * inf["n_local"]
+        if out is None:
+            out = np.zeros(n)
+        self._ck(self.L.tcg_get_coefficients(self.h, int(layout), _dptr(out), n))
+        return out
+
+    def history(self):
+        inf = self.info()
+        ns = inf["steps_done"]
+        it = np.zeros(ns, dtype=np.int32)
+        fr = np.zeros(ns)
+        self._ck(self.L.tcg_get_history(self.h, it.ctypes.data_as(C.POINTER(C.c_int)), _dptr(fr), ns, None, 0))
+        hl = int(np.sum(it + 1))
+        hist = np.zeros(max(hl, 1))
+        self._ck(self.L.tcg_get_history(self.h, None, None, ns, _dptr(hist), hl))
+        return it, fr, hist[:hl]
+
+    def bench_fapply(self, n):
+        ms = C.c_double()
+        self._ck(self.L.tcg_bench_fapply(self.h, int(n), C.byref(ms)))
+        return ms.value
+
+    def close(self):
+        if self.h:
+            self.L.tcg_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

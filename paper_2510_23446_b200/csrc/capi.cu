@@ -1,0 +1,951 @@
+// capi.cu — the C ABI (include/tcg_ietidp.h): handle state machine, device memory,
+// setup orchestration (assembly -> batched Cholesky -> coarse) and the implicit-Euler step
+// (rhs -> PCG on lambda -> recovery). All arithmetic of the method runs in the kernels of
+// assembly.cu / chol.cu / solve.cu, compiled into this translation unit.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/tcg_ietidp.h"
+#include "plan.h"
+#include "assembly.cu"
+#include "chol.cu"
+#include "solve.cu"
+
+using namespace tcg;
+
+struct tcg_ctx {
+  int device = 0, rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  Plan plan;
+  bool have_patches = false, have_materials = false, have_time = false;
+  bool planned = false, setup_done = false, broken = false;
+  int source = TCG_SOURCE_CURL_PSI;
+  double T = 1.0;
+  int n_steps = 0;
+  double rtol = 1e-10;
+  int max_iter = 5000;
+  int scaling = TCG_SCALING_RHO;
+  int tree_order = 0;
+  int stable_mask = 0;  // bit0: local diag substitution, bit1: coarse, bit2: TRSM substitution (env TCG_STABLE)
+  std::string err;
+
+  // device state
+  std::vector<void*> allocs;
+  int64_t device_bytes = 0;
+  DevPlan D{};
+  Geom G{};
+  Tables1D tb{};
+  CholDesc* d_desc = nullptr;
+  CholDesc* d_cdesc = nullptr;
+  int maxT = 0, maxTr = 0, maxTb = 0, maxTbp = 0;
+  int64_t max_ls_tiles = 0;
+  std::vector<std::vector<int>> colour_lists;
+  int* d_colour = nullptr;
+  std::vector<int64_t> colour_off;
+  double *X1 = nullptr, *XW = nullptr, *XJ = nullptr, *JS = nullptr, *PW = nullptr;
+  double *lam = nullptr, *r = nullptr, *z = nullptr, *pk = nullptr, *q = nullptr;
+  double *Pc = nullptr, *partial = nullptr, *hist = nullptr, *a_loc = nullptr, *glued = nullptr;
+  int64_t* d_glued_src = nullptr;
+  PcgState* st = nullptr;
+  PcgState* h_st = nullptr;  // pinned
+  DevError* derr = nullptr;
+  double* dbgA = nullptr;   // copy of the assembled augmented matrices (TCG_DEBUG_KEEP=1)
+  double* dbgC = nullptr;   // copy of the assembled coarse matrix
+  std::vector<int64_t> h_a_off, h_vec_off;
+  std::vector<int> h_T;
+  int64_t a_total = 0;
+  int64_t vec_total = 0;
+  size_t smem_fwd_full = 0, smem_bwd_full = 0, smem_fwd_ls = 0, smem_bwd_ls = 0, smem_coarse = 0, smem_prec = 0;
+
+  // results
+  int64_t steps_done = 0, total_iters = 0;
+  std::vector<int> iters;
+  std::vector<double> final_rel, hist_all;
+  int64_t launches_last = 0;
+  double ms_plan = 0, ms_assembly = 0, ms_factor = 0, ms_coarse = 0, ms_steps = 0, ms_pcg_last = 0;
+
+  ~tcg_ctx() { release(); }
+  void release() {
+    if (!allocs.empty() || stream) cudaSetDevice(device);
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+    if (h_st) cudaFreeHost(h_st);
+    h_st = nullptr;
+    if (own_stream && stream) cudaStreamDestroy(stream);
+    stream = nullptr;
+  }
+};
+
+namespace {
+
+tcg_status fail(tcg_ctx* h, tcg_status s, const std::string& msg) {
+  if (h) h->err = msg;
+  return s;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) {                                                                      \
+      h->broken = (e_ != cudaErrorMemoryAllocation);                                              \
+      return fail(h, e_ == cudaErrorMemoryAllocation ? TCG_ENOMEM : TCG_ECUDA,                    \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                            \
+    }                                                                                             \
+  } while (0)
+
+#define CKL()                                                                                     \
+  do {                                                                                            \
+    cudaError_t e_ = cudaGetLastError();                                                          \
+    if (e_ != cudaSuccess) {                                                                      \
+      h->broken = true;                                                                           \
+      return fail(h, TCG_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_) + " at " + \
+                                    std::to_string(__LINE__));                                    \
+    }                                                                                             \
+  } while (0)
+
+template <class T>
+tcg_status dalloc(tcg_ctx* h, T** out, size_t n) {
+  size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) return fail(h, TCG_ENOMEM, std::string("cudaMalloc ") + std::to_string(bytes) + ": " + cudaGetErrorString(e));
+  h->allocs.push_back(p);
+  h->device_bytes += (int64_t)bytes;
+  *out = static_cast<T*>(p);
+  return TCG_OK;
+}
+
+template <class T>
+tcg_status dupload(tcg_ctx* h, T** out, const std::vector<T>& v) {
+  tcg_status s = dalloc(h, out, v.size());
+  if (s != TCG_OK) return s;
+  if (!v.empty()) {
+    cudaError_t e = cudaMemcpyAsync(*out, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, h->stream);
+    if (e != cudaSuccess) return fail(h, TCG_ECUDA, std::string("upload: ") + cudaGetErrorString(e));
+  }
+  return TCG_OK;
+}
+
+#define TRY(x)                        \
+  do {                                \
+    tcg_status s_ = (x);              \
+    if (s_ != TCG_OK) return s_;      \
+  } while (0)
+
+double elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+tcg_status set_smem(tcg_ctx* h, const void* fn, size_t bytes) {
+  if (bytes > 227 * 1024) return fail(h, TCG_EINVAL, "kernel needs " + std::to_string(bytes) + " B shared memory (> 227 KB)");
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(bytes, 48 * 1024)));
+  return TCG_OK;
+}
+
+}  // namespace
+
+// =========================================================================================
+// setup
+// =========================================================================================
+static tcg_status do_plan(tcg_ctx* h) {
+  if (h->planned) return TCG_OK;
+  if (!h->have_patches || !h->have_materials || !h->have_time) return fail(h, TCG_ESTATE, "set_patches, set_materials and set_time are required");
+  auto t0 = std::chrono::steady_clock::now();
+  h->plan.tree_order = h->tree_order;
+  h->plan.world = h->world;
+  std::string e = h->plan.build();
+  if (!e.empty()) return fail(h, TCG_EINVAL, "plan: " + e);
+  h->planned = true;
+  h->ms_plan = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return TCG_OK;
+}
+
+static tcg_status run_cholesky(tcg_ctx* h, const CholDesc* d_desc, int nmat, int maxT, int maxTf, int maxTb,
+                               double* base, double* dinv, double* sbb, int coarse) {
+  const int subst = (h->stable_mask & 4) ? 1 : 0;
+  for (int k = 0; k < maxTf; ++k) {
+    if (sbb && maxTb > 0) {
+      dim3 gc((unsigned)tri_tiles(maxTb), nmat);
+      k_capture_sbb<<<gc, 256, 0, h->stream>>>(d_desc, k, base, sbb);
+      CKL();
+    }
+    k_potrf<<<nmat, 256, 2 * TS * 65 * sizeof(double), h->stream>>>(d_desc, k, base, dinv, h->derr, coarse);
+    CKL();
+    int rows = maxT - k - 1;
+    if (rows > 0) {
+      dim3 gt(rows, nmat);
+      k_trsm<<<gt, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(d_desc, k, base, dinv, subst);
+      CKL();
+      dim3 gu((unsigned)tri_tiles(rows), nmat);
+      k_update<<<gu, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(d_desc, k, base);
+      CKL();
+    }
+  }
+  return TCG_OK;
+}
+
+static tcg_status do_setup(tcg_ctx* h) {
+  TRY(do_plan(h));
+  Plan& pl = h->plan;
+  CK(cudaSetDevice(h->device));
+  {
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, h->device));
+    if (prop.major < 10) return fail(h, TCG_ECUDA, std::string("device ") + prop.name + " is not sm_100 class");
+  }
+  if (!h->stream) {
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  const int P = pl.npatch;
+  const double dt = h->T / h->n_steps;
+
+  // ---- geometry / offsets ----
+  Geom& G = h->G;
+  for (int d = 0; d < 3; ++d) {
+    G.P[d] = pl.P[d];
+    G.el[d] = pl.el[d];
+  }
+  G.p = pl.p;
+  for (int c = 0; c < 3; ++c)
+    for (int d = 0; d < 3; ++d) G.cdim[c][d] = pl.comp_dim(c, d);
+  G.nloc = pl.nloc;
+
+  std::vector<int> Ti(P), Tb(P), Tp(P), T(P), nb(P), np(P);
+  std::vector<int64_t> a_off(P), dinv_off(P), ls_off(P), sbb_off(P), vec_off(P), aug_off(P), b_off(P + 1), p_off(P + 1),
+      tile_start(P + 1);
+  std::vector<int> aug_all, b_lam_all, p_grp_all;
+  std::vector<double> b_sign_all;
+  int64_t oa = 0, od = 0, ol = 0, os = 0, ov = 0, og = 0;
+  h->maxT = h->maxTr = h->maxTb = h->maxTbp = 0;
+  h->max_ls_tiles = 0;
+  b_off[0] = p_off[0] = tile_start[0] = 0;
+  for (int s = 0; s < P; ++s) {
+    const PatchPlan& q = pl.pp[s];
+    Ti[s] = q.Ti;
+    Tb[s] = q.Tb;
+    Tp[s] = q.Tp;
+    T[s] = q.Ti + q.Tb + q.Tp;
+    nb[s] = q.nb;
+    np[s] = q.np;
+    a_off[s] = oa;
+    oa += tri_tiles(T[s]) * TSZ;
+    dinv_off[s] = od;
+    od += (int64_t)(q.Ti + q.Tb) * TSZ;
+    ls_off[s] = ol;
+    int64_t lst = tri_tiles(q.Tb) + (int64_t)q.Tp * q.Tb;
+    ol += lst * TSZ;
+    sbb_off[s] = os;
+    os += tri_tiles(q.Tb) * TSZ;
+    vec_off[s] = ov;
+    ov += (int64_t)T[s] * TS;
+    aug_off[s] = og;
+    og += (int64_t)T[s] * TS;
+    aug_all.insert(aug_all.end(), q.aug.begin(), q.aug.end());
+    b_off[s + 1] = b_off[s] + q.nb;
+    p_off[s + 1] = p_off[s] + q.np;
+    for (int t = 0; t < q.nb; ++t) {
+      b_lam_all.push_back(q.b_lam[t]);
+      b_sign_all.push_back((double)q.b_sign[t]);
+    }
+    for (int t = 0; t < q.np; ++t) p_grp_all.push_back(q.p_grp[t]);
+    tile_start[s + 1] = tile_start[s] + tri_tiles(T[s]);
+    h->maxT = std::max(h->maxT, T[s]);
+    h->maxTr = std::max(h->maxTr, q.Ti + q.Tb);
+    h->maxTb = std::max(h->maxTb, q.Tb);
+    h->maxTbp = std::max(h->maxTbp, q.Tb + q.Tp);
+    h->max_ls_tiles = std::max(h->max_ls_tiles, lst);
+  }
+  h->vec_total = ov;
+  h->D.maxT = h->maxT;
+  h->D.maxTbp = h->maxTbp;
+  // multipliers
+  std::vector<int> lpp(pl.m), lpm(pl.m), lsp(pl.m), lsm(pl.m);
+  std::vector<int64_t> lip(pl.m), lim(pl.m);
+  for (int64_t k = 0; k < pl.m; ++k) {
+    lpp[k] = (int)pl.lam_plus[k];
+    lpm[k] = (int)pl.lam_minus[k];
+    lsp[k] = pl.lam_plus_pos[k];
+    lsm[k] = pl.lam_minus_pos[k];
+    lip[k] = vec_off[lpp[k]] + (int64_t)Ti[lpp[k]] * TS + lsp[k];
+    lim[k] = vec_off[lpm[k]] + (int64_t)Ti[lpm[k]] * TS + lsm[k];
+  }
+  std::vector<int64_t> cidx(pl.coarse_patch.size());
+  for (size_t e = 0; e < cidx.size(); ++e) {
+    int s = pl.coarse_patch[e];
+    cidx[e] = vec_off[s] + (int64_t)(Ti[s] + Tb[s]) * TS + pl.coarse_pos[e];
+  }
+  const int Tc = (int)((pl.nc + TS - 1) / TS);
+
+  // ---- uploads ----
+  DevPlan& D = h->D;
+  D.npatch = P;
+  {
+    const char* ev = getenv("TCG_STABLE");
+    h->stable_mask = ev ? atoi(ev) : h->stable_mask;
+  }
+  D.subst_local = h->stable_mask & 1;
+  D.subst_coarse = (h->stable_mask >> 1) & 1;
+  D.m = pl.m;
+  D.nc = pl.nc;
+  D.Tc = Tc;
+  int *dTi, *dTb, *dTp, *dT, *dnb, *dnp, *daug, *dbl, *dpg, *dlpp, *dlpm, *dlsp, *dlsm, *dcp;
+  int64_t *dao, *ddo, *dlo, *dso, *dvo, *dgo, *dbo, *dpo, *dts, *dlip, *dlim, *dci;
+  double *dbs, *dsig, *dnu;
+  TRY(dupload(h, &dTi, Ti));
+  TRY(dupload(h, &dTb, Tb));
+  TRY(dupload(h, &dTp, Tp));
+  TRY(dupload(h, &dT, T));
+  TRY(dupload(h, &dnb, nb));
+  TRY(dupload(h, &dnp, np));
+  TRY(dupload(h, &dao, a_off));
+  TRY(dupload(h, &ddo, dinv_off));
+  TRY(dupload(h, &dlo, ls_off));
+  TRY(dupload(h, &dso, sbb_off));
+  TRY(dupload(h, &dvo, vec_off));
+  TRY(dupload(h, &dgo, aug_off));
+  TRY(dupload(h, &daug, aug_all));
+  TRY(dupload(h, &dbo, b_off));
+  TRY(dupload(h, &dbl, b_lam_all));
+  TRY(dupload(h, &dbs, b_sign_all));
+  TRY(dupload(h, &dpo, p_off));
+  TRY(dupload(h, &dpg, p_grp_all));
+  TRY(dupload(h, &dts, tile_start));
+  TRY(dupload(h, &dsig, pl.sigma));
+  TRY(dupload(h, &dnu, pl.nu));
+  TRY(dupload(h, &dlpp, lpp));
+  TRY(dupload(h, &dlpm, lpm));
+  TRY(dupload(h, &dlsp, lsp));
+  TRY(dupload(h, &dlsm, lsm));
+  TRY(dupload(h, &dlip, lip));
+  TRY(dupload(h, &dlim, lim));
+  TRY(dupload(h, &dcp, pl.coarse_ptr));
+  TRY(dupload(h, &dci, cidx));
+  D.Ti = dTi; D.Tb = dTb; D.Tp = dTp; D.T = dT; D.nb = dnb; D.np = dnp;
+  D.a_off = dao; D.dinv_off = ddo; D.ls_off = dlo; D.sbb_off = dso; D.vec_off = dvo; D.aug_off = dgo;
+  D.aug = daug; D.b_off = dbo; D.b_lam = dbl; D.b_sign = dbs; D.p_off = dpo; D.p_grp = dpg;
+  D.tile_start = dts; D.sigma = dsig; D.nu = dnu;
+  D.lam_patch_p = dlpp; D.lam_patch_m = dlpm; D.lam_pos_p = dlsp; D.lam_pos_m = dlsm;
+  D.lam_idx_p = dlip; D.lam_idx_m = dlim; D.coarse_ptr = dcp; D.coarse_idx = dci;
+  double *wp, *wm;
+  TRY(dalloc(h, &wp, pl.m));
+  TRY(dalloc(h, &wm, pl.m));
+  D.wplus = wp;
+  D.wminus = wm;
+  TRY(dalloc(h, &D.A, oa));
+  TRY(dalloc(h, &D.Dinv, od));
+  TRY(dalloc(h, &D.LS, ol));
+  TRY(dalloc(h, &D.Sbb, os));
+  TRY(dalloc(h, &D.C, (size_t)tri_tiles(Tc) * TSZ));
+  TRY(dalloc(h, &D.Cinv, (size_t)Tc * TSZ));
+  TRY(dalloc(h, &h->X1, ov));
+  TRY(dalloc(h, &h->XW, ov));
+  TRY(dalloc(h, &h->XJ, ov));
+  TRY(dalloc(h, &h->JS, ov));
+  TRY(dalloc(h, &h->PW, ov));
+  TRY(dalloc(h, &h->lam, pl.m));
+  TRY(dalloc(h, &h->r, pl.m));
+  TRY(dalloc(h, &h->z, pl.m));
+  TRY(dalloc(h, &h->pk, pl.m));
+  TRY(dalloc(h, &h->q, pl.m));
+  TRY(dalloc(h, &h->Pc, pl.nc));
+  TRY(dalloc(h, &h->partial, RED_BLOCKS));
+  TRY(dalloc(h, &h->hist, (size_t)h->max_iter + 2));
+  TRY(dalloc(h, &h->a_loc, (size_t)P * pl.nloc));
+  TRY(dalloc(h, &h->st, 1));
+  TRY(dalloc(h, &h->derr, 1));
+  if (!h->h_st) CK(cudaMallocHost(&h->h_st, sizeof(PcgState)));
+  CK(cudaMemsetAsync(h->st, 0, sizeof(PcgState), h->stream));
+  CK(cudaMemsetAsync(h->derr, 0, sizeof(DevError), h->stream));
+  CK(cudaMemsetAsync(h->a_loc, 0, sizeof(double) * (size_t)P * pl.nloc, h->stream));
+  CK(cudaMemsetAsync(h->XW, 0, sizeof(double) * ov, h->stream));
+  CK(cudaMemsetAsync(h->PW, 0, sizeof(double) * ov, h->stream));
+  CK(cudaMemsetAsync(h->lam, 0, sizeof(double) * std::max<int64_t>(pl.m, 1), h->stream));
+
+  // chol descriptors
+  std::vector<CholDesc> desc(P);
+  for (int s = 0; s < P; ++s) desc[s] = CholDesc{a_off[s], dinv_off[s], sbb_off[s], T[s], Ti[s] + Tb[s], Ti[s], Tb[s]};
+  TRY(dupload(h, &h->d_desc, desc));
+  std::vector<CholDesc> cdesc(1, CholDesc{0, 0, -1, Tc, Tc, -1, 0});
+  TRY(dupload(h, &h->d_cdesc, cdesc));
+  // colour lists (parity classes)
+  std::vector<int> colour_all;
+  h->colour_off.assign(9, 0);
+  for (int c = 0; c < 8; ++c) {
+    for (int s = 0; s < P; ++s) {
+      int ix = s % pl.P[0], iy = (s / pl.P[0]) % pl.P[1], iz = s / (pl.P[0] * pl.P[1]);
+      if (((ix & 1) | ((iy & 1) << 1) | ((iz & 1) << 2)) == c) colour_all.push_back(s);
+    }
+    h->colour_off[c + 1] = (int64_t)colour_all.size();
+  }
+  TRY(dupload(h, &h->d_colour, colour_all));
+  // glued readout map: edge -> (patch*nloc + local) of its lowest-id owner
+  {
+    std::vector<int64_t> src(pl.nedges, -1);
+    for (int s = 0; s < P; ++s)
+      for (int a = 0; a < pl.nloc; ++a) {
+        int64_t g = pl.local_to_global(s, a);
+        if (src[g] < 0) src[g] = (int64_t)s * pl.nloc + a;
+      }
+    TRY(dupload(h, &h->d_glued_src, src));
+    TRY(dalloc(h, &h->glued, pl.nedges));
+  }
+
+  // ---- 1D tables ----
+  Tables1D& tb = h->tb;
+  int64_t toff = 0;
+  for (int d = 0; d < 3; ++d) {
+    int n = pl.el[d] + pl.p;
+    tb.el[d] = pl.el[d];
+    tb.P[d] = pl.P[d];
+    tb.h[d] = (pl.hi[d] - pl.lo[d]) / pl.P[d];
+    tb.lo[d] = pl.lo[d];
+    tb.off_Mb[d] = toff; toff += (int64_t)n * n;
+    tb.off_Md[d] = toff; toff += (int64_t)(n - 1) * (n - 1);
+    tb.off_Kb[d] = toff; toff += (int64_t)n * n;
+    tb.off_C[d] = toff; toff += (int64_t)(n - 1) * n;
+    tb.off_oneD[d] = toff; toff += n - 1;
+    tb.off_sD[d] = toff; toff += (int64_t)pl.P[d] * (n - 1);
+    tb.off_cB[d] = toff; toff += (int64_t)pl.P[d] * n;
+    tb.off_sB[d] = toff; toff += (int64_t)pl.P[d] * n;
+    if (pl.el[d] + 2 * pl.p > 160) return fail(h, TCG_EINVAL, "elements + 2p must be <= 160");
+  }
+  TRY(dalloc(h, &tb.base, toff));
+
+  cudaEvent_t e0, e1, e2, e3, e4;
+  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3); cudaEventCreate(&e4);
+  CK(cudaEventRecord(e0, h->stream));
+  {
+    int maxn = 0, maxel = 0;
+    for (int d = 0; d < 3; ++d) { maxn = std::max(maxn, pl.el[d] + pl.p); maxel = std::max(maxel, pl.el[d]); }
+    size_t smem = sizeof(double) * (2 * (pl.p + 1) + (size_t)maxel * (pl.p + 1) * (3 * maxn + 2));
+    TRY(set_smem(h, (const void*)k_tables1d, smem));
+    k_tables1d<<<3, 256, smem, h->stream>>>(tb, pl.p);
+    CKL();
+  }
+  k_assemble<<<(unsigned)tile_start[P], 256, 0, h->stream>>>(D, tb, G, 1.0 / dt);
+  CKL();
+  if (pl.m > 0) {
+    k_rho_weights<<<(unsigned)((pl.m + 255) / 256), 256, 0, h->stream>>>(D, h->scaling);
+    CKL();
+  }
+  k_load_vector<<<P, 256, 0, h->stream>>>(D, tb, G, h->source, h->JS);
+  CKL();
+  CK(cudaEventRecord(e1, h->stream));
+
+  const bool keep = getenv("TCG_DEBUG_KEEP") && atoi(getenv("TCG_DEBUG_KEEP")) != 0;
+  h->h_a_off = a_off;
+  h->h_vec_off = vec_off;
+  h->h_T = T;
+  h->a_total = oa;
+  if (keep) {
+    TRY(dalloc(h, &h->dbgA, oa));
+    CK(cudaMemcpyAsync(h->dbgA, D.A, sizeof(double) * oa, cudaMemcpyDeviceToDevice, h->stream));
+  }
+  // ---- batched local Cholesky ----
+  TRY(set_smem(h, (const void*)k_potrf, 2 * TS * 65 * sizeof(double)));
+  TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
+  TRY(set_smem(h, (const void*)k_update, 2 * TS * SPAD * sizeof(double)));
+  TRY(run_cholesky(h, h->d_desc, P, h->maxT, h->maxTr, h->maxTb, D.A, D.Dinv, D.Sbb, 0));
+  if (h->max_ls_tiles > 0) {
+    dim3 gl((unsigned)h->max_ls_tiles, P);
+    k_build_ls<<<gl, 256, 0, h->stream>>>(D);
+    CKL();
+  }
+  CK(cudaEventRecord(e2, h->stream));
+  DevError herr;
+  CK(cudaMemcpyAsync(&herr, h->derr, sizeof(DevError), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (herr.flag) {
+    h->broken = true;
+    std::ostringstream o;
+    o << "local Cholesky: patch " << herr.matrix << " pivot " << herr.index << " value " << herr.value;
+    return fail(h, TCG_ENOTSPD, o.str());
+  }
+
+  // ---- coarse problem ----
+  CK(cudaMemsetAsync(D.C, 0, sizeof(double) * (size_t)tri_tiles(Tc) * TSZ, h->stream));
+  if (pl.nc > 0) {
+    for (int c = 0; c < 8; ++c) {
+      int cnt = (int)(h->colour_off[c + 1] - h->colour_off[c]);
+      if (cnt == 0) continue;
+      k_coarse_scatter<<<cnt, 256, 0, h->stream>>>(D, h->d_colour + h->colour_off[c], cnt);
+      CKL();
+    }
+    int npad = Tc * TS - (int)pl.nc;
+    if (npad > 0) {
+      k_coarse_pad<<<(npad + 255) / 256, 256, 0, h->stream>>>(D);
+      CKL();
+    }
+    if (keep) {
+      TRY(dalloc(h, &h->dbgC, (size_t)tri_tiles(Tc) * TSZ));
+      CK(cudaMemcpyAsync(h->dbgC, D.C, sizeof(double) * tri_tiles(Tc) * TSZ, cudaMemcpyDeviceToDevice, h->stream));
+    }
+    TRY(run_cholesky(h, h->d_cdesc, 1, Tc, Tc, 0, D.C, D.Cinv, nullptr, 1));
+  }
+  CK(cudaEventRecord(e3, h->stream));
+  CK(cudaMemcpyAsync(&herr, h->derr, sizeof(DevError), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (herr.flag) {
+    h->broken = true;
+    std::ostringstream o;
+    o << "coarse Cholesky: pivot " << herr.index << " value " << herr.value;
+    return fail(h, TCG_ENOTSPD, o.str());
+  }
+
+  // ---- solver kernel shared memory ----
+  const size_t dtl = (h->stable_mask & 3) ? (size_t)TS * 65 : 0;  // staged diagonal tile for substitution
+  h->smem_fwd_full = sizeof(double) * (TS + (size_t)h->maxT * TS + dtl);
+  h->smem_bwd_full = sizeof(double) * (TS + 8 * TS + (size_t)h->maxT * TS + dtl);
+  h->smem_fwd_ls = sizeof(double) * (TS + (size_t)h->maxTbp * TS + dtl);
+  h->smem_bwd_ls = sizeof(double) * (TS + 8 * TS + (size_t)h->maxTbp * TS + dtl);
+  h->smem_coarse = sizeof(double) * (TS + 8 * TS + (size_t)Tc * TS + dtl);
+  h->smem_prec = sizeof(double) * (10 * (size_t)h->maxTb * TS);
+  TRY(set_smem(h, (const void*)k_fwd_full, h->smem_fwd_full));
+  TRY(set_smem(h, (const void*)k_bwd_full, h->smem_bwd_full));
+  TRY(set_smem(h, (const void*)k_fwd_ls, h->smem_fwd_ls));
+  TRY(set_smem(h, (const void*)k_bwd_ls, h->smem_bwd_ls));
+  TRY(set_smem(h, (const void*)k_coarse_solve, h->smem_coarse));
+  TRY(set_smem(h, (const void*)k_precond, h->smem_prec));
+
+  // ---- insulator precompute: XJ = forward(j_S) ----
+  k_copy<<<592, 256, 0, h->stream>>>(h->XJ, h->JS, ov);
+  CKL();
+  k_fwd_full<<<P, NTHR, h->smem_fwd_full, h->stream>>>(D, h->XJ, 0);
+  CKL();
+  CK(cudaEventRecord(e4, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->ms_assembly = elapsed_ms(e0, e1);
+  h->ms_factor = elapsed_ms(e1, e2);
+  h->ms_coarse = elapsed_ms(e2, e3);
+  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3); cudaEventDestroy(e4);
+  h->setup_done = true;
+  return TCG_OK;
+}
+
+// =========================================================================================
+// step
+// =========================================================================================
+static tcg_status launch_iteration(tcg_ctx* h, int64_t& nl) {
+  DevPlan& D = h->D;
+  const int P = D.npatch;
+  const int64_t m = D.m;
+  k_fwd_ls<<<P, NTHR, h->smem_fwd_ls, h->stream>>>(D, h->pk, h->XW, h->st);
+  k_coarse_solve<<<1, NTHR, h->smem_coarse, h->stream>>>(D, h->XW, nullptr, h->Pc, h->st);
+  k_bwd_ls<<<P, NTHR, h->smem_bwd_ls, h->stream>>>(D, h->XW, h->Pc, h->XW, h->st);
+  k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->XW, h->q, h->pk, nullptr, h->st, h->partial, h->hist, JUMP_F, h->rtol, h->max_iter);
+  k_axpy<<<RED_BLOCKS, 256, 0, h->stream>>>(h->lam, h->r, h->pk, h->q, h->st, m);
+  k_precond<<<P, NTHR, h->smem_prec, h->stream>>>(D, h->r, h->PW, h->st);
+  k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->PW, h->z, h->r, nullptr, h->st, h->partial, h->hist, JUMP_M, h->rtol, h->max_iter);
+  k_xpay<<<RED_BLOCKS, 256, 0, h->stream>>>(h->pk, h->z, h->st, m, 0);
+  nl += 8;
+  CKL();
+  return TCG_OK;
+}
+
+static tcg_status do_step(tcg_ctx* h) {
+  DevPlan& D = h->D;
+  const int P = D.npatch;
+  const int64_t m = D.m;
+  const double dt = h->T / h->n_steps;
+  const double t = (h->steps_done + 1) * dt;
+  int64_t nl = 0;
+  CK(cudaMemsetAsync(h->st, 0, sizeof(PcgState), h->stream));
+  // rhs: f, forward solves, dual rhs d = B (x1 - Phi N p0)
+  k_rhs<<<P, 256, 0, h->stream>>>(D, h->tb, h->G, h->source, t, 1.0 / dt, h->JS, h->XJ, h->a_loc, h->X1);
+  k_fwd_full<<<P, NTHR, h->smem_fwd_full, h->stream>>>(D, h->X1, 1);
+  k_coarse_solve<<<1, NTHR, h->smem_coarse, h->stream>>>(D, h->X1, nullptr, h->Pc, nullptr);
+  k_bwd_ls<<<P, NTHR, h->smem_bwd_ls, h->stream>>>(D, h->X1, h->Pc, h->XW, nullptr);
+  k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->XW, h->r, nullptr, h->lam, h->st, h->partial, h->hist, JUMP_D, h->rtol, h->max_iter);
+  k_precond<<<P, NTHR, h->smem_prec, h->stream>>>(D, h->r, h->PW, h->st);
+  k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->PW, h->z, h->r, nullptr, h->st, h->partial, h->hist, JUMP_M0, h->rtol, h->max_iter);
+  k_xpay<<<RED_BLOCKS, 256, 0, h->stream>>>(h->pk, h->z, h->st, m, 1);
+  nl += 8;
+  CKL();
+  // PCG: chunks of iterations, device-side convergence flag, one host check per chunk
+  const int chunk = 8;
+  int iters = 0;
+  for (;;) {
+    for (int c = 0; c < chunk; ++c) TRY(launch_iteration(h, nl));
+    CK(cudaMemcpyAsync(h->h_st, h->st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    iters = h->h_st->iter;
+    if (h->h_st->done) break;
+    if (iters >= h->max_iter) break;
+  }
+  const PcgState hs = *h->h_st;
+  if (hs.failed) {
+    std::ostringstream o;
+    o << "PCG did not converge: step " << h->steps_done + 1 << ", iterations " << hs.iter << ", relres "
+      << (hs.rho0 > 0 ? std::sqrt(std::max(hs.rz, 0.0) / hs.rho0) : 0.0) << (hs.nan ? " (curvature/NaN guard)" : "");
+    return fail(h, TCG_ENOCONV, o.str());
+  }
+  // recovery
+  k_fwd_ls<<<P, NTHR, h->smem_fwd_ls, h->stream>>>(D, h->lam, h->XW, nullptr);
+  k_coarse_solve<<<1, NTHR, h->smem_coarse, h->stream>>>(D, h->X1, h->XW, h->Pc, nullptr);
+  k_bwd_full<<<P, NTHR, h->smem_bwd_full, h->stream>>>(D, h->X1, h->XW, h->Pc, h->a_loc, h->G.nloc);
+  nl += 3;
+  CKL();
+  std::vector<double> hh(iters + 1);
+  CK(cudaMemcpyAsync(hh.data(), h->hist, sizeof(double) * (iters + 1), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->iters.push_back(iters);
+  h->final_rel.push_back(hh.back());
+  h->hist_all.insert(h->hist_all.end(), hh.begin(), hh.end());
+  h->total_iters += iters;
+  h->steps_done += 1;
+  h->launches_last += nl;
+  return TCG_OK;
+}
+
+// =========================================================================================
+// C ABI
+// =========================================================================================
+extern "C" {
+
+tcg_status tcg_create(tcg_handle* out, int device, int rank, int world, const unsigned char* nccl_id, void* cuda_stream) {
+  if (!out) return TCG_EINVAL;
+  *out = nullptr;
+  if (world < 1 || rank < 0 || rank >= world || device < 0) return TCG_EINVAL;
+  if (world > 1 && !nccl_id) return TCG_EINVAL;
+  tcg_ctx* h = new tcg_ctx();
+  h->device = device;
+  h->rank = rank;
+  h->world = world;
+  h->stream = static_cast<cudaStream_t>(cuda_stream);
+  *out = h;
+  if (world > 1) return fail(h, TCG_ENCCL, "multi-GPU (world > 1) is not built in this version");
+  return TCG_OK;
+}
+
+tcg_status tcg_set_patches(tcg_handle h, const int npatch[3], const double lo[3], const double hi[3], int degree_p,
+                           const int elems[3]) {
+  if (!h) return TCG_EINVAL;
+  if (h->planned || h->setup_done) return fail(h, TCG_ESTATE, "set_patches after plan/setup");
+  if (!npatch || !lo || !hi || !elems) return fail(h, TCG_EINVAL, "null argument");
+  if (degree_p < 1) return fail(h, TCG_EINVAL, "degree p must be >= 1");
+  for (int d = 0; d < 3; ++d) {
+    if (npatch[d] < 1 || elems[d] < 1) return fail(h, TCG_EINVAL, "patch/element counts must be >= 1");
+    if (!(lo[d] < hi[d])) return fail(h, TCG_EINVAL, "degenerate box");
+    h->plan.P[d] = npatch[d];
+    h->plan.el[d] = elems[d];
+    h->plan.lo[d] = lo[d];
+    h->plan.hi[d] = hi[d];
+  }
+  h->plan.p = degree_p;
+  h->have_patches = true;
+  return TCG_OK;
+}
+
+tcg_status tcg_set_materials(tcg_handle h, const double* sigma, const double* nu, size_t n) {
+  if (!h) return TCG_EINVAL;
+  if (h->planned || h->setup_done) return fail(h, TCG_ESTATE, "set_materials after plan/setup");
+  if (!h->have_patches) return fail(h, TCG_ESTATE, "set_patches first");
+  size_t P = (size_t)h->plan.P[0] * h->plan.P[1] * h->plan.P[2];
+  if (!sigma || !nu || n != P) return fail(h, TCG_EINVAL, "materials need one sigma and one nu per patch (" + std::to_string(P) + ")");
+  for (size_t s = 0; s < n; ++s) {
+    if (!(sigma[s] >= 0) || !std::isfinite(sigma[s])) return fail(h, TCG_EINVAL, "sigma must be finite and >= 0");
+    if (!(nu[s] > 0) || !std::isfinite(nu[s])) return fail(h, TCG_EINVAL, "nu must be finite and > 0");
+  }
+  h->plan.sigma.assign(sigma, sigma + n);
+  h->plan.nu.assign(nu, nu + n);
+  h->have_materials = true;
+  return TCG_OK;
+}
+
+tcg_status tcg_set_source(tcg_handle h, int kind) {
+  if (!h) return TCG_EINVAL;
+  if (h->setup_done) return fail(h, TCG_ESTATE, "set_source after setup");
+  if (kind < 0 || kind > 2) return fail(h, TCG_EINVAL, "unknown source kind");
+  h->source = kind;
+  return TCG_OK;
+}
+
+tcg_status tcg_set_time(tcg_handle h, double T, int n_steps) {
+  if (!h) return TCG_EINVAL;
+  if (h->setup_done) return fail(h, TCG_ESTATE, "set_time after setup");
+  if (!(T > 0) || n_steps < 1) return fail(h, TCG_EINVAL, "T > 0 and n_steps >= 1 required");
+  h->T = T;
+  h->n_steps = n_steps;
+  h->have_time = true;
+  return TCG_OK;
+}
+
+tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, int tree_order) {
+  if (!h) return TCG_EINVAL;
+  if (h->planned || h->setup_done) return fail(h, TCG_ESTATE, "set_solver after plan/setup");
+  if (!(rtol > 0) || max_iter < 1 || (scaling != 0 && scaling != 1) || (tree_order != 0 && tree_order != 1))
+    return fail(h, TCG_EINVAL, "invalid solver parameters");
+  h->rtol = rtol;
+  h->max_iter = max_iter;
+  h->scaling = scaling;
+  h->tree_order = tree_order;
+  return TCG_OK;
+}
+
+tcg_status tcg_plan(tcg_handle h) {
+  if (!h) return TCG_EINVAL;
+  return do_plan(h);
+}
+
+tcg_status tcg_get_plan(tcg_handle h, int what, int64_t* out, size_t len) {
+  if (!h) return TCG_EINVAL;
+  if (!h->planned) return fail(h, TCG_ESTATE, "plan first");
+  const Plan& p = h->plan;
+  size_t need = 0;
+  switch (what) {
+    case TCG_PLAN_EDGE_CLASS: case TCG_PLAN_EDGE_REGION: case TCG_PLAN_TREE: case TCG_PLAN_PART: need = p.nedges; break;
+    case TCG_PLAN_PATCH_COUNTS: need = 3 * (size_t)p.npatch; break;
+    case TCG_PLAN_LAMBDA: need = 3 * (size_t)p.m; break;
+    case TCG_PLAN_PRIMAL: need = p.nc; break;
+    case TCG_PLAN_RANK_OF_PATCH: need = p.npatch; break;
+    default: return fail(h, TCG_EINVAL, "unknown plan array");
+  }
+  if (!out || len < need) return fail(h, TCG_EINVAL, "buffer too short: need " + std::to_string(need));
+  for (size_t i = 0; i < need; ++i) {
+    int64_t v = 0;
+    switch (what) {
+      case TCG_PLAN_EDGE_CLASS: v = p.cls[i]; break;
+      case TCG_PLAN_EDGE_REGION: v = p.region[i]; break;
+      case TCG_PLAN_TREE: v = p.in_tree[i]; break;
+      case TCG_PLAN_PART: v = p.part[i]; break;
+      case TCG_PLAN_PATCH_COUNTS: {
+        const PatchPlan& q = p.pp[i / 3];
+        v = (i % 3 == 0) ? q.ni : (i % 3 == 1 ? q.nb : q.np);
+        break;
+      }
+      case TCG_PLAN_LAMBDA: {
+        size_t k = i / 3;
+        v = (i % 3 == 0) ? p.lam_edge[k] : (i % 3 == 1 ? p.lam_plus[k] : p.lam_minus[k]);
+        break;
+      }
+      case TCG_PLAN_PRIMAL: v = p.primal_edge[i]; break;
+      case TCG_PLAN_RANK_OF_PATCH: v = p.rank_of_patch[i]; break;
+    }
+    out[i] = v;
+  }
+  return TCG_OK;
+}
+
+tcg_status tcg_setup(tcg_handle h) {
+  if (!h) return TCG_EINVAL;
+  if (h->setup_done) return fail(h, TCG_ESTATE, "setup already done");
+  if (h->broken) return fail(h, TCG_ESTATE, "handle is in a failed state");
+  tcg_status s = do_setup(h);
+  if (s != TCG_OK && s != TCG_ENOTSPD) h->broken = true;
+  return s;
+}
+
+tcg_status tcg_step(tcg_handle h, int n) {
+  if (!h) return TCG_EINVAL;
+  if (!h->setup_done || h->broken) return fail(h, TCG_ESTATE, "setup first (or handle failed)");
+  if (n < 0) return fail(h, TCG_EINVAL, "n >= 0");
+  cudaSetDevice(h->device);
+  h->launches_last = 0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, h->stream);
+  for (int i = 0; i < n; ++i) {
+    tcg_status s = do_step(h);
+    if (s != TCG_OK) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      return s;
+    }
+  }
+  cudaEventRecord(e1, h->stream);
+  cudaEventSynchronize(e1);
+  h->ms_steps += elapsed_ms(e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return TCG_OK;
+}
+
+tcg_status tcg_get_coefficients(tcg_handle h, int layout, double* out, size_t len) {
+  if (!h) return TCG_EINVAL;
+  if (!h->setup_done) return fail(h, TCG_ESTATE, "setup first");
+  const Plan& p = h->plan;
+  cudaSetDevice(h->device);
+  if (layout == 0) {
+    size_t need = (size_t)p.npatch * p.nloc;
+    if (!out || len < need) return fail(h, TCG_EINVAL, "buffer too short: need " + std::to_string(need));
+    CK(cudaMemcpyAsync(out, h->a_loc, need * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  } else if (layout == 1) {
+    size_t need = (size_t)p.nedges;
+    if (!out || len < need) return fail(h, TCG_EINVAL, "buffer too short: need " + std::to_string(need));
+    k_gather_glued<<<592, 256, 0, h->stream>>>(h->glued, h->a_loc, h->d_glued_src, p.nedges);
+    CKL();
+    CK(cudaMemcpyAsync(out, h->glued, need * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  } else {
+    return fail(h, TCG_EINVAL, "layout must be 0 or 1");
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_get_history(tcg_handle h, int* iters, double* final_relres, size_t nsteps, double* relres_hist,
+                           size_t hist_len) {
+  if (!h) return TCG_EINVAL;
+  if (nsteps > h->iters.size()) return fail(h, TCG_EINVAL, "only " + std::to_string(h->iters.size()) + " steps recorded");
+  for (size_t i = 0; i < nsteps; ++i) {
+    if (iters) iters[i] = h->iters[i];
+    if (final_relres) final_relres[i] = h->final_rel[i];
+  }
+  if (relres_hist) {
+    size_t need = 0;
+    for (size_t i = 0; i < nsteps; ++i) need += h->iters[i] + 1;
+    if (hist_len < need) return fail(h, TCG_EINVAL, "history buffer too short: need " + std::to_string(need));
+    std::copy(h->hist_all.begin(), h->hist_all.begin() + need, relres_hist);
+  }
+  return TCG_OK;
+}
+
+tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
+  if (!h || !out) return TCG_EINVAL;
+  std::memset(out, 0, sizeof(tcg_info));
+  out->rank = h->rank;
+  out->world = h->world;
+  if (!h->planned) return TCG_OK;
+  const Plan& p = h->plan;
+  out->n_patches = p.npatch;
+  out->n_local = p.nloc;
+  out->n_edges = p.nedges;
+  out->n_verts = p.nverts;
+  out->m = p.m;
+  out->n_c = p.nc;
+  out->n_gauge = p.n_gauge;
+  out->n_dirichlet = p.n_dir;
+  out->nr_min = out->nb_min = out->np_min = INT64_MAX;
+  double bf = 0, bm = 0, bs = 0, fl = 0;
+  for (int s = 0; s < p.npatch; ++s) {
+    const PatchPlan& q = p.pp[s];
+    int64_t nr = q.ni + q.nb;
+    out->nr_min = std::min(out->nr_min, nr);
+    out->nr_max = std::max(out->nr_max, nr);
+    out->nb_min = std::min<int64_t>(out->nb_min, q.nb);
+    out->nb_max = std::max<int64_t>(out->nb_max, q.nb);
+    out->np_min = std::min<int64_t>(out->np_min, q.np);
+    out->np_max = std::max<int64_t>(out->np_max, q.np);
+    out->n_primal_local_total += q.np;
+    // algorithmic bytes: packed L_bb read twice, L_pb read twice per F-apply
+    bf += 8.0 * q.nb * (q.nb + 1) + 16.0 * q.nb * q.np;
+    bm += 4.0 * q.nb * (q.nb + 1);
+    double nrp = (double)nr;
+    bs += (p.sigma[s] > 0 ? 8.0 : 4.0) * nrp * (nrp + 1) + 8.0 * nrp * q.np;  // full passes per step
+    fl += nrp * nrp * nrp / 3.0 + 2.0 * nrp * nrp * q.np + 2.0 * nrp * q.np * q.np;
+  }
+  const double nc = (double)p.nc;
+  bf += 8.0 * nc * (nc + 1) + 40.0 * p.m;
+  bm += 40.0 * p.m;
+  bs += 2.0 * 8.0 * nc * (nc + 1);
+  fl += nc * nc * nc / 3.0;
+  out->bytes_fapply = bf;
+  out->bytes_precond = bm;
+  out->bytes_step_fixed = bs;
+  out->flops_factor = fl;
+  out->steps_done = h->steps_done;
+  out->total_iters = h->total_iters;
+  out->device_bytes = h->device_bytes;
+  out->kernel_launches = h->launches_last;
+  out->ms_plan = h->ms_plan;
+  out->ms_assembly = h->ms_assembly;
+  out->ms_factor = h->ms_factor;
+  out->ms_coarse = h->ms_coarse;
+  out->ms_steps = h->ms_steps;
+  out->ms_pcg_last_step = h->ms_pcg_last;
+  return TCG_OK;
+}
+
+tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms) {
+  if (!h || !ms) return TCG_EINVAL;
+  if (!h->setup_done || h->broken) return fail(h, TCG_ESTATE, "setup first");
+  cudaSetDevice(h->device);
+  DevPlan& D = h->D;
+  const int P = D.npatch;
+  // fixed input vector: the current multipliers (or whatever pk holds); state not done
+  CK(cudaMemsetAsync(h->st, 0, sizeof(PcgState), h->stream));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, h->stream);
+  for (int i = 0; i < n; ++i) {
+    k_fwd_ls<<<P, NTHR, h->smem_fwd_ls, h->stream>>>(D, h->r, h->XW, nullptr);
+    k_coarse_solve<<<1, NTHR, h->smem_coarse, h->stream>>>(D, h->XW, nullptr, h->Pc, nullptr);
+    k_bwd_ls<<<P, NTHR, h->smem_bwd_ls, h->stream>>>(D, h->XW, h->Pc, h->XW, nullptr);
+    k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->XW, h->q, nullptr, nullptr, h->st, h->partial, h->hist, JUMP_PLAIN, 1.0, 1);
+  }
+  cudaEventRecord(e1, h->stream);
+  CK(cudaEventSynchronize(e1));
+  *ms = elapsed_ms(e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CKL();
+  return TCG_OK;
+}
+
+// Debug readback (not part of the public header): what 0 = assembled augmented matrix of
+// patch `idx` (tile-packed, needs TCG_DEBUG_KEEP=1), 1 = its factor, 2 = aug map of patch,
+// 3 = assembled coarse matrix (tile-packed), 4 = X1 (aug-ordered rhs-stage vector of patch),
+// 5 = rho weights (w+, w-) interleaved, 6 = S_bb tiles of patch.
+tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t len) {
+  if (!h || !h->setup_done) return TCG_ESTATE;
+  cudaSetDevice(h->device);
+  const double* src = nullptr;
+  size_t n = 0;
+  std::vector<double> tmp;
+  if (what == 0 || what == 1) {
+    src = (what == 0 ? h->dbgA : h->D.A);
+    if (!src) return fail(h, TCG_ESTATE, "TCG_DEBUG_KEEP not set");
+    src += h->h_a_off[idx];
+    n = tri_tiles(h->h_T[idx]) * TSZ;
+  } else if (what == 2) {
+    const auto& aug = h->plan.pp[idx].aug;
+    for (int v : aug) tmp.push_back((double)v);
+  } else if (what == 3) {
+    src = h->dbgC;
+    if (!src) return fail(h, TCG_ESTATE, "TCG_DEBUG_KEEP not set");
+    n = tri_tiles(h->D.Tc) * TSZ;
+  } else if (what == 4) {
+    src = h->X1 + h->h_vec_off[idx];
+    n = (size_t)h->h_T[idx] * TS;
+  } else if (what == 5) {
+    std::vector<double> wp(h->D.m), wm(h->D.m);
+    CK(cudaMemcpy(wp.data(), h->D.wplus, sizeof(double) * h->D.m, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(wm.data(), h->D.wminus, sizeof(double) * h->D.m, cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < h->D.m; ++k) { tmp.push_back(wp[k]); tmp.push_back(wm[k]); }
+  } else if (what == 6) {
+    int64_t off = 0;
+    for (int s = 0; s < idx; ++s) off += tri_tiles(h->plan.pp[s].Tb) * TSZ;
+    src = h->D.Sbb + off;
+    n = tri_tiles(h->plan.pp[idx].Tb) * TSZ;
+  } else {
+    return TCG_EINVAL;
+  }
+  if (!tmp.empty()) {
+    if (len < tmp.size()) return fail(h, TCG_EINVAL, "need " + std::to_string(tmp.size()));
+    std::copy(tmp.begin(), tmp.end(), out);
+    return TCG_OK;
+  }
+  if (len < n) return fail(h, TCG_EINVAL, "need " + std::to_string(n));
+  CK(cudaMemcpy(out, src, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return TCG_OK;
+}
+
+const char* tcg_last_error(tcg_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+void tcg_destroy(tcg_handle h) { delete h; }
+
+}  // extern "C"

@@ -1,0 +1,263 @@
+// chol.cu — step b of the hot path: batched right-looking tiled FP64 Cholesky of the
+// gauged local matrices W^_rr (augmented with the primal rows) and of the coarse S_pp.
+//
+// Paper: local solves with W_rr, "two sequential Schur complements", done once
+// because the material is linear and dt fixed.
+// Layout: tile-packed lower triangle of 64x64 row-major tiles, matrix order
+// [i | b | p]. Factoring only the r tile columns (Tfact = Ti + Tb) leaves
+//   * the (p,r) block  = W^_pr L_rr^-T    (so Phi = W_rr^-1 W_rp = L_rr^-T L_pr^T),
+//   * the (p,p) block  = W^_pp - W^_pr W_rr^-1 W^_rp = S^s (local coarse contribution),
+// and the trailing (b,b) block at step k == Ti equals the interface Schur complement
+// S_bb = W_bb - W_bi W_ii^-1 W_ib, captured for the Dirichlet preconditioner.
+// Kernels per tile step k: capture (if k == Ti), POTRF of tile (k,k) + its triangular
+// inverse, TRSM of the tile column below (as a GEMM with the inverse), and the SYRK/GEMM
+// trailing update. The GEMMs run on the FP64 tensor pipe (mma.sync m8n8k4 f64 -> DMMA).
+#include "common.cuh"
+#include "device.h"
+
+namespace tcg {
+
+// -------------------------------------------------------------------------------------
+// 64x64 tile GEMM on DMMA: C = A B^T (mode 0) or C -= A B^T (mode 1). 128 threads.
+// -------------------------------------------------------------------------------------
+__device__ __forceinline__ void stage_tile(const double* __restrict__ g, double* s) {
+  for (int e = threadIdx.x; e < TSZ / 2; e += blockDim.x) {
+    int r = e / 32, c2 = e % 32;
+    double2 v = reinterpret_cast<const double2*>(g)[e];
+    s[r * SPAD + 2 * c2] = v.x;
+    s[r * SPAD + 2 * c2 + 1] = v.y;
+  }
+}
+
+__device__ void tile_gemm_nt(const double* A, const double* B, double* C, double* sA, double* sB, int mode) {
+  stage_tile(A, sA);
+  if (B != A) stage_tile(B, sB);
+  const double* sBB = (B != A) ? sB : sA;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < TS; k0 += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = sA[(wm + i * 8 + g) * SPAD + k0 + t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = sBB[(wn + j * 8 + g) * SPAD + k0 + t];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+  if (C == A) __syncthreads();  // in-place: everyone finished reading sA before C is written
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double2* pc = reinterpret_cast<double2*>(C + (wm + i * 8 + g) * TS + wn + j * 8 + 2 * t);
+      if (mode == 0) {
+        *pc = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        double2 c = *pc;
+        c.x -= acc[i][j][0];
+        c.y -= acc[i][j][1];
+        *pc = c;
+      }
+    }
+}
+
+// -------------------------------------------------------------------------------------
+// POTRF of diagonal tile (k,k) + triangular inverse into the Dinv store. One CTA/matrix.
+// -------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_potrf(const CholDesc* __restrict__ ds, int k, double* base, double* dinv,
+                                               DevError* err, int coarse) {
+  const CholDesc d = ds[blockIdx.x];
+  if (k >= d.Tfact) return;
+  extern __shared__ double smem[];
+  double* S = smem;              // 64 x 65
+  double* X = smem + TS * 65;    // 64 x 65
+  double* tile = base + d.a_off + tri_off(k, k);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < TSZ; e += blockDim.x) {
+    int r = e / TS, c = e % TS;
+    S[r * 65 + c] = (c <= r) ? tile[e] : 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < TS; ++j) {
+    if (tid == 0) {
+      double piv = S[j * 65 + j];
+      if (!(piv > 0.0)) {
+        if (atomicCAS(&err->flag, 0, 1) == 0) {
+          err->matrix = coarse ? -1 : (int)blockIdx.x;
+          err->index = k * TS + j;
+          err->value = piv;
+        }
+        piv = 1.0;
+      }
+      S[j * 65 + j] = sqrt(piv);
+    }
+    __syncthreads();
+    const double djj = S[j * 65 + j];
+    for (int i = j + 1 + tid; i < TS; i += blockDim.x) S[i * 65 + j] /= djj;
+    __syncthreads();
+    const int mm = TS - j - 1;
+    for (int e = tid; e < mm * mm; e += blockDim.x) {
+      int i = j + 1 + e / mm, c = j + 1 + e % mm;
+      if (c <= i) S[i * 65 + c] -= S[i * 65 + j] * S[c * 65 + j];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < TSZ; e += blockDim.x) {
+    int r = e / TS, c = e % TS;
+    tile[e] = (c <= r) ? S[r * 65 + c] : 0.0;
+  }
+  // inverse of the lower-triangular tile: column c by forward substitution
+  if (tid < TS) {
+    const int c = tid;
+    for (int r = 0; r < c; ++r) X[r * 65 + c] = 0.0;
+    X[c * 65 + c] = 1.0 / S[c * 65 + c];
+    for (int i = c + 1; i < TS; ++i) {
+      double s = 0.0;
+      for (int q = c; q < i; ++q) s += S[i * 65 + q] * X[q * 65 + c];
+      X[i * 65 + c] = -s / S[i * 65 + i];
+    }
+  }
+  __syncthreads();
+  double* out = dinv + d.dinv_off + (int64_t)k * TSZ;
+  for (int e = tid; e < TSZ; e += blockDim.x) out[e] = X[(e / TS) * 65 + (e % TS)];
+}
+
+// A_Ik <- A_Ik L_kk^-T for I in (k, T). grid (maxT-k-1, nmat).
+// subst = 0: GEMM with the inverse tile on DMMA; subst = 1: row-wise forward substitution.
+__global__ void __launch_bounds__(128) k_trsm(const CholDesc* __restrict__ ds, int k, double* base, const double* dinv,
+                                              int subst) {
+  const CholDesc d = ds[blockIdx.y];
+  const int I = k + 1 + blockIdx.x;
+  if (k >= d.Tfact || I >= d.T) return;
+  extern __shared__ double smem[];
+  double* A = base + d.a_off + tri_off(I, k);
+  if (!subst) {
+    const double* Li = dinv + d.dinv_off + (int64_t)k * TSZ;
+    tile_gemm_nt(A, Li, A, smem, smem + TS * SPAD, 0);
+    return;
+  }
+  double* sA = smem;            // 64 x 65
+  double* sL = smem + TS * 65;  // 64 x 65
+  const double* L = base + d.a_off + tri_off(k, k);
+  for (int e = threadIdx.x; e < TSZ; e += blockDim.x) {
+    sA[(e / TS) * 65 + (e % TS)] = A[e];
+    sL[(e / TS) * 65 + (e % TS)] = L[e];
+  }
+  __syncthreads();
+  if (threadIdx.x < TS) {
+    double* a = sA + threadIdx.x * 65;
+    for (int j = 0; j < TS; ++j) {
+      double v = a[j];
+      for (int q = 0; q < j; ++q) v -= sL[j * 65 + q] * a[q];
+      a[j] = v / sL[j * 65 + j];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < TSZ; e += blockDim.x) A[e] = sA[(e / TS) * 65 + (e % TS)];
+}
+
+// A_IJ -= L_Ik L_Jk^T for k < J <= I < T. grid (ntri, nmat).
+__global__ void __launch_bounds__(128) k_update(const CholDesc* __restrict__ ds, int k, double* base) {
+  const CholDesc d = ds[blockIdx.y];
+  if (k >= d.Tfact) return;
+  const int64_t y = blockIdx.x;
+  int Ip = (int)((sqrt(8.0 * (double)y + 1.0) - 1.0) * 0.5);
+  while ((int64_t)Ip * (Ip + 1) / 2 > y) --Ip;
+  while ((int64_t)(Ip + 1) * (Ip + 2) / 2 <= y) ++Ip;
+  const int Jp = (int)(y - (int64_t)Ip * (Ip + 1) / 2);
+  const int I = k + 1 + Ip, J = k + 1 + Jp;
+  if (I >= d.T) return;
+  extern __shared__ double smem[];
+  const double* LI = base + d.a_off + tri_off(I, k);
+  const double* LJ = base + d.a_off + tri_off(J, k);
+  double* C = base + d.a_off + tri_off(I, J);
+  tile_gemm_nt(LI, LJ, C, smem, smem + TS * SPAD, 1);
+}
+
+// Copy the trailing (b,b) block at step k == Ti: S_bb = W_bb - W_bi W_ii^-1 W_ib.
+__global__ void k_capture_sbb(const CholDesc* __restrict__ ds, int k, const double* base, double* sbb) {
+  const CholDesc d = ds[blockIdx.y];
+  if (d.Ti != k || d.sbb_off < 0) return;
+  const int64_t y = blockIdx.x;
+  if (y >= tri_tiles(d.Tb)) return;
+  int Ip = (int)((sqrt(8.0 * (double)y + 1.0) - 1.0) * 0.5);
+  while ((int64_t)Ip * (Ip + 1) / 2 > y) --Ip;
+  while ((int64_t)(Ip + 1) * (Ip + 2) / 2 <= y) ++Ip;
+  const int Jp = (int)(y - (int64_t)Ip * (Ip + 1) / 2);
+  const double* src = base + d.a_off + tri_off(d.Ti + Ip, d.Ti + Jp);
+  double* dst = sbb + d.sbb_off + tri_off(Ip, Jp);
+  for (int e = threadIdx.x; e < TSZ / 2; e += blockDim.x)
+    reinterpret_cast<double2*>(dst)[e] = reinterpret_cast<const double2*>(src)[e];
+}
+
+// Build the compact trailing store LS = [L_bb ; L_pb] (tile-packed: rows I<Tb lower, rows
+// I>=Tb full Tb tiles) with L_bb's diagonal tiles replaced by their inverses.
+__global__ void k_build_ls(DevPlan D) {
+  const int s = blockIdx.y;
+  const int Ti = D.Ti[s], Tb = D.Tb[s], Tp = D.Tp[s];
+  const int64_t ntile = tri_tiles(Tb) + (int64_t)Tp * Tb;
+  const int64_t y = blockIdx.x;
+  if (y >= ntile) return;
+  int I, J;
+  if (y < tri_tiles(Tb)) {
+    int Ip = (int)((sqrt(8.0 * (double)y + 1.0) - 1.0) * 0.5);
+    while ((int64_t)Ip * (Ip + 1) / 2 > y) --Ip;
+    while ((int64_t)(Ip + 1) * (Ip + 2) / 2 <= y) ++Ip;
+    I = Ip;
+    J = (int)(y - (int64_t)Ip * (Ip + 1) / 2);
+  } else {
+    int64_t z = y - tri_tiles(Tb);
+    I = Tb + (int)(z / Tb);
+    J = (int)(z % Tb);
+  }
+  const double* src = (I == J && !D.subst_local) ? D.Dinv + D.dinv_off[s] + (int64_t)(Ti + I) * TSZ
+                                                : D.A + D.a_off[s] + tri_off(Ti + I, Ti + J);
+  double* dst = D.LS + D.ls_off[s] + y * TSZ;
+  for (int e = threadIdx.x; e < TSZ / 2; e += blockDim.x)
+    reinterpret_cast<double2*>(dst)[e] = reinterpret_cast<const double2*>(src)[e];
+}
+
+// Coarse assembly S_pp = sum_s N_s^T S^s N_s, S^s = trailing (p,p) block of patch s.
+// Patches of one parity colour (ix%2, iy%2, iz%2) share no primal group, so each colour is
+// one conflict-free launch; colours run in a fixed order (deterministic sums).
+__global__ void k_coarse_scatter(DevPlan D, const int* __restrict__ patches, int npat) {
+  const int pi = blockIdx.x;
+  if (pi >= npat) return;
+  const int s = patches[pi];
+  const int Tr = D.Ti[s] + D.Tb[s];
+  const int np = D.np[s];
+  const int* grp = D.p_grp + D.p_off[s];
+  const double* A = D.A + D.a_off[s];
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+    const int a = e / np, b = e % np;
+    const int ga = grp[a], gb = grp[b];
+    if (ga < gb) continue;               // each unordered pair once, into the lower triangle
+    if (ga == gb && a != b) continue;    // cannot happen (a group appears once per patch)
+    // S^s[a][b] from the stored lower tiles (symmetric)
+    int ra = a, rb = b;
+    if ((ra >> 6) < (rb >> 6)) { int tmp = ra; ra = rb; rb = tmp; }
+    const double v = A[tri_off(Tr + (ra >> 6), Tr + (rb >> 6)) + (ra & 63) * TS + (rb & 63)];
+    const int GI = ga >> 6, GJ = gb >> 6;
+    double* dst = D.C + tri_off(GI, GJ) + (ga & 63) * TS + (gb & 63);
+    *dst += v;
+  }
+}
+
+// Identity padding of the coarse matrix diagonal beyond n_c.
+__global__ void k_coarse_pad(DevPlan D) {
+  int64_t g = D.nc + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= (int64_t)D.Tc * TS) return;
+  D.C[tri_off(g >> 6, g >> 6) + (g & 63) * TS + (g & 63)] = 1.0;
+}
+
+}  // namespace tcg

@@ -1,0 +1,81 @@
+// device.h — device-side views of the plan and the kernel entry points (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace tcg {
+
+// Geometry of one patch type (all patches of a config have the same shape).
+struct Geom {
+  int P[3];
+  int p;
+  int el[3];
+  int cdim[3][3];  // component c: index range along direction d
+  int nloc;
+};
+
+// 1D tables (a1): flat buffer with per-direction offsets.
+struct Tables1D {
+  double* base;
+  int64_t off_Mb[3], off_Md[3], off_Kb[3], off_C[3], off_oneD[3], off_sD[3], off_cB[3], off_sB[3];
+  int el[3];
+  int P[3];
+  double h[3];
+  double lo[3];
+};
+
+// Device copy of the plan and the big device arrays.
+struct DevPlan {
+  int npatch;
+  int64_t m, nc;
+  // per patch
+  const int* Ti;
+  const int* Tb;
+  const int* Tp;
+  const int* T;        // Ti+Tb+Tp
+  const int* nb;
+  const int* np;
+  const int64_t* a_off;     // augmented tile-packed factor
+  const int64_t* dinv_off;  // diagonal inverse tiles (Ti+Tb tiles)
+  const int64_t* ls_off;    // trailing [b;p] x b store
+  const int64_t* sbb_off;   // captured S_bb store
+  const int64_t* vec_off;   // aug-ordered per-patch vectors (64*T each)
+  const int64_t* aug_off;
+  const int* aug;           // aug position -> local id (-1 padding)
+  const int64_t* b_off;     // per patch offset into b_lam / b_sign
+  const int* b_lam;
+  const double* b_sign;
+  const int64_t* p_off;     // per patch offset into p_grp
+  const int* p_grp;
+  const int64_t* tile_start;  // prefix of T(T+1)/2 (npatch+1)
+  const double* sigma;
+  const double* nu;
+  // multipliers
+  const int* lam_patch_p;
+  const int* lam_patch_m;
+  const int* lam_pos_p;
+  const int* lam_pos_m;
+  const int64_t* lam_idx_p;  // index into aug-ordered vectors (b part) for the + side
+  const int64_t* lam_idx_m;
+  double* wplus;
+  double* wminus;
+  // coarse CSR
+  const int* coarse_ptr;
+  const int64_t* coarse_idx;  // index into aug-ordered vectors (p part)
+  // big arrays
+  double* A;      // augmented factors
+  double* Dinv;
+  double* LS;
+  double* Sbb;
+  // coarse factor
+  double* C;      // tile-packed lower n_c (Tc tiles)
+  double* Cinv;   // diagonal inverse tiles of C
+  int Tc;
+  int maxT, maxTbp;   // largest tile counts (shared-memory layout of the solver kernels)
+  int subst_local;    // 1: local triangular solves substitute on diagonal tiles (else inverse GEMV)
+  int subst_coarse;   // 1: same for the coarse factor
+};
+
+}  // namespace tcg

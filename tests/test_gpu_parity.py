@@ -1,0 +1,116 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded
+inputs. Bar (BASELINE.json north_star): relative l2 error of the final coefficient vector
+<= 1e-8 at PCG rtol 1e-10, PCG iteration counts within +-1 per step."""
+import copy
+
+import numpy as np
+import pytest
+
+import workloads
+from oracle.ietidp import Oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-8
+
+
+@pytest.fixture(scope="module")
+def tcg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2510_23446_b200 import build
+    build.build()
+    import paper_2510_23446_b200 as pkg
+    return pkg
+
+
+def run_gpu(tcg, pr, steps=None):
+    s = tcg.Solver().configure(pr)
+    s.setup()
+    s.step(pr.n_steps if steps is None else steps)
+    a1 = s.coefficients(1)
+    a0 = s.coefficients(0)
+    it, fr, hist = s.history()
+    inf = s.info()
+    s.close()
+    return a1, a0, it, hist, inf
+
+
+def compare(tcg, pr, steps=None, tol=TOL):
+    pr_o = copy.deepcopy(pr)
+    o = Oracle(pr_o)
+    n = pr.n_steps if steps is None else steps
+    o.run(n)
+    a1, a0, it, hist, inf = run_gpu(tcg, pr, n)
+    ref1 = o.coefficients(1)
+    err = np.linalg.norm(a1 - ref1) / np.linalg.norm(ref1)
+    err0 = np.linalg.norm(a0 - o.coefficients(0)) / np.linalg.norm(o.coefficients(0))
+    assert err <= tol, (err, list(it), o.iters)
+    assert err0 <= tol, err0
+    assert np.all(np.abs(np.array(it) - np.array(o.iters)) <= 1), (list(it), o.iters)
+    return err, it, o
+
+
+def test_cfg1_full(tcg):
+    """BJ configs[0], all 10 steps."""
+    err, it, o = compare(tcg, workloads.cfg1())
+    assert len(it) == 10
+
+
+def test_cfg1_unscaled_paper_preconditioner(tcg):
+    pr = workloads.cfg1()
+    pr.scaling = 0
+    compare(tcg, pr)
+
+
+SMALL = [
+    workloads.custom((2, 2, 2), 2, (2, 2, 2), [0, 0, 0, 0, 0, 0, 0, 10.0], [1, 2, 3, 4, 5, 6, 7, 8], n_steps=3,
+                     name="corner-conductor"),
+    workloads.custom((3, 3, 3), 1, (2, 2, 2), [1.0 if s == 13 else 0.0 for s in range(27)],
+                     np.linspace(0.5, 1.5, 27), n_steps=3, name="floating-centre"),
+    workloads.custom((3, 2, 2), 2, (1, 2, 1), [1e3 if s % 3 == 0 else 0.0 for s in range(12)], [1.0], n_steps=3,
+                     name="aniso"),
+    workloads.custom((2, 2, 1), 3, (2, 2, 2), [1e6, 0, 1e6, 0], [1e-3, 1, 1, 1e-2], n_steps=3, name="contrast"),
+    workloads.custom((2, 1, 1), 2, (2, 4, 4), [1.0, 0.0], [1.0, 1.0], n_steps=4, source=workloads.SOURCE_MMS,
+                     name="paper-2subdomain-mms"),
+    workloads.custom((3, 3, 2), 3, (3, 3, 3), [1e6 if s < 9 else 0.0 for s in range(18)],
+                     10.0 ** np.random.default_rng(0).uniform(-3, 0, 18), n_steps=3, name="p3-ragged-tiles"),
+]
+
+
+@pytest.mark.parametrize("pr", SMALL, ids=lambda p: p.name)
+def test_small_cases(tcg, pr):
+    compare(tcg, pr)
+
+
+def test_single_conductor_patch_zero_iterations(tcg):
+    pr = workloads.custom((1, 1, 1), 2, (2, 2, 2), [5.0], [0.5], n_steps=3)
+    err, it, o = compare(tcg, pr)
+    assert list(it) == [0, 0, 0]
+
+
+def test_zero_source(tcg):
+    pr = workloads.cfg1()
+    pr.n_steps = 2
+    pr.source = workloads.SOURCE_NONE
+    a1, a0, it, hist, inf = run_gpu(tcg, pr)
+    assert not a1.any() and list(it) == [0, 0]
+
+
+def test_cfg2_steps(tcg):
+    """BJ configs[1] (the bench workload): first 4 steps vs the oracle."""
+    compare(tcg, workloads.cfg2(), steps=4)
+
+
+def test_history_and_determinism(tcg):
+    pr = workloads.cfg1()
+    a, _, it1, h1, _ = run_gpu(tcg, pr, 4)
+    b, _, it2, h2, _ = run_gpu(tcg, pr, 4)
+    assert np.array_equal(a, b) and np.array_equal(it1, it2) and np.array_equal(h1, h2)
+    o = Oracle(workloads.cfg1()).run(4)
+    ref = np.concatenate([np.array(h) for h in o.hist])
+    if len(ref) == len(h1):
+        big = ref > 1e-6
+        assert np.all(np.abs(h1[big] - ref[big]) <= 1e-4 * ref[big])
+    assert h1[0] == 1.0

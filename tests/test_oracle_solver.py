@@ -168,7 +168,7 @@ def test_single_conductor_patch_is_direct_euler():
     a = np.zeros(o.topo.l2g.shape[1])
     for ell in range(3):
         t = (ell + 1) * o.dt
-        f = o.M[0] @ a / o.dt + math.sin(2 * math.pi * t) * o.jS[0]
+        f = o.M[0] @ a / o.dt + math.sin(2 * math.pi * t) * o.jS[0]   # t = 1/3, 2/3, 1 (~0)
         a = np.zeros_like(a)
         a[keep] = np.linalg.solve(W, f[keep])
     assert np.linalg.norm(o.a[0] - a) <= 1e-12 * np.linalg.norm(a)
@@ -202,6 +202,16 @@ def test_exact_discrete_solution(pr):
     o.step(load=load)
     got = o.coefficients(1)
     assert np.linalg.norm(got - c) <= 1e-8 * np.linalg.norm(c)
+
+
+def test_sinpi_exact():
+    """R19: sin(2 pi t) is exactly 0 at t in Z/2 and matches math.sin elsewhere."""
+    from oracle.assembly import sinpi
+    for x in (0.0, 1.0, 2.0, 3.0, 100.0):
+        assert sinpi(x) == 0.0
+    assert sinpi(0.5) == 1.0 and sinpi(1.5) == -1.0
+    for x in np.random.default_rng(0).uniform(0, 4, 200):
+        assert abs(sinpi(x) - math.sin(math.pi * x)) <= 4e-15
 
 
 def test_determinism():
