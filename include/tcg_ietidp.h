@@ -85,13 +85,17 @@ typedef struct tcg_info {
   int64_t nr_min, nr_max, nb_min, nb_max, np_min, np_max;
   int64_t steps_done, total_iters;
   int64_t device_bytes; /* bytes of device memory held by the handle                      */
-  int64_t kernel_launches; /* kernels launched by the last tcg_step call                 */
+  int64_t kernel_launches; /* kernels launched by this handle so far (cumulative)         */
   double bytes_fapply;  /* algorithmic HBM bytes of one F-apply (all patches + coarse)    */
   double bytes_precond; /* algorithmic HBM bytes of one preconditioner apply             */
   double bytes_step_fixed; /* algorithmic HBM bytes of one step outside the PCG loop     */
   double flops_factor;  /* local + coarse factorisation flops                            */
   double ms_plan, ms_assembly, ms_factor, ms_coarse, ms_steps; /* device-event timings     */
   double ms_pcg_last_step;
+  double prof_ms;       /* summed device time of the profiled kernel's working launches (tcg_set_profile) */
+  int64_t prof_launches; /* number of those launches                                      */
+  double prof_bytes_per_launch; /* algorithmic HBM bytes of one launch of the profiled kernel */
+  int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by this handle (cumulative)  */
   int32_t rank, world;
   int32_t pad_;
 } tcg_info;
@@ -134,6 +138,11 @@ tcg_status tcg_get_plan(tcg_handle h, int what, int64_t* out, size_t len);
  * batched FP64 Cholesky, coarse problem assembly and factorisation. */
 tcg_status tcg_setup(tcg_handle h);
 
+/* Re-run the numeric setup (assembly, batched Cholesky, coarse factorisation) on the
+ * existing allocations and reset the time stepping to t = 0, A = 0 (one "pass over one
+ * batch of input" for benchmarking; the plan and device memory are reused). */
+tcg_status tcg_refactor(tcg_handle h);
+
 /* Collective: n implicit-Euler steps (each: rhs, PCG on lambda, recovery). */
 tcg_status tcg_step(tcg_handle h, int n);
 
@@ -154,6 +163,11 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out);
  * sequence forward solve -> coarse -> backward solve -> jump) on a fixed vector;
  * returns the device time in *ms. Requires setup. */
 tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms);
+
+/* Time every launch of one solver kernel with CUDA events on the library stream during
+ * subsequent tcg_step calls (1 fwd_ls, 2 bwd_ls, 3 coarse_solve, 4 precond, 5 fwd_full,
+ * 6 bwd_full; 0 = off). Results in tcg_info.prof_*. Resets the accumulators. */
+tcg_status tcg_set_profile(tcg_handle h, int kernel_id);
 
 const char* tcg_last_error(tcg_handle h);
 void tcg_destroy(tcg_handle h);

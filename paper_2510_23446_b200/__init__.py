@@ -21,8 +21,8 @@ STATUS_NAMES = {0: "TCG_OK", -1: "TCG_EINVAL", -2: "TCG_ESTATE", -3: "TCG_ENOTSP
 PLAN_EDGE_CLASS, PLAN_EDGE_REGION, PLAN_TREE, PLAN_PART, PLAN_PATCH_COUNTS, PLAN_LAMBDA, PLAN_PRIMAL, PLAN_RANK_OF_PATCH = range(8)
 
 EXPORTS = ["tcg_create", "tcg_set_patches", "tcg_set_materials", "tcg_set_source", "tcg_set_time", "tcg_set_solver",
-           "tcg_plan", "tcg_get_plan", "tcg_setup", "tcg_step", "tcg_get_coefficients", "tcg_get_history",
-           "tcg_get_info", "tcg_bench_fapply", "tcg_last_error", "tcg_destroy"]
+           "tcg_plan", "tcg_get_plan", "tcg_setup", "tcg_refactor", "tcg_step", "tcg_get_coefficients", "tcg_get_history",
+           "tcg_get_info", "tcg_bench_fapply", "tcg_set_profile", "tcg_last_error", "tcg_destroy"]
 
 
 class TcgInfo(C.Structure):
@@ -31,8 +31,8 @@ class TcgInfo(C.Structure):
         "nr_min", "nr_max", "nb_min", "nb_max", "np_min", "np_max", "steps_done", "total_iters", "device_bytes",
         "kernel_launches")] + [(n, C.c_double) for n in (
         "bytes_fapply", "bytes_precond", "bytes_step_fixed", "flops_factor", "ms_plan", "ms_assembly", "ms_factor",
-        "ms_coarse", "ms_steps", "ms_pcg_last_step")] + [("rank", C.c_int32), ("world", C.c_int32),
-                                                         ("pad_", C.c_int32)]
+        "ms_coarse", "ms_steps", "ms_pcg_last_step", "prof_ms")] + [("prof_launches", C.c_int64),
+        ("prof_bytes_per_launch", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32), ("pad_", C.c_int32)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_ if n != "pad_"}
@@ -66,11 +66,13 @@ def lib():
     L.tcg_plan.argtypes = [vp]
     L.tcg_get_plan.argtypes = [vp, C.c_int, i64p, C.c_size_t]
     L.tcg_setup.argtypes = [vp]
+    L.tcg_refactor.argtypes = [vp]
     L.tcg_step.argtypes = [vp, C.c_int]
     L.tcg_get_coefficients.argtypes = [vp, C.c_int, dp, C.c_size_t]
     L.tcg_get_history.argtypes = [vp, ip, dp, C.c_size_t, dp, C.c_size_t]
     L.tcg_get_info.argtypes = [vp, C.POINTER(TcgInfo)]
     L.tcg_bench_fapply.argtypes = [vp, C.c_int, dp]
+    L.tcg_set_profile.argtypes = [vp, C.c_int]
     L.tcg_last_error.argtypes = [vp]
     L.tcg_last_error.restype = C.c_char_p
     L.tcg_destroy.argtypes = [vp]
@@ -139,6 +141,9 @@ class Solver:
     def setup(self):
         self._ck(self.L.tcg_setup(self.h))
 
+    def refactor(self):
+        self._ck(self.L.tcg_refactor(self.h))
+
     def step(self, n=1):
         self._ck(self.L.tcg_step(self.h, int(n)))
 
@@ -165,6 +170,9 @@ class Solver:
         hist = np.zeros(max(hl, 1))
         self._ck(self.L.tcg_get_history(self.h, None, None, ns, _dptr(hist), hl))
         return it, fr, hist[:hl]
+
+    def set_profile(self, kernel_id):
+        self._ck(self.L.tcg_set_profile(self.h, int(kernel_id)))
 
     def bench_fapply(self, n):
         ms = C.c_double()

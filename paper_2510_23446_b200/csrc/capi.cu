@@ -64,6 +64,8 @@ struct tcg_ctx {
   std::vector<int64_t> h_a_off, h_vec_off;
   std::vector<int> h_T;
   int64_t a_total = 0;
+  int64_t total_tiles = 0;
+  size_t smem_tables = 0;
   int64_t vec_total = 0;
   size_t smem_fwd_full = 0, smem_bwd_full = 0, smem_fwd_ls = 0, smem_bwd_ls = 0, smem_coarse = 0, smem_prec = 0;
 
@@ -72,6 +74,15 @@ struct tcg_ctx {
   std::vector<int> iters;
   std::vector<double> final_rel, hist_all;
   int64_t launches_last = 0;
+  int64_t nlaunch = 0;  // kernels launched by this handle (cumulative)
+  int64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device bytes moved by this handle (cumulative)
+  // optional per-kernel timing (tcg_set_profile): event pairs around each launch of one kernel
+  int prof_id = 0;
+  std::vector<cudaEvent_t> prof_ev;   // 2 per pair
+  std::vector<int> prof_tag;          // PCG iteration index of the pair (-1 outside the loop)
+  size_t prof_used = 0;
+  double prof_ms = 0;
+  int64_t prof_count = 0;
   double ms_plan = 0, ms_assembly = 0, ms_factor = 0, ms_coarse = 0, ms_steps = 0, ms_pcg_last = 0;
 
   ~tcg_ctx() { release(); }
@@ -131,6 +142,7 @@ tcg_status dupload(tcg_ctx* h, T** out, const std::vector<T>& v) {
   if (s != TCG_OK) return s;
   if (!v.empty()) {
     cudaError_t e = cudaMemcpyAsync(*out, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, h->stream);
+    h->h2d_bytes += (int64_t)(v.size() * sizeof(T));
     if (e != cudaSuccess) return fail(h, TCG_ECUDA, std::string("upload: ") + cudaGetErrorString(e));
   }
   return TCG_OK;
@@ -179,19 +191,111 @@ static tcg_status run_cholesky(tcg_ctx* h, const CholDesc* d_desc, int nmat, int
     if (sbb && maxTb > 0) {
       dim3 gc((unsigned)tri_tiles(maxTb), nmat);
       k_capture_sbb<<<gc, 256, 0, h->stream>>>(d_desc, k, base, sbb);
+      ++h->nlaunch;
       CKL();
     }
     k_potrf<<<nmat, 256, 2 * TS * 65 * sizeof(double), h->stream>>>(d_desc, k, base, dinv, h->derr, coarse);
+    ++h->nlaunch;
     CKL();
     int rows = maxT - k - 1;
     if (rows > 0) {
       dim3 gt(rows, nmat);
       k_trsm<<<gt, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(d_desc, k, base, dinv, subst);
+      ++h->nlaunch;
       CKL();
       dim3 gu((unsigned)tri_tiles(rows), nmat);
       k_update<<<gu, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(d_desc, k, base);
+      ++h->nlaunch;
       CKL();
     }
+  }
+  return TCG_OK;
+}
+
+// Numeric setup (step a + b of the hot path): 1D tables, assembly, rho weights, load,
+// batched local Cholesky (+ S_bb capture), trailing stores, coarse assembly + Cholesky,
+// insulator load precompute. Re-runnable on the same allocations (tcg_refactor).
+static tcg_status do_numeric(tcg_ctx* h) {
+  Plan& pl = h->plan;
+  DevPlan& D = h->D;
+  const int P = D.npatch;
+  const int Tc = D.Tc;
+  const double dt = h->T / h->n_steps;
+  cudaEvent_t e0, e1, e2, e3;
+  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3);
+  CK(cudaMemsetAsync(h->derr, 0, sizeof(DevError), h->stream));
+  CK(cudaEventRecord(e0, h->stream));
+  k_tables1d<<<3, 256, h->smem_tables, h->stream>>>(h->tb, pl.p);
+  ++h->nlaunch;
+  CKL();
+  k_assemble<<<(unsigned)h->total_tiles, 256, 0, h->stream>>>(D, h->tb, h->G, 1.0 / dt);
+  ++h->nlaunch;
+  CKL();
+  if (pl.m > 0) {
+    k_rho_weights<<<(unsigned)((pl.m + 255) / 256), 256, 0, h->stream>>>(D, h->scaling);
+    ++h->nlaunch;
+    CKL();
+  }
+  k_load_vector<<<P, 256, 0, h->stream>>>(D, h->tb, h->G, h->source, h->JS);
+  ++h->nlaunch;
+  CKL();
+  CK(cudaEventRecord(e1, h->stream));
+  if (h->dbgA) CK(cudaMemcpyAsync(h->dbgA, D.A, sizeof(double) * h->a_total, cudaMemcpyDeviceToDevice, h->stream));
+  TRY(run_cholesky(h, h->d_desc, P, h->maxT, h->maxTr, h->maxTb, D.A, D.Dinv, D.Sbb, 0));
+  if (h->max_ls_tiles > 0) {
+    dim3 gl((unsigned)h->max_ls_tiles, P);
+    k_build_ls<<<gl, 256, 0, h->stream>>>(D);
+    ++h->nlaunch;
+    CKL();
+  }
+  CK(cudaEventRecord(e2, h->stream));
+  CK(cudaMemsetAsync(D.C, 0, sizeof(double) * (size_t)tri_tiles(Tc) * TSZ, h->stream));
+  if (pl.nc > 0) {
+    for (int c = 0; c < 8; ++c) {
+      int cnt = (int)(h->colour_off[c + 1] - h->colour_off[c]);
+      if (cnt == 0) continue;
+      k_coarse_scatter<<<cnt, 256, 0, h->stream>>>(D, h->d_colour + h->colour_off[c], cnt);
+      ++h->nlaunch;
+      CKL();
+    }
+    int npad = Tc * TS - (int)pl.nc;
+    if (npad > 0) {
+      k_coarse_pad<<<(npad + 255) / 256, 256, 0, h->stream>>>(D);
+      ++h->nlaunch;
+      CKL();
+    }
+    if (h->dbgC) CK(cudaMemcpyAsync(h->dbgC, D.C, sizeof(double) * tri_tiles(Tc) * TSZ, cudaMemcpyDeviceToDevice, h->stream));
+    TRY(run_cholesky(h, h->d_cdesc, 1, Tc, Tc, 0, D.C, D.Cinv, nullptr, 1));
+  }
+  // insulator precompute: XJ = forward(j_S)
+  k_copy<<<592, 256, 0, h->stream>>>(h->XJ, h->JS, h->vec_total);
+  ++h->nlaunch;
+  CKL();
+  k_fwd_full<<<P, NTHR, h->smem_fwd_full, h->stream>>>(D, h->XJ, 0);
+  ++h->nlaunch;
+  CKL();
+  CK(cudaEventRecord(e3, h->stream));
+  // reset the time-stepping state
+  CK(cudaMemsetAsync(h->a_loc, 0, sizeof(double) * (size_t)P * pl.nloc, h->stream));
+  DevError herr;
+  CK(cudaMemcpyAsync(&herr, h->derr, sizeof(DevError), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->ms_assembly = elapsed_ms(e0, e1);
+  h->ms_factor = elapsed_ms(e1, e2);
+  h->ms_coarse = elapsed_ms(e2, e3);
+  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3);
+  h->steps_done = 0;
+  h->total_iters = 0;
+  h->iters.clear();
+  h->final_rel.clear();
+  h->hist_all.clear();
+  if (herr.flag) {
+    h->broken = true;
+    std::ostringstream o;
+    if (herr.matrix >= 0) o << "local Cholesky: patch " << herr.matrix;
+    else o << "coarse Cholesky";
+    o << " pivot " << herr.index << " value " << herr.value;
+    return fail(h, TCG_ENOTSPD, o.str());
   }
   return TCG_OK;
 }
@@ -424,87 +528,11 @@ static tcg_status do_setup(tcg_ctx* h) {
   }
   TRY(dalloc(h, &tb.base, toff));
 
-  cudaEvent_t e0, e1, e2, e3, e4;
-  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3); cudaEventCreate(&e4);
-  CK(cudaEventRecord(e0, h->stream));
-  {
-    int maxn = 0, maxel = 0;
-    for (int d = 0; d < 3; ++d) { maxn = std::max(maxn, pl.el[d] + pl.p); maxel = std::max(maxel, pl.el[d]); }
-    size_t smem = sizeof(double) * (2 * (pl.p + 1) + (size_t)maxel * (pl.p + 1) * (3 * maxn + 2));
-    TRY(set_smem(h, (const void*)k_tables1d, smem));
-    k_tables1d<<<3, 256, smem, h->stream>>>(tb, pl.p);
-    CKL();
-  }
-  k_assemble<<<(unsigned)tile_start[P], 256, 0, h->stream>>>(D, tb, G, 1.0 / dt);
-  CKL();
-  if (pl.m > 0) {
-    k_rho_weights<<<(unsigned)((pl.m + 255) / 256), 256, 0, h->stream>>>(D, h->scaling);
-    CKL();
-  }
-  k_load_vector<<<P, 256, 0, h->stream>>>(D, tb, G, h->source, h->JS);
-  CKL();
-  CK(cudaEventRecord(e1, h->stream));
-
-  const bool keep = getenv("TCG_DEBUG_KEEP") && atoi(getenv("TCG_DEBUG_KEEP")) != 0;
   h->h_a_off = a_off;
   h->h_vec_off = vec_off;
   h->h_T = T;
   h->a_total = oa;
-  if (keep) {
-    TRY(dalloc(h, &h->dbgA, oa));
-    CK(cudaMemcpyAsync(h->dbgA, D.A, sizeof(double) * oa, cudaMemcpyDeviceToDevice, h->stream));
-  }
-  // ---- batched local Cholesky ----
-  TRY(set_smem(h, (const void*)k_potrf, 2 * TS * 65 * sizeof(double)));
-  TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
-  TRY(set_smem(h, (const void*)k_update, 2 * TS * SPAD * sizeof(double)));
-  TRY(run_cholesky(h, h->d_desc, P, h->maxT, h->maxTr, h->maxTb, D.A, D.Dinv, D.Sbb, 0));
-  if (h->max_ls_tiles > 0) {
-    dim3 gl((unsigned)h->max_ls_tiles, P);
-    k_build_ls<<<gl, 256, 0, h->stream>>>(D);
-    CKL();
-  }
-  CK(cudaEventRecord(e2, h->stream));
-  DevError herr;
-  CK(cudaMemcpyAsync(&herr, h->derr, sizeof(DevError), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  if (herr.flag) {
-    h->broken = true;
-    std::ostringstream o;
-    o << "local Cholesky: patch " << herr.matrix << " pivot " << herr.index << " value " << herr.value;
-    return fail(h, TCG_ENOTSPD, o.str());
-  }
-
-  // ---- coarse problem ----
-  CK(cudaMemsetAsync(D.C, 0, sizeof(double) * (size_t)tri_tiles(Tc) * TSZ, h->stream));
-  if (pl.nc > 0) {
-    for (int c = 0; c < 8; ++c) {
-      int cnt = (int)(h->colour_off[c + 1] - h->colour_off[c]);
-      if (cnt == 0) continue;
-      k_coarse_scatter<<<cnt, 256, 0, h->stream>>>(D, h->d_colour + h->colour_off[c], cnt);
-      CKL();
-    }
-    int npad = Tc * TS - (int)pl.nc;
-    if (npad > 0) {
-      k_coarse_pad<<<(npad + 255) / 256, 256, 0, h->stream>>>(D);
-      CKL();
-    }
-    if (keep) {
-      TRY(dalloc(h, &h->dbgC, (size_t)tri_tiles(Tc) * TSZ));
-      CK(cudaMemcpyAsync(h->dbgC, D.C, sizeof(double) * tri_tiles(Tc) * TSZ, cudaMemcpyDeviceToDevice, h->stream));
-    }
-    TRY(run_cholesky(h, h->d_cdesc, 1, Tc, Tc, 0, D.C, D.Cinv, nullptr, 1));
-  }
-  CK(cudaEventRecord(e3, h->stream));
-  CK(cudaMemcpyAsync(&herr, h->derr, sizeof(DevError), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  if (herr.flag) {
-    h->broken = true;
-    std::ostringstream o;
-    o << "coarse Cholesky: pivot " << herr.index << " value " << herr.value;
-    return fail(h, TCG_ENOTSPD, o.str());
-  }
-
+  h->total_tiles = tile_start[P];
   // ---- solver kernel shared memory ----
   const size_t dtl = (h->stable_mask & 3) ? (size_t)TS * 65 : 0;  // staged diagonal tile for substitution
   h->smem_fwd_full = sizeof(double) * (TS + (size_t)h->maxT * TS + dtl);
@@ -513,24 +541,26 @@ static tcg_status do_setup(tcg_ctx* h) {
   h->smem_bwd_ls = sizeof(double) * (TS + 8 * TS + (size_t)h->maxTbp * TS + dtl);
   h->smem_coarse = sizeof(double) * (TS + 8 * TS + (size_t)Tc * TS + dtl);
   h->smem_prec = sizeof(double) * (10 * (size_t)h->maxTb * TS);
+  {
+    int maxn = 0, maxel = 0;
+    for (int d = 0; d < 3; ++d) { maxn = std::max(maxn, pl.el[d] + pl.p); maxel = std::max(maxel, pl.el[d]); }
+    h->smem_tables = sizeof(double) * (2 * (pl.p + 1) + (size_t)maxel * (pl.p + 1) * (3 * maxn + 2));
+  }
+  TRY(set_smem(h, (const void*)k_tables1d, h->smem_tables));
+  TRY(set_smem(h, (const void*)k_potrf, 2 * TS * 65 * sizeof(double)));
+  TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
+  TRY(set_smem(h, (const void*)k_update, 2 * TS * SPAD * sizeof(double)));
   TRY(set_smem(h, (const void*)k_fwd_full, h->smem_fwd_full));
   TRY(set_smem(h, (const void*)k_bwd_full, h->smem_bwd_full));
   TRY(set_smem(h, (const void*)k_fwd_ls, h->smem_fwd_ls));
   TRY(set_smem(h, (const void*)k_bwd_ls, h->smem_bwd_ls));
   TRY(set_smem(h, (const void*)k_coarse_solve, h->smem_coarse));
   TRY(set_smem(h, (const void*)k_precond, h->smem_prec));
-
-  // ---- insulator precompute: XJ = forward(j_S) ----
-  k_copy<<<592, 256, 0, h->stream>>>(h->XJ, h->JS, ov);
-  CKL();
-  k_fwd_full<<<P, NTHR, h->smem_fwd_full, h->stream>>>(D, h->XJ, 0);
-  CKL();
-  CK(cudaEventRecord(e4, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  h->ms_assembly = elapsed_ms(e0, e1);
-  h->ms_factor = elapsed_ms(e1, e2);
-  h->ms_coarse = elapsed_ms(e2, e3);
-  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3); cudaEventDestroy(e4);
+  if (getenv("TCG_DEBUG_KEEP") && atoi(getenv("TCG_DEBUG_KEEP")) != 0) {
+    TRY(dalloc(h, &h->dbgA, oa));
+    TRY(dalloc(h, &h->dbgC, (size_t)tri_tiles(Tc) * TSZ));
+  }
+  TRY(do_numeric(h));
   h->setup_done = true;
   return TCG_OK;
 }
@@ -538,18 +568,62 @@ static tcg_status do_setup(tcg_ctx* h) {
 // =========================================================================================
 // step
 // =========================================================================================
-static tcg_status launch_iteration(tcg_ctx* h, int64_t& nl) {
+static void prof_begin(tcg_ctx* h, int id, int tag) {
+  if (h->prof_id != id) return;
+  if (2 * h->prof_used + 2 > h->prof_ev.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    h->prof_ev.push_back(a);
+    h->prof_ev.push_back(b);
+    h->prof_tag.push_back(0);
+  }
+  h->prof_tag[h->prof_used] = tag;
+  cudaEventRecord(h->prof_ev[2 * h->prof_used], h->stream);
+}
+static void prof_end(tcg_ctx* h, int id) {
+  if (h->prof_id != id) return;
+  cudaEventRecord(h->prof_ev[2 * h->prof_used + 1], h->stream);
+  h->prof_used++;
+}
+// after a stream sync: accumulate the pairs of launches that did work (tag < iters)
+static void prof_collect(tcg_ctx* h, int iters) {
+  for (size_t i = 0; i < h->prof_used; ++i) {
+    if (h->prof_tag[i] >= iters) continue;
+    h->prof_ms += elapsed_ms(h->prof_ev[2 * i], h->prof_ev[2 * i + 1]);
+    h->prof_count += 1;
+  }
+  h->prof_used = 0;
+}
+
+static tcg_status launch_iteration(tcg_ctx* h, int64_t& nl, int it) {
   DevPlan& D = h->D;
   const int P = D.npatch;
   const int64_t m = D.m;
+  prof_begin(h, 1, it);
   k_fwd_ls<<<P, NTHR, h->smem_fwd_ls, h->stream>>>(D, h->pk, h->XW, h->st);
+  ++h->nlaunch;
+  prof_end(h, 1);
+  prof_begin(h, 3, it);
   k_coarse_solve<<<1, NTHR, h->smem_coarse, h->stream>>>(D, h->XW, nullptr, h->Pc, h->st);
+  ++h->nlaunch;
+  prof_end(h, 3);
+  prof_begin(h, 2, it);
   k_bwd_ls<<<P, NTHR, h->smem_bwd_ls, h->stream>>>(D, h->XW, h->Pc, h->XW, h->st);
+  ++h->nlaunch;
+  prof_end(h, 2);
   k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->XW, h->q, h->pk, nullptr, h->st, h->partial, h->hist, JUMP_F, h->rtol, h->max_iter);
+  ++h->nlaunch;
   k_axpy<<<RED_BLOCKS, 256, 0, h->stream>>>(h->lam, h->r, h->pk, h->q, h->st, m);
+  ++h->nlaunch;
+  prof_begin(h, 4, it);
   k_precond<<<P, NTHR, h->smem_prec, h->stream>>>(D, h->r, h->PW, h->st);
+  ++h->nlaunch;
+  prof_end(h, 4);
   k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->PW, h->z, h->r, nullptr, h->st, h->partial, h->hist, JUMP_M, h->rtol, h->max_iter);
+  ++h->nlaunch;
   k_xpay<<<RED_BLOCKS, 256, 0, h->stream>>>(h->pk, h->z, h->st, m, 0);
+  ++h->nlaunch;
   nl += 8;
   CKL();
   return TCG_OK;
@@ -565,21 +639,33 @@ static tcg_status do_step(tcg_ctx* h) {
   CK(cudaMemsetAsync(h->st, 0, sizeof(PcgState), h->stream));
   // rhs: f, forward solves, dual rhs d = B (x1 - Phi N p0)
   k_rhs<<<P, 256, 0, h->stream>>>(D, h->tb, h->G, h->source, t, 1.0 / dt, h->JS, h->XJ, h->a_loc, h->X1);
+  ++h->nlaunch;
+  prof_begin(h, 5, -1);
   k_fwd_full<<<P, NTHR, h->smem_fwd_full, h->stream>>>(D, h->X1, 1);
+  ++h->nlaunch;
+  prof_end(h, 5);
   k_coarse_solve<<<1, NTHR, h->smem_coarse, h->stream>>>(D, h->X1, nullptr, h->Pc, nullptr);
+  ++h->nlaunch;
   k_bwd_ls<<<P, NTHR, h->smem_bwd_ls, h->stream>>>(D, h->X1, h->Pc, h->XW, nullptr);
+  ++h->nlaunch;
   k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->XW, h->r, nullptr, h->lam, h->st, h->partial, h->hist, JUMP_D, h->rtol, h->max_iter);
+  ++h->nlaunch;
   k_precond<<<P, NTHR, h->smem_prec, h->stream>>>(D, h->r, h->PW, h->st);
+  ++h->nlaunch;
   k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->PW, h->z, h->r, nullptr, h->st, h->partial, h->hist, JUMP_M0, h->rtol, h->max_iter);
+  ++h->nlaunch;
   k_xpay<<<RED_BLOCKS, 256, 0, h->stream>>>(h->pk, h->z, h->st, m, 1);
+  ++h->nlaunch;
   nl += 8;
   CKL();
   // PCG: chunks of iterations, device-side convergence flag, one host check per chunk
   const int chunk = 8;
   int iters = 0;
+  int launched = 0;
   for (;;) {
-    for (int c = 0; c < chunk; ++c) TRY(launch_iteration(h, nl));
+    for (int c = 0; c < chunk; ++c) TRY(launch_iteration(h, nl, launched++));
     CK(cudaMemcpyAsync(h->h_st, h->st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
+    h->d2h_bytes += (int64_t)sizeof(PcgState);
     CK(cudaStreamSynchronize(h->stream));
     iters = h->h_st->iter;
     if (h->h_st->done) break;
@@ -594,13 +680,20 @@ static tcg_status do_step(tcg_ctx* h) {
   }
   // recovery
   k_fwd_ls<<<P, NTHR, h->smem_fwd_ls, h->stream>>>(D, h->lam, h->XW, nullptr);
+  ++h->nlaunch;
   k_coarse_solve<<<1, NTHR, h->smem_coarse, h->stream>>>(D, h->X1, h->XW, h->Pc, nullptr);
+  ++h->nlaunch;
+  prof_begin(h, 6, -1);
   k_bwd_full<<<P, NTHR, h->smem_bwd_full, h->stream>>>(D, h->X1, h->XW, h->Pc, h->a_loc, h->G.nloc);
+  ++h->nlaunch;
+  prof_end(h, 6);
   nl += 3;
   CKL();
   std::vector<double> hh(iters + 1);
   CK(cudaMemcpyAsync(hh.data(), h->hist, sizeof(double) * (iters + 1), cudaMemcpyDeviceToHost, h->stream));
+  h->d2h_bytes += (int64_t)(sizeof(double) * (iters + 1));
   CK(cudaStreamSynchronize(h->stream));
+  prof_collect(h, iters);
   h->iters.push_back(iters);
   h->final_rel.push_back(hh.back());
   h->hist_all.insert(h->hist_all.end(), hh.begin(), hh.end());
@@ -748,6 +841,13 @@ tcg_status tcg_setup(tcg_handle h) {
   return s;
 }
 
+tcg_status tcg_refactor(tcg_handle h) {
+  if (!h) return TCG_EINVAL;
+  if (!h->setup_done || h->broken) return fail(h, TCG_ESTATE, "setup first (or handle failed)");
+  cudaSetDevice(h->device);
+  return do_numeric(h);
+}
+
 tcg_status tcg_step(tcg_handle h, int n) {
   if (!h) return TCG_EINVAL;
   if (!h->setup_done || h->broken) return fail(h, TCG_ESTATE, "setup first (or handle failed)");
@@ -783,12 +883,15 @@ tcg_status tcg_get_coefficients(tcg_handle h, int layout, double* out, size_t le
     size_t need = (size_t)p.npatch * p.nloc;
     if (!out || len < need) return fail(h, TCG_EINVAL, "buffer too short: need " + std::to_string(need));
     CK(cudaMemcpyAsync(out, h->a_loc, need * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    h->d2h_bytes += (int64_t)(need * sizeof(double));
   } else if (layout == 1) {
     size_t need = (size_t)p.nedges;
     if (!out || len < need) return fail(h, TCG_EINVAL, "buffer too short: need " + std::to_string(need));
     k_gather_glued<<<592, 256, 0, h->stream>>>(h->glued, h->a_loc, h->d_glued_src, p.nedges);
+    ++h->nlaunch;
     CKL();
     CK(cudaMemcpyAsync(out, h->glued, need * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    h->d2h_bytes += (int64_t)(need * sizeof(double));
   } else {
     return fail(h, TCG_EINVAL, "layout must be 0 or 1");
   }
@@ -859,7 +962,28 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
   out->steps_done = h->steps_done;
   out->total_iters = h->total_iters;
   out->device_bytes = h->device_bytes;
-  out->kernel_launches = h->launches_last;
+  out->kernel_launches = h->nlaunch;
+  out->prof_ms = h->prof_ms;
+  out->h2d_bytes = h->h2d_bytes;
+  out->d2h_bytes = h->d2h_bytes;
+  out->prof_launches = h->prof_count;
+  {
+    // algorithmic bytes per launch of the profiled kernel
+    double b = 0;
+    for (int s = 0; s < p.npatch; ++s) {
+      const PatchPlan& q = p.pp[s];
+      double nb = q.nb, np = q.np, nr = q.ni + q.nb;
+      switch (h->prof_id) {
+        case 1: case 2: b += 8.0 * (nb * (nb + 1) / 2 + nb * np) + 16.0 * nb + 8.0 * np; break;
+        case 4: b += 4.0 * nb * (nb + 1) + 16.0 * nb; break;
+        case 5: if (p.sigma[s] > 0) b += 8.0 * (nr * (nr + 1) / 2 + nr * np) + 16.0 * (nr + np); break;
+        case 6: b += 8.0 * (nr * (nr + 1) / 2 + nr * np) + 16.0 * (nr + np); break;
+        default: break;
+      }
+    }
+    if (h->prof_id == 3) b = 8.0 * nc * (nc + 1) + 16.0 * nc;
+    out->prof_bytes_per_launch = b;
+  }
   out->ms_plan = h->ms_plan;
   out->ms_assembly = h->ms_assembly;
   out->ms_factor = h->ms_factor;
@@ -883,9 +1007,13 @@ tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms) {
   cudaEventRecord(e0, h->stream);
   for (int i = 0; i < n; ++i) {
     k_fwd_ls<<<P, NTHR, h->smem_fwd_ls, h->stream>>>(D, h->r, h->XW, nullptr);
+    ++h->nlaunch;
     k_coarse_solve<<<1, NTHR, h->smem_coarse, h->stream>>>(D, h->XW, nullptr, h->Pc, nullptr);
+    ++h->nlaunch;
     k_bwd_ls<<<P, NTHR, h->smem_bwd_ls, h->stream>>>(D, h->XW, h->Pc, h->XW, nullptr);
+    ++h->nlaunch;
     k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->XW, h->q, nullptr, nullptr, h->st, h->partial, h->hist, JUMP_PLAIN, 1.0, 1);
+    ++h->nlaunch;
   }
   cudaEventRecord(e1, h->stream);
   CK(cudaEventSynchronize(e1));
@@ -941,6 +1069,16 @@ tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t 
   }
   if (len < n) return fail(h, TCG_EINVAL, "need " + std::to_string(n));
   CK(cudaMemcpy(out, src, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return TCG_OK;
+}
+
+tcg_status tcg_set_profile(tcg_handle h, int kernel_id) {
+  if (!h) return TCG_EINVAL;
+  if (kernel_id < 0 || kernel_id > 6) return fail(h, TCG_EINVAL, "kernel id 0..6");
+  h->prof_id = kernel_id;
+  h->prof_ms = 0;
+  h->prof_count = 0;
+  h->prof_used = 0;
   return TCG_OK;
 }
 
