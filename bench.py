@@ -31,7 +31,7 @@ import numpy as np  # noqa: E402
 
 import workloads  # noqa: E402
 
-KERNELS = {1: "k_fwd_ls", 2: "k_bwd_ls", 3: "k_coarse_solve", 4: "k_precond", 5: "k_fwd_full", 6: "k_bwd_full"}
+KERNELS = {5: "k_fwd_full", 6: "k_bwd_full", 7: "k_pcg"}
 
 
 def peaks():
@@ -241,9 +241,15 @@ def main():
             one_pass()
             i2 = s.info()
             if i2["prof_launches"] > 0:
+                bpl = i2["prof_bytes_per_launch"]
+                if kid == 7:
+                    # persistent PCG: per launch (= per Euler step) it * (B_F + B_M) + B_M (prologue z0)
+                    it, _, _ = s.history()
+                    bpl = float(np.mean([k * (i2["bytes_fapply"] + i2["bytes_precond"]) + i2["bytes_precond"]
+                                         for k in it]))
                 shares[KERNELS[kid]] = {"ms_per_pass": i2["prof_ms"], "launches": i2["prof_launches"],
                                         "us_per_launch": 1000 * i2["prof_ms"] / i2["prof_launches"],
-                                        "bytes_per_launch": i2["prof_bytes_per_launch"]}
+                                        "bytes_per_launch": bpl}
                 if best is None or i2["prof_ms"] > shares[KERNELS[best]]["ms_per_pass"]:
                     best = kid
         s.set_profile(0)

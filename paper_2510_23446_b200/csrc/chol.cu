@@ -200,33 +200,6 @@ __global__ void k_capture_sbb(const CholDesc* __restrict__ ds, int k, const doub
     reinterpret_cast<double2*>(dst)[e] = reinterpret_cast<const double2*>(src)[e];
 }
 
-// Build the compact trailing store LS = [L_bb ; L_pb] (tile-packed: rows I<Tb lower, rows
-// I>=Tb full Tb tiles) with L_bb's diagonal tiles replaced by their inverses.
-__global__ void k_build_ls(DevPlan D) {
-  const int s = blockIdx.y;
-  const int Ti = D.Ti[s], Tb = D.Tb[s], Tp = D.Tp[s];
-  const int64_t ntile = tri_tiles(Tb) + (int64_t)Tp * Tb;
-  const int64_t y = blockIdx.x;
-  if (y >= ntile) return;
-  int I, J;
-  if (y < tri_tiles(Tb)) {
-    int Ip = (int)((sqrt(8.0 * (double)y + 1.0) - 1.0) * 0.5);
-    while ((int64_t)Ip * (Ip + 1) / 2 > y) --Ip;
-    while ((int64_t)(Ip + 1) * (Ip + 2) / 2 <= y) ++Ip;
-    I = Ip;
-    J = (int)(y - (int64_t)Ip * (Ip + 1) / 2);
-  } else {
-    int64_t z = y - tri_tiles(Tb);
-    I = Tb + (int)(z / Tb);
-    J = (int)(z % Tb);
-  }
-  const double* src = (I == J && !D.subst_local) ? D.Dinv + D.dinv_off[s] + (int64_t)(Ti + I) * TSZ
-                                                : D.A + D.a_off[s] + tri_off(Ti + I, Ti + J);
-  double* dst = D.LS + D.ls_off[s] + y * TSZ;
-  for (int e = threadIdx.x; e < TSZ / 2; e += blockDim.x)
-    reinterpret_cast<double2*>(dst)[e] = reinterpret_cast<const double2*>(src)[e];
-}
-
 // Coarse assembly S_pp = sum_s N_s^T S^s N_s, S^s = trailing (p,p) block of patch s.
 // Patches of one parity colour (ix%2, iy%2, iz%2) share no primal group, so each colour is
 // one conflict-free launch; colours run in a fixed order (deterministic sums).
@@ -258,6 +231,142 @@ __global__ void k_coarse_pad(DevPlan D) {
   int64_t g = D.nc + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= (int64_t)D.Tc * TS) return;
   D.C[tri_off(g >> 6, g >> 6) + (g & 63) * TS + (g & 63)] = 1.0;
+}
+
+}  // namespace tcg
+
+namespace tcg {
+
+// -------------------------------------------------------------------------------------
+// Inverse factors for the chain-free PCG (DESIGN.md §5 "F-apply"):
+//   X = L^-1 by blocked inversion  X_II = L_II^-1,  X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ,
+//   Phi^T = L_pb X_bb  (= W_pr W_rr^-1 restricted to the b columns).
+// All tile products on DMMA. acc[4][4][2] holds a 64x64 tile as in tile_gemm_nt.
+// -------------------------------------------------------------------------------------
+__device__ __forceinline__ void stage_tile_T(const double* __restrict__ g, double* s) {  // s[n][k] = g[k][n]
+  for (int e = threadIdx.x; e < TSZ; e += blockDim.x) {
+    int k = e / TS, n = e % TS;
+    s[n * SPAD + k] = g[e];
+  }
+}
+
+__device__ __forceinline__ void mma_acc(const double* sA, const double* sB, double (&acc)[4][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+#pragma unroll 4
+  for (int k0 = 0; k0 < TS; k0 += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = sA[(wm + i * 8 + g) * SPAD + k0 + t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = sB[(wn + j * 8 + g) * SPAD + k0 + t];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+}
+
+__device__ __forceinline__ void acc_zero(double (&acc)[4][4][2]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+// write acc (scaled) to a row-major global tile
+__device__ __forceinline__ void acc_store(double* C, const double (&acc)[4][4][2], double scale) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<double2*>(C + (wm + i * 8 + g) * TS + wn + j * 8 + 2 * t) =
+          make_double2(scale * acc[i][j][0], scale * acc[i][j][1]);
+}
+
+// write acc into smem as the B operand of a following NN product (sB[n][k] = acc[k][n])
+__device__ __forceinline__ void acc_to_smemT(double* sB, const double (&acc)[4][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = wm + i * 8 + g, n = wn + j * 8 + 2 * t;
+      sB[n * SPAD + m] = acc[i][j][0];
+      sB[(n + 1) * SPAD + m] = acc[i][j][1];
+    }
+}
+
+struct InvDesc {
+  int64_t l_off;     // matrix L (tile-packed lower) base offset in Lbase
+  int64_t x_off;     // output X base offset (tile-packed lower, T tiles) in Xbase
+  int64_t dinv_off;  // diagonal inverses base in Dbase
+  int shift;         // L tile (I,J) = tile (shift+I, shift+J); diag inverse index shift+I
+  int T;             // tiles to invert
+};
+
+// Row I of X = L^-1 for every matrix with T > I. grid (I+1, nmat), 128 threads.
+__global__ void __launch_bounds__(128) k_trinv_row(const InvDesc* __restrict__ ds, int I, const double* Lbase,
+                                                   double* Xbase, const double* Dbase) {
+  const InvDesc d = ds[blockIdx.y];
+  const int J = blockIdx.x;
+  if (I >= d.T || J > I) return;
+  extern __shared__ double smem[];
+  double* sA = smem;
+  double* sB = smem + TS * SPAD;
+  const double* Linv = Dbase + d.dinv_off + (int64_t)(d.shift + I) * TSZ;
+  double* X = Xbase + d.x_off + tri_off(I, J);
+  if (J == I) {
+    for (int e = threadIdx.x; e < TSZ / 2; e += blockDim.x)
+      reinterpret_cast<double2*>(X)[e] = reinterpret_cast<const double2*>(Linv)[e];
+    return;
+  }
+  double acc[4][4][2];
+  acc_zero(acc);
+  for (int K = J; K < I; ++K) {
+    stage_tile(Lbase + d.l_off + tri_off(d.shift + I, d.shift + K), sA);
+    stage_tile_T(Xbase + d.x_off + tri_off(K, J), sB);
+    __syncthreads();
+    mma_acc(sA, sB, acc);
+    __syncthreads();
+  }
+  acc_to_smemT(sB, acc);
+  stage_tile(Linv, sA);
+  __syncthreads();
+  double acc2[4][4][2];
+  acc_zero(acc2);
+  mma_acc(sA, sB, acc2);
+  acc_store(X, acc2, -1.0);
+}
+
+// Phi^T tiles (Tp x Tb) of every patch: PhiT_{Ip,J} = sum_{K=J}^{Tb-1} L(Ti+Tb+Ip, Ti+K) X_bb(K,J),
+// written into the LS store below X_bb. grid (maxTp*maxTb, P), 128 threads.
+__global__ void __launch_bounds__(128) k_phiT(DevPlan D, int maxTb) {
+  const int s = blockIdx.y;
+  const int Ti = D.Ti[s], Tb = D.Tb[s], Tp = D.Tp[s];
+  const int Ip = blockIdx.x / maxTb, J = blockIdx.x % maxTb;
+  if (Ip >= Tp || J >= Tb) return;
+  extern __shared__ double smem[];
+  double* sA = smem;
+  double* sB = smem + TS * SPAD;
+  const double* A = D.A + D.a_off[s];
+  const double* X = D.LS + D.ls_off[s];
+  double acc[4][4][2];
+  acc_zero(acc);
+  for (int K = J; K < Tb; ++K) {
+    stage_tile(A + tri_off(Ti + Tb + Ip, Ti + K), sA);
+    stage_tile_T(X + tri_off(K, J), sB);
+    __syncthreads();
+    mma_acc(sA, sB, acc);
+    __syncthreads();
+  }
+  acc_store(D.LS + D.ls_off[s] + (tri_tiles(Tb) + (int64_t)Ip * Tb + J) * TSZ, acc, 1.0);
 }
 
 }  // namespace tcg

@@ -29,6 +29,7 @@ struct PcgState {
   int done;        // 1 once converged (or max_iter reached); later kernels are no-ops
   int failed;      // 1 if max_iter reached without convergence
   int nan;         // 1 if a NaN/negative curvature guard fired
+  int rp;          // buffer holding the final residual (persistent PCG)
   unsigned int counter[4];  // last-block-done counters for deterministic reductions
 };
 
