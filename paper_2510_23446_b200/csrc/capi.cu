@@ -71,12 +71,18 @@ struct tcg_ctx {
   InvDesc* d_inv = nullptr;
   InvDesc* d_cinv = nullptr;
   int maxTp = 0;
-  int n_p1 = 0, n_p5 = 0, n_sy = 0;
+  int n_p1 = 0, n_p5 = 0, n_sy = 0, n_p3 = 0, n_p4 = 0;
   int2* d_it_p1 = nullptr;
   int2* d_it_p5 = nullptr;
-  int* d_it_sy = nullptr;
+  int2* d_it_sy = nullptr;
+  int2* d_it_p3 = nullptr;
+  int2* d_it_p4 = nullptr;
+  double *PWc = nullptr, *Ypart = nullptr, *Ppart = nullptr;
+  int64_t* d_pwc_off = nullptr;
+  int coarse_ch = 1, coarse_maxch = 1;
   size_t smem_pcg = 0;
   int pcg_blocks = 0;
+  unsigned long long* tstamp = nullptr;  // TCG_PHASE_TIMING=1: per-phase timestamps of the persistent PCG
   size_t smem_tables = 0;
   int64_t vec_total = 0;
   size_t smem_fwd_full = 0, smem_bwd_full = 0;
@@ -498,6 +504,10 @@ static tcg_status do_setup(tcg_ctx* h) {
   TRY(dalloc(h, &h->Yc, (size_t)Tc * TS));
   TRY(dalloc(h, &h->partA, 4096));
   TRY(dalloc(h, &h->partB, 4096));
+  if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) {
+    TRY(dalloc(h, &h->tstamp, 8 * 64));
+    CK(cudaMemsetAsync(h->tstamp, 0, 8 * 64 * sizeof(unsigned long long), h->stream));
+  }
   CK(cudaMemsetAsync(h->Yv, 0, sizeof(double) * ov, h->stream));
   {
     std::vector<InvDesc> inv(P);
@@ -510,29 +520,45 @@ static tcg_status do_setup(tcg_ctx* h) {
     std::vector<InvDesc> cinv(1, InvDesc{0, 0, 0, 0, Tc});
     TRY(dupload(h, &h->d_cinv, cinv));
     // work items, largest first (round-robin over the persistent blocks)
-    std::vector<std::pair<int, int2>> p1, p5, sy;
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device);
+    const int64_t ctiles = tri_tiles(Tc);
+    h->coarse_ch = (int)std::max<int64_t>(1, std::min<int64_t>(64, ctiles / (4 * (int64_t)dev_sms)));
+    h->coarse_maxch = std::max(1, (Tc + h->coarse_ch - 1) / h->coarse_ch);
+    std::vector<std::pair<int, int2>> p1, p5, sy, p3, p4;
+    std::vector<int64_t> pwc_off(P);
+    int64_t opwc = 0;
     for (int s = 0; s < P; ++s) {
       for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.push_back({I < Tb[s] ? I + 1 : Tb[s], make_int2(s, I)});
       for (int J = 0; J < Tb[s]; ++J) p5.push_back({Tb[s] - J + Tp[s], make_int2(s, J)});
-      if (Tb[s] > 0) sy.push_back({Tb[s] * (Tb[s] + 1) / 2, make_int2(s, 0)});
+      for (int I = 0; I < Tb[s]; ++I) sy.push_back({I + 1, make_int2(s, I)});
+      pwc_off[s] = opwc;
+      opwc += (int64_t)Tb[s] * Tb[s] * TS;
     }
-    auto bycost = [](const std::pair<int, int2>& a, const std::pair<int, int2>& b) {
-      return a.first != b.first ? a.first > b.first : (a.second.x != b.second.x ? a.second.x < b.second.x : a.second.y < b.second.y);
+    const int ch = h->coarse_ch;
+    for (int I = 0; I < Tc; ++I)
+      for (int c = 0; c * ch <= I; ++c) p3.push_back({std::min(I + 1, (c + 1) * ch) - c * ch, make_int2(I, c)});
+    for (int J = 0; J < Tc; ++J)
+      for (int c = 0; J + c * ch < Tc; ++c) p4.push_back({std::min(Tc, J + (c + 1) * ch) - (J + c * ch), make_int2(J, c)});
+    auto bycost = [](const std::pair<int, int2>& x, const std::pair<int, int2>& y) {
+      return x.first != y.first ? x.first > y.first : (x.second.x != y.second.x ? x.second.x < y.second.x : x.second.y < y.second.y);
     };
-    std::stable_sort(p1.begin(), p1.end(), bycost);
-    std::stable_sort(p5.begin(), p5.end(), bycost);
-    std::stable_sort(sy.begin(), sy.end(), bycost);
-    std::vector<int2> v1, v5;
-    std::vector<int> vs;
-    for (auto& e : p1) v1.push_back(e.second);
-    for (auto& e : p5) v5.push_back(e.second);
-    for (auto& e : sy) vs.push_back(e.second.x);
-    h->n_p1 = (int)v1.size();
-    h->n_p5 = (int)v5.size();
-    h->n_sy = (int)vs.size();
-    TRY(dupload(h, &h->d_it_p1, v1));
-    TRY(dupload(h, &h->d_it_p5, v5));
-    TRY(dupload(h, &h->d_it_sy, vs));
+    auto upload = [&](std::vector<std::pair<int, int2>>& v, int2** dst, int* n) -> tcg_status {
+      std::stable_sort(v.begin(), v.end(), bycost);
+      std::vector<int2> w;
+      for (auto& e : v) w.push_back(e.second);
+      *n = (int)w.size();
+      return dupload(h, dst, w);
+    };
+    TRY(upload(p1, &h->d_it_p1, &h->n_p1));
+    TRY(upload(p5, &h->d_it_p5, &h->n_p5));
+    TRY(upload(sy, &h->d_it_sy, &h->n_sy));
+    TRY(upload(p3, &h->d_it_p3, &h->n_p3));
+    TRY(upload(p4, &h->d_it_p4, &h->n_p4));
+    TRY(dupload(h, &h->d_pwc_off, pwc_off));
+    TRY(dalloc(h, &h->PWc, opwc));
+    TRY(dalloc(h, &h->Ypart, (size_t)Tc * h->coarse_maxch * TS));
+    TRY(dalloc(h, &h->Ppart, (size_t)Tc * h->coarse_maxch * TS));
   }
   TRY(dalloc(h, &h->partial, RED_BLOCKS));
   TRY(dalloc(h, &h->hist, (size_t)h->max_iter + 2));
@@ -615,8 +641,8 @@ static tcg_status do_setup(tcg_ctx* h) {
     // persistent PCG: shared memory = max over its item kinds
     size_t p1 = (size_t)h->maxTb * TS;
     size_t p5 = (size_t)(h->maxTb + h->maxTp) * TS + 8 * TS;
-    size_t p34 = (size_t)CCH * TS + 8 * TS;
-    size_t syv = 10 * (size_t)h->maxTb * TS;
+    size_t p34 = (size_t)h->coarse_ch * TS + 8 * TS;
+    size_t syv = 9 * (size_t)h->maxTb * TS;
     h->smem_pcg = sizeof(double) * std::max(std::max(p1, p5), std::max(p34, syv));
     TRY(set_smem(h, (const void*)k_pcg, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_p1_lam, h->smem_pcg));
@@ -678,15 +704,6 @@ static void prof_collect(tcg_ctx* h, int iters) {
   h->prof_used = 0;
 }
 
-// coarse solve Pc = S_pp^-1 sum_s N_s^T (src1_p - src2_p) as two GEMV launches with X_c
-static void launch_coarse(tcg_ctx* h, const double* src1, const double* src2) {
-  if (h->D.Tc == 0) return;
-  k_p3<<<h->D.Tc, NTHR, h->smem_pcg, h->stream>>>(h->D, h->CX, src1, src2, h->Yc);
-  ++h->nlaunch;
-  k_p4<<<h->D.Tc, NTHR, h->smem_pcg, h->stream>>>(h->D, h->CX, h->Yc, h->Pc);
-  ++h->nlaunch;
-}
-
 static PcgArgs pcg_args(tcg_ctx* h) {
   PcgArgs A{};
   A.lam = h->lam;
@@ -699,8 +716,13 @@ static PcgArgs pcg_args(tcg_ctx* h) {
   A.XW = h->XW;
   A.Y = h->Yv;
   A.PW = h->PW;
-  A.Yc = h->Yc;
+  A.PWc = h->PWc;
+  A.pwc_off = h->d_pwc_off;
+  A.Ypart = h->Ypart;
+  A.Ppart = h->Ppart;
   A.Pc = h->Pc;
+  A.ch = h->coarse_ch;
+  A.maxch = h->coarse_maxch;
   A.partA = h->partA;
   A.partB = h->partB;
   A.hist = h->hist;
@@ -708,12 +730,29 @@ static PcgArgs pcg_args(tcg_ctx* h) {
   A.it_p1 = h->d_it_p1;
   A.it_p5 = h->d_it_p5;
   A.it_sy = h->d_it_sy;
+  A.it_p3 = h->d_it_p3;
+  A.it_p4 = h->d_it_p4;
   A.n_p1 = h->n_p1;
   A.n_p5 = h->n_p5;
   A.n_sy = h->n_sy;
+  A.n_p3 = h->n_p3;
+  A.n_p4 = h->n_p4;
   A.rtol = h->rtol;
   A.max_iter = h->max_iter;
+  A.tstamp = h->tstamp;
   return A;
+}
+
+// coarse solve Pc = S_pp^-1 sum_s N_s^T (src1_p - src2_p): chunked GEMVs with X_c, then Pc
+static void launch_coarse(tcg_ctx* h, const double* src1, const double* src2) {
+  if (h->D.Tc == 0) return;
+  PcgArgs A = pcg_args(h);
+  k_p3<<<h->n_p3, NTHR, h->smem_pcg, h->stream>>>(h->D, A, h->CX, src1, src2);
+  ++h->nlaunch;
+  k_p4<<<h->n_p4, NTHR, h->smem_pcg, h->stream>>>(h->D, A, h->CX);
+  ++h->nlaunch;
+  k_pc_sum<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(592, (h->D.nc + 255) / 256)), 256, 0, h->stream>>>(h->D, A);
+  ++h->nlaunch;
 }
 
 static tcg_status do_step(tcg_ctx* h) {
@@ -731,7 +770,7 @@ static tcg_status do_step(tcg_ctx* h) {
   prof_end(h, 5);
   launch_coarse(h, h->X1, nullptr);
   if (h->n_p5 > 0) {
-    k_p5<<<h->n_p5, NTHR, h->smem_pcg, h->stream>>>(D, h->d_it_p5, h->n_p5, h->X1, h->Pc, h->Yv);
+    k_p5<<<h->n_p5, NTHR, h->smem_pcg, h->stream>>>(D, pcg_args(h), h->X1);
     ++h->nlaunch;
   }
   k_dual_rhs<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->Yv, h->r, h->lam);
@@ -1087,7 +1126,7 @@ tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms) {
     }
     launch_coarse(h, h->XW, nullptr);
     if (h->n_p5 > 0) {
-      k_p5<<<h->n_p5, NTHR, h->smem_pcg, h->stream>>>(D, h->d_it_p5, h->n_p5, h->XW, h->Pc, h->Yv);
+      k_p5<<<h->n_p5, NTHR, h->smem_pcg, h->stream>>>(D, pcg_args(h), h->XW);
       ++h->nlaunch;
     }
     k_dual_rhs<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->Yv, h->q, h->z);
@@ -1132,6 +1171,11 @@ tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t 
     CK(cudaMemcpy(wp.data(), h->D.wplus, sizeof(double) * h->D.m, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(wm.data(), h->D.wminus, sizeof(double) * h->D.m, cudaMemcpyDeviceToHost));
     for (int64_t k = 0; k < h->D.m; ++k) { tmp.push_back(wp[k]); tmp.push_back(wm[k]); }
+  } else if (what == 7) {
+    if (!h->tstamp) return fail(h, TCG_ESTATE, "TCG_PHASE_TIMING not set");
+    std::vector<unsigned long long> ts(8 * 64);
+    CK(cudaMemcpy(ts.data(), h->tstamp, ts.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    for (auto v : ts) tmp.push_back((double)v);
   } else if (what == 6) {
     int64_t off = 0;
     for (int s = 0; s < idx; ++s) off += tri_tiles(h->plan.pp[s].Tb) * TSZ;
