@@ -71,14 +71,12 @@ struct tcg_ctx {
   InvDesc* d_inv = nullptr;
   InvDesc* d_cinv = nullptr;
   int maxTp = 0;
-  int n_p1 = 0, n_p5 = 0, n_sy = 0, n_p3 = 0, n_p4 = 0;
+  int n_p1 = 0, n_p5 = 0, n_sy = 0, n_pc = 0;
   int2* d_it_p1 = nullptr;
   int2* d_it_p5 = nullptr;
   int2* d_it_sy = nullptr;
-  int2* d_it_p3 = nullptr;
-  int2* d_it_p4 = nullptr;
-  double *PWc = nullptr, *Ypart = nullptr, *Ppart = nullptr;
-  int64_t* d_pwc_off = nullptr;
+  int2* d_it_pc = nullptr;
+  double *Sinv = nullptr, *Ppart = nullptr;
   int coarse_ch = 1, coarse_maxch = 1;
   size_t smem_pcg = 0;
   int pcg_blocks = 0;
@@ -297,6 +295,9 @@ static tcg_status do_numeric(tcg_ctx* h) {
       ++h->nlaunch;
       CKL();
     }
+    k_sinv<<<dim3(Tc, Tc), 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(h->CX, h->Sinv, Tc);
+    ++h->nlaunch;
+    CKL();
   }
   // insulator precompute: XJ = forward(j_S)
   k_copy<<<592, 256, 0, h->stream>>>(h->XJ, h->JS, h->vec_total);
@@ -522,24 +523,18 @@ static tcg_status do_setup(tcg_ctx* h) {
     // work items, largest first (round-robin over the persistent blocks)
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device);
-    const int64_t ctiles = tri_tiles(Tc);
+    const int64_t ctiles = (int64_t)Tc * Tc;
     h->coarse_ch = (int)std::max<int64_t>(1, std::min<int64_t>(64, ctiles / (4 * (int64_t)dev_sms)));
     h->coarse_maxch = std::max(1, (Tc + h->coarse_ch - 1) / h->coarse_ch);
-    std::vector<std::pair<int, int2>> p1, p5, sy, p3, p4;
-    std::vector<int64_t> pwc_off(P);
-    int64_t opwc = 0;
+    std::vector<std::pair<int, int2>> p1, p5, sy, pcv;
     for (int s = 0; s < P; ++s) {
       for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.push_back({I < Tb[s] ? I + 1 : Tb[s], make_int2(s, I)});
       for (int J = 0; J < Tb[s]; ++J) p5.push_back({Tb[s] - J + Tp[s], make_int2(s, J)});
-      for (int I = 0; I < Tb[s]; ++I) sy.push_back({I + 1, make_int2(s, I)});
-      pwc_off[s] = opwc;
-      opwc += (int64_t)Tb[s] * Tb[s] * TS;
+      for (int I = 0; I < Tb[s]; ++I) sy.push_back({Tb[s], make_int2(s, I)});
     }
     const int ch = h->coarse_ch;
     for (int I = 0; I < Tc; ++I)
-      for (int c = 0; c * ch <= I; ++c) p3.push_back({std::min(I + 1, (c + 1) * ch) - c * ch, make_int2(I, c)});
-    for (int J = 0; J < Tc; ++J)
-      for (int c = 0; J + c * ch < Tc; ++c) p4.push_back({std::min(Tc, J + (c + 1) * ch) - (J + c * ch), make_int2(J, c)});
+      for (int c = 0; c < h->coarse_maxch; ++c) pcv.push_back({std::min(Tc, (c + 1) * ch) - c * ch, make_int2(I, c)});
     auto bycost = [](const std::pair<int, int2>& x, const std::pair<int, int2>& y) {
       return x.first != y.first ? x.first > y.first : (x.second.x != y.second.x ? x.second.x < y.second.x : x.second.y < y.second.y);
     };
@@ -553,11 +548,8 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(upload(p1, &h->d_it_p1, &h->n_p1));
     TRY(upload(p5, &h->d_it_p5, &h->n_p5));
     TRY(upload(sy, &h->d_it_sy, &h->n_sy));
-    TRY(upload(p3, &h->d_it_p3, &h->n_p3));
-    TRY(upload(p4, &h->d_it_p4, &h->n_p4));
-    TRY(dupload(h, &h->d_pwc_off, pwc_off));
-    TRY(dalloc(h, &h->PWc, opwc));
-    TRY(dalloc(h, &h->Ypart, (size_t)Tc * h->coarse_maxch * TS));
+    TRY(upload(pcv, &h->d_it_pc, &h->n_pc));
+    TRY(dalloc(h, &h->Sinv, (size_t)Tc * Tc * TSZ));
     TRY(dalloc(h, &h->Ppart, (size_t)Tc * h->coarse_maxch * TS));
   }
   TRY(dalloc(h, &h->partial, RED_BLOCKS));
@@ -641,13 +633,13 @@ static tcg_status do_setup(tcg_ctx* h) {
     // persistent PCG: shared memory = max over its item kinds
     size_t p1 = (size_t)h->maxTb * TS;
     size_t p5 = (size_t)(h->maxTb + h->maxTp) * TS + 8 * TS;
-    size_t p34 = (size_t)h->coarse_ch * TS + 8 * TS;
-    size_t syv = 9 * (size_t)h->maxTb * TS;
+    size_t p34 = (size_t)h->coarse_ch * TS;
+    size_t syv = (size_t)h->maxTb * TS + 9 * TS;
     h->smem_pcg = sizeof(double) * std::max(std::max(p1, p5), std::max(p34, syv));
     TRY(set_smem(h, (const void*)k_pcg, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_p1_lam, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_p3, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_p4, h->smem_pcg));
+    TRY(set_smem(h, (const void*)k_pc, h->smem_pcg));
+    TRY(set_smem(h, (const void*)k_sinv, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_p5, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_trinv_row, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_phiT, 2 * TS * SPAD * sizeof(double)));
@@ -655,7 +647,11 @@ static tcg_status do_setup(tcg_ctx* h) {
     CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg, NTHR, h->smem_pcg));
     if (occ < 1) return fail(h, TCG_ECUDA, "persistent PCG kernel does not fit on an SM");
-    h->pcg_blocks = dev_sms * std::min(occ, 2);
+    {
+      const char* ev = getenv("TCG_PCG_BLOCKS_PER_SM");
+      int per = ev ? std::max(1, atoi(ev)) : 1;
+      h->pcg_blocks = dev_sms * std::min(occ, per);
+    }
     if (h->pcg_blocks > 4096) h->pcg_blocks = 4096;
   }
   TRY(set_smem(h, (const void*)k_tables1d, h->smem_tables));
@@ -711,14 +707,10 @@ static PcgArgs pcg_args(tcg_ctx* h) {
   A.r[1] = h->r2;
   A.pk[0] = h->pk;
   A.pk[1] = h->pk2;
-  A.z = h->z;
-  A.q = h->q;
   A.XW = h->XW;
   A.Y = h->Yv;
   A.PW = h->PW;
-  A.PWc = h->PWc;
-  A.pwc_off = h->d_pwc_off;
-  A.Ypart = h->Ypart;
+  A.Sinv = h->Sinv;
   A.Ppart = h->Ppart;
   A.Pc = h->Pc;
   A.ch = h->coarse_ch;
@@ -730,13 +722,11 @@ static PcgArgs pcg_args(tcg_ctx* h) {
   A.it_p1 = h->d_it_p1;
   A.it_p5 = h->d_it_p5;
   A.it_sy = h->d_it_sy;
-  A.it_p3 = h->d_it_p3;
-  A.it_p4 = h->d_it_p4;
+  A.it_pc = h->d_it_pc;
   A.n_p1 = h->n_p1;
   A.n_p5 = h->n_p5;
   A.n_sy = h->n_sy;
-  A.n_p3 = h->n_p3;
-  A.n_p4 = h->n_p4;
+  A.n_pc = h->n_pc;
   A.rtol = h->rtol;
   A.max_iter = h->max_iter;
   A.tstamp = h->tstamp;
@@ -747,9 +737,7 @@ static PcgArgs pcg_args(tcg_ctx* h) {
 static void launch_coarse(tcg_ctx* h, const double* src1, const double* src2) {
   if (h->D.Tc == 0) return;
   PcgArgs A = pcg_args(h);
-  k_p3<<<h->n_p3, NTHR, h->smem_pcg, h->stream>>>(h->D, A, h->CX, src1, src2);
-  ++h->nlaunch;
-  k_p4<<<h->n_p4, NTHR, h->smem_pcg, h->stream>>>(h->D, A, h->CX);
+  k_pc<<<h->n_pc, NTHR, h->smem_pcg, h->stream>>>(h->D, A, src1, src2);
   ++h->nlaunch;
   k_pc_sum<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(592, (h->D.nc + 255) / 256)), 256, 0, h->stream>>>(h->D, A);
   ++h->nlaunch;
@@ -779,8 +767,7 @@ static tcg_status do_step(tcg_ctx* h) {
   // PCG: one persistent cooperative launch, convergence decided on the device
   {
     PcgArgs A = pcg_args(h);
-    const double* cx = h->CX;
-    void* args[] = {(void*)&D, (void*)&A, (void*)&cx};
+    void* args[] = {(void*)&D, (void*)&A};
     prof_begin(h, 7, -1);
     CK(cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(h->pcg_blocks), dim3(NTHR), args, h->smem_pcg, h->stream));
     ++h->nlaunch;
@@ -1129,7 +1116,7 @@ tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms) {
       k_p5<<<h->n_p5, NTHR, h->smem_pcg, h->stream>>>(D, pcg_args(h), h->XW);
       ++h->nlaunch;
     }
-    k_dual_rhs<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->Yv, h->q, h->z);
+    k_dual_rhs<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->Yv, h->q, h->z);  // q = F r (z scratch)
     ++h->nlaunch;
   }
   cudaEventRecord(e1, h->stream);

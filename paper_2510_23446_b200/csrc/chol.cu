@@ -370,3 +370,26 @@ __global__ void __launch_bounds__(128) k_phiT(DevPlan D, int maxTb) {
 }
 
 }  // namespace tcg
+
+namespace tcg {
+
+// Full symmetric S_pp^-1 = X_c^T X_c (X_c = L_c^-1 tile-packed lower), stored as Tc x Tc
+// row-major 64x64 tiles: tile (I,J) = sum_{K >= max(I,J)} X_KI^T X_KJ. grid (Tc, Tc), 128 thr.
+__global__ void __launch_bounds__(128) k_sinv(const double* __restrict__ X, double* Sinv, int Tc) {
+  const int I = blockIdx.y, J = blockIdx.x;
+  extern __shared__ double smem[];
+  double* sA = smem;
+  double* sB = smem + TS * SPAD;
+  double acc[4][4][2];
+  acc_zero(acc);
+  for (int K = max(I, J); K < Tc; ++K) {
+    stage_tile_T(X + tri_off(K, I), sA);  // sA[m][k] = X_KI[k][m]
+    stage_tile_T(X + tri_off(K, J), sB);  // sB[n][k] = X_KJ[k][n]
+    __syncthreads();
+    mma_acc(sA, sB, acc);
+    __syncthreads();
+  }
+  acc_store(Sinv + ((int64_t)I * Tc + J) * TSZ, acc, 1.0);
+}
+
+}  // namespace tcg

@@ -8,9 +8,9 @@ for name in sys.argv[1:] or ["cfg2"]:
     s = tcg.Solver().configure(pr); s.setup(); s.step(2)
     out = np.zeros(512); L.tcg_debug_array(s.h, 7, 0, out.ctypes.data_as(C.POINTER(C.c_double)), 512)
     it, _, _ = s.history(); n = int(it[-1])
-    t = out.reshape(64, 8)[:n]
+    t = out.reshape(64, 8)[:n, :5]
     d = np.diff(np.concatenate([t, np.roll(t[:, :1], -1, axis=0)], axis=1), axis=1)[:-1] / 1000.0
-    names = ["P1 X_bb/PhiT", "P3 coarse lo", "P4 coarse up", "P5 y", "P6 jump q", "P7 symv", "P8 jump z", "tail"]
+    names = ["P1 X_bb/PhiT", "PC coarse", "P5 y + pFp", "P7 symv + rz", "tail"]
     print(name, "iters", n, "mean us per phase:", {k: round(float(v), 2) for k, v in zip(names, d.mean(axis=0))}, "total/iter", round(float(d.sum(axis=1).mean()), 2))
     inf = s.info(); print("  steps ms", inf["ms_steps"], "ms/step", inf["ms_steps"] / 2)
     s.close()
