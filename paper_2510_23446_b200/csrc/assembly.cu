@@ -296,6 +296,17 @@ __global__ void k_rho_weights(DevPlan D, int scaling) {
   D.wminus[k] = rho[0] / (rho[0] + rho[1]);
 }
 
+// Per b position: a_own = weight of this side, a_part = -(weight of the other side), so that
+// sign * (w+ y[+] - w- y[-]) = a_own y[own] + a_part y[partner].
+__global__ void k_btables(DevPlan D, int64_t nbtot) {
+  int64_t bb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (bb >= nbtot) return;
+  const int k = D.b_lam[bb];
+  const bool plus = D.b_sign[bb] > 0;
+  D.b_aown[bb] = plus ? D.wplus[k] : D.wminus[k];
+  D.b_apart[bb] = plus ? -D.wminus[k] : -D.wplus[k];
+}
+
 // Spatial load j_S,s = <S, w> in aug order (r and p positions; padding 0), from the
 // separable 1D source integrals. kind 1: S = (pi sx cy sz, -pi cx sy sz, 0);
 // kind 2: S = (sy sz, sx sz, sx sy).

@@ -66,6 +66,7 @@ struct tcg_ctx {
   std::vector<int> h_T;
   int64_t a_total = 0;
   int64_t total_tiles = 0;
+  int64_t nb_total = 0;
   // chain-free PCG
   double *CX = nullptr, *r2 = nullptr, *pk2 = nullptr, *Yv = nullptr, *Yc = nullptr, *partA = nullptr, *partB = nullptr;
   InvDesc* d_inv = nullptr;
@@ -251,6 +252,10 @@ static tcg_status do_numeric(tcg_ctx* h) {
     k_rho_weights<<<(unsigned)((pl.m + 255) / 256), 256, 0, h->stream>>>(D, h->scaling);
     ++h->nlaunch;
     CKL();
+  }
+  if (h->nb_total > 0) {
+    k_btables<<<(unsigned)((h->nb_total + 255) / 256), 256, 0, h->stream>>>(D, h->nb_total);
+    ++h->nlaunch;
   }
   k_load_vector<<<P, 256, 0, h->stream>>>(D, h->tb, h->G, h->source, h->JS);
   ++h->nlaunch;
@@ -475,6 +480,23 @@ static tcg_status do_setup(tcg_ctx* h) {
   D.tile_start = dts; D.sigma = dsig; D.nu = dnu;
   D.lam_patch_p = dlpp; D.lam_patch_m = dlpm; D.lam_pos_p = dlsp; D.lam_pos_m = dlsm;
   D.lam_idx_p = dlip; D.lam_idx_m = dlim; D.coarse_ptr = dcp; D.coarse_idx = dci;
+  {
+    // partner index of every b position (the other endpoint of its multiplier)
+    std::vector<int64_t> bpart(b_lam_all.size());
+    for (int s = 0; s < P; ++s) {
+      const PatchPlan& q = pl.pp[s];
+      for (int t = 0; t < q.nb; ++t) {
+        const int64_t k = q.b_lam[t];
+        bpart[b_off[s] + t] = (q.b_sign[t] > 0) ? lim[k] : lip[k];
+      }
+    }
+    int64_t* dbp;
+    TRY(dupload(h, &dbp, bpart));
+    D.b_part = dbp;
+    TRY(dalloc(h, &D.b_aown, bpart.size()));
+    TRY(dalloc(h, &D.b_apart, bpart.size()));
+    h->nb_total = (int64_t)bpart.size();
+  }
   double *wp, *wm;
   TRY(dalloc(h, &wp, pl.m));
   TRY(dalloc(h, &wm, pl.m));
@@ -649,7 +671,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     if (occ < 1) return fail(h, TCG_ECUDA, "persistent PCG kernel does not fit on an SM");
     {
       const char* ev = getenv("TCG_PCG_BLOCKS_PER_SM");
-      int per = ev ? std::max(1, atoi(ev)) : 1;
+      int per = ev ? std::max(1, atoi(ev)) : 2;
       h->pcg_blocks = dev_sms * std::min(occ, per);
     }
     if (h->pcg_blocks > 4096) h->pcg_blocks = 4096;

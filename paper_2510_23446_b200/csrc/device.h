@@ -47,6 +47,9 @@ struct DevPlan {
   const int64_t* b_off;     // per patch offset into b_lam / b_sign
   const int* b_lam;
   const double* b_sign;
+  const int64_t* b_part;    // per b position: aug-vector index of the multiplier's other endpoint
+  double* b_aown;           // per b position: B_D weight of this side (w+ or w-)
+  double* b_apart;          // per b position: -(weight of the other side)
   const int64_t* p_off;     // per patch offset into p_grp
   const int* p_grp;
   const int64_t* tile_start;  // prefix of T(T+1)/2 (npatch+1)

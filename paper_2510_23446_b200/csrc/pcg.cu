@@ -83,15 +83,14 @@ __device__ __forceinline__ double pc_get(const PcgArgs& A, int64_t g) {
   return v;
 }
 
-// ---- P1: row GEMV of [X_bb; Phi^T] with v gathered through the signed b-map ---------------
-// src(k) returns the lambda-space value of multiplier k.
+// ---- P1: row GEMV of [X_bb; Phi^T] with v = B_s^T p gathered per b position --------------
+// vsrc(b, pos) returns the signed value (B_s^T p)_pos, b = b_off[s] + pos.
 template <class Src>
-__device__ void p1_item(const DevPlan& D, int s, int I, Src src, double* XW, double* sv) {
+__device__ void p1_item(const DevPlan& D, int s, int I, Src vsrc, double* XW, double* sv) {
   const int Ti = D.Ti[s], Tb = D.Tb[s], nb = D.nb[s];
   const int Jn = (I < Tb) ? I + 1 : Tb;
-  const int* bl = D.b_lam + D.b_off[s];
-  const double* bs = D.b_sign + D.b_off[s];
-  for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x) sv[e] = (e < nb) ? bs[e] * src(bl[e]) : 0.0;
+  const int64_t bo = D.b_off[s];
+  for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x) sv[e] = (e < nb) ? vsrc(s, bo + e, e) : 0.0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
   double part[8];
@@ -206,22 +205,14 @@ __device__ double p5_item(const DevPlan& D, int s, int J, const double* W, PcF p
 // ---- P7: symmetric S_bb apply, one row block I of one patch (packed-lower storage: the
 // row's lower tiles as row GEMVs, the tiles below the diagonal as transposed GEMVs).
 // u = B_D^T r (weighted gather of usrc). Returns this item's share of u^T S_bb u.
+// usrc(s, b, pos) returns (B_D^(s)T r)_pos, b = b_off[s] + pos.
 template <class Src>
 __device__ double symv_item(const DevPlan& D, const PcgArgs& A, int s, int I, Src usrc, double* sm, double* red) {
   const int Ti = D.Ti[s], Tb = D.Tb[s], nb = D.nb[s];
   double* u = sm;               // Tb*64
   double* cr = u + Tb * TS;     // 8 * 64
-  const int* bl = D.b_lam + D.b_off[s];
-  const double* bs = D.b_sign + D.b_off[s];
-  for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) {
-    double val = 0.0;
-    if (i < nb) {
-      const int k = bl[i];
-      const double sg = bs[i];
-      val = sg * (sg > 0 ? D.wplus[k] : D.wminus[k]) * usrc(k);
-    }
-    u[i] = val;
-  }
+  const int64_t bo = D.b_off[s];
+  for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) u[i] = (i < nb) ? usrc(s, bo + i, i) : 0.0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
   const double* S = D.Sbb + D.sbb_off[s];
@@ -313,7 +304,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ta
 // Persistent cooperative PCG (one launch per implicit-Euler step). Input: r[0] = d,
 // lam = 0. Output: lam, history, state. All blocks run the same number of barriers.
 // =======================================================================================
-__global__ void __launch_bounds__(NTHR) k_pcg(DevPlan D, PcgArgs A) {
+__global__ void __launch_bounds__(NTHR, 2) k_pcg(DevPlan D, PcgArgs A) {
   extern __shared__ double sm[];
   __shared__ double red[NTHR];
   const int NB = gridDim.x, b = blockIdx.x;
@@ -324,16 +315,16 @@ __global__ void __launch_bounds__(NTHR) k_pcg(DevPlan D, PcgArgs A) {
   unsigned int bar_target = 0;
   int it = 0;
   const double* r0 = A.r[0];
-  // z_k from the last S_bb apply (PW) and the weights
-  auto zval = [&](int k) {
-    return D.wplus[k] * ldcg(A.PW + D.lam_idx_p[k]) - D.wminus[k] * ldcg(A.PW + D.lam_idx_m[k]);
-  };
+  // own/partner form of the jumps (per b position: a_own, a_part, partner index, sign, lambda)
+  auto own_idx = [&](int s, int pos) { return D.vec_off[s] + (int64_t)D.Ti[s] * TS + pos; };
 
   // ---- prologue: u = B_D^T r0, PW = S_bb u, rho0 = r0^T z0 = sum u.S u ----
   {
     double loc = 0.0;
     for (int i = b; i < A.n_sy; i += NB)
-      loc += symv_item(D, A, A.it_sy[i].x, A.it_sy[i].y, [&](int k) { return ldcg(r0 + k); }, sm, red);
+      loc += symv_item(D, A, A.it_sy[i].x, A.it_sy[i].y,
+                       [&](int, int64_t bb, int) { return D.b_aown[bb] * D.b_sign[bb] * ldcg(r0 + D.b_lam[bb]); },
+                       sm, red);
     for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) A.pk[0][k] = 0.0;
     if (threadIdx.x == 0) A.partB[b] = loc;
   }
@@ -360,10 +351,17 @@ __global__ void __launch_bounds__(NTHR) k_pcg(DevPlan D, PcgArgs A) {
     TSTAMP(0);
     const double* pprev = A.pk[pp];
     double* pcur = A.pk[pp ^ 1];
-    auto pnew = [&](int k) { return zval(k) + beta * ldcg(pprev + k); };
-    // P1: v = B^T p (p on the fly); w = X_bb v, -g = -Phi^T v; owners materialise p
-    for (int i = b; i < A.n_p1; i += NB) p1_item(D, A.it_p1[i].x, A.it_p1[i].y, pnew, A.XW, sm);
-    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) pcur[k] = pnew((int)k);
+    // p_k = z_k + beta p_prev,k with z = B_D (S_bb u) from P7; signed value at a b position:
+    // sign*z_k = a_own PW[own] + a_part PW[partner]
+    auto vnew = [&](int s, int64_t bb, int pos) {
+      return D.b_aown[bb] * ldcg(A.PW + own_idx(s, pos)) + D.b_apart[bb] * ldcg(A.PW + D.b_part[bb]) +
+             D.b_sign[bb] * beta * ldcg(pprev + D.b_lam[bb]);
+    };
+    // P1: v = B^T p (on the fly); w = X_bb v, -g = -Phi^T v; owners materialise p
+    for (int i = b; i < A.n_p1; i += NB) p1_item(D, A.it_p1[i].x, A.it_p1[i].y, vnew, A.XW, sm);
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
+      pcur[k] = D.wplus[k] * ldcg(A.PW + D.lam_idx_p[k]) - D.wminus[k] * ldcg(A.PW + D.lam_idx_m[k]) +
+                beta * ldcg(pprev + k);
     grid_barrier(bar, bar_target);
     TSTAMP(1);
     // PC: Pc = S_pp^-1 G (chunk partials)
@@ -385,17 +383,19 @@ __global__ void __launch_bounds__(NTHR) k_pcg(DevPlan D, PcgArgs A) {
     const double alpha = rho / pq;
     const double* rc = A.r[rp];
     double* rn = A.r[rp ^ 1];
-    auto rnew = [&](int k) {
-      return ldcg(rc + k) - alpha * (ldcg(A.Y + D.lam_idx_p[k]) - ldcg(A.Y + D.lam_idx_m[k]));
+    // u_pos = a_own (sign r_k - alpha sign q_k), sign q_k = Y[own] - Y[partner]
+    auto unew = [&](int s, int64_t bb, int pos) {
+      return D.b_aown[bb] * (D.b_sign[bb] * ldcg(rc + D.b_lam[bb]) -
+                             alpha * (ldcg(A.Y + own_idx(s, pos)) - ldcg(A.Y + D.b_part[bb])));
     };
     // P7: lambda, r updates (owners); S_bb apply of u = B_D^T r_new; partial r_new^T z
     {
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
         A.lam[k] += alpha * ldcg(pcur + k);
-        rn[k] = rnew((int)k);
+        rn[k] = ldcg(rc + k) - alpha * (ldcg(A.Y + D.lam_idx_p[k]) - ldcg(A.Y + D.lam_idx_m[k]));
       }
       double loc = 0.0;
-      for (int i = b; i < A.n_sy; i += NB) loc += symv_item(D, A, A.it_sy[i].x, A.it_sy[i].y, rnew, sm, red);
+      for (int i = b; i < A.n_sy; i += NB) loc += symv_item(D, A, A.it_sy[i].x, A.it_sy[i].y, unew, sm, red);
       if (threadIdx.x == 0) A.partB[b] = loc;
     }
     grid_barrier(bar, bar_target);
@@ -426,7 +426,8 @@ __global__ void __launch_bounds__(NTHR) k_p1_lam(DevPlan D, const int2* items, i
                                                  double* XW) {
   extern __shared__ double sm[];
   if (blockIdx.x >= n) return;
-  p1_item(D, items[blockIdx.x].x, items[blockIdx.x].y, [&](int k) { return lam[k]; }, XW, sm);
+  p1_item(D, items[blockIdx.x].x, items[blockIdx.x].y,
+          [&](int, int64_t bb, int) { return D.b_sign[bb] * lam[D.b_lam[bb]]; }, XW, sm);
 }
 __global__ void __launch_bounds__(NTHR) k_pc(DevPlan D, PcgArgs A, const double* src1, const double* src2) {
   extern __shared__ double sm[];
