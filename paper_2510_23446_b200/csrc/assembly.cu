@@ -339,65 +339,4 @@ __global__ void k_load_vector(DevPlan D, Tables1D tb, Geom G, int kind, double* 
   }
 }
 
-// Conductor rhs (aug order): f = (sigma/dt) M_ref a + phi(t) j_S, M applied entrywise from
-// the banded 1D factors (|i-i'| <= p). Insulator patches get f = phi(t) * XJ (precomputed
-// forward solve of j_S, see solve.cu), which is written by the same kernel.
-__global__ void __launch_bounds__(256) k_rhs(DevPlan D, Tables1D tb, Geom G, int kind, double t, double inv_dt,
-                                             const double* __restrict__ JS, const double* __restrict__ XJ,
-                                             const double* __restrict__ a_loc, double* X) {
-  const int s = blockIdx.x;
-  const double sig = D.sigma[s], nu = D.nu[s];
-  double phi = 0.0;
-  if (kind == 1) phi = sinpi(2.0 * t);
-  else if (kind == 2) phi = 2.0 * M_PI * M_PI * nu * (1.0 - exp(-t)) + sig * exp(-t);
-  const int R = D.T[s] * TS;
-  const int64_t vo = D.vec_off[s];
-  if (sig <= 0.0) {
-    for (int pos = threadIdx.x; pos < R; pos += blockDim.x) X[vo + pos] = phi * XJ[vo + pos];
-    return;
-  }
-  __shared__ T1 tt[3];
-  if (threadIdx.x < 3) {
-    int d = threadIdx.x;
-    tt[d].Mb = tb.base + tb.off_Mb[d];
-    tt[d].Md = tb.base + tb.off_Md[d];
-    tt[d].Kb = tb.base + tb.off_Kb[d];
-    tt[d].C = tb.base + tb.off_C[d];
-    tt[d].n = tb.el[d] + G.p;
-  }
-  __syncthreads();
-  const int* aug = D.aug + D.aug_off[s];
-  const double* as = a_loc + (int64_t)s * G.nloc;
-  const int p = G.p;
-  for (int pos = threadIdx.x; pos < R; pos += blockDim.x) {
-    int a = aug[pos];
-    if (a < 0) {
-      X[vo + pos] = 0.0;
-      continue;
-    }
-    LocalDof A = decode_local(G, a);
-    const int c = A.c;
-    int lo3[3], hi3[3];
-    for (int d = 0; d < 3; ++d) {
-      lo3[d] = max(0, A.i[d] - p);
-      hi3[d] = min(G.cdim[c][d] - 1, A.i[d] + p);
-    }
-    int off = 0;
-    for (int cc = 0; cc < c; ++cc) off += G.cdim[cc][0] * G.cdim[cc][1] * G.cdim[cc][2];
-    double acc = 0.0;
-    for (int k = lo3[2]; k <= hi3[2]; ++k) {
-      double fz = (c == 2) ? tt[2].md(A.i[2], k) : tt[2].mb(A.i[2], k);
-      for (int j = lo3[1]; j <= hi3[1]; ++j) {
-        double fy = (c == 1) ? tt[1].md(A.i[1], j) : tt[1].mb(A.i[1], j);
-        double fyz = fy * fz;
-        for (int i = lo3[0]; i <= hi3[0]; ++i) {
-          double fx = (c == 0) ? tt[0].md(A.i[0], i) : tt[0].mb(A.i[0], i);
-          acc += fx * fyz * as[off + i + G.cdim[c][0] * (j + G.cdim[c][1] * k)];
-        }
-      }
-    }
-    X[vo + pos] = sig * inv_dt * acc + phi * JS[vo + pos];
-  }
-}
-
 }  // namespace tcg

@@ -72,11 +72,19 @@ struct tcg_ctx {
   InvDesc* d_inv = nullptr;
   InvDesc* d_cinv = nullptr;
   int maxTp = 0;
-  int n_p1 = 0, n_p5 = 0, n_sy = 0, n_pc = 0;
+  int n_p1 = 0, n_p5 = 0, n_sy = 0, n_pc = 0, n_fw = 0, n_fw_all = 0, n_bw = 0;
   int2* d_it_p1 = nullptr;
   int2* d_it_p5 = nullptr;
   int2* d_it_sy = nullptr;
   int2* d_it_pc = nullptr;
+  int2* d_it_fw = nullptr;
+  int2* d_it_fw_all = nullptr;
+  int2* d_it_bw = nullptr;
+  double* xscratch = nullptr;      // per-patch scratch row for the in-place factor inversion
+  int64_t* d_scr_off = nullptr;
+  double* F = nullptr;             // conductor rhs (aug order)
+  int* d_iters = nullptr;          // per-step PCG iterations (device)
+  int64_t hist_cap = 0, hist_len = 0;
   double *Sinv = nullptr, *Ppart = nullptr;
   int coarse_ch = 1, coarse_maxch = 1;
   size_t smem_pcg = 0;
@@ -84,7 +92,6 @@ struct tcg_ctx {
   unsigned long long* tstamp = nullptr;  // TCG_PHASE_TIMING=1: per-phase timestamps of the persistent PCG
   size_t smem_tables = 0;
   int64_t vec_total = 0;
-  size_t smem_fwd_full = 0, smem_bwd_full = 0;
 
   // results
   int64_t steps_done = 0, total_iters = 0;
@@ -263,16 +270,13 @@ static tcg_status do_numeric(tcg_ctx* h) {
   CK(cudaEventRecord(e1, h->stream));
   if (h->dbgA) CK(cudaMemcpyAsync(h->dbgA, D.A, sizeof(double) * h->a_total, cudaMemcpyDeviceToDevice, h->stream));
   TRY(run_cholesky(h, h->d_desc, P, h->maxT, h->maxTr, h->maxTb, D.A, D.Dinv, D.Sbb, 0));
-  // inverse factors for the chain-free PCG: X_bb = L_bb^-1 (row by row), Phi^T = L_pb X_bb
-  for (int I = 0; I < h->maxTb; ++I) {
-    dim3 g(I + 1, P);
-    k_trinv_row<<<g, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(h->d_inv, I, D.A, D.LS, D.Dinv);
+  // coarse scatter reads S^s from the (p,p) blocks (untouched by the inversion below)
+  // in-place inverse of the augmented factor: Xaug = [L_rr^-1 ; W_pr W_rr^-1]
+  for (int I = 0; I < h->maxT; ++I) {
+    dim3 g(std::min(I + 1, h->maxTr), P);
+    k_xinv_row<<<g, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(D, I, h->xscratch, h->d_scr_off);
     ++h->nlaunch;
-    CKL();
-  }
-  if (h->maxTb > 0 && h->maxTp > 0) {
-    dim3 g(h->maxTp * h->maxTb, P);
-    k_phiT<<<g, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(D, h->maxTb);
+    k_xrow_copy<<<g, 256, 0, h->stream>>>(D, I, h->xscratch, h->d_scr_off);
     ++h->nlaunch;
     CKL();
   }
@@ -304,13 +308,14 @@ static tcg_status do_numeric(tcg_ctx* h) {
     ++h->nlaunch;
     CKL();
   }
-  // insulator precompute: XJ = forward(j_S)
-  k_copy<<<592, 256, 0, h->stream>>>(h->XJ, h->JS, h->vec_total);
+  // insulator precompute: XJ = [X_rr j_S,r ; j_S,p - Phi^T j_S,r]
   ++h->nlaunch;
   CKL();
-  k_fwd_full<<<P, NTHR, h->smem_fwd_full, h->stream>>>(D, h->XJ, 0);
-  ++h->nlaunch;
-  CKL();
+  if (h->n_fw_all > 0) {
+    k_fw<<<h->n_fw_all, NTHR, h->smem_pcg, h->stream>>>(D, h->d_it_fw_all, h->n_fw_all, h->JS, h->XJ);
+    ++h->nlaunch;
+    CKL();
+  }
   CK(cudaEventRecord(e3, h->stream));
   // reset the time-stepping state
   CK(cudaMemsetAsync(h->a_loc, 0, sizeof(double) * (size_t)P * pl.nloc, h->stream));
@@ -322,6 +327,7 @@ static tcg_status do_numeric(tcg_ctx* h) {
   h->ms_coarse = elapsed_ms(e2, e3);
   cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3);
   h->steps_done = 0;
+  h->hist_len = 0;
   h->total_iters = 0;
   h->iters.clear();
   h->final_rel.clear();
@@ -504,7 +510,19 @@ static tcg_status do_setup(tcg_ctx* h) {
   D.wminus = wm;
   TRY(dalloc(h, &D.A, oa));
   TRY(dalloc(h, &D.Dinv, od));
-  TRY(dalloc(h, &D.LS, ol));
+  {
+    std::vector<int64_t> so(P);
+    int64_t tot = 0;
+    for (int s = 0; s < P; ++s) {
+      so[s] = tot;
+      tot += (int64_t)(Ti[s] + Tb[s]) * TSZ;
+    }
+    TRY(dupload(h, &h->d_scr_off, so));
+    TRY(dalloc(h, &h->xscratch, tot));
+  }
+  TRY(dalloc(h, &h->F, ov));
+  TRY(dalloc(h, &h->d_iters, (size_t)h->n_steps + 1));
+  h->hist_cap = (int64_t)(h->n_steps + 1) * (h->max_iter + 1);
   TRY(dalloc(h, &D.Sbb, os));
   TRY(dalloc(h, &D.C, (size_t)tri_tiles(Tc) * TSZ));
   TRY(dalloc(h, &D.Cinv, (size_t)Tc * TSZ));
@@ -533,13 +551,8 @@ static tcg_status do_setup(tcg_ctx* h) {
   }
   CK(cudaMemsetAsync(h->Yv, 0, sizeof(double) * ov, h->stream));
   {
-    std::vector<InvDesc> inv(P);
     h->maxTp = 0;
-    for (int s = 0; s < P; ++s) {
-      inv[s] = InvDesc{a_off[s], ls_off[s], dinv_off[s], Ti[s], Tb[s]};
-      h->maxTp = std::max(h->maxTp, Tp[s]);
-    }
-    TRY(dupload(h, &h->d_inv, inv));
+    for (int s = 0; s < P; ++s) h->maxTp = std::max(h->maxTp, Tp[s]);
     std::vector<InvDesc> cinv(1, InvDesc{0, 0, 0, 0, Tc});
     TRY(dupload(h, &h->d_cinv, cinv));
     // work items, largest first (round-robin over the persistent blocks)
@@ -548,8 +561,15 @@ static tcg_status do_setup(tcg_ctx* h) {
     const int64_t ctiles = (int64_t)Tc * Tc;
     h->coarse_ch = (int)std::max<int64_t>(1, std::min<int64_t>(64, ctiles / (4 * (int64_t)dev_sms)));
     h->coarse_maxch = std::max(1, (Tc + h->coarse_ch - 1) / h->coarse_ch);
-    std::vector<std::pair<int, int2>> p1, p5, sy, pcv;
+    std::vector<std::pair<int, int2>> p1, p5, sy, pcv, fw, fwa, bw;
     for (int s = 0; s < P; ++s) {
+      const int Trs = Ti[s] + Tb[s];
+      for (int I = 0; I < T[s]; ++I) {
+        const int cost = I < Trs ? I + 1 : Trs;
+        if (pl.sigma[s] > 0) fw.push_back({cost, make_int2(s, I)});
+        fwa.push_back({cost, make_int2(s, I)});
+      }
+      for (int J = 0; J < std::max(Trs, 1); ++J) bw.push_back({T[s] - J, make_int2(s, J)});
       for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.push_back({I < Tb[s] ? I + 1 : Tb[s], make_int2(s, I)});
       for (int J = 0; J < Tb[s]; ++J) p5.push_back({Tb[s] - J + Tp[s], make_int2(s, J)});
       for (int I = 0; I < Tb[s]; ++I) sy.push_back({Tb[s], make_int2(s, I)});
@@ -571,11 +591,14 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(upload(p5, &h->d_it_p5, &h->n_p5));
     TRY(upload(sy, &h->d_it_sy, &h->n_sy));
     TRY(upload(pcv, &h->d_it_pc, &h->n_pc));
+    TRY(upload(fw, &h->d_it_fw, &h->n_fw));
+    TRY(upload(fwa, &h->d_it_fw_all, &h->n_fw_all));
+    TRY(upload(bw, &h->d_it_bw, &h->n_bw));
     TRY(dalloc(h, &h->Sinv, (size_t)Tc * Tc * TSZ));
     TRY(dalloc(h, &h->Ppart, (size_t)Tc * h->coarse_maxch * TS));
   }
   TRY(dalloc(h, &h->partial, RED_BLOCKS));
-  TRY(dalloc(h, &h->hist, (size_t)h->max_iter + 2));
+  TRY(dalloc(h, &h->hist, (size_t)(h->n_steps + 1) * (h->max_iter + 1)));
   TRY(dalloc(h, &h->a_loc, (size_t)P * pl.nloc));
   TRY(dalloc(h, &h->st, 1));
   TRY(dalloc(h, &h->derr, 1));
@@ -643,9 +666,6 @@ static tcg_status do_setup(tcg_ctx* h) {
   h->a_total = oa;
   h->total_tiles = tile_start[P];
   // ---- solver kernel shared memory ----
-  const size_t dtl = (h->stable_mask & 3) ? (size_t)TS * 65 : 0;  // staged diagonal tile for substitution
-  h->smem_fwd_full = sizeof(double) * (TS + (size_t)h->maxT * TS + dtl);
-  h->smem_bwd_full = sizeof(double) * (TS + 8 * TS + (size_t)h->maxT * TS + dtl);
   {
     int maxn = 0, maxel = 0;
     for (int d = 0; d < 3; ++d) { maxn = std::max(maxn, pl.el[d] + pl.p); maxel = std::max(maxel, pl.el[d]); }
@@ -657,17 +677,20 @@ static tcg_status do_setup(tcg_ctx* h) {
     size_t p5 = (size_t)(h->maxTb + h->maxTp) * TS + 8 * TS;
     size_t p34 = (size_t)h->coarse_ch * TS;
     size_t syv = (size_t)h->maxTb * TS + 9 * TS;
+    size_t fwb = (size_t)h->maxT * TS + 8 * TS;  // forward / backward full-factor items
+    p34 = std::max(p34, fwb);
     h->smem_pcg = sizeof(double) * std::max(std::max(p1, p5), std::max(p34, syv));
-    TRY(set_smem(h, (const void*)k_pcg, h->smem_pcg));
+    TRY(set_smem(h, (const void*)k_steps, h->smem_pcg));
+    TRY(set_smem(h, (const void*)k_fw, h->smem_pcg));
+    TRY(set_smem(h, (const void*)k_xinv_row, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_p1_lam, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_pc, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_sinv, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_p5, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_trinv_row, 2 * TS * SPAD * sizeof(double)));
-    TRY(set_smem(h, (const void*)k_phiT, 2 * TS * SPAD * sizeof(double)));
     int dev_sms = 0, occ = 0;
     CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_pcg, NTHR, h->smem_pcg));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps, NTHR, h->smem_pcg));
     if (occ < 1) return fail(h, TCG_ECUDA, "persistent PCG kernel does not fit on an SM");
     {
       const char* ev = getenv("TCG_PCG_BLOCKS_PER_SM");
@@ -680,8 +703,6 @@ static tcg_status do_setup(tcg_ctx* h) {
   TRY(set_smem(h, (const void*)k_potrf, 2 * TS * 65 * sizeof(double)));
   TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
   TRY(set_smem(h, (const void*)k_update, 2 * TS * SPAD * sizeof(double)));
-  TRY(set_smem(h, (const void*)k_fwd_full, h->smem_fwd_full));
-  TRY(set_smem(h, (const void*)k_bwd_full, h->smem_bwd_full));
   if (getenv("TCG_DEBUG_KEEP") && atoi(getenv("TCG_DEBUG_KEEP")) != 0) {
     TRY(dalloc(h, &h->dbgA, oa));
     TRY(dalloc(h, &h->dbgC, (size_t)tri_tiles(Tc) * TSZ));
@@ -722,16 +743,21 @@ static void prof_collect(tcg_ctx* h, int iters) {
   h->prof_used = 0;
 }
 
-static PcgArgs pcg_args(tcg_ctx* h) {
-  PcgArgs A{};
+static StepArgs step_args(tcg_ctx* h) {
+  StepArgs A{};
   A.lam = h->lam;
   A.r[0] = h->r;
   A.r[1] = h->r2;
   A.pk[0] = h->pk;
   A.pk[1] = h->pk2;
+  A.F = h->F;
+  A.Z = h->X1;
+  A.XJ = h->XJ;
+  A.JS = h->JS;
   A.XW = h->XW;
   A.Y = h->Yv;
   A.PW = h->PW;
+  A.a_loc = h->a_loc;
   A.Sinv = h->Sinv;
   A.Ppart = h->Ppart;
   A.Pc = h->Pc;
@@ -739,93 +765,85 @@ static PcgArgs pcg_args(tcg_ctx* h) {
   A.maxch = h->coarse_maxch;
   A.partA = h->partA;
   A.partB = h->partB;
-  A.hist = h->hist;
+  A.hist = h->hist + h->hist_len;
+  A.iters = h->d_iters;
   A.st = h->st;
   A.it_p1 = h->d_it_p1;
   A.it_p5 = h->d_it_p5;
   A.it_sy = h->d_it_sy;
   A.it_pc = h->d_it_pc;
+  A.it_fw = h->d_it_fw;
+  A.it_bw = h->d_it_bw;
   A.n_p1 = h->n_p1;
   A.n_p5 = h->n_p5;
   A.n_sy = h->n_sy;
   A.n_pc = h->n_pc;
+  A.n_fw = h->n_fw;
+  A.n_bw = h->n_bw;
+  A.tstamp = h->tstamp;
   A.rtol = h->rtol;
   A.max_iter = h->max_iter;
-  A.tstamp = h->tstamp;
+  A.source = h->source;
+  A.dt = h->T / h->n_steps;
+  A.step0 = (int)h->steps_done;
+  A.nsteps = 0;
+  A.tb = h->tb;
+  A.G = h->G;
   return A;
 }
 
-// coarse solve Pc = S_pp^-1 sum_s N_s^T (src1_p - src2_p): chunked GEMVs with X_c, then Pc
+// coarse solve Pc = S_pp^-1 sum_s N_s^T (src1_p - src2_p) (standalone: F-apply benchmark)
 static void launch_coarse(tcg_ctx* h, const double* src1, const double* src2) {
   if (h->D.Tc == 0) return;
-  PcgArgs A = pcg_args(h);
+  StepArgs A = step_args(h);
   k_pc<<<h->n_pc, NTHR, h->smem_pcg, h->stream>>>(h->D, A, src1, src2);
   ++h->nlaunch;
   k_pc_sum<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(592, (h->D.nc + 255) / 256)), 256, 0, h->stream>>>(h->D, A);
   ++h->nlaunch;
 }
 
-static tcg_status do_step(tcg_ctx* h) {
+// n implicit-Euler steps in ONE persistent cooperative launch (k_steps)
+static tcg_status do_steps(tcg_ctx* h, int n) {
+  if (n <= 0) return TCG_OK;
+  if (h->steps_done + n > h->n_steps) return fail(h, TCG_EINVAL, "more steps than set_time allows (n_steps)");
   DevPlan& D = h->D;
-  const int P = D.npatch;
-  const double dt = h->T / h->n_steps;
-  const double t = (h->steps_done + 1) * dt;
   CK(cudaMemsetAsync(h->st, 0, sizeof(PcgState), h->stream));
-  // rhs: f, full forward solves (conductors), p0 = S_pp^-1 (f_p - h), d = B (x1 - Phi N p0)
-  k_rhs<<<P, 256, 0, h->stream>>>(D, h->tb, h->G, h->source, t, 1.0 / dt, h->JS, h->XJ, h->a_loc, h->X1);
+  StepArgs A = step_args(h);
+  A.nsteps = n;
+  void* args[] = {(void*)&D, (void*)&A};
+  prof_begin(h, 7, -1);
+  CK(cudaLaunchCooperativeKernel((const void*)k_steps, dim3(h->pcg_blocks), dim3(NTHR), args, h->smem_pcg, h->stream));
   ++h->nlaunch;
-  prof_begin(h, 5, -1);
-  k_fwd_full<<<P, NTHR, h->smem_fwd_full, h->stream>>>(D, h->X1, 1);
-  ++h->nlaunch;
-  prof_end(h, 5);
-  launch_coarse(h, h->X1, nullptr);
-  if (h->n_p5 > 0) {
-    k_p5<<<h->n_p5, NTHR, h->smem_pcg, h->stream>>>(D, pcg_args(h), h->X1);
-    ++h->nlaunch;
-  }
-  k_dual_rhs<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->Yv, h->r, h->lam);
-  ++h->nlaunch;
-  CKL();
-  // PCG: one persistent cooperative launch, convergence decided on the device
-  {
-    PcgArgs A = pcg_args(h);
-    void* args[] = {(void*)&D, (void*)&A};
-    prof_begin(h, 7, -1);
-    CK(cudaLaunchCooperativeKernel((const void*)k_pcg, dim3(h->pcg_blocks), dim3(NTHR), args, h->smem_pcg, h->stream));
-    ++h->nlaunch;
-    prof_end(h, 7);
-  }
-  // recovery: v = B^T lam -> XW (w, -Phi^T v); p = S_pp^-1 sum N^T (x_p - (-Phi^T v)); full backward
-  if (h->n_p1 > 0) {
-    k_p1_lam<<<h->n_p1, NTHR, h->smem_pcg, h->stream>>>(D, h->d_it_p1, h->n_p1, h->lam, h->XW);
-    ++h->nlaunch;
-  }
-  launch_coarse(h, h->X1, h->XW);
-  prof_begin(h, 6, -1);
-  k_bwd_full<<<P, NTHR, h->smem_bwd_full, h->stream>>>(D, h->X1, h->XW, h->Pc, h->a_loc, h->G.nloc);
-  ++h->nlaunch;
-  prof_end(h, 6);
-  CKL();
+  prof_end(h, 7);
   CK(cudaMemcpyAsync(h->h_st, h->st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
   h->d2h_bytes += (int64_t)sizeof(PcgState);
   CK(cudaStreamSynchronize(h->stream));
-  const PcgState hs = *h->h_st;
-  const int iters = hs.iter;
   prof_collect(h, 1 << 30);
+  const PcgState hs = *h->h_st;
+  const int64_t hl = hs.counter[2];
+  std::vector<int> it(n);
+  CK(cudaMemcpy(it.data(), h->d_iters + h->steps_done, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  std::vector<double> hh(std::max<int64_t>(hl, 1));
+  if (hl > 0) CK(cudaMemcpy(hh.data(), h->hist + h->hist_len, sizeof(double) * hl, cudaMemcpyDeviceToHost));
+  h->d2h_bytes += (int64_t)(sizeof(int) * n + sizeof(double) * hl);
   if (hs.failed) {
+    const int bad = hs.rp;
     std::ostringstream o;
-    o << "PCG did not converge: step " << h->steps_done + 1 << ", iterations " << hs.iter << ", relres "
+    o << "PCG did not converge: step " << bad + 1 << ", iterations " << hs.iter << ", relres "
       << (hs.rho0 > 0 ? std::sqrt(std::max(hs.rz, 0.0) / hs.rho0) : 0.0) << (hs.nan ? " (curvature/NaN guard)" : "");
+    h->broken = true;
     return fail(h, TCG_ENOCONV, o.str());
   }
-  std::vector<double> hh(iters + 1);
-  CK(cudaMemcpy(hh.data(), h->hist, sizeof(double) * (iters + 1), cudaMemcpyDeviceToHost));
-  h->d2h_bytes += (int64_t)(sizeof(double) * (iters + 1));
-  h->iters.push_back(iters);
-  h->final_rel.push_back(hh.back());
-  h->hist_all.insert(h->hist_all.end(), hh.begin(), hh.end());
-  h->total_iters += iters;
-  h->steps_done += 1;
+  int64_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    h->iters.push_back(it[i]);
+    h->final_rel.push_back(hh[off + it[i]]);
+    off += it[i] + 1;
+    h->total_iters += it[i];
+  }
+  h->hist_all.insert(h->hist_all.end(), hh.begin(), hh.begin() + hl);
+  h->hist_len += hl;
+  h->steps_done += n;
   return TCG_OK;
 }
 
@@ -984,8 +1002,8 @@ tcg_status tcg_step(tcg_handle h, int n) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, h->stream);
-  for (int i = 0; i < n; ++i) {
-    tcg_status s = do_step(h);
+  {
+    tcg_status s = do_steps(h, n);
     if (s != TCG_OK) {
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
@@ -1135,11 +1153,13 @@ tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms) {
     }
     launch_coarse(h, h->XW, nullptr);
     if (h->n_p5 > 0) {
-      k_p5<<<h->n_p5, NTHR, h->smem_pcg, h->stream>>>(D, pcg_args(h), h->XW);
+      k_p5<<<h->n_p5, NTHR, h->smem_pcg, h->stream>>>(D, step_args(h), h->XW);
       ++h->nlaunch;
     }
-    k_dual_rhs<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->Yv, h->q, h->z);  // q = F r (z scratch)
-    ++h->nlaunch;
+    if (D.m > 0) {
+      k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->Yv, h->q);
+      ++h->nlaunch;
+    }
   }
   cudaEventRecord(e1, h->stream);
   CK(cudaEventSynchronize(e1));

@@ -393,3 +393,60 @@ __global__ void __launch_bounds__(128) k_sinv(const double* __restrict__ X, doub
 }
 
 }  // namespace tcg
+
+namespace tcg {
+
+// In-place inverse of the augmented local factor: row block I of every patch
+//   I <  Tr:  X_IJ = L_II^-1                          (J = I)
+//             X_IJ = -L_II^-1 sum_{K=J}^{I-1} L_IK X_KJ   (J < I)
+//   I >= Tr:  PhiT_IJ = sum_{K=J}^{Tr-1} L_IK X_KJ        (J < Tr; = W_pr W_rr^-1)
+// Rows < I already hold X, rows > I still hold L, so row I is computed into a per-patch
+// scratch row and copied back (k_xrow_copy) before row I+1. grid (maxTr, P), 128 threads.
+__global__ void __launch_bounds__(128) k_xinv_row(DevPlan D, int I, double* scratch, const int64_t* scr_off) {
+  const int s = blockIdx.y, J = blockIdx.x;
+  const int Tr = D.Ti[s] + D.Tb[s], T = D.T[s];
+  if (I >= T || J >= Tr || (I < Tr && J > I)) return;
+  extern __shared__ double smem[];
+  double* sA = smem;
+  double* sB = smem + TS * SPAD;
+  const double* A = D.A + D.a_off[s];
+  double* out = scratch + scr_off[s] + (int64_t)J * TSZ;
+  if (I < Tr && J == I) {
+    const double* Li = D.Dinv + D.dinv_off[s] + (int64_t)I * TSZ;
+    for (int e = threadIdx.x; e < TSZ / 2; e += blockDim.x)
+      reinterpret_cast<double2*>(out)[e] = reinterpret_cast<const double2*>(Li)[e];
+    return;
+  }
+  const int Kend = (I < Tr) ? I : Tr;
+  double acc[4][4][2];
+  acc_zero(acc);
+  for (int K = J; K < Kend; ++K) {
+    stage_tile(A + tri_off(I, K), sA);
+    stage_tile_T(A + tri_off(K, J), sB);
+    __syncthreads();
+    mma_acc(sA, sB, acc);
+    __syncthreads();
+  }
+  if (I >= Tr) {
+    acc_store(out, acc, 1.0);
+    return;
+  }
+  acc_to_smemT(sB, acc);
+  stage_tile(D.Dinv + D.dinv_off[s] + (int64_t)I * TSZ, sA);
+  __syncthreads();
+  double acc2[4][4][2];
+  acc_zero(acc2);
+  mma_acc(sA, sB, acc2);
+  acc_store(out, acc2, -1.0);
+}
+
+__global__ void k_xrow_copy(DevPlan D, int I, const double* scratch, const int64_t* scr_off) {
+  const int s = blockIdx.y, J = blockIdx.x;
+  const int Tr = D.Ti[s] + D.Tb[s], T = D.T[s];
+  if (I >= T || J >= Tr || (I < Tr && J > I)) return;
+  const double2* src = reinterpret_cast<const double2*>(scratch + scr_off[s] + (int64_t)J * TSZ);
+  double2* dst = reinterpret_cast<double2*>(D.A + D.a_off[s] + tri_off(I, J));
+  for (int e = threadIdx.x; e < TSZ / 2; e += blockDim.x) dst[e] = src[e];
+}
+
+}  // namespace tcg

@@ -1,52 +1,76 @@
-// pcg.cu — step c (the PCG on lambda) as chain-free GEMV work items in one persistent
-// cooperative kernel per implicit-Euler step (four grid barriers per PCG iteration).
+// pcg.cu — step c of the hot path: implicit-Euler time stepping (rhs, PCG on lambda,
+// recovery) as chain-free GEMV work items inside ONE persistent cooperative kernel that
+// runs n time steps (k_steps). No host round trip between steps or PCG iterations.
 //
-// Paper: PCG on the interface problem with the Dirichlet preconditioner, the dual
-// operator of the two sequential Schur complements; recurrences DESIGN.md R6.
-// Setup (chol.cu) leaves X_bb = L_bb^-1, Phi^T = L_pb X_bb (per patch) and the full
-// symmetric S_pp^-1 = X_c^T X_c. One PCG iteration is then:
-//   P1  p = z + beta p_prev (z = B_D S_bb B_D^T r from P7, on the fly); v_s = B_s^T p;
-//       w_s = X_bb v_s, (-g_s) = -Phi^T v_s                           items: patch row blocks
-//   PC  Pc = S_pp^-1 G, G = sum_s N_s^T (-g_s)  (= -S_pp^-1 g)        items: coarse row block x column chunk
-//   P5  y_s = X_bb^T w_s - Phi_b N_s Pc;  p^T F p = sum_s v_s . y_s   items: patch column blocks
-//   P7  alpha = rho / p^T F p; lambda += alpha p; r_new = r - alpha B y;
-//       u_s = B_D^T r_new, (S_bb u)_s;  r_new^T z = sum_s u_s . S_bb u_s   items: patch row blocks
-// so that every dot product is a sum of per-item partials (no separate jump phase): the
-// jump q = B y and z = B_D (S_bb u) are gathered on the fly where they are consumed.
-// Partials are summed in one fixed order by every block (bit-identical scalars, deterministic).
+// Paper: implicit Euler (eq. euler), the 3x3 block system after the e/p/r split
+// (P:L139-153), "two sequential Schur complements", PCG with the Dirichlet
+// preconditioner; recurrences DESIGN.md R6.
+// Setup (chol.cu) overwrites each patch's augmented Cholesky factor with its inverse
+//   Xaug = [X_rr = L_rr^-1 ; Phi^T = W_pr W_rr^-1]      (trailing b block of X_rr = L_bb^-1)
+// and builds S_pp^-1 = X_c^T X_c (full symmetric). Per step (phases separated by grid barriers):
+//   R1  f = (sigma/dt) M a + phi(t) j_S  (conductors);  insulators: Z = phi(t) XJ
+//   R2  Z_r = X_rr f_r,  Z_p = f_p - Phi^T f_r         (= L^-1 f, f_p - W_pr W_rr^-1 f_r)
+//   R3  Pc = S_pp^-1 sum_s N_s^T Z_p                     (p0)
+//   R4  y = X_bb^T Z_b - Phi_b N Pc ; d = B y            (dual rhs)
+//   R5  u = B_D^T d, S_bb u, rho0 = sum u.S u ; r = d, lambda = 0
+//   PCG iterations (4 barriers each):
+//   P1  p = z + beta p_prev (z gathered from the last S_bb apply); v = B^T p;
+//       w = X_bb v, (-g) = -Phi_b^T v
+//   PC  Pc = S_pp^-1 sum N^T (-g)
+//   P5  y = X_bb^T w - Phi_b N Pc ; p^T F p = sum_s v_s . y_s
+//   P7  alpha; lambda += alpha p; r -= alpha B y; u = B_D^T r, S_bb u; r^T z = sum u.S u
+//   E1  v = B^T lambda ; w, -Phi^T v                      (recovery)
+//   E2  Pc = S_pp^-1 sum N^T (Z_p + Phi^T v)              (= p)
+//   E3  a_r = X_rr^T (Z_r - [0; w_b]) - Phi N Pc ; a_p = N Pc ; a_e = 0
+// Partials are summed in one fixed order by every block: deterministic, identical scalars.
 #include "common.cuh"
 #include "device.h"
 
 namespace tcg {
 
-struct PcgArgs {
+struct StepArgs {
   // lambda-space vectors (m)
   double* lam;
   double* r[2];
   double* pk[2];
-  // per-patch aug-ordered vectors
-  double* XW;    // P1 output: b part w, p part -g
-  double* Y;     // P5 output: b part y
-  double* PW;    // P7 output: b part S_bb u
+  // per-patch aug-ordered vectors (64*T per patch)
+  double* F;     // R1 output (conductor rhs f)
+  double* Z;     // R2 output (Z_r = L^-1 f_r, Z_p = f_p - h)
+  double* XJ;    // setup: forward of j_S (insulator rhs template)
+  const double* JS;
+  double* XW;    // P1/E1 output: b part w, p part -g
+  double* Y;     // P5/R4 output: b part y
+  double* PW;    // S_bb apply output: b part
+  double* a_loc; // local coefficient vectors (npatch x nloc)
   // coarse
   const double* Sinv;  // full symmetric S_pp^-1, Tc x Tc row-major tiles
   double* Ppart;       // Tc x maxch x 64 chunk partials of Pc
   double* Pc;          // materialised coarse solution (standalone kernels)
-  int ch;              // tiles per coarse chunk
-  int maxch;
-  double* partA;       // per-block partials (P5)
-  double* partB;       // per-block partials (P7 / prologue)
-  double* hist;
+  int ch, maxch;
+  double* partA;
+  double* partB;
+  // per-step outputs
+  double* hist;        // concatenated histories (sum over steps of iters+1)
+  int* iters;          // per step
   PcgState* st;
   // item lists (sorted by decreasing cost)
   const int2* it_p1;  // (patch, row block of [b;p])
   const int2* it_p5;  // (patch, b column block)
   const int2* it_sy;  // (patch, b row block)
   const int2* it_pc;  // (coarse row block, column chunk)
-  int n_p1, n_p5, n_sy, n_pc;
+  const int2* it_fw;  // (conductor patch, aug row block)
+  const int2* it_bw;  // (patch, r column block)
+  int n_p1, n_p5, n_sy, n_pc, n_fw, n_bw;
   unsigned long long* tstamp;  // optional phase timestamps (block 0), 8 per iteration
   double rtol;
   int max_iter;
+  // time stepping
+  int source;
+  double dt;
+  int step0;    // steps done before this launch
+  int nsteps;   // steps to run
+  Tables1D tb;
+  Geom G;
 };
 
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
@@ -57,9 +81,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-__device__ __forceinline__ const double* ls_tile(const DevPlan& D, int s, int Tb, int I, int J) {
-  const double* L = D.LS + D.ls_off[s];
-  return I < Tb ? L + tri_off(I, J) : L + (tri_tiles(Tb) + (int64_t)(I - Tb) * Tb + J) * TSZ;
+// tile (I,J) of patch s's inverse factor Xaug (aug tile numbering)
+__device__ __forceinline__ const double* xtile(const DevPlan& D, int s, int I, int J) {
+  return D.A + D.a_off[s] + tri_off(I, J);
 }
 
 // fixed-order block reduction of one value per thread
@@ -76,15 +100,63 @@ __device__ __forceinline__ double block_sum(double local, double* red) {
 }
 
 // Coarse solution entry g from the PC chunk partials (fixed order).
-__device__ __forceinline__ double pc_get(const PcgArgs& A, int64_t g) {
+__device__ __forceinline__ double pc_get(const StepArgs& A, int64_t g) {
   const double* p = A.Ppart + ((g >> 6) * A.maxch) * TS + (g & 63);
   double v = 0.0;
   for (int c = 0; c < A.maxch; ++c) v += ldcg(p + (int64_t)c * TS);
   return v;
 }
 
-// ---- P1: row GEMV of [X_bb; Phi^T] with v = B_s^T p gathered per b position --------------
-// vsrc(b, pos) returns the signed value (B_s^T p)_pos, b = b_off[s] + pos.
+// ---- generic tile GEMVs over one tile row / column of Xaug ------------------------------
+// row:  part[r] += sum_{J=J0}^{J1-1} X(I,J)[row0+r][:] . x[(J-J0)*64 : ]      (x in smem)
+__device__ __forceinline__ void gemv_row(const DevPlan& D, int s, int I, int J0, int J1, const double* x,
+                                         double (&part)[8]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
+#pragma unroll 2
+  for (int J = J0; J < J1; ++J) {
+    const double* t = xtile(D, s, I, J) + row0 * TS + 2 * lane;
+    const double2 xv = *reinterpret_cast<const double2*>(x + (J - J0) * TS + 2 * lane);
+    double2 a[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
+  }
+}
+// col:  c[0..1] += sum_{I=I0}^{I1-1} X(I,J)[row0+r][2*lane..] * x[(I-I0)*64 + row0 + r]
+__device__ __forceinline__ void gemv_col(const DevPlan& D, int s, int J, int I0, int I1, const double* x, double& c0,
+                                         double& c1) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
+#pragma unroll 2
+  for (int I = I0; I < I1; ++I) {
+    const double* t = xtile(D, s, I, J) + row0 * TS + 2 * lane;
+    double2 a[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const double xr = x[(I - I0) * TS + row0 + r];
+      c0 += a[r].x * xr;
+      c1 += a[r].y * xr;
+    }
+  }
+}
+// finish a column GEMV: cross-warp sum into out64[0..63] (threads < 64 hold valid results)
+__device__ __forceinline__ double col_finish(double c0, double c1, double* cr) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  cr[warp * TS + 2 * lane] = c0;
+  cr[warp * TS + 2 * lane + 1] = c1;
+  __syncthreads();
+  double acc = 0.0;
+  if (threadIdx.x < TS) {
+#pragma unroll
+    for (int w = 0; w < NTHR / 32; ++w) acc += cr[w * TS + threadIdx.x];
+  }
+  return acc;
+}
+
+// ---- P1 / E1: [X_bb; Phi_b^T] v, v = B_s^T p gathered per b position ---------------------
+// vsrc(s, b, pos) returns (B_s^T p)_pos, b = b_off[s] + pos. Output XW: +w (b rows), -g (p rows).
 template <class Src>
 __device__ void p1_item(const DevPlan& D, int s, int I, Src vsrc, double* XW, double* sv) {
   const int Ti = D.Ti[s], Tb = D.Tb[s], nb = D.nb[s];
@@ -92,27 +164,18 @@ __device__ void p1_item(const DevPlan& D, int s, int I, Src vsrc, double* XW, do
   const int64_t bo = D.b_off[s];
   for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x) sv[e] = (e < nb) ? vsrc(s, bo + e, e) : 0.0;
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
   double part[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) part[r] = 0.0;
-#pragma unroll 2
-  for (int J = 0; J < Jn; ++J) {
-    const double* t = ls_tile(D, s, Tb, I, J) + row0 * TS + 2 * lane;
-    const double2 xv = *reinterpret_cast<const double2*>(sv + J * TS + 2 * lane);
-    double2 a[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
-  }
+  gemv_row(D, s, Ti + I, Ti, Ti + Jn, sv, part);
   const double sum = warp_reduce8(part);
+  const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
   if ((lane & 3) == 0) XW[D.vec_off[s] + (int64_t)(Ti + I) * TS + row0 + warp_reduce8_row()] = (I < Tb) ? sum : -sum;
   __syncthreads();
 }
 
-// ---- PC: Ppart[I][c] = sum_{J in chunk c} Sinv_IJ G_J,  G = sum_csr (src1 - src2) -----------
-__device__ void pc_item(const DevPlan& D, const PcgArgs& A, int I, int c, const double* src1, const double* src2,
+// ---- PC: Ppart[I][c] = sum_{J in chunk c} Sinv_IJ G_J,  G = sum_csr (src1 - src2) ----------
+__device__ void pc_item(const DevPlan& D, const StepArgs& A, int I, int c, const double* src1, const double* src2,
                         double* sm) {
   const int Tc = D.Tc;
   const int J0 = c * A.ch, J1 = min(Tc, J0 + A.ch);
@@ -148,18 +211,16 @@ __device__ void pc_item(const DevPlan& D, const PcgArgs& A, int I, int c, const 
   __syncthreads();
 }
 
-// ---- P5: column GEMV  y_J = sum_{I>=J} X_IJ^T w_I - sum_{p rows} PhiT_IJ^T (N Pc)_I ---------
-// Returns this item's share of p^T F p = v_J . y_J (vsrc gives the lambda values of p).
+// ---- P5 / R4: y_J = sum_{I>=J} X_bb,IJ^T w_I - sum_{p rows} PhiT_IJ^T (N Pc)_I -------------
+// Returns this item's share of v_J . y_J (vsrc gives (B_s^T p)_pos; pass zero for R4).
 template <class PcF, class Src>
 __device__ double p5_item(const DevPlan& D, int s, int J, const double* W, PcF pc, Src vsrc, double* Y, double* sm,
                           double* red) {
   const int Ti = D.Ti[s], Tb = D.Tb[s], Tp = D.Tp[s], np = D.np[s], nb = D.nb[s];
   const int Tr = Tb + (np > 0 ? Tp : 0);
-  double* sw = sm;                    // (Tr - J) * 64
-  double* cr = sm + (Tr - J) * TS;    // 8 * 64
+  double* sw = sm;                  // (Tr - J) * 64
+  double* cr = sm + (Tr - J) * TS;  // 8 * 64
   const int* grp = D.p_grp + D.p_off[s];
-  const int* bl = D.b_lam + D.b_off[s];
-  const double* bs = D.b_sign + D.b_off[s];
   const int64_t vo = D.vec_off[s] + (int64_t)Ti * TS;
   for (int e = threadIdx.x; e < (Tr - J) * TS; e += blockDim.x) {
     const int i = J * TS + e;  // row index in [b; p] numbering
@@ -172,45 +233,25 @@ __device__ double p5_item(const DevPlan& D, int s, int J, const double* W, PcF p
     sw[e] = val;
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
   double c0 = 0.0, c1 = 0.0;
-#pragma unroll 2
-  for (int I = J; I < Tr; ++I) {
-    const double* t = ls_tile(D, s, Tb, I, J) + row0 * TS + 2 * lane;
-    double2 a[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const double xr = sw[(I - J) * TS + row0 + r];
-      c0 += a[r].x * xr;
-      c1 += a[r].y * xr;
-    }
-  }
-  cr[warp * TS + 2 * lane] = c0;
-  cr[warp * TS + 2 * lane + 1] = c1;
-  __syncthreads();
+  gemv_col(D, s, Ti + J, Ti + J, Ti + Tr, sw, c0, c1);
+  const double acc = col_finish(c0, c1, cr);
   double contrib = 0.0;
   if (threadIdx.x < TS) {
-    double acc = 0.0;
-#pragma unroll
-    for (int w = 0; w < NTHR / 32; ++w) acc += cr[w * TS + threadIdx.x];
     Y[vo + (int64_t)J * TS + threadIdx.x] = acc;
     const int pos = J * TS + threadIdx.x;
-    if (pos < nb) contrib = bs[pos] * vsrc(bl[pos]) * acc;
+    if (pos < nb) contrib = vsrc(s, D.b_off[s] + pos, pos) * acc;
   }
   return block_sum(contrib, red);
 }
 
-// ---- P7: symmetric S_bb apply, one row block I of one patch (packed-lower storage: the
-// row's lower tiles as row GEMVs, the tiles below the diagonal as transposed GEMVs).
-// u = B_D^T r (weighted gather of usrc). Returns this item's share of u^T S_bb u.
-// usrc(s, b, pos) returns (B_D^(s)T r)_pos, b = b_off[s] + pos.
+// ---- P7 / R5: symmetric S_bb apply, one row block I of one patch --------------------------
+// usrc(s, b, pos) returns (B_D^(s)T r)_pos. Returns this item's share of u^T S_bb u.
 template <class Src>
-__device__ double symv_item(const DevPlan& D, const PcgArgs& A, int s, int I, Src usrc, double* sm, double* red) {
+__device__ double symv_item(const DevPlan& D, double* PW, int s, int I, Src usrc, double* sm, double* red) {
   const int Ti = D.Ti[s], Tb = D.Tb[s], nb = D.nb[s];
-  double* u = sm;               // Tb*64
-  double* cr = u + Tb * TS;     // 8 * 64
+  double* u = sm;            // Tb*64
+  double* cr = u + Tb * TS;  // 9 * 64
   const int64_t bo = D.b_off[s];
   for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) u[i] = (i < nb) ? usrc(s, bo + i, i) : 0.0;
   __syncthreads();
@@ -252,20 +293,75 @@ __device__ double symv_item(const DevPlan& D, const PcgArgs& A, int s, int I, Sr
     double acc = rs;
 #pragma unroll
     for (int w = 0; w < NTHR / 32; ++w) acc += cr[w * TS + row];
-    cr[8 * TS + row] = acc;  // staging slot after the 8 warp rows
+    cr[8 * TS + row] = acc;
   }
   __syncthreads();
   double contrib = 0.0;
   if (threadIdx.x < TS) {
     const double v = cr[8 * TS + threadIdx.x];
-    A.PW[D.vec_off[s] + (int64_t)(Ti + I) * TS + threadIdx.x] = v;
+    PW[D.vec_off[s] + (int64_t)(Ti + I) * TS + threadIdx.x] = v;
     contrib = u[I * TS + threadIdx.x] * v;
   }
   return block_sum(contrib, red);
 }
 
-// Sum of per-block partials in one fixed order (lane-strided + xor butterfly in warp 0),
-// broadcast through shared memory: bit-identical in every block.
+// ---- R2: forward item (conductor patch s, aug row block I): Z_I = X_IJ f_J / f_p - Phi^T f_r --
+__device__ void fw_item(const DevPlan& D, int s, int I, const double* Fv, double* Zv, double* sm) {
+  const int Tr = D.Ti[s] + D.Tb[s];
+  const int Jn = (I < Tr) ? I + 1 : Tr;
+  const int64_t vo = D.vec_off[s];
+  for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x) sm[e] = ldcg(Fv + vo + e);
+  __syncthreads();
+  double part[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) part[r] = 0.0;
+  gemv_row(D, s, I, 0, Jn, sm, part);
+  const double sum = warp_reduce8(part);
+  const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
+  if ((lane & 3) == 0) {
+    const int64_t idx = vo + (int64_t)I * TS + row0 + warp_reduce8_row();
+    Zv[idx] = (I < Tr) ? sum : ldcg(Fv + idx) - sum;
+  }
+  __syncthreads();
+}
+
+// ---- E3: backward item (patch s, r column block J): a_J = X_rr^T u - Phi N Pc, scattered ----
+template <class PcF>
+__device__ void bw_item(const DevPlan& D, int s, int J, const double* Zv, const double* XWv, PcF pc, double* a_loc,
+                        int nloc, double* sm) {
+  const int Ti = D.Ti[s], Tr = Ti + D.Tb[s], T = D.T[s], np = D.np[s];
+  const int64_t vo = D.vec_off[s];
+  const int* grp = D.p_grp + D.p_off[s];
+  const int* aug = D.aug + D.aug_off[s];
+  double* sx = sm;                 // (T - J) * 64
+  double* cr = sm + (T - J) * TS;  // 8 * 64
+  for (int e = threadIdx.x; e < (T - J) * TS; e += blockDim.x) {
+    const int i = J * TS + e;
+    double val;
+    if (i < Ti * TS) val = ldcg(Zv + vo + i);
+    else if (i < Tr * TS) val = ldcg(Zv + vo + i) - ldcg(XWv + vo + i);
+    else {
+      const int t = i - Tr * TS;
+      val = (t < np) ? -pc(grp[t]) : 0.0;
+    }
+    sx[e] = val;
+  }
+  __syncthreads();
+  double c0 = 0.0, c1 = 0.0;
+  gemv_col(D, s, J, J, T, sx, c0, c1);
+  const double acc = col_finish(c0, c1, cr);
+  double* as = a_loc + (int64_t)s * nloc;
+  if (threadIdx.x < TS) {
+    const int a = aug[J * TS + threadIdx.x];
+    if (a >= 0) as[a] = acc;
+  }
+  // primal values a_p = N Pc (written by the items of column block 0)
+  if (J == 0)
+    for (int t = threadIdx.x; t < np; t += blockDim.x) as[aug[Tr * TS + t]] = pc(grp[t]);
+  __syncthreads();
+}
+
+// Sum of per-block partials in one fixed order, broadcast: bit-identical in every block.
 __device__ __forceinline__ double sum_partials(const double* part, int n, double* bcast) {
   if (threadIdx.x < 32) {
     double t = 0.0;
@@ -279,9 +375,9 @@ __device__ __forceinline__ double sum_partials(const double* part, int n, double
   return r;
 }
 
-// Grid barrier for the cooperative (co-resident) launch: one monotonically increasing
-// arrival counter (zeroed by the host before the launch); thread 0 of each block arrives
-// with a release fence and polls with acquire loads until all blocks of this round arrived.
+// Grid barrier for the cooperative (co-resident) launch: monotone arrival counter (zeroed
+// by the host before the launch); thread 0 of each block arrives after a release fence and
+// polls with acquire loads until every block of this round arrived.
 __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& target) {
   __syncthreads();
   target += gridDim.x;
@@ -297,14 +393,73 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ta
   __syncthreads();
 }
 
+// rhs of one patch (R1): conductors F = (sigma/dt) M a + phi j_S, insulators Z = phi XJ
+__device__ void rhs_item(const DevPlan& D, const StepArgs& A, int s, double t) {
+  const double sig = D.sigma[s], nu = D.nu[s];
+  double phi = 0.0;
+  if (A.source == 1) phi = sinpi(2.0 * t);
+  else if (A.source == 2) phi = 2.0 * M_PI * M_PI * nu * (1.0 - exp(-t)) + sig * exp(-t);
+  const int R = D.T[s] * TS;
+  const int64_t vo = D.vec_off[s];
+  if (sig <= 0.0) {
+    for (int pos = threadIdx.x; pos < R; pos += blockDim.x) A.Z[vo + pos] = phi * ldcg(A.XJ + vo + pos);
+    return;
+  }
+  const Geom& G = A.G;
+  const Tables1D& tb = A.tb;
+  const int* aug = D.aug + D.aug_off[s];
+  const double* as = A.a_loc + (int64_t)s * G.nloc;
+  const int p = G.p;
+  const double inv_dt = 1.0 / A.dt;
+  for (int pos = threadIdx.x; pos < R; pos += blockDim.x) {
+    const int a = aug[pos];
+    if (a < 0) {
+      A.F[vo + pos] = 0.0;
+      continue;
+    }
+    int c = 0, rem = a;
+    for (;;) {
+      const int sz = G.cdim[c][0] * G.cdim[c][1] * G.cdim[c][2];
+      if (rem < sz) break;
+      rem -= sz;
+      ++c;
+    }
+    const int ii[3] = {rem % G.cdim[c][0], (rem / G.cdim[c][0]) % G.cdim[c][1], rem / (G.cdim[c][0] * G.cdim[c][1])};
+    int lo3[3], hi3[3];
+    for (int d = 0; d < 3; ++d) {
+      lo3[d] = max(0, ii[d] - p);
+      hi3[d] = min(G.cdim[c][d] - 1, ii[d] + p);
+    }
+    const int off = a - rem;
+    const int n0 = tb.el[0] + p, n1 = tb.el[1] + p, n2 = tb.el[2] + p;
+    // 1D factors: Md along direction c, Mb elsewhere
+    const double* fx = (c == 0) ? tb.base + tb.off_Md[0] + ii[0] * (n0 - 1) : tb.base + tb.off_Mb[0] + ii[0] * n0;
+    const double* fy = (c == 1) ? tb.base + tb.off_Md[1] + ii[1] * (n1 - 1) : tb.base + tb.off_Mb[1] + ii[1] * n1;
+    const double* fz = (c == 2) ? tb.base + tb.off_Md[2] + ii[2] * (n2 - 1) : tb.base + tb.off_Mb[2] + ii[2] * n2;
+    double acc = 0.0;
+    for (int k = lo3[2]; k <= hi3[2]; ++k) {
+      const double wz = fz[k];
+      for (int j = lo3[1]; j <= hi3[1]; ++j) {
+        const double wyz = fy[j] * wz;
+        const double* ar = as + off + G.cdim[c][0] * (j + G.cdim[c][1] * k);
+        double sx = 0.0;
+        for (int i = lo3[0]; i <= hi3[0]; ++i) sx += fx[i] * ldcg(ar + i);
+        acc += wyz * sx;
+      }
+    }
+    A.F[vo + pos] = sig * inv_dt * acc + phi * A.JS[vo + pos];
+  }
+}
+
 #define TSTAMP(slot) \
-  if (A.tstamp && b == 0 && threadIdx.x == 0 && it < 64) A.tstamp[it * 8 + (slot)] = gtimer()
+  if (A.tstamp && b == 0 && threadIdx.x == 0 && it < 64 && step == 0) A.tstamp[it * 8 + (slot)] = gtimer()
 
 // =======================================================================================
-// Persistent cooperative PCG (one launch per implicit-Euler step). Input: r[0] = d,
-// lam = 0. Output: lam, history, state. All blocks run the same number of barriers.
+// Persistent cooperative time stepper: A.nsteps implicit-Euler steps in one launch.
+// All blocks execute the same sequence of grid barriers (control flow depends only on
+// values every block computes identically).
 // =======================================================================================
-__global__ void __launch_bounds__(NTHR, 2) k_pcg(DevPlan D, PcgArgs A) {
+__global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   extern __shared__ double sm[];
   __shared__ double red[NTHR];
   const int NB = gridDim.x, b = blockIdx.x;
@@ -313,115 +468,154 @@ __global__ void __launch_bounds__(NTHR, 2) k_pcg(DevPlan D, PcgArgs A) {
   const int64_t k0 = min(m, (int64_t)b * chunk), k1 = min(m, k0 + chunk);
   unsigned int* bar = &A.st->counter[1];
   unsigned int bar_target = 0;
-  int it = 0;
-  const double* r0 = A.r[0];
-  // own/partner form of the jumps (per b position: a_own, a_part, partner index, sign, lambda)
   auto own_idx = [&](int s, int pos) { return D.vec_off[s] + (int64_t)D.Ti[s] * TS + pos; };
+  auto pcf = [&](int64_t g) { return pc_get(A, g); };
+  int64_t hoff = 0;
+  int total_status = 0;
 
-  // ---- prologue: u = B_D^T r0, PW = S_bb u, rho0 = r0^T z0 = sum u.S u ----
-  {
-    double loc = 0.0;
-    for (int i = b; i < A.n_sy; i += NB)
-      loc += symv_item(D, A, A.it_sy[i].x, A.it_sy[i].y,
-                       [&](int, int64_t bb, int) { return D.b_aown[bb] * D.b_sign[bb] * ldcg(r0 + D.b_lam[bb]); },
-                       sm, red);
-    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) A.pk[0][k] = 0.0;
-    if (threadIdx.x == 0) A.partB[b] = loc;
-  }
-  grid_barrier(bar, bar_target);
-  const double rho0 = sum_partials(A.partB, NB, red);
-  if (b == 0 && threadIdx.x == 0) {
-    A.hist[0] = 1.0;
-    A.st->rho0 = rho0;
-    A.st->rho = rho0;
-    A.st->iter = 0;
-  }
-  if (!(rho0 > 0.0) || m == 0) {
-    if (b == 0 && threadIdx.x == 0) {
-      A.st->done = 1;
-      if (!(rho0 >= 0.0)) { A.st->failed = 1; A.st->nan = 1; }
-    }
-    return;  // uniform across blocks
-  }
-  double rho = rho0, beta = 0.0;
-  int rp = 0, pp = 0;
-  int status = 0;  // 0 running, 1 converged, 2 failed
-  double rz = rho0;
-  for (;;) {
-    TSTAMP(0);
-    const double* pprev = A.pk[pp];
-    double* pcur = A.pk[pp ^ 1];
-    // p_k = z_k + beta p_prev,k with z = B_D (S_bb u) from P7; signed value at a b position:
-    // sign*z_k = a_own PW[own] + a_part PW[partner]
-    auto vnew = [&](int s, int64_t bb, int pos) {
-      return D.b_aown[bb] * ldcg(A.PW + own_idx(s, pos)) + D.b_apart[bb] * ldcg(A.PW + D.b_part[bb]) +
-             D.b_sign[bb] * beta * ldcg(pprev + D.b_lam[bb]);
-    };
-    // P1: v = B^T p (on the fly); w = X_bb v, -g = -Phi^T v; owners materialise p
-    for (int i = b; i < A.n_p1; i += NB) p1_item(D, A.it_p1[i].x, A.it_p1[i].y, vnew, A.XW, sm);
-    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
-      pcur[k] = D.wplus[k] * ldcg(A.PW + D.lam_idx_p[k]) - D.wminus[k] * ldcg(A.PW + D.lam_idx_m[k]) +
-                beta * ldcg(pprev + k);
+  for (int step = 0; step < A.nsteps; ++step) {
+    const double t = (A.step0 + step + 1) * A.dt;
+    int it = 0;
+    // ---- R1 rhs ----
+    for (int s = b; s < D.npatch; s += NB) rhs_item(D, A, s, t);
     grid_barrier(bar, bar_target);
-    TSTAMP(1);
-    // PC: Pc = S_pp^-1 G (chunk partials)
-    for (int i = b; i < A.n_pc; i += NB) pc_item(D, A, A.it_pc[i].x, A.it_pc[i].y, A.XW, nullptr, sm);
+    // ---- R2 forward (conductors) ----
+    for (int i = b; i < A.n_fw; i += NB) fw_item(D, A.it_fw[i].x, A.it_fw[i].y, A.F, A.Z, sm);
     grid_barrier(bar, bar_target);
-    TSTAMP(2);
-    // P5: y = X_bb^T w - Phi_b N Pc ; partial p^T F p
+    // ---- R3 p0 = S_pp^-1 sum N^T Z_p ----
+    for (int i = b; i < A.n_pc; i += NB) pc_item(D, A, A.it_pc[i].x, A.it_pc[i].y, A.Z, nullptr, sm);
+    grid_barrier(bar, bar_target);
+    // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
+    for (int i = b; i < A.n_p5; i += NB)
+      p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.Z, pcf, [&](int, int64_t, int) { return 0.0; }, A.Y, sm, red);
+    grid_barrier(bar, bar_target);
+    // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
     {
       double loc = 0.0;
-      for (int i = b; i < A.n_p5; i += NB)
-        loc += p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.XW, [&](int64_t g) { return pc_get(A, g); },
-                       [&](int k) { return ldcg(pcur + k); }, A.Y, sm, red);
-      if (threadIdx.x == 0) A.partA[b] = loc;
-    }
-    grid_barrier(bar, bar_target);
-    TSTAMP(3);
-    const double pq = sum_partials(A.partA, NB, red);
-    if (!(pq > 0.0)) { status = 2; break; }  // lost positive curvature (uniform)
-    const double alpha = rho / pq;
-    const double* rc = A.r[rp];
-    double* rn = A.r[rp ^ 1];
-    // u_pos = a_own (sign r_k - alpha sign q_k), sign q_k = Y[own] - Y[partner]
-    auto unew = [&](int s, int64_t bb, int pos) {
-      return D.b_aown[bb] * (D.b_sign[bb] * ldcg(rc + D.b_lam[bb]) -
-                             alpha * (ldcg(A.Y + own_idx(s, pos)) - ldcg(A.Y + D.b_part[bb])));
-    };
-    // P7: lambda, r updates (owners); S_bb apply of u = B_D^T r_new; partial r_new^T z
-    {
+      for (int i = b; i < A.n_sy; i += NB)
+        loc += symv_item(D, A.PW, A.it_sy[i].x, A.it_sy[i].y,
+                         [&](int s, int64_t bb, int pos) {
+                           return D.b_aown[bb] * (ldcg(A.Y + own_idx(s, pos)) - ldcg(A.Y + D.b_part[bb]));
+                         },
+                         sm, red);
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-        A.lam[k] += alpha * ldcg(pcur + k);
-        rn[k] = ldcg(rc + k) - alpha * (ldcg(A.Y + D.lam_idx_p[k]) - ldcg(A.Y + D.lam_idx_m[k]));
+        A.r[0][k] = ldcg(A.Y + D.lam_idx_p[k]) - ldcg(A.Y + D.lam_idx_m[k]);
+        A.pk[0][k] = 0.0;
+        A.lam[k] = 0.0;
       }
-      double loc = 0.0;
-      for (int i = b; i < A.n_sy; i += NB) loc += symv_item(D, A, A.it_sy[i].x, A.it_sy[i].y, unew, sm, red);
       if (threadIdx.x == 0) A.partB[b] = loc;
     }
     grid_barrier(bar, bar_target);
-    TSTAMP(4);
-    rz = sum_partials(A.partB, NB, red);
-    ++it;
-    const double rel = sqrt(fmax(rz, 0.0) / rho0);
-    if (b == 0 && threadIdx.x == 0) A.hist[it] = rel;
-    rp ^= 1;
-    pp ^= 1;
-    if (rel <= A.rtol) { status = 1; break; }
-    if (it >= A.max_iter || !(rz == rz)) { status = 2; break; }
-    beta = rz / rho;
-    rho = rz;
+    const double rho0 = sum_partials(A.partB, NB, red);
+    if (b == 0 && threadIdx.x == 0) A.hist[hoff] = 1.0;
+    int status = 0;  // 0 running, 1 converged, 2 failed
+    double rz = rho0;
+    if (!(rho0 >= 0.0)) status = 2;
+    else if (!(rho0 > 0.0) || m == 0) status = 1;  // d = 0: lambda = 0 after 0 iterations
+    double rho = rho0, beta = 0.0;
+    int rp = 0, pp = 0;
+    while (status == 0) {
+      TSTAMP(0);
+      const double* pprev = A.pk[pp];
+      double* pcur = A.pk[pp ^ 1];
+      // P1
+      auto vnew = [&](int s, int64_t bb, int pos) {
+        return D.b_aown[bb] * ldcg(A.PW + own_idx(s, pos)) + D.b_apart[bb] * ldcg(A.PW + D.b_part[bb]) +
+               D.b_sign[bb] * beta * ldcg(pprev + D.b_lam[bb]);
+      };
+      for (int i = b; i < A.n_p1; i += NB) p1_item(D, A.it_p1[i].x, A.it_p1[i].y, vnew, A.XW, sm);
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
+        pcur[k] = D.wplus[k] * ldcg(A.PW + D.lam_idx_p[k]) - D.wminus[k] * ldcg(A.PW + D.lam_idx_m[k]) +
+                  beta * ldcg(pprev + k);
+      grid_barrier(bar, bar_target);
+      TSTAMP(1);
+      // PC
+      for (int i = b; i < A.n_pc; i += NB) pc_item(D, A, A.it_pc[i].x, A.it_pc[i].y, A.XW, nullptr, sm);
+      grid_barrier(bar, bar_target);
+      TSTAMP(2);
+      // P5
+      {
+        double loc = 0.0;
+        for (int i = b; i < A.n_p5; i += NB)
+          loc += p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.XW, pcf,
+                         [&](int, int64_t bb, int) { return D.b_sign[bb] * ldcg(pcur + D.b_lam[bb]); }, A.Y, sm, red);
+        if (threadIdx.x == 0) A.partA[b] = loc;
+      }
+      grid_barrier(bar, bar_target);
+      TSTAMP(3);
+      const double pq = sum_partials(A.partA, NB, red);
+      if (!(pq > 0.0)) { status = 2; break; }  // lost positive curvature (uniform)
+      const double alpha = rho / pq;
+      const double* rc = A.r[rp];
+      double* rn = A.r[rp ^ 1];
+      auto unew = [&](int s, int64_t bb, int pos) {
+        return D.b_aown[bb] * (D.b_sign[bb] * ldcg(rc + D.b_lam[bb]) -
+                               alpha * (ldcg(A.Y + own_idx(s, pos)) - ldcg(A.Y + D.b_part[bb])));
+      };
+      // P7
+      {
+        for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+          A.lam[k] += alpha * ldcg(pcur + k);
+          rn[k] = ldcg(rc + k) - alpha * (ldcg(A.Y + D.lam_idx_p[k]) - ldcg(A.Y + D.lam_idx_m[k]));
+        }
+        double loc = 0.0;
+        for (int i = b; i < A.n_sy; i += NB) loc += symv_item(D, A.PW, A.it_sy[i].x, A.it_sy[i].y, unew, sm, red);
+        if (threadIdx.x == 0) A.partB[b] = loc;
+      }
+      grid_barrier(bar, bar_target);
+      TSTAMP(4);
+      rz = sum_partials(A.partB, NB, red);
+      ++it;
+      const double rel = sqrt(fmax(rz, 0.0) / rho0);
+      if (b == 0 && threadIdx.x == 0) A.hist[hoff + it] = rel;
+      rp ^= 1;
+      pp ^= 1;
+      if (rel <= A.rtol) status = 1;
+      else if (it >= A.max_iter || !(rz == rz)) status = 2;
+      beta = rz / rho;
+      rho = rz;
+    }
+    if (b == 0 && threadIdx.x == 0) {
+      A.iters[A.step0 + step] = it;
+      A.st->iter = it;
+      A.st->rho0 = rho0;
+      A.st->rz = rz;
+    }
+    if (status == 2) {  // uniform: report and stop the remaining steps
+      if (b == 0 && threadIdx.x == 0) {
+        A.st->failed = 1;
+        A.st->nan = !(rz == rz);
+        A.st->rp = A.step0 + step;  // failing step index
+      }
+      total_status = 2;
+      break;
+    }
+    hoff += it + 1;
+    // ---- E1 v = B^T lambda ; w, -Phi^T v ----
+    for (int i = b; i < A.n_p1; i += NB)
+      p1_item(D, A.it_p1[i].x, A.it_p1[i].y,
+              [&](int, int64_t bb, int) { return D.b_sign[bb] * ldcg(A.lam + D.b_lam[bb]); }, A.XW, sm);
+    grid_barrier(bar, bar_target);
+    // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
+    for (int i = b; i < A.n_pc; i += NB) pc_item(D, A, A.it_pc[i].x, A.it_pc[i].y, A.Z, A.XW, sm);
+    grid_barrier(bar, bar_target);
+    // ---- E3 a_r = X_rr^T (Z_r - [0; w_b]) - Phi N p, a_p = N p ----
+    for (int i = b; i < A.n_bw; i += NB) bw_item(D, A.it_bw[i].x, A.it_bw[i].y, A.Z, A.XW, pcf, A.a_loc, A.G.nloc, sm);
+    grid_barrier(bar, bar_target);
   }
   if (b == 0 && threadIdx.x == 0) {
-    A.st->iter = it;
-    A.st->rz = rz;
     A.st->done = 1;
-    A.st->failed = (status == 2);
-    A.st->nan = (status == 2 && !(rz == rz));
-    A.st->rp = rp;
+    if (total_status != 2) A.st->failed = 0;
+    A.st->counter[2] = (unsigned int)hoff;  // history length written
   }
 }
 
-// ---- standalone item kernels (rhs stage, recovery, F-apply benchmark): one item per block ----
+// ---- standalone item kernels (setup precompute, F-apply benchmark): one item per block ----
+__global__ void __launch_bounds__(NTHR) k_fw(DevPlan D, const int2* items, int n, const double* Fv, double* Zv) {
+  extern __shared__ double sm[];
+  if (blockIdx.x >= n) return;
+  fw_item(D, items[blockIdx.x].x, items[blockIdx.x].y, Fv, Zv, sm);
+}
 __global__ void __launch_bounds__(NTHR) k_p1_lam(DevPlan D, const int2* items, int n, const double* __restrict__ lam,
                                                  double* XW) {
   extern __shared__ double sm[];
@@ -429,30 +623,27 @@ __global__ void __launch_bounds__(NTHR) k_p1_lam(DevPlan D, const int2* items, i
   p1_item(D, items[blockIdx.x].x, items[blockIdx.x].y,
           [&](int, int64_t bb, int) { return D.b_sign[bb] * lam[D.b_lam[bb]]; }, XW, sm);
 }
-__global__ void __launch_bounds__(NTHR) k_pc(DevPlan D, PcgArgs A, const double* src1, const double* src2) {
+__global__ void __launch_bounds__(NTHR) k_pc(DevPlan D, StepArgs A, const double* src1, const double* src2) {
   extern __shared__ double sm[];
   if (blockIdx.x >= A.n_pc) return;
   pc_item(D, A, A.it_pc[blockIdx.x].x, A.it_pc[blockIdx.x].y, src1, src2, sm);
 }
-// materialise Pc from the chunk partials
-__global__ void k_pc_sum(DevPlan D, PcgArgs A) {
+__global__ void k_pc_sum(DevPlan D, StepArgs A) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D.nc; g += (int64_t)gridDim.x * blockDim.x)
     A.Pc[g] = pc_get(A, g);
 }
-__global__ void __launch_bounds__(NTHR) k_p5(DevPlan D, PcgArgs A, const double* W) {
+__global__ void __launch_bounds__(NTHR) k_p5(DevPlan D, StepArgs A, const double* W) {
   extern __shared__ double sm[];
   __shared__ double red[NTHR];
   if (blockIdx.x >= A.n_p5) return;
   p5_item(D, A.it_p5[blockIdx.x].x, A.it_p5[blockIdx.x].y, W, [&](int64_t g) { return ldcg(A.Pc + g); },
-          [&](int) { return 0.0; }, A.Y, sm, red);
+          [&](int, int64_t, int) { return 0.0; }, A.Y, sm, red);
 }
-// d = B y -> r[0], lam = 0
-__global__ void k_dual_rhs(DevPlan D, const double* Y, double* r0, double* lam) {
+// q = B y (F-apply benchmark output)
+__global__ void k_jump(DevPlan D, const double* Y, double* q) {
   const int64_t m = D.m;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
-    r0[k] = ldcg(Y + D.lam_idx_p[k]) - ldcg(Y + D.lam_idx_m[k]);
-    lam[k] = 0.0;
-  }
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x)
+    q[k] = ldcg(Y + D.lam_idx_p[k]) - ldcg(Y + D.lam_idx_m[k]);
 }
 
 }  // namespace tcg
