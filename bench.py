@@ -31,7 +31,7 @@ import numpy as np  # noqa: E402
 
 import workloads  # noqa: E402
 
-KERNELS = {5: "k_fwd_full", 6: "k_bwd_full", 7: "k_pcg"}
+KERNELS = {7: "k_steps"}
 
 
 def peaks():
@@ -243,10 +243,11 @@ def main():
             if i2["prof_launches"] > 0:
                 bpl = i2["prof_bytes_per_launch"]
                 if kid == 7:
-                    # persistent PCG: per launch (= per Euler step) it * (B_F + B_M) + B_M (prologue z0)
+                    # persistent stepper (one launch = n_t steps): per step it*(B_F+B_M) for the PCG,
+                    # + B_M (z0) + B_F (p0/d and recovery GEMVs) + the full-factor rhs/recovery bytes
                     it, _, _ = s.history()
-                    bpl = float(np.mean([k * (i2["bytes_fapply"] + i2["bytes_precond"]) + i2["bytes_precond"]
-                                         for k in it]))
+                    bpl = float(sum(k * (i2["bytes_fapply"] + i2["bytes_precond"]) + i2["bytes_precond"] +
+                                    i2["bytes_fapply"] + i2["bytes_step_fixed"] for k in it))
                 shares[KERNELS[kid]] = {"ms_per_pass": i2["prof_ms"], "launches": i2["prof_launches"],
                                         "us_per_launch": 1000 * i2["prof_ms"] / i2["prof_launches"],
                                         "bytes_per_launch": bpl}

@@ -80,6 +80,9 @@ struct tcg_ctx {
   int2* d_it_fw = nullptr;
   int2* d_it_fw_all = nullptr;
   int2* d_it_bw = nullptr;
+  int2* d_it_bwc = nullptr;
+  int2* d_it_rhs = nullptr;
+  int n_bwc = 0, n_rhs = 0;
   double* xscratch = nullptr;      // per-patch scratch row for the in-place factor inversion
   int64_t* d_scr_off = nullptr;
   double* F = nullptr;             // conductor rhs (aug order)
@@ -521,6 +524,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dalloc(h, &h->xscratch, tot));
   }
   TRY(dalloc(h, &h->F, ov));
+  CK(cudaMemsetAsync(h->F, 0, sizeof(double) * ov, h->stream));
   TRY(dalloc(h, &h->d_iters, (size_t)h->n_steps + 1));
   h->hist_cap = (int64_t)(h->n_steps + 1) * (h->max_iter + 1);
   TRY(dalloc(h, &D.Sbb, os));
@@ -546,8 +550,8 @@ static tcg_status do_setup(tcg_ctx* h) {
   TRY(dalloc(h, &h->partA, 4096));
   TRY(dalloc(h, &h->partB, 4096));
   if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) {
-    TRY(dalloc(h, &h->tstamp, 8 * 64));
-    CK(cudaMemsetAsync(h->tstamp, 0, 8 * 64 * sizeof(unsigned long long), h->stream));
+    TRY(dalloc(h, &h->tstamp, 8 * 64 + 16));
+    CK(cudaMemsetAsync(h->tstamp, 0, (8 * 64 + 16) * sizeof(unsigned long long), h->stream));
   }
   CK(cudaMemsetAsync(h->Yv, 0, sizeof(double) * ov, h->stream));
   {
@@ -561,7 +565,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     const int64_t ctiles = (int64_t)Tc * Tc;
     h->coarse_ch = (int)std::max<int64_t>(1, std::min<int64_t>(64, ctiles / (4 * (int64_t)dev_sms)));
     h->coarse_maxch = std::max(1, (Tc + h->coarse_ch - 1) / h->coarse_ch);
-    std::vector<std::pair<int, int2>> p1, p5, sy, pcv, fw, fwa, bw;
+    std::vector<std::pair<int, int2>> p1, p5, sy, pcv, fw, fwa, bw, bwc, rhs;
     for (int s = 0; s < P; ++s) {
       const int Trs = Ti[s] + Tb[s];
       for (int I = 0; I < T[s]; ++I) {
@@ -569,7 +573,14 @@ static tcg_status do_setup(tcg_ctx* h) {
         if (pl.sigma[s] > 0) fw.push_back({cost, make_int2(s, I)});
         fwa.push_back({cost, make_int2(s, I)});
       }
-      for (int J = 0; J < std::max(Trs, 1); ++J) bw.push_back({T[s] - J, make_int2(s, J)});
+      for (int J = 0; J < std::max(Trs, 1); ++J) {
+        bw.push_back({T[s] - J, make_int2(s, J)});
+        if (pl.sigma[s] > 0) bwc.push_back({T[s] - J, make_int2(s, J)});
+      }
+      if (pl.sigma[s] > 0)
+        for (int c = 0; c < 3; ++c) rhs.push_back({pl.nloc / 3, make_int2(s, c)});
+      else
+        rhs.push_back({T[s] * TS / 8, make_int2(s, -1)});
       for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.push_back({I < Tb[s] ? I + 1 : Tb[s], make_int2(s, I)});
       for (int J = 0; J < Tb[s]; ++J) p5.push_back({Tb[s] - J + Tp[s], make_int2(s, J)});
       for (int I = 0; I < Tb[s]; ++I) sy.push_back({Tb[s], make_int2(s, I)});
@@ -594,6 +605,18 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(upload(fw, &h->d_it_fw, &h->n_fw));
     TRY(upload(fwa, &h->d_it_fw_all, &h->n_fw_all));
     TRY(upload(bw, &h->d_it_bw, &h->n_bw));
+    TRY(upload(bwc, &h->d_it_bwc, &h->n_bwc));
+    TRY(upload(rhs, &h->d_it_rhs, &h->n_rhs));
+    // local id -> aug position
+    std::vector<int> l2a((size_t)P * pl.nloc, -1);
+    for (int s = 0; s < P; ++s) {
+      const auto& aug = pl.pp[s].aug;
+      for (size_t pos = 0; pos < aug.size(); ++pos)
+        if (aug[pos] >= 0) l2a[(size_t)s * pl.nloc + aug[pos]] = (int)pos;
+    }
+    int* dl2a;
+    TRY(dupload(h, &dl2a, l2a));
+    D.loc2aug = dl2a;
     TRY(dalloc(h, &h->Sinv, (size_t)Tc * Tc * TSZ));
     TRY(dalloc(h, &h->Ppart, (size_t)Tc * h->coarse_maxch * TS));
   }
@@ -678,6 +701,9 @@ static tcg_status do_setup(tcg_ctx* h) {
     size_t p34 = (size_t)h->coarse_ch * TS;
     size_t syv = (size_t)h->maxTb * TS + 9 * TS;
     size_t fwb = (size_t)h->maxT * TS + 8 * TS;  // forward / backward full-factor items
+    size_t maxcomp = 0;
+    for (int c = 0; c < 3; ++c) maxcomp = std::max(maxcomp, (size_t)pl.comp_dim(c, 0) * pl.comp_dim(c, 1) * pl.comp_dim(c, 2));
+    fwb = std::max(fwb, 2 * maxcomp);  // rhs mass apply (two component buffers)
     p34 = std::max(p34, fwb);
     h->smem_pcg = sizeof(double) * std::max(std::max(p1, p5), std::max(p34, syv));
     TRY(set_smem(h, (const void*)k_steps, h->smem_pcg));
@@ -774,6 +800,10 @@ static StepArgs step_args(tcg_ctx* h) {
   A.it_pc = h->d_it_pc;
   A.it_fw = h->d_it_fw;
   A.it_bw = h->d_it_bw;
+  A.it_bwc = h->d_it_bwc;
+  A.it_rhs = h->d_it_rhs;
+  A.n_bwc = h->n_bwc;
+  A.n_rhs = h->n_rhs;
   A.n_p1 = h->n_p1;
   A.n_p5 = h->n_p5;
   A.n_sy = h->n_sy;
@@ -1202,7 +1232,7 @@ tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t 
     for (int64_t k = 0; k < h->D.m; ++k) { tmp.push_back(wp[k]); tmp.push_back(wm[k]); }
   } else if (what == 7) {
     if (!h->tstamp) return fail(h, TCG_ESTATE, "TCG_PHASE_TIMING not set");
-    std::vector<unsigned long long> ts(8 * 64);
+    std::vector<unsigned long long> ts(8 * 64 + 16);
     CK(cudaMemcpy(ts.data(), h->tstamp, ts.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     for (auto v : ts) tmp.push_back((double)v);
   } else if (what == 6) {

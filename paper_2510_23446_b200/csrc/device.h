@@ -44,6 +44,7 @@ struct DevPlan {
   const int64_t* vec_off;   // aug-ordered per-patch vectors (64*T each)
   const int64_t* aug_off;
   const int* aug;           // aug position -> local id (-1 padding)
+  const int* loc2aug;       // per patch (npatch x nloc): local id -> aug position (-1 eliminated)
   const int64_t* b_off;     // per patch offset into b_lam / b_sign
   const int* b_lam;
   const double* b_sign;

@@ -59,8 +59,10 @@ struct StepArgs {
   const int2* it_sy;  // (patch, b row block)
   const int2* it_pc;  // (coarse row block, column chunk)
   const int2* it_fw;  // (conductor patch, aug row block)
-  const int2* it_bw;  // (patch, r column block)
-  int n_p1, n_p5, n_sy, n_pc, n_fw, n_bw;
+  const int2* it_bw;  // (patch, r column block), all patches
+  const int2* it_bwc; // (patch, r column block), conductor patches only
+  const int2* it_rhs; // (patch, component) for conductors, (patch, -1) for insulators
+  int n_p1, n_p5, n_sy, n_pc, n_fw, n_bw, n_bwc, n_rhs;
   unsigned long long* tstamp;  // optional phase timestamps (block 0), 8 per iteration
   double rtol;
   int max_iter;
@@ -393,66 +395,68 @@ __device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& ta
   __syncthreads();
 }
 
-// rhs of one patch (R1): conductors F = (sigma/dt) M a + phi j_S, insulators Z = phi XJ
-__device__ void rhs_item(const DevPlan& D, const StepArgs& A, int s, double t) {
+// rhs item (R1). c in {0,1,2}: component c of conductor patch s, F = (sigma/dt) M a + phi j_S
+// with the mass apply sum-factorised (M_c = F_z (x) F_y (x) F_x, F_d = Md along d == c, Mb else;
+// banded |i-i'| <= p) through shared memory; c = -1: insulator patch s, Z = phi(t) XJ.
+__device__ void rhs_item(const DevPlan& D, const StepArgs& A, int s, int c, double t, double* sm) {
   const double sig = D.sigma[s], nu = D.nu[s];
   double phi = 0.0;
   if (A.source == 1) phi = sinpi(2.0 * t);
   else if (A.source == 2) phi = 2.0 * M_PI * M_PI * nu * (1.0 - exp(-t)) + sig * exp(-t);
-  const int R = D.T[s] * TS;
   const int64_t vo = D.vec_off[s];
-  if (sig <= 0.0) {
+  if (c < 0) {
+    const int R = D.T[s] * TS;
     for (int pos = threadIdx.x; pos < R; pos += blockDim.x) A.Z[vo + pos] = phi * ldcg(A.XJ + vo + pos);
     return;
   }
   const Geom& G = A.G;
   const Tables1D& tb = A.tb;
-  const int* aug = D.aug + D.aug_off[s];
-  const double* as = A.a_loc + (int64_t)s * G.nloc;
   const int p = G.p;
-  const double inv_dt = 1.0 / A.dt;
-  for (int pos = threadIdx.x; pos < R; pos += blockDim.x) {
-    const int a = aug[pos];
-    if (a < 0) {
-      A.F[vo + pos] = 0.0;
-      continue;
-    }
-    int c = 0, rem = a;
-    for (;;) {
-      const int sz = G.cdim[c][0] * G.cdim[c][1] * G.cdim[c][2];
-      if (rem < sz) break;
-      rem -= sz;
-      ++c;
-    }
-    const int ii[3] = {rem % G.cdim[c][0], (rem / G.cdim[c][0]) % G.cdim[c][1], rem / (G.cdim[c][0] * G.cdim[c][1])};
-    int lo3[3], hi3[3];
-    for (int d = 0; d < 3; ++d) {
-      lo3[d] = max(0, ii[d] - p);
-      hi3[d] = min(G.cdim[c][d] - 1, ii[d] + p);
-    }
-    const int off = a - rem;
-    const int n0 = tb.el[0] + p, n1 = tb.el[1] + p, n2 = tb.el[2] + p;
-    // 1D factors: Md along direction c, Mb elsewhere
-    const double* fx = (c == 0) ? tb.base + tb.off_Md[0] + ii[0] * (n0 - 1) : tb.base + tb.off_Mb[0] + ii[0] * n0;
-    const double* fy = (c == 1) ? tb.base + tb.off_Md[1] + ii[1] * (n1 - 1) : tb.base + tb.off_Mb[1] + ii[1] * n1;
-    const double* fz = (c == 2) ? tb.base + tb.off_Md[2] + ii[2] * (n2 - 1) : tb.base + tb.off_Mb[2] + ii[2] * n2;
-    double acc = 0.0;
-    for (int k = lo3[2]; k <= hi3[2]; ++k) {
-      const double wz = fz[k];
-      for (int j = lo3[1]; j <= hi3[1]; ++j) {
-        const double wyz = fy[j] * wz;
-        const double* ar = as + off + G.cdim[c][0] * (j + G.cdim[c][1] * k);
-        double sx = 0.0;
-        for (int i = lo3[0]; i <= hi3[0]; ++i) sx += fx[i] * ldcg(ar + i);
-        acc += wyz * sx;
-      }
-    }
-    A.F[vo + pos] = sig * inv_dt * acc + phi * A.JS[vo + pos];
+  const int nx = G.cdim[c][0], ny = G.cdim[c][1], nz = G.cdim[c][2];
+  const int nn = nx * ny * nz;
+  int off = 0;
+  for (int cc = 0; cc < c; ++cc) off += G.cdim[cc][0] * G.cdim[cc][1] * G.cdim[cc][2];
+  const double* as = A.a_loc + (int64_t)s * G.nloc + off;
+  double* u0 = sm;
+  double* u1 = sm + nn;
+  // 1D factors (row-major; Md is (n-1)x(n-1), Mb n x n)
+  const int n0 = tb.el[0] + p, n1 = tb.el[1] + p, n2 = tb.el[2] + p;
+  const double* Fx = (c == 0) ? tb.base + tb.off_Md[0] : tb.base + tb.off_Mb[0];
+  const double* Fy = (c == 1) ? tb.base + tb.off_Md[1] : tb.base + tb.off_Mb[1];
+  const double* Fz = (c == 2) ? tb.base + tb.off_Md[2] : tb.base + tb.off_Mb[2];
+  const int ldx = (c == 0) ? n0 - 1 : n0, ldy = (c == 1) ? n1 - 1 : n1, ldz = (c == 2) ? n2 - 1 : n2;
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {  // x pass
+    const int i = e % nx, jk = e / nx;
+    double v = 0.0;
+    for (int q = max(0, i - p); q <= min(nx - 1, i + p); ++q) v += Fx[i * ldx + q] * ldcg(as + jk * nx + q);
+    u0[e] = v;
   }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {  // y pass
+    const int i = e % nx, j = (e / nx) % ny, k = e / (nx * ny);
+    double v = 0.0;
+    for (int q = max(0, j - p); q <= min(ny - 1, j + p); ++q) v += Fy[j * ldy + q] * u0[i + nx * (q + ny * k)];
+    u1[e] = v;
+  }
+  __syncthreads();
+  const int* l2a = D.loc2aug + (int64_t)s * G.nloc + off;
+  const double scale = sig / A.dt;
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {  // z pass + scatter into aug order
+    const int pos = l2a[e];
+    if (pos < 0) continue;
+    const int ij = e % (nx * ny), k = e / (nx * ny);
+    double v = 0.0;
+    for (int q = max(0, k - p); q <= min(nz - 1, k + p); ++q) v += Fz[k * ldz + q] * u1[ij + nx * ny * q];
+    A.F[vo + pos] = scale * v + phi * A.JS[vo + pos];
+  }
+  __syncthreads();
 }
 
 #define TSTAMP(slot) \
   if (A.tstamp && b == 0 && threadIdx.x == 0 && it < 64 && step == 0) A.tstamp[it * 8 + (slot)] = gtimer()
+// step-level stamps of step 0 (slots 512..527): R1..R5 ends, loop end, E1..E3 ends
+#define SSTAMP(slot) \
+  if (A.tstamp && b == 0 && threadIdx.x == 0 && step == 0) A.tstamp[512 + (slot)] = gtimer()
 
 // =======================================================================================
 // Persistent cooperative time stepper: A.nsteps implicit-Euler steps in one launch.
@@ -476,19 +480,24 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   for (int step = 0; step < A.nsteps; ++step) {
     const double t = (A.step0 + step + 1) * A.dt;
     int it = 0;
+    SSTAMP(0);
     // ---- R1 rhs ----
-    for (int s = b; s < D.npatch; s += NB) rhs_item(D, A, s, t);
+    for (int i = b; i < A.n_rhs; i += NB) rhs_item(D, A, A.it_rhs[i].x, A.it_rhs[i].y, t, sm);
     grid_barrier(bar, bar_target);
+    SSTAMP(1);
     // ---- R2 forward (conductors) ----
     for (int i = b; i < A.n_fw; i += NB) fw_item(D, A.it_fw[i].x, A.it_fw[i].y, A.F, A.Z, sm);
     grid_barrier(bar, bar_target);
+    SSTAMP(2);
     // ---- R3 p0 = S_pp^-1 sum N^T Z_p ----
     for (int i = b; i < A.n_pc; i += NB) pc_item(D, A, A.it_pc[i].x, A.it_pc[i].y, A.Z, nullptr, sm);
     grid_barrier(bar, bar_target);
+    SSTAMP(3);
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
     for (int i = b; i < A.n_p5; i += NB)
       p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.Z, pcf, [&](int, int64_t, int) { return 0.0; }, A.Y, sm, red);
     grid_barrier(bar, bar_target);
+    SSTAMP(4);
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
     {
       double loc = 0.0;
@@ -506,6 +515,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       if (threadIdx.x == 0) A.partB[b] = loc;
     }
     grid_barrier(bar, bar_target);
+    SSTAMP(5);
     const double rho0 = sum_partials(A.partB, NB, red);
     if (b == 0 && threadIdx.x == 0) A.hist[hoff] = 1.0;
     int status = 0;  // 0 running, 1 converged, 2 failed
@@ -591,17 +601,27 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       break;
     }
     hoff += it + 1;
+    SSTAMP(6);
     // ---- E1 v = B^T lambda ; w, -Phi^T v ----
     for (int i = b; i < A.n_p1; i += NB)
       p1_item(D, A.it_p1[i].x, A.it_p1[i].y,
               [&](int, int64_t bb, int) { return D.b_sign[bb] * ldcg(A.lam + D.b_lam[bb]); }, A.XW, sm);
     grid_barrier(bar, bar_target);
+    SSTAMP(7);
     // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
     for (int i = b; i < A.n_pc; i += NB) pc_item(D, A, A.it_pc[i].x, A.it_pc[i].y, A.Z, A.XW, sm);
     grid_barrier(bar, bar_target);
+    SSTAMP(8);
     // ---- E3 a_r = X_rr^T (Z_r - [0; w_b]) - Phi N p, a_p = N p ----
-    for (int i = b; i < A.n_bw; i += NB) bw_item(D, A.it_bw[i].x, A.it_bw[i].y, A.Z, A.XW, pcf, A.a_loc, A.G.nloc, sm);
+    // insulator coefficients feed no later step (no mass term): recover them only at the last step
+    {
+      const bool last = (step == A.nsteps - 1);
+      const int nbw = last ? A.n_bw : A.n_bwc;
+      const int2* itb = last ? A.it_bw : A.it_bwc;
+      for (int i = b; i < nbw; i += NB) bw_item(D, itb[i].x, itb[i].y, A.Z, A.XW, pcf, A.a_loc, A.G.nloc, sm);
+    }
     grid_barrier(bar, bar_target);
+    SSTAMP(9);
   }
   if (b == 0 && threadIdx.x == 0) {
     A.st->done = 1;
