@@ -243,11 +243,11 @@ def main():
             if i2["prof_launches"] > 0:
                 bpl = i2["prof_bytes_per_launch"]
                 if kid == 7:
-                    # persistent stepper (one launch = n_t steps): per step it*(B_F+B_M) for the PCG,
-                    # + B_M (z0) + B_F (p0/d and recovery GEMVs) + the full-factor rhs/recovery bytes
+                    # persistent stepper (one launch = n_t steps): per step it*(B_F+B_M) for the PCG
+                    # + bytes_step_fixed (conductor forward/backward, p0/d/recovery GEMVs, z0)
                     it, _, _ = s.history()
-                    bpl = float(sum(k * (i2["bytes_fapply"] + i2["bytes_precond"]) + i2["bytes_precond"] +
-                                    i2["bytes_fapply"] + i2["bytes_step_fixed"] for k in it))
+                    bpl = float(sum(k * (i2["bytes_fapply"] + i2["bytes_precond"]) + i2["bytes_step_fixed"]
+                                    for k in it))
                 shares[KERNELS[kid]] = {"ms_per_pass": i2["prof_ms"], "launches": i2["prof_launches"],
                                         "us_per_launch": 1000 * i2["prof_ms"] / i2["prof_launches"],
                                         "bytes_per_launch": bpl}

@@ -88,7 +88,8 @@ typedef struct tcg_info {
   int64_t kernel_launches; /* kernels launched by this handle so far (cumulative)         */
   double bytes_fapply;  /* algorithmic HBM bytes of one F-apply (all patches + coarse)    */
   double bytes_precond; /* algorithmic HBM bytes of one preconditioner apply             */
-  double bytes_step_fixed; /* algorithmic HBM bytes of one step outside the PCG loop     */
+  double bytes_step_fixed; /* algorithmic HBM bytes of one step outside the PCG iterations
+                              (conductor forward/backward solves, p0 / dual rhs / recovery, z0) */
   double flops_factor;  /* local + coarse factorisation flops                            */
   double ms_plan, ms_assembly, ms_factor, ms_coarse, ms_steps; /* device-event timings     */
   double ms_pcg_last_step;

@@ -1117,17 +1117,20 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
     out->np_min = std::min<int64_t>(out->np_min, q.np);
     out->np_max = std::max<int64_t>(out->np_max, q.np);
     out->n_primal_local_total += q.np;
-    // algorithmic bytes: packed L_bb read twice, L_pb read twice per F-apply
+    // algorithmic bytes: per F-apply [X_bb; Phi_b^T] read twice (P1, P5);
+    // per preconditioner apply packed S_bb read once
     bf += 8.0 * q.nb * (q.nb + 1) + 16.0 * q.nb * q.np;
     bm += 4.0 * q.nb * (q.nb + 1);
-    double nrp = (double)nr;
-    bs += (p.sigma[s] > 0 ? 8.0 : 4.0) * nrp * (nrp + 1) + 8.0 * nrp * q.np;  // full passes per step
+    const double nrp = (double)nr;
+    // per step outside PCG: conductors read [X_rr; Phi^T] twice (R2 forward, E3 backward)
+    if (p.sigma[s] > 0) bs += 2.0 * 8.0 * (nrp * (nrp + 1) / 2 + nrp * q.np);
     fl += nrp * nrp * nrp / 3.0 + 2.0 * nrp * nrp * q.np + 2.0 * nrp * q.np * q.np;
   }
   const double nc = (double)p.nc;
   bf += 8.0 * nc * (nc + 1) + 40.0 * p.m;
   bm += 40.0 * p.m;
-  bs += 2.0 * 8.0 * nc * (nc + 1);
+  // + the F-apply-like work of R3/R4/E1/E2 and the preconditioner apply of R5
+  bs += bf + bm;
   fl += nc * nc * nc / 3.0;
   out->bytes_fapply = bf;
   out->bytes_precond = bm;
