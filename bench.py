@@ -257,11 +257,20 @@ def main():
         if best is not None:
             b = shares[KERNELS[best]]
             achieved = b["bytes_per_launch"] / (b["us_per_launch"] * 1e-6) / 1e9
+            traffic = None
+            try:  # DRAM bytes of this kernel from the committed ncu --set full capture (profiles/)
+                with open(os.path.join(ROOT, "profiles", "round1_ncu_k_steps.json")) as f:
+                    nc = json.load(f).get(prob.name)
+                if nc and KERNELS[best] == nc["kernel"]:
+                    traffic = nc["dram_bytes_read"] + nc["dram_bytes_write"]
+            except Exception:
+                traffic = None
             roof = {"kernel": KERNELS[best], "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
-                    "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                    "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                     "share_of_pass": b["ms_per_pass"] / (max_ms / args.steps),
-                    "note": "algorithmic bytes per launch / event-timed launch duration; working set is "
-                            "L2-resident for cfg2 (effective, not HBM, bandwidth)"}
+                    "note": "achieved = algorithmic bytes per launch (one launch = all n_t steps) / event-timed "
+                            "launch duration; traffic = ncu DRAM bytes of that launch (profiles/round1_ncu_k_steps.json); "
+                            "cfg1/cfg2 are L2-resident (effective bandwidth, latency/barrier bound)"}
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
