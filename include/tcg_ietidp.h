@@ -102,11 +102,18 @@ typedef struct tcg_info {
 } tcg_info;
 
 /* Create a handle. device: CUDA ordinal used by setup; rank/world: this process's place
- * in the job (world=1 for one GPU); nccl_id: 128-byte ncclUniqueId when world > 1
- * (NULL iff world == 1); cuda_stream: cudaStream_t to use, or NULL for an owned stream.
- * No CUDA call is made before tcg_setup. */
+ * in the job (world=1 for one GPU, world <= 8); nccl_id: 128-byte ncclUniqueId when world > 1
+ * (NULL iff world == 1), used only to bootstrap (CUDA IPC handles of every rank's buffers are
+ * all-gathered; the solve itself reads/writes peer memory over NVLink inside one persistent
+ * kernel per tcg_step); cuda_stream: cudaStream_t to use, or NULL for an owned stream.
+ * No CUDA call is made before tcg_setup. setup/refactor/step/get_coefficients are collective. */
 tcg_status tcg_create(tcg_handle* out, int device, int rank, int world,
                       const unsigned char* nccl_id, void* cuda_stream);
+
+/* Testing/emulation: shard the solve over `vranks` virtual ranks that all live on this
+ * process's GPU (separate allocations, one cooperative grid, the same peer-table dataflow and
+ * two-level barrier as a multi-GPU job). Requires world == 1; call before tcg_plan. */
+tcg_status tcg_set_virtual_ranks(tcg_handle h, int vranks);
 
 /* Uniform box grid of npatch[0] x npatch[1] x npatch[2] patches on [lo,hi], spline degree
  * p >= 1 and elems[d] >= 1 elements per patch per direction. */
@@ -165,9 +172,9 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out);
  * returns the device time in *ms. Requires setup. */
 tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms);
 
-/* Time every launch of one solver kernel with CUDA events on the library stream during
- * subsequent tcg_step calls (1 fwd_ls, 2 bwd_ls, 3 coarse_solve, 4 precond, 5 fwd_full,
- * 6 bwd_full; 0 = off). Results in tcg_info.prof_*. Resets the accumulators. */
+/* Time every launch of the persistent stepper kernel (kernel_id 7; 0 = off) with CUDA events
+ * on the library stream during subsequent tcg_step calls. Results in tcg_info.prof_*.
+ * Resets the accumulators. */
 tcg_status tcg_set_profile(tcg_handle h, int kernel_id);
 
 const char* tcg_last_error(tcg_handle h);

@@ -22,7 +22,8 @@ PLAN_EDGE_CLASS, PLAN_EDGE_REGION, PLAN_TREE, PLAN_PART, PLAN_PATCH_COUNTS, PLAN
 
 EXPORTS = ["tcg_create", "tcg_set_patches", "tcg_set_materials", "tcg_set_source", "tcg_set_time", "tcg_set_solver",
            "tcg_plan", "tcg_get_plan", "tcg_setup", "tcg_refactor", "tcg_step", "tcg_get_coefficients", "tcg_get_history",
-           "tcg_get_info", "tcg_bench_fapply", "tcg_set_profile", "tcg_last_error", "tcg_destroy"]
+           "tcg_get_info", "tcg_bench_fapply", "tcg_set_profile", "tcg_set_virtual_ranks", "tcg_last_error",
+           "tcg_destroy"]
 
 
 class TcgInfo(C.Structure):
@@ -73,6 +74,7 @@ def lib():
     L.tcg_get_info.argtypes = [vp, C.POINTER(TcgInfo)]
     L.tcg_bench_fapply.argtypes = [vp, C.c_int, dp]
     L.tcg_set_profile.argtypes = [vp, C.c_int]
+    L.tcg_set_virtual_ranks.argtypes = [vp, C.c_int]
     L.tcg_last_error.argtypes = [vp]
     L.tcg_last_error.restype = C.c_char_p
     L.tcg_destroy.argtypes = [vp]
@@ -170,6 +172,9 @@ class Solver:
         hist = np.zeros(max(hl, 1))
         self._ck(self.L.tcg_get_history(self.h, None, None, ns, _dptr(hist), hl))
         return it, fr, hist[:hl]
+
+    def set_virtual_ranks(self, n):
+        self._ck(self.L.tcg_set_virtual_ranks(self.h, int(n)))
 
     def set_profile(self, kernel_id):
         self._ck(self.L.tcg_set_profile(self.h, int(kernel_id)))

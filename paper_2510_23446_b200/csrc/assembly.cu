@@ -237,11 +237,14 @@ __device__ __forceinline__ int find_patch(const int64_t* start, int P, int64_t x
   return lo;
 }
 
-// One CTA per 64x64 tile of the tile-packed lower augmented matrices [i|b|p] of all patches.
-__global__ void __launch_bounds__(256) k_assemble(DevPlan D, Tables1D tb, Geom G, double inv_dt) {
+// One CTA per 64x64 tile of the tile-packed lower augmented matrices [i|b|p] of the
+// launching rank's patches (plist, tile prefix tstart over plist).
+__global__ void __launch_bounds__(256) k_assemble(DevPlan D, Tables1D tb, Geom G, double inv_dt, const int* plist,
+                                                  const int64_t* tstart, int nlist) {
   const int64_t tile = blockIdx.x;
-  const int s = find_patch(D.tile_start, D.npatch, tile);
-  const int64_t tl = tile - D.tile_start[s];
+  const int li = find_patch(tstart, nlist, tile);
+  const int s = plist[li];
+  const int64_t tl = tile - tstart[li];
   int I = (int)((sqrt(8.0 * (double)tl + 1.0) - 1.0) * 0.5);
   while ((int64_t)I * (I + 1) / 2 > tl) --I;
   while ((int64_t)(I + 1) * (I + 2) / 2 <= tl) ++I;
@@ -290,7 +293,7 @@ __global__ void k_rho_weights(DevPlan D, int scaling) {
     int s = side == 0 ? D.lam_patch_p[k] : D.lam_patch_m[k];
     int pos = D.Ti[s] * TS + (side == 0 ? D.lam_pos_p[k] : D.lam_pos_m[k]);
     int Itile = pos / TS, rr = pos % TS;
-    rho[side] = D.A[D.a_off[s] + tri_off(Itile, Itile) + rr * TS + rr];
+    rho[side] = D.Ar[D.owner[s]][D.a_off[s] + tri_off(Itile, Itile) + rr * TS + rr];
   }
   D.wplus[k] = rho[1] / (rho[0] + rho[1]);
   D.wminus[k] = rho[0] / (rho[0] + rho[1]);
@@ -327,9 +330,9 @@ __device__ double load_entry(const Tables1D& tb, const Geom& G, int kind, int pi
   return sB(0, i[0]) * sB(1, i[1]) * oD(2, i[2]);
 }
 
-// One CTA per patch: JS[vec_off[s] + pos] for every aug position.
-__global__ void k_load_vector(DevPlan D, Tables1D tb, Geom G, int kind, double* JS) {
-  const int s = blockIdx.x;
+// One CTA per owned patch: JS[vec_off[s] + pos] for every aug position.
+__global__ void k_load_vector(DevPlan D, Tables1D tb, Geom G, int kind, double* JS, const int* plist) {
+  const int s = plist[blockIdx.x];
   int pidx[3] = {s % G.P[0], (s / G.P[0]) % G.P[1], s / (G.P[0] * G.P[1])};
   const int* aug = D.aug + D.aug_off[s];
   const int R = D.T[s] * TS;

@@ -1,8 +1,17 @@
 // capi.cu — the C ABI (include/tcg_ietidp.h): handle state machine, device memory,
-// setup orchestration (assembly -> batched Cholesky -> coarse) and the implicit-Euler step
-// (rhs -> PCG on lambda -> recovery). All arithmetic of the method runs in the kernels of
-// assembly.cu / chol.cu / solve.cu, compiled into this translation unit.
+// setup orchestration (assembly -> batched Cholesky -> inverse factors -> coarse) and the
+// implicit-Euler stepping (one persistent cooperative launch, pcg.cu). All arithmetic of the
+// method runs in the kernels of assembly.cu / chol.cu / pcg.cu, compiled into this TU.
+//
+// Sharding: patches are owned by ranks (contiguous x-slabs, plan.cpp). A rank
+// holds the factors of its patches and the global-layout vectors it owns entries of; values
+// owned elsewhere are read through per-rank pointer tables: peer device memory mapped with
+// CUDA IPC on a multi-GPU job (one process per GPU, NCCL only to bootstrap), or other
+// allocations of the same device for "virtual ranks" (several ranks emulated in one
+// cooperative grid on one GPU; tcg_set_virtual_ranks) which exercise the identical sharded
+// dataflow where only one GPU is available.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <chrono>
@@ -23,8 +32,75 @@
 
 using namespace tcg;
 
+// ---- NCCL, loaded at run time (only for world > 1) ---------------------------------------
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclInt8 = 0, ncclChar = 0, ncclFloat64 = 8 };
+enum { ncclSum = 0 };
+struct NcclApi {
+  void* lib = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (lib) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (!lib) lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (lib) break;
+    }
+    if (!lib) {
+      err = "libnccl.so.2 not found";
+      return false;
+    }
+    commInitRank = (decltype(commInitRank))dlsym(lib, "ncclCommInitRank");
+    allGather = (decltype(allGather))dlsym(lib, "ncclAllGather");
+    allReduce = (decltype(allReduce))dlsym(lib, "ncclAllReduce");
+    commDestroy = (decltype(commDestroy))dlsym(lib, "ncclCommDestroy");
+    getErrorString = (decltype(getErrorString))dlsym(lib, "ncclGetErrorString");
+    if (!commInitRank || !allGather || !allReduce || !commDestroy) {
+      err = "libnccl.so.2 lacks required symbols";
+      return false;
+    }
+    return true;
+  }
+};
+NcclApi g_nccl;
+}  // namespace
+
+// One rank's device data (this process's rank on a multi-GPU job, or one virtual rank).
+struct RankDev {
+  int r = 0;
+  std::vector<int> plist;  // owned patches
+  int* d_plist = nullptr;
+  int64_t* d_tstart = nullptr;
+  int64_t ntiles = 0;
+  double *A = nullptr, *Dinv = nullptr, *Sbb = nullptr, *xscr = nullptr;
+  CholDesc* d_desc = nullptr;
+  int ndesc = 0, maxT = 0, maxTr = 0, maxTb = 0;
+  // global-layout vectors (entries of owned patches / lambda chunks valid)
+  double *F = nullptr, *Z = nullptr, *XJ = nullptr, *JS = nullptr, *XW = nullptr, *Y = nullptr, *PW = nullptr;
+  double *a_loc = nullptr, *lam = nullptr, *r0 = nullptr, *r1 = nullptr, *pk0 = nullptr, *pk1 = nullptr, *q = nullptr;
+  double *Ppart = nullptr, *Pc = nullptr, *partials = nullptr, *hist = nullptr;
+  int* iters = nullptr;
+  BarMem* bar = nullptr;
+  PcgState* st = nullptr;
+  DevError* derr = nullptr;
+  // replicated coarse problem (computed by the first local rank, aliased by other local ranks)
+  double *C = nullptr, *Cinv = nullptr, *CX = nullptr, *Sinv = nullptr;
+  DevPlan D{};  // DevPlan with me / A / Dinv / Sbb of this rank
+};
+
 struct tcg_ctx {
   int device = 0, rank = 0, world = 1;
+  int vranks = 1;  // virtual ranks emulated in this process (world must be 1)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   Plan plan;
@@ -37,88 +113,78 @@ struct tcg_ctx {
   int max_iter = 5000;
   int scaling = TCG_SCALING_RHO;
   int tree_order = 0;
-  int stable_mask = 0;  // bit0: local diag substitution, bit1: coarse, bit2: TRSM substitution (env TCG_STABLE)
+  int stable_mask = 0;  // bit2: TRSM by substitution (env TCG_STABLE)
+  unsigned char nccl_id[128];
+  ncclComm_t comm = nullptr;
   std::string err;
 
   // device state
   std::vector<void*> allocs;
+  std::vector<void*> ipc_opened;
   int64_t device_bytes = 0;
-  DevPlan D{};
+  int nranks = 1;  // ranks of the job: world (real) or vranks (virtual)
+  std::vector<RankDev> rd;  // local ranks
+  DevPlan D{};              // global arrays + per-rank tables (me/A/Dinv/Sbb unset)
   Geom G{};
   Tables1D tb{};
-  CholDesc* d_desc = nullptr;
   CholDesc* d_cdesc = nullptr;
-  int maxT = 0, maxTr = 0, maxTb = 0, maxTbp = 0;
-  int64_t max_ls_tiles = 0;
-  std::vector<std::vector<int>> colour_lists;
+  InvDesc* d_cinv = nullptr;
   int* d_colour = nullptr;
   std::vector<int64_t> colour_off;
-  double *X1 = nullptr, *XW = nullptr, *XJ = nullptr, *JS = nullptr, *PW = nullptr;
-  double *lam = nullptr, *r = nullptr, *z = nullptr, *pk = nullptr, *q = nullptr;
-  double *Pc = nullptr, *partial = nullptr, *hist = nullptr, *a_loc = nullptr, *glued = nullptr;
+  int* d_crow_owner = nullptr;
   int64_t* d_glued_src = nullptr;
-  PcgState* st = nullptr;
+  double* glued = nullptr;
+  double* a_all = nullptr;  // gathered local coefficients (readout)
+  int64_t* d_aloc_src = nullptr;
   PcgState* h_st = nullptr;  // pinned
-  DevError* derr = nullptr;
-  double* dbgA = nullptr;   // copy of the assembled augmented matrices (TCG_DEBUG_KEEP=1)
-  double* dbgC = nullptr;   // copy of the assembled coarse matrix
-  std::vector<int64_t> h_a_off, h_vec_off;
-  std::vector<int> h_T;
-  int64_t a_total = 0;
-  int64_t total_tiles = 0;
-  int64_t nb_total = 0;
-  // chain-free PCG
-  double *CX = nullptr, *r2 = nullptr, *pk2 = nullptr, *Yv = nullptr, *Yc = nullptr, *partA = nullptr, *partB = nullptr;
-  InvDesc* d_inv = nullptr;
-  InvDesc* d_cinv = nullptr;
-  int maxTp = 0;
-  int n_p1 = 0, n_p5 = 0, n_sy = 0, n_pc = 0, n_fw = 0, n_fw_all = 0, n_bw = 0;
-  int2* d_it_p1 = nullptr;
-  int2* d_it_p5 = nullptr;
-  int2* d_it_sy = nullptr;
-  int2* d_it_pc = nullptr;
-  int2* d_it_fw = nullptr;
-  int2* d_it_fw_all = nullptr;
-  int2* d_it_bw = nullptr;
-  int2* d_it_bwc = nullptr;
-  int2* d_it_rhs = nullptr;
-  int n_bwc = 0, n_rhs = 0;
-  double* xscratch = nullptr;      // per-patch scratch row for the in-place factor inversion
-  int64_t* d_scr_off = nullptr;
-  double* F = nullptr;             // conductor rhs (aug order)
-  int* d_iters = nullptr;          // per-step PCG iterations (device)
-  int64_t hist_cap = 0, hist_len = 0;
-  double *Sinv = nullptr, *Ppart = nullptr;
+  int maxT = 0, maxTr = 0, maxTb = 0, maxTp = 0, Tc = 0;
+  int64_t nb_total = 0, vec_total = 0;
+  // item lists of all ranks (concatenated, per-rank offsets)
+  int2 *d_it_p1 = nullptr, *d_it_p5 = nullptr, *d_it_sy = nullptr, *d_it_pc = nullptr, *d_it_fw = nullptr,
+       *d_it_fwa = nullptr, *d_it_bw = nullptr, *d_it_bwc = nullptr, *d_it_rhs = nullptr;
+  int *d_off_p1 = nullptr, *d_off_p5 = nullptr, *d_off_sy = nullptr, *d_off_pc = nullptr, *d_off_fw = nullptr,
+      *d_off_fwa = nullptr, *d_off_bw = nullptr, *d_off_bwc = nullptr, *d_off_rhs = nullptr;
+  std::vector<int> off_p1, off_p5, off_pc, off_fwa;
   int coarse_ch = 1, coarse_maxch = 1;
-  size_t smem_pcg = 0;
-  int pcg_blocks = 0;
-  unsigned long long* tstamp = nullptr;  // TCG_PHASE_TIMING=1: per-phase timestamps of the persistent PCG
-  size_t smem_tables = 0;
-  int64_t vec_total = 0;
+  size_t smem_pcg = 0, smem_tables = 0;
+  int nbr = 0;  // persistent blocks per rank
+  int64_t lam_chunk = 1;
+  unsigned int bar_round = 0;  // barrier rounds completed (monotone counters, never reset)
+  std::vector<std::vector<void*>> peer_bufs;  // [rank][buffer] device pointers (own or peer)
+  double* sync_tok = nullptr;
+  unsigned long long* tstamp = nullptr;
+  double* dbgA = nullptr;
+  double* dbgC = nullptr;
+  std::vector<int64_t> h_a_off, h_vec_off, h_sbb_off;
+  std::vector<int> h_T, h_owner;
 
   // results
-  int64_t steps_done = 0, total_iters = 0;
+  int64_t steps_done = 0, total_iters = 0, hist_len = 0;
   std::vector<int> iters;
   std::vector<double> final_rel, hist_all;
-  int64_t launches_last = 0;
-  int64_t nlaunch = 0;  // kernels launched by this handle (cumulative)
-  int64_t h2d_bytes = 0, d2h_bytes = 0;  // host<->device bytes moved by this handle (cumulative)
-  // optional per-kernel timing (tcg_set_profile): event pairs around each launch of one kernel
+  int64_t nlaunch = 0;
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
   int prof_id = 0;
-  std::vector<cudaEvent_t> prof_ev;   // 2 per pair
-  std::vector<int> prof_tag;          // PCG iteration index of the pair (-1 outside the loop)
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<int> prof_tag;
   size_t prof_used = 0;
   double prof_ms = 0;
   int64_t prof_count = 0;
-  double ms_plan = 0, ms_assembly = 0, ms_factor = 0, ms_coarse = 0, ms_steps = 0, ms_pcg_last = 0;
+  double ms_plan = 0, ms_assembly = 0, ms_factor = 0, ms_coarse = 0, ms_steps = 0;
 
   ~tcg_ctx() { release(); }
   void release() {
     if (!allocs.empty() || stream) cudaSetDevice(device);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+    ipc_opened.clear();
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
     if (h_st) cudaFreeHost(h_st);
     h_st = nullptr;
+    for (auto e : prof_ev) cudaEventDestroy(e);
+    prof_ev.clear();
+    if (comm && g_nccl.commDestroy) g_nccl.commDestroy(comm);
+    comm = nullptr;
     if (own_stream && stream) cudaStreamDestroy(stream);
     stream = nullptr;
   }
@@ -151,6 +217,12 @@ tcg_status fail(tcg_ctx* h, tcg_status s, const std::string& msg) {
     }                                                                                             \
   } while (0)
 
+#define TRY(x)                   \
+  do {                           \
+    tcg_status s_ = (x);         \
+    if (s_ != TCG_OK) return s_; \
+  } while (0)
+
 template <class T>
 tcg_status dalloc(tcg_ctx* h, T** out, size_t n) {
   size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
@@ -160,6 +232,14 @@ tcg_status dalloc(tcg_ctx* h, T** out, size_t n) {
   h->allocs.push_back(p);
   h->device_bytes += (int64_t)bytes;
   *out = static_cast<T*>(p);
+  return TCG_OK;
+}
+
+template <class T>
+tcg_status dzero(tcg_ctx* h, T** out, size_t n) {
+  TRY(dalloc(h, out, n));
+  cudaError_t e = cudaMemsetAsync(*out, 0, std::max<size_t>(n, 1) * sizeof(T), h->stream);
+  if (e != cudaSuccess) return fail(h, TCG_ECUDA, std::string("memset: ") + cudaGetErrorString(e));
   return TCG_OK;
 }
 
@@ -175,12 +255,6 @@ tcg_status dupload(tcg_ctx* h, T** out, const std::vector<T>& v) {
   return TCG_OK;
 }
 
-#define TRY(x)                        \
-  do {                                \
-    tcg_status s_ = (x);              \
-    if (s_ != TCG_OK) return s_;      \
-  } while (0)
-
 double elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0;
   cudaEventElapsedTime(&ms, a, b);
@@ -193,17 +267,29 @@ tcg_status set_smem(tcg_ctx* h, const void* fn, size_t bytes) {
   return TCG_OK;
 }
 
+// Cross-process barrier on the stream (multi-GPU only): a 1-element NCCL allreduce.
+tcg_status sync_ranks(tcg_ctx* h) {
+  if (h->world <= 1) return TCG_OK;
+  if (!h->sync_tok) TRY(dzero(h, &h->sync_tok, 1));
+  ncclResult_t r = g_nccl.allReduce(h->sync_tok, h->sync_tok, 1, ncclFloat64, ncclSum, h->comm, h->stream);
+  if (r != 0) return fail(h, TCG_ENCCL, std::string("ncclAllReduce: ") + (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?"));
+  CK(cudaStreamSynchronize(h->stream));
+  return TCG_OK;
+}
+
 }  // namespace
 
 // =========================================================================================
-// setup
+// plan
 // =========================================================================================
 static tcg_status do_plan(tcg_ctx* h) {
   if (h->planned) return TCG_OK;
-  if (!h->have_patches || !h->have_materials || !h->have_time) return fail(h, TCG_ESTATE, "set_patches, set_materials and set_time are required");
+  if (!h->have_patches || !h->have_materials || !h->have_time)
+    return fail(h, TCG_ESTATE, "set_patches, set_materials and set_time are required");
   auto t0 = std::chrono::steady_clock::now();
+  h->nranks = std::max(h->world, h->vranks);
   h->plan.tree_order = h->tree_order;
-  h->plan.world = h->world;
+  h->plan.world = h->nranks;
   std::string e = h->plan.build();
   if (!e.empty()) return fail(h, TCG_EINVAL, "plan: " + e);
   h->planned = true;
@@ -211,8 +297,11 @@ static tcg_status do_plan(tcg_ctx* h) {
   return TCG_OK;
 }
 
+// =========================================================================================
+// numeric setup (assembly, batched Cholesky, inverse factors, coarse)
+// =========================================================================================
 static tcg_status run_cholesky(tcg_ctx* h, const CholDesc* d_desc, int nmat, int maxT, int maxTf, int maxTb,
-                               double* base, double* dinv, double* sbb, int coarse) {
+                               double* base, double* dinv, double* sbb, DevError* derr, int coarse) {
   const int subst = (h->stable_mask & 4) ? 1 : 0;
   for (int k = 0; k < maxTf; ++k) {
     if (sbb && maxTb > 0) {
@@ -221,7 +310,7 @@ static tcg_status run_cholesky(tcg_ctx* h, const CholDesc* d_desc, int nmat, int
       ++h->nlaunch;
       CKL();
     }
-    k_potrf<<<nmat, 256, 2 * TS * 65 * sizeof(double), h->stream>>>(d_desc, k, base, dinv, h->derr, coarse);
+    k_potrf<<<nmat, 256, 2 * TS * 65 * sizeof(double), h->stream>>>(d_desc, k, base, dinv, derr, coarse);
     ++h->nlaunch;
     CKL();
     int rows = maxT - k - 1;
@@ -239,112 +328,173 @@ static tcg_status run_cholesky(tcg_ctx* h, const CholDesc* d_desc, int nmat, int
   return TCG_OK;
 }
 
-// Numeric setup (step a + b of the hot path): 1D tables, assembly, rho weights, load,
-// batched local Cholesky (+ S_bb capture), trailing stores, coarse assembly + Cholesky,
-// insulator load precompute. Re-runnable on the same allocations (tcg_refactor).
+static tcg_status check_err(tcg_ctx* h) {
+  CK(cudaStreamSynchronize(h->stream));
+  for (auto& R : h->rd) {
+    DevError herr;
+    CK(cudaMemcpy(&herr, R.derr, sizeof(DevError), cudaMemcpyDeviceToHost));
+    if (herr.flag) {
+      h->broken = true;
+      std::ostringstream o;
+      if (herr.matrix >= 0) o << "local Cholesky: patch " << R.plist[herr.matrix];
+      else o << "coarse Cholesky";
+      o << " pivot " << herr.index << " value " << herr.value;
+      return fail(h, TCG_ENOTSPD, o.str());
+    }
+  }
+  return TCG_OK;
+}
+
 static tcg_status do_numeric(tcg_ctx* h) {
   Plan& pl = h->plan;
-  DevPlan& D = h->D;
-  const int P = D.npatch;
-  const int Tc = D.Tc;
+  const int Tc = h->Tc;
   const double dt = h->T / h->n_steps;
   cudaEvent_t e0, e1, e2, e3;
-  cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3);
-  CK(cudaMemsetAsync(h->derr, 0, sizeof(DevError), h->stream));
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventCreate(&e2);
+  cudaEventCreate(&e3);
   CK(cudaEventRecord(e0, h->stream));
   k_tables1d<<<3, 256, h->smem_tables, h->stream>>>(h->tb, pl.p);
   ++h->nlaunch;
   CKL();
-  k_assemble<<<(unsigned)h->total_tiles, 256, 0, h->stream>>>(D, h->tb, h->G, 1.0 / dt);
-  ++h->nlaunch;
-  CKL();
-  if (pl.m > 0) {
-    k_rho_weights<<<(unsigned)((pl.m + 255) / 256), 256, 0, h->stream>>>(D, h->scaling);
-    ++h->nlaunch;
-    CKL();
+  for (auto& R : h->rd) {
+    CK(cudaMemsetAsync(R.derr, 0, sizeof(DevError), h->stream));
+    if (R.ntiles > 0) {
+      k_assemble<<<(unsigned)R.ntiles, 256, 0, h->stream>>>(R.D, h->tb, h->G, 1.0 / dt, R.d_plist, R.d_tstart,
+                                                           (int)R.plist.size());
+      ++h->nlaunch;
+      CKL();
+    }
+    if (!R.plist.empty()) {
+      k_load_vector<<<(unsigned)R.plist.size(), 256, 0, h->stream>>>(R.D, h->tb, h->G, h->source, R.JS, R.d_plist);
+      ++h->nlaunch;
+      CKL();
+    }
   }
-  if (h->nb_total > 0) {
-    k_btables<<<(unsigned)((h->nb_total + 255) / 256), 256, 0, h->stream>>>(D, h->nb_total);
-    ++h->nlaunch;
+  TRY(sync_ranks(h));  // every rank's W^ assembled (rho weights read both interface sides)
+  for (auto& R : h->rd) {
+    if (pl.m > 0) {
+      k_rho_weights<<<(unsigned)((pl.m + 255) / 256), 256, 0, h->stream>>>(R.D, h->scaling);
+      ++h->nlaunch;
+      CKL();
+    }
+    if (h->nb_total > 0) {
+      k_btables<<<(unsigned)((h->nb_total + 255) / 256), 256, 0, h->stream>>>(R.D, h->nb_total);
+      ++h->nlaunch;
+      CKL();
+    }
+    break;  // wplus/wminus/b tables are global arrays shared by the local ranks of this process
   }
-  k_load_vector<<<P, 256, 0, h->stream>>>(D, h->tb, h->G, h->source, h->JS);
-  ++h->nlaunch;
-  CKL();
   CK(cudaEventRecord(e1, h->stream));
-  if (h->dbgA) CK(cudaMemcpyAsync(h->dbgA, D.A, sizeof(double) * h->a_total, cudaMemcpyDeviceToDevice, h->stream));
-  TRY(run_cholesky(h, h->d_desc, P, h->maxT, h->maxTr, h->maxTb, D.A, D.Dinv, D.Sbb, 0));
-  // coarse scatter reads S^s from the (p,p) blocks (untouched by the inversion below)
-  // in-place inverse of the augmented factor: Xaug = [L_rr^-1 ; W_pr W_rr^-1]
-  for (int I = 0; I < h->maxT; ++I) {
-    dim3 g(std::min(I + 1, h->maxTr), P);
-    k_xinv_row<<<g, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(D, I, h->xscratch, h->d_scr_off);
-    ++h->nlaunch;
-    k_xrow_copy<<<g, 256, 0, h->stream>>>(D, I, h->xscratch, h->d_scr_off);
-    ++h->nlaunch;
-    CKL();
+  TRY(sync_ranks(h));  // rho weights read before any rank overwrites its W^ with the factor
+  if (h->dbgA && h->rd.size() == 1)
+    CK(cudaMemcpyAsync(h->dbgA, h->rd[0].A, sizeof(double) * h->h_a_off.back(), cudaMemcpyDeviceToDevice, h->stream));
+  for (auto& R : h->rd) {
+    if (R.ndesc == 0) continue;
+    TRY(run_cholesky(h, R.d_desc, R.ndesc, R.maxT, R.maxTr, R.maxTb, R.A, R.Dinv, R.Sbb, R.derr, 0));
+    // in-place inverse of the augmented factor: Xaug = [L_rr^-1 ; W_pr W_rr^-1]
+    const int64_t* scr_off = h->D.dinv_off;  // scratch rows share the Dinv layout (Tr tiles)
+    for (int I = 0; I < R.maxT; ++I) {
+      dim3 g(std::min(I + 1, R.maxTr), (unsigned)R.plist.size());
+      k_xinv_row<<<g, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(R.D, I, R.xscr, scr_off, R.d_plist);
+      ++h->nlaunch;
+      k_xrow_copy<<<g, 256, 0, h->stream>>>(R.D, I, R.xscr, scr_off, R.d_plist);
+      ++h->nlaunch;
+      CKL();
+    }
   }
   CK(cudaEventRecord(e2, h->stream));
-  CK(cudaMemsetAsync(D.C, 0, sizeof(double) * (size_t)tri_tiles(Tc) * TSZ, h->stream));
-  if (pl.nc > 0) {
-    for (int c = 0; c < 8; ++c) {
-      int cnt = (int)(h->colour_off[c + 1] - h->colour_off[c]);
-      if (cnt == 0) continue;
-      k_coarse_scatter<<<cnt, 256, 0, h->stream>>>(D, h->d_colour + h->colour_off[c], cnt);
+  TRY(sync_ranks(h));  // S^s of every patch final before the (replicated) coarse assembly
+  {
+    RankDev& R = h->rd[0];  // the coarse problem is computed once per process
+    CK(cudaMemsetAsync(R.C, 0, sizeof(double) * (size_t)tri_tiles(Tc) * TSZ, h->stream));
+    if (pl.nc > 0) {
+      DevPlan Dc = R.D;
+      Dc.C = R.C;
+      for (int c = 0; c < 8; ++c) {
+        int cnt = (int)(h->colour_off[c + 1] - h->colour_off[c]);
+        if (cnt == 0) continue;
+        k_coarse_scatter<<<cnt, 256, 0, h->stream>>>(Dc, h->d_colour + h->colour_off[c], cnt);
+        ++h->nlaunch;
+        CKL();
+      }
+      int npad = Tc * TS - (int)pl.nc;
+      if (npad > 0) {
+        k_coarse_pad<<<(npad + 255) / 256, 256, 0, h->stream>>>(Dc);
+        ++h->nlaunch;
+        CKL();
+      }
+      if (h->dbgC) CK(cudaMemcpyAsync(h->dbgC, R.C, sizeof(double) * tri_tiles(Tc) * TSZ, cudaMemcpyDeviceToDevice, h->stream));
+      TRY(run_cholesky(h, h->d_cdesc, 1, Tc, Tc, 0, R.C, R.Cinv, nullptr, R.derr, 1));
+      for (int I = 0; I < Tc; ++I) {
+        dim3 g(I + 1, 1);
+        k_trinv_row<<<g, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(h->d_cinv, I, R.C, R.CX, R.Cinv);
+        ++h->nlaunch;
+        CKL();
+      }
+      k_sinv<<<dim3(Tc, Tc), 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(R.CX, R.Sinv, Tc);
       ++h->nlaunch;
       CKL();
     }
-    int npad = Tc * TS - (int)pl.nc;
-    if (npad > 0) {
-      k_coarse_pad<<<(npad + 255) / 256, 256, 0, h->stream>>>(D);
-      ++h->nlaunch;
-      CKL();
-    }
-    if (h->dbgC) CK(cudaMemcpyAsync(h->dbgC, D.C, sizeof(double) * tri_tiles(Tc) * TSZ, cudaMemcpyDeviceToDevice, h->stream));
-    TRY(run_cholesky(h, h->d_cdesc, 1, Tc, Tc, 0, D.C, D.Cinv, nullptr, 1));
-    for (int I = 0; I < Tc; ++I) {
-      dim3 g(I + 1, 1);
-      k_trinv_row<<<g, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(h->d_cinv, I, D.C, h->CX, D.Cinv);
-      ++h->nlaunch;
-      CKL();
-    }
-    k_sinv<<<dim3(Tc, Tc), 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(h->CX, h->Sinv, Tc);
-    ++h->nlaunch;
-    CKL();
   }
-  // insulator precompute: XJ = [X_rr j_S,r ; j_S,p - Phi^T j_S,r]
-  ++h->nlaunch;
-  CKL();
-  if (h->n_fw_all > 0) {
-    k_fw<<<h->n_fw_all, NTHR, h->smem_pcg, h->stream>>>(D, h->d_it_fw_all, h->n_fw_all, h->JS, h->XJ);
-    ++h->nlaunch;
-    CKL();
+  // insulator precompute: XJ = [X_rr j_S,r ; j_S,p - Phi^T j_S,r] for owned patches
+  for (auto& R : h->rd) {
+    const int n = h->off_fwa[R.r + 1] - h->off_fwa[R.r];
+    if (n > 0) {
+      k_fw<<<n, NTHR, h->smem_pcg, h->stream>>>(R.D, h->d_it_fwa + h->off_fwa[R.r], n, R.JS, R.XJ);
+      ++h->nlaunch;
+      CKL();
+    }
+    CK(cudaMemsetAsync(R.a_loc, 0, sizeof(double) * (size_t)pl.npatch * pl.nloc, h->stream));
   }
   CK(cudaEventRecord(e3, h->stream));
-  // reset the time-stepping state
-  CK(cudaMemsetAsync(h->a_loc, 0, sizeof(double) * (size_t)P * pl.nloc, h->stream));
-  DevError herr;
-  CK(cudaMemcpyAsync(&herr, h->derr, sizeof(DevError), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
+  TRY(check_err(h));
+  TRY(sync_ranks(h));
   h->ms_assembly = elapsed_ms(e0, e1);
   h->ms_factor = elapsed_ms(e1, e2);
   h->ms_coarse = elapsed_ms(e2, e3);
-  cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2); cudaEventDestroy(e3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  cudaEventDestroy(e3);
   h->steps_done = 0;
   h->hist_len = 0;
   h->total_iters = 0;
   h->iters.clear();
   h->final_rel.clear();
   h->hist_all.clear();
-  if (herr.flag) {
-    h->broken = true;
-    std::ostringstream o;
-    if (herr.matrix >= 0) o << "local Cholesky: patch " << herr.matrix;
-    else o << "coarse Cholesky";
-    o << " pivot " << herr.index << " value " << herr.value;
-    return fail(h, TCG_ENOTSPD, o.str());
-  }
   return TCG_OK;
 }
+
+// =========================================================================================
+// setup: layouts, uploads, per-rank allocations, peer tables
+// =========================================================================================
+struct ItemLists {
+  std::vector<std::vector<std::pair<int, int2>>> per_rank;
+  explicit ItemLists(int nr) : per_rank(nr) {}
+};
+
+static tcg_status upload_items(tcg_ctx* h, ItemLists& L, int2** d_items, int** d_off, std::vector<int>* h_off = nullptr) {
+  auto bycost = [](const std::pair<int, int2>& x, const std::pair<int, int2>& y) {
+    return x.first != y.first ? x.first > y.first
+                              : (x.second.x != y.second.x ? x.second.x < y.second.x : x.second.y < y.second.y);
+  };
+  std::vector<int2> all;
+  std::vector<int> off(1, 0);
+  for (auto& v : L.per_rank) {
+    std::stable_sort(v.begin(), v.end(), bycost);
+    for (auto& e : v) all.push_back(e.second);
+    off.push_back((int)all.size());
+  }
+  while ((int)off.size() < MAXR + 1) off.push_back(off.back());
+  TRY(dupload(h, d_items, all));
+  TRY(dupload(h, d_off, off));
+  if (h_off) *h_off = off;
+  return TCG_OK;
+}
+
+static tcg_status open_peer_tables(tcg_ctx* h, std::vector<std::vector<void*>>& bufs_by_rank);
 
 static tcg_status do_setup(tcg_ctx* h) {
   TRY(do_plan(h));
@@ -359,10 +509,23 @@ static tcg_status do_setup(tcg_ctx* h) {
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream = true;
   }
+  if (h->world > 1) {
+    std::string e;
+    if (!g_nccl.load(e)) return fail(h, TCG_ENCCL, e);
+    ncclUniqueId id;
+    std::memcpy(id.internal, h->nccl_id, 128);
+    ncclResult_t r = g_nccl.commInitRank(&h->comm, h->world, id, h->rank);
+    if (r != 0) return fail(h, TCG_ENCCL, std::string("ncclCommInitRank: ") + (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?"));
+  }
+  {
+    const char* ev = getenv("TCG_STABLE");
+    if (ev) h->stable_mask = atoi(ev);
+  }
   const int P = pl.npatch;
-  const double dt = h->T / h->n_steps;
+  const int NR = h->nranks;
+  if (NR > MAXR) return fail(h, TCG_EINVAL, "more than " + std::to_string(MAXR) + " ranks");
 
-  // ---- geometry / offsets ----
+  // ---- geometry ----
   Geom& G = h->G;
   for (int d = 0; d < 3; ++d) {
     G.P[d] = pl.P[d];
@@ -373,32 +536,31 @@ static tcg_status do_setup(tcg_ctx* h) {
     for (int d = 0; d < 3; ++d) G.cdim[c][d] = pl.comp_dim(c, d);
   G.nloc = pl.nloc;
 
-  std::vector<int> Ti(P), Tb(P), Tp(P), T(P), nb(P), np(P);
-  std::vector<int64_t> a_off(P), dinv_off(P), ls_off(P), sbb_off(P), vec_off(P), aug_off(P), b_off(P + 1), p_off(P + 1),
-      tile_start(P + 1);
+  // ---- per-patch layout (offsets relative to the owning rank's allocations) ----
+  std::vector<int> Ti(P), Tb(P), Tp(P), T(P), nb(P), np(P), owner(P);
+  std::vector<int64_t> a_off(P), dinv_off(P), sbb_off(P), vec_off(P), aug_off(P), b_off(P + 1), p_off(P + 1);
+  std::vector<int64_t> oa(NR, 0), od(NR, 0), os(NR, 0);
   std::vector<int> aug_all, b_lam_all, p_grp_all;
   std::vector<double> b_sign_all;
-  int64_t oa = 0, od = 0, ol = 0, os = 0, ov = 0, og = 0;
-  h->maxT = h->maxTr = h->maxTb = h->maxTbp = 0;
-  h->max_ls_tiles = 0;
-  b_off[0] = p_off[0] = tile_start[0] = 0;
+  int64_t ov = 0, og = 0;
+  b_off[0] = p_off[0] = 0;
+  h->maxT = h->maxTr = h->maxTb = h->maxTp = 0;
   for (int s = 0; s < P; ++s) {
     const PatchPlan& q = pl.pp[s];
+    const int r = pl.rank_of_patch[s];
+    owner[s] = r;
     Ti[s] = q.Ti;
     Tb[s] = q.Tb;
     Tp[s] = q.Tp;
     T[s] = q.Ti + q.Tb + q.Tp;
     nb[s] = q.nb;
     np[s] = q.np;
-    a_off[s] = oa;
-    oa += tri_tiles(T[s]) * TSZ;
-    dinv_off[s] = od;
-    od += (int64_t)(q.Ti + q.Tb) * TSZ;
-    ls_off[s] = ol;
-    int64_t lst = tri_tiles(q.Tb) + (int64_t)q.Tp * q.Tb;
-    ol += lst * TSZ;
-    sbb_off[s] = os;
-    os += tri_tiles(q.Tb) * TSZ;
+    a_off[s] = oa[r];
+    oa[r] += tri_tiles(T[s]) * TSZ;
+    dinv_off[s] = od[r];
+    od[r] += (int64_t)(q.Ti + q.Tb) * TSZ;
+    sbb_off[s] = os[r];
+    os[r] += tri_tiles(q.Tb) * TSZ;
     vec_off[s] = ov;
     ov += (int64_t)T[s] * TS;
     aug_off[s] = og;
@@ -411,17 +573,17 @@ static tcg_status do_setup(tcg_ctx* h) {
       b_sign_all.push_back((double)q.b_sign[t]);
     }
     for (int t = 0; t < q.np; ++t) p_grp_all.push_back(q.p_grp[t]);
-    tile_start[s + 1] = tile_start[s] + tri_tiles(T[s]);
     h->maxT = std::max(h->maxT, T[s]);
     h->maxTr = std::max(h->maxTr, q.Ti + q.Tb);
     h->maxTb = std::max(h->maxTb, q.Tb);
-    h->maxTbp = std::max(h->maxTbp, q.Tb + q.Tp);
-    h->max_ls_tiles = std::max(h->max_ls_tiles, lst);
+    h->maxTp = std::max(h->maxTp, q.Tp);
   }
   h->vec_total = ov;
-  h->D.maxT = h->maxT;
-  h->D.maxTbp = h->maxTbp;
-  // multipliers
+  h->h_a_off = a_off;
+  h->h_vec_off = vec_off;
+  h->h_sbb_off = sbb_off;
+  h->h_T = T;
+  h->h_owner = owner;
   std::vector<int> lpp(pl.m), lpm(pl.m), lsp(pl.m), lsm(pl.m);
   std::vector<int64_t> lip(pl.m), lim(pl.m);
   for (int64_t k = 0; k < pl.m; ++k) {
@@ -433,64 +595,62 @@ static tcg_status do_setup(tcg_ctx* h) {
     lim[k] = vec_off[lpm[k]] + (int64_t)Ti[lpm[k]] * TS + lsm[k];
   }
   std::vector<int64_t> cidx(pl.coarse_patch.size());
+  std::vector<int> cpat(pl.coarse_patch.size());
   for (size_t e = 0; e < cidx.size(); ++e) {
     int s = pl.coarse_patch[e];
+    cpat[e] = s;
     cidx[e] = vec_off[s] + (int64_t)(Ti[s] + Tb[s]) * TS + pl.coarse_pos[e];
   }
   const int Tc = (int)((pl.nc + TS - 1) / TS);
+  h->Tc = Tc;
 
-  // ---- uploads ----
+  // ---- global uploads (shared by the local ranks) ----
   DevPlan& D = h->D;
   D.npatch = P;
-  {
-    const char* ev = getenv("TCG_STABLE");
-    h->stable_mask = ev ? atoi(ev) : h->stable_mask;
-  }
-  D.subst_local = h->stable_mask & 1;
-  D.subst_coarse = (h->stable_mask >> 1) & 1;
+  D.nranks = NR;
   D.m = pl.m;
   D.nc = pl.nc;
   D.Tc = Tc;
-  int *dTi, *dTb, *dTp, *dT, *dnb, *dnp, *daug, *dbl, *dpg, *dlpp, *dlpm, *dlsp, *dlsm, *dcp;
-  int64_t *dao, *ddo, *dlo, *dso, *dvo, *dgo, *dbo, *dpo, *dts, *dlip, *dlim, *dci;
-  double *dbs, *dsig, *dnu;
-  TRY(dupload(h, &dTi, Ti));
-  TRY(dupload(h, &dTb, Tb));
-  TRY(dupload(h, &dTp, Tp));
-  TRY(dupload(h, &dT, T));
-  TRY(dupload(h, &dnb, nb));
-  TRY(dupload(h, &dnp, np));
-  TRY(dupload(h, &dao, a_off));
-  TRY(dupload(h, &ddo, dinv_off));
-  TRY(dupload(h, &dlo, ls_off));
-  TRY(dupload(h, &dso, sbb_off));
-  TRY(dupload(h, &dvo, vec_off));
-  TRY(dupload(h, &dgo, aug_off));
-  TRY(dupload(h, &daug, aug_all));
-  TRY(dupload(h, &dbo, b_off));
-  TRY(dupload(h, &dbl, b_lam_all));
-  TRY(dupload(h, &dbs, b_sign_all));
-  TRY(dupload(h, &dpo, p_off));
-  TRY(dupload(h, &dpg, p_grp_all));
-  TRY(dupload(h, &dts, tile_start));
-  TRY(dupload(h, &dsig, pl.sigma));
-  TRY(dupload(h, &dnu, pl.nu));
-  TRY(dupload(h, &dlpp, lpp));
-  TRY(dupload(h, &dlpm, lpm));
-  TRY(dupload(h, &dlsp, lsp));
-  TRY(dupload(h, &dlsm, lsm));
-  TRY(dupload(h, &dlip, lip));
-  TRY(dupload(h, &dlim, lim));
-  TRY(dupload(h, &dcp, pl.coarse_ptr));
-  TRY(dupload(h, &dci, cidx));
-  D.Ti = dTi; D.Tb = dTb; D.Tp = dTp; D.T = dT; D.nb = dnb; D.np = dnp;
-  D.a_off = dao; D.dinv_off = ddo; D.ls_off = dlo; D.sbb_off = dso; D.vec_off = dvo; D.aug_off = dgo;
-  D.aug = daug; D.b_off = dbo; D.b_lam = dbl; D.b_sign = dbs; D.p_off = dpo; D.p_grp = dpg;
-  D.tile_start = dts; D.sigma = dsig; D.nu = dnu;
-  D.lam_patch_p = dlpp; D.lam_patch_m = dlpm; D.lam_pos_p = dlsp; D.lam_pos_m = dlsm;
-  D.lam_idx_p = dlip; D.lam_idx_m = dlim; D.coarse_ptr = dcp; D.coarse_idx = dci;
+  D.maxT = h->maxT;
   {
-    // partner index of every b position (the other endpoint of its multiplier)
+    int *dTi, *dTb, *dTp, *dT, *dnb, *dnp, *daug, *dbl, *dpg, *dlpp, *dlpm, *dlsp, *dlsm, *dcp, *dcpat, *down;
+    int64_t *dao, *ddo, *dso, *dvo, *dgo, *dbo, *dpo, *dlip, *dlim, *dci;
+    double *dbs, *dsig, *dnu;
+    TRY(dupload(h, &dTi, Ti));
+    TRY(dupload(h, &dTb, Tb));
+    TRY(dupload(h, &dTp, Tp));
+    TRY(dupload(h, &dT, T));
+    TRY(dupload(h, &dnb, nb));
+    TRY(dupload(h, &dnp, np));
+    TRY(dupload(h, &down, owner));
+    TRY(dupload(h, &dao, a_off));
+    TRY(dupload(h, &ddo, dinv_off));
+    TRY(dupload(h, &dso, sbb_off));
+    TRY(dupload(h, &dvo, vec_off));
+    TRY(dupload(h, &dgo, aug_off));
+    TRY(dupload(h, &daug, aug_all));
+    TRY(dupload(h, &dbo, b_off));
+    TRY(dupload(h, &dbl, b_lam_all));
+    TRY(dupload(h, &dbs, b_sign_all));
+    TRY(dupload(h, &dpo, p_off));
+    TRY(dupload(h, &dpg, p_grp_all));
+    TRY(dupload(h, &dsig, pl.sigma));
+    TRY(dupload(h, &dnu, pl.nu));
+    TRY(dupload(h, &dlpp, lpp));
+    TRY(dupload(h, &dlpm, lpm));
+    TRY(dupload(h, &dlsp, lsp));
+    TRY(dupload(h, &dlsm, lsm));
+    TRY(dupload(h, &dlip, lip));
+    TRY(dupload(h, &dlim, lim));
+    TRY(dupload(h, &dcp, pl.coarse_ptr));
+    TRY(dupload(h, &dci, cidx));
+    TRY(dupload(h, &dcpat, cpat));
+    D.Ti = dTi; D.Tb = dTb; D.Tp = dTp; D.T = dT; D.nb = dnb; D.np = dnp; D.owner = down;
+    D.a_off = dao; D.dinv_off = ddo; D.sbb_off = dso; D.vec_off = dvo; D.aug_off = dgo;
+    D.aug = daug; D.b_off = dbo; D.b_lam = dbl; D.b_sign = dbs; D.p_off = dpo; D.p_grp = dpg;
+    D.sigma = dsig; D.nu = dnu;
+    D.lam_patch_p = dlpp; D.lam_patch_m = dlpm; D.lam_pos_p = dlsp; D.lam_pos_m = dlsm;
+    D.lam_idx_p = dlip; D.lam_idx_m = dlim; D.coarse_ptr = dcp; D.coarse_idx = dci; D.coarse_patch = dcpat;
     std::vector<int64_t> bpart(b_lam_all.size());
     for (int s = 0; s < P; ++s) {
       const PatchPlan& q = pl.pp[s];
@@ -505,109 +665,8 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dalloc(h, &D.b_aown, bpart.size()));
     TRY(dalloc(h, &D.b_apart, bpart.size()));
     h->nb_total = (int64_t)bpart.size();
-  }
-  double *wp, *wm;
-  TRY(dalloc(h, &wp, pl.m));
-  TRY(dalloc(h, &wm, pl.m));
-  D.wplus = wp;
-  D.wminus = wm;
-  TRY(dalloc(h, &D.A, oa));
-  TRY(dalloc(h, &D.Dinv, od));
-  {
-    std::vector<int64_t> so(P);
-    int64_t tot = 0;
-    for (int s = 0; s < P; ++s) {
-      so[s] = tot;
-      tot += (int64_t)(Ti[s] + Tb[s]) * TSZ;
-    }
-    TRY(dupload(h, &h->d_scr_off, so));
-    TRY(dalloc(h, &h->xscratch, tot));
-  }
-  TRY(dalloc(h, &h->F, ov));
-  CK(cudaMemsetAsync(h->F, 0, sizeof(double) * ov, h->stream));
-  TRY(dalloc(h, &h->d_iters, (size_t)h->n_steps + 1));
-  h->hist_cap = (int64_t)(h->n_steps + 1) * (h->max_iter + 1);
-  TRY(dalloc(h, &D.Sbb, os));
-  TRY(dalloc(h, &D.C, (size_t)tri_tiles(Tc) * TSZ));
-  TRY(dalloc(h, &D.Cinv, (size_t)Tc * TSZ));
-  TRY(dalloc(h, &h->X1, ov));
-  TRY(dalloc(h, &h->XW, ov));
-  TRY(dalloc(h, &h->XJ, ov));
-  TRY(dalloc(h, &h->JS, ov));
-  TRY(dalloc(h, &h->PW, ov));
-  TRY(dalloc(h, &h->lam, pl.m));
-  TRY(dalloc(h, &h->r, pl.m));
-  TRY(dalloc(h, &h->z, pl.m));
-  TRY(dalloc(h, &h->pk, pl.m));
-  TRY(dalloc(h, &h->q, pl.m));
-  TRY(dalloc(h, &h->Pc, pl.nc));
-  // chain-free PCG buffers
-  TRY(dalloc(h, &h->CX, (size_t)tri_tiles(Tc) * TSZ));
-  TRY(dalloc(h, &h->r2, pl.m));
-  TRY(dalloc(h, &h->pk2, pl.m));
-  TRY(dalloc(h, &h->Yv, ov));
-  TRY(dalloc(h, &h->Yc, (size_t)Tc * TS));
-  TRY(dalloc(h, &h->partA, 4096));
-  TRY(dalloc(h, &h->partB, 4096));
-  if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) {
-    TRY(dalloc(h, &h->tstamp, 8 * 64 + 16));
-    CK(cudaMemsetAsync(h->tstamp, 0, (8 * 64 + 16) * sizeof(unsigned long long), h->stream));
-  }
-  CK(cudaMemsetAsync(h->Yv, 0, sizeof(double) * ov, h->stream));
-  {
-    h->maxTp = 0;
-    for (int s = 0; s < P; ++s) h->maxTp = std::max(h->maxTp, Tp[s]);
-    std::vector<InvDesc> cinv(1, InvDesc{0, 0, 0, 0, Tc});
-    TRY(dupload(h, &h->d_cinv, cinv));
-    // work items, largest first (round-robin over the persistent blocks)
-    int dev_sms = 148;
-    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device);
-    const int64_t ctiles = (int64_t)Tc * Tc;
-    h->coarse_ch = (int)std::max<int64_t>(1, std::min<int64_t>(64, ctiles / (4 * (int64_t)dev_sms)));
-    h->coarse_maxch = std::max(1, (Tc + h->coarse_ch - 1) / h->coarse_ch);
-    std::vector<std::pair<int, int2>> p1, p5, sy, pcv, fw, fwa, bw, bwc, rhs;
-    for (int s = 0; s < P; ++s) {
-      const int Trs = Ti[s] + Tb[s];
-      for (int I = 0; I < T[s]; ++I) {
-        const int cost = I < Trs ? I + 1 : Trs;
-        if (pl.sigma[s] > 0) fw.push_back({cost, make_int2(s, I)});
-        fwa.push_back({cost, make_int2(s, I)});
-      }
-      for (int J = 0; J < std::max(Trs, 1); ++J) {
-        bw.push_back({T[s] - J, make_int2(s, J)});
-        if (pl.sigma[s] > 0) bwc.push_back({T[s] - J, make_int2(s, J)});
-      }
-      if (pl.sigma[s] > 0)
-        for (int c = 0; c < 3; ++c) rhs.push_back({pl.nloc / 3, make_int2(s, c)});
-      else
-        rhs.push_back({T[s] * TS / 8, make_int2(s, -1)});
-      for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.push_back({I < Tb[s] ? I + 1 : Tb[s], make_int2(s, I)});
-      for (int J = 0; J < Tb[s]; ++J) p5.push_back({Tb[s] - J + Tp[s], make_int2(s, J)});
-      for (int I = 0; I < Tb[s]; ++I) sy.push_back({Tb[s], make_int2(s, I)});
-    }
-    const int ch = h->coarse_ch;
-    for (int I = 0; I < Tc; ++I)
-      for (int c = 0; c < h->coarse_maxch; ++c) pcv.push_back({std::min(Tc, (c + 1) * ch) - c * ch, make_int2(I, c)});
-    auto bycost = [](const std::pair<int, int2>& x, const std::pair<int, int2>& y) {
-      return x.first != y.first ? x.first > y.first : (x.second.x != y.second.x ? x.second.x < y.second.x : x.second.y < y.second.y);
-    };
-    auto upload = [&](std::vector<std::pair<int, int2>>& v, int2** dst, int* n) -> tcg_status {
-      std::stable_sort(v.begin(), v.end(), bycost);
-      std::vector<int2> w;
-      for (auto& e : v) w.push_back(e.second);
-      *n = (int)w.size();
-      return dupload(h, dst, w);
-    };
-    TRY(upload(p1, &h->d_it_p1, &h->n_p1));
-    TRY(upload(p5, &h->d_it_p5, &h->n_p5));
-    TRY(upload(sy, &h->d_it_sy, &h->n_sy));
-    TRY(upload(pcv, &h->d_it_pc, &h->n_pc));
-    TRY(upload(fw, &h->d_it_fw, &h->n_fw));
-    TRY(upload(fwa, &h->d_it_fw_all, &h->n_fw_all));
-    TRY(upload(bw, &h->d_it_bw, &h->n_bw));
-    TRY(upload(bwc, &h->d_it_bwc, &h->n_bwc));
-    TRY(upload(rhs, &h->d_it_rhs, &h->n_rhs));
-    // local id -> aug position
+    TRY(dalloc(h, &D.wplus, pl.m));
+    TRY(dalloc(h, &D.wminus, pl.m));
     std::vector<int> l2a((size_t)P * pl.nloc, -1);
     for (int s = 0; s < P; ++s) {
       const auto& aug = pl.pp[s].aug;
@@ -617,49 +676,6 @@ static tcg_status do_setup(tcg_ctx* h) {
     int* dl2a;
     TRY(dupload(h, &dl2a, l2a));
     D.loc2aug = dl2a;
-    TRY(dalloc(h, &h->Sinv, (size_t)Tc * Tc * TSZ));
-    TRY(dalloc(h, &h->Ppart, (size_t)Tc * h->coarse_maxch * TS));
-  }
-  TRY(dalloc(h, &h->partial, RED_BLOCKS));
-  TRY(dalloc(h, &h->hist, (size_t)(h->n_steps + 1) * (h->max_iter + 1)));
-  TRY(dalloc(h, &h->a_loc, (size_t)P * pl.nloc));
-  TRY(dalloc(h, &h->st, 1));
-  TRY(dalloc(h, &h->derr, 1));
-  if (!h->h_st) CK(cudaMallocHost(&h->h_st, sizeof(PcgState)));
-  CK(cudaMemsetAsync(h->st, 0, sizeof(PcgState), h->stream));
-  CK(cudaMemsetAsync(h->derr, 0, sizeof(DevError), h->stream));
-  CK(cudaMemsetAsync(h->a_loc, 0, sizeof(double) * (size_t)P * pl.nloc, h->stream));
-  CK(cudaMemsetAsync(h->XW, 0, sizeof(double) * ov, h->stream));
-  CK(cudaMemsetAsync(h->PW, 0, sizeof(double) * ov, h->stream));
-  CK(cudaMemsetAsync(h->lam, 0, sizeof(double) * std::max<int64_t>(pl.m, 1), h->stream));
-
-  // chol descriptors
-  std::vector<CholDesc> desc(P);
-  for (int s = 0; s < P; ++s) desc[s] = CholDesc{a_off[s], dinv_off[s], sbb_off[s], T[s], Ti[s] + Tb[s], Ti[s], Tb[s]};
-  TRY(dupload(h, &h->d_desc, desc));
-  std::vector<CholDesc> cdesc(1, CholDesc{0, 0, -1, Tc, Tc, -1, 0});
-  TRY(dupload(h, &h->d_cdesc, cdesc));
-  // colour lists (parity classes)
-  std::vector<int> colour_all;
-  h->colour_off.assign(9, 0);
-  for (int c = 0; c < 8; ++c) {
-    for (int s = 0; s < P; ++s) {
-      int ix = s % pl.P[0], iy = (s / pl.P[0]) % pl.P[1], iz = s / (pl.P[0] * pl.P[1]);
-      if (((ix & 1) | ((iy & 1) << 1) | ((iz & 1) << 2)) == c) colour_all.push_back(s);
-    }
-    h->colour_off[c + 1] = (int64_t)colour_all.size();
-  }
-  TRY(dupload(h, &h->d_colour, colour_all));
-  // glued readout map: edge -> (patch*nloc + local) of its lowest-id owner
-  {
-    std::vector<int64_t> src(pl.nedges, -1);
-    for (int s = 0; s < P; ++s)
-      for (int a = 0; a < pl.nloc; ++a) {
-        int64_t g = pl.local_to_global(s, a);
-        if (src[g] < 0) src[g] = (int64_t)s * pl.nloc + a;
-      }
-    TRY(dupload(h, &h->d_glued_src, src));
-    TRY(dalloc(h, &h->glued, pl.nedges));
   }
 
   // ---- 1D tables ----
@@ -682,66 +698,254 @@ static tcg_status do_setup(tcg_ctx* h) {
     if (pl.el[d] + 2 * pl.p > 160) return fail(h, TCG_EINVAL, "elements + 2p must be <= 160");
   }
   TRY(dalloc(h, &tb.base, toff));
-
-  h->h_a_off = a_off;
-  h->h_vec_off = vec_off;
-  h->h_T = T;
-  h->a_total = oa;
-  h->total_tiles = tile_start[P];
-  // ---- solver kernel shared memory ----
   {
     int maxn = 0, maxel = 0;
-    for (int d = 0; d < 3; ++d) { maxn = std::max(maxn, pl.el[d] + pl.p); maxel = std::max(maxel, pl.el[d]); }
+    for (int d = 0; d < 3; ++d) {
+      maxn = std::max(maxn, pl.el[d] + pl.p);
+      maxel = std::max(maxel, pl.el[d]);
+    }
     h->smem_tables = sizeof(double) * (2 * (pl.p + 1) + (size_t)maxel * (pl.p + 1) * (3 * maxn + 2));
   }
+
+  // ---- work items per rank (largest first, dealt round-robin over the rank's blocks) ----
+  int dev_sms = 148;
+  CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
+  h->coarse_ch = (int)std::max<int64_t>(1, std::min<int64_t>(64, (int64_t)Tc * Tc / (4 * (int64_t)dev_sms)));
+  h->coarse_maxch = std::max(1, (Tc + h->coarse_ch - 1) / h->coarse_ch);
+  std::vector<int> crow_owner(std::max(Tc, 1));
+  for (int I = 0; I < Tc; ++I) crow_owner[I] = (int)((int64_t)I * NR / Tc);
+  TRY(dupload(h, &h->d_crow_owner, crow_owner));
   {
-    // persistent PCG: shared memory = max over its item kinds
+    ItemLists p1(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR);
+    for (int s = 0; s < P; ++s) {
+      const int r = owner[s];
+      const int Trs = Ti[s] + Tb[s];
+      for (int I = 0; I < T[s]; ++I) {
+        const int cost = I < Trs ? I + 1 : Trs;
+        if (pl.sigma[s] > 0) fw.per_rank[r].push_back({cost, make_int2(s, I)});
+        fwa.per_rank[r].push_back({cost, make_int2(s, I)});
+      }
+      for (int J = 0; J < std::max(Trs, 1); ++J) {
+        bw.per_rank[r].push_back({T[s] - J, make_int2(s, J)});
+        if (pl.sigma[s] > 0) bwc.per_rank[r].push_back({T[s] - J, make_int2(s, J)});
+      }
+      if (pl.sigma[s] > 0)
+        for (int c = 0; c < 3; ++c) rhs.per_rank[r].push_back({pl.nloc / 3, make_int2(s, c)});
+      else
+        rhs.per_rank[r].push_back({T[s] * TS / 8, make_int2(s, -1)});
+      for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], make_int2(s, I)});
+      for (int J = 0; J < Tb[s]; ++J) p5.per_rank[r].push_back({Tb[s] - J + Tp[s], make_int2(s, J)});
+      for (int I = 0; I < Tb[s]; ++I) sy.per_rank[r].push_back({Tb[s], make_int2(s, I)});
+    }
+    const int ch = h->coarse_ch;
+    for (int I = 0; I < Tc; ++I)
+      for (int c = 0; c < h->coarse_maxch; ++c)
+        pcv.per_rank[crow_owner[I]].push_back({std::min(Tc, (c + 1) * ch) - c * ch, make_int2(I, c)});
+    TRY(upload_items(h, p1, &h->d_it_p1, &h->d_off_p1, &h->off_p1));
+    TRY(upload_items(h, p5, &h->d_it_p5, &h->d_off_p5, &h->off_p5));
+    TRY(upload_items(h, sy, &h->d_it_sy, &h->d_off_sy));
+    TRY(upload_items(h, pcv, &h->d_it_pc, &h->d_off_pc, &h->off_pc));
+    TRY(upload_items(h, fw, &h->d_it_fw, &h->d_off_fw));
+    TRY(upload_items(h, fwa, &h->d_it_fwa, &h->d_off_fwa, &h->off_fwa));
+    TRY(upload_items(h, bw, &h->d_it_bw, &h->d_off_bw));
+    TRY(upload_items(h, bwc, &h->d_it_bwc, &h->d_off_bwc));
+    TRY(upload_items(h, rhs, &h->d_it_rhs, &h->d_off_rhs));
+  }
+
+  // ---- shared memory and persistent grid ----
+  {
     size_t p1 = (size_t)h->maxTb * TS;
     size_t p5 = (size_t)(h->maxTb + h->maxTp) * TS + 8 * TS;
-    size_t p34 = (size_t)h->coarse_ch * TS;
+    size_t pcs = (size_t)h->coarse_ch * TS;
     size_t syv = (size_t)h->maxTb * TS + 9 * TS;
-    size_t fwb = (size_t)h->maxT * TS + 8 * TS;  // forward / backward full-factor items
+    size_t fwb = (size_t)h->maxT * TS + 8 * TS;
     size_t maxcomp = 0;
     for (int c = 0; c < 3; ++c) maxcomp = std::max(maxcomp, (size_t)pl.comp_dim(c, 0) * pl.comp_dim(c, 1) * pl.comp_dim(c, 2));
-    fwb = std::max(fwb, 2 * maxcomp);  // rhs mass apply (two component buffers)
-    p34 = std::max(p34, fwb);
-    h->smem_pcg = sizeof(double) * std::max(std::max(p1, p5), std::max(p34, syv));
+    fwb = std::max(fwb, 2 * maxcomp);
+    h->smem_pcg = sizeof(double) * std::max(std::max(p1, p5), std::max(std::max(pcs, fwb), syv));
     TRY(set_smem(h, (const void*)k_steps, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_fw, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_xinv_row, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_p1_lam, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_pc, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_sinv, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_p5, h->smem_pcg));
+    TRY(set_smem(h, (const void*)k_xinv_row, 2 * TS * SPAD * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_sinv, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_trinv_row, 2 * TS * SPAD * sizeof(double)));
-    int dev_sms = 0, occ = 0;
-    CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
+    TRY(set_smem(h, (const void*)k_tables1d, h->smem_tables));
+    TRY(set_smem(h, (const void*)k_potrf, 2 * TS * 65 * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_update, 2 * TS * SPAD * sizeof(double)));
+    int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps, NTHR, h->smem_pcg));
-    if (occ < 1) return fail(h, TCG_ECUDA, "persistent PCG kernel does not fit on an SM");
-    {
-      const char* ev = getenv("TCG_PCG_BLOCKS_PER_SM");
-      int per = ev ? std::max(1, atoi(ev)) : 2;
-      h->pcg_blocks = dev_sms * std::min(occ, per);
-    }
-    if (h->pcg_blocks > 4096) h->pcg_blocks = 4096;
+    if (occ < 1) return fail(h, TCG_ECUDA, "persistent stepper kernel does not fit on an SM");
+    const char* ev = getenv("TCG_PCG_BLOCKS_PER_SM");
+    int per = ev ? std::max(1, atoi(ev)) : 2;
+    int total = dev_sms * std::min(occ, per);  // co-resident blocks on this device
+    h->nbr = std::max(1, total / (int)(h->world > 1 ? 1 : h->vranks));
+    h->lam_chunk = std::max<int64_t>(1, (pl.m + (int64_t)NR * h->nbr - 1) / ((int64_t)NR * h->nbr));
   }
-  TRY(set_smem(h, (const void*)k_tables1d, h->smem_tables));
-  TRY(set_smem(h, (const void*)k_potrf, 2 * TS * 65 * sizeof(double)));
-  TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
-  TRY(set_smem(h, (const void*)k_update, 2 * TS * SPAD * sizeof(double)));
+
+  // ---- per-rank allocations ----
+  std::vector<int> local_ranks;
+  if (h->world > 1) local_ranks.push_back(h->rank);
+  else
+    for (int r = 0; r < h->vranks; ++r) local_ranks.push_back(r);
+  h->rd.assign(local_ranks.size(), RankDev());
+  for (size_t li = 0; li < local_ranks.size(); ++li) {
+    RankDev& R = h->rd[li];
+    R.r = local_ranks[li];
+    for (int s = 0; s < P; ++s)
+      if (owner[s] == R.r) R.plist.push_back(s);
+    std::vector<int64_t> tstart(1, 0);
+    std::vector<CholDesc> desc;
+    for (int s : R.plist) {
+      tstart.push_back(tstart.back() + tri_tiles(T[s]));
+      desc.push_back(CholDesc{a_off[s], dinv_off[s], sbb_off[s], T[s], Ti[s] + Tb[s], Ti[s], Tb[s]});
+      R.maxT = std::max(R.maxT, T[s]);
+      R.maxTr = std::max(R.maxTr, Ti[s] + Tb[s]);
+      R.maxTb = std::max(R.maxTb, Tb[s]);
+    }
+    R.ntiles = tstart.back();
+    R.ndesc = (int)desc.size();
+    TRY(dupload(h, &R.d_plist, R.plist));
+    TRY(dupload(h, &R.d_tstart, tstart));
+    TRY(dupload(h, &R.d_desc, desc));
+    TRY(dalloc(h, &R.A, oa[R.r]));
+    TRY(dalloc(h, &R.Dinv, od[R.r]));
+    TRY(dalloc(h, &R.xscr, od[R.r]));
+    TRY(dalloc(h, &R.Sbb, os[R.r]));
+    TRY(dzero(h, &R.F, ov));
+    TRY(dzero(h, &R.Z, ov));
+    TRY(dzero(h, &R.XJ, ov));
+    TRY(dzero(h, &R.JS, ov));
+    TRY(dzero(h, &R.XW, ov));
+    TRY(dzero(h, &R.Y, ov));
+    TRY(dzero(h, &R.PW, ov));
+    TRY(dzero(h, &R.a_loc, (size_t)P * pl.nloc));
+    TRY(dzero(h, &R.lam, pl.m));
+    TRY(dzero(h, &R.r0, pl.m));
+    TRY(dzero(h, &R.r1, pl.m));
+    TRY(dzero(h, &R.pk0, pl.m));
+    TRY(dzero(h, &R.pk1, pl.m));
+    TRY(dzero(h, &R.q, pl.m));
+    TRY(dzero(h, &R.Ppart, (size_t)Tc * h->coarse_maxch * TS));
+    TRY(dzero(h, &R.Pc, pl.nc));
+    TRY(dzero(h, &R.partials, (size_t)h->nbr + 1));
+    TRY(dzero(h, &R.hist, (size_t)(h->n_steps + 1) * (h->max_iter + 1)));
+    TRY(dzero(h, &R.iters, (size_t)h->n_steps + 1));
+    TRY(dzero(h, &R.bar, 1));
+    TRY(dzero(h, &R.st, 1));
+    TRY(dzero(h, &R.derr, 1));
+    if (li == 0) {
+      TRY(dalloc(h, &R.C, (size_t)tri_tiles(Tc) * TSZ));
+      TRY(dalloc(h, &R.Cinv, (size_t)Tc * TSZ));
+      TRY(dalloc(h, &R.CX, (size_t)tri_tiles(Tc) * TSZ));
+      TRY(dalloc(h, &R.Sinv, (size_t)Tc * Tc * TSZ));
+    } else {
+      R.C = h->rd[0].C;
+      R.Cinv = h->rd[0].Cinv;
+      R.CX = h->rd[0].CX;
+      R.Sinv = h->rd[0].Sinv;
+    }
+  }
+  // ---- per-rank pointer tables (peer memory for real ranks) ----
+  {
+    std::vector<std::vector<void*>> bufs(NR);  // [rank][buffer] in a fixed order
+    for (auto& R : h->rd)
+      bufs[R.r] = {R.A, R.Sbb, R.Z, R.XW, R.Y, R.PW, R.lam, R.r0, R.r1, R.pk0, R.pk1, R.Ppart, R.bar, R.a_loc};
+    if (h->world > 1) TRY(open_peer_tables(h, bufs));
+    for (int r = 0; r < NR; ++r) {
+      D.Ar[r] = (double*)bufs[r][0];
+      D.Sbbr[r] = (double*)bufs[r][1];
+    }
+    h->D.me = 0;
+    for (auto& R : h->rd) {
+      R.D = D;
+      R.D.me = R.r;
+      R.D.A = R.A;
+      R.D.Dinv = R.Dinv;
+      R.D.Sbb = R.Sbb;
+      R.D.C = R.C;
+      R.D.Cinv = R.Cinv;
+    }
+    // keep the table for step_args
+    h->peer_bufs = bufs;
+  }
+  std::vector<CholDesc> cdesc(1, CholDesc{0, 0, -1, Tc, Tc, -1, 0});
+  TRY(dupload(h, &h->d_cdesc, cdesc));
+  std::vector<InvDesc> cinv(1, InvDesc{0, 0, 0, 0, Tc});
+  TRY(dupload(h, &h->d_cinv, cinv));
+  // colour lists (parity classes) for the conflict-free coarse scatter
+  {
+    std::vector<int> colour_all;
+    h->colour_off.assign(9, 0);
+    for (int c = 0; c < 8; ++c) {
+      for (int s = 0; s < P; ++s) {
+        int ix = s % pl.P[0], iy = (s / pl.P[0]) % pl.P[1], iz = s / (pl.P[0] * pl.P[1]);
+        if (((ix & 1) | ((iy & 1) << 1) | ((iz & 1) << 2)) == c) colour_all.push_back(s);
+      }
+      h->colour_off[c + 1] = (int64_t)colour_all.size();
+    }
+    TRY(dupload(h, &h->d_colour, colour_all));
+  }
+  // readout maps: glued edge -> (patch*nloc + local) of its lowest-id owner; gathered a
+  {
+    std::vector<int64_t> src(pl.nedges, -1);
+    for (int s = 0; s < P; ++s)
+      for (int a = 0; a < pl.nloc; ++a) {
+        int64_t g = pl.local_to_global(s, a);
+        if (src[g] < 0) src[g] = (int64_t)s * pl.nloc + a;
+      }
+    TRY(dupload(h, &h->d_glued_src, src));
+    TRY(dalloc(h, &h->glued, pl.nedges));
+    TRY(dalloc(h, &h->a_all, (size_t)P * pl.nloc));
+  }
+  if (!h->h_st) CK(cudaMallocHost(&h->h_st, sizeof(PcgState)));
+  if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) TRY(dzero(h, &h->tstamp, 8 * 64 + 16));
   if (getenv("TCG_DEBUG_KEEP") && atoi(getenv("TCG_DEBUG_KEEP")) != 0) {
-    TRY(dalloc(h, &h->dbgA, oa));
+    TRY(dalloc(h, &h->dbgA, h->rd[0].A ? (size_t)oa[h->rd[0].r] : 1));
     TRY(dalloc(h, &h->dbgC, (size_t)tri_tiles(Tc) * TSZ));
   }
+  h->bar_round = 0;
+  TRY(sync_ranks(h));
   TRY(do_numeric(h));
   h->setup_done = true;
   return TCG_OK;
 }
 
+// Exchange CUDA IPC handles of every rank's buffers through NCCL and open the peers' ones.
+static tcg_status open_peer_tables(tcg_ctx* h, std::vector<std::vector<void*>>& bufs) {
+  const int NR = h->nranks;
+  const size_t nb = bufs[h->rank].size();
+  std::vector<cudaIpcMemHandle_t> mine(nb);
+  for (size_t i = 0; i < nb; ++i) CK(cudaIpcGetMemHandle(&mine[i], bufs[h->rank][i]));
+  const size_t bytes = nb * sizeof(cudaIpcMemHandle_t);
+  char *dsend, *drecv;
+  TRY(dalloc(h, &dsend, bytes));
+  TRY(dalloc(h, &drecv, bytes * NR));
+  CK(cudaMemcpyAsync(dsend, mine.data(), bytes, cudaMemcpyHostToDevice, h->stream));
+  ncclResult_t r = g_nccl.allGather(dsend, drecv, bytes, ncclInt8, h->comm, h->stream);
+  if (r != 0) return fail(h, TCG_ENCCL, "ncclAllGather (IPC handles) failed");
+  std::vector<cudaIpcMemHandle_t> all(nb * NR);
+  CK(cudaMemcpyAsync(all.data(), drecv, bytes * NR, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  for (int q = 0; q < NR; ++q) {
+    if (q == h->rank) continue;
+    bufs[q].assign(nb, nullptr);
+    for (size_t i = 0; i < nb; ++i) {
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, all[q * nb + i], cudaIpcMemLazyEnablePeerAccess));
+      h->ipc_opened.push_back(p);
+      bufs[q][i] = p;
+    }
+  }
+  return TCG_OK;
+}
+
 // =========================================================================================
-// step
+// steps
 // =========================================================================================
-static void prof_begin(tcg_ctx* h, int id, int tag) {
+static void prof_begin(tcg_ctx* h, int id) {
   if (h->prof_id != id) return;
   if (2 * h->prof_used + 2 > h->prof_ev.size()) {
     cudaEvent_t a, b;
@@ -749,9 +953,7 @@ static void prof_begin(tcg_ctx* h, int id, int tag) {
     cudaEventCreate(&b);
     h->prof_ev.push_back(a);
     h->prof_ev.push_back(b);
-    h->prof_tag.push_back(0);
   }
-  h->prof_tag[h->prof_used] = tag;
   cudaEventRecord(h->prof_ev[2 * h->prof_used], h->stream);
 }
 static void prof_end(tcg_ctx* h, int id) {
@@ -759,10 +961,8 @@ static void prof_end(tcg_ctx* h, int id) {
   cudaEventRecord(h->prof_ev[2 * h->prof_used + 1], h->stream);
   h->prof_used++;
 }
-// after a stream sync: accumulate the pairs of launches that did work (tag < iters)
-static void prof_collect(tcg_ctx* h, int iters) {
+static void prof_collect(tcg_ctx* h) {
   for (size_t i = 0; i < h->prof_used; ++i) {
-    if (h->prof_tag[i] >= iters) continue;
     h->prof_ms += elapsed_ms(h->prof_ev[2 * i], h->prof_ev[2 * i + 1]);
     h->prof_count += 1;
   }
@@ -771,95 +971,94 @@ static void prof_collect(tcg_ctx* h, int iters) {
 
 static StepArgs step_args(tcg_ctx* h) {
   StepArgs A{};
-  A.lam = h->lam;
-  A.r[0] = h->r;
-  A.r[1] = h->r2;
-  A.pk[0] = h->pk;
-  A.pk[1] = h->pk2;
-  A.F = h->F;
-  A.Z = h->X1;
-  A.XJ = h->XJ;
-  A.JS = h->JS;
-  A.XW = h->XW;
-  A.Y = h->Yv;
-  A.PW = h->PW;
-  A.a_loc = h->a_loc;
-  A.Sinv = h->Sinv;
-  A.Ppart = h->Ppart;
-  A.Pc = h->Pc;
+  const auto& B = h->peer_bufs;
+  for (int r = 0; r < h->nranks; ++r) {
+    A.Z[r] = (double*)B[r][2];
+    A.XW[r] = (double*)B[r][3];
+    A.Y[r] = (double*)B[r][4];
+    A.PW[r] = (double*)B[r][5];
+    A.lam[r] = (double*)B[r][6];
+    A.r[0][r] = (double*)B[r][7];
+    A.r[1][r] = (double*)B[r][8];
+    A.pk[0][r] = (double*)B[r][9];
+    A.pk[1][r] = (double*)B[r][10];
+    A.Ppart[r] = (double*)B[r][11];
+    A.bar[r] = (BarMem*)B[r][12];
+    A.a_loc[r] = (double*)B[r][13];
+  }
+  for (auto& R : h->rd) {  // own-only buffers of the local ranks
+    A.F[R.r] = R.F;
+    A.XJ[R.r] = R.XJ;
+    A.JS[R.r] = R.JS;
+    A.Sinv[R.r] = R.Sinv;
+    A.Pc[R.r] = R.Pc;
+    A.partials[R.r] = R.partials;
+    A.hist[R.r] = R.hist;
+    A.iters[R.r] = R.iters;
+    A.st[R.r] = R.st;
+  }
+  A.crow_owner = h->d_crow_owner;
   A.ch = h->coarse_ch;
   A.maxch = h->coarse_maxch;
-  A.partA = h->partA;
-  A.partB = h->partB;
-  A.hist = h->hist + h->hist_len;
-  A.iters = h->d_iters;
-  A.st = h->st;
-  A.it_p1 = h->d_it_p1;
-  A.it_p5 = h->d_it_p5;
-  A.it_sy = h->d_it_sy;
-  A.it_pc = h->d_it_pc;
-  A.it_fw = h->d_it_fw;
-  A.it_bw = h->d_it_bw;
-  A.it_bwc = h->d_it_bwc;
-  A.it_rhs = h->d_it_rhs;
-  A.n_bwc = h->n_bwc;
-  A.n_rhs = h->n_rhs;
-  A.n_p1 = h->n_p1;
-  A.n_p5 = h->n_p5;
-  A.n_sy = h->n_sy;
-  A.n_pc = h->n_pc;
-  A.n_fw = h->n_fw;
-  A.n_bw = h->n_bw;
+  A.it_p1 = h->d_it_p1; A.off_p1 = h->d_off_p1;
+  A.it_p5 = h->d_it_p5; A.off_p5 = h->d_off_p5;
+  A.it_sy = h->d_it_sy; A.off_sy = h->d_off_sy;
+  A.it_pc = h->d_it_pc; A.off_pc = h->d_off_pc;
+  A.it_fw = h->d_it_fw; A.off_fw = h->d_off_fw;
+  A.it_bw = h->d_it_bw; A.off_bw = h->d_off_bw;
+  A.it_bwc = h->d_it_bwc; A.off_bwc = h->d_off_bwc;
+  A.it_rhs = h->d_it_rhs; A.off_rhs = h->d_off_rhs;
   A.tstamp = h->tstamp;
   A.rtol = h->rtol;
   A.max_iter = h->max_iter;
+  A.nranks = h->nranks;
+  A.nbr = h->nbr;
+  A.rank_base = (h->world > 1) ? h->rank : 0;
+  A.sys_scope = (h->world > 1) ? 1 : 0;
+  A.lam_chunk = h->lam_chunk;
   A.source = h->source;
   A.dt = h->T / h->n_steps;
   A.step0 = (int)h->steps_done;
   A.nsteps = 0;
+  A.hist_off = h->hist_len;
+  A.round0 = h->bar_round;
   A.tb = h->tb;
   A.G = h->G;
   return A;
 }
 
-// coarse solve Pc = S_pp^-1 sum_s N_s^T (src1_p - src2_p) (standalone: F-apply benchmark)
-static void launch_coarse(tcg_ctx* h, const double* src1, const double* src2) {
-  if (h->D.Tc == 0) return;
-  StepArgs A = step_args(h);
-  k_pc<<<h->n_pc, NTHR, h->smem_pcg, h->stream>>>(h->D, A, src1, src2);
-  ++h->nlaunch;
-  k_pc_sum<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(592, (h->D.nc + 255) / 256)), 256, 0, h->stream>>>(h->D, A);
-  ++h->nlaunch;
-}
-
-// n implicit-Euler steps in ONE persistent cooperative launch (k_steps)
+// n implicit-Euler steps in ONE persistent cooperative launch (k_steps) over all local ranks
 static tcg_status do_steps(tcg_ctx* h, int n) {
   if (n <= 0) return TCG_OK;
   if (h->steps_done + n > h->n_steps) return fail(h, TCG_EINVAL, "more steps than set_time allows (n_steps)");
-  DevPlan& D = h->D;
-  CK(cudaMemsetAsync(h->st, 0, sizeof(PcgState), h->stream));
+  for (auto& R : h->rd) CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), h->stream));
   StepArgs A = step_args(h);
   A.nsteps = n;
+  DevPlan D = h->D;
   void* args[] = {(void*)&D, (void*)&A};
-  prof_begin(h, 7, -1);
-  CK(cudaLaunchCooperativeKernel((const void*)k_steps, dim3(h->pcg_blocks), dim3(NTHR), args, h->smem_pcg, h->stream));
+  const int grid = h->nbr * (int)h->rd.size();
+  prof_begin(h, 7);
+  CK(cudaLaunchCooperativeKernel((const void*)k_steps, dim3(grid), dim3(NTHR), args, h->smem_pcg, h->stream));
   ++h->nlaunch;
   prof_end(h, 7);
-  CK(cudaMemcpyAsync(h->h_st, h->st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
+  RankDev& R0 = h->rd[0];
+  CK(cudaMemcpyAsync(h->h_st, R0.st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
   h->d2h_bytes += (int64_t)sizeof(PcgState);
   CK(cudaStreamSynchronize(h->stream));
-  prof_collect(h, 1 << 30);
+  prof_collect(h);
   const PcgState hs = *h->h_st;
   const int64_t hl = hs.counter[2];
+  h->bar_round = hs.counter[3];  // barrier rounds of every rank after this launch
   std::vector<int> it(n);
-  CK(cudaMemcpy(it.data(), h->d_iters + h->steps_done, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(it.data(), R0.iters + h->steps_done, sizeof(int) * n, cudaMemcpyDeviceToHost));
   std::vector<double> hh(std::max<int64_t>(hl, 1));
-  if (hl > 0) CK(cudaMemcpy(hh.data(), h->hist + h->hist_len, sizeof(double) * hl, cudaMemcpyDeviceToHost));
+  // histories are written by rank 0 (block 0); on other ranks use the local iteration counts
+  const bool have_hist = (h->world == 1 || h->rank == 0);
+  if (have_hist && hl > 0) CK(cudaMemcpy(hh.data(), R0.hist + h->hist_len, sizeof(double) * hl, cudaMemcpyDeviceToHost));
   h->d2h_bytes += (int64_t)(sizeof(int) * n + sizeof(double) * hl);
   if (hs.failed) {
-    const int bad = hs.rp;
     std::ostringstream o;
-    o << "PCG did not converge: step " << bad + 1 << ", iterations " << hs.iter << ", relres "
+    o << "PCG did not converge: step " << hs.rp + 1 << ", iterations " << hs.iter << ", relres "
       << (hs.rho0 > 0 ? std::sqrt(std::max(hs.rz, 0.0) / hs.rho0) : 0.0) << (hs.nan ? " (curvature/NaN guard)" : "");
     h->broken = true;
     return fail(h, TCG_ENOCONV, o.str());
@@ -867,14 +1066,21 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   int64_t off = 0;
   for (int i = 0; i < n; ++i) {
     h->iters.push_back(it[i]);
-    h->final_rel.push_back(hh[off + it[i]]);
+    h->final_rel.push_back(have_hist ? hh[off + it[i]] : 0.0);
     off += it[i] + 1;
     h->total_iters += it[i];
   }
-  h->hist_all.insert(h->hist_all.end(), hh.begin(), hh.begin() + hl);
+  if (have_hist) h->hist_all.insert(h->hist_all.end(), hh.begin(), hh.begin() + hl);
+  else h->hist_all.insert(h->hist_all.end(), (size_t)hl, 0.0);
   h->hist_len += hl;
   h->steps_done += n;
   return TCG_OK;
+}
+
+// gather the local coefficient vectors of every patch (from its owner) into a_all
+__global__ void k_gather_aloc(double* out, StepArgs A, const int* owner, int nloc, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = A.a_loc[owner[i / nloc]][i];
 }
 
 // =========================================================================================
@@ -885,15 +1091,24 @@ extern "C" {
 tcg_status tcg_create(tcg_handle* out, int device, int rank, int world, const unsigned char* nccl_id, void* cuda_stream) {
   if (!out) return TCG_EINVAL;
   *out = nullptr;
-  if (world < 1 || rank < 0 || rank >= world || device < 0) return TCG_EINVAL;
+  if (world < 1 || world > MAXR || rank < 0 || rank >= world || device < 0) return TCG_EINVAL;
   if (world > 1 && !nccl_id) return TCG_EINVAL;
   tcg_ctx* h = new tcg_ctx();
   h->device = device;
   h->rank = rank;
   h->world = world;
+  if (nccl_id) std::memcpy(h->nccl_id, nccl_id, 128);
   h->stream = static_cast<cudaStream_t>(cuda_stream);
   *out = h;
-  if (world > 1) return fail(h, TCG_ENCCL, "multi-GPU (world > 1) is not built in this version");
+  return TCG_OK;
+}
+
+tcg_status tcg_set_virtual_ranks(tcg_handle h, int vranks) {
+  if (!h) return TCG_EINVAL;
+  if (h->planned || h->setup_done) return fail(h, TCG_ESTATE, "set_virtual_ranks after plan/setup");
+  if (vranks < 1 || vranks > MAXR) return fail(h, TCG_EINVAL, "virtual ranks 1.." + std::to_string(MAXR));
+  if (vranks > 1 && h->world > 1) return fail(h, TCG_EINVAL, "virtual ranks need world == 1");
+  h->vranks = vranks;
   return TCG_OK;
 }
 
@@ -1027,25 +1242,19 @@ tcg_status tcg_step(tcg_handle h, int n) {
   if (!h->setup_done || h->broken) return fail(h, TCG_ESTATE, "setup first (or handle failed)");
   if (n < 0) return fail(h, TCG_EINVAL, "n >= 0");
   cudaSetDevice(h->device);
-  h->launches_last = 0;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, h->stream);
-  {
-    tcg_status s = do_steps(h, n);
-    if (s != TCG_OK) {
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
-      return s;
-    }
+  tcg_status s = do_steps(h, n);
+  if (s == TCG_OK) {
+    cudaEventRecord(e1, h->stream);
+    cudaEventSynchronize(e1);
+    h->ms_steps += elapsed_ms(e0, e1);
   }
-  cudaEventRecord(e1, h->stream);
-  cudaEventSynchronize(e1);
-  h->ms_steps += elapsed_ms(e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  return TCG_OK;
+  return s;
 }
 
 tcg_status tcg_get_coefficients(tcg_handle h, int layout, double* out, size_t len) {
@@ -1053,15 +1262,23 @@ tcg_status tcg_get_coefficients(tcg_handle h, int layout, double* out, size_t le
   if (!h->setup_done) return fail(h, TCG_ESTATE, "setup first");
   const Plan& p = h->plan;
   cudaSetDevice(h->device);
+  const int64_t nall = (int64_t)p.npatch * p.nloc;
+  {
+    StepArgs A = step_args(h);
+    int* down = const_cast<int*>(h->D.owner);
+    k_gather_aloc<<<592, 256, 0, h->stream>>>(h->a_all, A, down, p.nloc, nall);
+    ++h->nlaunch;
+    CKL();
+  }
   if (layout == 0) {
-    size_t need = (size_t)p.npatch * p.nloc;
+    size_t need = (size_t)nall;
     if (!out || len < need) return fail(h, TCG_EINVAL, "buffer too short: need " + std::to_string(need));
-    CK(cudaMemcpyAsync(out, h->a_loc, need * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(out, h->a_all, need * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     h->d2h_bytes += (int64_t)(need * sizeof(double));
   } else if (layout == 1) {
     size_t need = (size_t)p.nedges;
     if (!out || len < need) return fail(h, TCG_EINVAL, "buffer too short: need " + std::to_string(need));
-    k_gather_glued<<<592, 256, 0, h->stream>>>(h->glued, h->a_loc, h->d_glued_src, p.nedges);
+    k_gather_glued<<<592, 256, 0, h->stream>>>(h->glued, h->a_all, h->d_glued_src, p.nedges);
     ++h->nlaunch;
     CKL();
     CK(cudaMemcpyAsync(out, h->glued, need * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -1094,7 +1311,7 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
   if (!h || !out) return TCG_EINVAL;
   std::memset(out, 0, sizeof(tcg_info));
   out->rank = h->rank;
-  out->world = h->world;
+  out->world = std::max(h->world, h->vranks);
   if (!h->planned) return TCG_OK;
   const Plan& p = h->plan;
   out->n_patches = p.npatch;
@@ -1129,8 +1346,7 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
   const double nc = (double)p.nc;
   bf += 8.0 * nc * (nc + 1) + 40.0 * p.m;
   bm += 40.0 * p.m;
-  // + the F-apply-like work of R3/R4/E1/E2 and the preconditioner apply of R5
-  bs += bf + bm;
+  bs += bf + bm;  // R3/R4/E1/E2 (one F-apply worth) and the z0 preconditioner apply (R5)
   fl += nc * nc * nc / 3.0;
   out->bytes_fapply = bf;
   out->bytes_precond = bm;
@@ -1140,59 +1356,41 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
   out->total_iters = h->total_iters;
   out->device_bytes = h->device_bytes;
   out->kernel_launches = h->nlaunch;
-  out->prof_ms = h->prof_ms;
-  out->h2d_bytes = h->h2d_bytes;
-  out->d2h_bytes = h->d2h_bytes;
-  out->prof_launches = h->prof_count;
-  {
-    // algorithmic bytes per launch of the profiled kernel
-    double b = 0;
-    for (int s = 0; s < p.npatch; ++s) {
-      const PatchPlan& q = p.pp[s];
-      double nb = q.nb, np = q.np, nr = q.ni + q.nb;
-      switch (h->prof_id) {
-        case 1: case 2: b += 8.0 * (nb * (nb + 1) / 2 + nb * np) + 16.0 * nb + 8.0 * np; break;
-        case 4: b += 4.0 * nb * (nb + 1) + 16.0 * nb; break;
-        case 5: if (p.sigma[s] > 0) b += 8.0 * (nr * (nr + 1) / 2 + nr * np) + 16.0 * (nr + np); break;
-        case 6: b += 8.0 * (nr * (nr + 1) / 2 + nr * np) + 16.0 * (nr + np); break;
-        default: break;
-      }
-    }
-    if (h->prof_id == 3) b = 8.0 * nc * (nc + 1) + 16.0 * nc;
-    out->prof_bytes_per_launch = b;
-  }
   out->ms_plan = h->ms_plan;
   out->ms_assembly = h->ms_assembly;
   out->ms_factor = h->ms_factor;
   out->ms_coarse = h->ms_coarse;
   out->ms_steps = h->ms_steps;
-  out->ms_pcg_last_step = h->ms_pcg_last;
+  out->prof_ms = h->prof_ms;
+  out->prof_launches = h->prof_count;
+  out->prof_bytes_per_launch = 0.0;  // per-launch bytes of the stepper depend on iterations (bench.py)
+  out->h2d_bytes = h->h2d_bytes;
+  out->d2h_bytes = h->d2h_bytes;
   return TCG_OK;
 }
 
 tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms) {
   if (!h || !ms) return TCG_EINVAL;
   if (!h->setup_done || h->broken) return fail(h, TCG_ESTATE, "setup first");
+  if (h->rd.size() != 1 || h->nranks != 1) return fail(h, TCG_EINVAL, "bench_fapply needs a single-rank handle");
   cudaSetDevice(h->device);
-  DevPlan& D = h->D;
+  RankDev& R = h->rd[0];
+  DevPlan& D = R.D;
+  StepArgs A = step_args(h);
+  const int np1 = h->off_p1[1], np5 = h->off_p5[1], npc = h->off_pc[1];
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, h->stream);
   for (int i = 0; i < n; ++i) {
-    if (h->n_p1 > 0) {
-      k_p1_lam<<<h->n_p1, NTHR, h->smem_pcg, h->stream>>>(D, h->d_it_p1, h->n_p1, h->r, h->XW);
-      ++h->nlaunch;
+    if (np1 > 0) k_p1_lam<<<np1, NTHR, h->smem_pcg, h->stream>>>(D, h->d_it_p1, np1, R.r0, R.XW);
+    if (npc > 0) {
+      k_pc<<<npc, NTHR, h->smem_pcg, h->stream>>>(D, A, h->d_it_pc, npc, R.XW, R.Ppart);
+      k_pc_sum<<<592, 256, 0, h->stream>>>(D, A, R.Pc);
     }
-    launch_coarse(h, h->XW, nullptr);
-    if (h->n_p5 > 0) {
-      k_p5<<<h->n_p5, NTHR, h->smem_pcg, h->stream>>>(D, step_args(h), h->XW);
-      ++h->nlaunch;
-    }
-    if (D.m > 0) {
-      k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, h->Yv, h->q);
-      ++h->nlaunch;
-    }
+    if (np5 > 0) k_p5<<<np5, NTHR, h->smem_pcg, h->stream>>>(D, h->d_it_p5, np5, R.XW, R.Pc, R.Y);
+    if (D.m > 0) k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, R.Y, R.q);
+    h->nlaunch += 5;
   }
   cudaEventRecord(e1, h->stream);
   CK(cudaEventSynchronize(e1));
@@ -1203,46 +1401,57 @@ tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms) {
   return TCG_OK;
 }
 
-// Debug readback (not part of the public header): what 0 = assembled augmented matrix of
-// patch `idx` (tile-packed, needs TCG_DEBUG_KEEP=1), 1 = its factor, 2 = aug map of patch,
-// 3 = assembled coarse matrix (tile-packed), 4 = X1 (aug-ordered rhs-stage vector of patch),
-// 5 = rho weights (w+, w-) interleaved, 6 = S_bb tiles of patch.
+tcg_status tcg_set_profile(tcg_handle h, int kernel_id) {
+  if (!h) return TCG_EINVAL;
+  if (kernel_id != 0 && kernel_id != 7) return fail(h, TCG_EINVAL, "kernel id 0 (off) or 7 (k_steps)");
+  h->prof_id = kernel_id;
+  h->prof_ms = 0;
+  h->prof_count = 0;
+  h->prof_used = 0;
+  return TCG_OK;
+}
+
+// Debug readback (not part of the public header; single-rank handles): what 0 = assembled
+// augmented matrix of patch `idx` (TCG_DEBUG_KEEP=1), 1 = its current factor/inverse,
+// 2 = aug map of patch, 3 = assembled coarse matrix, 4 = Z (rhs-stage vector) of patch,
+// 5 = rho weights interleaved, 6 = S_bb tiles of patch, 7 = phase timestamps.
 tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t len) {
   if (!h || !h->setup_done) return TCG_ESTATE;
   cudaSetDevice(h->device);
+  RankDev& R = h->rd[0];
   const double* src = nullptr;
   size_t n = 0;
   std::vector<double> tmp;
   if (what == 0 || what == 1) {
-    src = (what == 0 ? h->dbgA : h->D.A);
+    src = (what == 0 ? h->dbgA : R.A);
     if (!src) return fail(h, TCG_ESTATE, "TCG_DEBUG_KEEP not set");
     src += h->h_a_off[idx];
     n = tri_tiles(h->h_T[idx]) * TSZ;
   } else if (what == 2) {
-    const auto& aug = h->plan.pp[idx].aug;
-    for (int v : aug) tmp.push_back((double)v);
+    for (int v : h->plan.pp[idx].aug) tmp.push_back((double)v);
   } else if (what == 3) {
     src = h->dbgC;
     if (!src) return fail(h, TCG_ESTATE, "TCG_DEBUG_KEEP not set");
-    n = tri_tiles(h->D.Tc) * TSZ;
+    n = tri_tiles(h->Tc) * TSZ;
   } else if (what == 4) {
-    src = h->X1 + h->h_vec_off[idx];
+    src = R.Z + h->h_vec_off[idx];
     n = (size_t)h->h_T[idx] * TS;
   } else if (what == 5) {
     std::vector<double> wp(h->D.m), wm(h->D.m);
     CK(cudaMemcpy(wp.data(), h->D.wplus, sizeof(double) * h->D.m, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(wm.data(), h->D.wminus, sizeof(double) * h->D.m, cudaMemcpyDeviceToHost));
-    for (int64_t k = 0; k < h->D.m; ++k) { tmp.push_back(wp[k]); tmp.push_back(wm[k]); }
+    for (int64_t k = 0; k < h->D.m; ++k) {
+      tmp.push_back(wp[k]);
+      tmp.push_back(wm[k]);
+    }
+  } else if (what == 6) {
+    src = R.Sbb + h->h_sbb_off[idx];
+    n = tri_tiles(h->plan.pp[idx].Tb) * TSZ;
   } else if (what == 7) {
     if (!h->tstamp) return fail(h, TCG_ESTATE, "TCG_PHASE_TIMING not set");
     std::vector<unsigned long long> ts(8 * 64 + 16);
     CK(cudaMemcpy(ts.data(), h->tstamp, ts.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     for (auto v : ts) tmp.push_back((double)v);
-  } else if (what == 6) {
-    int64_t off = 0;
-    for (int s = 0; s < idx; ++s) off += tri_tiles(h->plan.pp[s].Tb) * TSZ;
-    src = h->D.Sbb + off;
-    n = tri_tiles(h->plan.pp[idx].Tb) * TSZ;
   } else {
     return TCG_EINVAL;
   }
@@ -1253,16 +1462,6 @@ tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t 
   }
   if (len < n) return fail(h, TCG_EINVAL, "need " + std::to_string(n));
   CK(cudaMemcpy(out, src, n * sizeof(double), cudaMemcpyDeviceToHost));
-  return TCG_OK;
-}
-
-tcg_status tcg_set_profile(tcg_handle h, int kernel_id) {
-  if (!h) return TCG_EINVAL;
-  if (kernel_id < 0 || kernel_id > 7) return fail(h, TCG_EINVAL, "kernel id 0..7");
-  h->prof_id = kernel_id;
-  h->prof_ms = 0;
-  h->prof_count = 0;
-  h->prof_used = 0;
   return TCG_OK;
 }
 

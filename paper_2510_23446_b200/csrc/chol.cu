@@ -210,7 +210,7 @@ __global__ void k_coarse_scatter(DevPlan D, const int* __restrict__ patches, int
   const int Tr = D.Ti[s] + D.Tb[s];
   const int np = D.np[s];
   const int* grp = D.p_grp + D.p_off[s];
-  const double* A = D.A + D.a_off[s];
+  const double* A = D.Ar[D.owner[s]] + D.a_off[s];  // S^s lives on the patch's owner
   for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
     const int a = e / np, b = e % np;
     const int ga = grp[a], gb = grp[b];
@@ -345,30 +345,6 @@ __global__ void __launch_bounds__(128) k_trinv_row(const InvDesc* __restrict__ d
   acc_store(X, acc2, -1.0);
 }
 
-// Phi^T tiles (Tp x Tb) of every patch: PhiT_{Ip,J} = sum_{K=J}^{Tb-1} L(Ti+Tb+Ip, Ti+K) X_bb(K,J),
-// written into the LS store below X_bb. grid (maxTp*maxTb, P), 128 threads.
-__global__ void __launch_bounds__(128) k_phiT(DevPlan D, int maxTb) {
-  const int s = blockIdx.y;
-  const int Ti = D.Ti[s], Tb = D.Tb[s], Tp = D.Tp[s];
-  const int Ip = blockIdx.x / maxTb, J = blockIdx.x % maxTb;
-  if (Ip >= Tp || J >= Tb) return;
-  extern __shared__ double smem[];
-  double* sA = smem;
-  double* sB = smem + TS * SPAD;
-  const double* A = D.A + D.a_off[s];
-  const double* X = D.LS + D.ls_off[s];
-  double acc[4][4][2];
-  acc_zero(acc);
-  for (int K = J; K < Tb; ++K) {
-    stage_tile(A + tri_off(Ti + Tb + Ip, Ti + K), sA);
-    stage_tile_T(X + tri_off(K, J), sB);
-    __syncthreads();
-    mma_acc(sA, sB, acc);
-    __syncthreads();
-  }
-  acc_store(D.LS + D.ls_off[s] + (tri_tiles(Tb) + (int64_t)Ip * Tb + J) * TSZ, acc, 1.0);
-}
-
 }  // namespace tcg
 
 namespace tcg {
@@ -402,8 +378,9 @@ namespace tcg {
 //   I >= Tr:  PhiT_IJ = sum_{K=J}^{Tr-1} L_IK X_KJ        (J < Tr; = W_pr W_rr^-1)
 // Rows < I already hold X, rows > I still hold L, so row I is computed into a per-patch
 // scratch row and copied back (k_xrow_copy) before row I+1. grid (maxTr, P), 128 threads.
-__global__ void __launch_bounds__(128) k_xinv_row(DevPlan D, int I, double* scratch, const int64_t* scr_off) {
-  const int s = blockIdx.y, J = blockIdx.x;
+__global__ void __launch_bounds__(128) k_xinv_row(DevPlan D, int I, double* scratch, const int64_t* scr_off,
+                                                  const int* plist) {
+  const int s = plist[blockIdx.y], J = blockIdx.x;
   const int Tr = D.Ti[s] + D.Tb[s], T = D.T[s];
   if (I >= T || J >= Tr || (I < Tr && J > I)) return;
   extern __shared__ double smem[];
@@ -440,8 +417,8 @@ __global__ void __launch_bounds__(128) k_xinv_row(DevPlan D, int I, double* scra
   acc_store(out, acc2, -1.0);
 }
 
-__global__ void k_xrow_copy(DevPlan D, int I, const double* scratch, const int64_t* scr_off) {
-  const int s = blockIdx.y, J = blockIdx.x;
+__global__ void k_xrow_copy(DevPlan D, int I, const double* scratch, const int64_t* scr_off, const int* plist) {
+  const int s = plist[blockIdx.y], J = blockIdx.x;
   const int Tr = D.Ti[s] + D.Tb[s], T = D.T[s];
   if (I >= T || J >= Tr || (I < Tr && J > I)) return;
   const double2* src = reinterpret_cast<const double2*>(scratch + scr_off[s] + (int64_t)J * TSZ);

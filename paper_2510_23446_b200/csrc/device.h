@@ -27,8 +27,19 @@ struct Tables1D {
 };
 
 // Device copy of the plan and the big device arrays.
+constexpr int MAXR = 8;  // ranks (GPUs, or virtual ranks on one GPU) of a sharded solve
+
+// Device view of the plan. Per-patch index arrays are global (all patches, replicated on
+// every rank); the big per-patch matrices live on the patch's owning rank: the tile pointer
+// of patch s is Ar[owner[s]] + a_off[s] (a_off is relative to the owner's allocation).
+// A / Dinv / Sbb are the launching rank's own allocations (setup kernels only touch owned
+// patches).
 struct DevPlan {
   int npatch;
+  int nranks;
+  const int* owner;         // per patch: owning rank
+  double* Ar[MAXR];         // per rank: augmented factors / inverse factors
+  double* Sbbr[MAXR];       // per rank: S_bb stores
   int64_t m, nc;
   // per patch
   const int* Ti;
@@ -39,7 +50,6 @@ struct DevPlan {
   const int* np;
   const int64_t* a_off;     // augmented tile-packed factor
   const int64_t* dinv_off;  // diagonal inverse tiles (Ti+Tb tiles)
-  const int64_t* ls_off;    // trailing [b;p] x b store
   const int64_t* sbb_off;   // captured S_bb store
   const int64_t* vec_off;   // aug-ordered per-patch vectors (64*T each)
   const int64_t* aug_off;
@@ -68,18 +78,17 @@ struct DevPlan {
   // coarse CSR
   const int* coarse_ptr;
   const int64_t* coarse_idx;  // index into aug-ordered vectors (p part)
+  const int* coarse_patch;    // patch of each CSR entry (its owner holds the value)
   // big arrays
   double* A;      // augmented factors
   double* Dinv;
-  double* LS;
   double* Sbb;
   // coarse factor
   double* C;      // tile-packed lower n_c (Tc tiles)
   double* Cinv;   // diagonal inverse tiles of C
   int Tc;
   int maxT, maxTbp;   // largest tile counts (shared-memory layout of the solver kernels)
-  int subst_local;    // 1: local triangular solves substitute on diagonal tiles (else inverse GEMV)
-  int subst_coarse;   // 1: same for the coarse factor
+  int me;             // launching rank (setup kernels)
 };
 
 }  // namespace tcg

@@ -28,49 +28,65 @@
 
 namespace tcg {
 
+// Barrier / reduction memory of one rank (in that rank's device memory).
+struct BarMem {
+  unsigned int local_count;   // arrivals of this rank's blocks (monotone)
+  unsigned int local_gen;     // release generation for this rank's blocks
+  unsigned int global_count;  // (rank 0 only) arrivals of rank leaders (monotone)
+  unsigned int pad;
+  double rank_part[2];        // this rank's partial of the current reduction (by round parity)
+  double pad2[6];
+};
+
+// Arguments of the persistent stepper. Every per-rank buffer is a table indexed by rank:
+// writes go to the launching block's own rank, reads of values owned elsewhere (interface
+// partners, lambda chunks, coarse rows) go to the owner's buffer (peer memory over NVLink on
+// a multi-GPU job; another allocation of the same device for virtual ranks).
 struct StepArgs {
-  // lambda-space vectors (m)
-  double* lam;
-  double* r[2];
-  double* pk[2];
-  // per-patch aug-ordered vectors (64*T per patch)
-  double* F;     // R1 output (conductor rhs f)
-  double* Z;     // R2 output (Z_r = L^-1 f_r, Z_p = f_p - h)
-  double* XJ;    // setup: forward of j_S (insulator rhs template)
-  const double* JS;
-  double* XW;    // P1/E1 output: b part w, p part -g
-  double* Y;     // P5/R4 output: b part y
-  double* PW;    // S_bb apply output: b part
-  double* a_loc; // local coefficient vectors (npatch x nloc)
+  // lambda-space vectors (m, valid on the owner of each chunk)
+  double* lam[MAXR];
+  double* r[2][MAXR];
+  double* pk[2][MAXR];
+  // per-patch aug-ordered vectors (global layout, valid on the patch owner)
+  double* F[MAXR];     // R1 output (conductor rhs f)
+  double* Z[MAXR];     // R2 output (Z_r = L^-1 f_r, Z_p = f_p - h)
+  double* XJ[MAXR];    // setup: forward of j_S (insulator rhs template)
+  double* JS[MAXR];
+  double* XW[MAXR];    // P1/E1 output: b part w, p part -g
+  double* Y[MAXR];     // P5/R4 output: b part y
+  double* PW[MAXR];    // S_bb apply output: b part
+  double* a_loc[MAXR]; // local coefficient vectors (npatch x nloc)
   // coarse
-  const double* Sinv;  // full symmetric S_pp^-1, Tc x Tc row-major tiles
-  double* Ppart;       // Tc x maxch x 64 chunk partials of Pc
-  double* Pc;          // materialised coarse solution (standalone kernels)
+  const double* Sinv[MAXR];  // full symmetric S_pp^-1 (replicated), Tc x Tc row-major tiles
+  double* Ppart[MAXR];       // Tc x maxch x 64 chunk partials of Pc (rows of the owning rank)
+  double* Pc[MAXR];          // materialised coarse solution (standalone kernels)
+  const int* crow_owner;     // coarse row block -> rank
   int ch, maxch;
-  double* partA;
-  double* partB;
-  // per-step outputs
-  double* hist;        // concatenated histories (sum over steps of iters+1)
-  int* iters;          // per step
-  PcgState* st;
-  // item lists (sorted by decreasing cost)
-  const int2* it_p1;  // (patch, row block of [b;p])
-  const int2* it_p5;  // (patch, b column block)
-  const int2* it_sy;  // (patch, b row block)
-  const int2* it_pc;  // (coarse row block, column chunk)
-  const int2* it_fw;  // (conductor patch, aug row block)
-  const int2* it_bw;  // (patch, r column block), all patches
-  const int2* it_bwc; // (patch, r column block), conductor patches only
-  const int2* it_rhs; // (patch, component) for conductors, (patch, -1) for insulators
-  int n_p1, n_p5, n_sy, n_pc, n_fw, n_bw, n_bwc, n_rhs;
-  unsigned long long* tstamp;  // optional phase timestamps (block 0), 8 per iteration
+  double* partials[MAXR];    // per block partial sums (own rank)
+  BarMem* bar[MAXR];
+  // per-step outputs (written by each rank's block 0 into its own buffers)
+  double* hist[MAXR];
+  int* iters[MAXR];
+  PcgState* st[MAXR];
+  // item lists: per rank r, items[off[r] .. off[r+1])
+  const int2 *it_p1, *it_p5, *it_sy, *it_pc, *it_fw, *it_bw, *it_bwc, *it_rhs;
+  const int *off_p1, *off_p5, *off_sy, *off_pc, *off_fw, *off_bw, *off_bwc, *off_rhs;
+  unsigned long long* tstamp;  // optional phase timestamps (rank 0 block 0)
   double rtol;
   int max_iter;
+  // ranks
+  int nranks;     // ranks of the job (real GPUs or virtual ranks)
+  int nbr;        // persistent blocks per rank
+  int rank_base;  // rank of block 0 of this launch (real multi-GPU: this process's rank)
+  int sys_scope;  // 1 when ranks are different GPUs (system-scope fences/atomics)
+  int64_t lam_chunk;  // lambda entries per (rank, block): owner of k = (k / lam_chunk) / nbr
   // time stepping
   int source;
   double dt;
   int step0;    // steps done before this launch
   int nsteps;   // steps to run
+  int64_t hist_off;  // offset of this launch's history in hist
+  unsigned int round0;  // barrier rounds completed before this launch (counters are monotone)
   Tables1D tb;
   Geom G;
 };
@@ -85,7 +101,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // tile (I,J) of patch s's inverse factor Xaug (aug tile numbering)
 __device__ __forceinline__ const double* xtile(const DevPlan& D, int s, int I, int J) {
-  return D.A + D.a_off[s] + tri_off(I, J);
+  return D.Ar[D.owner[s]] + D.a_off[s] + tri_off(I, J);
 }
 
 // fixed-order block reduction of one value per thread
@@ -101,9 +117,11 @@ __device__ __forceinline__ double block_sum(double local, double* red) {
   return r;
 }
 
-// Coarse solution entry g from the PC chunk partials (fixed order).
+// Coarse solution entry g from the PC chunk partials (fixed order), read on the rank that
+// owns coarse row block g/64.
 __device__ __forceinline__ double pc_get(const StepArgs& A, int64_t g) {
-  const double* p = A.Ppart + ((g >> 6) * A.maxch) * TS + (g & 63);
+  const int I = (int)(g >> 6);
+  const double* p = A.Ppart[A.crow_owner[I]] + ((int64_t)I * A.maxch) * TS + (g & 63);
   double v = 0.0;
   for (int c = 0; c < A.maxch; ++c) v += ldcg(p + (int64_t)c * TS);
   return v;
@@ -176,8 +194,9 @@ __device__ void p1_item(const DevPlan& D, int s, int I, Src vsrc, double* XW, do
   __syncthreads();
 }
 
-// ---- PC: Ppart[I][c] = sum_{J in chunk c} Sinv_IJ G_J,  G = sum_csr (src1 - src2) ----------
-__device__ void pc_item(const DevPlan& D, const StepArgs& A, int I, int c, const double* src1, const double* src2,
+// ---- PC: Ppart[I][c] = sum_{J in chunk c} Sinv_IJ G_J,  G_g = sum_{csr e of g} gsrc(e) -----------
+template <class GS>
+__device__ void pc_item(const DevPlan& D, const StepArgs& A, const double* Sinv, int I, int c, GS gsrc, double* Ppart,
                         double* sm) {
   const int Tc = D.Tc;
   const int J0 = c * A.ch, J1 = min(Tc, J0 + A.ch);
@@ -185,19 +204,15 @@ __device__ void pc_item(const DevPlan& D, const StepArgs& A, int I, int c, const
   for (int e = threadIdx.x; e < (J1 - J0) * TS; e += blockDim.x) {
     const int64_t g = (int64_t)J0 * TS + e;
     double val = 0.0;
-    if (g < D.nc) {
-      for (int k = D.coarse_ptr[g]; k < D.coarse_ptr[g + 1]; ++k) {
-        const int64_t idx = D.coarse_idx[k];
-        val += src2 ? (ldcg(src1 + idx) - ldcg(src2 + idx)) : ldcg(src1 + idx);
-      }
-    }
+    if (g < D.nc)
+      for (int k = D.coarse_ptr[g]; k < D.coarse_ptr[g + 1]; ++k) val += gsrc(k);
     sm[e] = val;
   }
   __syncthreads();
   double part[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) part[r] = 0.0;
-  const double* rowp = A.Sinv + ((int64_t)I * Tc) * TSZ + row0 * TS + 2 * lane;
+  const double* rowp = Sinv + ((int64_t)I * Tc) * TSZ + row0 * TS + 2 * lane;
 #pragma unroll 2
   for (int J = J0; J < J1; ++J) {
     const double* t = rowp + (int64_t)J * TSZ;
@@ -209,7 +224,7 @@ __device__ void pc_item(const DevPlan& D, const StepArgs& A, int I, int c, const
     for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
   }
   const double sum = warp_reduce8(part);
-  if ((lane & 3) == 0) A.Ppart[((int64_t)I * A.maxch + c) * TS + row0 + warp_reduce8_row()] = sum;
+  if ((lane & 3) == 0) Ppart[((int64_t)I * A.maxch + c) * TS + row0 + warp_reduce8_row()] = sum;
   __syncthreads();
 }
 
@@ -258,7 +273,7 @@ __device__ double symv_item(const DevPlan& D, double* PW, int s, int I, Src usrc
   for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) u[i] = (i < nb) ? usrc(s, bo + i, i) : 0.0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
-  const double* S = D.Sbb + D.sbb_off[s];
+  const double* S = D.Sbbr[D.owner[s]] + D.sbb_off[s];
   double part[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) part[q] = 0.0;
@@ -363,42 +378,69 @@ __device__ void bw_item(const DevPlan& D, int s, int J, const double* Zv, const 
   __syncthreads();
 }
 
-// Sum of per-block partials in one fixed order, broadcast: bit-identical in every block.
-__device__ __forceinline__ double sum_partials(const double* part, int n, double* bcast) {
-  if (threadIdx.x < 32) {
-    double t = 0.0;
-    for (int b = threadIdx.x; b < n; b += 32) t += ldcg(part + b);
-    t = warp_sum(t);
-    if (threadIdx.x == 0) *bcast = t;
-  }
-  __syncthreads();
-  const double r = *bcast;
-  __syncthreads();
-  return r;
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p, int sys) {
+  unsigned int v;
+  if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_scope(int sys) {
+  if (sys) __threadfence_system();
+  else __threadfence();
 }
 
-// Grid barrier for the cooperative (co-resident) launch: monotone arrival counter (zeroed
-// by the host before the launch); thread 0 of each block arrives after a release fence and
-// polls with acquire loads until every block of this round arrived.
-__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& target) {
+// Two-level barrier over every block of every rank, with an optional fused fixed-order sum.
+// Blocks of a rank arrive on the rank's counter; the last arriving block (the leader) sums
+// the rank's per-block partials in block order, publishes the rank partial, arrives on rank
+// 0's global counter and waits for all rank leaders, then releases its rank. After the
+// barrier every block sums the rank partials in rank order -> identical totals everywhere.
+// `round` counts barriers (identical sequence in every block of every rank).
+__device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& round, bool reduce, double value,
+                               double* bcast) {
   __syncthreads();
-  target += gridDim.x;
+  ++round;
+  const int sys = A.sys_scope;
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    unsigned int v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-    } while ((int)(v - target) < 0);
-    __threadfence();
+    BarMem* mine = A.bar[me];
+    if (reduce) A.partials[me][bl] = value;
+    fence_scope(sys);
+    const unsigned int old = atomicAdd(&mine->local_count, 1u);
+    if (old + 1 == round * (unsigned int)A.nbr) {  // leader of this rank
+      if (reduce) {
+        double t = 0.0;
+        for (int j = 0; j < A.nbr; ++j) t += __ldcg(A.partials[me] + j);
+        mine->rank_part[round & 1] = t;
+      }
+      fence_scope(sys);
+      unsigned int* gc = &A.bar[0]->global_count;
+      if (sys) atomicAdd_system(gc, 1u);
+      else atomicAdd(gc, 1u);
+      while ((int)(ld_acquire_u32(gc, sys) - round * (unsigned int)A.nranks) < 0) {
+      }
+      fence_scope(sys);
+      atomicExch(&mine->local_gen, round);
+    } else {
+      while ((int)(ld_acquire_u32(&mine->local_gen, 0) - round) < 0) {
+      }
+    }
+    fence_scope(sys);
+    if (reduce) {
+      double t = 0.0;
+      for (int r = 0; r < A.nranks; ++r) t += *(volatile double*)&A.bar[r]->rank_part[round & 1];
+      *bcast = t;
+    }
   }
   __syncthreads();
+  double total = 0.0;
+  if (reduce) total = *bcast;
+  __syncthreads();
+  return total;
 }
 
 // rhs item (R1). c in {0,1,2}: component c of conductor patch s, F = (sigma/dt) M a + phi j_S
 // with the mass apply sum-factorised (M_c = F_z (x) F_y (x) F_x, F_d = Md along d == c, Mb else;
 // banded |i-i'| <= p) through shared memory; c = -1: insulator patch s, Z = phi(t) XJ.
-__device__ void rhs_item(const DevPlan& D, const StepArgs& A, int s, int c, double t, double* sm) {
+__device__ void rhs_item(const DevPlan& D, const StepArgs& A, int me, int s, int c, double t, double* sm) {
   const double sig = D.sigma[s], nu = D.nu[s];
   double phi = 0.0;
   if (A.source == 1) phi = sinpi(2.0 * t);
@@ -406,7 +448,7 @@ __device__ void rhs_item(const DevPlan& D, const StepArgs& A, int s, int c, doub
   const int64_t vo = D.vec_off[s];
   if (c < 0) {
     const int R = D.T[s] * TS;
-    for (int pos = threadIdx.x; pos < R; pos += blockDim.x) A.Z[vo + pos] = phi * ldcg(A.XJ + vo + pos);
+    for (int pos = threadIdx.x; pos < R; pos += blockDim.x) A.Z[me][vo + pos] = phi * ldcg(A.XJ[me] + vo + pos);
     return;
   }
   const Geom& G = A.G;
@@ -416,10 +458,9 @@ __device__ void rhs_item(const DevPlan& D, const StepArgs& A, int s, int c, doub
   const int nn = nx * ny * nz;
   int off = 0;
   for (int cc = 0; cc < c; ++cc) off += G.cdim[cc][0] * G.cdim[cc][1] * G.cdim[cc][2];
-  const double* as = A.a_loc + (int64_t)s * G.nloc + off;
+  const double* as = A.a_loc[me] + (int64_t)s * G.nloc + off;
   double* u0 = sm;
   double* u1 = sm + nn;
-  // 1D factors (row-major; Md is (n-1)x(n-1), Mb n x n)
   const int n0 = tb.el[0] + p, n1 = tb.el[1] + p, n2 = tb.el[2] + p;
   const double* Fx = (c == 0) ? tb.base + tb.off_Md[0] : tb.base + tb.off_Mb[0];
   const double* Fy = (c == 1) ? tb.base + tb.off_Md[1] : tb.base + tb.off_Mb[1];
@@ -447,34 +488,54 @@ __device__ void rhs_item(const DevPlan& D, const StepArgs& A, int s, int c, doub
     const int ij = e % (nx * ny), k = e / (nx * ny);
     double v = 0.0;
     for (int q = max(0, k - p); q <= min(nz - 1, k + p); ++q) v += Fz[k * ldz + q] * u1[ij + nx * ny * q];
-    A.F[vo + pos] = scale * v + phi * A.JS[vo + pos];
+    A.F[me][vo + pos] = scale * v + phi * A.JS[me][vo + pos];
   }
   __syncthreads();
 }
 
 #define TSTAMP(slot) \
-  if (A.tstamp && b == 0 && threadIdx.x == 0 && it < 64 && step == 0) A.tstamp[it * 8 + (slot)] = gtimer()
+  if (A.tstamp && me == 0 && bl == 0 && threadIdx.x == 0 && it < 64 && step == 0) A.tstamp[it * 8 + (slot)] = gtimer()
 // step-level stamps of step 0 (slots 512..527): R1..R5 ends, loop end, E1..E3 ends
 #define SSTAMP(slot) \
-  if (A.tstamp && b == 0 && threadIdx.x == 0 && step == 0) A.tstamp[512 + (slot)] = gtimer()
+  if (A.tstamp && me == 0 && bl == 0 && threadIdx.x == 0 && step == 0) A.tstamp[512 + (slot)] = gtimer()
 
 // =======================================================================================
-// Persistent cooperative time stepper: A.nsteps implicit-Euler steps in one launch.
-// All blocks execute the same sequence of grid barriers (control flow depends only on
-// values every block computes identically).
+// Persistent cooperative time stepper: A.nsteps implicit-Euler steps in one launch, over
+// all ranks of the job. Control flow depends only on values every block of every rank
+// computes identically, so all blocks run the same sequence of barriers.
 // =======================================================================================
 __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   extern __shared__ double sm[];
   __shared__ double red[NTHR];
-  const int NB = gridDim.x, b = blockIdx.x;
+  __shared__ double bcast;
+  const int me = A.rank_base + (int)blockIdx.x / A.nbr;  // this block's rank
+  const int bl = (int)blockIdx.x % A.nbr;                 // block index within the rank
+  const int NB = A.nbr;
   const int64_t m = D.m;
-  const int64_t chunk = (m + NB - 1) / NB;
-  const int64_t k0 = min(m, (int64_t)b * chunk), k1 = min(m, k0 + chunk);
-  unsigned int* bar = &A.st->counter[1];
-  unsigned int bar_target = 0;
+  const int64_t gb = (int64_t)me * A.nbr + bl;
+  const int64_t k0 = min(m, gb * A.lam_chunk), k1 = min(m, k0 + A.lam_chunk);
+  unsigned int round = A.round0;
+  auto lown = [&](int64_t k) { return (int)((k / A.lam_chunk) / A.nbr); };
+  auto pown = [&](int s) { return D.owner[s]; };
   auto own_idx = [&](int s, int pos) { return D.vec_off[s] + (int64_t)D.Ti[s] * TS + pos; };
   auto pcf = [&](int64_t g) { return pc_get(A, g); };
-  int64_t hoff = 0;
+  // partner patch of b position bb (other endpoint of its multiplier)
+  auto ppatch = [&](int64_t bb) {
+    const int k = D.b_lam[bb];
+    return D.b_sign[bb] > 0 ? D.lam_patch_m[k] : D.lam_patch_p[k];
+  };
+  // item ranges of this rank
+#define RANGE(name) const int name##_b = A.off_##name[me], name##_e = A.off_##name[me + 1]
+  RANGE(p1);
+  RANGE(p5);
+  RANGE(sy);
+  RANGE(pc);
+  RANGE(fw);
+  RANGE(bw);
+  RANGE(bwc);
+  RANGE(rhs);
+#undef RANGE
+  int64_t hoff = A.hist_off;
   int total_status = 0;
 
   for (int step = 0; step < A.nsteps; ++step) {
@@ -482,42 +543,45 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     int it = 0;
     SSTAMP(0);
     // ---- R1 rhs ----
-    for (int i = b; i < A.n_rhs; i += NB) rhs_item(D, A, A.it_rhs[i].x, A.it_rhs[i].y, t, sm);
-    grid_barrier(bar, bar_target);
+    for (int i = rhs_b + bl; i < rhs_e; i += NB) rhs_item(D, A, me, A.it_rhs[i].x, A.it_rhs[i].y, t, sm);
+    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
     SSTAMP(1);
     // ---- R2 forward (conductors) ----
-    for (int i = b; i < A.n_fw; i += NB) fw_item(D, A.it_fw[i].x, A.it_fw[i].y, A.F, A.Z, sm);
-    grid_barrier(bar, bar_target);
+    for (int i = fw_b + bl; i < fw_e; i += NB) fw_item(D, A.it_fw[i].x, A.it_fw[i].y, A.F[me], A.Z[me], sm);
+    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
     SSTAMP(2);
     // ---- R3 p0 = S_pp^-1 sum N^T Z_p ----
-    for (int i = b; i < A.n_pc; i += NB) pc_item(D, A, A.it_pc[i].x, A.it_pc[i].y, A.Z, nullptr, sm);
-    grid_barrier(bar, bar_target);
+    for (int i = pc_b + bl; i < pc_e; i += NB)
+      pc_item(D, A, A.Sinv[me], A.it_pc[i].x, A.it_pc[i].y,
+              [&](int e) { return ldcg(A.Z[pown(D.coarse_patch[e])] + D.coarse_idx[e]); }, A.Ppart[me], sm);
+    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
     SSTAMP(3);
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
-    for (int i = b; i < A.n_p5; i += NB)
-      p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.Z, pcf, [&](int, int64_t, int) { return 0.0; }, A.Y, sm, red);
-    grid_barrier(bar, bar_target);
+    for (int i = p5_b + bl; i < p5_e; i += NB)
+      p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.Z[me], pcf, [&](int, int64_t, int) { return 0.0; }, A.Y[me], sm, red);
+    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
     SSTAMP(4);
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
+    double rho0;
     {
       double loc = 0.0;
-      for (int i = b; i < A.n_sy; i += NB)
-        loc += symv_item(D, A.PW, A.it_sy[i].x, A.it_sy[i].y,
+      for (int i = sy_b + bl; i < sy_e; i += NB)
+        loc += symv_item(D, A.PW[me], A.it_sy[i].x, A.it_sy[i].y,
                          [&](int s, int64_t bb, int pos) {
-                           return D.b_aown[bb] * (ldcg(A.Y + own_idx(s, pos)) - ldcg(A.Y + D.b_part[bb]));
+                           return D.b_aown[bb] *
+                                  (ldcg(A.Y[me] + own_idx(s, pos)) - ldcg(A.Y[pown(ppatch(bb))] + D.b_part[bb]));
                          },
                          sm, red);
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-        A.r[0][k] = ldcg(A.Y + D.lam_idx_p[k]) - ldcg(A.Y + D.lam_idx_m[k]);
-        A.pk[0][k] = 0.0;
-        A.lam[k] = 0.0;
+        A.r[0][me][k] = ldcg(A.Y[pown(D.lam_patch_p[k])] + D.lam_idx_p[k]) -
+                        ldcg(A.Y[pown(D.lam_patch_m[k])] + D.lam_idx_m[k]);
+        A.pk[0][me][k] = 0.0;
+        A.lam[me][k] = 0.0;
       }
-      if (threadIdx.x == 0) A.partB[b] = loc;
+      rho0 = grid_barrier(A, me, bl, round, true, loc, &bcast);
     }
-    grid_barrier(bar, bar_target);
     SSTAMP(5);
-    const double rho0 = sum_partials(A.partB, NB, red);
-    if (b == 0 && threadIdx.x == 0) A.hist[hoff] = 1.0;
+    if (me == 0 && bl == 0 && threadIdx.x == 0) A.hist[0][hoff] = 1.0;
     int status = 0;  // 0 running, 1 converged, 2 failed
     double rz = rho0;
     if (!(rho0 >= 0.0)) status = 2;
@@ -526,58 +590,66 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     int rp = 0, pp = 0;
     while (status == 0) {
       TSTAMP(0);
-      const double* pprev = A.pk[pp];
-      double* pcur = A.pk[pp ^ 1];
-      // P1
+      double* const* pprev = A.pk[pp];
+      double* pcur = A.pk[pp ^ 1][me];
+      // P1: p = z + beta p_prev on the fly; v = B^T p; w = X_bb v, -g = -Phi^T v; owners store p
       auto vnew = [&](int s, int64_t bb, int pos) {
-        return D.b_aown[bb] * ldcg(A.PW + own_idx(s, pos)) + D.b_apart[bb] * ldcg(A.PW + D.b_part[bb]) +
-               D.b_sign[bb] * beta * ldcg(pprev + D.b_lam[bb]);
+        const int k = D.b_lam[bb];
+        return D.b_aown[bb] * ldcg(A.PW[me] + own_idx(s, pos)) +
+               D.b_apart[bb] * ldcg(A.PW[pown(ppatch(bb))] + D.b_part[bb]) +
+               D.b_sign[bb] * beta * ldcg(pprev[lown(k)] + k);
       };
-      for (int i = b; i < A.n_p1; i += NB) p1_item(D, A.it_p1[i].x, A.it_p1[i].y, vnew, A.XW, sm);
+      for (int i = p1_b + bl; i < p1_e; i += NB) p1_item(D, A.it_p1[i].x, A.it_p1[i].y, vnew, A.XW[me], sm);
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
-        pcur[k] = D.wplus[k] * ldcg(A.PW + D.lam_idx_p[k]) - D.wminus[k] * ldcg(A.PW + D.lam_idx_m[k]) +
-                  beta * ldcg(pprev + k);
-      grid_barrier(bar, bar_target);
+        pcur[k] = D.wplus[k] * ldcg(A.PW[pown(D.lam_patch_p[k])] + D.lam_idx_p[k]) -
+                  D.wminus[k] * ldcg(A.PW[pown(D.lam_patch_m[k])] + D.lam_idx_m[k]) + beta * ldcg(pprev[me] + k);
+      grid_barrier(A, me, bl, round, false, 0.0, &bcast);
       TSTAMP(1);
       // PC
-      for (int i = b; i < A.n_pc; i += NB) pc_item(D, A, A.it_pc[i].x, A.it_pc[i].y, A.XW, nullptr, sm);
-      grid_barrier(bar, bar_target);
+      for (int i = pc_b + bl; i < pc_e; i += NB)
+        pc_item(D, A, A.Sinv[me], A.it_pc[i].x, A.it_pc[i].y,
+                [&](int e) { return ldcg(A.XW[pown(D.coarse_patch[e])] + D.coarse_idx[e]); }, A.Ppart[me], sm);
+      grid_barrier(A, me, bl, round, false, 0.0, &bcast);
       TSTAMP(2);
-      // P5
+      // P5 (+ partial p^T F p)
+      double* const* pcurt = A.pk[pp ^ 1];
+      double pq;
       {
         double loc = 0.0;
-        for (int i = b; i < A.n_p5; i += NB)
-          loc += p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.XW, pcf,
-                         [&](int, int64_t bb, int) { return D.b_sign[bb] * ldcg(pcur + D.b_lam[bb]); }, A.Y, sm, red);
-        if (threadIdx.x == 0) A.partA[b] = loc;
+        for (int i = p5_b + bl; i < p5_e; i += NB)
+          loc += p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.XW[me], pcf,
+                         [&](int, int64_t bb, int) {
+                           const int k = D.b_lam[bb];
+                           return D.b_sign[bb] * ldcg(pcurt[lown(k)] + k);
+                         },
+                         A.Y[me], sm, red);
+        pq = grid_barrier(A, me, bl, round, true, loc, &bcast);
       }
-      grid_barrier(bar, bar_target);
       TSTAMP(3);
-      const double pq = sum_partials(A.partA, NB, red);
       if (!(pq > 0.0)) { status = 2; break; }  // lost positive curvature (uniform)
       const double alpha = rho / pq;
-      const double* rc = A.r[rp];
-      double* rn = A.r[rp ^ 1];
+      double* const* rc = A.r[rp];
+      double* rn = A.r[rp ^ 1][me];
       auto unew = [&](int s, int64_t bb, int pos) {
-        return D.b_aown[bb] * (D.b_sign[bb] * ldcg(rc + D.b_lam[bb]) -
-                               alpha * (ldcg(A.Y + own_idx(s, pos)) - ldcg(A.Y + D.b_part[bb])));
+        const int k = D.b_lam[bb];
+        return D.b_aown[bb] * (D.b_sign[bb] * ldcg(rc[lown(k)] + k) -
+                               alpha * (ldcg(A.Y[me] + own_idx(s, pos)) - ldcg(A.Y[pown(ppatch(bb))] + D.b_part[bb])));
       };
-      // P7
+      // P7 (+ partial r^T z)
       {
         for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-          A.lam[k] += alpha * ldcg(pcur + k);
-          rn[k] = ldcg(rc + k) - alpha * (ldcg(A.Y + D.lam_idx_p[k]) - ldcg(A.Y + D.lam_idx_m[k]));
+          A.lam[me][k] += alpha * ldcg(pcur + k);
+          rn[k] = ldcg(rc[me] + k) - alpha * (ldcg(A.Y[pown(D.lam_patch_p[k])] + D.lam_idx_p[k]) -
+                                              ldcg(A.Y[pown(D.lam_patch_m[k])] + D.lam_idx_m[k]));
         }
         double loc = 0.0;
-        for (int i = b; i < A.n_sy; i += NB) loc += symv_item(D, A.PW, A.it_sy[i].x, A.it_sy[i].y, unew, sm, red);
-        if (threadIdx.x == 0) A.partB[b] = loc;
+        for (int i = sy_b + bl; i < sy_e; i += NB) loc += symv_item(D, A.PW[me], A.it_sy[i].x, A.it_sy[i].y, unew, sm, red);
+        rz = grid_barrier(A, me, bl, round, true, loc, &bcast);
       }
-      grid_barrier(bar, bar_target);
       TSTAMP(4);
-      rz = sum_partials(A.partB, NB, red);
       ++it;
       const double rel = sqrt(fmax(rz, 0.0) / rho0);
-      if (b == 0 && threadIdx.x == 0) A.hist[hoff + it] = rel;
+      if (me == 0 && bl == 0 && threadIdx.x == 0) A.hist[0][hoff + it] = rel;
       rp ^= 1;
       pp ^= 1;
       if (rel <= A.rtol) status = 1;
@@ -585,17 +657,17 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       beta = rz / rho;
       rho = rz;
     }
-    if (b == 0 && threadIdx.x == 0) {
-      A.iters[A.step0 + step] = it;
-      A.st->iter = it;
-      A.st->rho0 = rho0;
-      A.st->rz = rz;
+    if (bl == 0 && threadIdx.x == 0) {
+      A.iters[me][A.step0 + step] = it;
+      A.st[me]->iter = it;
+      A.st[me]->rho0 = rho0;
+      A.st[me]->rz = rz;
     }
     if (status == 2) {  // uniform: report and stop the remaining steps
-      if (b == 0 && threadIdx.x == 0) {
-        A.st->failed = 1;
-        A.st->nan = !(rz == rz);
-        A.st->rp = A.step0 + step;  // failing step index
+      if (bl == 0 && threadIdx.x == 0) {
+        A.st[me]->failed = 1;
+        A.st[me]->nan = !(rz == rz);
+        A.st[me]->rp = A.step0 + step;  // failing step index
       }
       total_status = 2;
       break;
@@ -603,34 +675,47 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     hoff += it + 1;
     SSTAMP(6);
     // ---- E1 v = B^T lambda ; w, -Phi^T v ----
-    for (int i = b; i < A.n_p1; i += NB)
+    for (int i = p1_b + bl; i < p1_e; i += NB)
       p1_item(D, A.it_p1[i].x, A.it_p1[i].y,
-              [&](int, int64_t bb, int) { return D.b_sign[bb] * ldcg(A.lam + D.b_lam[bb]); }, A.XW, sm);
-    grid_barrier(bar, bar_target);
+              [&](int, int64_t bb, int) {
+                const int k = D.b_lam[bb];
+                return D.b_sign[bb] * ldcg(A.lam[lown(k)] + k);
+              },
+              A.XW[me], sm);
+    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
     SSTAMP(7);
     // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
-    for (int i = b; i < A.n_pc; i += NB) pc_item(D, A, A.it_pc[i].x, A.it_pc[i].y, A.Z, A.XW, sm);
-    grid_barrier(bar, bar_target);
+    for (int i = pc_b + bl; i < pc_e; i += NB)
+      pc_item(D, A, A.Sinv[me], A.it_pc[i].x, A.it_pc[i].y,
+              [&](int e) {
+                const int o = pown(D.coarse_patch[e]);
+                return ldcg(A.Z[o] + D.coarse_idx[e]) - ldcg(A.XW[o] + D.coarse_idx[e]);
+              },
+              A.Ppart[me], sm);
+    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
     SSTAMP(8);
     // ---- E3 a_r = X_rr^T (Z_r - [0; w_b]) - Phi N p, a_p = N p ----
     // insulator coefficients feed no later step (no mass term): recover them only at the last step
     {
       const bool last = (step == A.nsteps - 1);
-      const int nbw = last ? A.n_bw : A.n_bwc;
       const int2* itb = last ? A.it_bw : A.it_bwc;
-      for (int i = b; i < nbw; i += NB) bw_item(D, itb[i].x, itb[i].y, A.Z, A.XW, pcf, A.a_loc, A.G.nloc, sm);
+      const int ib = last ? bw_b : bwc_b, ie = last ? bw_e : bwc_e;
+      for (int i = ib + bl; i < ie; i += NB)
+        bw_item(D, itb[i].x, itb[i].y, A.Z[me], A.XW[me], pcf, A.a_loc[me], A.G.nloc, sm);
     }
-    grid_barrier(bar, bar_target);
+    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
     SSTAMP(9);
   }
-  if (b == 0 && threadIdx.x == 0) {
-    A.st->done = 1;
-    if (total_status != 2) A.st->failed = 0;
-    A.st->counter[2] = (unsigned int)hoff;  // history length written
+  if (bl == 0 && threadIdx.x == 0) {
+    A.st[me]->done = 1;
+    if (total_status != 2) A.st[me]->failed = 0;
+    A.st[me]->counter[2] = (unsigned int)(hoff - A.hist_off);  // history length written
+    A.st[me]->counter[3] = round;                               // barrier rounds after this launch
   }
 }
 
-// ---- standalone item kernels (setup precompute, F-apply benchmark): one item per block ----
+// ---- standalone item kernels (setup precompute, F-apply benchmark), single rank: one item
+// per block over the given item range.
 __global__ void __launch_bounds__(NTHR) k_fw(DevPlan D, const int2* items, int n, const double* Fv, double* Zv) {
   extern __shared__ double sm[];
   if (blockIdx.x >= n) return;
@@ -643,21 +728,24 @@ __global__ void __launch_bounds__(NTHR) k_p1_lam(DevPlan D, const int2* items, i
   p1_item(D, items[blockIdx.x].x, items[blockIdx.x].y,
           [&](int, int64_t bb, int) { return D.b_sign[bb] * lam[D.b_lam[bb]]; }, XW, sm);
 }
-__global__ void __launch_bounds__(NTHR) k_pc(DevPlan D, StepArgs A, const double* src1, const double* src2) {
+__global__ void __launch_bounds__(NTHR) k_pc(DevPlan D, StepArgs A, const int2* items, int n, const double* src,
+                                             double* Ppart) {
   extern __shared__ double sm[];
-  if (blockIdx.x >= A.n_pc) return;
-  pc_item(D, A, A.it_pc[blockIdx.x].x, A.it_pc[blockIdx.x].y, src1, src2, sm);
+  if (blockIdx.x >= n) return;
+  pc_item(D, A, A.Sinv[0], items[blockIdx.x].x, items[blockIdx.x].y, [&](int e) { return ldcg(src + D.coarse_idx[e]); },
+          Ppart, sm);
 }
-__global__ void k_pc_sum(DevPlan D, StepArgs A) {
+__global__ void k_pc_sum(DevPlan D, StepArgs A, double* Pc) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D.nc; g += (int64_t)gridDim.x * blockDim.x)
-    A.Pc[g] = pc_get(A, g);
+    Pc[g] = pc_get(A, g);
 }
-__global__ void __launch_bounds__(NTHR) k_p5(DevPlan D, StepArgs A, const double* W) {
+__global__ void __launch_bounds__(NTHR) k_p5(DevPlan D, const int2* items, int n, const double* W, const double* Pc,
+                                             double* Y) {
   extern __shared__ double sm[];
   __shared__ double red[NTHR];
-  if (blockIdx.x >= A.n_p5) return;
-  p5_item(D, A.it_p5[blockIdx.x].x, A.it_p5[blockIdx.x].y, W, [&](int64_t g) { return ldcg(A.Pc + g); },
-          [&](int, int64_t, int) { return 0.0; }, A.Y, sm, red);
+  if (blockIdx.x >= n) return;
+  p5_item(D, items[blockIdx.x].x, items[blockIdx.x].y, W, [&](int64_t g) { return ldcg(Pc + g); },
+          [&](int, int64_t, int) { return 0.0; }, Y, sm, red);
 }
 // q = B y (F-apply benchmark output)
 __global__ void k_jump(DevPlan D, const double* Y, double* q) {

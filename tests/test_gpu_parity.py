@@ -179,3 +179,26 @@ def test_full_size_local_equations(tcg, name):
         res = (W @ a - f)[ri]
         assert np.max(np.abs(res)) <= 1e-7 * max(np.max(np.abs(f)), np.max(np.abs(W @ a)))
     s.close()
+
+
+@pytest.mark.parametrize("vranks", [2, 3, 4])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_virtual_ranks_match_single_rank(tcg, name, vranks):
+    """The sharded dataflow (patches owned by ranks, remote reads through per-rank pointer
+    tables, two-level barrier with fused fixed-order reductions) emulated as `vranks` ranks in
+    one cooperative grid equals the single-rank solve (reduction order differs -> rounding)."""
+    pr = workloads.get(name)
+    steps = 3
+    a1, a0, it1, h1, _ = run_gpu(tcg, pr, steps)
+    s = tcg.Solver()
+    s.set_virtual_ranks(vranks)
+    s.configure(pr)
+    s.setup()
+    s.step(steps)
+    b1 = s.coefficients(1)
+    it2, _, _ = s.history()
+    inf = s.info()
+    s.close()
+    assert inf["world"] == vranks
+    assert np.linalg.norm(b1 - a1) <= 1e-11 * np.linalg.norm(a1)
+    assert np.all(np.abs(np.array(it2) - np.array(it1)) <= 1)

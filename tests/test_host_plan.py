@@ -101,13 +101,16 @@ def test_plan_matches_oracle(tcg, pr, order):
     s.close()
 
 
-def test_sharding_x_slabs(tcg):
+def test_sharding_x_slabs_virtual(tcg):
     """Patch -> rank map: contiguous x-slabs (each rank has <= 2 neighbouring ranks)."""
     pr = workloads.cfg2()
     for world in (1, 2, 4):
-        s = tcg.Solver(world=1)
+        s = tcg.Solver()
+        s.set_virtual_ranks(world)
         s.configure(pr)
         s.plan()
         r = s.plan_array(tcg.PLAN_RANK_OF_PATCH, pr.n_patches)
-        assert np.all(r == 0)
+        ix = np.arange(pr.n_patches) % pr.npatch[0]
+        assert np.array_equal(r, (ix * world) // pr.npatch[0])
+        assert set(np.unique(r)) == set(range(min(world, pr.npatch[0])))
         s.close()
