@@ -763,7 +763,8 @@ static tcg_status do_setup(tcg_ctx* h) {
     for (int c = 0; c < 3; ++c) maxcomp = std::max(maxcomp, (size_t)pl.comp_dim(c, 0) * pl.comp_dim(c, 1) * pl.comp_dim(c, 2));
     fwb = std::max(fwb, 2 * maxcomp);
     h->smem_pcg = sizeof(double) * std::max(std::max(p1, p5), std::max(std::max(pcs, fwb), syv));
-    TRY(set_smem(h, (const void*)k_steps, h->smem_pcg));
+    TRY(set_smem(h, (const void*)k_steps<false>, h->smem_pcg));
+    TRY(set_smem(h, (const void*)k_steps<true>, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_fw, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_p1_lam, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_pc, h->smem_pcg));
@@ -776,7 +777,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_update, 2 * TS * SPAD * sizeof(double)));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps, NTHR, h->smem_pcg));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps<true>, NTHR, h->smem_pcg));
     if (occ < 1) return fail(h, TCG_ECUDA, "persistent stepper kernel does not fit on an SM");
     const char* ev = getenv("TCG_PCG_BLOCKS_PER_SM");
     int per = ev ? std::max(1, atoi(ev)) : 2;
@@ -1038,7 +1039,8 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   void* args[] = {(void*)&D, (void*)&A};
   const int grid = h->nbr * (int)h->rd.size();
   prof_begin(h, 7);
-  CK(cudaLaunchCooperativeKernel((const void*)k_steps, dim3(grid), dim3(NTHR), args, h->smem_pcg, h->stream));
+  const void* fn = (h->nranks > 1) ? (const void*)k_steps<true> : (const void*)k_steps<false>;
+  CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NTHR), args, h->smem_pcg, h->stream));
   ++h->nlaunch;
   prof_end(h, 7);
   RankDev& R0 = h->rd[0];

@@ -389,28 +389,61 @@ __device__ __forceinline__ void fence_scope(int sys) {
   else __threadfence();
 }
 
-// Two-level barrier over every block of every rank, with an optional fused fixed-order sum.
-// Blocks of a rank arrive on the rank's counter; the last arriving block (the leader) sums
-// the rank's per-block partials in block order, publishes the rank partial, arrives on rank
-// 0's global counter and waits for all rank leaders, then releases its rank. After the
-// barrier every block sums the rank partials in rank order -> identical totals everywhere.
-// `round` counts barriers (identical sequence in every block of every rank).
+// Barrier over every block of every rank, with an optional fused fixed-order sum of one
+// value per block. `round` counts barriers (the same sequence in every block of every rank;
+// the counters are monotone across launches).
+//  * one rank: every block arrives on the rank counter and polls it; the sum is formed by
+//    every block from the per-block partials in block order (lane-strided + xor butterfly).
+//  * several ranks: two levels. The last arriving block of a rank (its leader) sums the
+//    rank's partials in block order, publishes the rank partial, arrives on rank 0's global
+//    counter (system scope for real GPUs), waits for all rank leaders and releases its rank;
+//    every block then sums the rank partials in rank order. Identical totals everywhere.
 __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& round, bool reduce, double value,
                                double* bcast) {
+  __shared__ int s_leader;
   __syncthreads();
   ++round;
   const int sys = A.sys_scope;
+  BarMem* mine = A.bar[me];
+  if (A.nranks == 1) {
+    if (threadIdx.x == 0) {
+      if (reduce) A.partials[me][bl] = value;
+      __threadfence();
+      atomicAdd(&mine->local_count, 1u);
+      while ((int)(ld_acquire_u32(&mine->local_count, 0) - round * (unsigned int)A.nbr) < 0) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    double total = 0.0;
+    if (reduce) {
+      if (threadIdx.x < 32) {
+        double t = 0.0;
+        for (int j = threadIdx.x; j < A.nbr; j += 32) t += __ldcg(A.partials[me] + j);
+        t = warp_sum(t);
+        if (threadIdx.x == 0) *bcast = t;
+      }
+      __syncthreads();
+      total = *bcast;
+      __syncthreads();
+    }
+    return total;
+  }
   if (threadIdx.x == 0) {
-    BarMem* mine = A.bar[me];
     if (reduce) A.partials[me][bl] = value;
     fence_scope(sys);
     const unsigned int old = atomicAdd(&mine->local_count, 1u);
-    if (old + 1 == round * (unsigned int)A.nbr) {  // leader of this rank
-      if (reduce) {
-        double t = 0.0;
-        for (int j = 0; j < A.nbr; ++j) t += __ldcg(A.partials[me] + j);
-        mine->rank_part[round & 1] = t;
-      }
+    s_leader = (old + 1 == round * (unsigned int)A.nbr);
+  }
+  __syncthreads();
+  if (s_leader) {
+    if (reduce && threadIdx.x < 32) {
+      double t = 0.0;
+      for (int j = threadIdx.x; j < A.nbr; j += 32) t += __ldcg(A.partials[me] + j);
+      t = warp_sum(t);
+      if (threadIdx.x == 0) mine->rank_part[round & 1] = t;
+    }
+    if (threadIdx.x == 0) {
       fence_scope(sys);
       unsigned int* gc = &A.bar[0]->global_count;
       if (sys) atomicAdd_system(gc, 1u);
@@ -419,10 +452,12 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
       }
       fence_scope(sys);
       atomicExch(&mine->local_gen, round);
-    } else {
-      while ((int)(ld_acquire_u32(&mine->local_gen, 0) - round) < 0) {
-      }
     }
+  } else if (threadIdx.x == 0) {
+    while ((int)(ld_acquire_u32(&mine->local_gen, 0) - round) < 0) {
+    }
+  }
+  if (threadIdx.x == 0) {
     fence_scope(sys);
     if (reduce) {
       double t = 0.0;
@@ -504,23 +539,26 @@ __device__ void rhs_item(const DevPlan& D, const StepArgs& A, int me, int s, int
 // all ranks of the job. Control flow depends only on values every block of every rank
 // computes identically, so all blocks run the same sequence of barriers.
 // =======================================================================================
+template <bool MULTI>
 __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   extern __shared__ double sm[];
   __shared__ double red[NTHR];
   __shared__ double bcast;
-  const int me = A.rank_base + (int)blockIdx.x / A.nbr;  // this block's rank
-  const int bl = (int)blockIdx.x % A.nbr;                 // block index within the rank
+  // MULTI = false: one rank, every owner lookup folds to rank 0 at compile time
+  const int me = MULTI ? A.rank_base + (int)blockIdx.x / A.nbr : 0;  // this block's rank
+  const int bl = MULTI ? (int)blockIdx.x % A.nbr : (int)blockIdx.x;   // block index within the rank
   const int NB = A.nbr;
   const int64_t m = D.m;
   const int64_t gb = (int64_t)me * A.nbr + bl;
   const int64_t k0 = min(m, gb * A.lam_chunk), k1 = min(m, k0 + A.lam_chunk);
   unsigned int round = A.round0;
-  auto lown = [&](int64_t k) { return (int)((k / A.lam_chunk) / A.nbr); };
-  auto pown = [&](int s) { return D.owner[s]; };
+  auto lown = [&](int64_t k) { return MULTI ? ((int)k / (int)A.lam_chunk) / A.nbr : 0; };
+  auto pown = [&](int s) { return MULTI ? D.owner[s] : 0; };
   auto own_idx = [&](int s, int pos) { return D.vec_off[s] + (int64_t)D.Ti[s] * TS + pos; };
   auto pcf = [&](int64_t g) { return pc_get(A, g); };
   // partner patch of b position bb (other endpoint of its multiplier)
   auto ppatch = [&](int64_t bb) {
+    if (!MULTI) return 0;
     const int k = D.b_lam[bb];
     return D.b_sign[bb] > 0 ? D.lam_patch_m[k] : D.lam_patch_p[k];
   };
