@@ -10,8 +10,10 @@ timed with CUDA events on the library's stream, L2 flushed (256 MiB write) betwe
 timed steps outside the event pairs, max over ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl reference]
-Under torchrun (N>1) every rank solves its own replica (sharded NCCL
-solve is the next step), so value = N * n_t * K / max_rank_time, scaling "weak".
+Under torchrun (N>1) the patches of ONE solve are sharded over the N GPUs (x-slabs; ranks
+read interface/coarse/lambda values from peer memory over NVLink inside one persistent
+kernel per rank; NCCL only bootstraps), value = n_t * K / max_rank_time, scaling "strong".
+TCG_BENCH_REPLICAS=1 runs N independent replicas instead (scaling "weak").
 """
 from __future__ import annotations
 
@@ -189,7 +191,16 @@ def main():
     torch.cuda.set_device(local)
     import paper_2510_23446_b200 as tcg
     stream = torch.cuda.Stream()
-    s = tcg.Solver(device=local, stream=stream.cuda_stream)
+    sharded = world > 1 and os.environ.get("TCG_BENCH_REPLICAS", "0") != "1"
+
+    def make_solver(strm):
+        if not sharded:
+            return tcg.Solver(device=local, stream=strm)
+        obj = [tcg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return tcg.Solver(device=local, rank=rank, world=world, nccl_id=obj[0], stream=strm)
+
+    s = make_solver(stream.cuda_stream)
     s.configure(prob)
     s.setup()
     n_t = prob.n_steps
@@ -227,7 +238,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
     max_ms = float(t.item())
-    value = world * n_t * args.steps / (max_ms / 1000.0)
+    # sharded: one solve over all GPUs (strong scaling); replicas: one solve per GPU
+    value = (1 if sharded else world) * n_t * args.steps / (max_ms / 1000.0)
     inf = s.info()
 
     # ---- roofline of the dominant kernel (separate instrumented passes) ----
@@ -280,7 +292,7 @@ def main():
         for _ in range(args.e2e_steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            u = tcg.Solver(device=local)
+            u = make_solver(None)
             u.configure(prob)
             u.setup()
             u.step(n_t)
@@ -289,7 +301,7 @@ def main():
             u.close()
             tt.append(time.perf_counter() - t0)
             h2d, d2h = ii["h2d_bytes"], ii["d2h_bytes"]
-        e2e_val = world * n_t / float(np.median(tt))
+        e2e_val = (1 if sharded else world) * n_t / float(np.median(tt))
         e2e = {"value": e2e_val, "unit": "steps/s", "h2d_bytes_per_step": h2d / n_t, "d2h_bytes_per_step": d2h / n_t,
                "note": "per pass: create + host arrays + setup (plan, H2D, assembly, factorisation) + n_t steps + "
                        "coefficient readback; wall clock, median of %d" % args.e2e_steps}
@@ -306,10 +318,13 @@ def main():
         iters_per_step = inf["total_iters"] / max(inf["steps_done"], 1)
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": config_desc(prob), "l2": "flushed between timed steps (256 MiB write)",
-                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "parallelism": (f"patch-sharded over {world} GPUs (x-slabs; NVLink peer memory, one "
+                                       "persistent kernel per rank)") if sharded else
+                                      ("replicas" if world > 1 else "single GPU"),
                        "patches": prob.n_patches, "m": inf["m"], "n_c": inf["n_c"]},
             "pcg_iters_per_s": value * iters_per_step,
             "pcg_iters_per_step": iters_per_step,

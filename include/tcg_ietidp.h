@@ -110,6 +110,10 @@ typedef struct tcg_info {
 tcg_status tcg_create(tcg_handle* out, int device, int rank, int world,
                       const unsigned char* nccl_id, void* cuda_stream);
 
+/* Fill out[128] with a fresh ncclUniqueId (rank 0 of a multi-GPU job calls this and
+ * broadcasts the bytes to the other ranks, e.g. through torch.distributed). */
+tcg_status tcg_nccl_unique_id(unsigned char* out);
+
 /* Testing/emulation: shard the solve over `vranks` virtual ranks that all live on this
  * process's GPU (separate allocations, one cooperative grid, the same peer-table dataflow and
  * two-level barrier as a multi-GPU job). Requires world == 1; call before tcg_plan. */

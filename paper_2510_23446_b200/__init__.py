@@ -22,7 +22,7 @@ PLAN_EDGE_CLASS, PLAN_EDGE_REGION, PLAN_TREE, PLAN_PART, PLAN_PATCH_COUNTS, PLAN
 
 EXPORTS = ["tcg_create", "tcg_set_patches", "tcg_set_materials", "tcg_set_source", "tcg_set_time", "tcg_set_solver",
            "tcg_plan", "tcg_get_plan", "tcg_setup", "tcg_refactor", "tcg_step", "tcg_get_coefficients", "tcg_get_history",
-           "tcg_get_info", "tcg_bench_fapply", "tcg_set_profile", "tcg_set_virtual_ranks", "tcg_last_error",
+           "tcg_get_info", "tcg_bench_fapply", "tcg_set_profile", "tcg_set_virtual_ranks", "tcg_nccl_unique_id", "tcg_last_error",
            "tcg_destroy"]
 
 
@@ -75,6 +75,7 @@ def lib():
     L.tcg_bench_fapply.argtypes = [vp, C.c_int, dp]
     L.tcg_set_profile.argtypes = [vp, C.c_int]
     L.tcg_set_virtual_ranks.argtypes = [vp, C.c_int]
+    L.tcg_nccl_unique_id.argtypes = [C.c_char_p]
     L.tcg_last_error.argtypes = [vp]
     L.tcg_last_error.restype = C.c_char_p
     L.tcg_destroy.argtypes = [vp]
@@ -88,6 +89,15 @@ def lib():
 
 def _dptr(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for a multi-GPU handle (rank 0 creates, all ranks pass it)."""
+    buf = C.create_string_buffer(128)
+    st = lib().tcg_nccl_unique_id(buf)
+    if st != TCG_OK:
+        raise TcgError(st, "ncclGetUniqueId failed")
+    return buf.raw
 
 
 class Solver:

@@ -44,6 +44,7 @@ enum { ncclSum = 0 };
 struct NcclApi {
   void* lib = nullptr;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
@@ -61,6 +62,7 @@ struct NcclApi {
       return false;
     }
     commInitRank = (decltype(commInitRank))dlsym(lib, "ncclCommInitRank");
+    getUniqueId = (decltype(getUniqueId))dlsym(lib, "ncclGetUniqueId");
     allGather = (decltype(allGather))dlsym(lib, "ncclAllGather");
     allReduce = (decltype(allReduce))dlsym(lib, "ncclAllReduce");
     commDestroy = (decltype(commDestroy))dlsym(lib, "ncclCommDestroy");
@@ -1102,6 +1104,16 @@ tcg_status tcg_create(tcg_handle* out, int device, int rank, int world, const un
   if (nccl_id) std::memcpy(h->nccl_id, nccl_id, 128);
   h->stream = static_cast<cudaStream_t>(cuda_stream);
   *out = h;
+  return TCG_OK;
+}
+
+tcg_status tcg_nccl_unique_id(unsigned char* out) {
+  if (!out) return TCG_EINVAL;
+  std::string e;
+  if (!g_nccl.load(e) || !g_nccl.getUniqueId) return TCG_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.getUniqueId(&id) != 0) return TCG_ENCCL;
+  std::memcpy(out, id.internal, 128);
   return TCG_OK;
 }
 

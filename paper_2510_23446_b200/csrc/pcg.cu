@@ -378,6 +378,8 @@ __device__ void bw_item(const DevPlan& D, int s, int J, const double* Zv, const 
   __syncthreads();
 }
 
+constexpr unsigned long long kBarrierTimeoutNs = 30ull * 1000000000ull;  // 30 s watchdog
+
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p, int sys) {
   unsigned int v;
   if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -410,7 +412,9 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
       if (reduce) A.partials[me][bl] = value;
       __threadfence();
       atomicAdd(&mine->local_count, 1u);
+      const unsigned long long t0 = gtimer();
       while ((int)(ld_acquire_u32(&mine->local_count, 0) - round * (unsigned int)A.nbr) < 0) {
+        if (gtimer() - t0 > kBarrierTimeoutNs) __trap();  // a missing block: fail, never hang
       }
       __threadfence();
     }
@@ -448,13 +452,17 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
       unsigned int* gc = &A.bar[0]->global_count;
       if (sys) atomicAdd_system(gc, 1u);
       else atomicAdd(gc, 1u);
+      const unsigned long long t0 = gtimer();
       while ((int)(ld_acquire_u32(gc, sys) - round * (unsigned int)A.nranks) < 0) {
+        if (gtimer() - t0 > kBarrierTimeoutNs) __trap();  // a missing rank: fail, never hang
       }
       fence_scope(sys);
       atomicExch(&mine->local_gen, round);
     }
   } else if (threadIdx.x == 0) {
+    const unsigned long long t0 = gtimer();
     while ((int)(ld_acquire_u32(&mine->local_gen, 0) - round) < 0) {
+      if (gtimer() - t0 > kBarrierTimeoutNs) __trap();
     }
   }
   if (threadIdx.x == 0) {
