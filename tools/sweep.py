@@ -1,0 +1,39 @@
+"""Per-config measurement sweep (single GPU): setup time, steps/s, iterations, algorithmic
+bandwidth of the stepper and its fraction of the measured HBM peak. Prints one JSON per config."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import workloads
+import paper_2510_23446_b200 as tcg
+
+peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
+for name in sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"]:
+    pr = workloads.get(name)
+    stream = torch.cuda.Stream()
+    t0 = time.time()
+    s = tcg.Solver(stream=stream.cuda_stream).configure(pr)
+    s.setup()
+    t_setup_wall = time.time() - t0
+    inf0 = s.info()
+    # warm pass, then timed pass (refactor + n_t steps), events on the library stream
+    s.refactor(); s.step(pr.n_steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream); s.refactor(); e1.record(stream); e1.synchronize(); ms_setup = e0.elapsed_time(e1)
+    s.set_profile(7)
+    e0.record(stream); s.step(pr.n_steps); e1.record(stream); e1.synchronize(); ms_steps = e0.elapsed_time(e1)
+    inf = s.info(); it, fr, _ = s.history()
+    bytes_launch = float(sum(k * (inf["bytes_fapply"] + inf["bytes_precond"]) + inf["bytes_step_fixed"] for k in it))
+    gbs = bytes_launch / (inf["prof_ms"] * 1e-3) / 1e9
+    out = {"config": name, "patches": pr.n_patches, "m": inf["m"], "n_c": inf["n_c"], "nr_max": inf["nr_max"],
+           "nb_max": inf["nb_max"], "device_GB": inf["device_bytes"] / 1e9,
+           "setup_ms": ms_setup, "setup_wall_s_first": t_setup_wall, "n_t": pr.n_steps,
+           "steps_ms": ms_steps, "pass_steps_per_s": pr.n_steps / ((ms_setup + ms_steps) * 1e-3),
+           "stepping_steps_per_s": pr.n_steps / (ms_steps * 1e-3), "iters_mean": float(np.mean(it)),
+           "iters_max": int(np.max(it)), "pcg_iters_per_s": float(np.sum(it)) / (ms_steps * 1e-3),
+           "final_relres_max": float(np.max(fr)), "k_steps_alg_GBps": gbs, "frac_of_measured_hbm": gbs / peak,
+           "factor_flops": inf["flops_factor"], "factor_TFLOPs": inf["flops_factor"] / (ms_setup * 1e-3) / 1e12}
+    print(json.dumps(out), flush=True)
+    s.close()
+    del s
+    torch.cuda.empty_cache()
