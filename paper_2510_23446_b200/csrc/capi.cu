@@ -121,7 +121,8 @@ struct tcg_ctx {
   std::string err;
 
   // device state
-  std::vector<void*> allocs;
+  std::vector<void*> allocs;       // cudaMalloc (multi-GPU: IPC-exportable)
+  std::vector<void*> pool_allocs;  // cudaMallocAsync from the retained default pool
   std::vector<void*> ipc_opened;
   int64_t device_bytes = 0;
   int nranks = 1;  // ranks of the job: world (real) or vranks (virtual)
@@ -176,9 +177,12 @@ struct tcg_ctx {
 
   ~tcg_ctx() { release(); }
   void release() {
-    if (!allocs.empty() || stream) cudaSetDevice(device);
+    if (!allocs.empty() || !pool_allocs.empty() || stream) cudaSetDevice(device);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     ipc_opened.clear();
+    for (void* p : pool_allocs) cudaFreeAsync(p, stream);
+    pool_allocs.clear();
+    if (stream) cudaStreamSynchronize(stream);
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
     if (h_st) cudaFreeHost(h_st);
@@ -225,13 +229,34 @@ tcg_status fail(tcg_ctx* h, tcg_status s, const std::string& msg) {
     if (s_ != TCG_OK) return s_; \
   } while (0)
 
+// Device allocations: single-process handles use the device's stream-ordered memory pool,
+// configured to keep freed memory (so re-creating a handle costs no driver allocations);
+// multi-GPU handles use cudaMalloc (their buffers are exported with CUDA IPC).
+void retain_pool(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 template <class T>
 tcg_status dalloc(tcg_ctx* h, T** out, size_t n) {
   size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, bytes);
+  cudaError_t e;
+  if (h->world == 1) {
+    retain_pool(h->device);
+    e = cudaMallocAsync(&p, bytes, h->stream);
+    if (e == cudaSuccess) h->pool_allocs.push_back(p);
+  } else {
+    e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) h->allocs.push_back(p);
+  }
   if (e != cudaSuccess) return fail(h, TCG_ENOMEM, std::string("cudaMalloc ") + std::to_string(bytes) + ": " + cudaGetErrorString(e));
-  h->allocs.push_back(p);
   h->device_bytes += (int64_t)bytes;
   *out = static_cast<T*>(p);
   return TCG_OK;
