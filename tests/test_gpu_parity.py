@@ -148,6 +148,80 @@ def test_refactor_resets(tcg):
     s.close()
 
 
+def _glued_ids(pr, s):
+    """Glued edge id of every local DOF of patch s (structured indexing, independent of both
+    the oracle's brute-force topology and the library's plan)."""
+    n = [e + pr.p for e in pr.elems]
+    N = [P * (nd - 1) + 1 for P, nd in zip(pr.npatch, n)]
+    ix, iy, iz = s % pr.npatch[0], (s // pr.npatch[0]) % pr.npatch[1], s // (pr.npatch[0] * pr.npatch[1])
+    off, out = 0, []
+    for c in range(3):
+        dims = [nd - (1 if d == c else 0) for d, nd in enumerate(n)]
+        edims = [Nd - (1 if d == c else 0) for d, Nd in enumerate(N)]
+        k, j, i = np.meshgrid(np.arange(dims[2]), np.arange(dims[1]), np.arange(dims[0]), indexing="ij")
+        gi, gj, gk = i + ix * (n[0] - 1), j + iy * (n[1] - 1), k + iz * (n[2] - 1)
+        out.append(off + (gi + edims[0] * (gj + edims[1] * gk)).ravel())
+        off += edims[0] * edims[1] * edims[2]
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("name,samples", [("cfg3", 3), ("cfg4", 3), ("cfg5", 2)])
+def test_full_size_properties(tcg, name, samples):
+    """BASELINE.json configs[2..4] at full size in the bench launch configuration, two steps,
+    checked by properties that hold at any size: (a) PCG reached rtol every step; (b) the two
+    local copies of every interface DOF agree (the jump B a_r = 0 the multipliers enforce, up to
+    the PCG tolerance); (c) on sampled patches, assembled independently by the oracle's element
+    loop, the interior rows of the step-2 equation W^ a2 = M a1/dt + phi(t2) j_S hold (no
+    multiplier or primal term acts there)."""
+    from oracle import assembly
+    pr = workloads.get(name)
+    s = tcg.Solver().configure(pr)
+    s.setup()
+    s.step(1)
+    a1 = s.coefficients(0)
+    s.step(1)
+    a2 = s.coefficients(0)
+    it, fr, _ = s.history()
+    part = s.plan_array(tcg.PLAN_PART, s.info()["n_edges"])
+    s.close()
+    assert np.all(fr <= pr.rtol)
+    P = pr.n_patches
+    nloc = len(a2) // P
+    gids = [_glued_ids(pr, p) for p in range(P)]
+    allg = np.concatenate(gids)
+    nown = np.bincount(allg, minlength=len(part))
+    # (b) interface continuity: max over b-edges of |copy_1 - copy_2| relative to max |a|
+    first = np.full(len(part), np.nan)
+    worst = 0.0
+    for p in range(P):
+        g = gids[p]
+        vals = a2[p * nloc:(p + 1) * nloc]
+        m = (part[g] == 2) & (nown[g] == 2)
+        seen = ~np.isnan(first[g]) & m
+        if seen.any():
+            worst = max(worst, float(np.max(np.abs(first[g][seen] - vals[seen]))))
+        newm = m & np.isnan(first[g])
+        first[g[newm]] = vals[newm]
+    assert worst <= 1e-6 * np.max(np.abs(a2)), worst
+    # (c) interior equations on sampled patches
+    rng = np.random.default_rng(1)
+    picks = list(rng.choice(np.nonzero(pr.sigma > 0)[0], 1)) + list(rng.choice(np.nonzero(pr.sigma == 0)[0], samples - 1))
+    t2 = 2 * pr.dt
+    for p in picks:
+        idx = (p % pr.npatch[0], (p // pr.npatch[0]) % pr.npatch[1], p // (pr.npatch[0] * pr.npatch[1]))
+        lo = [pr.lo[d] + (pr.hi[d] - pr.lo[d]) * idx[d] / pr.npatch[d] for d in range(3)]
+        hi = [pr.lo[d] + (pr.hi[d] - pr.lo[d]) * (idx[d] + 1) / pr.npatch[d] for d in range(3)]
+        sp = assembly.PatchSpace(pr.p, pr.elems, lo, hi)
+        K, M, jS = assembly.assemble_patch(sp, pr.nu[p], pr.sigma[p], pr.source)
+        x1, x2 = a1[p * nloc:(p + 1) * nloc], a2[p * nloc:(p + 1) * nloc]
+        f = M @ x1 / pr.dt + assembly.source_time_factor(pr.source, t2, pr.nu[p], pr.sigma[p]) * jS
+        lhs = (K + M / pr.dt) @ x2
+        g = gids[p]
+        rows = (part[g] == 2) & (nown[g] == 1)
+        scale = max(np.max(np.abs(f)), np.max(np.abs(lhs)))
+        assert np.max(np.abs((lhs - f)[rows])) <= 1e-7 * scale, (p, np.max(np.abs((lhs - f)[rows])), scale)
+
+
 @pytest.mark.parametrize("name", ["cfg3"])
 def test_full_size_local_equations(tcg, name):
     """BASELINE.json configs[2] at full size, first step, checked by properties the oracle can
