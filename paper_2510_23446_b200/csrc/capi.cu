@@ -929,7 +929,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dalloc(h, &h->a_all, (size_t)P * pl.nloc));
   }
   if (!h->h_st) CK(cudaMallocHost(&h->h_st, sizeof(PcgState)));
-  if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) TRY(dzero(h, &h->tstamp, 8 * 64 + 16));
+  if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) TRY(dzero(h, &h->tstamp, 8 * 64 + 16 + 8 * 4096));
   if (getenv("TCG_DEBUG_KEEP") && atoi(getenv("TCG_DEBUG_KEEP")) != 0) {
     TRY(dalloc(h, &h->dbgA, h->rd[0].A ? (size_t)oa[h->rd[0].r] : 1));
     TRY(dalloc(h, &h->dbgC, (size_t)tri_tiles(Tc) * TSZ));
@@ -1488,7 +1488,7 @@ tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t 
     n = tri_tiles(h->plan.pp[idx].Tb) * TSZ;
   } else if (what == 7) {
     if (!h->tstamp) return fail(h, TCG_ESTATE, "TCG_PHASE_TIMING not set");
-    std::vector<unsigned long long> ts(8 * 64 + 16);
+    std::vector<unsigned long long> ts(8 * 64 + 16 + 8 * 4096);
     CK(cudaMemcpy(ts.data(), h->tstamp, ts.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     for (auto v : ts) tmp.push_back((double)v);
   } else {

@@ -104,26 +104,36 @@ __device__ __forceinline__ const double* xtile(const DevPlan& D, int s, int I, i
   return D.Ar[D.owner[s]] + D.a_off[s] + tri_off(I, J);
 }
 
-// fixed-order block reduction of one value per thread
+// fixed-order block reduction of one value per thread: xor-butterfly warp sums (lane 0's
+// value), then the 8 warp sums in warp order. Every thread returns the same value.
 __device__ __forceinline__ double block_sum(double local, double* red) {
-  red[threadIdx.x] = local;
+  const double w = warp_sum(local);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
   __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  const double r = red[0];
+  double r = 0.0;
+#pragma unroll
+  for (int i = 0; i < NTHR / 32; ++i) r += red[i];
   __syncthreads();
   return r;
 }
 
-// Coarse solution entry g from the PC chunk partials (fixed order), read on the rank that
-// owns coarse row block g/64.
+// Coarse solution entry g from the PC chunk partials (fixed chunk order), read on the rank
+// that owns coarse row block g/64. Loads are issued 4 at a time, summed in chunk order.
+template <bool MULTI>
 __device__ __forceinline__ double pc_get(const StepArgs& A, int64_t g) {
   const int I = (int)(g >> 6);
-  const double* p = A.Ppart[A.crow_owner[I]] + ((int64_t)I * A.maxch) * TS + (g & 63);
+  const double* p = A.Ppart[MULTI ? A.crow_owner[I] : 0] + ((int64_t)I * A.maxch) * TS + (g & 63);
   double v = 0.0;
-  for (int c = 0; c < A.maxch; ++c) v += ldcg(p + (int64_t)c * TS);
+  int c = 0;
+  for (; c + 4 <= A.maxch; c += 4) {
+    const double a0 = ldcg(p + (int64_t)c * TS), a1 = ldcg(p + (int64_t)(c + 1) * TS),
+                 a2 = ldcg(p + (int64_t)(c + 2) * TS), a3 = ldcg(p + (int64_t)(c + 3) * TS);
+    v += a0;
+    v += a1;
+    v += a2;
+    v += a3;
+  }
+  for (; c < A.maxch; ++c) v += ldcg(p + (int64_t)c * TS);
   return v;
 }
 
@@ -230,15 +240,20 @@ __device__ void pc_item(const DevPlan& D, const StepArgs& A, const double* Sinv,
 
 // ---- P5 / R4: y_J = sum_{I>=J} X_bb,IJ^T w_I - sum_{p rows} PhiT_IJ^T (N Pc)_I -------------
 // Returns this item's share of v_J . y_J (vsrc gives (B_s^T p)_pos; pass zero for R4).
+#define SUBSTAMP(k) \
+  if (sub) { __syncthreads(); if (threadIdx.x == 0) sub[k] = gtimer(); }
 template <class PcF, class Src>
 __device__ double p5_item(const DevPlan& D, int s, int J, const double* W, PcF pc, Src vsrc, double* Y, double* sm,
-                          double* red) {
+                          double* red, unsigned long long* sub = nullptr) {
   const int Ti = D.Ti[s], Tb = D.Tb[s], Tp = D.Tp[s], np = D.np[s], nb = D.nb[s];
   const int Tr = Tb + (np > 0 ? Tp : 0);
   double* sw = sm;                  // (Tr - J) * 64
   double* cr = sm + (Tr - J) * TS;  // 8 * 64
   const int* grp = D.p_grp + D.p_off[s];
   const int64_t vo = D.vec_off[s] + (int64_t)Ti * TS;
+  // v_J entry of this thread (threads < 64), fetched early so its latency overlaps the gather
+  double vj = 0.0;
+  if (threadIdx.x < TS && J * TS + (int)threadIdx.x < nb) vj = vsrc(s, D.b_off[s] + J * TS + threadIdx.x, J * TS + threadIdx.x);
   for (int e = threadIdx.x; e < (Tr - J) * TS; e += blockDim.x) {
     const int i = J * TS + e;  // row index in [b; p] numbering
     double val;
@@ -250,16 +265,20 @@ __device__ double p5_item(const DevPlan& D, int s, int J, const double* W, PcF p
     sw[e] = val;
   }
   __syncthreads();
+  SUBSTAMP(0);
   double c0 = 0.0, c1 = 0.0;
   gemv_col(D, s, Ti + J, Ti + J, Ti + Tr, sw, c0, c1);
+  SUBSTAMP(1);
   const double acc = col_finish(c0, c1, cr);
   double contrib = 0.0;
   if (threadIdx.x < TS) {
     Y[vo + (int64_t)J * TS + threadIdx.x] = acc;
-    const int pos = J * TS + threadIdx.x;
-    if (pos < nb) contrib = vsrc(s, D.b_off[s] + pos, pos) * acc;
+    contrib = vj * acc;
   }
-  return block_sum(contrib, red);
+  SUBSTAMP(2);
+  const double rr = block_sum(contrib, red);
+  SUBSTAMP(3);
+  return rr;
 }
 
 // ---- P7 / R5: symmetric S_bb apply, one row block I of one patch --------------------------
@@ -386,6 +405,9 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p, in
   else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void red_release_gpu(unsigned int* p, unsigned int v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void fence_scope(int sys) {
   if (sys) __threadfence_system();
   else __threadfence();
@@ -408,30 +430,22 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
   const int sys = A.sys_scope;
   BarMem* mine = A.bar[me];
   if (A.nranks == 1) {
+    // arrival = release-add on the rank counter (orders this block's writes, made visible
+    // to thread 0 by the __syncthreads above); departure = acquire poll
     if (threadIdx.x == 0) {
       if (reduce) A.partials[me][bl] = value;
-      __threadfence();
-      atomicAdd(&mine->local_count, 1u);
+      red_release_gpu(&mine->local_count, 1u);
       const unsigned long long t0 = gtimer();
       while ((int)(ld_acquire_u32(&mine->local_count, 0) - round * (unsigned int)A.nbr) < 0) {
         if (gtimer() - t0 > kBarrierTimeoutNs) __trap();  // a missing block: fail, never hang
       }
-      __threadfence();
     }
     __syncthreads();
-    double total = 0.0;
-    if (reduce) {
-      if (threadIdx.x < 32) {
-        double t = 0.0;
-        for (int j = threadIdx.x; j < A.nbr; j += 32) t += __ldcg(A.partials[me] + j);
-        t = warp_sum(t);
-        if (threadIdx.x == 0) *bcast = t;
-      }
-      __syncthreads();
-      total = *bcast;
-      __syncthreads();
-    }
-    return total;
+    if (!reduce) return 0.0;
+    // fixed-order sum of the block partials, loaded by all threads in one round trip
+    double t = 0.0;
+    for (int j = threadIdx.x; j < A.nbr; j += NTHR) t += __ldcg(A.partials[me] + j);
+    return block_sum(t, bcast);
   }
   if (threadIdx.x == 0) {
     if (reduce) A.partials[me][bl] = value;
@@ -441,10 +455,10 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
   }
   __syncthreads();
   if (s_leader) {
-    if (reduce && threadIdx.x < 32) {
+    if (reduce) {
       double t = 0.0;
-      for (int j = threadIdx.x; j < A.nbr; j += 32) t += __ldcg(A.partials[me] + j);
-      t = warp_sum(t);
+      for (int j = threadIdx.x; j < A.nbr; j += NTHR) t += __ldcg(A.partials[me] + j);
+      t = block_sum(t, bcast);
       if (threadIdx.x == 0) mine->rank_part[round & 1] = t;
     }
     if (threadIdx.x == 0) {
@@ -541,6 +555,12 @@ __device__ void rhs_item(const DevPlan& D, const StepArgs& A, int me, int s, int
 // step-level stamps of step 0 (slots 512..527): R1..R5 ends, loop end, E1..E3 ends
 #define SSTAMP(slot) \
   if (A.tstamp && me == 0 && bl == 0 && threadIdx.x == 0 && step == 0) A.tstamp[512 + (slot)] = gtimer()
+// per-block work-end stamps of PCG iteration 2 of step 0 (slots 528 + 8*block + phase)
+#define WSTAMP(slot)                                                        \
+  if (A.tstamp && step == 0 && it == 2) {                                   \
+    __syncthreads();                                                        \
+    if (threadIdx.x == 0 && gb < 4096) A.tstamp[528 + gb * 8 + (slot)] = gtimer(); \
+  }
 
 // =======================================================================================
 // Persistent cooperative time stepper: A.nsteps implicit-Euler steps in one launch, over
@@ -551,7 +571,7 @@ template <bool MULTI>
 __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   extern __shared__ double sm[];
   __shared__ double red[NTHR];
-  __shared__ double bcast;
+  __shared__ double bcast[NTHR / 32];
   // MULTI = false: one rank, every owner lookup folds to rank 0 at compile time
   const int me = MULTI ? A.rank_base + (int)blockIdx.x / A.nbr : 0;  // this block's rank
   const int bl = MULTI ? (int)blockIdx.x % A.nbr : (int)blockIdx.x;   // block index within the rank
@@ -563,7 +583,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   auto lown = [&](int64_t k) { return MULTI ? ((int)k / (int)A.lam_chunk) / A.nbr : 0; };
   auto pown = [&](int s) { return MULTI ? D.owner[s] : 0; };
   auto own_idx = [&](int s, int pos) { return D.vec_off[s] + (int64_t)D.Ti[s] * TS + pos; };
-  auto pcf = [&](int64_t g) { return pc_get(A, g); };
+  auto pcf = [&](int64_t g) { return pc_get<MULTI>(A, g); };
   // partner patch of b position bb (other endpoint of its multiplier)
   auto ppatch = [&](int64_t bb) {
     if (!MULTI) return 0;
@@ -590,22 +610,22 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     SSTAMP(0);
     // ---- R1 rhs ----
     for (int i = rhs_b + bl; i < rhs_e; i += NB) rhs_item(D, A, me, A.it_rhs[i].x, A.it_rhs[i].y, t, sm);
-    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
+    grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(1);
     // ---- R2 forward (conductors) ----
     for (int i = fw_b + bl; i < fw_e; i += NB) fw_item(D, A.it_fw[i].x, A.it_fw[i].y, A.F[me], A.Z[me], sm);
-    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
+    grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(2);
     // ---- R3 p0 = S_pp^-1 sum N^T Z_p ----
     for (int i = pc_b + bl; i < pc_e; i += NB)
       pc_item(D, A, A.Sinv[me], A.it_pc[i].x, A.it_pc[i].y,
               [&](int e) { return ldcg(A.Z[pown(D.coarse_patch[e])] + D.coarse_idx[e]); }, A.Ppart[me], sm);
-    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
+    grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(3);
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
     for (int i = p5_b + bl; i < p5_e; i += NB)
       p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.Z[me], pcf, [&](int, int64_t, int) { return 0.0; }, A.Y[me], sm, red);
-    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
+    grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(4);
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
     double rho0;
@@ -624,7 +644,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         A.pk[0][me][k] = 0.0;
         A.lam[me][k] = 0.0;
       }
-      rho0 = grid_barrier(A, me, bl, round, true, loc, &bcast);
+      rho0 = grid_barrier(A, me, bl, round, true, loc, bcast);
     }
     SSTAMP(5);
     if (me == 0 && bl == 0 && threadIdx.x == 0) A.hist[0][hoff] = 1.0;
@@ -649,13 +669,15 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
         pcur[k] = D.wplus[k] * ldcg(A.PW[pown(D.lam_patch_p[k])] + D.lam_idx_p[k]) -
                   D.wminus[k] * ldcg(A.PW[pown(D.lam_patch_m[k])] + D.lam_idx_m[k]) + beta * ldcg(pprev[me] + k);
-      grid_barrier(A, me, bl, round, false, 0.0, &bcast);
+      WSTAMP(0);
+      grid_barrier(A, me, bl, round, false, 0.0, bcast);
       TSTAMP(1);
       // PC
       for (int i = pc_b + bl; i < pc_e; i += NB)
         pc_item(D, A, A.Sinv[me], A.it_pc[i].x, A.it_pc[i].y,
                 [&](int e) { return ldcg(A.XW[pown(D.coarse_patch[e])] + D.coarse_idx[e]); }, A.Ppart[me], sm);
-      grid_barrier(A, me, bl, round, false, 0.0, &bcast);
+      WSTAMP(1);
+      grid_barrier(A, me, bl, round, false, 0.0, bcast);
       TSTAMP(2);
       // P5 (+ partial p^T F p)
       double* const* pcurt = A.pk[pp ^ 1];
@@ -668,8 +690,10 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                            const int k = D.b_lam[bb];
                            return D.b_sign[bb] * ldcg(pcurt[lown(k)] + k);
                          },
-                         A.Y[me], sm, red);
-        pq = grid_barrier(A, me, bl, round, true, loc, &bcast);
+                         A.Y[me], sm, red,
+                         (A.tstamp && step == 0 && it == 2 && gb < 4096) ? A.tstamp + 528 + gb * 8 + 4 : nullptr);
+        WSTAMP(2);
+        pq = grid_barrier(A, me, bl, round, true, loc, bcast);
       }
       TSTAMP(3);
       if (!(pq > 0.0)) { status = 2; break; }  // lost positive curvature (uniform)
@@ -690,7 +714,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         }
         double loc = 0.0;
         for (int i = sy_b + bl; i < sy_e; i += NB) loc += symv_item(D, A.PW[me], A.it_sy[i].x, A.it_sy[i].y, unew, sm, red);
-        rz = grid_barrier(A, me, bl, round, true, loc, &bcast);
+        WSTAMP(3);
+        rz = grid_barrier(A, me, bl, round, true, loc, bcast);
       }
       TSTAMP(4);
       ++it;
@@ -728,7 +753,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                 return D.b_sign[bb] * ldcg(A.lam[lown(k)] + k);
               },
               A.XW[me], sm);
-    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
+    grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(7);
     // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
     for (int i = pc_b + bl; i < pc_e; i += NB)
@@ -738,7 +763,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                 return ldcg(A.Z[o] + D.coarse_idx[e]) - ldcg(A.XW[o] + D.coarse_idx[e]);
               },
               A.Ppart[me], sm);
-    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
+    grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(8);
     // ---- E3 a_r = X_rr^T (Z_r - [0; w_b]) - Phi N p, a_p = N p ----
     // insulator coefficients feed no later step (no mass term): recover them only at the last step
@@ -749,7 +774,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       for (int i = ib + bl; i < ie; i += NB)
         bw_item(D, itb[i].x, itb[i].y, A.Z[me], A.XW[me], pcf, A.a_loc[me], A.G.nloc, sm);
     }
-    grid_barrier(A, me, bl, round, false, 0.0, &bcast);
+    grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(9);
   }
   if (bl == 0 && threadIdx.x == 0) {
@@ -783,7 +808,7 @@ __global__ void __launch_bounds__(NTHR) k_pc(DevPlan D, StepArgs A, const int2* 
 }
 __global__ void k_pc_sum(DevPlan D, StepArgs A, double* Pc) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D.nc; g += (int64_t)gridDim.x * blockDim.x)
-    Pc[g] = pc_get(A, g);
+    Pc[g] = pc_get<true>(A, g);
 }
 __global__ void __launch_bounds__(NTHR) k_p5(DevPlan D, const int2* items, int n, const double* W, const double* Pc,
                                              double* Y) {
