@@ -88,7 +88,7 @@ struct RankDev {
   CholDesc* d_desc = nullptr;
   int ndesc = 0, maxT = 0, maxTr = 0, maxTb = 0;
   // global-layout vectors (entries of owned patches / lambda chunks valid)
-  double *F = nullptr, *Z = nullptr, *XJ = nullptr, *JS = nullptr, *XW = nullptr, *Y = nullptr, *PW = nullptr;
+  double *F = nullptr, *Z = nullptr, *XJ = nullptr, *JS = nullptr, *XW = nullptr, *Y = nullptr, *Y2 = nullptr, *PW = nullptr;
   double *a_loc = nullptr, *lam = nullptr, *r0 = nullptr, *r1 = nullptr, *pk0 = nullptr, *pk1 = nullptr, *q = nullptr;
   double *Ppart = nullptr, *Pc = nullptr, *partials = nullptr, *hist = nullptr;
   int* iters = nullptr;
@@ -142,12 +142,12 @@ struct tcg_ctx {
   PcgState* h_st = nullptr;  // pinned
   int maxT = 0, maxTr = 0, maxTb = 0, maxTp = 0, Tc = 0;
   int64_t nb_total = 0, vec_total = 0;
-  // item lists of all ranks (concatenated, per-rank offsets)
-  int2 *d_it_p1 = nullptr, *d_it_p5 = nullptr, *d_it_sy = nullptr, *d_it_pc = nullptr, *d_it_fw = nullptr,
-       *d_it_fwa = nullptr, *d_it_bw = nullptr, *d_it_bwc = nullptr, *d_it_rhs = nullptr;
-  int *d_off_p1 = nullptr, *d_off_p5 = nullptr, *d_off_sy = nullptr, *d_off_pc = nullptr, *d_off_fw = nullptr,
-      *d_off_fwa = nullptr, *d_off_bw = nullptr, *d_off_bwc = nullptr, *d_off_rhs = nullptr;
-  std::vector<int> off_p1, off_p5, off_pc, off_fwa;
+  // stepper work items per phase: ItemDesc lists ordered by (rank, block), per-block offsets
+  ItemDesc* d_items[NPH] = {};
+  int* d_boff[NPH] = {};
+  std::vector<int> h_boff[NPH];
+  int cache_items = 0, cache_lam = 0;
+  size_t smem_steps = 0;  // dynamic shared memory of k_steps: item scratch + caches
   int coarse_ch = 1, coarse_maxch = 1;
   size_t smem_pcg = 0, smem_tables = 0;
   int nbr = 0;  // persistent blocks per rank
@@ -467,9 +467,9 @@ static tcg_status do_numeric(tcg_ctx* h) {
   }
   // insulator precompute: XJ = [X_rr j_S,r ; j_S,p - Phi^T j_S,r] for owned patches
   for (auto& R : h->rd) {
-    const int n = h->off_fwa[R.r + 1] - h->off_fwa[R.r];
+    const int b0 = h->h_boff[PH_FWA][R.r * h->nbr], n = h->h_boff[PH_FWA][(R.r + 1) * h->nbr] - b0;
     if (n > 0) {
-      k_fw<<<n, NTHR, h->smem_pcg, h->stream>>>(R.D, h->d_it_fwa + h->off_fwa[R.r], n, R.JS, R.XJ);
+      k_fw<<<n, NTHR, h->smem_pcg, h->stream>>>(R.D, h->d_items[PH_FWA] + b0, n, R.JS, R.XJ);
       ++h->nlaunch;
       CKL();
     }
@@ -497,27 +497,56 @@ static tcg_status do_numeric(tcg_ctx* h) {
 // =========================================================================================
 // setup: layouts, uploads, per-rank allocations, peer tables
 // =========================================================================================
+// Work items of one stepper phase, per rank: (cost, item). Dealt to the rank's nbr persistent
+// blocks by LPT (largest first onto the least-loaded block; ties to the lower block), each
+// block's items kept in that order. A fixed per-item overhead models the gather latency.
 struct ItemLists {
-  std::vector<std::vector<std::pair<int, int2>>> per_rank;
+  std::vector<std::vector<std::pair<int, ItemDesc>>> per_rank;
   explicit ItemLists(int nr) : per_rank(nr) {}
 };
 
-static tcg_status upload_items(tcg_ctx* h, ItemLists& L, int2** d_items, int** d_off, std::vector<int>* h_off = nullptr) {
-  auto bycost = [](const std::pair<int, int2>& x, const std::pair<int, int2>& y) {
+static tcg_status upload_items(tcg_ctx* h, ItemLists& L, int ph, int overhead) {
+  const int nbr = h->nbr;
+  auto bycost = [](const std::pair<int, ItemDesc>& x, const std::pair<int, ItemDesc>& y) {
     return x.first != y.first ? x.first > y.first
-                              : (x.second.x != y.second.x ? x.second.x < y.second.x : x.second.y < y.second.y);
+                              : (x.second.s != y.second.s ? x.second.s < y.second.s : x.second.I < y.second.I);
   };
-  std::vector<int2> all;
-  std::vector<int> off(1, 0);
+  std::vector<ItemDesc> all;
+  std::vector<int> boff(1, 0);
+  const char* fe = getenv("TCG_STEP_FLAGS");
+  const int flags = fe ? atoi(fe) : 0;
   for (auto& v : L.per_rank) {
     std::stable_sort(v.begin(), v.end(), bycost);
-    for (auto& e : v) all.push_back(e.second);
-    off.push_back((int)all.size());
+    if (flags & 2) {  // experiment: round-robin dealing of the cost-sorted items
+      std::vector<std::vector<ItemDesc>> blk(nbr);
+      for (size_t i = 0; i < v.size(); ++i) blk[i % nbr].push_back(v[i].second);
+      for (int b = 0; b < nbr; ++b) {
+        all.insert(all.end(), blk[b].begin(), blk[b].end());
+        boff.push_back((int)all.size());
+      }
+      continue;
+    }
+    std::vector<std::vector<ItemDesc>> blk(nbr);
+    std::vector<std::pair<int64_t, int>> heap;  // (load, block) min-heap
+    for (int b = 0; b < nbr; ++b) heap.push_back({0, b});
+    auto cmp = [](const std::pair<int64_t, int>& x, const std::pair<int64_t, int>& y) { return x > y; };
+    std::make_heap(heap.begin(), heap.end(), cmp);
+    for (auto& e : v) {
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      auto& top = heap.back();
+      blk[top.second].push_back(e.second);
+      top.first += e.first + overhead;
+      std::push_heap(heap.begin(), heap.end(), cmp);
+    }
+    for (int b = 0; b < nbr; ++b) {
+      all.insert(all.end(), blk[b].begin(), blk[b].end());
+      boff.push_back((int)all.size());
+    }
   }
-  while ((int)off.size() < MAXR + 1) off.push_back(off.back());
-  TRY(dupload(h, d_items, all));
-  TRY(dupload(h, d_off, off));
-  if (h_off) *h_off = off;
+  if (all.empty()) all.push_back(ItemDesc{});
+  TRY(dupload(h, &h->d_items[ph], all));
+  TRY(dupload(h, &h->d_boff[ph], boff));
+  h->h_boff[ph] = boff;
   return TCG_OK;
 }
 
@@ -734,52 +763,12 @@ static tcg_status do_setup(tcg_ctx* h) {
     h->smem_tables = sizeof(double) * (2 * (pl.p + 1) + (size_t)maxel * (pl.p + 1) * (3 * maxn + 2));
   }
 
-  // ---- work items per rank (largest first, dealt round-robin over the rank's blocks) ----
+  // ---- shared memory and persistent grid ----
   int dev_sms = 148;
   CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
   h->coarse_ch = (int)std::max<int64_t>(1, std::min<int64_t>(64, (int64_t)Tc * Tc / (4 * (int64_t)dev_sms)));
   h->coarse_maxch = std::max(1, (Tc + h->coarse_ch - 1) / h->coarse_ch);
-  std::vector<int> crow_owner(std::max(Tc, 1));
-  for (int I = 0; I < Tc; ++I) crow_owner[I] = (int)((int64_t)I * NR / Tc);
-  TRY(dupload(h, &h->d_crow_owner, crow_owner));
-  {
-    ItemLists p1(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR);
-    for (int s = 0; s < P; ++s) {
-      const int r = owner[s];
-      const int Trs = Ti[s] + Tb[s];
-      for (int I = 0; I < T[s]; ++I) {
-        const int cost = I < Trs ? I + 1 : Trs;
-        if (pl.sigma[s] > 0) fw.per_rank[r].push_back({cost, make_int2(s, I)});
-        fwa.per_rank[r].push_back({cost, make_int2(s, I)});
-      }
-      for (int J = 0; J < std::max(Trs, 1); ++J) {
-        bw.per_rank[r].push_back({T[s] - J, make_int2(s, J)});
-        if (pl.sigma[s] > 0) bwc.per_rank[r].push_back({T[s] - J, make_int2(s, J)});
-      }
-      if (pl.sigma[s] > 0)
-        for (int c = 0; c < 3; ++c) rhs.per_rank[r].push_back({pl.nloc / 3, make_int2(s, c)});
-      else
-        rhs.per_rank[r].push_back({T[s] * TS / 8, make_int2(s, -1)});
-      for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], make_int2(s, I)});
-      for (int J = 0; J < Tb[s]; ++J) p5.per_rank[r].push_back({Tb[s] - J + Tp[s], make_int2(s, J)});
-      for (int I = 0; I < Tb[s]; ++I) sy.per_rank[r].push_back({Tb[s], make_int2(s, I)});
-    }
-    const int ch = h->coarse_ch;
-    for (int I = 0; I < Tc; ++I)
-      for (int c = 0; c < h->coarse_maxch; ++c)
-        pcv.per_rank[crow_owner[I]].push_back({std::min(Tc, (c + 1) * ch) - c * ch, make_int2(I, c)});
-    TRY(upload_items(h, p1, &h->d_it_p1, &h->d_off_p1, &h->off_p1));
-    TRY(upload_items(h, p5, &h->d_it_p5, &h->d_off_p5, &h->off_p5));
-    TRY(upload_items(h, sy, &h->d_it_sy, &h->d_off_sy));
-    TRY(upload_items(h, pcv, &h->d_it_pc, &h->d_off_pc, &h->off_pc));
-    TRY(upload_items(h, fw, &h->d_it_fw, &h->d_off_fw));
-    TRY(upload_items(h, fwa, &h->d_it_fwa, &h->d_off_fwa, &h->off_fwa));
-    TRY(upload_items(h, bw, &h->d_it_bw, &h->d_off_bw));
-    TRY(upload_items(h, bwc, &h->d_it_bwc, &h->d_off_bwc));
-    TRY(upload_items(h, rhs, &h->d_it_rhs, &h->d_off_rhs));
-  }
-
-  // ---- shared memory and persistent grid ----
+  int per = 2;  // persistent blocks per SM
   {
     size_t p1 = (size_t)h->maxTb * TS;
     size_t p5 = (size_t)(h->maxTb + h->maxTp) * TS + 8 * TS;
@@ -789,9 +778,9 @@ static tcg_status do_setup(tcg_ctx* h) {
     size_t maxcomp = 0;
     for (int c = 0; c < 3; ++c) maxcomp = std::max(maxcomp, (size_t)pl.comp_dim(c, 0) * pl.comp_dim(c, 1) * pl.comp_dim(c, 2));
     fwb = std::max(fwb, 2 * maxcomp);
-    h->smem_pcg = sizeof(double) * std::max(std::max(p1, p5), std::max(std::max(pcs, fwb), syv));
-    TRY(set_smem(h, (const void*)k_steps<false>, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_steps<true>, h->smem_pcg));
+    size_t scratch = std::max(std::max(p1, p5), std::max(std::max(pcs, fwb), syv));
+    scratch = (scratch + 1) & ~(size_t)1;  // keep the item cache 16-byte aligned
+    h->smem_pcg = sizeof(double) * scratch;
     TRY(set_smem(h, (const void*)k_fw, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_p1_lam, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_pc, h->smem_pcg));
@@ -803,14 +792,118 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(set_smem(h, (const void*)k_potrf, 2 * TS * 65 * sizeof(double)));
     TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_update, 2 * TS * SPAD * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_steps<false>, h->smem_pcg));
+    TRY(set_smem(h, (const void*)k_steps<true>, h->smem_pcg));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps<true>, NTHR, h->smem_pcg));
     if (occ < 1) return fail(h, TCG_ECUDA, "persistent stepper kernel does not fit on an SM");
     const char* ev = getenv("TCG_PCG_BLOCKS_PER_SM");
-    int per = ev ? std::max(1, atoi(ev)) : 2;
-    int total = dev_sms * std::min(occ, per);  // co-resident blocks on this device
+    per = std::min(occ, ev ? std::max(1, atoi(ev)) : 2);
+    int total = dev_sms * per;  // co-resident blocks on this device
     h->nbr = std::max(1, total / (int)(h->world > 1 ? 1 : h->vranks));
     h->lam_chunk = std::max<int64_t>(1, (pl.m + (int64_t)NR * h->nbr - 1) / ((int64_t)NR * h->nbr));
+  }
+
+  {
+    // per-iteration working set of the stepper ([X_bb; Phi_b^T], S_bb, S_pp^-1): when it is
+    // L2-resident the L1 prefetch of the first tiles only adds instructions (bit 0 = off)
+    double ws = 8.0 * (double)pl.nc * pl.nc;
+    for (int s2 = 0; s2 < P; ++s2) {
+      const double b = pl.pp[s2].nb, q = pl.pp[s2].np;
+      ws += 8.0 * (b * (b + 1) / 2 + b * q) + 4.0 * b * (b + 1);
+    }
+    const char* fe = getenv("TCG_STEP_FLAGS");
+    const int flags = fe ? atoi(fe) : (ws < 48e6 ? 1 : 0);
+    CK(cudaMemcpyToSymbol(c_step_flags, &flags, sizeof(int)));
+  }
+  // ---- work items per rank, dealt to the rank's persistent blocks (LPT) ----
+  std::vector<int> crow_owner(std::max(Tc, 1));
+  for (int I = 0; I < Tc; ++I) crow_owner[I] = (int)((int64_t)I * NR / Tc);
+  TRY(dupload(h, &h->d_crow_owner, crow_owner));
+  {
+    auto desc = [&](int s, int I) {
+      ItemDesc d{};
+      d.s = s;
+      d.I = I;
+      d.Ti = Ti[s]; d.Tb = Tb[s]; d.Tp = Tp[s]; d.T = T[s];
+      d.nb = nb[s]; d.np = np[s];
+      d.a_off = a_off[s]; d.vec_off = vec_off[s]; d.b_off = b_off[s]; d.p_off = p_off[s]; d.sbb_off = sbb_off[s];
+      return d;
+    };
+    ItemLists p1(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR);
+    for (int s = 0; s < P; ++s) {
+      const int r = owner[s];
+      const int Trs = Ti[s] + Tb[s];
+      for (int I = 0; I < T[s]; ++I) {
+        const int cost = I < Trs ? I + 1 : Trs;
+        if (pl.sigma[s] > 0) fw.per_rank[r].push_back({cost, desc(s, I)});
+        fwa.per_rank[r].push_back({cost, desc(s, I)});
+      }
+      for (int J = 0; J < std::max(Trs, 1); ++J) {
+        bw.per_rank[r].push_back({T[s] - J, desc(s, J)});
+        if (pl.sigma[s] > 0) bwc.per_rank[r].push_back({T[s] - J, desc(s, J)});
+      }
+      if (pl.sigma[s] > 0)
+        for (int c = 0; c < 3; ++c) rhs.per_rank[r].push_back({pl.nloc / 3, desc(s, c)});
+      else
+        rhs.per_rank[r].push_back({T[s] * TS / 8, desc(s, -1)});
+      for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
+      for (int J = 0; J < Tb[s]; ++J) {
+        p5.per_rank[r].push_back({Tb[s] - J, desc(s, J)});
+        if (np[s] > 0) {
+          ItemDesc d = desc(s, J);
+          d.part = 1;
+          p5.per_rank[r].push_back({Tp[s], d});
+        }
+      }
+      for (int I = 0; I < Tb[s]; ++I) sy.per_rank[r].push_back({Tb[s], desc(s, I)});
+    }
+    const int ch = h->coarse_ch;
+    for (int I = 0; I < Tc; ++I)
+      for (int c = 0; c < h->coarse_maxch; ++c) {
+        ItemDesc d{};
+        d.s = I;
+        d.I = c;
+        pcv.per_rank[crow_owner[I]].push_back({std::min(Tc, (c + 1) * ch) - c * ch, d});
+      }
+    // fixed per-item overhead (tile units) of the latency-bound item phases
+    TRY(upload_items(h, p1, PH_P1, 2));
+    TRY(upload_items(h, pcv, PH_PC, 2));
+    TRY(upload_items(h, p5, PH_P5, 2));
+    TRY(upload_items(h, sy, PH_SY, 2));
+    TRY(upload_items(h, fw, PH_FW, 2));
+    TRY(upload_items(h, fwa, PH_FWA, 2));
+    TRY(upload_items(h, bw, PH_BW, 2));
+    TRY(upload_items(h, bwc, PH_BWC, 2));
+    TRY(upload_items(h, rhs, PH_RHS, 0));
+  }
+  // shared-memory caches of the per-iteration item lists and the lambda chunk, if they fit
+  // next to the scratch at `per` blocks per SM
+  {
+    int max_items = 0;
+    for (int gb = 0; gb < NR * h->nbr; ++gb) {
+      int n = 0;
+      for (int ph = 0; ph < NCACHE; ++ph) n += h->h_boff[ph][gb + 1] - h->h_boff[ph][gb];
+      max_items = std::max(max_items, n);
+    }
+    const size_t items_b = (size_t)max_items * sizeof(ItemDesc);
+    const size_t lam_b = (size_t)h->lam_chunk * sizeof(LamC);
+    int smem_sm = 0, reserved = 0;
+    CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
+    CK(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, h->device));
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, k_steps<true>));
+    const int64_t budget = (int64_t)smem_sm / per - reserved - (int64_t)fa.sharedSizeBytes - 256;
+    const char* ev = getenv("TCG_NO_SMEM_CACHE");
+    const bool allow = !(ev && atoi(ev) != 0);
+    h->cache_items = allow && (int64_t)(h->smem_pcg + items_b) <= budget && items_b <= 48 * 1024;
+    h->cache_lam = allow && (int64_t)(h->smem_pcg + (h->cache_items ? items_b : 0) + lam_b) <= budget && lam_b <= 32 * 1024;
+    h->smem_steps = h->smem_pcg + (h->cache_items ? items_b : 0) + (h->cache_lam ? lam_b : 0);
+    TRY(set_smem(h, (const void*)k_steps<false>, h->smem_steps));
+    TRY(set_smem(h, (const void*)k_steps<true>, h->smem_steps));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps<true>, NTHR, h->smem_steps));
+    if (occ < per) return fail(h, TCG_ECUDA, "persistent stepper: shared-memory caches broke occupancy");
   }
 
   // ---- per-rank allocations ----
@@ -848,6 +941,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dzero(h, &R.JS, ov));
     TRY(dzero(h, &R.XW, ov));
     TRY(dzero(h, &R.Y, ov));
+    TRY(dzero(h, &R.Y2, ov));
     TRY(dzero(h, &R.PW, ov));
     TRY(dzero(h, &R.a_loc, (size_t)P * pl.nloc));
     TRY(dzero(h, &R.lam, pl.m));
@@ -880,7 +974,7 @@ static tcg_status do_setup(tcg_ctx* h) {
   {
     std::vector<std::vector<void*>> bufs(NR);  // [rank][buffer] in a fixed order
     for (auto& R : h->rd)
-      bufs[R.r] = {R.A, R.Sbb, R.Z, R.XW, R.Y, R.PW, R.lam, R.r0, R.r1, R.pk0, R.pk1, R.Ppart, R.bar, R.a_loc};
+      bufs[R.r] = {R.A, R.Sbb, R.Z, R.XW, R.Y, R.PW, R.lam, R.r0, R.r1, R.pk0, R.pk1, R.Ppart, R.bar, R.a_loc, R.Y2};
     if (h->world > 1) TRY(open_peer_tables(h, bufs));
     for (int r = 0; r < NR; ++r) {
       D.Ar[r] = (double*)bufs[r][0];
@@ -1013,6 +1107,7 @@ static StepArgs step_args(tcg_ctx* h) {
     A.Ppart[r] = (double*)B[r][11];
     A.bar[r] = (BarMem*)B[r][12];
     A.a_loc[r] = (double*)B[r][13];
+    A.Y2[r] = (double*)B[r][14];
   }
   for (auto& R : h->rd) {  // own-only buffers of the local ranks
     A.F[R.r] = R.F;
@@ -1028,14 +1123,13 @@ static StepArgs step_args(tcg_ctx* h) {
   A.crow_owner = h->d_crow_owner;
   A.ch = h->coarse_ch;
   A.maxch = h->coarse_maxch;
-  A.it_p1 = h->d_it_p1; A.off_p1 = h->d_off_p1;
-  A.it_p5 = h->d_it_p5; A.off_p5 = h->d_off_p5;
-  A.it_sy = h->d_it_sy; A.off_sy = h->d_off_sy;
-  A.it_pc = h->d_it_pc; A.off_pc = h->d_off_pc;
-  A.it_fw = h->d_it_fw; A.off_fw = h->d_off_fw;
-  A.it_bw = h->d_it_bw; A.off_bw = h->d_off_bw;
-  A.it_bwc = h->d_it_bwc; A.off_bwc = h->d_off_bwc;
-  A.it_rhs = h->d_it_rhs; A.off_rhs = h->d_off_rhs;
+  for (int ph = 0; ph < NPH; ++ph) {
+    A.items[ph] = h->d_items[ph];
+    A.boff[ph] = h->d_boff[ph];
+  }
+  A.cache_items = h->cache_items;
+  A.cache_lam = h->cache_lam;
+  A.scratch = (int)(h->smem_pcg / sizeof(double));
   A.tstamp = h->tstamp;
   A.rtol = h->rtol;
   A.max_iter = h->max_iter;
@@ -1067,7 +1161,7 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   const int grid = h->nbr * (int)h->rd.size();
   prof_begin(h, 7);
   const void* fn = (h->nranks > 1) ? (const void*)k_steps<true> : (const void*)k_steps<false>;
-  CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NTHR), args, h->smem_pcg, h->stream));
+  CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NTHR), args, h->smem_steps, h->stream));
   ++h->nlaunch;
   prof_end(h, 7);
   RankDev& R0 = h->rd[0];
@@ -1416,19 +1510,19 @@ tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms) {
   RankDev& R = h->rd[0];
   DevPlan& D = R.D;
   StepArgs A = step_args(h);
-  const int np1 = h->off_p1[1], np5 = h->off_p5[1], npc = h->off_pc[1];
+  const int np1 = h->h_boff[PH_P1][h->nbr], np5 = h->h_boff[PH_P5][h->nbr], npc = h->h_boff[PH_PC][h->nbr];
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, h->stream);
   for (int i = 0; i < n; ++i) {
-    if (np1 > 0) k_p1_lam<<<np1, NTHR, h->smem_pcg, h->stream>>>(D, h->d_it_p1, np1, R.r0, R.XW);
+    if (np1 > 0) k_p1_lam<<<np1, NTHR, h->smem_pcg, h->stream>>>(D, h->d_items[PH_P1], np1, R.r0, R.XW);
     if (npc > 0) {
-      k_pc<<<npc, NTHR, h->smem_pcg, h->stream>>>(D, A, h->d_it_pc, npc, R.XW, R.Ppart);
+      k_pc<<<npc, NTHR, h->smem_pcg, h->stream>>>(D, A, h->d_items[PH_PC], npc, R.XW, R.Ppart);
       k_pc_sum<<<592, 256, 0, h->stream>>>(D, A, R.Pc);
     }
-    if (np5 > 0) k_p5<<<np5, NTHR, h->smem_pcg, h->stream>>>(D, h->d_it_p5, np5, R.XW, R.Pc, R.Y);
-    if (D.m > 0) k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, R.Y, R.q);
+    if (np5 > 0) k_p5<<<np5, NTHR, h->smem_pcg, h->stream>>>(D, h->d_items[PH_P5], np5, R.XW, R.Pc, R.Y, R.Y2);
+    if (D.m > 0) k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, R.Y, R.Y2, R.q);
     h->nlaunch += 5;
   }
   cudaEventRecord(e1, h->stream);

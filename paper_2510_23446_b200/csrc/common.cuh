@@ -33,6 +33,21 @@ struct PcgState {
   unsigned int counter[4];  // last-block-done counters for deterministic reductions
 };
 
+// One work item of the persistent stepper with the scalars of its patch embedded, so that
+// an item costs one (shared-memory) load instead of an index -> patch-table chain.
+//   P1/P5/SY/FW/BW: s = patch, I = tile row/column block; RHS: I = component (-1 insulator);
+//   PC: s = coarse row block, I = column chunk.
+struct __align__(16) ItemDesc {
+  int s, I;
+  int Ti, Tb, Tp, T;
+  int nb, np;
+  int64_t a_off, vec_off, b_off, p_off, sbb_off;
+  int part, pad;  // P5: 0 = X_bb^T tiles (-> Y), 1 = Phi_b tiles (-> Y2)
+};
+// item phases of the stepper; the first NCACHE are the per-iteration ones (shared-memory cache)
+enum { PH_P1 = 0, PH_PC, PH_P5, PH_SY, PH_FW, PH_FWA, PH_BW, PH_BWC, PH_RHS, NPH };
+constexpr int NCACHE = 4;
+
 // Per-matrix descriptor for the batched tiled Cholesky (patches and the coarse matrix).
 struct CholDesc {
   int64_t a_off;     // offset (doubles) of the tile-packed lower matrix

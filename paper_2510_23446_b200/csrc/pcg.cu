@@ -23,6 +23,12 @@
 //   E2  Pc = S_pp^-1 sum N^T (Z_p + Phi^T v)              (= p)
 //   E3  a_r = X_rr^T (Z_r - [0; w_b]) - Phi N Pc ; a_p = N Pc ; a_e = 0
 // Partials are summed in one fixed order by every block: deterministic, identical scalars.
+//
+// Latency design (the small configs are L2-resident and bound by dependent-load chains):
+// each block's items are fixed for the whole launch (host LPT dealing, ItemDesc carries the
+// patch scalars) and the per-iteration item lists and the block's lambda-chunk index data are
+// copied to shared memory once per launch; every GEMV issues its first tile's loads before
+// the gather of its input vector, so the two latencies overlap.
 #include "common.cuh"
 #include "device.h"
 
@@ -36,6 +42,13 @@ struct BarMem {
   unsigned int pad;
   double rank_part[2];        // this rank's partial of the current reduction (by round parity)
   double pad2[6];
+};
+
+// lambda-chunk index data of one multiplier (shared-memory cache of the block's chunk)
+struct LamC {
+  int64_t ip, im;  // aug-vector indices of the + and - side
+  double wp, wm;   // B_D weights of the two sides
+  int pp, pm;      // patches of the two sides
 };
 
 // Arguments of the persistent stepper. Every per-rank buffer is a table indexed by rank:
@@ -53,7 +66,8 @@ struct StepArgs {
   double* XJ[MAXR];    // setup: forward of j_S (insulator rhs template)
   double* JS[MAXR];
   double* XW[MAXR];    // P1/E1 output: b part w, p part -g
-  double* Y[MAXR];     // P5/R4 output: b part y
+  double* Y[MAXR];     // P5/R4 output: b part y, X_bb^T part (y = Y + Y2)
+  double* Y2[MAXR];    // P5/R4 output: b part y, -Phi_b N Pc part
   double* PW[MAXR];    // S_bb apply output: b part
   double* a_loc[MAXR]; // local coefficient vectors (npatch x nloc)
   // coarse
@@ -68,9 +82,12 @@ struct StepArgs {
   double* hist[MAXR];
   int* iters[MAXR];
   PcgState* st[MAXR];
-  // item lists: per rank r, items[off[r] .. off[r+1])
-  const int2 *it_p1, *it_p5, *it_sy, *it_pc, *it_fw, *it_bw, *it_bwc, *it_rhs;
-  const int *off_p1, *off_p5, *off_sy, *off_pc, *off_fw, *off_bw, *off_bwc, *off_rhs;
+  // work items per phase: block gb = rank * nbr + bl owns items[ph][boff[ph][gb] .. boff[ph][gb+1])
+  const ItemDesc* items[NPH];
+  const int* boff[NPH];
+  int cache_items;  // 1: the block's per-iteration item lists are copied to shared memory
+  int cache_lam;    // 1: the block's lambda-chunk index data are copied to shared memory
+  int scratch;      // doubles of item scratch at the start of dynamic shared memory (even)
   unsigned long long* tstamp;  // optional phase timestamps (rank 0 block 0)
   double rtol;
   int max_iter;
@@ -97,11 +114,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
-}
-
-// tile (I,J) of patch s's inverse factor Xaug (aug tile numbering)
-__device__ __forceinline__ const double* xtile(const DevPlan& D, int s, int I, int J) {
-  return D.Ar[D.owner[s]] + D.a_off[s] + tri_off(I, J);
 }
 
 // fixed-order block reduction of one value per thread: xor-butterfly warp sums (lane 0's
@@ -137,14 +149,36 @@ __device__ __forceinline__ double pc_get(const StepArgs& A, int64_t g) {
   return v;
 }
 
-// ---- generic tile GEMVs over one tile row / column of Xaug ------------------------------
-// row:  part[r] += sum_{J=J0}^{J1-1} X(I,J)[row0+r][:] . x[(J-J0)*64 : ]      (x in smem)
-__device__ __forceinline__ void gemv_row(const DevPlan& D, int s, int I, int J0, int J1, const double* x,
-                                         double (&part)[8]) {
+// ---- tile GEMVs with the input gather overlapped ------------------------------------------
+// Warp w owns rows 8w..8w+7 of every 64x64 tile, lane l columns 2l, 2l+1. The first two
+// tiles are prefetched into L1 (non-binding, no registers held), then gather() fills the
+// input vector in shared memory, then the tiles are streamed (2 tiles of loads in flight).
+// experiment switches (TCG_STEP_FLAGS): bit 0 = no L1 prefetch of the first tiles
+__constant__ int c_step_flags;
+__device__ __forceinline__ void prefetch_l1(const double* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+template <class TileF>
+__device__ __forceinline__ void prefetch_tiles(TileF tile, int J0, int J1) {
+  const int off = (threadIdx.x >> 5) * 8 * TS + 2 * (threadIdx.x & 31);
+  for (int J = J0; J < min(J1, J0 + 2); ++J) {
+    const double* t = tile(J) + off;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) prefetch_l1(t + r * TS);
+  }
+}
+// row:  part[r] += sum_{J=J0}^{J1-1} tile(J)[row0+r][:] . x[(J-J0)*64 : ]
+template <class TileF, class Gather>
+__device__ __forceinline__ void gemv_row_g(TileF tile, int J0, int J1, const double* x, Gather gather,
+                                           double (&part)[8]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
+  const int off = row0 * TS + 2 * lane;
+  if (!(c_step_flags & 1)) prefetch_tiles(tile, J0, J1);
+  gather();
+  __syncthreads();
 #pragma unroll 2
   for (int J = J0; J < J1; ++J) {
-    const double* t = xtile(D, s, I, J) + row0 * TS + 2 * lane;
+    const double* t = tile(J) + off;
     const double2 xv = *reinterpret_cast<const double2*>(x + (J - J0) * TS + 2 * lane);
     double2 a[8];
 #pragma unroll
@@ -153,13 +187,18 @@ __device__ __forceinline__ void gemv_row(const DevPlan& D, int s, int I, int J0,
     for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
   }
 }
-// col:  c[0..1] += sum_{I=I0}^{I1-1} X(I,J)[row0+r][2*lane..] * x[(I-I0)*64 + row0 + r]
-__device__ __forceinline__ void gemv_col(const DevPlan& D, int s, int J, int I0, int I1, const double* x, double& c0,
-                                         double& c1) {
+// col:  c[0..1] += sum_{I=I0}^{I1-1} tile(I)[row0+r][2*lane..] * x[(I-I0)*64 + row0 + r]
+template <class TileF, class Gather>
+__device__ __forceinline__ void gemv_col_g(TileF tile, int I0, int I1, const double* x, Gather gather, double& c0,
+                                           double& c1) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
+  const int off = row0 * TS + 2 * lane;
+  if (!(c_step_flags & 1)) prefetch_tiles(tile, I0, I1);
+  gather();
+  __syncthreads();
 #pragma unroll 2
   for (int I = I0; I < I1; ++I) {
-    const double* t = xtile(D, s, I, J) + row0 * TS + 2 * lane;
+    const double* t = tile(I) + off;
     double2 a[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
@@ -186,93 +225,93 @@ __device__ __forceinline__ double col_finish(double c0, double c1, double* cr) {
 }
 
 // ---- P1 / E1: [X_bb; Phi_b^T] v, v = B_s^T p gathered per b position ---------------------
-// vsrc(s, b, pos) returns (B_s^T p)_pos, b = b_off[s] + pos. Output XW: +w (b rows), -g (p rows).
+// vsrc(it, b, pos) returns (B_s^T p)_pos, b = b_off + pos. Output XW: +w (b rows), -g (p rows).
+// Xr = the rank's inverse-factor store.
 template <class Src>
-__device__ void p1_item(const DevPlan& D, int s, int I, Src vsrc, double* XW, double* sv) {
-  const int Ti = D.Ti[s], Tb = D.Tb[s], nb = D.nb[s];
+__device__ __forceinline__ void p1_item(const ItemDesc& it, const double* Xr, Src vsrc, double* XW, double* sv) {
+  const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   const int Jn = (I < Tb) ? I + 1 : Tb;
-  const int64_t bo = D.b_off[s];
-  for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x) sv[e] = (e < nb) ? vsrc(s, bo + e, e) : 0.0;
-  __syncthreads();
+  const double* X = Xr + it.a_off;
   double part[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) part[r] = 0.0;
-  gemv_row(D, s, Ti + I, Ti, Ti + Jn, sv, part);
+  gemv_row_g([&](int J) { return X + tri_off(Ti + I, J); }, Ti, Ti + Jn, sv,
+             [&] {
+               for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x)
+                 sv[e] = (e < nb) ? vsrc(it, it.b_off + e, e) : 0.0;
+             },
+             part);
   const double sum = warp_reduce8(part);
   const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
-  if ((lane & 3) == 0) XW[D.vec_off[s] + (int64_t)(Ti + I) * TS + row0 + warp_reduce8_row()] = (I < Tb) ? sum : -sum;
+  if ((lane & 3) == 0) XW[it.vec_off + (int64_t)(Ti + I) * TS + row0 + warp_reduce8_row()] = (I < Tb) ? sum : -sum;
   __syncthreads();
 }
 
 // ---- PC: Ppart[I][c] = sum_{J in chunk c} Sinv_IJ G_J,  G_g = sum_{csr e of g} gsrc(e) -----------
 template <class GS>
-__device__ void pc_item(const DevPlan& D, const StepArgs& A, const double* Sinv, int I, int c, GS gsrc, double* Ppart,
+__device__ __forceinline__ void pc_item(const DevPlan& D, const StepArgs& A, const double* Sinv, int I, int c, GS gsrc, double* Ppart,
                         double* sm) {
   const int Tc = D.Tc;
   const int J0 = c * A.ch, J1 = min(Tc, J0 + A.ch);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
-  for (int e = threadIdx.x; e < (J1 - J0) * TS; e += blockDim.x) {
-    const int64_t g = (int64_t)J0 * TS + e;
-    double val = 0.0;
-    if (g < D.nc)
-      for (int k = D.coarse_ptr[g]; k < D.coarse_ptr[g + 1]; ++k) val += gsrc(k);
-    sm[e] = val;
-  }
-  __syncthreads();
+  const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
+  const double* rowp = Sinv + ((int64_t)I * Tc) * TSZ;
   double part[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) part[r] = 0.0;
-  const double* rowp = Sinv + ((int64_t)I * Tc) * TSZ + row0 * TS + 2 * lane;
-#pragma unroll 2
-  for (int J = J0; J < J1; ++J) {
-    const double* t = rowp + (int64_t)J * TSZ;
-    const double2 xv = *reinterpret_cast<const double2*>(sm + (J - J0) * TS + 2 * lane);
-    double2 a[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
-  }
+  gemv_row_g([&](int J) { return rowp + (int64_t)J * TSZ; }, J0, J1, sm,
+             [&] {
+               for (int e = threadIdx.x; e < (J1 - J0) * TS; e += blockDim.x) {
+                 const int64_t g = (int64_t)J0 * TS + e;
+                 double val = 0.0;
+                 if (g < D.nc)
+                   for (int k = D.coarse_ptr[g]; k < D.coarse_ptr[g + 1]; ++k) val += gsrc(k);
+                 sm[e] = val;
+               }
+             },
+             part);
   const double sum = warp_reduce8(part);
   if ((lane & 3) == 0) Ppart[((int64_t)I * A.maxch + c) * TS + row0 + warp_reduce8_row()] = sum;
   __syncthreads();
 }
 
-// ---- P5 / R4: y_J = sum_{I>=J} X_bb,IJ^T w_I - sum_{p rows} PhiT_IJ^T (N Pc)_I -------------
-// Returns this item's share of v_J . y_J (vsrc gives (B_s^T p)_pos; pass zero for R4).
 #define SUBSTAMP(k) \
   if (sub) { __syncthreads(); if (threadIdx.x == 0) sub[k] = gtimer(); }
+// ---- P5 / R4: y_J = sum_{I>=J} X_bb,IJ^T w_I - sum_{p rows} PhiT_IJ^T (N Pc)_I -------------
+// Split in two items so no single item streams more than max(Tb, Tp) tiles: part 0 the X_bb^T
+// tiles (-> Y), part 1 the Phi_b tiles (-> Y2); consumers read y = Y + Y2. Returns this item's
+// share of v_J . y_J (vsrc gives (B_s^T p)_pos; pass zero for R4).
 template <class PcF, class Src>
-__device__ double p5_item(const DevPlan& D, int s, int J, const double* W, PcF pc, Src vsrc, double* Y, double* sm,
-                          double* red, unsigned long long* sub = nullptr) {
-  const int Ti = D.Ti[s], Tb = D.Tb[s], Tp = D.Tp[s], np = D.np[s], nb = D.nb[s];
-  const int Tr = Tb + (np > 0 ? Tp : 0);
-  double* sw = sm;                  // (Tr - J) * 64
-  double* cr = sm + (Tr - J) * TS;  // 8 * 64
-  const int* grp = D.p_grp + D.p_off[s];
-  const int64_t vo = D.vec_off[s] + (int64_t)Ti * TS;
+__device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, const double* W, const int* p_grp,
+                                          PcF pc, Src vsrc, double* Y, double* Y2, double* sm, double* red,
+                                          unsigned long long* sub = nullptr) {
+  const int J = it.I, Ti = it.Ti, Tb = it.Tb, np = it.np, nb = it.nb;
+  const bool ppart = it.part != 0;
+  const int I0 = ppart ? Tb : J, I1 = ppart ? Tb + it.Tp : Tb;
+  double* sw = sm;                  // (I1 - I0) * 64
+  double* cr = sm + (I1 - I0) * TS; // 8 * 64
+  const int* grp = p_grp + it.p_off;
+  const int64_t vo = it.vec_off + (int64_t)Ti * TS;
+  const double* X = Xr + it.a_off;
   // v_J entry of this thread (threads < 64), fetched early so its latency overlaps the gather
   double vj = 0.0;
-  if (threadIdx.x < TS && J * TS + (int)threadIdx.x < nb) vj = vsrc(s, D.b_off[s] + J * TS + threadIdx.x, J * TS + threadIdx.x);
-  for (int e = threadIdx.x; e < (Tr - J) * TS; e += blockDim.x) {
-    const int i = J * TS + e;  // row index in [b; p] numbering
-    double val;
-    if (i < Tb * TS) val = ldcg(W + vo + i);
-    else {
-      const int t = i - Tb * TS;
-      val = (t < np) ? -pc(grp[t]) : 0.0;
-    }
-    sw[e] = val;
-  }
-  __syncthreads();
-  SUBSTAMP(0);
+  if (threadIdx.x < TS && J * TS + (int)threadIdx.x < nb)
+    vj = vsrc(it, it.b_off + J * TS + threadIdx.x, J * TS + threadIdx.x);
   double c0 = 0.0, c1 = 0.0;
-  gemv_col(D, s, Ti + J, Ti + J, Ti + Tr, sw, c0, c1);
+  gemv_col_g([&](int I) { return X + tri_off(Ti + I, Ti + J); }, I0, I1, sw,
+             [&] {
+               for (int e = threadIdx.x; e < (I1 - I0) * TS; e += blockDim.x) {
+                 double val;
+                 if (!ppart) val = ldcg(W + vo + I0 * TS + e);
+                 else val = (e < np) ? -pc(grp[e]) : 0.0;
+                 sw[e] = val;
+               }
+             },
+             c0, c1);
   SUBSTAMP(1);
   const double acc = col_finish(c0, c1, cr);
   double contrib = 0.0;
   if (threadIdx.x < TS) {
-    Y[vo + (int64_t)J * TS + threadIdx.x] = acc;
+    (ppart ? Y2 : Y)[vo + (int64_t)J * TS + threadIdx.x] = acc;
     contrib = vj * acc;
   }
   SUBSTAMP(2);
@@ -282,30 +321,23 @@ __device__ double p5_item(const DevPlan& D, int s, int J, const double* W, PcF p
 }
 
 // ---- P7 / R5: symmetric S_bb apply, one row block I of one patch --------------------------
-// usrc(s, b, pos) returns (B_D^(s)T r)_pos. Returns this item's share of u^T S_bb u.
+// usrc(it, b, pos) returns (B_D^(s)T r)_pos. Returns this item's share of u^T S_bb u.
 template <class Src>
-__device__ double symv_item(const DevPlan& D, double* PW, int s, int I, Src usrc, double* sm, double* red) {
-  const int Ti = D.Ti[s], Tb = D.Tb[s], nb = D.nb[s];
+__device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm, double* red) {
+  const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   double* u = sm;            // Tb*64
   double* cr = u + Tb * TS;  // 9 * 64
-  const int64_t bo = D.b_off[s];
-  for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) u[i] = (i < nb) ? usrc(s, bo + i, i) : 0.0;
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
-  const double* S = D.Sbbr[D.owner[s]] + D.sbb_off[s];
+  const double* S = Sr + it.sbb_off;
   double part[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) part[q] = 0.0;
-#pragma unroll 2
-  for (int J = 0; J <= I; ++J) {  // row part: S_IJ u_J
-    const double* t = S + tri_off(I, J) + row0 * TS + 2 * lane;
-    const double2 xv = *reinterpret_cast<const double2*>(u + J * TS + 2 * lane);
-    double2 a[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = ldg2(t + q * TS);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) part[q] += a[q].x * xv.x + a[q].y * xv.y;
-  }
+  // row part: S_IJ u_J (J <= I), the u gather overlapped with the first tile's loads
+  gemv_row_g([&](int J) { return S + tri_off(I, J); }, 0, I + 1, u,
+             [&] {
+               for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) u[i] = (i < nb) ? usrc(it, it.b_off + i, i) : 0.0;
+             },
+             part);
   double c0 = 0.0, c1 = 0.0;
 #pragma unroll 2
   for (int J = I + 1; J < Tb; ++J) {  // column part: S_JI^T u_J
@@ -335,23 +367,26 @@ __device__ double symv_item(const DevPlan& D, double* PW, int s, int I, Src usrc
   double contrib = 0.0;
   if (threadIdx.x < TS) {
     const double v = cr[8 * TS + threadIdx.x];
-    PW[D.vec_off[s] + (int64_t)(Ti + I) * TS + threadIdx.x] = v;
+    PW[it.vec_off + (int64_t)(Ti + I) * TS + threadIdx.x] = v;
     contrib = u[I * TS + threadIdx.x] * v;
   }
   return block_sum(contrib, red);
 }
 
 // ---- R2: forward item (conductor patch s, aug row block I): Z_I = X_IJ f_J / f_p - Phi^T f_r --
-__device__ void fw_item(const DevPlan& D, int s, int I, const double* Fv, double* Zv, double* sm) {
-  const int Tr = D.Ti[s] + D.Tb[s];
+__device__ __forceinline__ void fw_item(const ItemDesc& it, const double* Xr, const double* Fv, double* Zv, double* sm) {
+  const int I = it.I, Tr = it.Ti + it.Tb;
   const int Jn = (I < Tr) ? I + 1 : Tr;
-  const int64_t vo = D.vec_off[s];
-  for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x) sm[e] = ldcg(Fv + vo + e);
-  __syncthreads();
+  const int64_t vo = it.vec_off;
+  const double* X = Xr + it.a_off;
   double part[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) part[r] = 0.0;
-  gemv_row(D, s, I, 0, Jn, sm, part);
+  gemv_row_g([&](int J) { return X + tri_off(I, J); }, 0, Jn, sm,
+             [&] {
+               for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x) sm[e] = ldcg(Fv + vo + e);
+             },
+             part);
   const double sum = warp_reduce8(part);
   const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
   if ((lane & 3) == 0) {
@@ -363,28 +398,31 @@ __device__ void fw_item(const DevPlan& D, int s, int I, const double* Fv, double
 
 // ---- E3: backward item (patch s, r column block J): a_J = X_rr^T u - Phi N Pc, scattered ----
 template <class PcF>
-__device__ void bw_item(const DevPlan& D, int s, int J, const double* Zv, const double* XWv, PcF pc, double* a_loc,
-                        int nloc, double* sm) {
-  const int Ti = D.Ti[s], Tr = Ti + D.Tb[s], T = D.T[s], np = D.np[s];
-  const int64_t vo = D.vec_off[s];
-  const int* grp = D.p_grp + D.p_off[s];
+__device__ __forceinline__ void bw_item(const DevPlan& D, const ItemDesc& it, const double* Xr, const double* Zv, const double* XWv,
+                        PcF pc, double* a_loc, int nloc, double* sm) {
+  const int s = it.s, J = it.I, Ti = it.Ti, Tr = Ti + it.Tb, T = it.T, np = it.np;
+  const int64_t vo = it.vec_off;
+  const int* grp = D.p_grp + it.p_off;
   const int* aug = D.aug + D.aug_off[s];
+  const double* X = Xr + it.a_off;
   double* sx = sm;                 // (T - J) * 64
   double* cr = sm + (T - J) * TS;  // 8 * 64
-  for (int e = threadIdx.x; e < (T - J) * TS; e += blockDim.x) {
-    const int i = J * TS + e;
-    double val;
-    if (i < Ti * TS) val = ldcg(Zv + vo + i);
-    else if (i < Tr * TS) val = ldcg(Zv + vo + i) - ldcg(XWv + vo + i);
-    else {
-      const int t = i - Tr * TS;
-      val = (t < np) ? -pc(grp[t]) : 0.0;
-    }
-    sx[e] = val;
-  }
-  __syncthreads();
   double c0 = 0.0, c1 = 0.0;
-  gemv_col(D, s, J, J, T, sx, c0, c1);
+  gemv_col_g([&](int I) { return X + tri_off(I, J); }, J, T, sx,
+             [&] {
+               for (int e = threadIdx.x; e < (T - J) * TS; e += blockDim.x) {
+                 const int i = J * TS + e;
+                 double val;
+                 if (i < Ti * TS) val = ldcg(Zv + vo + i);
+                 else if (i < Tr * TS) val = ldcg(Zv + vo + i) - ldcg(XWv + vo + i);
+                 else {
+                   const int t = i - Tr * TS;
+                   val = (t < np) ? -pc(grp[t]) : 0.0;
+                 }
+                 sx[e] = val;
+               }
+             },
+             c0, c1);
   const double acc = col_finish(c0, c1, cr);
   double* as = a_loc + (int64_t)s * nloc;
   if (threadIdx.x < TS) {
@@ -497,14 +535,15 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
 // rhs item (R1). c in {0,1,2}: component c of conductor patch s, F = (sigma/dt) M a + phi j_S
 // with the mass apply sum-factorised (M_c = F_z (x) F_y (x) F_x, F_d = Md along d == c, Mb else;
 // banded |i-i'| <= p) through shared memory; c = -1: insulator patch s, Z = phi(t) XJ.
-__device__ void rhs_item(const DevPlan& D, const StepArgs& A, int me, int s, int c, double t, double* sm) {
+__device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, int me, const ItemDesc& it, double t, double* sm) {
+  const int s = it.s, c = it.I;
   const double sig = D.sigma[s], nu = D.nu[s];
   double phi = 0.0;
   if (A.source == 1) phi = sinpi(2.0 * t);
   else if (A.source == 2) phi = 2.0 * M_PI * M_PI * nu * (1.0 - exp(-t)) + sig * exp(-t);
-  const int64_t vo = D.vec_off[s];
+  const int64_t vo = it.vec_off;
   if (c < 0) {
-    const int R = D.T[s] * TS;
+    const int R = it.T * TS;
     for (int pos = threadIdx.x; pos < R; pos += blockDim.x) A.Z[me][vo + pos] = phi * ldcg(A.XJ[me] + vo + pos);
     return;
   }
@@ -550,17 +589,23 @@ __device__ void rhs_item(const DevPlan& D, const StepArgs& A, int me, int s, int
   __syncthreads();
 }
 
+
 #define TSTAMP(slot) \
   if (A.tstamp && me == 0 && bl == 0 && threadIdx.x == 0 && it < 64 && step == 0) A.tstamp[it * 8 + (slot)] = gtimer()
 // step-level stamps of step 0 (slots 512..527): R1..R5 ends, loop end, E1..E3 ends
 #define SSTAMP(slot) \
   if (A.tstamp && me == 0 && bl == 0 && threadIdx.x == 0 && step == 0) A.tstamp[512 + (slot)] = gtimer()
 // per-block work-end stamps of PCG iteration 2 of step 0 (slots 528 + 8*block + phase)
-#define WSTAMP(slot)                                                        \
-  if (A.tstamp && step == 0 && it == 2) {                                   \
-    __syncthreads();                                                        \
-    if (threadIdx.x == 0 && gb < 4096) A.tstamp[528 + gb * 8 + (slot)] = gtimer(); \
+#define WSTAMP(slot)                                                                   \
+  if (A.tstamp && step == 0 && it == 2) {                                              \
+    __syncthreads();                                                                   \
+    if (threadIdx.x == 0 && gb < 4096) A.tstamp[528 + gb * 8 + (slot)] = gtimer();     \
   }
+
+// loop over this block's items of phase ph (shared-memory copy or global list)
+#define FOR_ITEMS(ph, var)                                  \
+  for (int j_##var = 0; j_##var < s_icnt[ph]; ++j_##var)    \
+    if (const ItemDesc& var = s_ip[ph][j_##var]; true)
 
 // =======================================================================================
 // Persistent cooperative time stepper: A.nsteps implicit-Euler steps in one launch, over
@@ -569,38 +614,73 @@ __device__ void rhs_item(const DevPlan& D, const StepArgs& A, int me, int s, int
 // =======================================================================================
 template <bool MULTI>
 __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   __shared__ double red[NTHR];
   __shared__ double bcast[NTHR / 32];
+  __shared__ const ItemDesc* s_ip[NPH];
+  __shared__ int s_icnt[NPH];
+  __shared__ const LamC* s_lc;
   // MULTI = false: one rank, every owner lookup folds to rank 0 at compile time
   const int me = MULTI ? A.rank_base + (int)blockIdx.x / A.nbr : 0;  // this block's rank
   const int bl = MULTI ? (int)blockIdx.x % A.nbr : (int)blockIdx.x;   // block index within the rank
-  const int NB = A.nbr;
   const int64_t m = D.m;
   const int64_t gb = (int64_t)me * A.nbr + bl;
   const int64_t k0 = min(m, gb * A.lam_chunk), k1 = min(m, k0 + A.lam_chunk);
+  const int nk = (int)(k1 - k0);
   unsigned int round = A.round0;
+  const double* Xr = D.Ar[me];
+  const double* Sr = D.Sbbr[me];
+  // ---- per-launch setup: item lists (and lambda-chunk index data) into shared memory ----
+  {
+    ItemDesc* ic = reinterpret_cast<ItemDesc*>(sm + A.scratch);
+    int pos = 0;
+#pragma unroll
+    for (int ph = 0; ph < NPH; ++ph)  // constant indices: no local copy of the parameter block
+      if (threadIdx.x == ph) {
+        const int b = A.boff[ph][gb], e = A.boff[ph][gb + 1];
+        s_icnt[ph] = e - b;
+        s_ip[ph] = A.items[ph] + b;
+      }
+    __syncthreads();
+    if (A.cache_items) {
+      for (int ph = 0; ph < NCACHE; ++ph) {
+        const int n = s_icnt[ph];
+        const int4* src = reinterpret_cast<const int4*>(s_ip[ph]);
+        int4* dst = reinterpret_cast<int4*>(ic + pos);
+        for (int q = threadIdx.x; q < n * (int)(sizeof(ItemDesc) / 16); q += blockDim.x) dst[q] = src[q];
+        __syncthreads();
+        if (threadIdx.x == 0) s_ip[ph] = ic + pos;
+        pos += n;
+      }
+    }
+    LamC* lc = reinterpret_cast<LamC*>(ic + pos);
+    if (A.cache_lam) {
+      for (int q = threadIdx.x; q < nk; q += blockDim.x) {
+        const int64_t k = k0 + q;
+        lc[q] = LamC{D.lam_idx_p[k], D.lam_idx_m[k], D.wplus[k], D.wminus[k], D.lam_patch_p[k], D.lam_patch_m[k]};
+      }
+    }
+    if (threadIdx.x == 0) s_lc = A.cache_lam ? lc : nullptr;
+    __syncthreads();
+  }
+  const LamC* lc = s_lc;
+  auto lidx_p = [&](int64_t k) { return lc ? lc[k - k0].ip : D.lam_idx_p[k]; };
+  auto lidx_m = [&](int64_t k) { return lc ? lc[k - k0].im : D.lam_idx_m[k]; };
+  auto lw_p = [&](int64_t k) { return lc ? lc[k - k0].wp : D.wplus[k]; };
+  auto lw_m = [&](int64_t k) { return lc ? lc[k - k0].wm : D.wminus[k]; };
+  auto lpat_p = [&](int64_t k) { return MULTI ? (lc ? lc[k - k0].pp : D.lam_patch_p[k]) : 0; };
+  auto lpat_m = [&](int64_t k) { return MULTI ? (lc ? lc[k - k0].pm : D.lam_patch_m[k]) : 0; };
   auto lown = [&](int64_t k) { return MULTI ? ((int)k / (int)A.lam_chunk) / A.nbr : 0; };
   auto pown = [&](int s) { return MULTI ? D.owner[s] : 0; };
-  auto own_idx = [&](int s, int pos) { return D.vec_off[s] + (int64_t)D.Ti[s] * TS + pos; };
+  auto own_idx = [&](const ItemDesc& it, int pos) { return it.vec_off + (int64_t)it.Ti * TS + pos; };
   auto pcf = [&](int64_t g) { return pc_get<MULTI>(A, g); };
+  auto yv = [&](int o, int64_t i) { return ldcg(A.Y[o] + i) + ldcg(A.Y2[o] + i); };  // y = Y + Y2
   // partner patch of b position bb (other endpoint of its multiplier)
   auto ppatch = [&](int64_t bb) {
     if (!MULTI) return 0;
     const int k = D.b_lam[bb];
     return D.b_sign[bb] > 0 ? D.lam_patch_m[k] : D.lam_patch_p[k];
   };
-  // item ranges of this rank
-#define RANGE(name) const int name##_b = A.off_##name[me], name##_e = A.off_##name[me + 1]
-  RANGE(p1);
-  RANGE(p5);
-  RANGE(sy);
-  RANGE(pc);
-  RANGE(fw);
-  RANGE(bw);
-  RANGE(bwc);
-  RANGE(rhs);
-#undef RANGE
   int64_t hoff = A.hist_off;
   int total_status = 0;
 
@@ -609,38 +689,38 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     int it = 0;
     SSTAMP(0);
     // ---- R1 rhs ----
-    for (int i = rhs_b + bl; i < rhs_e; i += NB) rhs_item(D, A, me, A.it_rhs[i].x, A.it_rhs[i].y, t, sm);
+    FOR_ITEMS(PH_RHS, w) rhs_item(D, A, me, w, t, sm);
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(1);
     // ---- R2 forward (conductors) ----
-    for (int i = fw_b + bl; i < fw_e; i += NB) fw_item(D, A.it_fw[i].x, A.it_fw[i].y, A.F[me], A.Z[me], sm);
+    FOR_ITEMS(PH_FW, w) fw_item(w, Xr, A.F[me], A.Z[me], sm);
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(2);
     // ---- R3 p0 = S_pp^-1 sum N^T Z_p ----
-    for (int i = pc_b + bl; i < pc_e; i += NB)
-      pc_item(D, A, A.Sinv[me], A.it_pc[i].x, A.it_pc[i].y,
-              [&](int e) { return ldcg(A.Z[pown(D.coarse_patch[e])] + D.coarse_idx[e]); }, A.Ppart[me], sm);
+    FOR_ITEMS(PH_PC, w)
+      pc_item(D, A, A.Sinv[me], w.s, w.I, [&](int e) { return ldcg(A.Z[pown(D.coarse_patch[e])] + D.coarse_idx[e]); },
+              A.Ppart[me], sm);
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(3);
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
-    for (int i = p5_b + bl; i < p5_e; i += NB)
-      p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.Z[me], pcf, [&](int, int64_t, int) { return 0.0; }, A.Y[me], sm, red);
+    FOR_ITEMS(PH_P5, w)
+      p5_item(w, Xr, A.Z[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], sm,
+              red);
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(4);
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
     double rho0;
     {
       double loc = 0.0;
-      for (int i = sy_b + bl; i < sy_e; i += NB)
-        loc += symv_item(D, A.PW[me], A.it_sy[i].x, A.it_sy[i].y,
-                         [&](int s, int64_t bb, int pos) {
+      FOR_ITEMS(PH_SY, w)
+        loc += symv_item(w, Sr, A.PW[me],
+                         [&](const ItemDesc& iw, int64_t bb, int pos) {
                            return D.b_aown[bb] *
-                                  (ldcg(A.Y[me] + own_idx(s, pos)) - ldcg(A.Y[pown(ppatch(bb))] + D.b_part[bb]));
+                                  (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), D.b_part[bb]));
                          },
                          sm, red);
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-        A.r[0][me][k] = ldcg(A.Y[pown(D.lam_patch_p[k])] + D.lam_idx_p[k]) -
-                        ldcg(A.Y[pown(D.lam_patch_m[k])] + D.lam_idx_m[k]);
+        A.r[0][me][k] = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
         A.pk[0][me][k] = 0.0;
         A.lam[me][k] = 0.0;
       }
@@ -659,23 +739,32 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       double* const* pprev = A.pk[pp];
       double* pcur = A.pk[pp ^ 1][me];
       // P1: p = z + beta p_prev on the fly; v = B^T p; w = X_bb v, -g = -Phi^T v; owners store p
-      auto vnew = [&](int s, int64_t bb, int pos) {
-        const int k = D.b_lam[bb];
-        return D.b_aown[bb] * ldcg(A.PW[me] + own_idx(s, pos)) +
-               D.b_apart[bb] * ldcg(A.PW[pown(ppatch(bb))] + D.b_part[bb]) +
-               D.b_sign[bb] * beta * ldcg(pprev[lown(k)] + k);
-      };
-      for (int i = p1_b + bl; i < p1_e; i += NB) p1_item(D, A.it_p1[i].x, A.it_p1[i].y, vnew, A.XW[me], sm);
-      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
-        pcur[k] = D.wplus[k] * ldcg(A.PW[pown(D.lam_patch_p[k])] + D.lam_idx_p[k]) -
-                  D.wminus[k] * ldcg(A.PW[pown(D.lam_patch_m[k])] + D.lam_idx_m[k]) + beta * ldcg(pprev[me] + k);
+      {
+        // the block's own lambda chunk first (independent loads in flight before the items)
+        double pv = 0.0;
+        const int64_t kq = k0 + threadIdx.x;
+        if (kq < k1)
+          pv = lw_p(kq) * ldcg(A.PW[pown(lpat_p(kq))] + lidx_p(kq)) -
+               lw_m(kq) * ldcg(A.PW[pown(lpat_m(kq))] + lidx_m(kq)) + beta * ldcg(pprev[me] + kq);
+        auto vnew = [&](const ItemDesc& iw, int64_t bb, int pos) {
+          const int k = D.b_lam[bb];
+          return D.b_aown[bb] * ldcg(A.PW[me] + own_idx(iw, pos)) +
+                 D.b_apart[bb] * ldcg(A.PW[pown(ppatch(bb))] + D.b_part[bb]) +
+                 D.b_sign[bb] * beta * ldcg(pprev[lown(k)] + k);
+        };
+        FOR_ITEMS(PH_P1, w) p1_item(w, Xr, vnew, A.XW[me], sm);
+        if (kq < k1) pcur[kq] = pv;
+        for (int64_t k = kq + blockDim.x; k < k1; k += blockDim.x)
+          pcur[k] = lw_p(k) * ldcg(A.PW[pown(lpat_p(k))] + lidx_p(k)) -
+                    lw_m(k) * ldcg(A.PW[pown(lpat_m(k))] + lidx_m(k)) + beta * ldcg(pprev[me] + k);
+      }
       WSTAMP(0);
       grid_barrier(A, me, bl, round, false, 0.0, bcast);
       TSTAMP(1);
       // PC
-      for (int i = pc_b + bl; i < pc_e; i += NB)
-        pc_item(D, A, A.Sinv[me], A.it_pc[i].x, A.it_pc[i].y,
-                [&](int e) { return ldcg(A.XW[pown(D.coarse_patch[e])] + D.coarse_idx[e]); }, A.Ppart[me], sm);
+      FOR_ITEMS(PH_PC, w)
+        pc_item(D, A, A.Sinv[me], w.s, w.I, [&](int e) { return ldcg(A.XW[pown(D.coarse_patch[e])] + D.coarse_idx[e]); },
+                A.Ppart[me], sm);
       WSTAMP(1);
       grid_barrier(A, me, bl, round, false, 0.0, bcast);
       TSTAMP(2);
@@ -684,13 +773,13 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       double pq;
       {
         double loc = 0.0;
-        for (int i = p5_b + bl; i < p5_e; i += NB)
-          loc += p5_item(D, A.it_p5[i].x, A.it_p5[i].y, A.XW[me], pcf,
-                         [&](int, int64_t bb, int) {
+        FOR_ITEMS(PH_P5, w)
+          loc += p5_item(w, Xr, A.XW[me], D.p_grp, pcf,
+                         [&](const ItemDesc&, int64_t bb, int) {
                            const int k = D.b_lam[bb];
                            return D.b_sign[bb] * ldcg(pcurt[lown(k)] + k);
                          },
-                         A.Y[me], sm, red,
+                         A.Y[me], A.Y2[me], sm, red,
                          (A.tstamp && step == 0 && it == 2 && gb < 4096) ? A.tstamp + 528 + gb * 8 + 4 : nullptr);
         WSTAMP(2);
         pq = grid_barrier(A, me, bl, round, true, loc, bcast);
@@ -700,20 +789,19 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       const double alpha = rho / pq;
       double* const* rc = A.r[rp];
       double* rn = A.r[rp ^ 1][me];
-      auto unew = [&](int s, int64_t bb, int pos) {
+      auto unew = [&](const ItemDesc& iw, int64_t bb, int pos) {
         const int k = D.b_lam[bb];
         return D.b_aown[bb] * (D.b_sign[bb] * ldcg(rc[lown(k)] + k) -
-                               alpha * (ldcg(A.Y[me] + own_idx(s, pos)) - ldcg(A.Y[pown(ppatch(bb))] + D.b_part[bb])));
+                               alpha * (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), D.b_part[bb])));
       };
       // P7 (+ partial r^T z)
       {
         for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
           A.lam[me][k] += alpha * ldcg(pcur + k);
-          rn[k] = ldcg(rc[me] + k) - alpha * (ldcg(A.Y[pown(D.lam_patch_p[k])] + D.lam_idx_p[k]) -
-                                              ldcg(A.Y[pown(D.lam_patch_m[k])] + D.lam_idx_m[k]));
+          rn[k] = ldcg(rc[me] + k) - alpha * (yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k)));
         }
         double loc = 0.0;
-        for (int i = sy_b + bl; i < sy_e; i += NB) loc += symv_item(D, A.PW[me], A.it_sy[i].x, A.it_sy[i].y, unew, sm, red);
+        FOR_ITEMS(PH_SY, w) loc += symv_item(w, Sr, A.PW[me], unew, sm, red);
         WSTAMP(3);
         rz = grid_barrier(A, me, bl, round, true, loc, bcast);
       }
@@ -746,9 +834,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     hoff += it + 1;
     SSTAMP(6);
     // ---- E1 v = B^T lambda ; w, -Phi^T v ----
-    for (int i = p1_b + bl; i < p1_e; i += NB)
-      p1_item(D, A.it_p1[i].x, A.it_p1[i].y,
-              [&](int, int64_t bb, int) {
+    FOR_ITEMS(PH_P1, w)
+      p1_item(w, Xr,
+              [&](const ItemDesc&, int64_t bb, int) {
                 const int k = D.b_lam[bb];
                 return D.b_sign[bb] * ldcg(A.lam[lown(k)] + k);
               },
@@ -756,8 +844,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(7);
     // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
-    for (int i = pc_b + bl; i < pc_e; i += NB)
-      pc_item(D, A, A.Sinv[me], A.it_pc[i].x, A.it_pc[i].y,
+    FOR_ITEMS(PH_PC, w)
+      pc_item(D, A, A.Sinv[me], w.s, w.I,
               [&](int e) {
                 const int o = pown(D.coarse_patch[e]);
                 return ldcg(A.Z[o] + D.coarse_idx[e]) - ldcg(A.XW[o] + D.coarse_idx[e]);
@@ -767,12 +855,10 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     SSTAMP(8);
     // ---- E3 a_r = X_rr^T (Z_r - [0; w_b]) - Phi N p, a_p = N p ----
     // insulator coefficients feed no later step (no mass term): recover them only at the last step
-    {
-      const bool last = (step == A.nsteps - 1);
-      const int2* itb = last ? A.it_bw : A.it_bwc;
-      const int ib = last ? bw_b : bwc_b, ie = last ? bw_e : bwc_e;
-      for (int i = ib + bl; i < ie; i += NB)
-        bw_item(D, itb[i].x, itb[i].y, A.Z[me], A.XW[me], pcf, A.a_loc[me], A.G.nloc, sm);
+    if (step == A.nsteps - 1) {
+      FOR_ITEMS(PH_BW, w) bw_item(D, w, Xr, A.Z[me], A.XW[me], pcf, A.a_loc[me], A.G.nloc, sm);
+    } else {
+      FOR_ITEMS(PH_BWC, w) bw_item(D, w, Xr, A.Z[me], A.XW[me], pcf, A.a_loc[me], A.G.nloc, sm);
     }
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(9);
@@ -787,42 +873,44 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
 
 // ---- standalone item kernels (setup precompute, F-apply benchmark), single rank: one item
 // per block over the given item range.
-__global__ void __launch_bounds__(NTHR) k_fw(DevPlan D, const int2* items, int n, const double* Fv, double* Zv) {
-  extern __shared__ double sm[];
+__global__ void __launch_bounds__(NTHR) k_fw(DevPlan D, const ItemDesc* items, int n, const double* Fv, double* Zv) {
+  extern __shared__ __align__(16) double sm[];
   if (blockIdx.x >= n) return;
-  fw_item(D, items[blockIdx.x].x, items[blockIdx.x].y, Fv, Zv, sm);
+  fw_item(items[blockIdx.x], D.A, Fv, Zv, sm);
 }
-__global__ void __launch_bounds__(NTHR) k_p1_lam(DevPlan D, const int2* items, int n, const double* __restrict__ lam,
+__global__ void __launch_bounds__(NTHR) k_p1_lam(DevPlan D, const ItemDesc* items, int n, const double* __restrict__ lam,
                                                  double* XW) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   if (blockIdx.x >= n) return;
-  p1_item(D, items[blockIdx.x].x, items[blockIdx.x].y,
-          [&](int, int64_t bb, int) { return D.b_sign[bb] * lam[D.b_lam[bb]]; }, XW, sm);
+  p1_item(items[blockIdx.x], D.A, [&](const ItemDesc&, int64_t bb, int) { return D.b_sign[bb] * lam[D.b_lam[bb]]; },
+          XW, sm);
 }
-__global__ void __launch_bounds__(NTHR) k_pc(DevPlan D, StepArgs A, const int2* items, int n, const double* src,
+__global__ void __launch_bounds__(NTHR) k_pc(DevPlan D, StepArgs A, const ItemDesc* items, int n, const double* src,
                                              double* Ppart) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   if (blockIdx.x >= n) return;
-  pc_item(D, A, A.Sinv[0], items[blockIdx.x].x, items[blockIdx.x].y, [&](int e) { return ldcg(src + D.coarse_idx[e]); },
+  pc_item(D, A, A.Sinv[0], items[blockIdx.x].s, items[blockIdx.x].I, [&](int e) { return ldcg(src + D.coarse_idx[e]); },
           Ppart, sm);
 }
 __global__ void k_pc_sum(DevPlan D, StepArgs A, double* Pc) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D.nc; g += (int64_t)gridDim.x * blockDim.x)
     Pc[g] = pc_get<true>(A, g);
 }
-__global__ void __launch_bounds__(NTHR) k_p5(DevPlan D, const int2* items, int n, const double* W, const double* Pc,
-                                             double* Y) {
-  extern __shared__ double sm[];
+__global__ void __launch_bounds__(NTHR) k_p5(DevPlan D, const ItemDesc* items, int n, const double* W, const double* Pc,
+                                             double* Y, double* Y2) {
+  extern __shared__ __align__(16) double sm[];
   __shared__ double red[NTHR];
   if (blockIdx.x >= n) return;
-  p5_item(D, items[blockIdx.x].x, items[blockIdx.x].y, W, [&](int64_t g) { return ldcg(Pc + g); },
-          [&](int, int64_t, int) { return 0.0; }, Y, sm, red);
+  p5_item(items[blockIdx.x], D.A, W, D.p_grp, [&](int64_t g) { return ldcg(Pc + g); },
+          [&](const ItemDesc&, int64_t, int) { return 0.0; }, Y, Y2, sm, red);
 }
-// q = B y (F-apply benchmark output)
-__global__ void k_jump(DevPlan D, const double* Y, double* q) {
+// q = B y (F-apply benchmark output), y = Y + Y2
+__global__ void k_jump(DevPlan D, const double* Y, const double* Y2, double* q) {
   const int64_t m = D.m;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x)
-    q[k] = ldcg(Y + D.lam_idx_p[k]) - ldcg(Y + D.lam_idx_m[k]);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ip = D.lam_idx_p[k], im = D.lam_idx_m[k];
+    q[k] = (ldcg(Y + ip) + ldcg(Y2 + ip)) - (ldcg(Y + im) + ldcg(Y2 + im));
+  }
 }
 
 }  // namespace tcg

@@ -30,11 +30,11 @@ for name in sys.argv[1:] or ["cfg2"]:
         print(f"  it2 {names[ph]:14s} work {1e-3*(we.max()-start[ph]):6.2f}  median-block work {1e-3*(np.median(we)-start[ph]):6.2f}"
               f"  min {1e-3*(we.min()-start[ph]):6.2f}  bar {1e-3*(release-we.max()):6.2f} us  (blocks {nb})")
     sub = out[528:].reshape(4096, 8)[:nb, 4:8]
-    has = sub[:, 0] > 0
+    has = sub[:, 1] > 0
     if has.any():
         st = start[2]
         q = (sub[has] - st) / 1000.0
-        print("  it2 P5 sub-stamps (us from phase start; max / median over item blocks): gathered, gemv, Y-write, block_sum:",
+        print("  it2 P5 sub-stamps (us from phase start; max / median over item blocks): -, gather+gemv, Y-write, block_sum:",
               np.round(q.max(axis=0), 2), np.round(np.median(q, axis=0), 2), "item blocks", int(has.sum()))
     inf = s.info(); print("  steps ms", inf["ms_steps"], "ms/step", inf["ms_steps"] / 2)
     s.close()
