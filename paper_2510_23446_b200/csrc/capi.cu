@@ -146,7 +146,8 @@ struct tcg_ctx {
   ItemDesc* d_items[NPH] = {};
   int* d_boff[NPH] = {};
   std::vector<int> h_boff[NPH];
-  int cache_items = 0, cache_lam = 0;
+  int cache_items = 0, cache_lam = 0, cache_pcprog = 0;
+  int64_t* d_pcprog = nullptr;
   size_t smem_steps = 0;  // dynamic shared memory of k_steps: item scratch + caches
   int coarse_ch = 1, coarse_maxch = 1;
   size_t smem_pcg = 0, smem_tables = 0;
@@ -556,6 +557,10 @@ static tcg_status do_setup(tcg_ctx* h) {
   TRY(do_plan(h));
   Plan& pl = h->plan;
   CK(cudaSetDevice(h->device));
+  if (const char* pe = getenv("TCG_ALLOC_PAD_KB")) {  // experiment: shift the device-memory layout
+    char* pad;
+    TRY(dalloc(h, &pad, (size_t)atoll(pe) * 1024));
+  }
   {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, h->device));
@@ -859,11 +864,34 @@ static tcg_status do_setup(tcg_ctx* h) {
       for (int I = 0; I < Tb[s]; ++I) sy.per_rank[r].push_back({Tb[s], desc(s, I)});
     }
     const int ch = h->coarse_ch;
+    // PC gather programs (one per column chunk; shared by the chunk's row-block items)
+    std::vector<int64_t> prog;
+    std::vector<int64_t> prog_off(h->coarse_maxch), prog_len(h->coarse_maxch);
+    for (int c = 0; c < h->coarse_maxch; ++c) {
+      const int J0 = c * ch, J1 = std::min(Tc, J0 + ch);
+      const int nE = (J1 - J0) * TS;
+      prog_off[c] = (int64_t)prog.size();
+      std::vector<int64_t> offs(nE + 1, 0), ent;
+      for (int e = 0; e < nE; ++e) {
+        const int64_t g = (int64_t)J0 * TS + e;
+        if (g < pl.nc)
+          for (int k = pl.coarse_ptr[g]; k < pl.coarse_ptr[g + 1]; ++k)
+            ent.push_back(cidx[k] | ((int64_t)owner[cpat[k]] << 56));
+        offs[e + 1] = (int64_t)ent.size();
+      }
+      prog.insert(prog.end(), offs.begin(), offs.end());
+      prog.insert(prog.end(), ent.begin(), ent.end());
+      prog_len[c] = (int64_t)prog.size() - prog_off[c];
+    }
+    if (prog.empty()) prog.push_back(0);
+    TRY(dupload(h, &h->d_pcprog, prog));
     for (int I = 0; I < Tc; ++I)
       for (int c = 0; c < h->coarse_maxch; ++c) {
         ItemDesc d{};
         d.s = I;
         d.I = c;
+        d.vec_off = prog_off[c];
+        d.b_off = prog_len[c];
         pcv.per_rank[crow_owner[I]].push_back({std::min(Tc, (c + 1) * ch) - c * ch, d});
       }
     // fixed per-item overhead (tile units) of the latency-bound item phases
@@ -887,6 +915,19 @@ static tcg_status do_setup(tcg_ctx* h) {
       max_items = std::max(max_items, n);
     }
     const size_t items_b = (size_t)max_items * sizeof(ItemDesc);
+    int64_t max_prog = 0;
+    {
+      std::vector<ItemDesc> hp;  // host copy of the PC item list (ordered like the device one)
+      hp.resize(h->h_boff[PH_PC].back());
+      if (!hp.empty())
+        CK(cudaMemcpy(hp.data(), h->d_items[PH_PC], hp.size() * sizeof(ItemDesc), cudaMemcpyDeviceToHost));
+      for (int gb = 0; gb < NR * h->nbr; ++gb) {
+        int64_t n = 0;
+        for (int j = h->h_boff[PH_PC][gb]; j < h->h_boff[PH_PC][gb + 1]; ++j) n += hp[j].b_off;
+        max_prog = std::max<int64_t>(max_prog, (n + 1) & ~(int64_t)1);
+      }
+    }
+    const size_t prog_b = (size_t)max_prog * sizeof(int64_t);
     const size_t lam_b = (size_t)h->lam_chunk * sizeof(LamC);
     int smem_sm = 0, reserved = 0;
     CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
@@ -897,8 +938,10 @@ static tcg_status do_setup(tcg_ctx* h) {
     const char* ev = getenv("TCG_NO_SMEM_CACHE");
     const bool allow = !(ev && atoi(ev) != 0);
     h->cache_items = allow && (int64_t)(h->smem_pcg + items_b) <= budget && items_b <= 48 * 1024;
-    h->cache_lam = allow && (int64_t)(h->smem_pcg + (h->cache_items ? items_b : 0) + lam_b) <= budget && lam_b <= 32 * 1024;
-    h->smem_steps = h->smem_pcg + (h->cache_items ? items_b : 0) + (h->cache_lam ? lam_b : 0);
+    h->cache_pcprog = allow && h->cache_items && (int64_t)(h->smem_pcg + items_b + prog_b) <= budget && prog_b <= 32 * 1024;
+    const size_t used = h->smem_pcg + (h->cache_items ? items_b : 0) + (h->cache_pcprog ? prog_b : 0);
+    h->cache_lam = allow && (int64_t)(used + lam_b) <= budget && lam_b <= 32 * 1024;
+    h->smem_steps = used + (h->cache_lam ? lam_b : 0);
     TRY(set_smem(h, (const void*)k_steps<false>, h->smem_steps));
     TRY(set_smem(h, (const void*)k_steps<true>, h->smem_steps));
     int occ = 0;
@@ -1128,6 +1171,8 @@ static StepArgs step_args(tcg_ctx* h) {
     A.boff[ph] = h->d_boff[ph];
   }
   A.cache_items = h->cache_items;
+  A.cache_pcprog = h->cache_pcprog;
+  A.pcprog = h->d_pcprog;
   A.cache_lam = h->cache_lam;
   A.scratch = (int)(h->smem_pcg / sizeof(double));
   A.tstamp = h->tstamp;

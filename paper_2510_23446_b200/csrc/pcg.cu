@@ -85,6 +85,8 @@ struct StepArgs {
   // work items per phase: block gb = rank * nbr + bl owns items[ph][boff[ph][gb] .. boff[ph][gb+1])
   const ItemDesc* items[NPH];
   const int* boff[NPH];
+  const int64_t* pcprog;  // PC gather programs: per item offs[nE+1], then (owner << 56 | aug index)
+  int cache_pcprog;  // 1: the block's PC programs are copied to shared memory
   int cache_items;  // 1: the block's per-iteration item lists are copied to shared memory
   int cache_lam;    // 1: the block's lambda-chunk index data are copied to shared memory
   int scratch;      // doubles of item scratch at the start of dynamic shared memory (even)
@@ -248,11 +250,16 @@ __device__ __forceinline__ void p1_item(const ItemDesc& it, const double* Xr, Sr
 }
 
 // ---- PC: Ppart[I][c] = sum_{J in chunk c} Sinv_IJ G_J,  G_g = sum_{csr e of g} gsrc(e) -----------
+// prog: this item's gather program: offs[0..nE] (relative to the entry list), then one
+// entry (owner rank << 56 | aug-vector index) per csr element of the chunk's groups.
+constexpr int64_t kIdxMask = (1ll << 56) - 1;
 template <class GS>
-__device__ __forceinline__ void pc_item(const DevPlan& D, const StepArgs& A, const double* Sinv, int I, int c, GS gsrc, double* Ppart,
-                        double* sm) {
+__device__ __forceinline__ void pc_item(const DevPlan& D, const StepArgs& A, const double* Sinv, int I, int c,
+                                        const int64_t* prog, GS gsrc, double* Ppart, double* sm) {
   const int Tc = D.Tc;
   const int J0 = c * A.ch, J1 = min(Tc, J0 + A.ch);
+  const int nE = (J1 - J0) * TS;
+  const int64_t* ent = prog + nE + 1;
   const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
   const double* rowp = Sinv + ((int64_t)I * Tc) * TSZ;
   double part[8];
@@ -260,11 +267,13 @@ __device__ __forceinline__ void pc_item(const DevPlan& D, const StepArgs& A, con
   for (int r = 0; r < 8; ++r) part[r] = 0.0;
   gemv_row_g([&](int J) { return rowp + (int64_t)J * TSZ; }, J0, J1, sm,
              [&] {
-               for (int e = threadIdx.x; e < (J1 - J0) * TS; e += blockDim.x) {
-                 const int64_t g = (int64_t)J0 * TS + e;
+               for (int e = threadIdx.x; e < nE; e += blockDim.x) {
+                 const int q0 = (int)prog[e], q1 = (int)prog[e + 1];
                  double val = 0.0;
-                 if (g < D.nc)
-                   for (int k = D.coarse_ptr[g]; k < D.coarse_ptr[g + 1]; ++k) val += gsrc(k);
+                 for (int q = q0; q < q1; ++q) {
+                   const int64_t v = ent[q];
+                   val += gsrc(v & kIdxMask, (int)(v >> 56));
+                 }
                  sm[e] = val;
                }
              },
@@ -602,6 +611,16 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
     if (threadIdx.x == 0 && gb < 4096) A.tstamp[528 + gb * 8 + (slot)] = gtimer();     \
   }
 
+// the coarse phase: this block's PC items with their gather programs (shared or global)
+#define PC_PHASE(GS)                                                                      \
+  {                                                                                       \
+    int64_t po = 0;                                                                       \
+    FOR_ITEMS(PH_PC, w) {                                                                 \
+      const int64_t* prog = s_pcbase ? s_pcbase + po : A.pcprog + w.vec_off;              \
+      po += w.b_off;                                                                      \
+      pc_item(D, A, A.Sinv[me], w.s, w.I, prog, GS, A.Ppart[me], sm);                     \
+    }                                                                                     \
+  }
 // loop over this block's items of phase ph (shared-memory copy or global list)
 #define FOR_ITEMS(ph, var)                                  \
   for (int j_##var = 0; j_##var < s_icnt[ph]; ++j_##var)    \
@@ -620,6 +639,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   __shared__ const ItemDesc* s_ip[NPH];
   __shared__ int s_icnt[NPH];
   __shared__ const LamC* s_lc;
+  __shared__ const int64_t* s_pcbase;
   // MULTI = false: one rank, every owner lookup folds to rank 0 at compile time
   const int me = MULTI ? A.rank_base + (int)blockIdx.x / A.nbr : 0;  // this block's rank
   const int bl = MULTI ? (int)blockIdx.x % A.nbr : (int)blockIdx.x;   // block index within the rank
@@ -653,7 +673,19 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         pos += n;
       }
     }
-    LamC* lc = reinterpret_cast<LamC*>(ic + pos);
+    int64_t* pcp = reinterpret_cast<int64_t*>(ic + pos);
+    int64_t plen = 0;
+    if (A.cache_pcprog) {
+      const ItemDesc* pit = s_ip[PH_PC];
+      for (int j = 0; j < s_icnt[PH_PC]; ++j) {
+        const int64_t o = pit[j].vec_off, n = pit[j].b_off;
+        for (int64_t q = threadIdx.x; q < n; q += blockDim.x) pcp[plen + q] = A.pcprog[o + q];
+        plen += n;
+      }
+      plen = (plen + 1) & ~(int64_t)1;  // keep 16-byte alignment
+    }
+    if (threadIdx.x == 0) s_pcbase = A.cache_pcprog ? pcp : nullptr;
+    LamC* lc = reinterpret_cast<LamC*>(pcp + plen);
     if (A.cache_lam) {
       for (int q = threadIdx.x; q < nk; q += blockDim.x) {
         const int64_t k = k0 + q;
@@ -697,9 +729,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(2);
     // ---- R3 p0 = S_pp^-1 sum N^T Z_p ----
-    FOR_ITEMS(PH_PC, w)
-      pc_item(D, A, A.Sinv[me], w.s, w.I, [&](int e) { return ldcg(A.Z[pown(D.coarse_patch[e])] + D.coarse_idx[e]); },
-              A.Ppart[me], sm);
+    PC_PHASE([&](int64_t i, int o) { return ldcg(A.Z[MULTI ? o : 0] + i); });
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(3);
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
@@ -762,9 +792,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       grid_barrier(A, me, bl, round, false, 0.0, bcast);
       TSTAMP(1);
       // PC
-      FOR_ITEMS(PH_PC, w)
-        pc_item(D, A, A.Sinv[me], w.s, w.I, [&](int e) { return ldcg(A.XW[pown(D.coarse_patch[e])] + D.coarse_idx[e]); },
-                A.Ppart[me], sm);
+      PC_PHASE([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); });
       WSTAMP(1);
       grid_barrier(A, me, bl, round, false, 0.0, bcast);
       TSTAMP(2);
@@ -844,13 +872,10 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(7);
     // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
-    FOR_ITEMS(PH_PC, w)
-      pc_item(D, A, A.Sinv[me], w.s, w.I,
-              [&](int e) {
-                const int o = pown(D.coarse_patch[e]);
-                return ldcg(A.Z[o] + D.coarse_idx[e]) - ldcg(A.XW[o] + D.coarse_idx[e]);
-              },
-              A.Ppart[me], sm);
+    PC_PHASE([&](int64_t i, int o) {
+      const int r = MULTI ? o : 0;
+      return ldcg(A.Z[r] + i) - ldcg(A.XW[r] + i);
+    });
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
     SSTAMP(8);
     // ---- E3 a_r = X_rr^T (Z_r - [0; w_b]) - Phi N p, a_p = N p ----
@@ -889,8 +914,8 @@ __global__ void __launch_bounds__(NTHR) k_pc(DevPlan D, StepArgs A, const ItemDe
                                              double* Ppart) {
   extern __shared__ __align__(16) double sm[];
   if (blockIdx.x >= n) return;
-  pc_item(D, A, A.Sinv[0], items[blockIdx.x].s, items[blockIdx.x].I, [&](int e) { return ldcg(src + D.coarse_idx[e]); },
-          Ppart, sm);
+  pc_item(D, A, A.Sinv[0], items[blockIdx.x].s, items[blockIdx.x].I, A.pcprog + items[blockIdx.x].vec_off,
+          [&](int64_t i, int) { return ldcg(src + i); }, Ppart, sm);
 }
 __global__ void k_pc_sum(DevPlan D, StepArgs A, double* Pc) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D.nc; g += (int64_t)gridDim.x * blockDim.x)
