@@ -146,6 +146,10 @@ struct tcg_ctx {
   ItemDesc* d_items[NPH] = {};
   int* d_boff[NPH] = {};
   std::vector<int> h_boff[NPH];
+  std::vector<ItemDesc> h_items[NPH];
+  int* d_bpl = nullptr;
+  int* d_bploff = nullptr;
+  int cache_bpos = 0;
   int cache_items = 0, cache_lam = 0, cache_pcprog = 0;
   int64_t* d_pcprog = nullptr;
   size_t smem_steps = 0;  // dynamic shared memory of k_steps: item scratch + caches
@@ -506,7 +510,7 @@ struct ItemLists {
   explicit ItemLists(int nr) : per_rank(nr) {}
 };
 
-static tcg_status upload_items(tcg_ctx* h, ItemLists& L, int ph, int overhead) {
+static tcg_status deal_items(tcg_ctx* h, ItemLists& L, int ph, int overhead) {
   const int nbr = h->nbr;
   auto bycost = [](const std::pair<int, ItemDesc>& x, const std::pair<int, ItemDesc>& y) {
     return x.first != y.first ? x.first > y.first
@@ -544,9 +548,8 @@ static tcg_status upload_items(tcg_ctx* h, ItemLists& L, int ph, int overhead) {
       boff.push_back((int)all.size());
     }
   }
-  if (all.empty()) all.push_back(ItemDesc{});
-  TRY(dupload(h, &h->d_items[ph], all));
-  TRY(dupload(h, &h->d_boff[ph], boff));
+  for (auto& d : all) d.bc = -1;
+  h->h_items[ph] = all;
   h->h_boff[ph] = boff;
   return TCG_OK;
 }
@@ -797,10 +800,11 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(set_smem(h, (const void*)k_potrf, 2 * TS * 65 * sizeof(double)));
     TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_update, 2 * TS * SPAD * sizeof(double)));
-    TRY(set_smem(h, (const void*)k_steps<false>, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_steps<true>, h->smem_pcg));
+    for (const void* f : {(const void*)k_steps<false, false>, (const void*)k_steps<true, false>,
+                          (const void*)k_steps<false, true>, (const void*)k_steps<true, true>})
+      TRY(set_smem(h, f, h->smem_pcg));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps<true>, NTHR, h->smem_pcg));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps<true, true>, NTHR, h->smem_pcg));
     if (occ < 1) return fail(h, TCG_ECUDA, "persistent stepper kernel does not fit on an SM");
     const char* ev = getenv("TCG_PCG_BLOCKS_PER_SM");
     per = std::min(occ, ev ? std::max(1, atoi(ev)) : 2);
@@ -895,15 +899,15 @@ static tcg_status do_setup(tcg_ctx* h) {
         pcv.per_rank[crow_owner[I]].push_back({std::min(Tc, (c + 1) * ch) - c * ch, d});
       }
     // fixed per-item overhead (tile units) of the latency-bound item phases
-    TRY(upload_items(h, p1, PH_P1, 2));
-    TRY(upload_items(h, pcv, PH_PC, 2));
-    TRY(upload_items(h, p5, PH_P5, 2));
-    TRY(upload_items(h, sy, PH_SY, 2));
-    TRY(upload_items(h, fw, PH_FW, 2));
-    TRY(upload_items(h, fwa, PH_FWA, 2));
-    TRY(upload_items(h, bw, PH_BW, 2));
-    TRY(upload_items(h, bwc, PH_BWC, 2));
-    TRY(upload_items(h, rhs, PH_RHS, 0));
+    TRY(deal_items(h, p1, PH_P1, 2));
+    TRY(deal_items(h, pcv, PH_PC, 2));
+    TRY(deal_items(h, p5, PH_P5, 2));
+    TRY(deal_items(h, sy, PH_SY, 2));
+    TRY(deal_items(h, fw, PH_FW, 2));
+    TRY(deal_items(h, fwa, PH_FWA, 2));
+    TRY(deal_items(h, bw, PH_BW, 2));
+    TRY(deal_items(h, bwc, PH_BWC, 2));
+    TRY(deal_items(h, rhs, PH_RHS, 0));
   }
   // shared-memory caches of the per-iteration item lists and the lambda chunk, if they fit
   // next to the scratch at `per` blocks per SM
@@ -917,10 +921,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     const size_t items_b = (size_t)max_items * sizeof(ItemDesc);
     int64_t max_prog = 0;
     {
-      std::vector<ItemDesc> hp;  // host copy of the PC item list (ordered like the device one)
-      hp.resize(h->h_boff[PH_PC].back());
-      if (!hp.empty())
-        CK(cudaMemcpy(hp.data(), h->d_items[PH_PC], hp.size() * sizeof(ItemDesc), cudaMemcpyDeviceToHost));
+      const std::vector<ItemDesc>& hp = h->h_items[PH_PC];
       for (int gb = 0; gb < NR * h->nbr; ++gb) {
         int64_t n = 0;
         for (int j = h->h_boff[PH_PC][gb]; j < h->h_boff[PH_PC][gb + 1]; ++j) n += hp[j].b_off;
@@ -933,7 +934,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
     CK(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, h->device));
     cudaFuncAttributes fa;
-    CK(cudaFuncGetAttributes(&fa, k_steps<true>));
+    CK(cudaFuncGetAttributes(&fa, k_steps<true, true>));
     const int64_t budget = (int64_t)smem_sm / per - reserved - (int64_t)fa.sharedSizeBytes - 256;
     const char* ev = getenv("TCG_NO_SMEM_CACHE");
     const bool allow = !(ev && atoi(ev) != 0);
@@ -941,11 +942,51 @@ static tcg_status do_setup(tcg_ctx* h) {
     h->cache_pcprog = allow && h->cache_items && (int64_t)(h->smem_pcg + items_b + prog_b) <= budget && prog_b <= 32 * 1024;
     const size_t used = h->smem_pcg + (h->cache_items ? items_b : 0) + (h->cache_pcprog ? prog_b : 0);
     h->cache_lam = allow && (int64_t)(used + lam_b) <= budget && lam_b <= 32 * 1024;
-    h->smem_steps = used + (h->cache_lam ? lam_b : 0);
-    TRY(set_smem(h, (const void*)k_steps<false>, h->smem_steps));
-    TRY(set_smem(h, (const void*)k_steps<true>, h->smem_steps));
+    size_t used2 = used + (h->cache_lam ? lam_b : 0);
+    // b-position records of the patches of each block's P1 / P5 / SY items
+    std::vector<int> bpl, bploff(1, 0);
+    size_t max_bp = 0;
+    for (int gb = 0; gb < NR * h->nbr; ++gb) {
+      std::vector<int> pats;
+      for (int ph : {PH_P1, PH_P5, PH_SY})
+        for (int j = h->h_boff[ph][gb]; j < h->h_boff[ph][gb + 1]; ++j) pats.push_back(h->h_items[ph][j].s);
+      std::sort(pats.begin(), pats.end());
+      pats.erase(std::unique(pats.begin(), pats.end()), pats.end());
+      int off = 0;
+      for (int sp : pats) {
+        bpl.push_back(sp);
+        bpl.push_back(off);
+        off += nb[sp];
+      }
+      bploff.push_back((int)(bpl.size() / 2));
+      max_bp = std::max(max_bp, (size_t)off * sizeof(BPos));
+    }
+    h->cache_bpos = allow && h->cache_items && (int64_t)(used2 + max_bp) <= budget && max_bp <= 48 * 1024;
+    if (h->cache_bpos) {
+      used2 += max_bp;
+      for (int ph : {PH_P1, PH_P5, PH_SY})
+        for (int gb = 0; gb < NR * h->nbr; ++gb)
+          for (int j = h->h_boff[ph][gb]; j < h->h_boff[ph][gb + 1]; ++j) {
+            ItemDesc& d = h->h_items[ph][j];
+            for (int q = bploff[gb]; q < bploff[gb + 1]; ++q)
+              if (bpl[2 * q] == d.s) d.bc = bpl[2 * q + 1];
+          }
+    }
+    if (bpl.empty()) bpl.assign(2, 0);
+    TRY(dupload(h, &h->d_bpl, bpl));
+    TRY(dupload(h, &h->d_bploff, bploff));
+    for (int ph = 0; ph < NPH; ++ph) {
+      std::vector<ItemDesc> all = h->h_items[ph];
+      if (all.empty()) all.push_back(ItemDesc{});
+      TRY(dupload(h, &h->d_items[ph], all));
+      TRY(dupload(h, &h->d_boff[ph], h->h_boff[ph]));
+    }
+    h->smem_steps = used2;
+    for (const void* f : {(const void*)k_steps<false, false>, (const void*)k_steps<true, false>,
+                          (const void*)k_steps<false, true>, (const void*)k_steps<true, true>})
+      TRY(set_smem(h, f, h->smem_steps));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps<true>, NTHR, h->smem_steps));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps<true, true>, NTHR, h->smem_steps));
     if (occ < per) return fail(h, TCG_ECUDA, "persistent stepper: shared-memory caches broke occupancy");
   }
 
@@ -1172,6 +1213,9 @@ static StepArgs step_args(tcg_ctx* h) {
   }
   A.cache_items = h->cache_items;
   A.cache_pcprog = h->cache_pcprog;
+  A.cache_bpos = h->cache_bpos;
+  A.bpl = h->d_bpl;
+  A.bploff = h->d_bploff;
   A.pcprog = h->d_pcprog;
   A.cache_lam = h->cache_lam;
   A.scratch = (int)(h->smem_pcg / sizeof(double));
@@ -1205,7 +1249,8 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   void* args[] = {(void*)&D, (void*)&A};
   const int grid = h->nbr * (int)h->rd.size();
   prof_begin(h, 7);
-  const void* fn = (h->nranks > 1) ? (const void*)k_steps<true> : (const void*)k_steps<false>;
+  const void* fn = (h->nranks > 1) ? (h->cache_bpos ? (const void*)k_steps<true, true> : (const void*)k_steps<true, false>)
+                                     : (h->cache_bpos ? (const void*)k_steps<false, true> : (const void*)k_steps<false, false>);
   CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NTHR), args, h->smem_steps, h->stream));
   ++h->nlaunch;
   prof_end(h, 7);

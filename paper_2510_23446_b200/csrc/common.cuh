@@ -42,7 +42,15 @@ struct __align__(16) ItemDesc {
   int Ti, Tb, Tp, T;
   int nb, np;
   int64_t a_off, vec_off, b_off, p_off, sbb_off;
-  int part, pad;  // P5: 0 = X_bb^T tiles (-> Y), 1 = Phi_b tiles (-> Y2)
+  int part;  // P5: 0 = X_bb^T tiles (-> Y), 1 = Phi_b tiles (-> Y2)
+  int bc;    // P1/P5/SY: offset of the patch's b-position records in the block's shared cache (-1: none)
+};
+// b-position record (shared-memory cache of a block's patches): multiplier k, its sign on
+// this side, B_D weights of this side (aown) and of the partner (apart), partner aug index
+struct BPos {
+  int64_t part;
+  int k, pad;
+  double aown, apart, sign;
 };
 // item phases of the stepper; the first NCACHE are the per-iteration ones (shared-memory cache)
 enum { PH_P1 = 0, PH_PC, PH_P5, PH_SY, PH_FW, PH_FWA, PH_BW, PH_BWC, PH_RHS, NPH };

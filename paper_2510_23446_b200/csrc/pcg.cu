@@ -87,6 +87,9 @@ struct StepArgs {
   const int* boff[NPH];
   const int64_t* pcprog;  // PC gather programs: per item offs[nE+1], then (owner << 56 | aug index)
   int cache_pcprog;  // 1: the block's PC programs are copied to shared memory
+  const int* bpl;     // per block: (patch, cache offset) pairs of the patches whose b records it caches
+  const int* bploff;  // block gb owns pairs bploff[gb] .. bploff[gb+1]
+  int cache_bpos;     // 1: b-position records cached (ItemDesc::bc valid)
   int cache_items;  // 1: the block's per-iteration item lists are copied to shared memory
   int cache_lam;    // 1: the block's lambda-chunk index data are copied to shared memory
   int scratch;      // doubles of item scratch at the start of dynamic shared memory (even)
@@ -631,7 +634,7 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
 // all ranks of the job. Control flow depends only on values every block of every rank
 // computes identically, so all blocks run the same sequence of barriers.
 // =======================================================================================
-template <bool MULTI>
+template <bool MULTI, bool BC>
 __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red[NTHR];
@@ -640,6 +643,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   __shared__ int s_icnt[NPH];
   __shared__ const LamC* s_lc;
   __shared__ const int64_t* s_pcbase;
+  __shared__ const BPos* s_bp;
   // MULTI = false: one rank, every owner lookup folds to rank 0 at compile time
   const int me = MULTI ? A.rank_base + (int)blockIdx.x / A.nbr : 0;  // this block's rank
   const int bl = MULTI ? (int)blockIdx.x % A.nbr : (int)blockIdx.x;   // block index within the rank
@@ -693,9 +697,30 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       }
     }
     if (threadIdx.x == 0) s_lc = A.cache_lam ? lc : nullptr;
+    BPos* bc = reinterpret_cast<BPos*>(lc + (A.cache_lam ? nk : 0));
+    if (BC) {
+      for (int q = A.bploff[gb]; q < A.bploff[gb + 1]; ++q) {
+        const int s = A.bpl[2 * q], off = A.bpl[2 * q + 1];
+        int nbs = 0;
+        int64_t bo = 0;
+        nbs = D.nb[s];
+        bo = D.b_off[s];
+        for (int e = threadIdx.x; e < nbs; e += blockDim.x) {
+          const int64_t bb = bo + e;
+          bc[off + e] = BPos{D.b_part[bb], D.b_lam[bb], 0, D.b_aown[bb], D.b_apart[bb], D.b_sign[bb]};
+        }
+      }
+    }
+    if (threadIdx.x == 0) s_bp = bc;
     __syncthreads();
   }
   const LamC* lc = s_lc;
+  const BPos* bpc = s_bp;
+  // b-position record of (item, bb = b_off + pos): shared cache or the global tables
+  auto bget = [&](const ItemDesc& iw, int64_t bb, int pos) -> BPos {
+    if (BC && iw.bc >= 0) return bpc[iw.bc + pos];
+    return BPos{D.b_part[bb], D.b_lam[bb], 0, D.b_aown[bb], D.b_apart[bb], D.b_sign[bb]};
+  };
   auto lidx_p = [&](int64_t k) { return lc ? lc[k - k0].ip : D.lam_idx_p[k]; };
   auto lidx_m = [&](int64_t k) { return lc ? lc[k - k0].im : D.lam_idx_m[k]; };
   auto lw_p = [&](int64_t k) { return lc ? lc[k - k0].wp : D.wplus[k]; };
@@ -745,8 +770,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       FOR_ITEMS(PH_SY, w)
         loc += symv_item(w, Sr, A.PW[me],
                          [&](const ItemDesc& iw, int64_t bb, int pos) {
-                           return D.b_aown[bb] *
-                                  (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), D.b_part[bb]));
+                           const BPos q = bget(iw, bb, pos);
+                           return q.aown * (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), q.part));
                          },
                          sm, red);
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
@@ -777,10 +802,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           pv = lw_p(kq) * ldcg(A.PW[pown(lpat_p(kq))] + lidx_p(kq)) -
                lw_m(kq) * ldcg(A.PW[pown(lpat_m(kq))] + lidx_m(kq)) + beta * ldcg(pprev[me] + kq);
         auto vnew = [&](const ItemDesc& iw, int64_t bb, int pos) {
-          const int k = D.b_lam[bb];
-          return D.b_aown[bb] * ldcg(A.PW[me] + own_idx(iw, pos)) +
-                 D.b_apart[bb] * ldcg(A.PW[pown(ppatch(bb))] + D.b_part[bb]) +
-                 D.b_sign[bb] * beta * ldcg(pprev[lown(k)] + k);
+          const BPos q = bget(iw, bb, pos);
+          return q.aown * ldcg(A.PW[me] + own_idx(iw, pos)) + q.apart * ldcg(A.PW[pown(ppatch(bb))] + q.part) +
+                 q.sign * beta * ldcg(pprev[lown(q.k)] + q.k);
         };
         FOR_ITEMS(PH_P1, w) p1_item(w, Xr, vnew, A.XW[me], sm);
         if (kq < k1) pcur[kq] = pv;
@@ -803,9 +827,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         double loc = 0.0;
         FOR_ITEMS(PH_P5, w)
           loc += p5_item(w, Xr, A.XW[me], D.p_grp, pcf,
-                         [&](const ItemDesc&, int64_t bb, int) {
-                           const int k = D.b_lam[bb];
-                           return D.b_sign[bb] * ldcg(pcurt[lown(k)] + k);
+                         [&](const ItemDesc& iw, int64_t bb, int pos) {
+                           const BPos q = bget(iw, bb, pos);
+                           return q.sign * ldcg(pcurt[lown(q.k)] + q.k);
                          },
                          A.Y[me], A.Y2[me], sm, red,
                          (A.tstamp && step == 0 && it == 2 && gb < 4096) ? A.tstamp + 528 + gb * 8 + 4 : nullptr);
@@ -818,9 +842,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       double* const* rc = A.r[rp];
       double* rn = A.r[rp ^ 1][me];
       auto unew = [&](const ItemDesc& iw, int64_t bb, int pos) {
-        const int k = D.b_lam[bb];
-        return D.b_aown[bb] * (D.b_sign[bb] * ldcg(rc[lown(k)] + k) -
-                               alpha * (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), D.b_part[bb])));
+        const BPos q = bget(iw, bb, pos);
+        return q.aown * (q.sign * ldcg(rc[lown(q.k)] + q.k) - alpha * (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), q.part)));
       };
       // P7 (+ partial r^T z)
       {
@@ -864,9 +887,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     // ---- E1 v = B^T lambda ; w, -Phi^T v ----
     FOR_ITEMS(PH_P1, w)
       p1_item(w, Xr,
-              [&](const ItemDesc&, int64_t bb, int) {
-                const int k = D.b_lam[bb];
-                return D.b_sign[bb] * ldcg(A.lam[lown(k)] + k);
+              [&](const ItemDesc& iw, int64_t bb, int pos) {
+                const BPos q = bget(iw, bb, pos);
+                return q.sign * ldcg(A.lam[lown(q.k)] + q.k);
               },
               A.XW[me], sm);
     grid_barrier(A, me, bl, round, false, 0.0, bcast);
