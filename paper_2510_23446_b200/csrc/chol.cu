@@ -72,64 +72,102 @@ __device__ void tile_gemm_nt(const double* A, const double* B, double* C, double
 }
 
 // -------------------------------------------------------------------------------------
-// POTRF of diagonal tile (k,k) + triangular inverse into the Dinv store. One CTA/matrix.
+// POTRF of diagonal tile (k,k) fused with its triangular inverse (into the Dinv store).
+// One CTA (256 threads = 16x16) per matrix; thread (ty,tx) keeps elements
+// (i,c) = (ty+16a, tx+16b), a,b < 4, of L and of X = L^-1 in registers. Column j:
+//   pivot d = sqrt(W_jj); l_i = W_ij / d (i > j); X_jc /= d (c <= j);
+//   W_ic -= l_i l_c (j < c <= i);  X_ic -= l_i X_jc (c <= j < i)
+// i.e. right-looking Cholesky and right-looking forward elimination of L X = I in the same
+// sweep; column/row j are broadcast through double-buffered shared memory (2 barriers/column).
 // -------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_potrf(const CholDesc* __restrict__ ds, int k, double* base, double* dinv,
                                                DevError* err, int coarse) {
   const CholDesc d = ds[blockIdx.x];
   if (k >= d.Tfact) return;
-  extern __shared__ double smem[];
-  double* S = smem;              // 64 x 65
-  double* X = smem + TS * 65;    // 64 x 65
+  __shared__ double colb[2][TS], rowb[2][TS], pv[2];
   double* tile = base + d.a_off + tri_off(k, k);
-  const int tid = threadIdx.x;
-  for (int e = tid; e < TSZ; e += blockDim.x) {
-    int r = e / TS, c = e % TS;
-    S[r * 65 + c] = (c <= r) ? tile[e] : 0.0;
-  }
-  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double sv[4][4], xv[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      sv[a][b] = (c <= i) ? tile[i * TS + c] : 0.0;
+      xv[a][b] = (c == i) ? 1.0 : 0.0;
+    }
   for (int j = 0; j < TS; ++j) {
-    if (tid == 0) {
-      double piv = S[j * 65 + j];
-      if (!(piv > 0.0)) {
-        if (atomicCAS(&err->flag, 0, 1) == 0) {
-          err->matrix = coarse ? -1 : (int)blockIdx.x;
-          err->index = k * TS + j;
-          err->value = piv;
-        }
-        piv = 1.0;
+    const int jb = j >> 4, jr = j & 15, buf = j & 1;
+    if (ty == jr && tx == jr) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (a == jb) pv[buf] = sv[a][a];
+    }
+    __syncthreads();
+    double piv = pv[buf];
+    if (!(piv > 0.0)) {
+      if (threadIdx.x == 0 && atomicCAS(&err->flag, 0, 1) == 0) {
+        err->matrix = coarse ? -1 : (int)blockIdx.x;
+        err->index = k * TS + j;
+        err->value = piv;
       }
-      S[j * 65 + j] = sqrt(piv);
+      piv = 1.0;
+    }
+    const double dj = sqrt(piv), inv = 1.0 / dj;
+    if (tx == jr) {  // column j of L
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (b == jb) {
+            const int i = ty + 16 * a;
+            if (i > j) {
+              const double l = sv[a][b] * inv;
+              sv[a][b] = l;
+              colb[buf][i] = l;
+            } else if (i == j) {
+              sv[a][b] = dj;
+            }
+          }
+    }
+    if (ty == jr) {  // row j of X
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (a == jb) {
+            const int c = tx + 16 * b;
+            if (c <= j) {
+              const double x = xv[a][b] * inv;
+              xv[a][b] = x;
+              rowb[buf][c] = x;
+            }
+          }
     }
     __syncthreads();
-    const double djj = S[j * 65 + j];
-    for (int i = j + 1 + tid; i < TS; i += blockDim.x) S[i * 65 + j] /= djj;
-    __syncthreads();
-    const int mm = TS - j - 1;
-    for (int e = tid; e < mm * mm; e += blockDim.x) {
-      int i = j + 1 + e / mm, c = j + 1 + e % mm;
-      if (c <= i) S[i * 65 + c] -= S[i * 65 + j] * S[c * 65 + j];
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < TSZ; e += blockDim.x) {
-    int r = e / TS, c = e % TS;
-    tile[e] = (c <= r) ? S[r * 65 + c] : 0.0;
-  }
-  // inverse of the lower-triangular tile: column c by forward substitution
-  if (tid < TS) {
-    const int c = tid;
-    for (int r = 0; r < c; ++r) X[r * 65 + c] = 0.0;
-    X[c * 65 + c] = 1.0 / S[c * 65 + c];
-    for (int i = c + 1; i < TS; ++i) {
-      double s = 0.0;
-      for (int q = c; q < i; ++q) s += S[i * 65 + q] * X[q * 65 + c];
-      X[i * 65 + c] = -s / S[i * 65 + i];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = ty + 16 * a;
+      if (i > j) {
+        const double li = colb[buf][i];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int c = tx + 16 * b;
+          if (c > j && c <= i) sv[a][b] -= li * colb[buf][c];
+          else if (c <= j) xv[a][b] -= li * rowb[buf][c];
+        }
+      }
     }
   }
-  __syncthreads();
   double* out = dinv + d.dinv_off + (int64_t)k * TSZ;
-  for (int e = tid; e < TSZ; e += blockDim.x) out[e] = X[(e / TS) * 65 + (e % TS)];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, c = tx + 16 * b;
+      tile[i * TS + c] = (c <= i) ? sv[a][b] : 0.0;
+      out[i * TS + c] = (c <= i) ? xv[a][b] : 0.0;
+    }
 }
 
 // A_Ik <- A_Ik L_kk^-T for I in (k, T). grid (maxT-k-1, nmat).
