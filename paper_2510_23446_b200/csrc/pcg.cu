@@ -847,12 +847,25 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       };
       // P7 (+ partial r^T z)
       {
-        for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-          A.lam[me][k] += alpha * ldcg(pcur + k);
-          rn[k] = ldcg(rc[me] + k) - alpha * (yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k)));
+        // the block's lambda chunk: loads issued before the items, stores after them
+        const int64_t kq = k0 + threadIdx.x;
+        double lv = 0.0, pv = 0.0, rv = 0.0, yd = 0.0;
+        if (kq < k1) {
+          lv = A.lam[me][kq];
+          pv = ldcg(pcur + kq);
+          rv = ldcg(rc[me] + kq);
+          yd = yv(pown(lpat_p(kq)), lidx_p(kq)) - yv(pown(lpat_m(kq)), lidx_m(kq));
         }
         double loc = 0.0;
         FOR_ITEMS(PH_SY, w) loc += symv_item(w, Sr, A.PW[me], unew, sm, red);
+        if (kq < k1) {
+          A.lam[me][kq] = lv + alpha * pv;
+          rn[kq] = rv - alpha * yd;
+        }
+        for (int64_t k = kq + blockDim.x; k < k1; k += blockDim.x) {
+          A.lam[me][k] += alpha * ldcg(pcur + k);
+          rn[k] = ldcg(rc[me] + k) - alpha * (yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k)));
+        }
         WSTAMP(3);
         rz = grid_barrier(A, me, bl, round, true, loc, bcast);
       }
