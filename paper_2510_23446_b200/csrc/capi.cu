@@ -151,6 +151,7 @@ struct tcg_ctx {
   int* d_bploff = nullptr;
   int cache_bpos = 0;
   int cache_items = 0, cache_lam = 0, cache_pcprog = 0;
+  int npf = 0;  // prefetched tiles per phase (stepper)
   int64_t* d_pcprog = nullptr;
   size_t smem_steps = 0;  // dynamic shared memory of k_steps: item scratch + caches
   int coarse_ch = 1, coarse_maxch = 1;
@@ -934,7 +935,15 @@ static tcg_status do_setup(tcg_ctx* h) {
     CK(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, h->device));
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, k_steps<true, true>));
-    const int64_t budget = (int64_t)smem_sm / per - reserved - (int64_t)fa.sharedSizeBytes - 256;
+    int64_t budget = (int64_t)smem_sm / per - reserved - (int64_t)fa.sharedSizeBytes - 256;
+    // tile prefetch buffer first (bulk copies of the next phase's first tiles during barriers)
+    {
+      const char* ne = getenv("TCG_NPF");
+      int npf = ne ? std::max(0, std::min(2, atoi(ne))) : 1;  // 2 tiles shrink L1 too much on the HBM-bound configs
+      while (npf > 0 && (int64_t)(h->smem_pcg + (size_t)npf * TSZ * sizeof(double)) > budget) --npf;
+      h->npf = npf;
+      budget -= (int64_t)npf * TSZ * sizeof(double);
+    }
     const char* ev = getenv("TCG_NO_SMEM_CACHE");
     const bool allow = !(ev && atoi(ev) != 0);
     h->cache_items = allow && (int64_t)(h->smem_pcg + items_b) <= budget && items_b <= 48 * 1024;
@@ -980,7 +989,7 @@ static tcg_status do_setup(tcg_ctx* h) {
       TRY(dupload(h, &h->d_items[ph], all));
       TRY(dupload(h, &h->d_boff[ph], h->h_boff[ph]));
     }
-    h->smem_steps = used2;
+    h->smem_steps = used2 + (size_t)h->npf * TSZ * sizeof(double);
     for (const void* f : {(const void*)k_steps<false, false>, (const void*)k_steps<true, false>,
                           (const void*)k_steps<false, true>, (const void*)k_steps<true, true>})
       TRY(set_smem(h, f, h->smem_steps));
@@ -1218,6 +1227,7 @@ static StepArgs step_args(tcg_ctx* h) {
   A.pcprog = h->d_pcprog;
   A.cache_lam = h->cache_lam;
   A.scratch = (int)(h->smem_pcg / sizeof(double));
+  A.npf = h->npf;
   A.tstamp = h->tstamp;
   A.rtol = h->rtol;
   A.max_iter = h->max_iter;

@@ -92,7 +92,8 @@ struct StepArgs {
   int cache_bpos;     // 1: b-position records cached (ItemDesc::bc valid)
   int cache_items;  // 1: the block's per-iteration item lists are copied to shared memory
   int cache_lam;    // 1: the block's lambda-chunk index data are copied to shared memory
-  int scratch;      // doubles of item scratch at the start of dynamic shared memory (even)
+  int scratch;      // doubles of item scratch (after the prefetch tiles) in dynamic shared memory (even)
+  int npf;          // tiles of the next phase's first item bulk-copied to shared memory during a barrier
   unsigned long long* tstamp;  // optional phase timestamps (rank 0 block 0)
   double rtol;
   int max_iter;
@@ -119,6 +120,36 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// ---- bulk async copies (TMA engine, cp.async.bulk) into shared memory, mbarrier-tracked ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* mb) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mb)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* mb) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mb))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mb, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(mb)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ double2 lds2(const double* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
 }
 
 // fixed-order block reduction of one value per thread: xor-butterfly warp sums (lane 0's
@@ -173,16 +204,27 @@ __device__ __forceinline__ void prefetch_tiles(TileF tile, int J0, int J1) {
   }
 }
 // row:  part[r] += sum_{J=J0}^{J1-1} tile(J)[row0+r][:] . x[(J-J0)*64 : ]
+// The first npf tiles were copied to shared memory (pft) by a bulk copy issued during the
+// preceding grid barrier; the rest stream from global memory.
 template <class TileF, class Gather>
 __device__ __forceinline__ void gemv_row_g(TileF tile, int J0, int J1, const double* x, Gather gather,
-                                           double (&part)[8]) {
+                                           double (&part)[8], const double* pft = nullptr, int npf = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
   const int off = row0 * TS + 2 * lane;
-  if (!(c_step_flags & 1)) prefetch_tiles(tile, J0, J1);
+  if (!(c_step_flags & 1)) prefetch_tiles(tile, J0 + npf, J1);
   gather();
   __syncthreads();
+  for (int J = J0; J < min(J1, J0 + npf); ++J) {
+    const double* t = pft + (J - J0) * TSZ + off;
+    const double2 xv = *reinterpret_cast<const double2*>(x + (J - J0) * TS + 2 * lane);
+    double2 a[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = lds2(t + r * TS);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
+  }
 #pragma unroll 2
-  for (int J = J0; J < J1; ++J) {
+  for (int J = J0 + npf; J < J1; ++J) {
     const double* t = tile(J) + off;
     const double2 xv = *reinterpret_cast<const double2*>(x + (J - J0) * TS + 2 * lane);
     double2 a[8];
@@ -195,14 +237,26 @@ __device__ __forceinline__ void gemv_row_g(TileF tile, int J0, int J1, const dou
 // col:  c[0..1] += sum_{I=I0}^{I1-1} tile(I)[row0+r][2*lane..] * x[(I-I0)*64 + row0 + r]
 template <class TileF, class Gather>
 __device__ __forceinline__ void gemv_col_g(TileF tile, int I0, int I1, const double* x, Gather gather, double& c0,
-                                           double& c1) {
+                                           double& c1, const double* pft = nullptr, int npf = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
   const int off = row0 * TS + 2 * lane;
-  if (!(c_step_flags & 1)) prefetch_tiles(tile, I0, I1);
+  if (!(c_step_flags & 1)) prefetch_tiles(tile, I0 + npf, I1);
   gather();
   __syncthreads();
+  for (int I = I0; I < min(I1, I0 + npf); ++I) {
+    const double* t = pft + (I - I0) * TSZ + off;
+    double2 a[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = lds2(t + r * TS);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const double xr = x[(I - I0) * TS + row0 + r];
+      c0 += a[r].x * xr;
+      c1 += a[r].y * xr;
+    }
+  }
 #pragma unroll 2
-  for (int I = I0; I < I1; ++I) {
+  for (int I = I0 + npf; I < I1; ++I) {
     const double* t = tile(I) + off;
     double2 a[8];
 #pragma unroll
@@ -233,7 +287,8 @@ __device__ __forceinline__ double col_finish(double c0, double c1, double* cr) {
 // vsrc(it, b, pos) returns (B_s^T p)_pos, b = b_off + pos. Output XW: +w (b rows), -g (p rows).
 // Xr = the rank's inverse-factor store.
 template <class Src>
-__device__ __forceinline__ void p1_item(const ItemDesc& it, const double* Xr, Src vsrc, double* XW, double* sv) {
+__device__ __forceinline__ void p1_item(const ItemDesc& it, const double* Xr, Src vsrc, double* XW, double* sv,
+                                        const double* pft = nullptr, int npf = 0) {
   const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   const int Jn = (I < Tb) ? I + 1 : Tb;
   const double* X = Xr + it.a_off;
@@ -245,7 +300,7 @@ __device__ __forceinline__ void p1_item(const ItemDesc& it, const double* Xr, Sr
                for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x)
                  sv[e] = (e < nb) ? vsrc(it, it.b_off + e, e) : 0.0;
              },
-             part);
+             part, pft, npf);
   const double sum = warp_reduce8(part);
   const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
   if ((lane & 3) == 0) XW[it.vec_off + (int64_t)(Ti + I) * TS + row0 + warp_reduce8_row()] = (I < Tb) ? sum : -sum;
@@ -258,7 +313,8 @@ __device__ __forceinline__ void p1_item(const ItemDesc& it, const double* Xr, Sr
 constexpr int64_t kIdxMask = (1ll << 56) - 1;
 template <class GS>
 __device__ __forceinline__ void pc_item(const DevPlan& D, const StepArgs& A, const double* Sinv, int I, int c,
-                                        const int64_t* prog, GS gsrc, double* Ppart, double* sm) {
+                                        const int64_t* prog, GS gsrc, double* Ppart, double* sm,
+                                        const double* pft = nullptr, int npf = 0) {
   const int Tc = D.Tc;
   const int J0 = c * A.ch, J1 = min(Tc, J0 + A.ch);
   const int nE = (J1 - J0) * TS;
@@ -280,7 +336,7 @@ __device__ __forceinline__ void pc_item(const DevPlan& D, const StepArgs& A, con
                  sm[e] = val;
                }
              },
-             part);
+             part, pft, npf);
   const double sum = warp_reduce8(part);
   if ((lane & 3) == 0) Ppart[((int64_t)I * A.maxch + c) * TS + row0 + warp_reduce8_row()] = sum;
   __syncthreads();
@@ -295,7 +351,8 @@ __device__ __forceinline__ void pc_item(const DevPlan& D, const StepArgs& A, con
 template <class PcF, class Src>
 __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, const double* W, const int* p_grp,
                                           PcF pc, Src vsrc, double* Y, double* Y2, double* sm, double* red,
-                                          unsigned long long* sub = nullptr) {
+                                          unsigned long long* sub = nullptr, const double* pft = nullptr,
+                                          int npf = 0) {
   const int J = it.I, Ti = it.Ti, Tb = it.Tb, np = it.np, nb = it.nb;
   const bool ppart = it.part != 0;
   const int I0 = ppart ? Tb : J, I1 = ppart ? Tb + it.Tp : Tb;
@@ -318,7 +375,7 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
                  sw[e] = val;
                }
              },
-             c0, c1);
+             c0, c1, pft, npf);
   SUBSTAMP(1);
   const double acc = col_finish(c0, c1, cr);
   double contrib = 0.0;
@@ -335,7 +392,8 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
 // ---- P7 / R5: symmetric S_bb apply, one row block I of one patch --------------------------
 // usrc(it, b, pos) returns (B_D^(s)T r)_pos. Returns this item's share of u^T S_bb u.
 template <class Src>
-__device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm, double* red) {
+__device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm,
+                                            double* red, const double* pft = nullptr, int npf = 0) {
   const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   double* u = sm;            // Tb*64
   double* cr = u + Tb * TS;  // 9 * 64
@@ -349,7 +407,7 @@ __device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr
              [&] {
                for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) u[i] = (i < nb) ? usrc(it, it.b_off + i, i) : 0.0;
              },
-             part);
+             part, pft, npf);
   double c0 = 0.0, c1 = 0.0;
 #pragma unroll 2
   for (int J = I + 1; J < Tb; ++J) {  // column part: S_JI^T u_J
@@ -472,8 +530,14 @@ __device__ __forceinline__ void fence_scope(int sys) {
 //    rank's partials in block order, publishes the rank partial, arrives on rank 0's global
 //    counter (system scope for real GPUs), waits for all rank leaders and releases its rank;
 //    every block then sums the rank partials in rank order. Identical totals everywhere.
+struct NoHook {
+  __device__ void operator()() const {}
+};
+// hook(): run by thread 0 right after this block's arrival, before it waits (used to issue the
+// bulk copies of the next phase's first tiles so they stream in during the wait)
+template <class Hook = NoHook>
 __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& round, bool reduce, double value,
-                               double* bcast) {
+                               double* bcast, Hook hook = Hook()) {
   __shared__ int s_leader;
   __syncthreads();
   ++round;
@@ -485,6 +549,7 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
     if (threadIdx.x == 0) {
       if (reduce) A.partials[me][bl] = value;
       red_release_gpu(&mine->local_count, 1u);
+      hook();
       const unsigned long long t0 = gtimer();
       while ((int)(ld_acquire_u32(&mine->local_count, 0) - round * (unsigned int)A.nbr) < 0) {
         if (gtimer() - t0 > kBarrierTimeoutNs) __trap();  // a missing block: fail, never hang
@@ -502,6 +567,7 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
     fence_scope(sys);
     const unsigned int old = atomicAdd(&mine->local_count, 1u);
     s_leader = (old + 1 == round * (unsigned int)A.nbr);
+    hook();
   }
   __syncthreads();
   if (s_leader) {
@@ -621,7 +687,7 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
     FOR_ITEMS(PH_PC, w) {                                                                 \
       const int64_t* prog = s_pcbase ? s_pcbase + po : A.pcprog + w.vec_off;              \
       po += w.b_off;                                                                      \
-      pc_item(D, A, A.Sinv[me], w.s, w.I, prog, GS, A.Ppart[me], sm);                     \
+      pc_item(D, A, A.Sinv[me], w.s, w.I, prog, GS, A.Ppart[me], smw, PF0(j_w));          \
     }                                                                                     \
   }
 // loop over this block's items of phase ph (shared-memory copy or global list)
@@ -644,6 +710,10 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   __shared__ const LamC* s_lc;
   __shared__ const int64_t* s_pcbase;
   __shared__ const BPos* s_bp;
+  __shared__ __align__(8) unsigned long long s_mb;  // mbarrier of the tile prefetch
+  __shared__ int s_pfn;                            // tiles prefetched for the coming phase
+  double* const tbuf = sm;                         // A.npf prefetched tiles
+  double* const smw = sm + (size_t)A.npf * TSZ;    // item scratch
   // MULTI = false: one rank, every owner lookup folds to rank 0 at compile time
   const int me = MULTI ? A.rank_base + (int)blockIdx.x / A.nbr : 0;  // this block's rank
   const int bl = MULTI ? (int)blockIdx.x % A.nbr : (int)blockIdx.x;   // block index within the rank
@@ -656,8 +726,12 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   const double* Sr = D.Sbbr[me];
   // ---- per-launch setup: item lists (and lambda-chunk index data) into shared memory ----
   {
-    ItemDesc* ic = reinterpret_cast<ItemDesc*>(sm + A.scratch);
+    ItemDesc* ic = reinterpret_cast<ItemDesc*>(smw + A.scratch);
     int pos = 0;
+    if (threadIdx.x == 0) {
+      mbar_init(&s_mb);
+      s_pfn = 0;
+    }
 #pragma unroll
     for (int ph = 0; ph < NPH; ++ph)  // constant indices: no local copy of the parameter block
       if (threadIdx.x == ph) {
@@ -738,30 +812,80 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     const int k = D.b_lam[bb];
     return D.b_sign[bb] > 0 ? D.lam_patch_m[k] : D.lam_patch_p[k];
   };
+  // ---- tile prefetch: the first item of phase ph, up to A.npf tiles (thread 0, in a barrier) ----
+  unsigned int pf_par = 0;
+  auto pf_issue = [&](int ph) {
+    int n = 0;
+    const double* src[2] = {nullptr, nullptr};
+    if (A.npf > 0 && s_icnt[ph] > 0) {
+      const ItemDesc& w = s_ip[ph][0];
+      if (ph == PH_P1) {
+        const int Jn = (w.I < w.Tb) ? w.I + 1 : w.Tb;
+        n = min(Jn, A.npf);
+        for (int q = 0; q < n; ++q) src[q] = Xr + w.a_off + tri_off(w.Ti + w.I, w.Ti + q);
+      } else if (ph == PH_PC) {
+        const int J0 = w.I * A.ch, J1 = min(D.Tc, J0 + A.ch);
+        n = min(J1 - J0, A.npf);
+        for (int q = 0; q < n; ++q) src[q] = A.Sinv[me] + ((int64_t)w.s * D.Tc + J0 + q) * TSZ;
+      } else if (ph == PH_P5) {
+        const int I0 = w.part ? w.Tb : w.I, I1 = w.part ? w.Tb + w.Tp : w.Tb;
+        n = min(I1 - I0, A.npf);
+        for (int q = 0; q < n; ++q) src[q] = Xr + w.a_off + tri_off(w.Ti + I0 + q, w.Ti + w.I);
+      } else if (ph == PH_SY) {
+        n = min(w.I + 1, A.npf);
+        for (int q = 0; q < n; ++q) src[q] = Sr + w.sbb_off + tri_off(w.I, q);
+      }
+    }
+    if (n > 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&s_mb, (uint32_t)(n * TSZ * sizeof(double)));
+      for (int q = 0; q < n; ++q) bulk_g2s(tbuf + q * TSZ, src[q], TSZ * sizeof(double), &s_mb);
+    }
+    s_pfn = n;
+  };
+  // phase start: wait for the prefetched tiles (all threads); returns their count
+  auto pf_wait = [&]() -> int {
+    const int n = s_pfn;
+    if (n > 0) {
+      mbar_wait(&s_mb, pf_par);
+      pf_par ^= 1u;
+    }
+    return n;
+  };
+  auto hook = [&](int ph) { return [&, ph]() { pf_issue(ph); }; };
   int64_t hoff = A.hist_off;
   int total_status = 0;
 
+  // grid barrier that issues the next phase's tile prefetch during the wait and, after it,
+  // waits for the tiles (npf_cur = tiles of that phase's first item now in tbuf)
+  int npf_cur = 0;
+  auto bar = [&](int ph_next, bool reduce, double v) -> double {
+    const double r = grid_barrier(A, me, bl, round, reduce, v, bcast, [&]() { pf_issue(ph_next); });
+    npf_cur = pf_wait();
+    return r;
+  };
+#define PF0(j) ((j) == 0 ? tbuf : nullptr), ((j) == 0 ? npf_cur : 0)
   for (int step = 0; step < A.nsteps; ++step) {
     const double t = (A.step0 + step + 1) * A.dt;
     int it = 0;
     SSTAMP(0);
     // ---- R1 rhs ----
-    FOR_ITEMS(PH_RHS, w) rhs_item(D, A, me, w, t, sm);
-    grid_barrier(A, me, bl, round, false, 0.0, bcast);
+    FOR_ITEMS(PH_RHS, w) rhs_item(D, A, me, w, t, smw);
+    bar(-1, false, 0.0);
     SSTAMP(1);
     // ---- R2 forward (conductors) ----
-    FOR_ITEMS(PH_FW, w) fw_item(w, Xr, A.F[me], A.Z[me], sm);
-    grid_barrier(A, me, bl, round, false, 0.0, bcast);
+    FOR_ITEMS(PH_FW, w) fw_item(w, Xr, A.F[me], A.Z[me], smw);
+    bar(PH_PC, false, 0.0);
     SSTAMP(2);
     // ---- R3 p0 = S_pp^-1 sum N^T Z_p ----
     PC_PHASE([&](int64_t i, int o) { return ldcg(A.Z[MULTI ? o : 0] + i); });
-    grid_barrier(A, me, bl, round, false, 0.0, bcast);
+    bar(PH_P5, false, 0.0);
     SSTAMP(3);
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
     FOR_ITEMS(PH_P5, w)
-      p5_item(w, Xr, A.Z[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], sm,
-              red);
-    grid_barrier(A, me, bl, round, false, 0.0, bcast);
+      p5_item(w, Xr, A.Z[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
+              red, nullptr, PF0(j_w));
+    bar(PH_SY, false, 0.0);
     SSTAMP(4);
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
     double rho0;
@@ -773,13 +897,13 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                            const BPos q = bget(iw, bb, pos);
                            return q.aown * (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), q.part));
                          },
-                         sm, red);
+                         smw, red, PF0(j_w));
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
         A.r[0][me][k] = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
         A.pk[0][me][k] = 0.0;
         A.lam[me][k] = 0.0;
       }
-      rho0 = grid_barrier(A, me, bl, round, true, loc, bcast);
+      rho0 = bar(PH_P1, true, loc);
     }
     SSTAMP(5);
     if (me == 0 && bl == 0 && threadIdx.x == 0) A.hist[0][hoff] = 1.0;
@@ -806,19 +930,19 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           return q.aown * ldcg(A.PW[me] + own_idx(iw, pos)) + q.apart * ldcg(A.PW[pown(ppatch(bb))] + q.part) +
                  q.sign * beta * ldcg(pprev[lown(q.k)] + q.k);
         };
-        FOR_ITEMS(PH_P1, w) p1_item(w, Xr, vnew, A.XW[me], sm);
+        FOR_ITEMS(PH_P1, w) p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w));
         if (kq < k1) pcur[kq] = pv;
         for (int64_t k = kq + blockDim.x; k < k1; k += blockDim.x)
           pcur[k] = lw_p(k) * ldcg(A.PW[pown(lpat_p(k))] + lidx_p(k)) -
                     lw_m(k) * ldcg(A.PW[pown(lpat_m(k))] + lidx_m(k)) + beta * ldcg(pprev[me] + k);
       }
       WSTAMP(0);
-      grid_barrier(A, me, bl, round, false, 0.0, bcast);
+      bar(PH_PC, false, 0.0);
       TSTAMP(1);
       // PC
       PC_PHASE([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); });
       WSTAMP(1);
-      grid_barrier(A, me, bl, round, false, 0.0, bcast);
+      bar(PH_P5, false, 0.0);
       TSTAMP(2);
       // P5 (+ partial p^T F p)
       double* const* pcurt = A.pk[pp ^ 1];
@@ -831,10 +955,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                            const BPos q = bget(iw, bb, pos);
                            return q.sign * ldcg(pcurt[lown(q.k)] + q.k);
                          },
-                         A.Y[me], A.Y2[me], sm, red,
-                         (A.tstamp && step == 0 && it == 2 && gb < 4096) ? A.tstamp + 528 + gb * 8 + 4 : nullptr);
+                         A.Y[me], A.Y2[me], smw, red,
+                         (A.tstamp && step == 0 && it == 2 && gb < 4096) ? A.tstamp + 528 + gb * 8 + 4 : nullptr,
+                         PF0(j_w));
         WSTAMP(2);
-        pq = grid_barrier(A, me, bl, round, true, loc, bcast);
+        pq = bar(PH_SY, true, loc);
       }
       TSTAMP(3);
       if (!(pq > 0.0)) { status = 2; break; }  // lost positive curvature (uniform)
@@ -857,7 +982,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           yd = yv(pown(lpat_p(kq)), lidx_p(kq)) - yv(pown(lpat_m(kq)), lidx_m(kq));
         }
         double loc = 0.0;
-        FOR_ITEMS(PH_SY, w) loc += symv_item(w, Sr, A.PW[me], unew, sm, red);
+        FOR_ITEMS(PH_SY, w) loc += symv_item(w, Sr, A.PW[me], unew, smw, red, PF0(j_w));
         if (kq < k1) {
           A.lam[me][kq] = lv + alpha * pv;
           rn[kq] = rv - alpha * yd;
@@ -867,7 +992,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           rn[k] = ldcg(rc[me] + k) - alpha * (yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k)));
         }
         WSTAMP(3);
-        rz = grid_barrier(A, me, bl, round, true, loc, bcast);
+        rz = bar(PH_P1, true, loc);
       }
       TSTAMP(4);
       ++it;
@@ -904,24 +1029,24 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                 const BPos q = bget(iw, bb, pos);
                 return q.sign * ldcg(A.lam[lown(q.k)] + q.k);
               },
-              A.XW[me], sm);
-    grid_barrier(A, me, bl, round, false, 0.0, bcast);
+              A.XW[me], smw, PF0(j_w));
+    bar(PH_PC, false, 0.0);
     SSTAMP(7);
     // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
     PC_PHASE([&](int64_t i, int o) {
       const int r = MULTI ? o : 0;
       return ldcg(A.Z[r] + i) - ldcg(A.XW[r] + i);
     });
-    grid_barrier(A, me, bl, round, false, 0.0, bcast);
+    bar(-1, false, 0.0);
     SSTAMP(8);
     // ---- E3 a_r = X_rr^T (Z_r - [0; w_b]) - Phi N p, a_p = N p ----
     // insulator coefficients feed no later step (no mass term): recover them only at the last step
     if (step == A.nsteps - 1) {
-      FOR_ITEMS(PH_BW, w) bw_item(D, w, Xr, A.Z[me], A.XW[me], pcf, A.a_loc[me], A.G.nloc, sm);
+      FOR_ITEMS(PH_BW, w) bw_item(D, w, Xr, A.Z[me], A.XW[me], pcf, A.a_loc[me], A.G.nloc, smw);
     } else {
-      FOR_ITEMS(PH_BWC, w) bw_item(D, w, Xr, A.Z[me], A.XW[me], pcf, A.a_loc[me], A.G.nloc, sm);
+      FOR_ITEMS(PH_BWC, w) bw_item(D, w, Xr, A.Z[me], A.XW[me], pcf, A.a_loc[me], A.G.nloc, smw);
     }
-    grid_barrier(A, me, bl, round, false, 0.0, bcast);
+    bar(-1, false, 0.0);
     SSTAMP(9);
   }
   if (bl == 0 && threadIdx.x == 0) {
