@@ -284,6 +284,23 @@ def main():
                             "launch duration; traffic = ncu DRAM bytes of that launch (profiles/round1_ncu_k_steps.json); "
                             "cfg1/cfg2 are L2-resident (effective bandwidth, latency/barrier bound)"}
 
+    # ---- F-apply (BASELINE metric's second half): the dual operator alone, isolated loop ----
+    fap = None
+    if world == 1 and not args.no_roofline:
+        peak, peak_kind = peaks()
+        lam = np.random.default_rng(0).standard_normal(inf["m"])
+        s.apply_F(lam)
+        est = s.bench_fapply(2) / 2.0
+        nrep = int(max(5, min(1000, 200.0 / max(est, 1e-3))))
+        ms_f = s.bench_fapply(nrep)
+        bf = inf["bytes_fapply"]
+        gbs = bf / (ms_f / nrep * 1e-3) / 1e9
+        fap = {"GBps": gbs, "frac": gbs / peak, "peak": peak, "us_per_apply": 1000.0 * ms_f / nrep,
+               "bytes_per_apply": bf, "applies": nrep,
+               "note": "q = F p in the persistent kernel (P1 row GEMVs, coarse S_pp^-1 GEMV, column GEMVs, jump; "
+                       "4 grid barriers per apply), algorithmic bytes B_F (DESIGN.md §5) / event-timed duration"
+                       + ("; working set L2-resident: effective bandwidth" if bf < 60e6 else "")}
+
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if args.e2e_steps > 0:
@@ -329,7 +346,7 @@ def main():
             "pcg_iters_per_s": value * iters_per_step,
             "pcg_iters_per_step": iters_per_step,
             "setup_ms": inf["ms_assembly"] + inf["ms_factor"] + inf["ms_coarse"],
-            "roofline": roof, "kernel_shares": shares, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "fapply": fap, "kernel_shares": shares, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -171,9 +171,20 @@ tcg_status tcg_get_history(tcg_handle h, int* iters, double* final_relres, size_
 
 tcg_status tcg_get_info(tcg_handle h, tcg_info* out);
 
+/* The dual operator of the IETI-DP system ("two sequential Schur complements";
+ * SURVEY §8(a) c2):  q = F lam = B W~^-1 B^T lam
+ *   = B_r W_rr^-1 B_r^T lam + B_r Phi N S_pp^-1 N^T Phi^T B_r^T lam,
+ * computed exactly as one PCG iteration computes it (X_bb / Phi_b^T row GEMVs, coarse
+ * S_pp^-1 GEMV, X_bb^T / Phi_b column GEMVs, jump) inside the persistent stepper kernel.
+ * lam, q: host arrays of m = tcg_info.m doubles in multiplier order (caller-owned; lam is
+ * copied in, q written). The lambda operand stays resident for tcg_bench_fapply.
+ * Errors: TCG_EINVAL (m mismatch, NULL, multi-process handle), TCG_ESTATE (no setup). */
+tcg_status tcg_fapply(tcg_handle h, const double* lam, double* q, size_t m);
+
 /* Benchmark hook: `n` applications of the dual operator F (the exact per-iteration
- * sequence forward solve -> coarse -> backward solve -> jump) on a fixed vector;
- * returns the device time in *ms. Requires setup. */
+ * sequence: P1 row GEMVs -> coarse -> column GEMVs -> jump, 4 grid barriers each) in one
+ * launch of the persistent kernel, on the operand of the last tcg_fapply (zeros before);
+ * returns the device time in *ms. Requires setup; single-process handles. */
 tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms);
 
 /* Time every launch of the persistent stepper kernel (kernel_id 7; 0 = off) with CUDA events

@@ -22,7 +22,7 @@ PLAN_EDGE_CLASS, PLAN_EDGE_REGION, PLAN_TREE, PLAN_PART, PLAN_PATCH_COUNTS, PLAN
 
 EXPORTS = ["tcg_create", "tcg_set_patches", "tcg_set_materials", "tcg_set_source", "tcg_set_time", "tcg_set_solver",
            "tcg_plan", "tcg_get_plan", "tcg_setup", "tcg_refactor", "tcg_step", "tcg_get_coefficients", "tcg_get_history",
-           "tcg_get_info", "tcg_bench_fapply", "tcg_set_profile", "tcg_set_virtual_ranks", "tcg_nccl_unique_id", "tcg_last_error",
+           "tcg_get_info", "tcg_fapply", "tcg_bench_fapply", "tcg_set_profile", "tcg_set_virtual_ranks", "tcg_nccl_unique_id", "tcg_last_error",
            "tcg_destroy"]
 
 
@@ -72,6 +72,7 @@ def lib():
     L.tcg_get_coefficients.argtypes = [vp, C.c_int, dp, C.c_size_t]
     L.tcg_get_history.argtypes = [vp, ip, dp, C.c_size_t, dp, C.c_size_t]
     L.tcg_get_info.argtypes = [vp, C.POINTER(TcgInfo)]
+    L.tcg_fapply.argtypes = [vp, dp, dp, C.c_size_t]
     L.tcg_bench_fapply.argtypes = [vp, C.c_int, dp]
     L.tcg_set_profile.argtypes = [vp, C.c_int]
     L.tcg_set_virtual_ranks.argtypes = [vp, C.c_int]
@@ -188,6 +189,13 @@ class Solver:
 
     def set_profile(self, kernel_id):
         self._ck(self.L.tcg_set_profile(self.h, int(kernel_id)))
+
+    def apply_F(self, lam):
+        """q = F lam (the dual operator, through the C ABI; lam of length m)."""
+        lam = np.ascontiguousarray(lam, dtype=np.float64)
+        q = np.empty_like(lam)
+        self._ck(self.L.tcg_fapply(self.h, _dptr(lam), _dptr(q), lam.size))
+        return q
 
     def bench_fapply(self, n):
         ms = C.c_double()

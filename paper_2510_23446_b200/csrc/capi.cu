@@ -791,9 +791,6 @@ static tcg_status do_setup(tcg_ctx* h) {
     scratch = (scratch + 1) & ~(size_t)1;  // keep the item cache 16-byte aligned
     h->smem_pcg = sizeof(double) * scratch;
     TRY(set_smem(h, (const void*)k_fw, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_p1_lam, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_pc, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_p5, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_xinv_row, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_sinv, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_trinv_row, 2 * TS * SPAD * sizeof(double)));
@@ -1228,6 +1225,7 @@ static StepArgs step_args(tcg_ctx* h) {
   A.cache_lam = h->cache_lam;
   A.scratch = (int)(h->smem_pcg / sizeof(double));
   A.npf = h->npf;
+  A.mode = 0;
   A.tstamp = h->tstamp;
   A.rtol = h->rtol;
   A.max_iter = h->max_iter;
@@ -1601,35 +1599,58 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
   return TCG_OK;
 }
 
-tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms) {
-  if (!h || !ms) return TCG_EINVAL;
+// n applications q = F p inside the persistent stepper (mode 1), p = pk[0], q -> r[1]; *ms =
+// device time (CUDA events on the library stream). Single-process handles.
+static tcg_status run_fapply(tcg_ctx* h, int n, double* ms) {
   if (!h->setup_done || h->broken) return fail(h, TCG_ESTATE, "setup first");
-  if (h->rd.size() != 1 || h->nranks != 1) return fail(h, TCG_EINVAL, "bench_fapply needs a single-rank handle");
-  cudaSetDevice(h->device);
-  RankDev& R = h->rd[0];
-  DevPlan& D = R.D;
+  if (h->world > 1) return fail(h, TCG_EINVAL, "F-apply hooks need a single-process handle");
+  CK(cudaSetDevice(h->device));
+  for (auto& R : h->rd) CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), h->stream));
   StepArgs A = step_args(h);
-  const int np1 = h->h_boff[PH_P1][h->nbr], np5 = h->h_boff[PH_P5][h->nbr], npc = h->h_boff[PH_PC][h->nbr];
+  A.nsteps = n;
+  A.mode = 1;
+  DevPlan D = h->D;
+  void* args[] = {(void*)&D, (void*)&A};
+  const int grid = h->nbr * (int)h->rd.size();
+  const void* fn = (h->nranks > 1) ? (h->cache_bpos ? (const void*)k_steps<true, true> : (const void*)k_steps<true, false>)
+                                     : (h->cache_bpos ? (const void*)k_steps<false, true> : (const void*)k_steps<false, false>);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, h->stream);
-  for (int i = 0; i < n; ++i) {
-    if (np1 > 0) k_p1_lam<<<np1, NTHR, h->smem_pcg, h->stream>>>(D, h->d_items[PH_P1], np1, R.r0, R.XW);
-    if (npc > 0) {
-      k_pc<<<npc, NTHR, h->smem_pcg, h->stream>>>(D, A, h->d_items[PH_PC], npc, R.XW, R.Ppart);
-      k_pc_sum<<<592, 256, 0, h->stream>>>(D, A, R.Pc);
-    }
-    if (np5 > 0) k_p5<<<np5, NTHR, h->smem_pcg, h->stream>>>(D, h->d_items[PH_P5], np5, R.XW, R.Pc, R.Y, R.Y2);
-    if (D.m > 0) k_jump<<<RED_BLOCKS, 256, 0, h->stream>>>(D, R.Y, R.Y2, R.q);
-    h->nlaunch += 5;
-  }
+  CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NTHR), args, h->smem_steps, h->stream));
+  ++h->nlaunch;
   cudaEventRecord(e1, h->stream);
-  CK(cudaEventSynchronize(e1));
-  *ms = elapsed_ms(e0, e1);
+  CK(cudaMemcpyAsync(h->h_st, h->rd[0].st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->bar_round = h->h_st->counter[3];
+  if (ms) *ms = elapsed_ms(e0, e1);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  CKL();
+  return TCG_OK;
+}
+
+tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms) {
+  if (!h || !ms || n < 1) return h ? fail(h, TCG_EINVAL, "n >= 1 and ms required") : TCG_EINVAL;
+  return run_fapply(h, n, ms);
+}
+
+tcg_status tcg_fapply(tcg_handle h, const double* lam, double* q, size_t m) {
+  if (!h || !lam || !q) return TCG_EINVAL;
+  if (!h->setup_done || h->broken) return fail(h, TCG_ESTATE, "setup first");
+  if (m != (size_t)h->plan.m) return fail(h, TCG_EINVAL, "need m = " + std::to_string(h->plan.m));
+  if (h->world > 1) return fail(h, TCG_EINVAL, "F-apply hooks need a single-process handle");
+  CK(cudaSetDevice(h->device));
+  // p = lam in every local rank's copy (each reads its own chunk); q gathered from the owners
+  for (auto& R : h->rd) CK(cudaMemcpyAsync(R.pk0, lam, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream));
+  h->h2d_bytes += (int64_t)(sizeof(double) * m);
+  TRY(run_fapply(h, 1, nullptr));
+  const int64_t per = (int64_t)h->lam_chunk * h->nbr;  // lambda entries per rank
+  for (auto& R : h->rd) {
+    const int64_t k0 = std::min<int64_t>((int64_t)m, per * R.r), k1 = std::min<int64_t>((int64_t)m, k0 + per);
+    if (k1 > k0) CK(cudaMemcpy(q + k0, R.r1 + k0, sizeof(double) * (k1 - k0), cudaMemcpyDeviceToHost));
+  }
+  h->d2h_bytes += (int64_t)(sizeof(double) * m);
   return TCG_OK;
 }
 

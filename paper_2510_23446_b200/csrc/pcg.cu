@@ -94,6 +94,7 @@ struct StepArgs {
   int cache_lam;    // 1: the block's lambda-chunk index data are copied to shared memory
   int scratch;      // doubles of item scratch (after the prefetch tiles) in dynamic shared memory (even)
   int npf;          // tiles of the next phase's first item bulk-copied to shared memory during a barrier
+  int mode;         // 0: nsteps implicit-Euler steps; 1: nsteps applications q = F p (p = pk[0], q -> r[1])
   unsigned long long* tstamp;  // optional phase timestamps (rank 0 block 0)
   double rtol;
   int max_iter;
@@ -865,7 +866,30 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     return r;
   };
 #define PF0(j) ((j) == 0 ? tbuf : nullptr), ((j) == 0 ? npf_cur : 0)
-  for (int step = 0; step < A.nsteps; ++step) {
+  // ---- mode 1: the dual operator alone, q = F p, A.nsteps times (F-apply benchmark / test) ----
+  for (int rep = 0; A.mode == 1 && rep < A.nsteps; ++rep) {
+    const int step = -1, it = -1;  // no stamps
+    (void)step;
+    (void)it;
+    FOR_ITEMS(PH_P1, w)
+      p1_item(w, Xr,
+              [&](const ItemDesc& iw, int64_t bb, int pos) {
+                const BPos q = bget(iw, bb, pos);
+                return q.sign * ldcg(A.pk[0][lown(q.k)] + q.k);
+              },
+              A.XW[me], smw, PF0(j_w));
+    bar(PH_PC, false, 0.0);
+    PC_PHASE([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); });
+    bar(PH_P5, false, 0.0);
+    FOR_ITEMS(PH_P5, w)
+      p5_item(w, Xr, A.XW[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
+              red, nullptr, PF0(j_w));
+    bar(-1, false, 0.0);
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
+      A.r[1][me][k] = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
+    bar(PH_P1, false, 0.0);
+  }
+  for (int step = 0; A.mode == 0 && step < A.nsteps; ++step) {
     const double t = (A.step0 + step + 1) * A.dt;
     int it = 0;
     SSTAMP(0);
@@ -1057,46 +1081,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   }
 }
 
-// ---- standalone item kernels (setup precompute, F-apply benchmark), single rank: one item
+// ---- standalone item kernel (setup precompute of the insulator rhs template), one item
 // per block over the given item range.
 __global__ void __launch_bounds__(NTHR) k_fw(DevPlan D, const ItemDesc* items, int n, const double* Fv, double* Zv) {
   extern __shared__ __align__(16) double sm[];
   if (blockIdx.x >= n) return;
   fw_item(items[blockIdx.x], D.A, Fv, Zv, sm);
 }
-__global__ void __launch_bounds__(NTHR) k_p1_lam(DevPlan D, const ItemDesc* items, int n, const double* __restrict__ lam,
-                                                 double* XW) {
-  extern __shared__ __align__(16) double sm[];
-  if (blockIdx.x >= n) return;
-  p1_item(items[blockIdx.x], D.A, [&](const ItemDesc&, int64_t bb, int) { return D.b_sign[bb] * lam[D.b_lam[bb]]; },
-          XW, sm);
-}
-__global__ void __launch_bounds__(NTHR) k_pc(DevPlan D, StepArgs A, const ItemDesc* items, int n, const double* src,
-                                             double* Ppart) {
-  extern __shared__ __align__(16) double sm[];
-  if (blockIdx.x >= n) return;
-  pc_item(D, A, A.Sinv[0], items[blockIdx.x].s, items[blockIdx.x].I, A.pcprog + items[blockIdx.x].vec_off,
-          [&](int64_t i, int) { return ldcg(src + i); }, Ppart, sm);
-}
-__global__ void k_pc_sum(DevPlan D, StepArgs A, double* Pc) {
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D.nc; g += (int64_t)gridDim.x * blockDim.x)
-    Pc[g] = pc_get<true>(A, g);
-}
-__global__ void __launch_bounds__(NTHR) k_p5(DevPlan D, const ItemDesc* items, int n, const double* W, const double* Pc,
-                                             double* Y, double* Y2) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ double red[NTHR];
-  if (blockIdx.x >= n) return;
-  p5_item(items[blockIdx.x], D.A, W, D.p_grp, [&](int64_t g) { return ldcg(Pc + g); },
-          [&](const ItemDesc&, int64_t, int) { return 0.0; }, Y, Y2, sm, red);
-}
-// q = B y (F-apply benchmark output), y = Y + Y2
-__global__ void k_jump(DevPlan D, const double* Y, const double* Y2, double* q) {
-  const int64_t m = D.m;
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t ip = D.lam_idx_p[k], im = D.lam_idx_m[k];
-    q[k] = (ldcg(Y + ip) + ldcg(Y2 + ip)) - (ldcg(Y + im) + ldcg(Y2 + im));
-  }
-}
-
 }  // namespace tcg

@@ -276,3 +276,24 @@ def test_virtual_ranks_match_single_rank(tcg, name, vranks):
     assert inf["world"] == vranks
     assert np.linalg.norm(b1 - a1) <= 1e-11 * np.linalg.norm(a1)
     assert np.all(np.abs(np.array(it2) - np.array(it1)) <= 1)
+
+
+@pytest.mark.parametrize("name,vranks", [("cfg1", 1), ("cfg2", 1), ("cfg2", 3), ("contrast", 1)])
+def test_apply_F_matches_oracle(tcg, name, vranks):
+    """The dual operator alone (tcg_fapply, the persistent kernel's F-apply mode) against the
+    oracle's F = B W~^-1 B^T (full-storage solves, no shared code) on a seeded lambda."""
+    pr = next(p for p in SMALL if p.name == name) if name == "contrast" else workloads.get(name)
+    o = Oracle(copy.deepcopy(pr))
+    lam = np.random.default_rng(7).standard_normal(o.part.m)
+    ref = o.F(lam)
+    s = tcg.Solver().configure(pr)
+    if vranks > 1:
+        s.set_virtual_ranks(vranks)
+    s.setup()
+    q = s.apply_F(lam)
+    ms = s.bench_fapply(3)
+    q2 = s.apply_F(lam)
+    s.close()
+    err = np.linalg.norm(q - ref) / np.linalg.norm(ref)
+    assert err <= 1e-11, err
+    assert np.array_equal(q, q2) and ms > 0.0

@@ -12,7 +12,7 @@ import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
         d=json.loads(l); ks=d['kernel_shares']['k_steps']
-        print('BENCH $v', d['config']['workload'][:4], 'value', round(d['value'],1), 'ms/pass', round(d['ms_per_step'],3), 'k_steps ms', round(ks['ms_per_pass'],3), 'roof', round(d['roofline']['frac'],4), 'setup_ms', round(d['setup_ms'],3), 'e2e', round(d['e2e']['value'],1), 'clk', d['clocks']['sm_mhz'], d['clocks']['reasons'])
+        print('BENCH $v', d['config']['workload'][:4], 'value', round(d['value'],1), 'ms/pass', round(d['ms_per_step'],3), 'k_steps ms', round(ks['ms_per_pass'],3), 'roof', round(d['roofline']['frac'],4), 'setup_ms', round(d['setup_ms'],3), 'fapply GB/s', round((d.get('fapply') or {}).get('GBps',0)), round((d.get('fapply') or {}).get('us_per_apply',0),2), 'us', 'e2e', round(d['e2e']['value'],1), 'clk', d['clocks']['sm_mhz'], d['clocks']['reasons'])
     elif 'Error' in l or 'error' in l: print(l.rstrip())
 "
 done; done
