@@ -343,7 +343,7 @@ static tcg_status run_cholesky(tcg_ctx* h, const CholDesc* d_desc, int nmat, int
       ++h->nlaunch;
       CKL();
     }
-    k_potrf<<<nmat, 256, 0, h->stream>>>(d_desc, k, base, dinv, derr, coarse);
+    k_potrf<<<nmat, 256, 2 * TS * PS * sizeof(double), h->stream>>>(d_desc, k, base, dinv, derr, coarse);
     ++h->nlaunch;
     CKL();
     int rows = maxT - k - 1;
@@ -795,6 +795,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(set_smem(h, (const void*)k_sinv, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_trinv_row, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_tables1d, h->smem_tables));
+    TRY(set_smem(h, (const void*)k_potrf, 2 * TS * PS * sizeof(double)));
     TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_update, 2 * TS * SPAD * sizeof(double)));
     for (const void* f : {(const void*)k_steps<false, false>, (const void*)k_steps<true, false>,

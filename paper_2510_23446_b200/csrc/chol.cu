@@ -73,101 +73,148 @@ __device__ void tile_gemm_nt(const double* A, const double* B, double* C, double
 
 // -------------------------------------------------------------------------------------
 // POTRF of diagonal tile (k,k) fused with its triangular inverse (into the Dinv store).
-// One CTA (256 threads = 16x16) per matrix; thread (ty,tx) keeps elements
-// (i,c) = (ty+16a, tx+16b), a,b < 4, of L and of X = L^-1 in registers. Column j:
-//   pivot d = sqrt(W_jj); l_i = W_ij / d (i > j); X_jc /= d (c <= j);
-//   W_ic -= l_i l_c (j < c <= i);  X_ic -= l_i X_jc (c <= j < i)
-// i.e. right-looking Cholesky and right-looking forward elimination of L X = I in the same
-// sweep; column/row j are broadcast through double-buffered shared memory (2 barriers/column).
+// One CTA (256 threads) per matrix, the tile and X = L^-1 in shared memory (row stride 65).
+// Blocked by 8-column panels (few barriers; the per-column latency chain stays inside one
+// warp):
+//   panel p (warp 0, lane l = rows c0+l and c0+32+l in registers, shuffles): unblocked
+//     Cholesky of the 8 panel columns;
+//   trailing update (all threads): W_ic -= sum_{q<8} L_i,c0+q L_c,c0+q for c0+8 <= c <= i;
+//   X = L^-1 by right-looking forward elimination of L X = I in the same panels: warp 0
+//     finishes the 8 panel rows of X, the trailing phase subtracts their rank-8 contribution
+//     from the rows below.
 // -------------------------------------------------------------------------------------
+constexpr int PS = TS + 1;  // padded shared row stride of the POTRF tiles
+#ifdef POTRF_PROBE_ON
+__device__ long long g_probe[4096];
+#define POTRF_PROBE(slot) if (blockIdx.x == 0 && lane == 0 && p < 2) { asm volatile("" ::: "memory"); g_probe[(8 * p + jj) * 4 + (slot)] = clock64(); }
+#else
+#define POTRF_PROBE(x)
+#endif
 __global__ void __launch_bounds__(256) k_potrf(const CholDesc* __restrict__ ds, int k, double* base, double* dinv,
                                                DevError* err, int coarse) {
   const CholDesc d = ds[blockIdx.x];
   if (k >= d.Tfact) return;
-  __shared__ double colb[2][TS], rowb[2][TS], pv[2];
+  extern __shared__ double psm[];
+  double* As = psm;            // 64 x PS
+  double* Xs = psm + TS * PS;  // 64 x PS
+  __shared__ double dinvd[TS];  // 1 / L_jj
   double* tile = base + d.a_off + tri_off(k, k);
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  double sv[4][4], xv[4][4];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  for (int e = t; e < TSZ; e += blockDim.x) {
+    const int i = e >> 6, c = e & 63;
+    As[i * PS + c] = (c <= i) ? tile[e] : 0.0;
+    Xs[i * PS + c] = (c == i) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int p = 0; p < 8; ++p) {
+    const int c0 = 8 * p;
+    if (warp == 0) {
+      // lane l owns rows c0+l and c0+32+l of the 8-column panel in registers; column j of L
+      // is broadcast by shuffles (fully unrolled: no local memory, no barriers)
+      const int r1 = c0 + lane, r2 = c0 + 32 + lane;
+      const bool v1 = r1 < TS, v2 = r2 < TS;
+      double a1[8], a2[8];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = ty + 16 * a, c = tx + 16 * b;
-      sv[a][b] = (c <= i) ? tile[i * TS + c] : 0.0;
-      xv[a][b] = (c == i) ? 1.0 : 0.0;
-    }
-  for (int j = 0; j < TS; ++j) {
-    const int jb = j >> 4, jr = j & 15, buf = j & 1;
-    if (ty == jr && tx == jr) {
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-        if (a == jb) pv[buf] = sv[a][a];
-    }
-    __syncthreads();
-    double piv = pv[buf];
-    if (!(piv > 0.0)) {
-      if (threadIdx.x == 0 && atomicCAS(&err->flag, 0, 1) == 0) {
-        err->matrix = coarse ? -1 : (int)blockIdx.x;
-        err->index = k * TS + j;
-        err->value = piv;
+      for (int q = 0; q < 8; ++q) {
+        a1[q] = v1 ? As[r1 * PS + c0 + q] : 0.0;
+        a2[q] = v2 ? As[r2 * PS + c0 + q] : 0.0;
       }
-      piv = 1.0;
-    }
-    const double dj = sqrt(piv), inv = 1.0 / dj;
-    if (tx == jr) {  // column j of L
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if (b == jb) {
-            const int i = ty + 16 * a;
-            if (i > j) {
-              const double l = sv[a][b] * inv;
-              sv[a][b] = l;
-              colb[buf][i] = l;
-            } else if (i == j) {
-              sv[a][b] = dj;
-            }
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = c0 + jj;
+        POTRF_PROBE(0);
+        double piv = __shfl_sync(0xffffffffu, a1[jj], jj);
+        if (!(piv > 0.0)) {
+          if (lane == 0 && atomicCAS(&err->flag, 0, 1) == 0) {
+            err->matrix = coarse ? -1 : (int)blockIdx.x;
+            err->index = k * TS + j;
+            err->value = piv;
           }
-    }
-    if (ty == jr) {  // row j of X
+          piv = 1.0;
+        }
+        const double inv = rsqrt(piv);
+        POTRF_PROBE(1);
+        a1[jj] = (r1 > j) ? a1[jj] * inv : (r1 == j ? piv * inv : a1[jj]);
+        a2[jj] *= inv;
+        if (lane == 0) dinvd[j] = inv;
+        POTRF_PROBE(2);
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+        for (int q = jj + 1; q < 8; ++q) {
+          const double lc = __shfl_sync(0xffffffffu, a1[jj], q);  // L[c0+q][j]
+          a1[q] = (r1 >= c0 + q) ? a1[q] - a1[jj] * lc : a1[q];
+          a2[q] -= a2[jj] * lc;
+        }
+        POTRF_PROBE(3);
+      }
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-          if (a == jb) {
-            const int c = tx + 16 * b;
-            if (c <= j) {
-              const double x = xv[a][b] * inv;
-              xv[a][b] = x;
-              rowb[buf][c] = x;
-            }
-          }
+      for (int q = 0; q < 8; ++q) {
+        if (v1) As[r1 * PS + c0 + q] = (c0 + q <= r1) ? a1[q] : 0.0;
+        if (v2) As[r2 * PS + c0 + q] = a2[q];
+      }
+      __syncwarp();
+      // rows c0..c0+7 of X (lane = columns lane, lane+32): X_jc = (X_jc - sum_{c0<=q<j} L_jq X_qc) / L_jj
+      double x1[8], x2[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = c0 + jj;
+        double u1 = Xs[j * PS + lane], u2 = Xs[j * PS + lane + 32];
+#pragma unroll
+        for (int q = 0; q < jj; ++q) {
+          const double l = As[j * PS + c0 + q];
+          u1 -= l * x1[q];
+          u2 -= l * x2[q];
+        }
+        x1[jj] = u1 * dinvd[j];
+        x2[jj] = u2 * dinvd[j];
+        Xs[j * PS + lane] = x1[jj];
+        Xs[j * PS + lane + 32] = x2[jj];
+      }
     }
     __syncthreads();
+    // trailing updates, thread = (column c, every 4th row): W (columns >= c0+8, rows >= c) and
+    // X (columns < c0+8, rows >= c0+8): rank-8 with the panel columns / panel rows
+    {
+      const int c = t & 63, ir = t >> 6;
+      if (c < c0 + 8) {
+        double xc[8];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int i = ty + 16 * a;
-      if (i > j) {
-        const double li = colb[buf][i];
+        for (int q = 0; q < 8; ++q) xc[q] = Xs[(c0 + q) * PS + c];
+        for (int i = c0 + 8 + ir; i < TS; i += 8) {
+          const int i2 = i + 4;
+          double acc = Xs[i * PS + c], acc2 = (i2 < TS) ? Xs[i2 * PS + c] : 0.0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int c = tx + 16 * b;
-          if (c > j && c <= i) sv[a][b] -= li * colb[buf][c];
-          else if (c <= j) xv[a][b] -= li * rowb[buf][c];
+          for (int q = 0; q < 8; ++q) {
+            acc -= As[i * PS + c0 + q] * xc[q];
+            if (i2 < TS) acc2 -= As[i2 * PS + c0 + q] * xc[q];
+          }
+          Xs[i * PS + c] = acc;
+          if (i2 < TS) Xs[i2 * PS + c] = acc2;
+        }
+      } else {
+        double lc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) lc[q] = As[c * PS + c0 + q];
+        for (int i = c0 + 8 + ir; i < TS; i += 8) {  // two rows per trip: independent chains
+          const int i2 = i + 4;
+          double acc = As[i * PS + c], acc2 = (i2 < TS) ? As[i2 * PS + c] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            acc -= As[i * PS + c0 + q] * lc[q];
+            if (i2 < TS) acc2 -= As[i2 * PS + c0 + q] * lc[q];
+          }
+          if (i >= c) As[i * PS + c] = acc;
+          if (i2 < TS && i2 >= c) As[i2 * PS + c] = acc2;
         }
       }
     }
+    __syncthreads();
   }
   double* out = dinv + d.dinv_off + (int64_t)k * TSZ;
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = ty + 16 * a, c = tx + 16 * b;
-      tile[i * TS + c] = (c <= i) ? sv[a][b] : 0.0;
-      out[i * TS + c] = (c <= i) ? xv[a][b] : 0.0;
-    }
+  for (int e = t; e < TSZ; e += blockDim.x) {
+    const int i = e >> 6, c = e & 63;
+    tile[e] = (c <= i) ? As[i * PS + c] : 0.0;
+    out[e] = (c <= i) ? Xs[i * PS + c] : 0.0;
+  }
 }
 
 // A_Ik <- A_Ik L_kk^-T for I in (k, T). grid (maxT-k-1, nmat).
