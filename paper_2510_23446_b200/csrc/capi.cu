@@ -29,6 +29,8 @@
 #include "chol.cu"
 #include "solve.cu"
 #include "pcg.cu"
+#include "nd.cu"
+#include "coarse_nd.h"
 
 using namespace tcg;
 
@@ -142,6 +144,27 @@ struct tcg_ctx {
   PcgState* h_st = nullptr;  // pinned
   int maxT = 0, maxTr = 0, maxTb = 0, maxTp = 0, Tc = 0;
   int64_t nb_total = 0, vec_total = 0;
+  // sparse coarse problem (nested dissection + multifrontal); sparse = 0: dense S_pp^-1
+  int sparse = 0;
+  CoarseND nd;
+  struct NDDev {
+    double *FR = nullptr, *FDinv = nullptr, *Fscr = nullptr, *CW = nullptr, *Pcs = nullptr;
+    int64_t fr_size = 0;
+    std::vector<std::vector<int>> lvl;            // node ids per height
+    std::vector<CholDesc*> ldesc;                 // per level
+    std::vector<int*> lplist;                     // per level node list (device)
+    std::vector<int> lmaxT, lmaxTV;
+    std::vector<std::vector<int*>> lkids;         // [level][slot] children (device)
+    std::vector<std::vector<int>> nkids;
+    DevPlan Dn{};                                 // patch-like view of the nodes (k_xinv_row)
+    int *tv = nullptr, *tt = nullptr, *nv = nullptr, *nbv = nullptr, *parent = nullptr;
+    int64_t *aoff = nullptr, *moff = nullptr, *map = nullptr, *xo = nullptr;
+    int* ext = nullptr;
+    int64_t* prog = nullptr;
+    int *vl = nullptr, *bl = nullptr;
+    ItemDesc *fw = nullptr, *bw = nullptr;
+    int *fw_off = nullptr, *bw_off = nullptr;     // [(level) * (nblocks + 1) + block]
+  } ndd;
   // stepper work items per phase: ItemDesc lists ordered by (rank, block), per-block offsets
   ItemDesc* d_items[NPH] = {};
   int* d_boff[NPH] = {};
@@ -361,6 +384,50 @@ static tcg_status run_cholesky(tcg_ctx* h, const CholDesc* d_desc, int nmat, int
   return TCG_OK;
 }
 
+// Sparse coarse numeric setup: zero + pad the frontal matrices, scatter every patch's S^s,
+// then bottom-up per level: extend-add the children's update matrices, partial Cholesky of
+// the V columns, in-place inverse [L_VV^-1 ; L_BV L_VV^-1].
+static tcg_status numeric_sparse_coarse(tcg_ctx* h) {
+  auto& g = h->ndd;
+  const auto& N = h->nd.nd;
+  const int nn = (int)N.size();
+  RankDev& R = h->rd[0];
+  if (nn == 0) return TCG_OK;
+  CK(cudaMemsetAsync(g.FR, 0, sizeof(double) * (size_t)g.fr_size, h->stream));
+  k_nd_pad<<<nn, 256, 0, h->stream>>>(g.tv, g.tt, g.nv, g.nbv, g.aoff, g.FR);
+  ++h->nlaunch;
+  CKL();
+  for (int c = 0; c < 8; ++c) {
+    const int cnt = (int)(h->colour_off[c + 1] - h->colour_off[c]);
+    if (cnt == 0) continue;
+    k_nd_scatter<<<cnt, 256, 0, h->stream>>>(R.D, h->d_colour + h->colour_off[c], cnt, g.moff, g.map, g.FR);
+    ++h->nlaunch;
+    CKL();
+  }
+  for (int lv = 0; lv <= h->nd.H; ++lv) {
+    const int nlv = (int)g.lvl[lv].size();
+    if (nlv == 0) continue;
+    for (int slot = 0; slot < 2; ++slot) {
+      const int nk = g.nkids[lv][slot];
+      if (nk == 0) continue;
+      k_nd_extend<<<dim3(64, nk), 256, 0, h->stream>>>(g.lkids[lv][slot], nk, g.parent, g.tv, g.nbv, g.aoff, g.xo, g.ext,
+                                                       g.FR);
+      ++h->nlaunch;
+      CKL();
+    }
+    TRY(run_cholesky(h, g.ldesc[lv], nlv, g.lmaxT[lv], g.lmaxTV[lv], 0, g.FR, g.FDinv, nullptr, R.derr, 1));
+    for (int I = 0; I < g.lmaxT[lv]; ++I) {
+      dim3 gr(std::max(1, std::min(I + 1, g.lmaxTV[lv])), (unsigned)nlv);
+      k_xinv_row<<<gr, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(g.Dn, I, g.Fscr, g.Dn.dinv_off, g.lplist[lv]);
+      ++h->nlaunch;
+      k_xrow_copy<<<gr, 256, 0, h->stream>>>(g.Dn, I, g.Fscr, g.Dn.dinv_off, g.lplist[lv]);
+      ++h->nlaunch;
+      CKL();
+    }
+  }
+  return TCG_OK;
+}
+
 static tcg_status check_err(tcg_ctx* h) {
   CK(cudaStreamSynchronize(h->stream));
   for (auto& R : h->rd) {
@@ -439,7 +506,9 @@ static tcg_status do_numeric(tcg_ctx* h) {
   }
   CK(cudaEventRecord(e2, h->stream));
   TRY(sync_ranks(h));  // S^s of every patch final before the (replicated) coarse assembly
-  {
+  if (h->sparse) {
+    TRY(numeric_sparse_coarse(h));
+  } else {
     RankDev& R = h->rd[0];  // the coarse problem is computed once per process
     CK(cudaMemsetAsync(R.C, 0, sizeof(double) * (size_t)tri_tiles(Tc) * TSZ, h->stream));
     if (pl.nc > 0) {
@@ -552,6 +621,241 @@ static tcg_status deal_items(tcg_ctx* h, ItemLists& L, int ph, int overhead) {
   for (auto& d : all) d.bc = -1;
   h->h_items[ph] = all;
   h->h_boff[ph] = boff;
+  return TCG_OK;
+}
+
+// Sparse coarse problem: nested-dissection symbolic analysis (coarse_nd.h), node
+// storage, assembly maps, per-level factorisation descriptors, the forward gather programs and
+// the stepper's per-level work items (single-rank handles; requires h->nbr).
+static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner, const std::vector<int64_t>& cidx,
+                                      const std::vector<int>& cpat) {
+  Plan& pl = h->plan;
+  CoarseND& nd = h->nd;
+  nd = CoarseND();
+  nd.build(pl);
+  const auto& N = nd.nd;
+  const int nn = (int)N.size();
+  auto& g = h->ndd;
+  std::vector<int64_t> aoff(nn), doff(nn), voff(nn);
+  int64_t fa = 0, fd = 0, fv = 0;
+  for (int x = 0; x < nn; ++x) {
+    aoff[x] = fa;
+    fa += tri_tiles(N[x].T) * TSZ;
+    doff[x] = fd;
+    fd += (int64_t)N[x].TV * TSZ;
+    voff[x] = fv;
+    fv += (int64_t)N[x].T * TS;
+  }
+  g.fr_size = fa;
+  TRY(dalloc(h, &g.FR, std::max<int64_t>(fa, 1)));
+  TRY(dalloc(h, &g.FDinv, std::max<int64_t>(fd, 1)));
+  TRY(dalloc(h, &g.Fscr, std::max<int64_t>(fd, 1)));
+  TRY(dzero(h, &g.CW, std::max<int64_t>(fv, 1)));
+  TRY(dzero(h, &g.Pcs, std::max<int64_t>(pl.nc, 1)));
+  std::vector<int> tv(nn), tt(nn), nvv(nn), nbv(nn), par(nn), zero(nn, 0);
+  for (int x = 0; x < nn; ++x) {
+    tv[x] = N[x].TV;
+    tt[x] = N[x].T;
+    nvv[x] = (int)N[x].V.size();
+    nbv[x] = (int)N[x].B.size();
+    par[x] = N[x].parent;
+  }
+  int *dzero_i, *dtv, *dtt;
+  int64_t *daoff, *ddoff;
+  TRY(dupload(h, &dzero_i, zero));
+  TRY(dupload(h, &dtv, tv));
+  TRY(dupload(h, &dtt, tt));
+  TRY(dupload(h, &g.nv, nvv));
+  TRY(dupload(h, &g.nbv, nbv));
+  TRY(dupload(h, &g.parent, par));
+  TRY(dupload(h, &daoff, aoff));
+  TRY(dupload(h, &ddoff, doff));
+  g.tv = dtv;
+  g.tt = dtt;
+  g.aoff = daoff;
+  g.Dn = DevPlan{};
+  g.Dn.Ti = dzero_i;
+  g.Dn.Tb = dtv;
+  g.Dn.T = dtt;
+  g.Dn.a_off = daoff;
+  g.Dn.dinv_off = ddoff;
+  g.Dn.A = g.FR;
+  g.Dn.Dinv = g.FDinv;
+  // levels: factorisation descriptors, node lists, child slots
+  g.lvl.assign(nd.H + 1, {});
+  for (int x = 0; x < nn; ++x) g.lvl[N[x].height].push_back(x);
+  g.ldesc.assign(nd.H + 1, nullptr);
+  g.lplist.assign(nd.H + 1, nullptr);
+  g.lmaxT.assign(nd.H + 1, 0);
+  g.lmaxTV.assign(nd.H + 1, 0);
+  g.lkids.assign(nd.H + 1, {});
+  g.nkids.assign(nd.H + 1, {});
+  for (int lv = 0; lv <= nd.H; ++lv) {
+    std::vector<CholDesc> dsc;
+    for (int x : g.lvl[lv]) {
+      dsc.push_back(CholDesc{aoff[x], doff[x], -1, N[x].T, N[x].TV, -1, 0});
+      g.lmaxT[lv] = std::max(g.lmaxT[lv], N[x].T);
+      g.lmaxTV[lv] = std::max(g.lmaxTV[lv], N[x].TV);
+    }
+    TRY(dupload(h, &g.ldesc[lv], dsc));
+    TRY(dupload(h, &g.lplist[lv], g.lvl[lv]));
+    for (int slot = 0; slot < 2; ++slot) {
+      std::vector<int> kids;
+      for (int x : g.lvl[lv])
+        if ((int)N[x].child.size() > slot) kids.push_back(N[x].child[slot]);
+      int* dk = nullptr;
+      if (!kids.empty()) TRY(dupload(h, &dk, kids));
+      g.lkids[lv].push_back(dk);
+      g.nkids[lv].push_back((int)kids.size());
+    }
+    for (int x : g.lvl[lv])
+      if (N[x].child.size() > 2) return fail(h, TCG_EINVAL, "nested dissection: more than 2 children");
+  }
+  // S^s -> frontal scatter maps (one entry per (a, b) of each patch, -1 = counted elsewhere)
+  {
+    std::vector<int64_t> moff(pl.npatch + 1, 0), map;
+    for (int s2 = 0; s2 < pl.npatch; ++s2) {
+      const auto& grp = pl.pp[s2].p_grp;
+      const int np2 = (int)grp.size();
+      moff[s2 + 1] = moff[s2] + (int64_t)np2 * np2;
+      for (int a = 0; a < np2; ++a)
+        for (int b = 0; b < np2; ++b) {
+          const int ga = grp[a], gb = grp[b];
+          if (ga < gb) {
+            map.push_back(-1);
+            continue;
+          }
+          const int x = std::min(nd.node_of[ga], nd.node_of[gb]);  // postorder: descendant first
+          const int fa2 = nd.fpos(x, ga), fb2 = nd.fpos(x, gb);
+          if (fa2 < 0 || fb2 < 0) return fail(h, TCG_EINVAL, "nested dissection: coupled pair outside a front");
+          const int r = std::max(fa2, fb2), c = std::min(fa2, fb2);
+          map.push_back(aoff[x] + tri_off(r >> 6, c >> 6) + (int64_t)(r & 63) * TS + (c & 63));
+        }
+    }
+    if (map.empty()) map.push_back(-1);
+    TRY(dupload(h, &g.moff, moff));
+    TRY(dupload(h, &g.map, map));
+  }
+  // extend-add maps and forward gather programs
+  std::vector<int64_t> xo(nn + 1, 0);
+  std::vector<int> ext;
+  std::vector<std::vector<std::vector<int64_t>>> src(nn);  // [node][frontal pos] sources
+  for (int x = 0; x < nn; ++x) {
+    src[x].assign((size_t)N[x].T * TS, {});
+    for (size_t e = 0; e < N[x].V.size(); ++e) {
+      const int gg = N[x].V[e];
+      for (int k = pl.coarse_ptr[gg]; k < pl.coarse_ptr[gg + 1]; ++k)
+        src[x][e].push_back(cidx[k] | ((int64_t)owner[cpat[k]] << 56));
+    }
+  }
+  for (int c = 0; c < nn; ++c) {
+    xo[c] = (int64_t)ext.size();
+    const int p = N[c].parent;
+    for (size_t i = 0; i < N[c].B.size(); ++i) {
+      const int pp2 = nd.fpos(p, N[c].B[i]);
+      if (pp2 < 0) return fail(h, TCG_EINVAL, "nested dissection: update row outside the parent front");
+      ext.push_back(pp2);
+      src[p][pp2].push_back((voff[c] + (int64_t)N[c].TV * TS + (int64_t)i) | (1ll << 55));
+    }
+  }
+  xo[nn] = (int64_t)ext.size();
+  if (ext.empty()) ext.push_back(0);
+  TRY(dupload(h, &g.xo, xo));
+  TRY(dupload(h, &g.ext, ext));
+  std::vector<int64_t> prog, poff(nn);
+  std::vector<int> vl, bl;
+  std::vector<int64_t> vlo(nn), blo(nn);
+  for (int x = 0; x < nn; ++x) {
+    poff[x] = (int64_t)prog.size();
+    const size_t ne = src[x].size();
+    std::vector<int64_t> offs(ne + 1, 0), ent;
+    for (size_t e = 0; e < ne; ++e) {
+      for (int64_t v : src[x][e]) ent.push_back(v);
+      offs[e + 1] = (int64_t)ent.size();
+    }
+    prog.insert(prog.end(), offs.begin(), offs.end());
+    prog.insert(prog.end(), ent.begin(), ent.end());
+    vlo[x] = (int64_t)vl.size();
+    vl.insert(vl.end(), N[x].V.begin(), N[x].V.end());
+    blo[x] = (int64_t)bl.size();
+    bl.insert(bl.end(), N[x].B.begin(), N[x].B.end());
+  }
+  if (prog.empty()) prog.push_back(0);
+  if (vl.empty()) vl.push_back(0);
+  if (bl.empty()) bl.push_back(0);
+  TRY(dupload(h, &g.prog, prog));
+  TRY(dupload(h, &g.vl, vl));
+  TRY(dupload(h, &g.bl, bl));
+  // stepper items: forward rows (x, I < T) and backward V columns (x, J < TV), per level, LPT
+  const int nb2 = h->nbr;
+  std::vector<ItemDesc> fwi, bwi;
+  std::vector<int> fwo(1, 0), bwo(1, 0);
+  for (int lv = 0; lv <= nd.H; ++lv) {
+    for (int dir = 0; dir < 2; ++dir) {
+      std::vector<std::pair<int, ItemDesc>> items;
+      for (int x : g.lvl[lv]) {
+        ItemDesc d{};
+        d.s = x;
+        d.Ti = 0;
+        d.Tb = N[x].TV;
+        d.Tp = N[x].TB;
+        d.T = N[x].T;
+        d.nb = (int)N[x].B.size();
+        d.np = (int)N[x].V.size();
+        d.a_off = aoff[x];
+        d.vec_off = voff[x];
+        d.p_off = poff[x];
+        d.b_off = blo[x];
+        d.sbb_off = vlo[x];
+        d.bc = -1;
+        if (dir == 0) {
+          const int rows = (N[x].parent >= 0) ? N[x].T : N[x].TV;  // the root passes nothing up
+          for (int I = 0; I < rows; ++I) {
+            d.I = I;
+            items.push_back({(I < N[x].TV ? I + 1 : N[x].TV) + 1, d});
+          }
+        } else {
+          for (int J = 0; J < N[x].TV; ++J) {
+            d.I = J;
+            items.push_back({N[x].T - J, d});
+          }
+        }
+      }
+      std::stable_sort(items.begin(), items.end(), [](const auto& a, const auto& b) {
+        return a.first != b.first ? a.first > b.first : (a.second.s != b.second.s ? a.second.s < b.second.s : a.second.I < b.second.I);
+      });
+      std::vector<std::vector<ItemDesc>> blk(nb2);
+      std::vector<std::pair<int64_t, int>> heap;
+      for (int b = 0; b < nb2; ++b) heap.push_back({0, b});
+      auto cmp = [](const std::pair<int64_t, int>& a, const std::pair<int64_t, int>& b) { return a > b; };
+      std::make_heap(heap.begin(), heap.end(), cmp);
+      for (auto& e : items) {
+        std::pop_heap(heap.begin(), heap.end(), cmp);
+        blk[heap.back().second].push_back(e.second);
+        heap.back().first += e.first + 2;
+        std::push_heap(heap.begin(), heap.end(), cmp);
+      }
+      auto& all = dir == 0 ? fwi : bwi;
+      auto& off = dir == 0 ? fwo : bwo;
+      for (int b = 0; b < nb2; ++b) {
+        all.insert(all.end(), blk[b].begin(), blk[b].end());
+        off.push_back((int)all.size());
+      }
+    }
+  }
+  if (fwi.empty()) fwi.push_back(ItemDesc{});
+  if (bwi.empty()) bwi.push_back(ItemDesc{});
+  {  // forward rows gather up to T_V tiles of the node rhs into the item scratch
+    int maxTV = 0;
+    for (const auto& n : N) maxTV = std::max(maxTV, n.TV);
+    size_t need = (size_t)maxTV * TS + 16 * TS;
+    need = (need + 1) & ~(size_t)1;
+    h->smem_pcg = std::max(h->smem_pcg, need * sizeof(double));
+  }
+  TRY(dupload(h, &g.fw, fwi));
+  TRY(dupload(h, &g.bw, bwi));
+  TRY(dupload(h, &g.fw_off, fwo));
+  TRY(dupload(h, &g.bw_off, bwo));
   return TCG_OK;
 }
 
@@ -823,6 +1127,12 @@ static tcg_status do_setup(tcg_ctx* h) {
     const int flags = fe ? atoi(fe) : (ws < 48e6 ? 1 : 0);
     CK(cudaMemcpyToSymbol(c_step_flags, &flags, sizeof(int)));
   }
+  // ---- coarse problem: dense S_pp^-1 (small n_c) or sparse multifrontal ----
+  {
+    const char* ce = getenv("TCG_COARSE");  // "dense", "sparse", default auto
+    const bool want = ce ? (std::strcmp(ce, "sparse") == 0) : (pl.nc > 8192);
+    h->sparse = (want && NR == 1 && pl.nc > 0) ? 1 : 0;
+  }
   // ---- work items per rank, dealt to the rank's persistent blocks (LPT) ----
   std::vector<int> crow_owner(std::max(Tc, 1));
   for (int I = 0; I < Tc; ++I) crow_owner[I] = (int)((int64_t)I * NR / Tc);
@@ -887,7 +1197,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     }
     if (prog.empty()) prog.push_back(0);
     TRY(dupload(h, &h->d_pcprog, prog));
-    for (int I = 0; I < Tc; ++I)
+    for (int I = 0; I < (h->sparse ? 0 : Tc); ++I)
       for (int c = 0; c < h->coarse_maxch; ++c) {
         ItemDesc d{};
         d.s = I;
@@ -906,6 +1216,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(deal_items(h, bw, PH_BW, 2));
     TRY(deal_items(h, bwc, PH_BWC, 2));
     TRY(deal_items(h, rhs, PH_RHS, 0));
+    if (h->sparse) TRY(setup_sparse_coarse(h, owner, cidx, cpat));
   }
   // shared-memory caches of the per-iteration item lists and the lambda chunk, if they fit
   // next to the scratch at `per` blocks per SM
@@ -1049,10 +1360,11 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dzero(h, &R.st, 1));
     TRY(dzero(h, &R.derr, 1));
     if (li == 0) {
-      TRY(dalloc(h, &R.C, (size_t)tri_tiles(Tc) * TSZ));
-      TRY(dalloc(h, &R.Cinv, (size_t)Tc * TSZ));
-      TRY(dalloc(h, &R.CX, (size_t)tri_tiles(Tc) * TSZ));
-      TRY(dalloc(h, &R.Sinv, (size_t)Tc * Tc * TSZ));
+      const int Tcd = h->sparse ? 1 : Tc;  // the sparse coarse keeps no dense factor / inverse
+      TRY(dalloc(h, &R.C, (size_t)tri_tiles(Tcd) * TSZ));
+      TRY(dalloc(h, &R.Cinv, (size_t)Tcd * TSZ));
+      TRY(dalloc(h, &R.CX, (size_t)tri_tiles(Tcd) * TSZ));
+      TRY(dalloc(h, &R.Sinv, (size_t)Tcd * Tcd * TSZ));
     } else {
       R.C = h->rd[0].C;
       R.Cinv = h->rd[0].Cinv;
@@ -1227,6 +1539,21 @@ static StepArgs step_args(tcg_ctx* h) {
   A.scratch = (int)(h->smem_pcg / sizeof(double));
   A.npf = h->npf;
   A.mode = 0;
+  A.sparse = h->sparse;
+  if (h->sparse) {
+    const auto& g = h->ndd;
+    A.cf_levels = h->nd.H + 1;
+    A.cf_fw = g.fw;
+    A.cf_fw_off = g.fw_off;
+    A.cf_bw = g.bw;
+    A.cf_bw_off = g.bw_off;
+    A.FR = g.FR;
+    A.cf_prog = g.prog;
+    A.cf_vl = g.vl;
+    A.cf_bl = g.bl;
+    A.CW = g.CW;
+    A.Pcs = g.Pcs;
+  }
   A.tstamp = h->tstamp;
   A.rtol = h->rtol;
   A.max_iter = h->max_iter;

@@ -95,6 +95,19 @@ struct StepArgs {
   int scratch;      // doubles of item scratch (after the prefetch tiles) in dynamic shared memory (even)
   int npf;          // tiles of the next phase's first item bulk-copied to shared memory during a barrier
   int mode;         // 0: nsteps implicit-Euler steps; 1: nsteps applications q = F p (p = pk[0], q -> r[1])
+  // sparse coarse: per level forward rows / backward columns of the node factors
+  int sparse;
+  int cf_levels;                 // tree height + 1
+  const ItemDesc* cf_fw;         // block gb, level lv: items [cf_fw_off[lv * nbr + gb], .. + 1)
+  const int* cf_fw_off;
+  const ItemDesc* cf_bw;
+  const int* cf_bw_off;
+  const double* FR;              // node inverse factors [L_VV^-1 ; L_BV L_VV^-1] (tile-packed)
+  const int64_t* cf_prog;        // forward gather programs (offs, then tagged sources)
+  const int* cf_vl;              // node V groups
+  const int* cf_bl;              // node B groups
+  double* CW;                    // node forward vectors (y_V ; f_B - L_BV y_V)
+  double* Pcs;                   // coarse solution by primal group
   unsigned long long* tstamp;  // optional phase timestamps (rank 0 block 0)
   double rtol;
   int max_iter;
@@ -506,6 +519,78 @@ __device__ __forceinline__ void bw_item(const DevPlan& D, const ItemDesc& it, co
   __syncthreads();
 }
 
+// ---- sparse coarse forward row I of node x: y_V = L_VV^-1 f_V (rows < TV) or the update
+// f_B - L_BV L_VV^-1 f_V (rows >= TV), f gathered by the node's program: tag bit 55 set = the
+// child's forward vector (CW), else gsrc(aug index, owner rank) of a patch's primal row.
+constexpr int64_t kTag = 1ll << 55, kIdx55 = kTag - 1;
+template <class GS>
+__device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, const int64_t* prog, GS gsrc, double* CW,
+                                         double* sm) {
+  const int I = it.I, TV = it.Tb, T = it.T;
+  const int Jn = (I < TV) ? I + 1 : TV;
+  const double* X = FR + it.a_off;
+  const int64_t* offs = prog + it.p_off;
+  const int64_t* ent = offs + (int64_t)T * TS + 1;
+  auto fval = [&](int e) {
+    double v = 0.0;
+    for (int64_t q = offs[e]; q < offs[e + 1]; ++q) {
+      const int64_t en = ent[q];
+      v += (en & kTag) ? ldcg(CW + (en & kIdx55)) : gsrc(en & kIdx55, (int)(en >> 56));
+    }
+    return v;
+  };
+  double part[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) part[r] = 0.0;
+  gemv_row_g([&](int J) { return X + tri_off(I, J); }, 0, Jn, sm,
+             [&] {
+               for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x) sm[e] = fval(e);
+             },
+             part);
+  const double sum = warp_reduce8(part);
+  const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
+  if ((lane & 3) == 0) {
+    const int row = I * TS + row0 + warp_reduce8_row();
+    CW[it.vec_off + row] = (I < TV) ? sum : fval(row) - sum;
+  }
+  __syncthreads();
+}
+// ---- sparse coarse backward column block J of node x: x_V = L_VV^-T y_V - (L_BV L_VV^-1)^T x_B
+// (rows streamed in chunks of `ch` tiles through the shared scratch: B can be long)
+template <class Dummy = int>
+__device__ __forceinline__ void bwc_item(const ItemDesc& it, const double* FR, const double* CW, const int* vl,
+                                         const int* bl, double* Pcs, double* sm, int ch) {
+  const int J = it.I, TV = it.Tb, T = it.T, nV = it.np, nB = it.nb;
+  const double* X = FR + it.a_off;
+  double* sx = sm;
+  double* cr = sm + (int64_t)ch * TS;
+  double c0 = 0.0, c1 = 0.0;
+  for (int I0 = J; I0 < T; I0 += ch) {
+    const int I1 = min(T, I0 + ch);
+    gemv_col_g([&](int I) { return X + tri_off(I, J); }, I0, I1, sx,
+               [&] {
+                 for (int e = threadIdx.x; e < (I1 - I0) * TS; e += blockDim.x) {
+                   const int i = I0 * TS + e;
+                   double val;
+                   if (i < TV * TS) val = ldcg(CW + it.vec_off + i);
+                   else {
+                     const int t = i - TV * TS;
+                     val = (t < nB) ? -ldcg(Pcs + bl[it.b_off + t]) : 0.0;
+                   }
+                   sx[e] = val;
+                 }
+               },
+               c0, c1);
+    __syncthreads();  // sx reused by the next chunk
+  }
+  const double acc = col_finish(c0, c1, cr);
+  if (threadIdx.x < TS) {
+    const int j = J * TS + threadIdx.x;
+    if (j < nV) Pcs[vl[it.sbb_off + j]] = acc;
+  }
+  __syncthreads();
+}
+
 constexpr unsigned long long kBarrierTimeoutNs = 30ull * 1000000000ull;  // 30 s watchdog
 
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p, int sys) {
@@ -805,7 +890,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   auto lown = [&](int64_t k) { return MULTI ? ((int)k / (int)A.lam_chunk) / A.nbr : 0; };
   auto pown = [&](int s) { return MULTI ? D.owner[s] : 0; };
   auto own_idx = [&](const ItemDesc& it, int pos) { return it.vec_off + (int64_t)it.Ti * TS + pos; };
-  auto pcf = [&](int64_t g) { return pc_get<MULTI>(A, g); };
+  auto pcf = [&](int64_t g) { return A.sparse ? ldcg(A.Pcs + g) : pc_get<MULTI>(A, g); };
   auto yv = [&](int o, int64_t i) { return ldcg(A.Y[o] + i) + ldcg(A.Y2[o] + i); };  // y = Y + Y2
   // partner patch of b position bb (other endpoint of its multiplier)
   auto ppatch = [&](int64_t bb) {
@@ -866,6 +951,26 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     return r;
   };
 #define PF0(j) ((j) == 0 ? tbuf : nullptr), ((j) == 0 ? npf_cur : 0)
+  // sparse coarse solve S_pp x = sum_s N_s^T (src): forward levels bottom-up, backward levels
+  // top-down, a grid barrier between levels (the caller's barrier follows the last one)
+  auto coarse_sparse = [&](auto gsrc) {
+    for (int lv = 0; lv < A.cf_levels; ++lv) {
+      const int b = A.cf_fw_off[lv * A.nbr + bl], e = A.cf_fw_off[lv * A.nbr + bl + 1];
+      for (int j = b; j < e; ++j) fwc_item(A.cf_fw[j], A.FR, A.cf_prog, gsrc, A.CW, smw);
+      bar(-1, false, 0.0);
+    }
+    for (int lv = A.cf_levels - 1; lv >= 0; --lv) {
+      const int b = A.cf_bw_off[lv * A.nbr + bl], e = A.cf_bw_off[lv * A.nbr + bl + 1];
+      for (int j = b; j < e; ++j) bwc_item(A.cf_bw[j], A.FR, A.CW, A.cf_vl, A.cf_bl, A.Pcs, smw, A.scratch / TS - 9);
+      if (lv > 0) bar(-1, false, 0.0);
+    }
+  };
+#define COARSE(GS)                \
+  if (A.sparse) {                 \
+    coarse_sparse(GS);            \
+  } else {                        \
+    PC_PHASE(GS);                 \
+  }
   // ---- mode 1: the dual operator alone, q = F p, A.nsteps times (F-apply benchmark / test) ----
   for (int rep = 0; A.mode == 1 && rep < A.nsteps; ++rep) {
     const int step = -1, it = -1;  // no stamps
@@ -879,7 +984,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
               },
               A.XW[me], smw, PF0(j_w));
     bar(PH_PC, false, 0.0);
-    PC_PHASE([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); });
+    COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
     bar(PH_P5, false, 0.0);
     FOR_ITEMS(PH_P5, w)
       p5_item(w, Xr, A.XW[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
@@ -902,7 +1007,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     bar(PH_PC, false, 0.0);
     SSTAMP(2);
     // ---- R3 p0 = S_pp^-1 sum N^T Z_p ----
-    PC_PHASE([&](int64_t i, int o) { return ldcg(A.Z[MULTI ? o : 0] + i); });
+    COARSE(([&](int64_t i, int o) { return ldcg(A.Z[MULTI ? o : 0] + i); }));
     bar(PH_P5, false, 0.0);
     SSTAMP(3);
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
@@ -964,7 +1069,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       bar(PH_PC, false, 0.0);
       TSTAMP(1);
       // PC
-      PC_PHASE([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); });
+      COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
       WSTAMP(1);
       bar(PH_P5, false, 0.0);
       TSTAMP(2);
@@ -1057,10 +1162,10 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     bar(PH_PC, false, 0.0);
     SSTAMP(7);
     // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
-    PC_PHASE([&](int64_t i, int o) {
+    COARSE(([&](int64_t i, int o) {
       const int r = MULTI ? o : 0;
       return ldcg(A.Z[r] + i) - ldcg(A.XW[r] + i);
-    });
+    }));
     bar(-1, false, 0.0);
     SSTAMP(8);
     // ---- E3 a_r = X_rr^T (Z_r - [0; w_b]) - Phi N p, a_p = N p ----

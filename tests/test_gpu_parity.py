@@ -297,3 +297,43 @@ def test_apply_F_matches_oracle(tcg, name, vranks):
     err = np.linalg.norm(q - ref) / np.linalg.norm(ref)
     assert err <= 1e-11, err
     assert np.array_equal(q, q2) and ms > 0.0
+
+
+@pytest.fixture
+def sparse_coarse(monkeypatch):
+    """Force the nested-dissection multifrontal coarse solver for small cases."""
+    monkeypatch.setenv("TCG_COARSE", "sparse")
+    yield
+
+
+@pytest.mark.parametrize("name", ["cfg1", "corner-conductor", "floating-centre", "contrast", "p3-ragged-tiles"])
+def test_sparse_coarse_matches_oracle(tcg, sparse_coarse, name):
+    """The sparse coarse path (nested dissection, multifrontal factor, per-level forward /
+    backward solves in the persistent kernel) against the oracle's dense coarse Cholesky."""
+    pr = workloads.cfg1() if name == "cfg1" else next(p for p in SMALL if p.name == name)
+    compare(tcg, pr)
+
+
+def test_sparse_coarse_cfg2_steps_and_F(tcg, sparse_coarse):
+    compare(tcg, workloads.cfg2(), steps=3)
+    o = Oracle(workloads.cfg2())
+    lam = np.random.default_rng(3).standard_normal(o.part.m)
+    s = tcg.Solver().configure(workloads.cfg2())
+    s.setup()
+    q = s.apply_F(lam)
+    s.close()
+    ref = o.F(lam)
+    assert np.linalg.norm(q - ref) / np.linalg.norm(ref) <= 1e-11
+
+
+def test_sparse_vs_dense_coarse_cfg4(tcg, monkeypatch):
+    """cfg4 (n_c ~ 15.7k, sparse by default) against the dense S_pp^-1 path, first 2 steps."""
+    pr = workloads.cfg4()
+    res = {}
+    for mode in ("sparse", "dense"):
+        monkeypatch.setenv("TCG_COARSE", mode)
+        a1, a0, it, hist, inf = run_gpu(tcg, pr, 2)
+        res[mode] = (a1, list(it))
+    a, b = res["sparse"][0], res["dense"][0]
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-9
+    assert all(abs(x - y) <= 1 for x, y in zip(res["sparse"][1], res["dense"][1]))
