@@ -99,6 +99,10 @@ typedef struct tcg_info {
   int64_t h2d_bytes, d2h_bytes; /* host<->device bytes moved by this handle (cumulative)  */
   int32_t rank, world;
   int32_t pad_;
+  int32_t coarse_sparse;  /* 1: nested-dissection multifrontal coarse, 0: dense S_pp^-1 */
+  int64_t coarse_nodes;   /* separator-tree nodes of the sparse coarse (0 if dense)          */
+  int64_t coarse_levels;  /* tree height + 1: forward + backward phases per coarse solve     */
+  double coarse_factor_bytes; /* bytes of the coarse inverse factors read per coarse solve   */
 } tcg_info;
 
 /* Create a handle. device: CUDA ordinal used by setup; rank/world: this process's place

@@ -33,7 +33,8 @@ class TcgInfo(C.Structure):
         "kernel_launches")] + [(n, C.c_double) for n in (
         "bytes_fapply", "bytes_precond", "bytes_step_fixed", "flops_factor", "ms_plan", "ms_assembly", "ms_factor",
         "ms_coarse", "ms_steps", "ms_pcg_last_step", "prof_ms")] + [("prof_launches", C.c_int64),
-        ("prof_bytes_per_launch", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32), ("pad_", C.c_int32)]
+        ("prof_bytes_per_launch", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32), ("pad_", C.c_int32),
+        ("coarse_sparse", C.c_int32), ("coarse_nodes", C.c_int64), ("coarse_levels", C.c_int64), ("coarse_factor_bytes", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_ if n != "pad_"}

@@ -1902,10 +1902,40 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
     fl += nrp * nrp * nrp / 3.0 + 2.0 * nrp * nrp * q.np + 2.0 * nrp * q.np * q.np;
   }
   const double nc = (double)p.nc;
-  bf += 8.0 * nc * (nc + 1) + 40.0 * p.m;
+  if (h->sparse) {
+    // sparse coarse: forward and backward each read every node's [L_VV^-1 (lower) ; L_BV L_VV^-1]
+    for (const auto& n : h->nd.nd) {
+      const double v = (double)n.V.size(), b = (double)n.B.size();
+      bf += 2.0 * 8.0 * (v * (v + 1) / 2 + v * b);
+    }
+    bf += 40.0 * p.m;
+  } else {
+    bf += 8.0 * nc * (nc + 1) + 40.0 * p.m;  // dense S_pp^-1 read once = two triangular passes
+  }
   bm += 40.0 * p.m;
   bs += bf + bm;  // R3/R4/E1/E2 (one F-apply worth) and the z0 preconditioner apply (R5)
-  fl += nc * nc * nc / 3.0;
+  if (h->sparse) {
+    for (const auto& n : h->nd.nd) {  // partial Cholesky of the V columns + in-place inverse
+      const double v = (double)n.V.size(), b = (double)n.B.size();
+      fl += v * v * v / 3.0 + v * v * b + v * b * b + v * v * v / 3.0 + v * v * b;
+    }
+  } else {
+    fl += nc * nc * nc / 3.0;
+  }
+  out->coarse_sparse = h->sparse;
+  out->coarse_nodes = h->sparse ? (int64_t)h->nd.nd.size() : 0;
+  out->coarse_levels = h->sparse ? h->nd.H + 1 : 1;
+  {
+    double cb = 0.0;
+    if (h->sparse)
+      for (const auto& n : h->nd.nd) {
+        const double v = (double)n.V.size(), b = (double)n.B.size();
+        cb += 2.0 * 8.0 * (v * (v + 1) / 2 + v * b);
+      }
+    else
+      cb = 8.0 * nc * nc;
+    out->coarse_factor_bytes = cb;
+  }
   out->bytes_fapply = bf;
   out->bytes_precond = bm;
   out->bytes_step_fixed = bs;
