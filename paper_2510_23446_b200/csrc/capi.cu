@@ -164,6 +164,8 @@ struct tcg_ctx {
     int *vl = nullptr, *bl = nullptr;
     ItemDesc *fw = nullptr, *bw = nullptr;
     int *fw_off = nullptr, *bw_off = nullptr;     // [(level) * (nblocks + 1) + block]
+    double* pb = nullptr;                          // backward chunk partials
+    unsigned int* cnt = nullptr;                   // backward chunk counters
   } ndd;
   // stepper work items per phase: ItemDesc lists ordered by (rank, block), per-block offsets
   ItemDesc* d_items[NPH] = {};
@@ -286,6 +288,8 @@ tcg_status dalloc(tcg_ctx* h, T** out, size_t n) {
     if (e == cudaSuccess) h->allocs.push_back(p);
   }
   if (e != cudaSuccess) return fail(h, TCG_ENOMEM, std::string("cudaMalloc ") + std::to_string(bytes) + ": " + cudaGetErrorString(e));
+  static const bool poison = getenv("TCG_POISON") && atoi(getenv("TCG_POISON")) != 0;  // debug: NaN-fill
+  if (poison) cudaMemsetAsync(p, 0xff, bytes, h->stream);
   h->device_bytes += (int64_t)bytes;
   *out = static_cast<T*>(p);
   return TCG_OK;
@@ -788,6 +792,8 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
   TRY(dupload(h, &g.bl, bl));
   // stepper items: forward rows (x, I < T) and backward V columns (x, J < TV), per level, LPT
   const int nb2 = h->nbr;
+  int64_t npb = 0;
+  int ncnt = 0;
   std::vector<ItemDesc> fwi, bwi;
   std::vector<int> fwo(1, 0), bwo(1, 0);
   for (int lv = 0; lv <= nd.H; ++lv) {
@@ -817,7 +823,15 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
         } else {
           for (int J = 0; J < N[x].TV; ++J) {
             d.I = J;
-            items.push_back({N[x].T - J, d});
+            const int nch = (N[x].T - J + kBwChunk - 1) / kBwChunk;  // row chunks of this column
+            d.bc = nch;
+            d.p_off = npb;   // first partial slot
+            d.Ti = ncnt++;   // arrival counter
+            npb += nch;
+            for (int c = 0; c < nch; ++c) {
+              d.part = c;
+              items.push_back({std::min(kBwChunk, N[x].T - J - c * kBwChunk), d});
+            }
           }
         }
       }
@@ -856,6 +870,8 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
   TRY(dupload(h, &g.bw, bwi));
   TRY(dupload(h, &g.fw_off, fwo));
   TRY(dupload(h, &g.bw_off, bwo));
+  TRY(dzero(h, &g.pb, std::max<int64_t>(npb, 1) * TS));
+  TRY(dzero(h, &g.cnt, std::max(ncnt, 1)));
   return TCG_OK;
 }
 
@@ -1353,7 +1369,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dzero(h, &R.q, pl.m));
     TRY(dzero(h, &R.Ppart, (size_t)Tc * h->coarse_maxch * TS));
     TRY(dzero(h, &R.Pc, pl.nc));
-    TRY(dzero(h, &R.partials, (size_t)h->nbr + 1));
+    TRY(dzero(h, &R.partials, 2 * (size_t)h->nbr + 1));
     TRY(dzero(h, &R.hist, (size_t)(h->n_steps + 1) * (h->max_iter + 1)));
     TRY(dzero(h, &R.iters, (size_t)h->n_steps + 1));
     TRY(dzero(h, &R.bar, 1));
@@ -1539,6 +1555,7 @@ static StepArgs step_args(tcg_ctx* h) {
   A.scratch = (int)(h->smem_pcg / sizeof(double));
   A.npf = h->npf;
   A.mode = 0;
+  A.dbg_stop = getenv("TCG_DEBUG_STOP") ? atoi(getenv("TCG_DEBUG_STOP")) : 0;
   A.sparse = h->sparse;
   if (h->sparse) {
     const auto& g = h->ndd;
@@ -1553,6 +1570,8 @@ static StepArgs step_args(tcg_ctx* h) {
     A.cf_bl = g.bl;
     A.CW = g.CW;
     A.Pcs = g.Pcs;
+    A.cf_pb = g.pb;
+    A.cf_cnt = g.cnt;
   }
   A.tstamp = h->tstamp;
   A.rtol = h->rtol;
@@ -1589,6 +1608,7 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NTHR), args, h->smem_steps, h->stream));
   ++h->nlaunch;
   prof_end(h, 7);
+
   RankDev& R0 = h->rd[0];
   CK(cudaMemcpyAsync(h->h_st, R0.st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
   h->d2h_bytes += (int64_t)sizeof(PcgState);
@@ -2058,6 +2078,11 @@ tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t 
   } else if (what == 6) {
     src = R.Sbb + h->h_sbb_off[idx];
     n = tri_tiles(h->plan.pp[idx].Tb) * TSZ;
+  } else if (what == 8) {  // sparse coarse solution (by primal group) and forward vectors
+    if (!h->sparse) return fail(h, TCG_ESTATE, "dense coarse");
+    std::vector<double> a((size_t)h->plan.nc);
+    CK(cudaMemcpy(a.data(), h->ndd.Pcs, sizeof(double) * a.size(), cudaMemcpyDeviceToHost));
+    tmp = a;
   } else if (what == 7) {
     if (!h->tstamp) return fail(h, TCG_ESTATE, "TCG_PHASE_TIMING not set");
     std::vector<unsigned long long> ts(8 * 64 + 16 + 8 * 4096);

@@ -95,6 +95,7 @@ struct StepArgs {
   int scratch;      // doubles of item scratch (after the prefetch tiles) in dynamic shared memory (even)
   int npf;          // tiles of the next phase's first item bulk-copied to shared memory during a barrier
   int mode;         // 0: nsteps implicit-Euler steps; 1: nsteps applications q = F p (p = pk[0], q -> r[1])
+  int dbg_stop;     // debug: 1 = return after the first step's R3 coarse solve
   // sparse coarse: per level forward rows / backward columns of the node factors
   int sparse;
   int cf_levels;                 // tree height + 1
@@ -108,6 +109,8 @@ struct StepArgs {
   const int* cf_bl;              // node B groups
   double* CW;                    // node forward vectors (y_V ; f_B - L_BV y_V)
   double* Pcs;                   // coarse solution by primal group
+  double* cf_pb;                 // backward chunk partial sums (64 per chunk)
+  unsigned int* cf_cnt;          // backward chunk arrival counters (monotone)
   unsigned long long* tstamp;  // optional phase timestamps (rank 0 block 0)
   double rtol;
   int max_iter;
@@ -203,7 +206,8 @@ __device__ __forceinline__ double pc_get(const StepArgs& A, int64_t g) {
 // Warp w owns rows 8w..8w+7 of every 64x64 tile, lane l columns 2l, 2l+1. The first two
 // tiles are prefetched into L1 (non-binding, no registers held), then gather() fills the
 // input vector in shared memory, then the tiles are streamed (2 tiles of loads in flight).
-// experiment switches (TCG_STEP_FLAGS): bit 0 = no L1 prefetch of the first tiles
+// experiment switches (TCG_STEP_FLAGS): bit 0 = no L1 prefetch of the first tiles; bits 4+ph =
+// no bulk-copy prefetch for phase ph
 __constant__ int c_step_flags;
 __device__ __forceinline__ void prefetch_l1(const double* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
@@ -234,6 +238,7 @@ __device__ __forceinline__ void gemv_row_g(TileF tile, int J0, int J1, const dou
     double2 a[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) a[r] = lds2(t + r * TS);
+
 #pragma unroll
     for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
   }
@@ -556,17 +561,25 @@ __device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, c
   __syncthreads();
 }
 // ---- sparse coarse backward column block J of node x: x_V = L_VV^-T y_V - (L_BV L_VV^-1)^T x_B
-// (rows streamed in chunks of `ch` tiles through the shared scratch: B can be long)
+// Long columns (B can hold thousands of groups) are split into row chunks (ItemDesc: part =
+// chunk, bc = chunks, p_off = first partial slot, Ti = counter): each chunk writes its partial
+// column sum, the last arriving chunk (monotone counter) adds the partials in chunk order.
+// Rows are streamed through the shared scratch `ch` tiles at a time.
+constexpr int kBwChunk = 8;  // row tiles per backward chunk item
 template <class Dummy = int>
 __device__ __forceinline__ void bwc_item(const ItemDesc& it, const double* FR, const double* CW, const int* vl,
-                                         const int* bl, double* Pcs, double* sm, int ch) {
+                                         const int* bl, double* Pcs, double* PB, unsigned int* cnt, double* sm,
+                                         int ch) {
   const int J = it.I, TV = it.Tb, T = it.T, nV = it.np, nB = it.nb;
+  const int nch = it.bc, c = it.part;
+  const int Ib = J + c * kBwChunk, Ie = (nch > 1) ? min(T, Ib + kBwChunk) : T;
   const double* X = FR + it.a_off;
   double* sx = sm;
   double* cr = sm + (int64_t)ch * TS;
+  __shared__ int s_last;
   double c0 = 0.0, c1 = 0.0;
-  for (int I0 = J; I0 < T; I0 += ch) {
-    const int I1 = min(T, I0 + ch);
+  for (int I0 = Ib; I0 < Ie; I0 += ch) {
+    const int I1 = min(Ie, I0 + ch);
     gemv_col_g([&](int I) { return X + tri_off(I, J); }, I0, I1, sx,
                [&] {
                  for (int e = threadIdx.x; e < (I1 - I0) * TS; e += blockDim.x) {
@@ -584,9 +597,27 @@ __device__ __forceinline__ void bwc_item(const ItemDesc& it, const double* FR, c
     __syncthreads();  // sx reused by the next chunk
   }
   const double acc = col_finish(c0, c1, cr);
-  if (threadIdx.x < TS) {
-    const int j = J * TS + threadIdx.x;
-    if (j < nV) Pcs[vl[it.sbb_off + j]] = acc;
+  if (nch == 1) {
+    if (threadIdx.x < TS) {
+      const int j = J * TS + threadIdx.x;
+      if (j < nV) Pcs[vl[it.sbb_off + j]] = acc;
+    }
+    __syncthreads();
+    return;
+  }
+  if (threadIdx.x < TS) PB[(it.p_off + c) * TS + threadIdx.x] = acc;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = ((atomicAdd(cnt + it.Ti, 1u) + 1) % (unsigned)nch) == 0;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (threadIdx.x < TS) {
+      double v = 0.0;
+      for (int q = 0; q < nch; ++q) v += ldcg(PB + (it.p_off + q) * TS + threadIdx.x);
+      const int j = J * TS + threadIdx.x;
+      if (j < nV) Pcs[vl[it.sbb_off + j]] = v;
+    }
   }
   __syncthreads();
 }
@@ -607,6 +638,9 @@ __device__ __forceinline__ void fence_scope(int sys) {
   else __threadfence();
 }
 
+// The per-block partials are double-buffered by round parity: a fast block may already write
+// the partial of the next reducing barrier while a slow one still sums the previous round's
+// (P5 and P7 reduce back to back; blocks without items run ahead).
 // Barrier over every block of every rank, with an optional fused fixed-order sum of one
 // value per block. `round` counts barriers (the same sequence in every block of every rank;
 // the counters are monotone across launches).
@@ -633,7 +667,7 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
     // arrival = release-add on the rank counter (orders this block's writes, made visible
     // to thread 0 by the __syncthreads above); departure = acquire poll
     if (threadIdx.x == 0) {
-      if (reduce) A.partials[me][bl] = value;
+      if (reduce) A.partials[me][(round & 1) * A.nbr + bl] = value;
       red_release_gpu(&mine->local_count, 1u);
       hook();
       const unsigned long long t0 = gtimer();
@@ -645,11 +679,11 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
     if (!reduce) return 0.0;
     // fixed-order sum of the block partials, loaded by all threads in one round trip
     double t = 0.0;
-    for (int j = threadIdx.x; j < A.nbr; j += NTHR) t += __ldcg(A.partials[me] + j);
+    for (int j = threadIdx.x; j < A.nbr; j += NTHR) t += __ldcg(A.partials[me] + (round & 1) * A.nbr + j);
     return block_sum(t, bcast);
   }
   if (threadIdx.x == 0) {
-    if (reduce) A.partials[me][bl] = value;
+    if (reduce) A.partials[me][(round & 1) * A.nbr + bl] = value;
     fence_scope(sys);
     const unsigned int old = atomicAdd(&mine->local_count, 1u);
     s_leader = (old + 1 == round * (unsigned int)A.nbr);
@@ -659,7 +693,7 @@ __device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& 
   if (s_leader) {
     if (reduce) {
       double t = 0.0;
-      for (int j = threadIdx.x; j < A.nbr; j += NTHR) t += __ldcg(A.partials[me] + j);
+      for (int j = threadIdx.x; j < A.nbr; j += NTHR) t += __ldcg(A.partials[me] + (round & 1) * A.nbr + j);
       t = block_sum(t, bcast);
       if (threadIdx.x == 0) mine->rank_part[round & 1] = t;
     }
@@ -903,7 +937,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   auto pf_issue = [&](int ph) {
     int n = 0;
     const double* src[2] = {nullptr, nullptr};
-    if (A.npf > 0 && s_icnt[ph] > 0) {
+    if (A.npf > 0 && ph >= 0 && ph < NCACHE && !((c_step_flags >> (4 + ph)) & 1) && s_icnt[ph] > 0) {
       const ItemDesc& w = s_ip[ph][0];
       if (ph == PH_P1) {
         const int Jn = (w.I < w.Tb) ? w.I + 1 : w.Tb;
@@ -946,6 +980,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   // waits for the tiles (npf_cur = tiles of that phase's first item now in tbuf)
   int npf_cur = 0;
   auto bar = [&](int ph_next, bool reduce, double v) -> double {
+    // every thread orders its generic-proxy reads of tbuf before the async-proxy (bulk copy)
+    // overwrite that thread 0 issues after the barrier's __syncthreads (WAR across proxies)
+    if (A.npf > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     const double r = grid_barrier(A, me, bl, round, reduce, v, bcast, [&]() { pf_issue(ph_next); });
     npf_cur = pf_wait();
     return r;
@@ -961,7 +998,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     }
     for (int lv = A.cf_levels - 1; lv >= 0; --lv) {
       const int b = A.cf_bw_off[lv * A.nbr + bl], e = A.cf_bw_off[lv * A.nbr + bl + 1];
-      for (int j = b; j < e; ++j) bwc_item(A.cf_bw[j], A.FR, A.CW, A.cf_vl, A.cf_bl, A.Pcs, smw, A.scratch / TS - 9);
+      for (int j = b; j < e; ++j)
+        bwc_item(A.cf_bw[j], A.FR, A.CW, A.cf_vl, A.cf_bl, A.Pcs, A.cf_pb, A.cf_cnt, smw, A.scratch / TS - 9);
       if (lv > 0) bar(-1, false, 0.0);
     }
   };
@@ -1009,6 +1047,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     // ---- R3 p0 = S_pp^-1 sum N^T Z_p ----
     COARSE(([&](int64_t i, int o) { return ldcg(A.Z[MULTI ? o : 0] + i); }));
     bar(PH_P5, false, 0.0);
+    if (A.dbg_stop == 1) break;
     SSTAMP(3);
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
     FOR_ITEMS(PH_P5, w)

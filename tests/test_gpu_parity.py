@@ -337,3 +337,25 @@ def test_sparse_vs_dense_coarse_cfg4(tcg, monkeypatch):
     a, b = res["sparse"][0], res["dense"][0]
     assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-9
     assert all(abs(x - y) <= 1 for x, y in zip(res["sparse"][1], res["dense"][1]))
+
+
+def test_back_to_back_reductions_no_race(tcg, monkeypatch):
+    """Regression: P5 and P7 end in reducing barriers back to back; blocks without items run
+    ahead and write the next round's partial while slow blocks still sum the previous round
+    (the partials are double-buffered by round parity). Small cases leave most of the 296
+    blocks idle, the sparse coarse and no shared-memory caches widen the window."""
+    monkeypatch.setenv("TCG_COARSE", "sparse")
+    monkeypatch.setenv("TCG_NO_SMEM_CACHE", "1")
+    cc = next(p for p in SMALL if p.name == "corner-conductor")
+    fc = next(p for p in SMALL if p.name == "floating-centre")
+    o_it = {}
+    for pr in (cc, fc):
+        o = Oracle(copy.deepcopy(pr))
+        o.run(pr.n_steps)
+        o_it[pr.name] = (o.iters, o.coefficients(1))
+    for rep in range(3):
+        for pr in (cc, fc):
+            a1, _, it, _, _ = run_gpu(tcg, pr)
+            its, ref = o_it[pr.name]
+            assert list(it) == its, (rep, pr.name, list(it), its)
+            assert np.linalg.norm(a1 - ref) / np.linalg.norm(ref) <= TOL
