@@ -422,7 +422,7 @@ static tcg_status numeric_sparse_coarse(tcg_ctx* h) {
     TRY(run_cholesky(h, g.ldesc[lv], nlv, g.lmaxT[lv], g.lmaxTV[lv], 0, g.FR, g.FDinv, nullptr, R.derr, 1));
     for (int I = 0; I < g.lmaxT[lv]; ++I) {
       dim3 gr(std::max(1, std::min(I + 1, g.lmaxTV[lv])), (unsigned)nlv);
-      k_xinv_row<<<gr, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(g.Dn, I, g.Fscr, g.Dn.dinv_off, g.lplist[lv]);
+      k_xinv_row<<<gr, 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(g.Dn, I, g.Fscr, g.Dn.dinv_off, g.lplist[lv]);
       ++h->nlaunch;
       k_xrow_copy<<<gr, 256, 0, h->stream>>>(g.Dn, I, g.Fscr, g.Dn.dinv_off, g.lplist[lv]);
       ++h->nlaunch;
@@ -501,7 +501,7 @@ static tcg_status do_numeric(tcg_ctx* h) {
     const int64_t* scr_off = h->D.dinv_off;  // scratch rows share the Dinv layout (Tr tiles)
     for (int I = 0; I < R.maxT; ++I) {
       dim3 g(std::min(I + 1, R.maxTr), (unsigned)R.plist.size());
-      k_xinv_row<<<g, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(R.D, I, R.xscr, scr_off, R.d_plist);
+      k_xinv_row<<<g, 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(R.D, I, R.xscr, scr_off, R.d_plist);
       ++h->nlaunch;
       k_xrow_copy<<<g, 256, 0, h->stream>>>(R.D, I, R.xscr, scr_off, R.d_plist);
       ++h->nlaunch;
@@ -535,11 +535,11 @@ static tcg_status do_numeric(tcg_ctx* h) {
       TRY(run_cholesky(h, h->d_cdesc, 1, Tc, Tc, 0, R.C, R.Cinv, nullptr, R.derr, 1));
       for (int I = 0; I < Tc; ++I) {
         dim3 g(I + 1, 1);
-        k_trinv_row<<<g, 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(h->d_cinv, I, R.C, R.CX, R.Cinv);
+        k_trinv_row<<<g, 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(h->d_cinv, I, R.C, R.CX, R.Cinv);
         ++h->nlaunch;
         CKL();
       }
-      k_sinv<<<dim3(Tc, Tc), 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(R.CX, R.Sinv, Tc);
+      k_sinv<<<dim3(Tc, Tc), 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(R.CX, R.Sinv, Tc);
       ++h->nlaunch;
       CKL();
     }
@@ -1111,9 +1111,9 @@ static tcg_status do_setup(tcg_ctx* h) {
     scratch = (scratch + 1) & ~(size_t)1;  // keep the item cache 16-byte aligned
     h->smem_pcg = sizeof(double) * scratch;
     TRY(set_smem(h, (const void*)k_fw, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_xinv_row, 2 * TS * SPAD * sizeof(double)));
-    TRY(set_smem(h, (const void*)k_sinv, 2 * TS * SPAD * sizeof(double)));
-    TRY(set_smem(h, (const void*)k_trinv_row, 2 * TS * SPAD * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_xinv_row, 4 * TS * SPAD * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_sinv, 4 * TS * SPAD * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_trinv_row, 4 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_tables1d, h->smem_tables));
     TRY(set_smem(h, (const void*)k_potrf, 2 * TS * PS * sizeof(double)));
     TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));

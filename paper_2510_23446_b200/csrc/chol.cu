@@ -388,6 +388,96 @@ __device__ __forceinline__ void acc_to_smemT(double* sB, const double (&acc)[4][
     }
 }
 
+// ---- cp.async-staged DMMA tile products (two-stage pipeline over a K loop of tiles) -------
+// Tiles are copied untransposed (row-major, row stride SPAD, 16-byte cp.async chunks); the
+// fragment loads pick the operand orientation: A as [m][k] (AT = false) or as the transpose
+// of a [k][m] tile (AT = true); B as [k][n] (BT = false) or as the transpose of [n][k]
+// (BT = true). SPAD = 68: every orientation reads conflict-free half-warps.
+__device__ __forceinline__ uint32_t cvta_s(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(cvta_s(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void stage_async(const double* __restrict__ g, double* s) {
+  for (int c = threadIdx.x; c < TS * (TS / 2); c += blockDim.x) {
+    const int r = c >> 5, q = c & 31;
+    cp_async16(s + r * SPAD + 2 * q, g + r * TS + 2 * q);
+  }
+}
+template <bool AT, bool BT>
+__device__ __forceinline__ void mma_acc2(const double* sA, const double* sB, double (&acc)[4][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+#pragma unroll 4
+  for (int k0 = 0; k0 < TS; k0 += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = AT ? sA[(k0 + t) * SPAD + wm + i * 8 + g] : sA[(wm + i * 8 + g) * SPAD + k0 + t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = BT ? sB[(wn + j * 8 + g) * SPAD + k0 + t] : sB[(k0 + t) * SPAD + wn + j * 8 + g];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+}
+// acc += sum_{q < nk} op(A_q) op(B_q); sm holds 4 tiles (2 stages x {A, B})
+template <bool AT, bool BT, class AF, class BF>
+__device__ __forceinline__ void mma_stream(AF atile, BF btile, int nk, double* sm, double (&acc)[4][4][2]) {
+  if (nk <= 0) return;
+  constexpr int STG = 2 * TS * SPAD;  // one stage = {A, B}
+  stage_async(atile(0), sm);
+  stage_async(btile(0), sm + TS * SPAD);
+  cp_commit();
+  for (int q = 0; q < nk; ++q) {
+    if (q + 1 < nk) {
+      double* nx = sm + ((q + 1) & 1) * STG;
+      stage_async(atile(q + 1), nx);
+      stage_async(btile(q + 1), nx + TS * SPAD);
+    }
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    const double* cu = sm + (q & 1) * STG;
+    mma_acc2<AT, BT>(cu, cu + TS * SPAD, acc);
+    __syncthreads();
+  }
+}
+// acc (64x64 row-major [m][n]) into shared memory with row stride SPAD
+__device__ __forceinline__ void acc_to_smem(double* s, const double (&acc)[4][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      double* p = s + (wm + i * 8 + g) * SPAD + wn + j * 8 + 2 * t;
+      p[0] = acc[i][j][0];
+      p[1] = acc[i][j][1];
+    }
+}
+// out = scale * A * T with T = acc (NN), A a row-major global tile; sm: >= 2 tiles
+__device__ __forceinline__ void mul_left_store(const double* Ag, const double (&acc)[4][4][2], double scale, double* out,
+                                               double* sm) {
+  double* sA = sm;
+  double* sT = sm + TS * SPAD;
+  acc_to_smem(sT, acc);
+  stage_async(Ag, sA);
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  double acc2[4][4][2];
+  acc_zero(acc2);
+  mma_acc2<false, false>(sA, sT, acc2);
+  acc_store(out, acc2, scale);
+}
+
 struct InvDesc {
   int64_t l_off;     // matrix L (tile-packed lower) base offset in Lbase
   int64_t x_off;     // output X base offset (tile-packed lower, T tiles) in Xbase
@@ -402,9 +492,7 @@ __global__ void __launch_bounds__(128) k_trinv_row(const InvDesc* __restrict__ d
   const InvDesc d = ds[blockIdx.y];
   const int J = blockIdx.x;
   if (I >= d.T || J > I) return;
-  extern __shared__ double smem[];
-  double* sA = smem;
-  double* sB = smem + TS * SPAD;
+  extern __shared__ __align__(16) double smem[];
   const double* Linv = Dbase + d.dinv_off + (int64_t)(d.shift + I) * TSZ;
   double* X = Xbase + d.x_off + tri_off(I, J);
   if (J == I) {
@@ -414,20 +502,9 @@ __global__ void __launch_bounds__(128) k_trinv_row(const InvDesc* __restrict__ d
   }
   double acc[4][4][2];
   acc_zero(acc);
-  for (int K = J; K < I; ++K) {
-    stage_tile(Lbase + d.l_off + tri_off(d.shift + I, d.shift + K), sA);
-    stage_tile_T(Xbase + d.x_off + tri_off(K, J), sB);
-    __syncthreads();
-    mma_acc(sA, sB, acc);
-    __syncthreads();
-  }
-  acc_to_smemT(sB, acc);
-  stage_tile(Linv, sA);
-  __syncthreads();
-  double acc2[4][4][2];
-  acc_zero(acc2);
-  mma_acc(sA, sB, acc2);
-  acc_store(X, acc2, -1.0);
+  mma_stream<false, false>([&](int q) { return Lbase + d.l_off + tri_off(d.shift + I, d.shift + J + q); },
+                           [&](int q) { return Xbase + d.x_off + tri_off(J + q, J); }, I - J, smem, acc);
+  mul_left_store(Linv, acc, -1.0, X, smem);
 }
 
 }  // namespace tcg
@@ -438,18 +515,12 @@ namespace tcg {
 // row-major 64x64 tiles: tile (I,J) = sum_{K >= max(I,J)} X_KI^T X_KJ. grid (Tc, Tc), 128 thr.
 __global__ void __launch_bounds__(128) k_sinv(const double* __restrict__ X, double* Sinv, int Tc) {
   const int I = blockIdx.y, J = blockIdx.x;
-  extern __shared__ double smem[];
-  double* sA = smem;
-  double* sB = smem + TS * SPAD;
+  extern __shared__ __align__(16) double smem[];
   double acc[4][4][2];
   acc_zero(acc);
-  for (int K = max(I, J); K < Tc; ++K) {
-    stage_tile_T(X + tri_off(K, I), sA);  // sA[m][k] = X_KI[k][m]
-    stage_tile_T(X + tri_off(K, J), sB);  // sB[n][k] = X_KJ[k][n]
-    __syncthreads();
-    mma_acc(sA, sB, acc);
-    __syncthreads();
-  }
+  const int K0 = max(I, J);
+  mma_stream<true, false>([&](int q) { return X + tri_off(K0 + q, I); }, [&](int q) { return X + tri_off(K0 + q, J); },
+                          Tc - K0, smem, acc);
   acc_store(Sinv + ((int64_t)I * Tc + J) * TSZ, acc, 1.0);
 }
 
@@ -468,9 +539,7 @@ __global__ void __launch_bounds__(128) k_xinv_row(DevPlan D, int I, double* scra
   const int s = plist[blockIdx.y], J = blockIdx.x;
   const int Tr = D.Ti[s] + D.Tb[s], T = D.T[s];
   if (I >= T || J >= Tr || (I < Tr && J > I)) return;
-  extern __shared__ double smem[];
-  double* sA = smem;
-  double* sB = smem + TS * SPAD;
+  extern __shared__ __align__(16) double smem[];
   const double* A = D.A + D.a_off[s];
   double* out = scratch + scr_off[s] + (int64_t)J * TSZ;
   if (I < Tr && J == I) {
@@ -482,24 +551,14 @@ __global__ void __launch_bounds__(128) k_xinv_row(DevPlan D, int I, double* scra
   const int Kend = (I < Tr) ? I : Tr;
   double acc[4][4][2];
   acc_zero(acc);
-  for (int K = J; K < Kend; ++K) {
-    stage_tile(A + tri_off(I, K), sA);
-    stage_tile_T(A + tri_off(K, J), sB);
-    __syncthreads();
-    mma_acc(sA, sB, acc);
-    __syncthreads();
-  }
+  // rows < I already hold X = L^-1, rows >= I still hold L: sum_{K=J}^{Kend-1} L_IK X_KJ
+  mma_stream<false, false>([&](int q) { return A + tri_off(I, J + q); }, [&](int q) { return A + tri_off(J + q, J); },
+                           Kend - J, smem, acc);
   if (I >= Tr) {
     acc_store(out, acc, 1.0);
     return;
   }
-  acc_to_smemT(sB, acc);
-  stage_tile(D.Dinv + D.dinv_off[s] + (int64_t)I * TSZ, sA);
-  __syncthreads();
-  double acc2[4][4][2];
-  acc_zero(acc2);
-  mma_acc(sA, sB, acc2);
-  acc_store(out, acc2, -1.0);
+  mul_left_store(D.Dinv + D.dinv_off[s] + (int64_t)I * TSZ, acc, -1.0, out, smem);
 }
 
 __global__ void k_xrow_copy(DevPlan D, int I, const double* scratch, const int64_t* scr_off, const int* plist) {
