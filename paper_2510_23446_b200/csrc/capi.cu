@@ -818,7 +818,16 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
           const int rows = (N[x].parent >= 0) ? N[x].T : N[x].TV;  // the root passes nothing up
           for (int I = 0; I < rows; ++I) {
             d.I = I;
-            items.push_back({(I < N[x].TV ? I + 1 : N[x].TV) + 1, d});
+            const int Jn = I < N[x].TV ? I + 1 : N[x].TV;
+            const int nch = std::max(1, (Jn + kFwChunk - 1) / kFwChunk);  // column chunks of this row
+            d.bc = nch;
+            d.sbb_off = npb;  // first partial slot (fw items do not use the V list)
+            d.Ti = ncnt++;
+            npb += nch;
+            for (int c = 0; c < nch; ++c) {
+              d.part = c;
+              items.push_back({std::min(kFwChunk, std::max(1, Jn - c * kFwChunk)) + 1, d});
+            }
           }
         } else {
           for (int J = 0; J < N[x].TV; ++J) {
@@ -2083,6 +2092,15 @@ tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t 
     std::vector<double> a((size_t)h->plan.nc);
     CK(cudaMemcpy(a.data(), h->ndd.Pcs, sizeof(double) * a.size(), cudaMemcpyDeviceToHost));
     tmp = a;
+  } else if (what == 9) {  // sparse coarse tree: per node (height, n_V, n_B, T_V, T_B)
+    for (const auto& n : h->nd.nd) {
+      tmp.push_back(n.height);
+      tmp.push_back((double)n.V.size());
+      tmp.push_back((double)n.B.size());
+      tmp.push_back(n.TV);
+      tmp.push_back(n.TB);
+    }
+    if (tmp.empty()) tmp.push_back(0);
   } else if (what == 7) {
     if (!h->tstamp) return fail(h, TCG_ESTATE, "TCG_PHASE_TIMING not set");
     std::vector<unsigned long long> ts(8 * 64 + 16 + 8 * 4096);

@@ -527,15 +527,22 @@ __device__ __forceinline__ void bw_item(const DevPlan& D, const ItemDesc& it, co
 // ---- sparse coarse forward row I of node x: y_V = L_VV^-1 f_V (rows < TV) or the update
 // f_B - L_BV L_VV^-1 f_V (rows >= TV), f gathered by the node's program: tag bit 55 set = the
 // child's forward vector (CW), else gsrc(aug index, owner rank) of a patch's primal row.
+// Rows are split into column chunks of kFwChunk tiles (ItemDesc: part = chunk, bc = chunks,
+// sbb_off = first partial slot, Ti = counter): each chunk writes its partial row (chunk 0 also
+// the row's own f for B rows), the last arriving chunk adds them in chunk order.
 constexpr int64_t kTag = 1ll << 55, kIdx55 = kTag - 1;
+constexpr int kFwChunk = 4;
 template <class GS>
 __device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, const int64_t* prog, GS gsrc, double* CW,
-                                         double* sm) {
+                                         double* PB, unsigned int* cnt, double* sm) {
   const int I = it.I, TV = it.Tb, T = it.T;
   const int Jn = (I < TV) ? I + 1 : TV;
+  const int nch = it.bc, c = it.part;
+  const int J0 = (nch > 1) ? c * kFwChunk : 0, J1 = (nch > 1) ? min(Jn, J0 + kFwChunk) : Jn;
   const double* X = FR + it.a_off;
   const int64_t* offs = prog + it.p_off;
   const int64_t* ent = offs + (int64_t)T * TS + 1;
+  __shared__ int s_lastf;
   auto fval = [&](int e) {
     double v = 0.0;
     for (int64_t q = offs[e]; q < offs[e + 1]; ++q) {
@@ -544,19 +551,38 @@ __device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, c
     }
     return v;
   };
+  const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
+  const int row = I * TS + row0 + warp_reduce8_row();
+  // the row's own f (B rows, chunk 0): loads issued before the GEMV
+  double frow = 0.0;
+  if (I >= TV && c == 0 && (lane & 3) == 0) frow = fval(row);
   double part[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) part[r] = 0.0;
-  gemv_row_g([&](int J) { return X + tri_off(I, J); }, 0, Jn, sm,
+  gemv_row_g([&](int J) { return X + tri_off(I, J); }, J0, J1, sm,
              [&] {
-               for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x) sm[e] = fval(e);
+               for (int e = threadIdx.x; e < (J1 - J0) * TS; e += blockDim.x) sm[e] = fval(J0 * TS + e);
              },
              part);
   const double sum = warp_reduce8(part);
-  const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
-  if ((lane & 3) == 0) {
-    const int row = I * TS + row0 + warp_reduce8_row();
-    CW[it.vec_off + row] = (I < TV) ? sum : fval(row) - sum;
+  const double mine = (I < TV) ? sum : frow - sum;  // this chunk's share of the output
+  if (nch == 1) {
+    if ((lane & 3) == 0) CW[it.vec_off + row] = mine;
+    __syncthreads();
+    return;
+  }
+  if ((lane & 3) == 0) PB[(it.sbb_off + c) * TS + row0 + warp_reduce8_row()] = mine;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_lastf = ((atomicAdd(cnt + it.Ti, 1u) + 1) % (unsigned)nch) == 0;
+  __syncthreads();
+  if (s_lastf) {
+    __threadfence();
+    if (threadIdx.x < TS) {
+      double v = 0.0;
+      for (int q = 0; q < nch; ++q) v += ldcg(PB + (it.sbb_off + q) * TS + threadIdx.x);
+      CW[it.vec_off + I * TS + threadIdx.x] = v;
+    }
   }
   __syncthreads();
 }
@@ -565,7 +591,7 @@ __device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, c
 // chunk, bc = chunks, p_off = first partial slot, Ti = counter): each chunk writes its partial
 // column sum, the last arriving chunk (monotone counter) adds the partials in chunk order.
 // Rows are streamed through the shared scratch `ch` tiles at a time.
-constexpr int kBwChunk = 8;  // row tiles per backward chunk item
+constexpr int kBwChunk = 4;  // row tiles per backward chunk item
 template <class Dummy = int>
 __device__ __forceinline__ void bwc_item(const ItemDesc& it, const double* FR, const double* CW, const int* vl,
                                          const int* bl, double* Pcs, double* PB, unsigned int* cnt, double* sm,
@@ -993,7 +1019,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   auto coarse_sparse = [&](auto gsrc) {
     for (int lv = 0; lv < A.cf_levels; ++lv) {
       const int b = A.cf_fw_off[lv * A.nbr + bl], e = A.cf_fw_off[lv * A.nbr + bl + 1];
-      for (int j = b; j < e; ++j) fwc_item(A.cf_fw[j], A.FR, A.cf_prog, gsrc, A.CW, smw);
+      for (int j = b; j < e; ++j) fwc_item(A.cf_fw[j], A.FR, A.cf_prog, gsrc, A.CW, A.cf_pb, A.cf_cnt, smw);
       bar(-1, false, 0.0);
     }
     for (int lv = A.cf_levels - 1; lv >= 0; --lv) {
