@@ -14,6 +14,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <map>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -584,7 +585,7 @@ struct ItemLists {
   explicit ItemLists(int nr) : per_rank(nr) {}
 };
 
-static tcg_status deal_items(tcg_ctx* h, ItemLists& L, int ph, int overhead) {
+static tcg_status deal_items(tcg_ctx* h, ItemLists& L, int ph, int overhead, bool group = false) {
   const int nbr = h->nbr;
   auto bycost = [](const std::pair<int, ItemDesc>& x, const std::pair<int, ItemDesc>& y) {
     return x.first != y.first ? x.first > y.first
@@ -610,14 +611,53 @@ static tcg_status deal_items(tcg_ctx* h, ItemLists& L, int ph, int overhead) {
     for (int b = 0; b < nbr; ++b) heap.push_back({0, b});
     auto cmp = [](const std::pair<int64_t, int>& x, const std::pair<int64_t, int>& y) { return x > y; };
     std::make_heap(heap.begin(), heap.end(), cmp);
-    for (auto& e : v) {
-      std::pop_heap(heap.begin(), heap.end(), cmp);
-      auto& top = heap.back();
-      blk[top.second].push_back(e.second);
-      top.first += e.first + overhead;
-      std::push_heap(heap.begin(), heap.end(), cmp);
+    if (group) {
+      // many patches per block: deal whole (patch, part) groups, so each block gathers a
+      // patch's input vector once for all its rows / columns
+      std::vector<std::pair<int64_t, std::vector<ItemDesc>>> grp;
+      std::map<std::pair<int, int>, size_t> keys;
+      for (auto& e : v) {
+        const std::pair<int, int> key{e.second.s, e.second.part};
+        auto kit = keys.find(key);
+        size_t gi;
+        if (kit == keys.end()) {
+          gi = grp.size();
+          keys[key] = gi;
+          grp.push_back({0, {}});
+        } else {
+          gi = kit->second;
+        }
+        grp[gi].first += e.first + 1;
+        grp[gi].second.push_back(e.second);
+      }
+      std::stable_sort(grp.begin(), grp.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+      for (auto& gr : grp) {
+        std::pop_heap(heap.begin(), heap.end(), cmp);
+        auto& top = heap.back();
+        blk[top.second].insert(blk[top.second].end(), gr.second.begin(), gr.second.end());
+        top.first += gr.first + overhead;
+        std::push_heap(heap.begin(), heap.end(), cmp);
+      }
+    } else {
+      for (auto& e : v) {
+        std::pop_heap(heap.begin(), heap.end(), cmp);
+        auto& top = heap.back();
+        blk[top.second].push_back(e.second);
+        top.first += e.first + overhead;
+        std::push_heap(heap.begin(), heap.end(), cmp);
+      }
     }
     for (int b = 0; b < nbr; ++b) {
+      // same-patch items adjacent: the kernel gathers a patch's input once per run
+      std::stable_sort(blk[b].begin(), blk[b].end(), [](const ItemDesc& x, const ItemDesc& y) {
+        return x.s != y.s ? x.s < y.s : (x.part != y.part ? x.part < y.part : x.I < y.I);
+      });
+      // gather codes (bits 4-5 of part): reuse the previous item's input / gather all of it
+      std::vector<int> code(blk[b].size());
+      auto same = [&](size_t a, size_t c) { return blk[b][a].s == blk[b][c].s && blk[b][a].part == blk[b][c].part; };
+      for (size_t j = 0; j < blk[b].size(); ++j)
+        code[j] = (j > 0 && same(j - 1, j)) ? 0 : ((j + 1 < blk[b].size() && same(j + 1, j)) ? 2 : 1);
+      for (size_t j = 0; j < blk[b].size(); ++j) blk[b][j].part |= code[j] << 4;
       all.insert(all.end(), blk[b].begin(), blk[b].end());
       boff.push_back((int)all.size());
     }
@@ -1232,10 +1272,12 @@ static tcg_status do_setup(tcg_ctx* h) {
         pcv.per_rank[crow_owner[I]].push_back({std::min(Tc, (c + 1) * ch) - c * ch, d});
       }
     // fixed per-item overhead (tile units) of the latency-bound item phases
-    TRY(deal_items(h, p1, PH_P1, 2));
+    // whole-patch dealing when there are many patches per block (cfg5: 2048 patches)
+    const bool grp = (int64_t)P >= 2 * (int64_t)NR * h->nbr && !(getenv("TCG_NO_GROUP") && atoi(getenv("TCG_NO_GROUP")));
+    TRY(deal_items(h, p1, PH_P1, 2, grp));
     TRY(deal_items(h, pcv, PH_PC, 2));
-    TRY(deal_items(h, p5, PH_P5, 2));
-    TRY(deal_items(h, sy, PH_SY, 2));
+    TRY(deal_items(h, p5, PH_P5, 2, grp));
+    TRY(deal_items(h, sy, PH_SY, 2));  // (grouping the S_bb rows of a patch measured slower)
     TRY(deal_items(h, fw, PH_FW, 2));
     TRY(deal_items(h, fwa, PH_FWA, 2));
     TRY(deal_items(h, bw, PH_BW, 2));

@@ -42,7 +42,8 @@ struct __align__(16) ItemDesc {
   int Ti, Tb, Tp, T;
   int nb, np;
   int64_t a_off, vec_off, b_off, p_off, sbb_off;
-  int part;  // P5: 0 = X_bb^T tiles (-> Y), 1 = Phi_b tiles (-> Y2)
+  int part;  // P5: bit 0: 0 = X_bb^T tiles (-> Y), 1 = Phi_b tiles (-> Y2); bits 4-5: gather code
+             // (pcg.cu GAT); coarse items: chunk index
   int bc;    // P1/P5/SY: offset of the patch's b-position records in the block's shared cache (-1: none)
 };
 // b-position record (shared-memory cache of a block's patches): multiplier k, its sign on

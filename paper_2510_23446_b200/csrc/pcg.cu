@@ -305,9 +305,10 @@ __device__ __forceinline__ double col_finish(double c0, double c1, double* cr) {
 // ---- P1 / E1: [X_bb; Phi_b^T] v, v = B_s^T p gathered per b position ---------------------
 // vsrc(it, b, pos) returns (B_s^T p)_pos, b = b_off + pos. Output XW: +w (b rows), -g (p rows).
 // Xr = the rank's inverse-factor store.
+// gat = false: sv still holds this patch's v from the previous item of the same patch
 template <class Src>
 __device__ __forceinline__ void p1_item(const ItemDesc& it, const double* Xr, Src vsrc, double* XW, double* sv,
-                                        const double* pft = nullptr, int npf = 0) {
+                                        const double* pft = nullptr, int npf = 0, int gat = 1) {
   const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   const int Jn = (I < Tb) ? I + 1 : Tb;
   const double* X = Xr + it.a_off;
@@ -316,8 +317,10 @@ __device__ __forceinline__ void p1_item(const ItemDesc& it, const double* Xr, Sr
   for (int r = 0; r < 8; ++r) part[r] = 0.0;
   gemv_row_g([&](int J) { return X + tri_off(Ti + I, J); }, Ti, Ti + Jn, sv,
              [&] {
-               for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x)
-                 sv[e] = (e < nb) ? vsrc(it, it.b_off + e, e) : 0.0;
+               if (gat) {
+                 const int ne = (gat == 2) ? Tb * TS : Jn * TS;  // the full vector only if reused
+                 for (int e = threadIdx.x; e < ne; e += blockDim.x) sv[e] = (e < nb) ? vsrc(it, it.b_off + e, e) : 0.0;
+               }
              },
              part, pft, npf);
   const double sum = warp_reduce8(part);
@@ -371,12 +374,16 @@ template <class PcF, class Src>
 __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, const double* W, const int* p_grp,
                                           PcF pc, Src vsrc, double* Y, double* Y2, double* sm, double* red,
                                           unsigned long long* sub = nullptr, const double* pft = nullptr,
-                                          int npf = 0) {
+                                          int npf = 0, int gat = 1) {
   const int J = it.I, Ti = it.Ti, Tb = it.Tb, np = it.np, nb = it.nb;
-  const bool ppart = it.part != 0;
+  const bool ppart = (it.part & 1) != 0;
   const int I0 = ppart ? Tb : J, I1 = ppart ? Tb + it.Tp : Tb;
-  double* sw = sm;                  // (I1 - I0) * 64
-  double* cr = sm + (I1 - I0) * TS; // 8 * 64
+  // the whole b (part 0) or p (part 1) input of the patch, reused by the next item of the
+  // same patch and part (gat = false)
+  const int G0 = ppart ? Tb : 0;
+  double* sfull = sm;                   // (I1 - G0) * 64
+  double* sw = sm + (I0 - G0) * TS;     // rows I0.. of the input
+  double* cr = sm + (I1 - G0) * TS;     // 8 * 64
   const int* grp = p_grp + it.p_off;
   const int64_t vo = it.vec_off + (int64_t)Ti * TS;
   const double* X = Xr + it.a_off;
@@ -387,12 +394,13 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
   double c0 = 0.0, c1 = 0.0;
   gemv_col_g([&](int I) { return X + tri_off(Ti + I, Ti + J); }, I0, I1, sw,
              [&] {
-               for (int e = threadIdx.x; e < (I1 - I0) * TS; e += blockDim.x) {
-                 double val;
-                 if (!ppart) val = ldcg(W + vo + I0 * TS + e);
-                 else val = (e < np) ? -pc(grp[e]) : 0.0;
-                 sw[e] = val;
-               }
+               if (gat)
+                 for (int e = (gat == 2 ? 0 : (I0 - G0) * TS) + threadIdx.x; e < (I1 - G0) * TS; e += blockDim.x) {
+                   double val;
+                   if (!ppart) val = ldcg(W + vo + e);
+                   else val = (e < np) ? -pc(grp[e]) : 0.0;
+                   sfull[e] = val;
+                 }
              },
              c0, c1, pft, npf);
   SUBSTAMP(1);
@@ -412,7 +420,7 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
 // usrc(it, b, pos) returns (B_D^(s)T r)_pos. Returns this item's share of u^T S_bb u.
 template <class Src>
 __device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm,
-                                            double* red, const double* pft = nullptr, int npf = 0) {
+                                            double* red, const double* pft = nullptr, int npf = 0, bool gat = true) {
   const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   double* u = sm;            // Tb*64
   double* cr = u + Tb * TS;  // 9 * 64
@@ -424,7 +432,8 @@ __device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr
   // row part: S_IJ u_J (J <= I), the u gather overlapped with the first tile's loads
   gemv_row_g([&](int J) { return S + tri_off(I, J); }, 0, I + 1, u,
              [&] {
-               for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) u[i] = (i < nb) ? usrc(it, it.b_off + i, i) : 0.0;
+               if (gat)
+                 for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) u[i] = (i < nb) ? usrc(it, it.b_off + i, i) : 0.0;
              },
              part, pft, npf);
   double c0 = 0.0, c1 = 0.0;
@@ -836,6 +845,12 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
       pc_item(D, A, A.Sinv[me], w.s, w.I, prog, GS, A.Ppart[me], smw, PF0(j_w));          \
     }                                                                                     \
   }
+// first item of a run of items of the same patch (and P5 part) in this block's list: only it
+// gathers the patch's input vector, the following items reuse it from shared memory
+// gather code of an item, set by the host in bits 4-5 of ItemDesc::part: 0 = reuse the
+// previous item's gather, 1 = gather this item's rows, 2 = gather the whole patch vector (the
+// next item of this block is of the same patch and part)
+#define GAT(ph, var) (((var).part >> 4) & 3)
 // loop over this block's items of phase ph (shared-memory copy or global list)
 #define FOR_ITEMS(ph, var)                                  \
   for (int j_##var = 0; j_##var < s_icnt[ph]; ++j_##var)    \
@@ -974,7 +989,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         n = min(J1 - J0, A.npf);
         for (int q = 0; q < n; ++q) src[q] = A.Sinv[me] + ((int64_t)w.s * D.Tc + J0 + q) * TSZ;
       } else if (ph == PH_P5) {
-        const int I0 = w.part ? w.Tb : w.I, I1 = w.part ? w.Tb + w.Tp : w.Tb;
+        const int I0 = (w.part & 1) ? w.Tb : w.I, I1 = (w.part & 1) ? w.Tb + w.Tp : w.Tb;
         n = min(I1 - I0, A.npf);
         for (int q = 0; q < n; ++q) src[q] = Xr + w.a_off + tri_off(w.Ti + I0 + q, w.Ti + w.I);
       } else if (ph == PH_SY) {
@@ -1046,13 +1061,13 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                 const BPos q = bget(iw, bb, pos);
                 return q.sign * ldcg(A.pk[0][lown(q.k)] + q.k);
               },
-              A.XW[me], smw, PF0(j_w));
+              A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
     bar(PH_PC, false, 0.0);
     COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
     bar(PH_P5, false, 0.0);
     FOR_ITEMS(PH_P5, w)
       p5_item(w, Xr, A.XW[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
-              red, nullptr, PF0(j_w));
+              red, nullptr, PF0(j_w), GAT(PH_P5, w));
     bar(-1, false, 0.0);
     for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
       A.r[1][me][k] = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
@@ -1078,7 +1093,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
     FOR_ITEMS(PH_P5, w)
       p5_item(w, Xr, A.Z[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
-              red, nullptr, PF0(j_w));
+              red, nullptr, PF0(j_w), GAT(PH_P5, w));
     bar(PH_SY, false, 0.0);
     SSTAMP(4);
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
@@ -1091,7 +1106,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                            const BPos q = bget(iw, bb, pos);
                            return q.aown * (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), q.part));
                          },
-                         smw, red, PF0(j_w));
+                         smw, red, PF0(j_w), GAT(PH_SY, w));
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
         A.r[0][me][k] = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
         A.pk[0][me][k] = 0.0;
@@ -1124,7 +1139,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           return q.aown * ldcg(A.PW[me] + own_idx(iw, pos)) + q.apart * ldcg(A.PW[pown(ppatch(bb))] + q.part) +
                  q.sign * beta * ldcg(pprev[lown(q.k)] + q.k);
         };
-        FOR_ITEMS(PH_P1, w) p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w));
+        FOR_ITEMS(PH_P1, w) p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
         if (kq < k1) pcur[kq] = pv;
         for (int64_t k = kq + blockDim.x; k < k1; k += blockDim.x)
           pcur[k] = lw_p(k) * ldcg(A.PW[pown(lpat_p(k))] + lidx_p(k)) -
@@ -1151,7 +1166,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                          },
                          A.Y[me], A.Y2[me], smw, red,
                          (A.tstamp && step == 0 && it == 2 && gb < 4096) ? A.tstamp + 528 + gb * 8 + 4 : nullptr,
-                         PF0(j_w));
+                         PF0(j_w), GAT(PH_P5, w));
         WSTAMP(2);
         pq = bar(PH_SY, true, loc);
       }
@@ -1176,7 +1191,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           yd = yv(pown(lpat_p(kq)), lidx_p(kq)) - yv(pown(lpat_m(kq)), lidx_m(kq));
         }
         double loc = 0.0;
-        FOR_ITEMS(PH_SY, w) loc += symv_item(w, Sr, A.PW[me], unew, smw, red, PF0(j_w));
+        FOR_ITEMS(PH_SY, w) loc += symv_item(w, Sr, A.PW[me], unew, smw, red, PF0(j_w), GAT(PH_SY, w));
         if (kq < k1) {
           A.lam[me][kq] = lv + alpha * pv;
           rn[kq] = rv - alpha * yd;
@@ -1223,7 +1238,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                 const BPos q = bget(iw, bb, pos);
                 return q.sign * ldcg(A.lam[lown(q.k)] + q.k);
               },
-              A.XW[me], smw, PF0(j_w));
+              A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
     bar(PH_PC, false, 0.0);
     SSTAMP(7);
     // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
