@@ -405,7 +405,8 @@ static tcg_status numeric_sparse_coarse(tcg_ctx* h) {
   for (int c = 0; c < 8; ++c) {
     const int cnt = (int)(h->colour_off[c + 1] - h->colour_off[c]);
     if (cnt == 0) continue;
-    k_nd_scatter<<<cnt, 256, 0, h->stream>>>(R.D, h->d_colour + h->colour_off[c], cnt, g.moff, g.map, g.FR);
+    const int chunks = std::max(1, std::min(32, 2 * 148 / std::max(cnt, 1)));
+    k_nd_scatter<<<dim3(cnt, chunks), 256, 0, h->stream>>>(R.D, h->d_colour + h->colour_off[c], cnt, g.moff, g.map, g.FR);
     ++h->nlaunch;
     CKL();
   }
@@ -522,7 +523,8 @@ static tcg_status do_numeric(tcg_ctx* h) {
       for (int c = 0; c < 8; ++c) {
         int cnt = (int)(h->colour_off[c + 1] - h->colour_off[c]);
         if (cnt == 0) continue;
-        k_coarse_scatter<<<cnt, 256, 0, h->stream>>>(Dc, h->d_colour + h->colour_off[c], cnt);
+        const int chunks = std::max(1, std::min(32, 2 * 148 / std::max(cnt, 1)));  // fill the GPU
+        k_coarse_scatter<<<dim3(cnt, chunks), 256, 0, h->stream>>>(Dc, h->d_colour + h->colour_off[c], cnt);
         ++h->nlaunch;
         CKL();
       }

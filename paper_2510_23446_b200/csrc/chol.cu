@@ -289,14 +289,14 @@ __global__ void k_capture_sbb(const CholDesc* __restrict__ ds, int k, const doub
 // Patches of one parity colour (ix%2, iy%2, iz%2) share no primal group, so each colour is
 // one conflict-free launch; colours run in a fixed order (deterministic sums).
 __global__ void k_coarse_scatter(DevPlan D, const int* __restrict__ patches, int npat) {
-  const int pi = blockIdx.x;
+  const int pi = blockIdx.x;  // grid (npat, chunks): chunk y takes entries y, y + gridDim.y, ...
   if (pi >= npat) return;
   const int s = patches[pi];
   const int Tr = D.Ti[s] + D.Tb[s];
   const int np = D.np[s];
   const int* grp = D.p_grp + D.p_off[s];
   const double* A = D.Ar[D.owner[s]] + D.a_off[s];  // S^s lives on the patch's owner
-  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < np * np; e += gridDim.y * blockDim.x) {
     const int a = e / np, b = e % np;
     const int ga = grp[a], gb = grp[b];
     if (ga < gb) continue;               // each unordered pair once, into the lower triangle

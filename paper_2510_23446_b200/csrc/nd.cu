@@ -39,7 +39,7 @@ __global__ void k_nd_scatter(DevPlan D, const int* __restrict__ patches, int npa
   const int np = D.np[s];
   const double* A = D.Ar[D.owner[s]] + D.a_off[s];
   const int64_t* mp = map + moff[s];
-  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < np * np; e += gridDim.y * blockDim.x) {
     const int64_t t = mp[e];
     if (t < 0) continue;
     int ra = e / np, rb = e % np;
