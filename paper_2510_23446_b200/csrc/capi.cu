@@ -165,6 +165,7 @@ struct tcg_ctx {
     int *vl = nullptr, *bl = nullptr;
     ItemDesc *fw = nullptr, *bw = nullptr;
     int *fw_off = nullptr, *bw_off = nullptr;     // [(level) * (nblocks + 1) + block]
+    int kw = 1;                                    // forward gather sources per position
     double* pb = nullptr;                          // backward chunk partials
     unsigned int* cnt = nullptr;                   // backward chunk counters
   } ndd;
@@ -811,16 +812,15 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
   std::vector<int64_t> prog, poff(nn);
   std::vector<int> vl, bl;
   std::vector<int64_t> vlo(nn), blo(nn);
+  int kw = 1;
+  for (int x = 0; x < nn; ++x)
+    for (const auto& v : src[x]) kw = std::max(kw, (int)v.size());
+  if (kw > kKwMax) return fail(h, TCG_EINVAL, "sparse coarse: more than kKwMax sources per frontal position");
+  g.kw = kw;
   for (int x = 0; x < nn; ++x) {
-    poff[x] = (int64_t)prog.size();
-    const size_t ne = src[x].size();
-    std::vector<int64_t> offs(ne + 1, 0), ent;
-    for (size_t e = 0; e < ne; ++e) {
-      for (int64_t v : src[x][e]) ent.push_back(v);
-      offs[e + 1] = (int64_t)ent.size();
-    }
-    prog.insert(prog.end(), offs.begin(), offs.end());
-    prog.insert(prog.end(), ent.begin(), ent.end());
+    poff[x] = (int64_t)prog.size();  // fixed width: kw slots per position, -1 = none
+    for (const auto& v : src[x])
+      for (int q = 0; q < kw; ++q) prog.push_back(q < (int)v.size() ? v[q] : -1);
     vlo[x] = (int64_t)vl.size();
     vl.insert(vl.end(), N[x].V.begin(), N[x].V.end());
     blo[x] = (int64_t)bl.size();
@@ -1494,7 +1494,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dalloc(h, &h->a_all, (size_t)P * pl.nloc));
   }
   if (!h->h_st) CK(cudaMallocHost(&h->h_st, sizeof(PcgState)));
-  if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) TRY(dzero(h, &h->tstamp, 8 * 64 + 16 + 8 * 4096));
+  if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) TRY(dzero(h, &h->tstamp, 8 * 64 + 16 + 8 * 4096 + 8 * 64));
   if (getenv("TCG_DEBUG_KEEP") && atoi(getenv("TCG_DEBUG_KEEP")) != 0) {
     TRY(dalloc(h, &h->dbgA, h->rd[0].A ? (size_t)oa[h->rd[0].r] : 1));
     TRY(dalloc(h, &h->dbgC, (size_t)tri_tiles(Tc) * TSZ));
@@ -1619,6 +1619,7 @@ static StepArgs step_args(tcg_ctx* h) {
     A.cf_bw_off = g.bw_off;
     A.FR = g.FR;
     A.cf_prog = g.prog;
+    A.cf_kw = g.kw;
     A.cf_vl = g.vl;
     A.cf_bl = g.bl;
     A.CW = g.CW;
@@ -2147,7 +2148,7 @@ tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t 
     if (tmp.empty()) tmp.push_back(0);
   } else if (what == 7) {
     if (!h->tstamp) return fail(h, TCG_ESTATE, "TCG_PHASE_TIMING not set");
-    std::vector<unsigned long long> ts(8 * 64 + 16 + 8 * 4096);
+    std::vector<unsigned long long> ts(8 * 64 + 16 + 8 * 4096 + 8 * 64);
     CK(cudaMemcpy(ts.data(), h->tstamp, ts.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     for (auto v : ts) tmp.push_back((double)v);
   } else {

@@ -104,7 +104,8 @@ struct StepArgs {
   const ItemDesc* cf_bw;
   const int* cf_bw_off;
   const double* FR;              // node inverse factors [L_VV^-1 ; L_BV L_VV^-1] (tile-packed)
-  const int64_t* cf_prog;        // forward gather programs (offs, then tagged sources)
+  const int64_t* cf_prog;        // forward gather sources: cf_kw tagged slots per frontal position
+  int cf_kw;
   const int* cf_vl;              // node V groups
   const int* cf_bl;              // node B groups
   double* CW;                    // node forward vectors (y_V ; f_B - L_BV y_V)
@@ -541,23 +542,26 @@ __device__ __forceinline__ void bw_item(const DevPlan& D, const ItemDesc& it, co
 // the row's own f for B rows), the last arriving chunk adds them in chunk order.
 constexpr int64_t kTag = 1ll << 55, kIdx55 = kTag - 1;
 constexpr int kFwChunk = 4;
+constexpr int kKwMax = 8;  // sources per frontal position (host checks)
 template <class GS>
-__device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, const int64_t* prog, GS gsrc, double* CW,
-                                         double* PB, unsigned int* cnt, double* sm) {
+__device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, const int64_t* prog, int kw, GS gsrc,
+                                         double* CW, double* PB, unsigned int* cnt, double* sm) {
   const int I = it.I, TV = it.Tb, T = it.T;
   const int Jn = (I < TV) ? I + 1 : TV;
   const int nch = it.bc, c = it.part;
   const int J0 = (nch > 1) ? c * kFwChunk : 0, J1 = (nch > 1) ? min(Jn, J0 + kFwChunk) : Jn;
   const double* X = FR + it.a_off;
-  const int64_t* offs = prog + it.p_off;
-  const int64_t* ent = offs + (int64_t)T * TS + 1;
   __shared__ int s_lastf;
+  // fixed-width sources: kw slots per frontal position (-1 = none), all issued at once
   auto fval = [&](int e) {
+    const int64_t* sp = prog + it.p_off + (int64_t)e * kw;
+    int64_t en[kKwMax];
+#pragma unroll
+    for (int q = 0; q < kKwMax; ++q) en[q] = (q < kw) ? sp[q] : -1;
     double v = 0.0;
-    for (int64_t q = offs[e]; q < offs[e + 1]; ++q) {
-      const int64_t en = ent[q];
-      v += (en & kTag) ? ldcg(CW + (en & kIdx55)) : gsrc(en & kIdx55, (int)(en >> 56));
-    }
+#pragma unroll
+    for (int q = 0; q < kKwMax; ++q)
+      if (en[q] >= 0) v += (en[q] & kTag) ? ldcg(CW + (en[q] & kIdx55)) : gsrc(en[q] & kIdx55, (int)(en[q] >> 56));
     return v;
   };
   const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
@@ -1031,18 +1035,29 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
 #define PF0(j) ((j) == 0 ? tbuf : nullptr), ((j) == 0 ? npf_cur : 0)
   // sparse coarse solve S_pp x = sum_s N_s^T (src): forward levels bottom-up, backward levels
   // top-down, a grid barrier between levels (the caller's barrier follows the last one)
+  // (phase-timing builds: block 0 stamps every level of the coarse solves of step 0 into
+  // tstamp[528 + 8 * 4096 + ...], slot = call * 64 + level phase)
+  int cstamp_call = 0;
+  auto cstamp = [&](int k) {
+    if (A.tstamp && me == 0 && bl == 0 && threadIdx.x == 0 && cstamp_call < 8 && k < 64)
+      A.tstamp[528 + 8 * 4096 + cstamp_call * 64 + k] = gtimer();
+  };
   auto coarse_sparse = [&](auto gsrc) {
+    cstamp(0);
     for (int lv = 0; lv < A.cf_levels; ++lv) {
       const int b = A.cf_fw_off[lv * A.nbr + bl], e = A.cf_fw_off[lv * A.nbr + bl + 1];
-      for (int j = b; j < e; ++j) fwc_item(A.cf_fw[j], A.FR, A.cf_prog, gsrc, A.CW, A.cf_pb, A.cf_cnt, smw);
+      for (int j = b; j < e; ++j) fwc_item(A.cf_fw[j], A.FR, A.cf_prog, A.cf_kw, gsrc, A.CW, A.cf_pb, A.cf_cnt, smw);
       bar(-1, false, 0.0);
+      cstamp(1 + lv);
     }
     for (int lv = A.cf_levels - 1; lv >= 0; --lv) {
       const int b = A.cf_bw_off[lv * A.nbr + bl], e = A.cf_bw_off[lv * A.nbr + bl + 1];
       for (int j = b; j < e; ++j)
         bwc_item(A.cf_bw[j], A.FR, A.CW, A.cf_vl, A.cf_bl, A.Pcs, A.cf_pb, A.cf_cnt, smw, A.scratch / TS - 9);
       if (lv > 0) bar(-1, false, 0.0);
+      cstamp(2 * A.cf_levels - lv);
     }
+    ++cstamp_call;
   };
 #define COARSE(GS)                \
   if (A.sparse) {                 \
