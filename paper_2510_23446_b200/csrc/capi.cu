@@ -840,6 +840,17 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
   std::vector<int> fwo(1, 0), bwo(1, 0);
   for (int lv = 0; lv <= nd.H; ++lv) {
     for (int dir = 0; dir < 2; ++dir) {
+      // chunk width of this level: about one chunk per block in total (at least 4 tiles)
+      int64_t lvl_tiles = 0;
+      for (int x : g.lvl[lv]) {
+        if (dir == 0) {
+          const int rows = (N[x].parent >= 0) ? N[x].T : N[x].TV;
+          for (int I = 0; I < rows; ++I) lvl_tiles += I < N[x].TV ? I + 1 : N[x].TV;
+        } else {
+          for (int J = 0; J < N[x].TV; ++J) lvl_tiles += N[x].T - J;
+        }
+      }
+      const int cw = (int)std::max<int64_t>(4, std::min<int64_t>(64, (lvl_tiles + nb2 - 1) / nb2));
       std::vector<std::pair<int, ItemDesc>> items;
       for (int x : g.lvl[lv]) {
         ItemDesc d{};
@@ -861,27 +872,29 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
           for (int I = 0; I < rows; ++I) {
             d.I = I;
             const int Jn = I < N[x].TV ? I + 1 : N[x].TV;
-            const int nch = std::max(1, (Jn + kFwChunk - 1) / kFwChunk);  // column chunks of this row
+            const int nch = std::max(1, (Jn + cw - 1) / cw);  // column chunks of this row
             d.bc = nch;
+            d.Tp = cw;
             d.sbb_off = npb;  // first partial slot (fw items do not use the V list)
             d.Ti = ncnt++;
             npb += nch;
             for (int c = 0; c < nch; ++c) {
               d.part = c;
-              items.push_back({std::min(kFwChunk, std::max(1, Jn - c * kFwChunk)) + 1, d});
+              items.push_back({std::min(cw, std::max(1, Jn - c * cw)) + 1, d});
             }
           }
         } else {
           for (int J = 0; J < N[x].TV; ++J) {
             d.I = J;
-            const int nch = (N[x].T - J + kBwChunk - 1) / kBwChunk;  // row chunks of this column
+            const int nch = (N[x].T - J + cw - 1) / cw;  // row chunks of this column
             d.bc = nch;
+            d.Tp = cw;
             d.p_off = npb;   // first partial slot
             d.Ti = ncnt++;   // arrival counter
             npb += nch;
             for (int c = 0; c < nch; ++c) {
               d.part = c;
-              items.push_back({std::min(kBwChunk, N[x].T - J - c * kBwChunk), d});
+              items.push_back({std::min(cw, N[x].T - J - c * cw), d});
             }
           }
         }

@@ -537,11 +537,10 @@ __device__ __forceinline__ void bw_item(const DevPlan& D, const ItemDesc& it, co
 // ---- sparse coarse forward row I of node x: y_V = L_VV^-1 f_V (rows < TV) or the update
 // f_B - L_BV L_VV^-1 f_V (rows >= TV), f gathered by the node's program: tag bit 55 set = the
 // child's forward vector (CW), else gsrc(aug index, owner rank) of a patch's primal row.
-// Rows are split into column chunks of kFwChunk tiles (ItemDesc: part = chunk, bc = chunks,
+// Rows are split into column chunks of Tp tiles (ItemDesc: part = chunk, bc = chunks,
 // sbb_off = first partial slot, Ti = counter): each chunk writes its partial row (chunk 0 also
 // the row's own f for B rows), the last arriving chunk adds them in chunk order.
 constexpr int64_t kTag = 1ll << 55, kIdx55 = kTag - 1;
-constexpr int kFwChunk = 4;
 constexpr int kKwMax = 8;  // sources per frontal position (host checks)
 template <class GS>
 __device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, const int64_t* prog, int kw, GS gsrc,
@@ -549,7 +548,8 @@ __device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, c
   const int I = it.I, TV = it.Tb, T = it.T;
   const int Jn = (I < TV) ? I + 1 : TV;
   const int nch = it.bc, c = it.part;
-  const int J0 = (nch > 1) ? c * kFwChunk : 0, J1 = (nch > 1) ? min(Jn, J0 + kFwChunk) : Jn;
+  const int cw = it.Tp;  // chunk width (tiles), chosen per level by the host
+  const int J0 = (nch > 1) ? c * cw : 0, J1 = (nch > 1) ? min(Jn, J0 + cw) : Jn;
   const double* X = FR + it.a_off;
   __shared__ int s_lastf;
   // fixed-width sources: kw slots per frontal position (-1 = none), all issued at once
@@ -604,14 +604,14 @@ __device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, c
 // chunk, bc = chunks, p_off = first partial slot, Ti = counter): each chunk writes its partial
 // column sum, the last arriving chunk (monotone counter) adds the partials in chunk order.
 // Rows are streamed through the shared scratch `ch` tiles at a time.
-constexpr int kBwChunk = 4;  // row tiles per backward chunk item
 template <class Dummy = int>
 __device__ __forceinline__ void bwc_item(const ItemDesc& it, const double* FR, const double* CW, const int* vl,
                                          const int* bl, double* Pcs, double* PB, unsigned int* cnt, double* sm,
                                          int ch) {
   const int J = it.I, TV = it.Tb, T = it.T, nV = it.np, nB = it.nb;
   const int nch = it.bc, c = it.part;
-  const int Ib = J + c * kBwChunk, Ie = (nch > 1) ? min(T, Ib + kBwChunk) : T;
+  const int cw = it.Tp;  // chunk height (tiles), chosen per level by the host
+  const int Ib = J + c * cw, Ie = (nch > 1) ? min(T, Ib + cw) : T;
   const double* X = FR + it.a_off;
   double* sx = sm;
   double* cr = sm + (int64_t)ch * TS;
