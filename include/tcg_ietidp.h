@@ -90,7 +90,7 @@ typedef struct tcg_info {
   double bytes_precond; /* algorithmic HBM bytes of one preconditioner apply             */
   double bytes_step_fixed; /* algorithmic HBM bytes of one step outside the PCG iterations
                               (conductor forward/backward solves, p0 / dual rhs / recovery, z0) */
-  double flops_factor;  /* local + coarse factorisation flops                            */
+  double flops_factor;  /* local + coarse factorisation and inverse-factor flops (unpadded) */
   double ms_plan, ms_assembly, ms_factor, ms_coarse, ms_steps; /* device-event timings     */
   double ms_pcg_last_step;
   double prof_ms;       /* summed device time of the profiled kernel's working launches (tcg_set_profile) */

@@ -1986,7 +1986,10 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
     const double nrp = (double)nr;
     // per step outside PCG: conductors read [X_rr; Phi^T] twice (R2 forward, E3 backward)
     if (p.sigma[s] > 0) bs += 2.0 * 8.0 * (nrp * (nrp + 1) / 2 + nrp * q.np);
+    // Cholesky + p-row TRSM + S^s update, then the inverse factors X_rr = L_rr^-1 (nr^3/3) and
+    // X_pr = L_pr X_rr (np nr^2)
     fl += nrp * nrp * nrp / 3.0 + 2.0 * nrp * nrp * q.np + 2.0 * nrp * q.np * q.np;
+    fl += nrp * nrp * nrp / 3.0 + nrp * nrp * q.np;
   }
   const double nc = (double)p.nc;
   if (h->sparse) {
