@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <map>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -209,6 +210,15 @@ struct tcg_ctx {
   double ms_plan = 0, ms_assembly = 0, ms_factor = 0, ms_coarse = 0, ms_steps = 0;
 
   ~tcg_ctx() { release(); }
+  // pinned PcgState buffers are recycled across handles (cudaMallocHost costs ~ms)
+  static std::vector<PcgState*>& pinned_free() {
+    static std::vector<PcgState*> v;
+    return v;
+  }
+  static std::mutex& pinned_mu() {
+    static std::mutex m;
+    return m;
+  }
   void release() {
     if (!allocs.empty() || !pool_allocs.empty() || stream) cudaSetDevice(device);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
@@ -218,7 +228,10 @@ struct tcg_ctx {
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
-    if (h_st) cudaFreeHost(h_st);
+    if (h_st) {
+      std::lock_guard<std::mutex> lk(pinned_mu());
+      pinned_free().push_back(h_st);
+    }
     h_st = nullptr;
     for (auto e : prof_ev) cudaEventDestroy(e);
     prof_ev.clear();
@@ -941,8 +954,29 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
 
 static tcg_status open_peer_tables(tcg_ctx* h, std::vector<std::vector<void*>>& bufs_by_rank);
 
+// host-side timeline of do_setup (TCG_HOST_TIMING=1: one line on stderr per setup)
+struct HostMarks {
+  bool on = getenv("TCG_HOST_TIMING") && atoi(getenv("TCG_HOST_TIMING")) != 0;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  std::string line;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    char b[96];
+    snprintf(b, sizeof b, " %s %.3f", what, std::chrono::duration<double, std::milli>(t - last).count());
+    line += b;
+    last = t;
+  }
+  ~HostMarks() {
+    if (on) fprintf(stderr, "[tcg host ms]%s total %.3f\n", line.c_str(),
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 static tcg_status do_setup(tcg_ctx* h) {
+  HostMarks hm;
   TRY(do_plan(h));
+  hm.mark("plan");
   Plan& pl = h->plan;
   CK(cudaSetDevice(h->device));
   if (const char* pe = getenv("TCG_ALLOC_PAD_KB")) {  // experiment: shift the device-memory layout
@@ -950,9 +984,9 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dalloc(h, &pad, (size_t)atoll(pe) * 1024));
   }
   {
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, h->device));
-    if (prop.major < 10) return fail(h, TCG_ECUDA, std::string("device ") + prop.name + " is not sm_100 class");
+    int major = 0;  // (cudaGetDeviceProperties costs milliseconds per call)
+    CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, h->device));
+    if (major < 10) return fail(h, TCG_ECUDA, "device " + std::to_string(h->device) + " is not sm_100 class");
   }
   if (!h->stream) {
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -974,6 +1008,7 @@ static tcg_status do_setup(tcg_ctx* h) {
   const int NR = h->nranks;
   if (NR > MAXR) return fail(h, TCG_EINVAL, "more than " + std::to_string(MAXR) + " ranks");
 
+  hm.mark("pre-geometry");
   // ---- geometry ----
   Geom& G = h->G;
   for (int d = 0; d < 3; ++d) {
@@ -985,6 +1020,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     for (int d = 0; d < 3; ++d) G.cdim[c][d] = pl.comp_dim(c, d);
   G.nloc = pl.nloc;
 
+  hm.mark("geometry");
   // ---- per-patch layout (offsets relative to the owning rank's allocations) ----
   std::vector<int> Ti(P), Tb(P), Tp(P), T(P), nb(P), np(P), owner(P);
   std::vector<int64_t> a_off(P), dinv_off(P), sbb_off(P), vec_off(P), aug_off(P), b_off(P + 1), p_off(P + 1);
@@ -1053,6 +1089,7 @@ static tcg_status do_setup(tcg_ctx* h) {
   const int Tc = (int)((pl.nc + TS - 1) / TS);
   h->Tc = Tc;
 
+  hm.mark("layout");
   // ---- global uploads (shared by the local ranks) ----
   DevPlan& D = h->D;
   D.npatch = P;
@@ -1127,6 +1164,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     D.loc2aug = dl2a;
   }
 
+  hm.mark("uploads");
   // ---- 1D tables ----
   Tables1D& tb = h->tb;
   int64_t toff = 0;
@@ -1156,6 +1194,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     h->smem_tables = sizeof(double) * (2 * (pl.p + 1) + (size_t)maxel * (pl.p + 1) * (3 * maxn + 2));
   }
 
+  hm.mark("tables");
   // ---- shared memory and persistent grid ----
   int dev_sms = 148;
   CK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
@@ -1207,6 +1246,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     const int flags = fe ? atoi(fe) : (ws < 48e6 ? 1 : 0);
     CK(cudaMemcpyToSymbol(c_step_flags, &flags, sizeof(int)));
   }
+  hm.mark("smem");
   // ---- coarse problem: dense S_pp^-1 (small n_c) or sparse multifrontal ----
   {
     const char* ce = getenv("TCG_COARSE");  // "dense", "sparse", default auto
@@ -1389,6 +1429,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     if (occ < per) return fail(h, TCG_ECUDA, "persistent stepper: shared-memory caches broke occupancy");
   }
 
+  hm.mark("items+caches");
   // ---- per-rank allocations ----
   std::vector<int> local_ranks;
   if (h->world > 1) local_ranks.push_back(h->rank);
@@ -1454,6 +1495,7 @@ static tcg_status do_setup(tcg_ctx* h) {
       R.Sinv = h->rd[0].Sinv;
     }
   }
+  hm.mark("rank-alloc");
   // ---- per-rank pointer tables (peer memory for real ranks) ----
   {
     std::vector<std::vector<void*>> bufs(NR);  // [rank][buffer] in a fixed order
@@ -1506,7 +1548,16 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dalloc(h, &h->glued, pl.nedges));
     TRY(dalloc(h, &h->a_all, (size_t)P * pl.nloc));
   }
-  if (!h->h_st) CK(cudaMallocHost(&h->h_st, sizeof(PcgState)));
+  if (!h->h_st) {
+    {
+      std::lock_guard<std::mutex> lk(tcg_ctx::pinned_mu());
+      if (!tcg_ctx::pinned_free().empty()) {
+        h->h_st = tcg_ctx::pinned_free().back();
+        tcg_ctx::pinned_free().pop_back();
+      }
+    }
+    if (!h->h_st) CK(cudaMallocHost(&h->h_st, sizeof(PcgState)));
+  }
   if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) TRY(dzero(h, &h->tstamp, 8 * 64 + 16 + 8 * 4096 + 8 * 64));
   if (getenv("TCG_DEBUG_KEEP") && atoi(getenv("TCG_DEBUG_KEEP")) != 0) {
     TRY(dalloc(h, &h->dbgA, h->rd[0].A ? (size_t)oa[h->rd[0].r] : 1));
@@ -1514,7 +1565,9 @@ static tcg_status do_setup(tcg_ctx* h) {
   }
   h->bar_round = 0;
   TRY(sync_ranks(h));
+  hm.mark("tables+state");
   TRY(do_numeric(h));
+  hm.mark("numeric");
   h->setup_done = true;
   return TCG_OK;
 }

@@ -1,3 +1,7 @@
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
 // plan.cpp — host planning: glued topology, ranked-Kruskal tree, partition, numbering.
 // See plan.h for the paper passages and DESIGN.md readings followed.
 #include "plan.h"
@@ -96,6 +100,15 @@ int ceil_tiles(int v) { return (v + TILE - 1) / TILE; }
 
 std::string Plan::build() {
   std::ostringstream err;
+  const bool tm = getenv("TCG_HOST_TIMING") && atoi(getenv("TCG_HOST_TIMING")) != 0;
+  auto tlast = std::chrono::steady_clock::now();
+  std::string tline;
+#define PMARK(w)                                                                                       \
+  if (tm) {                                                                                            \
+    const auto t_ = std::chrono::steady_clock::now();                                                  \
+    tline += std::string(" ") + (w) + " " + std::to_string(std::chrono::duration<double, std::milli>(t_ - tlast).count()); \
+    tlast = t_;                                                                                        \
+  }
   if (p < 1) return "degree p must be >= 1";
   for (int d = 0; d < 3; ++d) {
     if (P[d] < 1 || el[d] < 1) return "patch and element counts must be >= 1";
@@ -121,57 +134,101 @@ std::string Plan::build() {
   eoff[3] = off;
   nedges = off;
 
+  PMARK("head");
   // ---- classes and regions (R3) ----
   cls.assign(nedges, CLS_I);
   region.assign(nedges, 0);
   std::vector<uint8_t> nown(nedges, 0);
-  for (int64_t e = 0; e < nedges; ++e) {
-    int c;
-    int64_t x[3];
-    edge_coords(e, c, x[0], x[1], x[2]);
-    bool bnd = false;
-    int nlay = 0;
-    for (int d = 0; d < 3; ++d) {
-      if (d == c) continue;
-      if (x[d] == 0 || x[d] == N[d] - 1) bnd = true;
-      else if (x[d] % (n[d] - 1) == 0) ++nlay;
+  // per direction and vertex coordinate x: patch-layer / boundary flags and the (one or two)
+  // patch indices whose closure contains the layer x (transverse), or the patch holding the
+  // edge [x, x+1] (along the edge); the edge loops below run in edge-id order
+  std::vector<int> t_first[3], t_cnt[3], a_patch[3];
+  std::vector<uint8_t> t_bnd[3], t_lay[3];
+  for (int d = 0; d < 3; ++d) {
+    const int64_t h = n[d] - 1;
+    t_first[d].resize(N[d]);
+    t_cnt[d].resize(N[d]);
+    t_bnd[d].resize(N[d]);
+    t_lay[d].resize(N[d]);
+    a_patch[d].resize(N[d]);
+    for (int64_t x = 0; x < N[d]; ++x) {
+      t_bnd[d][x] = (x == 0 || x == N[d] - 1);
+      t_lay[d][x] = !t_bnd[d][x] && (x % h == 0);
+      if (x % h == 0) {
+        const int q = (int)(x / h);
+        t_first[d][x] = q - 1 >= 0 ? q - 1 : q;
+        t_cnt[d][x] = (q - 1 >= 0) + (q < P[d]);
+      } else {
+        t_first[d][x] = (int)(x / h);
+        t_cnt[d][x] = 1;
+      }
+      a_patch[d][x] = (int)std::min<int64_t>(x / h, P[d] - 1);
     }
-    cls[e] = bnd ? CLS_D : (nlay == 2 ? CLS_WB : (nlay == 1 ? CLS_F : CLS_I));
-    int ow[8], cnt;
-    owners(e, ow, cnt);
-    nown[e] = (uint8_t)cnt;
-    uint8_t r = 0;
-    for (int q = 0; q < cnt; ++q) r |= (sigma[ow[q]] > 0) ? 1 : 2;
-    region[e] = r;
+  }
+  std::vector<uint8_t> sflag(npatch);
+  for (int s = 0; s < npatch; ++s) sflag[s] = (sigma[s] > 0) ? 1 : 2;
+  {
+    int64_t e = 0;
+    for (int c = 0; c < 3; ++c)
+      for (int64_t k = 0; k < edim[c][2]; ++k)
+        for (int64_t j = 0; j < edim[c][1]; ++j)
+          for (int64_t i = 0; i < edim[c][0]; ++i, ++e) {
+            const int64_t x[3] = {i, j, k};
+            bool bnd = false;
+            int nlay = 0;
+            int f[3], cn[3];
+            for (int d = 0; d < 3; ++d) {
+              if (d == c) {
+                f[d] = a_patch[d][x[d]];
+                cn[d] = 1;
+                continue;
+              }
+              bnd = bnd || t_bnd[d][x[d]];
+              nlay += t_lay[d][x[d]];
+              f[d] = t_first[d][x[d]];
+              cn[d] = t_cnt[d][x[d]];
+            }
+            cls[e] = bnd ? CLS_D : (nlay == 2 ? CLS_WB : (nlay == 1 ? CLS_F : CLS_I));
+            nown[e] = (uint8_t)(cn[0] * cn[1] * cn[2]);
+            uint8_t r = 0;
+            for (int z = 0; z < cn[2]; ++z)
+              for (int y = 0; y < cn[1]; ++y)
+                for (int q = 0; q < cn[0]; ++q) r |= sflag[(f[0] + q) + P[0] * ((f[1] + y) + P[1] * (f[2] + z))];
+            region[e] = r;
+          }
   }
 
+  PMARK("classes");
   // ---- ranked Kruskal tree (R2) ----
   // rank 0 D; 1..3 conductor-owned WB/F/I; 4..6 insulator-only WB/F/I
-  std::vector<std::vector<int64_t>> bucket(7);
-  for (int64_t e = 0; e < nedges; ++e) {
-    int rk;
-    if (cls[e] == CLS_D) rk = 0;
-    else rk = ((region[e] & 1) ? 1 : 4) + (cls[e] == CLS_WB ? 0 : (cls[e] == CLS_F ? 1 : 2));
-    bucket[rk].push_back(e);
-  }
+  std::vector<uint8_t> rank_of(nedges);
+  for (int64_t e = 0; e < nedges; ++e)
+    rank_of[e] = cls[e] == CLS_D ? 0 : ((region[e] & 1) ? 1 : 4) + (cls[e] == CLS_WB ? 0 : (cls[e] == CLS_F ? 1 : 2));
   in_tree.assign(nedges, 0);
   DSU dsu(nverts);
   int64_t ntree = 0;
+  const int64_t vstride[3] = {1, N[0], N[0] * N[1]};
   for (int rk = 0; rk < 7; ++rk) {
-    auto& b = bucket[rk];
-    if (tree_order == 1) std::reverse(b.begin(), b.end());
-    for (int64_t e : b) {
-      int c;
-      int64_t x[3];
-      edge_coords(e, c, x[0], x[1], x[2]);
-      int64_t va = x[0] + N[0] * (x[1] + N[1] * x[2]);
-      int64_t y[3] = {x[0], x[1], x[2]};
-      y[c] += 1;
-      int64_t vb = y[0] + N[0] * (y[1] + N[1] * y[2]);
-      if (dsu.unite(va, vb)) {
+    auto visit = [&](int64_t e, int c, int64_t i, int64_t j, int64_t k) {
+      if (rank_of[e] != rk) return;
+      const int64_t va = i + N[0] * (j + N[1] * k);
+      if (dsu.unite(va, va + vstride[c])) {
         in_tree[e] = 1;
         ++ntree;
       }
+    };
+    if (tree_order == 1) {  // descending ids within each rank
+      int64_t e = nedges - 1;
+      for (int c = 2; c >= 0; --c)
+        for (int64_t k = edim[c][2] - 1; k >= 0; --k)
+          for (int64_t j = edim[c][1] - 1; j >= 0; --j)
+            for (int64_t i = edim[c][0] - 1; i >= 0; --i, --e) visit(e, c, i, j, k);
+    } else {
+      int64_t e = 0;
+      for (int c = 0; c < 3; ++c)
+        for (int64_t k = 0; k < edim[c][2]; ++k)
+          for (int64_t j = 0; j < edim[c][1]; ++j)
+            for (int64_t i = 0; i < edim[c][0]; ++i, ++e) visit(e, c, i, j, k);
     }
   }
   if (ntree != nverts - 1) {
@@ -179,6 +236,7 @@ std::string Plan::build() {
     return err.str();
   }
 
+  PMARK("tree");
   // ---- partition (R1) ----
   part.assign(nedges, PART_R);
   n_gauge = n_dir = 0;
@@ -196,6 +254,7 @@ std::string Plan::build() {
     if (part[e] == PART_R && nown[e] > 2) return "an r-DOF with more than two owners";
   }
 
+  PMARK("partition");
   // ---- numbering: multipliers (b-edges ascending) and primal groups ----
   std::vector<int64_t> lam_of(nedges, -1), grp_of(nedges, -1);
   lam_edge.clear();
@@ -216,16 +275,43 @@ std::string Plan::build() {
   lam_plus_pos.assign(m, -1);
   lam_minus_pos.assign(m, -1);
 
+  PMARK("numbering");
   // ---- per patch lists, aug order [i | pad | b | pad | p | pad] ----
   pp.assign(npatch, PatchPlan());
   std::vector<std::vector<std::pair<int, int>>> grp_owners(nc);
   for (int s = 0; s < npatch; ++s) {
     PatchPlan& q = pp[s];
     std::vector<int32_t> li, lb, lp;
-    for (int a = 0; a < nloc; ++a) {
-      int64_t g = local_to_global(s, a);
-      if (part[g] == PART_R) (nown[g] == 1 ? li : lb).push_back(a);
-      else if (part[g] == PART_P) lp.push_back(a);
+    std::vector<int64_t> gb, gpv;  // global ids of the b and p DOFs
+    std::vector<int8_t> sb;        // b DOFs: +1 if this patch is the lower-id owner
+    {
+      const int sx = s % P[0], sy = (s / P[0]) % P[1], sz = s / (P[0] * P[1]);
+      const int64_t o3[3] = {(int64_t)sx * (n[0] - 1), (int64_t)sy * (n[1] - 1), (int64_t)sz * (n[2] - 1)};
+      int a = 0;
+      for (int c = 0; c < 3; ++c)
+        for (int k = 0; k < comp_dim(c, 2); ++k)
+          for (int j = 0; j < comp_dim(c, 1); ++j)
+            for (int i = 0; i < comp_dim(c, 0); ++i, ++a) {
+              const int64_t g = edge_id(c, o3[0] + i, o3[1] + j, o3[2] + k);
+              if (part[g] == PART_R) {
+                if (nown[g] == 1) {
+                  li.push_back(a);
+                } else {
+                  // two owners: they differ along the one transverse direction whose local
+                  // coordinate is on the patch's low (other patch has the lower id) or high face
+                  const int lc[3] = {i, j, k};
+                  int8_t sg = 1;
+                  for (int d = 0; d < 3; ++d)
+                    if (d != c && t_lay[d][o3[d] + lc[d]]) sg = (lc[d] == 0) ? -1 : 1;
+                  lb.push_back(a);
+                  gb.push_back(g);
+                  sb.push_back(sg);
+                }
+              } else if (part[g] == PART_P) {
+                lp.push_back(a);
+                gpv.push_back(g);
+              }
+            }
     }
     q.ni = (int)li.size();
     q.nb = (int)lb.size();
@@ -240,12 +326,10 @@ std::string Plan::build() {
     q.b_lam.resize(q.nb);
     q.b_sign.resize(q.nb);
     for (int t = 0; t < q.nb; ++t) {
-      int64_t g = local_to_global(s, lb[t]);
-      int ow[8], cnt;
-      owners(g, ow, cnt);
+      const int64_t g = gb[t];
       int64_t k = lam_of[g];
       q.b_lam[t] = (int32_t)k;
-      if (s == ow[0]) {
+      if (sb[t] > 0) {
         q.b_sign[t] = 1;
         lam_plus[k] = s;
         lam_plus_pos[k] = t;
@@ -257,13 +341,14 @@ std::string Plan::build() {
     }
     q.p_grp.resize(q.np);
     for (int t = 0; t < q.np; ++t) {
-      int64_t g = local_to_global(s, lp[t]);
+      const int64_t g = gpv[t];
       q.p_grp[t] = (int32_t)grp_of[g];
       grp_owners[grp_of[g]].push_back({s, t});
     }
   }
   for (int64_t k = 0; k < m; ++k)
     if (lam_plus[k] < 0 || lam_minus[k] < 0) return "multiplier without two owners";
+  PMARK("patches");
   coarse_ptr.assign(nc + 1, 0);
   coarse_patch.clear();
   coarse_pos.clear();
@@ -277,12 +362,16 @@ std::string Plan::build() {
     coarse_ptr[g + 1] = (int32_t)coarse_patch.size();
   }
 
+  PMARK("coarse");
   // ---- sharding: contiguous x-slabs of patches ----
   rank_of_patch.assign(npatch, 0);
   for (int s = 0; s < npatch; ++s) {
     int ix = s % P[0];
     rank_of_patch[s] = (int)((int64_t)ix * world / P[0]);
   }
+  PMARK("shard");
+  if (tm) fprintf(stderr, "[tcg plan ms]%s\n", tline.c_str());
+#undef PMARK
   return "";
 }
 

@@ -59,6 +59,29 @@ __global__ void kbar(unsigned* cnt, double* partials, int nb, int iters, int var
         }
       }
       __syncthreads();
+    } else if (variant == 6) {
+      // slot polling: every block writes (value | sentinel-free) into its slot of buffer
+      // round % 3; every thread polls its share of the slots until none holds the sentinel;
+      // the slot of round - 2 is reset after the round completes (triple buffering)
+      const unsigned long long SENT = 0x7ff4deadbeef0000ull;
+      unsigned long long* slots = reinterpret_cast<unsigned long long*>(partials + 4096);
+      const int buf = round % 3;
+      if (threadIdx.x == 0) {
+        const double v = (double)(blockIdx.x + it);
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(slots + buf * 4096 + blockIdx.x), "l"(__double_as_longlong(v)) : "memory");
+      }
+      double t = 0.0;
+      for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+        unsigned long long v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(slots + buf * 4096 + j) : "memory");
+        } while (v == SENT);
+        t += __longlong_as_double(v);
+      }
+      const double tot = block_sum(t, red);
+      if (reduce) acc += tot;
+      if (threadIdx.x == 0) slots[((round + 2) % 3) * 4096 + blockIdx.x] = SENT;  // previous round's slot (read again in round + 2)
+      continue;
     } else if (variant == 4 || variant == 5) {
       // master: block 0 watches 8 arrival counters, then writes every block's release slot
       // (triple-buffered, sentinel = NaN payload) carrying the reduced value
@@ -137,11 +160,11 @@ int main() {
   cudaMalloc(&partials, 8 * 4096 * 4);
   cudaMalloc(&out, 8);
   const char* names[] = {"red.release + ld.acquire poll", "red.release + relaxed poll + fence", "acquire poll + nanosleep",
-                         "two-level (16-block groups)", "master + per-block slots", "master + slots + nanosleep"};
+                         "two-level (16-block groups)", "master + per-block slots", "master + slots + nanosleep", "slot polling (triple buffer)"};
   for (int per = 1; per <= 2; ++per) {
     const int nb = sms * per;
     for (int reduce = 0; reduce < 2; ++reduce)
-      for (int v = 0; v < 6; ++v) {
+      for (int v = 0; v < 7; ++v) {
         int iters = 2000;
         void* args[] = {&cnt, &partials, (void*)&nb, &iters, &v, &reduce, &out};
         cudaMemset(cnt, 0, 4096);

@@ -1,17 +1,19 @@
+"""Wall-clock breakdown of one end-to-end pass through the public API (bench.py's e2e leg):
+create, configure (host arrays), setup (plan, H2D, assembly, factorisation), steps, readback."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, workloads, paper_2510_23446_b200 as tcg
-import torch
-torch.cuda.init()
-pr = workloads.get(sys.argv[1] if len(sys.argv) > 1 else "cfg2")
-for rep in range(4):
-    t = [time.perf_counter()]
-    s = tcg.Solver(); t.append(time.perf_counter())
-    s.configure(pr); t.append(time.perf_counter())
-    s.plan(); t.append(time.perf_counter())
-    s.setup(); t.append(time.perf_counter())
-    s.step(pr.n_steps); t.append(time.perf_counter())
-    a = s.coefficients(1); t.append(time.perf_counter())
-    s.close(); t.append(time.perf_counter())
-    d = np.diff(t) * 1000
-    print("create %.1f configure %.1f plan %.1f setup %.1f step %.1f coef %.1f close %.1f  total %.1f ms" % (*d, sum(d)))
+sys.path.insert(0, os.getcwd())
+import torch, workloads, paper_2510_23446_b200 as tcg
+for name in sys.argv[1:] or ["cfg2"]:
+    prob = workloads.get(name)
+    for rep in range(4):
+        torch.cuda.synchronize()
+        t = [time.perf_counter()]
+        u = tcg.Solver(device=0); t.append(time.perf_counter())
+        u.configure(prob); t.append(time.perf_counter())
+        u.setup(); torch.cuda.synchronize(); t.append(time.perf_counter())
+        u.step(prob.n_steps); t.append(time.perf_counter())
+        a = u.coefficients(1); t.append(time.perf_counter())
+        inf = u.info(); u.close(); t.append(time.perf_counter())
+        d = [1e3 * (b - a) for a, b in zip(t[:-1], t[1:])]
+        print(name, rep, "ms: create %.2f configure %.2f setup %.2f (plan %.2f assembly %.2f factor %.2f coarse %.2f) steps %.2f readback %.2f close %.2f total %.2f"
+              % (d[0], d[1], d[2], inf["ms_plan"], inf["ms_assembly"], inf["ms_factor"], inf["ms_coarse"], d[3], d[4], d[5], sum(d)))
