@@ -301,6 +301,31 @@ def main():
                        "4 grid barriers per apply), algorithmic bytes B_F (DESIGN.md §5) / event-timed duration"
                        + ("; working set L2-resident: effective bandwidth" if bf < 60e6 else "")}
 
+    # ---- warm start: same passes with lambda0 = gamma lambda^(l) ----
+    # (an option, not the headline: the paper's PCG starts from lambda0 = 0)
+    warm = None
+    if world == 1 and not args.no_roofline:
+        it_cold = s.history()[0]
+        s.set_warm_start(1)
+        one_pass()
+        ms_w, kw = 0.0, max(1, min(3, args.steps))
+        for _ in range(kw):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            one_pass()
+            e1.record(stream)
+            e1.synchronize()
+            ms_w += e0.elapsed_time(e1)
+        it_w = s.history()[0]
+        s.set_warm_start(0)
+        warm = {"value": n_t * kw / (ms_w / 1000.0), "unit": "steps/s", "passes": kw,
+                "pcg_iters_per_step": float(np.mean(it_w)), "cold_pcg_iters_per_step": float(np.mean(it_cold)),
+                "note": "tcg_set_warm_start(1): PCG from gamma*lambda of the previous step (Galerkin scale), "
+                        "one extra F-apply + preconditioner apply per step; same timing protocol as value"}
+
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if args.e2e_steps > 0:
@@ -346,7 +371,7 @@ def main():
             "pcg_iters_per_s": value * iters_per_step,
             "pcg_iters_per_step": iters_per_step,
             "setup_ms": inf["ms_assembly"] + inf["ms_factor"] + inf["ms_coarse"],
-            "roofline": roof, "fapply": fap, "kernel_shares": shares, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "fapply": fap, "warm_start": warm, "kernel_shares": shares, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

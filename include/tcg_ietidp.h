@@ -143,6 +143,18 @@ tcg_status tcg_set_time(tcg_handle h, double T, int n_steps);
  * 1: descending (gauge-invariance test). Defaults 1e-10, 5000, RHO, 0. */
 tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, int tree_order);
 
+/* Warm start (the paper's outlook P:L550 on cheaper PCG): on = 1 starts
+ * the PCG of every step after the first from the Galerkin-scaled previous multipliers,
+ * lambda0 = gamma lambda^(l), gamma = lambda^T d / lambda^T F lambda (the multiple of
+ * lambda^(l) closest to the solution in the F-norm, so never a worse start than 0; gamma
+ * = 0 if the denominator is not positive), r0 = d - gamma F lambda^(l) (one extra F-apply
+ * and preconditioner apply per step, not counted as iterations). The stopping reference stays sqrt(d^T M^-1 d) (the
+ * cold-start r0^T z0), so warm and cold runs stop at the same absolute residual; a step
+ * whose warm residual already meets it takes 0 iterations. d = 0 gives lambda = 0. on = 0
+ * (default) is the paper's lambda0 = 0. May be called at any time; it applies from the
+ * next tcg_step. EINVAL unless on is 0 or 1. */
+tcg_status tcg_set_warm_start(tcg_handle h, int on);
+
 /* Host-only planning (no CUDA): topology, ranked-Kruskal tree, e/p/r partition,
  * multiplier and primal numbering, patch->rank sharding. Idempotent. */
 tcg_status tcg_plan(tcg_handle h);

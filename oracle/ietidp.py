@@ -203,16 +203,33 @@ class Oracle:
         pr = self.prob
         return assembly.source_time_factor(pr.source, t, pr.nu[s], pr.sigma[s])
 
-    def pcg(self, d):
-        """Classical Hestenes-Stiefel PCG from lam0 = 0 (R6)."""
+    def pcg(self, d, lam0=None):
+        """Classical Hestenes-Stiefel PCG from lam0 = 0 (R6), or, warm start
+        (R20), from the Galerkin-scaled previous multipliers
+        gamma lam0, gamma = lam0^T d / lam0^T F lam0 (the F-norm-best multiple; 0 if the
+        denominator is not positive), with r0 = d - gamma F lam0; the stopping reference
+        is sqrt(d^T M^-1 d) in both cases (the cold r0^T z0)."""
         pr = self.prob
-        lam = np.zeros_like(d)
-        r = d.copy()
-        z = self.precond(r)
-        rho = rho0 = float(r @ z)
-        hist = [1.0]
+        z = self.precond(d)
+        rho = rho0 = float(d @ z)
         if rho0 == 0.0 or len(d) == 0:
-            return lam, 0, hist
+            return np.zeros_like(d), 0, [1.0]
+        if lam0 is None:
+            lam = np.zeros_like(d)
+            r = d.copy()
+            hist = [1.0]
+        else:
+            q = self.F(lam0)
+            den = float(lam0 @ q)
+            gamma = float(lam0 @ d) / den if den > 0.0 else 0.0
+            lam = gamma * lam0
+            r = d - gamma * q
+            z = self.precond(r)
+            rho = float(r @ z)
+            rel = np.sqrt(max(rho, 0.0) / rho0)
+            hist = [rel]
+            if rel <= pr.rtol:
+                return lam, 0, hist
         pk = z.copy()
         k = 0
         while True:
@@ -250,7 +267,8 @@ class Oracle:
         fpg = self.NT(fp)
         p0 = _solve(self.Spp_cf, fpg - self.NT(h))
         d = self.Bj([x1[s] - self.Phi[s] @ p0[pt.p_grp[s]] for s in range(P)])
-        lam, k, hist = self.pcg(d)
+        warm = getattr(self.prob, "warm_start", 0) and self.ell > 0
+        lam, k, hist = self.pcg(d, self.lam if warm else None)
         v = self.Bt(lam)
         pc = _solve(self.Spp_cf, fpg - self.NT([h[s] - self.Phi[s].T @ v[s] for s in range(P)]))
         for s in range(P):

@@ -20,7 +20,7 @@ STATUS_NAMES = {0: "TCG_OK", -1: "TCG_EINVAL", -2: "TCG_ESTATE", -3: "TCG_ENOTSP
                 -5: "TCG_ECUDA", -6: "TCG_ENCCL", -7: "TCG_ENOMEM"}
 PLAN_EDGE_CLASS, PLAN_EDGE_REGION, PLAN_TREE, PLAN_PART, PLAN_PATCH_COUNTS, PLAN_LAMBDA, PLAN_PRIMAL, PLAN_RANK_OF_PATCH = range(8)
 
-EXPORTS = ["tcg_create", "tcg_set_patches", "tcg_set_materials", "tcg_set_source", "tcg_set_time", "tcg_set_solver",
+EXPORTS = ["tcg_create", "tcg_set_patches", "tcg_set_materials", "tcg_set_source", "tcg_set_time", "tcg_set_solver", "tcg_set_warm_start",
            "tcg_plan", "tcg_get_plan", "tcg_setup", "tcg_refactor", "tcg_step", "tcg_get_coefficients", "tcg_get_history",
            "tcg_get_info", "tcg_fapply", "tcg_bench_fapply", "tcg_set_profile", "tcg_set_virtual_ranks", "tcg_nccl_unique_id", "tcg_last_error",
            "tcg_destroy"]
@@ -65,6 +65,7 @@ def lib():
     L.tcg_set_source.argtypes = [vp, C.c_int]
     L.tcg_set_time.argtypes = [vp, C.c_double, C.c_int]
     L.tcg_set_solver.argtypes = [vp, C.c_double, C.c_int, C.c_int, C.c_int]
+    L.tcg_set_warm_start.argtypes = [vp, C.c_int]
     L.tcg_plan.argtypes = [vp]
     L.tcg_get_plan.argtypes = [vp, C.c_int, i64p, C.c_size_t]
     L.tcg_setup.argtypes = [vp]
@@ -135,6 +136,11 @@ class Solver:
     def set_solver(self, rtol=1e-10, max_iter=5000, scaling=1, tree_order=0):
         self._ck(self.L.tcg_set_solver(self.h, float(rtol), int(max_iter), int(scaling), int(tree_order)))
 
+    def set_warm_start(self, on=True):
+        """PCG of every step after the first starts from the previous step's lambda (f2)."""
+        self._ck(self.L.tcg_set_warm_start(self.h, int(bool(on))))
+        return self
+
     def configure(self, prob):
         """Set everything from a problem description with the fields of workloads.Problem."""
         self.set_patches(prob.npatch, prob.lo, prob.hi, prob.p, prob.elems)
@@ -142,6 +148,7 @@ class Solver:
         self.set_source(prob.source)
         self.set_time(prob.T, prob.n_steps)
         self.set_solver(prob.rtol, prob.max_iter, prob.scaling, prob.tree_order)
+        self.set_warm_start(getattr(prob, "warm_start", 0))
         return self
 
     def plan(self):

@@ -180,6 +180,7 @@ struct tcg_ctx {
   int cache_bpos = 0;
   int cache_items = 0, cache_lam = 0, cache_pcprog = 0;
   int npf = 0;  // prefetched tiles per phase (stepper)
+  int warm = 0;  // PCG from the previous step's lambda (tcg_set_warm_start)
   int64_t* d_pcprog = nullptr;
   size_t smem_steps = 0;  // dynamic shared memory of k_steps: item scratch + caches
   int coarse_ch = 1, coarse_maxch = 1;
@@ -1673,6 +1674,7 @@ static StepArgs step_args(tcg_ctx* h) {
   A.cache_lam = h->cache_lam;
   A.scratch = (int)(h->smem_pcg / sizeof(double));
   A.npf = h->npf;
+  A.warm = h->warm;
   A.mode = 0;
   A.dbg_stop = getenv("TCG_DEBUG_STOP") ? atoi(getenv("TCG_DEBUG_STOP")) : 0;
   A.sparse = h->sparse;
@@ -1872,6 +1874,13 @@ tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, 
   h->max_iter = max_iter;
   h->scaling = scaling;
   h->tree_order = tree_order;
+  return TCG_OK;
+}
+
+tcg_status tcg_set_warm_start(tcg_handle h, int on) {
+  if (!h) return TCG_EINVAL;
+  if (on != 0 && on != 1) return fail(h, TCG_EINVAL, "warm start is 0 or 1");
+  h->warm = on;
   return TCG_OK;
 }
 

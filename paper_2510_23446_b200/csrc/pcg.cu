@@ -96,6 +96,7 @@ struct StepArgs {
   int npf;          // tiles of the next phase's first item bulk-copied to shared memory during a barrier
   int mode;         // 0: nsteps implicit-Euler steps; 1: nsteps applications q = F p (p = pk[0], q -> r[1])
   int dbg_stop;     // debug: 1 = return after the first step's R3 coarse solve
+  int warm;         // 1: PCG starts from gamma * the previous step's lambda, step >= 1
   // sparse coarse: per level forward rows / backward columns of the node factors
   int sparse;
   int cf_levels;                 // tree height + 1
@@ -1112,6 +1113,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     bar(PH_SY, false, 0.0);
     SSTAMP(4);
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
+    // (warm start: lambda keeps the previous step's value; rho0 = d^T M^-1 d stays the
+    // reference of the stopping rule, so warm and cold runs share one absolute target)
+    const bool warm = A.warm && (A.step0 + step > 0);
     double rho0;
     {
       double loc = 0.0;
@@ -1125,18 +1129,71 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
         A.r[0][me][k] = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
         A.pk[0][me][k] = 0.0;
-        A.lam[me][k] = 0.0;
+        if (!warm) A.lam[me][k] = 0.0;
       }
       rho0 = bar(PH_P1, true, loc);
     }
     SSTAMP(5);
-    if (me == 0 && bl == 0 && threadIdx.x == 0) A.hist[0][hoff] = 1.0;
     int status = 0;  // 0 running, 1 converged, 2 failed
     double rz = rho0;
     if (!(rho0 >= 0.0)) status = 2;
     else if (!(rho0 > 0.0) || m == 0) status = 1;  // d = 0: lambda = 0 after 0 iterations
     double rho = rho0, beta = 0.0;
     int rp = 0, pp = 0;
+    double rel0 = 1.0;
+    if (warm && status == 1) {  // d = 0: the solution is lambda = 0, not the previous one
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) A.lam[me][k] = 0.0;
+      bar(PH_P1, false, 0.0);
+    }
+    if (warm && status == 0) {
+      // ---- W1-W3: q = F lambda_prev (the F-apply of the loop with p := lambda_prev), with
+      // the Galerkin scale gamma = lambda^T d / lambda^T F lambda (two reductions) ----
+      double ld = 0.0;
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) ld += ldcg(A.lam[me] + k) * ldcg(A.r[0][me] + k);
+      ld = block_sum(ld, red);
+      FOR_ITEMS(PH_P1, w)
+        p1_item(w, Xr,
+                [&](const ItemDesc& iw, int64_t bb, int pos) {
+                  const BPos q = bget(iw, bb, pos);
+                  return q.sign * ldcg(A.lam[lown(q.k)] + q.k);
+                },
+                A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
+      const double gnum = bar(PH_PC, true, ld);
+      COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
+      bar(PH_P5, false, 0.0);
+      double lq = 0.0;
+      FOR_ITEMS(PH_P5, w)
+        lq += p5_item(w, Xr, A.XW[me], D.p_grp, pcf,
+                      [&](const ItemDesc& iw, int64_t bb, int pos) {
+                        const BPos q = bget(iw, bb, pos);
+                        return q.sign * ldcg(A.lam[lown(q.k)] + q.k);
+                      },
+                      A.Y[me], A.Y2[me], smw, red, nullptr, PF0(j_w), GAT(PH_P5, w));
+      const double gden = bar(PH_SY, true, lq);
+      const double gamma = (gden > 0.0) ? gnum / gden : 0.0;  // uniform
+      // ---- W4: lambda0 = gamma lambda_prev, r0 = d - gamma F lambda_prev (the P7 formulas
+      // with alpha = gamma), z0 = M^-1 r0 ----
+      double loc = 0.0;
+      FOR_ITEMS(PH_SY, w)
+        loc += symv_item(w, Sr, A.PW[me],
+                         [&](const ItemDesc& iw, int64_t bb, int pos) {
+                           const BPos q = bget(iw, bb, pos);
+                           return q.aown * (q.sign * ldcg(A.r[0][lown(q.k)] + q.k) -
+                                            gamma * (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), q.part)));
+                         },
+                         smw, red, PF0(j_w), GAT(PH_SY, w));
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        A.r[1][me][k] = ldcg(A.r[0][me] + k) - gamma * (yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k)));
+        A.lam[me][k] *= gamma;
+      }
+      rz = bar(PH_P1, true, loc);
+      rho = rz;
+      rp = 1;
+      rel0 = sqrt(fmax(rz, 0.0) / rho0);
+      if (!(rz == rz)) status = 2;
+      else if (rel0 <= A.rtol) status = 1;
+    }
+    if (me == 0 && bl == 0 && threadIdx.x == 0) A.hist[0][hoff] = rel0;
     while (status == 0) {
       TSTAMP(0);
       double* const* pprev = A.pk[pp];

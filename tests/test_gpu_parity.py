@@ -359,3 +359,38 @@ def test_back_to_back_reductions_no_race(tcg, monkeypatch):
             its, ref = o_it[pr.name]
             assert list(it) == its, (rep, pr.name, list(it), its)
             assert np.linalg.norm(a1 - ref) / np.linalg.norm(ref) <= TOL
+
+
+@pytest.mark.parametrize("name,steps,vranks", [("cfg1", 10, 1), ("contrast", 6, 1), ("cfg2", 8, 1), ("cfg2", 4, 3)])
+def test_warm_start_matches_oracle(tcg, name, steps, vranks):
+    """Warm start (R20): the GPU's Galerkin-scaled lambda0 and
+    r0 = d - gamma F lambda_prev against the oracle's warm PCG, every step; on cfg2 it saves
+    PCG iterations against the cold start (oracle and GPU agree on both)."""
+    pr = next(p for p in SMALL if p.name == name) if name == "contrast" else workloads.get(name)
+    pr = copy.deepcopy(pr)
+    pr.warm_start = 1
+    steps = min(steps, pr.n_steps)
+    o = Oracle(copy.deepcopy(pr))
+    o.run(steps)
+    s = tcg.Solver().configure(pr)
+    if vranks > 1:
+        s.set_virtual_ranks(vranks)
+    s.setup()
+    s.step(steps)
+    a1 = s.coefficients(1)
+    it, _, hist = s.history()
+    s.close()
+    ref = o.coefficients(1)
+    tol = 1e-6 if name == "contrast" else TOL
+    err = np.linalg.norm(a1 - ref) / np.linalg.norm(ref)
+    assert err <= tol, (err, list(it), o.iters)
+    assert np.all(np.abs(np.array(it) - np.array(o.iters)) <= 1), (list(it), o.iters)
+    if name == "cfg2":
+        cold = copy.deepcopy(pr)
+        cold.warm_start = 0
+        c = tcg.Solver().configure(cold)
+        c.setup()
+        c.step(steps)
+        itc = c.history()[0]
+        c.close()
+        assert sum(it[1:]) < sum(itc[1:]), (list(it), list(itc))
