@@ -143,17 +143,19 @@ tcg_status tcg_set_time(tcg_handle h, double T, int n_steps);
  * 1: descending (gauge-invariance test). Defaults 1e-10, 5000, RHO, 0. */
 tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, int tree_order);
 
-/* Warm start (the paper's outlook P:L550 on cheaper PCG): on = 1 starts
- * the PCG of every step after the first from the Galerkin-scaled previous multipliers,
- * lambda0 = gamma lambda^(l), gamma = lambda^T d / lambda^T F lambda (the multiple of
- * lambda^(l) closest to the solution in the F-norm, so never a worse start than 0; gamma
- * = 0 if the denominator is not positive), r0 = d - gamma F lambda^(l) (one extra F-apply
- * and preconditioner apply per step, not counted as iterations). The stopping reference stays sqrt(d^T M^-1 d) (the
- * cold-start r0^T z0), so warm and cold runs stop at the same absolute residual; a step
- * whose warm residual already meets it takes 0 iterations. d = 0 gives lambda = 0. on = 0
- * (default) is the paper's lambda0 = 0. May be called at any time; it applies from the
- * next tcg_step. EINVAL unless on is 0 or 1. */
-tcg_status tcg_set_warm_start(tcg_handle h, int on);
+/* Warm start (the paper's outlook P:L550 on cheaper PCG; R20).
+ * k = 0 (default): the paper's lambda0 = 0. k in 1..4: from step 1 on the PCG starts from the
+ * Galerkin projection of the step's solution on the span of the previous k solutions W_j:
+ * lambda0 = sum_j c_j W_j, G c = W^T d, G_ij = (W_i^T FW_j + W_j^T FW_i)/2 with FW_j = d_j - r_j
+ * (each step's right-hand side minus its final PCG residual, i.e. F W_j to the tolerance: no
+ * extra F-apply), solved by Cholesky in step order skipping columns with pivot <= 1e-12
+ * max G_ii; r0 = d - sum_j c_j FW_j, then one preconditioner apply (not counted as an
+ * iteration). The stopping reference stays sqrt(d^T M^-1 d) (the cold r0^T z0), so warm and
+ * cold runs stop at one absolute residual; a step whose start already meets it takes 0
+ * iterations; d = 0 gives lambda = 0. tcg_refactor restarts the history (step 0 is cold).
+ * Takes effect from the next tcg_step; device memory (2k+1 lambda-length vectors per rank)
+ * is allocated then. EINVAL unless 0 <= k <= 4. */
+tcg_status tcg_set_warm_start(tcg_handle h, int k);
 
 /* Host-only planning (no CUDA): topology, ranked-Kruskal tree, e/p/r partition,
  * multiplier and primal numbering, patch->rank sharding. Idempotent. */

@@ -49,6 +49,33 @@ def _solve(cf, b):
     return sla.cho_solve(cf, b, check_finite=False)
 
 
+def chol_skip_solve(G, b, tol=1e-12):
+    """Solve G c = b for a small symmetric G by Cholesky in index order, skipping (c_j = 0)
+    every column whose pivot is <= tol * max_i G_ii (numerically dependent directions).
+    Used by the warm start (R20), written out so the GPU's copy can follow it."""
+    k = len(b)
+    L = np.zeros((k, k))
+    act = [False] * k
+    gmax = max((G[i, i] for i in range(k)), default=0.0)
+    for j in range(k):
+        s = G[j, j] - sum(L[j, q] * L[j, q] for q in range(j) if act[q])
+        if not (s > tol * gmax):
+            continue
+        act[j] = True
+        L[j, j] = np.sqrt(s)
+        for i in range(j + 1, k):
+            L[i, j] = (G[i, j] - sum(L[i, q] * L[j, q] for q in range(j) if act[q])) / L[j, j]
+    y = np.zeros(k)
+    for j in range(k):
+        if act[j]:
+            y[j] = (b[j] - sum(L[j, q] * y[q] for q in range(j) if act[q])) / L[j, j]
+    c = np.zeros(k)
+    for j in reversed(range(k)):
+        if act[j]:
+            c[j] = (y[j] - sum(L[q, j] * c[q] for q in range(j + 1, k) if act[q])) / L[j, j]
+    return c
+
+
 class Oracle:
     def __init__(self, prob, assemble=True):
         self.prob = prob
@@ -64,6 +91,7 @@ class Oracle:
         self.ell = 0
         self.iters = []
         self.hist = []
+        self.warm_W, self.warm_FW = [], []  # previous solutions and F times them (R20)
 
     # ---- setup -------------------------------------------------------------------
     def patch_box(self, s):
@@ -203,33 +231,39 @@ class Oracle:
         pr = self.prob
         return assembly.source_time_factor(pr.source, t, pr.nu[s], pr.sigma[s])
 
-    def pcg(self, d, lam0=None):
+    def pcg(self, d, W=None, FW=None):
         """Classical Hestenes-Stiefel PCG from lam0 = 0 (R6), or, warm start
-        (R20), from the Galerkin-scaled previous multipliers
-        gamma lam0, gamma = lam0^T d / lam0^T F lam0 (the F-norm-best multiple; 0 if the
-        denominator is not positive), with r0 = d - gamma F lam0; the stopping reference
-        is sqrt(d^T M^-1 d) in both cases (the cold r0^T z0)."""
+        (R20), from the Galerkin projection of the solution on
+        the span of previous solutions W_j: lam0 = sum_j c_j W_j with
+        G c = W^T d, G_ij = (W_i^T FW_j + W_j^T FW_i)/2, FW_j = F W_j taken as d_j - r_j
+        (the step's right-hand side minus its final recurrence residual), solved by
+        chol_skip_solve; r0 = d - sum_j c_j FW_j. The stopping reference is
+        sqrt(d^T M^-1 d) in both cases (the cold r0^T z0). Returns (lam, iterations,
+        relres history, final recurrence residual)."""
         pr = self.prob
         z = self.precond(d)
         rho = rho0 = float(d @ z)
         if rho0 == 0.0 or len(d) == 0:
-            return np.zeros_like(d), 0, [1.0]
-        if lam0 is None:
+            return np.zeros_like(d), 0, [1.0], np.zeros_like(d)
+        if not W:
             lam = np.zeros_like(d)
             r = d.copy()
             hist = [1.0]
         else:
-            q = self.F(lam0)
-            den = float(lam0 @ q)
-            gamma = float(lam0 @ d) / den if den > 0.0 else 0.0
-            lam = gamma * lam0
-            r = d - gamma * q
+            k = len(W)
+            G = np.zeros((k, k))
+            for i in range(k):
+                for j in range(k):
+                    G[i, j] = 0.5 * (float(W[i] @ FW[j]) + float(W[j] @ FW[i]))
+            c = chol_skip_solve(G, np.array([float(w @ d) for w in W]))
+            lam = sum(c[j] * W[j] for j in range(k))
+            r = d - sum(c[j] * FW[j] for j in range(k))
             z = self.precond(r)
             rho = float(r @ z)
             rel = np.sqrt(max(rho, 0.0) / rho0)
             hist = [rel]
             if rel <= pr.rtol:
-                return lam, 0, hist
+                return lam, 0, hist, r
         pk = z.copy()
         k = 0
         while True:
@@ -243,7 +277,7 @@ class Oracle:
             rel = np.sqrt(max(rhon, 0.0) / rho0)
             hist.append(rel)
             if rel <= pr.rtol:
-                return lam, k, hist
+                return lam, k, hist, r
             if k >= pr.max_iter:
                 raise NoConvergence(f"step {self.ell}: {k} iterations, relres {rel}")
             beta = rhon / rho
@@ -267,8 +301,13 @@ class Oracle:
         fpg = self.NT(fp)
         p0 = _solve(self.Spp_cf, fpg - self.NT(h))
         d = self.Bj([x1[s] - self.Phi[s] @ p0[pt.p_grp[s]] for s in range(P)])
-        warm = getattr(self.prob, "warm_start", 0) and self.ell > 0
-        lam, k, hist = self.pcg(d, self.lam if warm else None)
+        kw = int(getattr(self.prob, "warm_start", 0))
+        if self.ell == 0:
+            self.warm_W, self.warm_FW = [], []
+        lam, k, hist, r = self.pcg(d, self.warm_W[-kw:] if kw else None, self.warm_FW[-kw:] if kw else None)
+        if kw:
+            self.warm_W = (self.warm_W + [lam.copy()])[-kw:]
+            self.warm_FW = (self.warm_FW + [d - r])[-kw:]
         v = self.Bt(lam)
         pc = _solve(self.Spp_cf, fpg - self.NT([h[s] - self.Phi[s].T @ v[s] for s in range(P)]))
         for s in range(P):

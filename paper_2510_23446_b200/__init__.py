@@ -136,9 +136,10 @@ class Solver:
     def set_solver(self, rtol=1e-10, max_iter=5000, scaling=1, tree_order=0):
         self._ck(self.L.tcg_set_solver(self.h, float(rtol), int(max_iter), int(scaling), int(tree_order)))
 
-    def set_warm_start(self, on=True):
-        """PCG of every step after the first starts from the previous step's lambda (f2)."""
-        self._ck(self.L.tcg_set_warm_start(self.h, int(bool(on))))
+    def set_warm_start(self, k=4):
+        """PCG of every step after the first starts from the Galerkin projection on the
+        previous k solutions (R20); 0 = the paper's lambda0 = 0."""
+        self._ck(self.L.tcg_set_warm_start(self.h, int(k)))
         return self
 
     def configure(self, prob):

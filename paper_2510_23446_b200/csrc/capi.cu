@@ -89,6 +89,7 @@ struct RankDev {
   int64_t* d_tstart = nullptr;
   int64_t ntiles = 0;
   double *A = nullptr, *Dinv = nullptr, *Sbb = nullptr, *xscr = nullptr;
+  double *Wr = nullptr, *FWr = nullptr, *dsave = nullptr, *wpart = nullptr;  // warm start (lazy)
   CholDesc* d_desc = nullptr;
   int ndesc = 0, maxT = 0, maxTr = 0, maxTb = 0;
   // global-layout vectors (entries of owned patches / lambda chunks valid)
@@ -180,7 +181,7 @@ struct tcg_ctx {
   int cache_bpos = 0;
   int cache_items = 0, cache_lam = 0, cache_pcprog = 0;
   int npf = 0;  // prefetched tiles per phase (stepper)
-  int warm = 0;  // PCG from the previous step's lambda (tcg_set_warm_start)
+  int warm = 0;  // warm-start subspace dimension k (tcg_set_warm_start), 0 = off
   int64_t* d_pcprog = nullptr;
   size_t smem_steps = 0;  // dynamic shared memory of k_steps: item scratch + caches
   int coarse_ch = 1, coarse_maxch = 1;
@@ -1675,6 +1676,12 @@ static StepArgs step_args(tcg_ctx* h) {
   A.scratch = (int)(h->smem_pcg / sizeof(double));
   A.npf = h->npf;
   A.warm = h->warm;
+  for (auto& R : h->rd) {
+    A.Wr[R.r] = R.Wr;
+    A.FWr[R.r] = R.FWr;
+    A.dsave[R.r] = R.dsave;
+    A.wpart[R.r] = R.wpart;
+  }
   A.mode = 0;
   A.dbg_stop = getenv("TCG_DEBUG_STOP") ? atoi(getenv("TCG_DEBUG_STOP")) : 0;
   A.sparse = h->sparse;
@@ -1719,6 +1726,15 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   if (n <= 0) return TCG_OK;
   if (h->steps_done + n > h->n_steps) return fail(h, TCG_EINVAL, "more steps than set_time allows (n_steps)");
   for (auto& R : h->rd) CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), h->stream));
+  if (h->warm)
+    for (auto& R : h->rd)
+      if (!R.Wr) {  // warm-start rings: k solutions and k F-products at the lambda level
+        const size_t m = (size_t)std::max<int64_t>(1, h->plan.m);
+        TRY(dzero(h, &R.Wr, (size_t)KW * m));
+        TRY(dzero(h, &R.FWr, (size_t)KW * m));
+        TRY(dzero(h, &R.dsave, m));
+        TRY(dzero(h, &R.wpart, (size_t)2 * h->nbr * KW_NV));
+      }
   StepArgs A = step_args(h);
   A.nsteps = n;
   DevPlan D = h->D;
@@ -1879,7 +1895,7 @@ tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, 
 
 tcg_status tcg_set_warm_start(tcg_handle h, int on) {
   if (!h) return TCG_EINVAL;
-  if (on != 0 && on != 1) return fail(h, TCG_EINVAL, "warm start is 0 or 1");
+  if (on < 0 || on > KW) return fail(h, TCG_EINVAL, "warm start subspace dimension must be in [0, " + std::to_string(KW) + "]");
   h->warm = on;
   return TCG_OK;
 }
@@ -2116,6 +2132,15 @@ static tcg_status run_fapply(tcg_ctx* h, int n, double* ms) {
   if (h->world > 1) return fail(h, TCG_EINVAL, "F-apply hooks need a single-process handle");
   CK(cudaSetDevice(h->device));
   for (auto& R : h->rd) CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), h->stream));
+  if (h->warm)
+    for (auto& R : h->rd)
+      if (!R.Wr) {  // warm-start rings: k solutions and k F-products at the lambda level
+        const size_t m = (size_t)std::max<int64_t>(1, h->plan.m);
+        TRY(dzero(h, &R.Wr, (size_t)KW * m));
+        TRY(dzero(h, &R.FWr, (size_t)KW * m));
+        TRY(dzero(h, &R.dsave, m));
+        TRY(dzero(h, &R.wpart, (size_t)2 * h->nbr * KW_NV));
+      }
   StepArgs A = step_args(h);
   A.nsteps = n;
   A.mode = 1;

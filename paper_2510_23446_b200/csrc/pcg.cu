@@ -55,6 +55,9 @@ struct LamC {
 // writes go to the launching block's own rank, reads of values owned elsewhere (interface
 // partners, lambda chunks, coarse rows) go to the owner's buffer (peer memory over NVLink on
 // a multi-GPU job; another allocation of the same device for virtual ranks).
+constexpr int KW = 4;                         // largest warm-start subspace
+constexpr int KW_NV = KW + KW * (KW + 1) / 2;  // W_j.d and the upper triangle of G
+__host__ __device__ constexpr int kw_idx(int i, int j) { return KW + i * KW - i * (i - 1) / 2 + (j - i); }  // i <= j
 struct StepArgs {
   // lambda-space vectors (m, valid on the owner of each chunk)
   double* lam[MAXR];
@@ -96,7 +99,11 @@ struct StepArgs {
   int npf;          // tiles of the next phase's first item bulk-copied to shared memory during a barrier
   int mode;         // 0: nsteps implicit-Euler steps; 1: nsteps applications q = F p (p = pk[0], q -> r[1])
   int dbg_stop;     // debug: 1 = return after the first step's R3 coarse solve
-  int warm;         // 1: PCG starts from gamma * the previous step's lambda, step >= 1
+  int warm;         // k > 0: PCG starts from the Galerkin projection on the previous k solutions (f2)
+  double* Wr[MAXR];     // warm start: ring of the previous k solutions (slot = global step % k), own rank
+  double* FWr[MAXR];    // and of d_j - r_j (= F W_j up to the tolerance)
+  double* dsave[MAXR];  // this step's d (lambda level)
+  double* wpart[MAXR];  // per-block partial dot products (2 x nbr x KW_NV), one rank
   // sparse coarse: per level forward rows / backward columns of the node factors
   int sparse;
   int cf_levels;                 // tree height + 1
@@ -1113,9 +1120,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     bar(PH_SY, false, 0.0);
     SSTAMP(4);
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
-    // (warm start: lambda keeps the previous step's value; rho0 = d^T M^-1 d stays the
-    // reference of the stopping rule, so warm and cold runs share one absolute target)
-    const bool warm = A.warm && (A.step0 + step > 0);
+    // (warm start: rho0 = d^T M^-1 d stays the reference of the stopping rule, so warm and
+    // cold runs share one absolute target)
+    const int nW = A.warm ? min(A.step0 + step, A.warm) : 0;
     double rho0;
     {
       double loc = 0.0;
@@ -1127,9 +1134,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                          },
                          smw, red, PF0(j_w), GAT(PH_SY, w));
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-        A.r[0][me][k] = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
+        const double dk = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
+        A.r[0][me][k] = dk;
         A.pk[0][me][k] = 0.0;
-        if (!warm) A.lam[me][k] = 0.0;
+        A.lam[me][k] = 0.0;
+        if (A.warm) A.dsave[me][k] = dk;
       }
       rho0 = bar(PH_P1, true, loc);
     }
@@ -1141,51 +1150,130 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     double rho = rho0, beta = 0.0;
     int rp = 0, pp = 0;
     double rel0 = 1.0;
-    if (warm && status == 1) {  // d = 0: the solution is lambda = 0, not the previous one
-      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) A.lam[me][k] = 0.0;
-      bar(PH_P1, false, 0.0);
-    }
-    if (warm && status == 0) {
-      // ---- W1-W3: q = F lambda_prev (the F-apply of the loop with p := lambda_prev), with
-      // the Galerkin scale gamma = lambda^T d / lambda^T F lambda (two reductions) ----
-      double ld = 0.0;
-      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) ld += ldcg(A.lam[me] + k) * ldcg(A.r[0][me] + k);
-      ld = block_sum(ld, red);
-      FOR_ITEMS(PH_P1, w)
-        p1_item(w, Xr,
-                [&](const ItemDesc& iw, int64_t bb, int pos) {
-                  const BPos q = bget(iw, bb, pos);
-                  return q.sign * ldcg(A.lam[lown(q.k)] + q.k);
-                },
-                A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
-      const double gnum = bar(PH_PC, true, ld);
-      COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
-      bar(PH_P5, false, 0.0);
-      double lq = 0.0;
-      FOR_ITEMS(PH_P5, w)
-        lq += p5_item(w, Xr, A.XW[me], D.p_grp, pcf,
-                      [&](const ItemDesc& iw, int64_t bb, int pos) {
-                        const BPos q = bget(iw, bb, pos);
-                        return q.sign * ldcg(A.lam[lown(q.k)] + q.k);
-                      },
-                      A.Y[me], A.Y2[me], smw, red, nullptr, PF0(j_w), GAT(PH_P5, w));
-      const double gden = bar(PH_SY, true, lq);
-      const double gamma = (gden > 0.0) ? gnum / gden : 0.0;  // uniform
-      // ---- W4: lambda0 = gamma lambda_prev, r0 = d - gamma F lambda_prev (the P7 formulas
-      // with alpha = gamma), z0 = M^-1 r0 ----
+    if (nW > 0 && status == 0) {
+      // ---- W1: Galerkin start on span{W_j} (oracle Oracle.pcg, R20): dot products
+      // b_j = W_j.d, G_ij = (W_i.FW_j + W_j.FW_i)/2 over the block's lambda chunk ----
+      __shared__ double s_g[KW_NV], s_c[KW];
+      const int64_t gs = A.step0 + step;
+      double acc[KW_NV];
+#pragma unroll
+      for (int v = 0; v < KW_NV; ++v) acc[v] = 0.0;
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const double dk = ldcg(A.dsave[me] + k);
+        double wv[KW], fv[KW];
+#pragma unroll
+        for (int j = 0; j < KW; ++j) {
+          wv[j] = fv[j] = 0.0;
+          if (j < nW) {
+            const int64_t so = ((gs - nW + j) % A.warm) * m + k;
+            wv[j] = ldcg(A.Wr[me] + so);
+            fv[j] = ldcg(A.FWr[me] + so);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < KW; ++j) acc[j] += wv[j] * dk;
+#pragma unroll
+        for (int i = 0; i < KW; ++i)
+#pragma unroll
+          for (int j = i; j < KW; ++j) acc[kw_idx(i, j)] += 0.5 * (wv[i] * fv[j] + wv[j] * fv[i]);
+      }
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+      for (int v = 0; v < KW_NV; ++v) {
+        const double t = warp_sum(acc[v]);
+        if (lane == 0) red[warp * KW_NV + v] = t;
+      }
+      __syncthreads();
+      if (threadIdx.x < KW_NV) {
+        double t = 0.0;
+        for (int w2 = 0; w2 < NTHR / 32; ++w2) t += red[w2 * KW_NV + threadIdx.x];
+        if (!MULTI) A.wpart[me][((gs & 1) * A.nbr + bl) * KW_NV + threadIdx.x] = t;
+        else s_g[threadIdx.x] = t;
+      }
+      if (!MULTI) {
+        bar(-1, false, 0.0);
+        // fixed-order sums over the blocks (warp v % 8 sums value v), identical in every block
+        for (int v = warp; v < KW_NV; v += NTHR / 32) {
+          double t = 0.0;
+          for (int b2 = lane; b2 < A.nbr; b2 += 32) t += ldcg(A.wpart[me] + ((gs & 1) * A.nbr + b2) * KW_NV + v);
+          t = warp_sum(t);
+          if (lane == 0) s_g[v] = t;
+        }
+        __syncthreads();
+      } else {
+        __syncthreads();
+        for (int v = 0; v < KW_NV; ++v) {
+          const double pv = s_g[v];
+          const double t = bar(-1, true, pv);
+          __syncthreads();
+          if (threadIdx.x == 0) s_g[v] = t;
+          __syncthreads();
+        }
+      }
+      // G c = b by Cholesky in index order, skipping columns whose pivot <= 1e-12 max G_ii
+      // (the oracle's chol_skip_solve); one thread, broadcast through shared memory
+      if (threadIdx.x == 0) {
+        double L[KW][KW], y[KW], c[KW];
+        bool act[KW];
+        double gmax = 0.0;
+        for (int i = 0; i < nW; ++i) gmax = fmax(gmax, s_g[kw_idx(i, i)]);
+        for (int j = 0; j < KW; ++j) {
+          act[j] = false;
+          y[j] = c[j] = 0.0;
+          for (int i = 0; i < KW; ++i) L[i][j] = 0.0;
+        }
+        for (int j = 0; j < nW; ++j) {
+          double sj = s_g[kw_idx(j, j)];
+          for (int q = 0; q < j; ++q)
+            if (act[q]) sj -= L[j][q] * L[j][q];
+          if (!(sj > 1e-12 * gmax)) continue;
+          act[j] = true;
+          L[j][j] = sqrt(sj);
+          for (int i = j + 1; i < nW; ++i) {
+            double t = s_g[kw_idx(j, i)];
+            for (int q = 0; q < j; ++q)
+              if (act[q]) t -= L[i][q] * L[j][q];
+            L[i][j] = t / L[j][j];
+          }
+        }
+        for (int j = 0; j < nW; ++j)
+          if (act[j]) {
+            double t = s_g[j];
+            for (int q = 0; q < j; ++q)
+              if (act[q]) t -= L[j][q] * y[q];
+            y[j] = t / L[j][j];
+          }
+        for (int j = nW - 1; j >= 0; --j)
+          if (act[j]) {
+            double t = y[j];
+            for (int q = j + 1; q < nW; ++q)
+              if (act[q]) t -= L[q][j] * c[q];
+            c[j] = t / L[j][j];
+          }
+        for (int j = 0; j < KW; ++j) s_c[j] = c[j];
+      }
+      __syncthreads();
+      // lambda0 = sum c_j W_j, r0 = d - sum c_j FW_j (own chunk)
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        double l0 = 0.0, rr = ldcg(A.dsave[me] + k);
+        for (int j = 0; j < nW; ++j) {
+          const int64_t so = ((gs - nW + j) % A.warm) * m + k;
+          l0 += s_c[j] * ldcg(A.Wr[me] + so);
+          rr -= s_c[j] * ldcg(A.FWr[me] + so);
+        }
+        A.lam[me][k] = l0;
+        A.r[1][me][k] = rr;
+      }
+      bar(PH_SY, false, 0.0);
+      // ---- W2: z0 = M^-1 r0, rho = r0^T z0 ----
       double loc = 0.0;
       FOR_ITEMS(PH_SY, w)
         loc += symv_item(w, Sr, A.PW[me],
                          [&](const ItemDesc& iw, int64_t bb, int pos) {
                            const BPos q = bget(iw, bb, pos);
-                           return q.aown * (q.sign * ldcg(A.r[0][lown(q.k)] + q.k) -
-                                            gamma * (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), q.part)));
+                           return q.aown * q.sign * ldcg(A.r[1][lown(q.k)] + q.k);
                          },
                          smw, red, PF0(j_w), GAT(PH_SY, w));
-      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-        A.r[1][me][k] = ldcg(A.r[0][me] + k) - gamma * (yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k)));
-        A.lam[me][k] *= gamma;
-      }
       rz = bar(PH_P1, true, loc);
       rho = rz;
       rp = 1;
@@ -1302,6 +1390,14 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       break;
     }
     hoff += it + 1;
+    if (A.warm) {  // this step's solution and d - r (= F lambda) into the ring (own chunk)
+      const int64_t so = ((int64_t)(A.step0 + step) % A.warm) * m;
+      const double* rf = A.r[rp][me];
+      for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        A.Wr[me][so + k] = A.lam[me][k];
+        A.FWr[me][so + k] = ldcg(A.dsave[me] + k) - ldcg(rf + k);
+      }
+    }
     SSTAMP(6);
     // ---- E1 v = B^T lambda ; w, -Phi^T v ----
     FOR_ITEMS(PH_P1, w)

@@ -361,14 +361,21 @@ def test_back_to_back_reductions_no_race(tcg, monkeypatch):
             assert np.linalg.norm(a1 - ref) / np.linalg.norm(ref) <= TOL
 
 
-@pytest.mark.parametrize("name,steps,vranks", [("cfg1", 10, 1), ("contrast", 6, 1), ("cfg2", 8, 1), ("cfg2", 4, 3)])
-def test_warm_start_matches_oracle(tcg, name, steps, vranks):
-    """Warm start (R20): the GPU's Galerkin-scaled lambda0 and
-    r0 = d - gamma F lambda_prev against the oracle's warm PCG, every step; on cfg2 it saves
-    PCG iterations against the cold start (oracle and GPU agree on both)."""
-    pr = next(p for p in SMALL if p.name == name) if name == "contrast" else workloads.get(name)
+@pytest.mark.parametrize("name,steps,vranks,k", [("cfg1", 10, 1, 4), ("cfg1", 10, 1, 1), ("contrast", 6, 1, 4),
+                                                 ("cfg2", 8, 1, 4), ("cfg2", 6, 3, 4), ("insulators", 7, 1, 3)])
+def test_warm_start_matches_oracle(tcg, name, steps, vranks, k):
+    """Warm start (R20): the GPU's Galerkin projection on the
+    previous k solutions (ring buffers, d - r products, skip-Cholesky in thread 0) against
+    the oracle's warm PCG, every step; on cfg2 it saves PCG iterations against the cold start.
+    'insulators' has exact starts (0 iterations after step 0), a d = 0 step (t = 1/2) and a
+    rank-1 subspace; it stops at t = 7/8 (at t = 1 the solution is exactly 0)."""
+    if name == "insulators":
+        pr = workloads.custom((2, 2, 1), 1, (2, 2, 2), [0.0] * 4, [1.0, 2.0, 1.0, 3.0], name="insulators")
+        pr.n_steps = 8
+    else:
+        pr = next(p for p in SMALL if p.name == name) if name == "contrast" else workloads.get(name)
     pr = copy.deepcopy(pr)
-    pr.warm_start = 1
+    pr.warm_start = k
     steps = min(steps, pr.n_steps)
     o = Oracle(copy.deepcopy(pr))
     o.run(steps)
@@ -385,6 +392,8 @@ def test_warm_start_matches_oracle(tcg, name, steps, vranks):
     err = np.linalg.norm(a1 - ref) / np.linalg.norm(ref)
     assert err <= tol, (err, list(it), o.iters)
     assert np.all(np.abs(np.array(it) - np.array(o.iters)) <= 1), (list(it), o.iters)
+    if name == "insulators":
+        assert all(i == 0 for i in it[1:]), list(it)
     if name == "cfg2":
         cold = copy.deepcopy(pr)
         cold.warm_start = 0

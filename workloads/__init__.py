@@ -41,7 +41,7 @@ class Problem:
     max_iter: int = 5000
     scaling: int = 1                     # 0 = none (paper P:L170), 1 = rho (BJ.ns "scaled")
     tree_order: int = 0                  # 0 ascending ids within a rank, 1 descending
-    warm_start: int = 0                  # 0: lambda0 = 0 (paper); 1: previous step's lambda
+    warm_start: int = 0                  # 0: lambda0 = 0 (paper); k: projection on the last k solutions
     extra: dict = field(default_factory=dict)
 
     @property
