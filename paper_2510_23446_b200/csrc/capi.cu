@@ -170,6 +170,10 @@ struct tcg_ctx {
     int kw = 1;                                    // forward gather sources per position
     double* pb = nullptr;                          // backward chunk partials
     unsigned int* cnt = nullptr;                   // backward chunk counters
+    int4* node = nullptr;                          // per node: parent, #fw items, #bw items, #children's fw items
+    int2* bwdep = nullptr;                         // per node: backward dependency (ancestor or -1), its item count
+    unsigned int* dflow = nullptr;                 // 3 x nodes dataflow counters (zeroed per launch)
+    int nn = 0;
   } ndd;
   // stepper work items per phase: ItemDesc lists ordered by (rank, block), per-block offsets
   ItemDesc* d_items[NPH] = {};
@@ -945,6 +949,29 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
     need = (need + 1) & ~(size_t)1;
     h->smem_pcg = std::max(h->smem_pcg, need * sizeof(double));
   }
+  {  // dataflow between levels (no grid barriers inside a coarse solve): item counts per node
+    std::vector<int4> nodev(nn);
+    for (int x = 0; x < nn; ++x) nodev[x] = make_int4(N[x].parent, 0, 0, 0);
+    for (const auto& d : fwi)
+      if (d.bc > 0) nodev[d.s].y++;
+    for (const auto& d : bwi)
+      if (d.bc > 0) nodev[d.s].z++;
+    for (int x = 0; x < nn; ++x)
+      if (N[x].parent >= 0) nodev[N[x].parent].w += nodev[x].y;
+    // backward dependency: the nearest ancestor with backward items (its x_V are x's x_B
+    // values, and it finishes after all of its own ancestors), -1 if none; the kernel also
+    // waits for x's own forward rows (y_V)
+    std::vector<int2> dep(nn);
+    for (int x = 0; x < nn; ++x) {
+      int a = N[x].parent;
+      while (a >= 0 && nodev[a].z == 0) a = N[a].parent;
+      dep[x] = a >= 0 ? make_int2(a, nodev[a].z) : make_int2(-1, 0);
+    }
+    TRY(dupload(h, &g.node, nodev));
+    TRY(dupload(h, &g.bwdep, dep));
+    TRY(dzero(h, &g.dflow, (size_t)3 * std::max(nn, 1)));
+    g.nn = nn;
+  }
   TRY(dupload(h, &g.fw, fwi));
   TRY(dupload(h, &g.bw, bwi));
   TRY(dupload(h, &g.fw_off, fwo));
@@ -1701,6 +1728,11 @@ static StepArgs step_args(tcg_ctx* h) {
     A.Pcs = g.Pcs;
     A.cf_pb = g.pb;
     A.cf_cnt = g.cnt;
+    A.cf_node = g.node;
+    A.cf_bwdep = g.bwdep;
+    A.cf_dflow = g.dflow;
+    A.cf_nn = g.nn;
+    A.cf_sync = getenv("TCG_CF_LEVELSYNC") && atoi(getenv("TCG_CF_LEVELSYNC")) != 0;
   }
   A.tstamp = h->tstamp;
   A.rtol = h->rtol;
@@ -1726,6 +1758,7 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   if (n <= 0) return TCG_OK;
   if (h->steps_done + n > h->n_steps) return fail(h, TCG_EINVAL, "more steps than set_time allows (n_steps)");
   for (auto& R : h->rd) CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), h->stream));
+  if (h->sparse) CK(cudaMemsetAsync(h->ndd.dflow, 0, 3 * sizeof(unsigned int) * std::max(h->ndd.nn, 1), h->stream));
   if (h->warm)
     for (auto& R : h->rd)
       if (!R.Wr) {  // warm-start rings: k solutions and k F-products at the lambda level
@@ -2132,6 +2165,7 @@ static tcg_status run_fapply(tcg_ctx* h, int n, double* ms) {
   if (h->world > 1) return fail(h, TCG_EINVAL, "F-apply hooks need a single-process handle");
   CK(cudaSetDevice(h->device));
   for (auto& R : h->rd) CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), h->stream));
+  if (h->sparse) CK(cudaMemsetAsync(h->ndd.dflow, 0, 3 * sizeof(unsigned int) * std::max(h->ndd.nn, 1), h->stream));
   if (h->warm)
     for (auto& R : h->rd)
       if (!R.Wr) {  // warm-start rings: k solutions and k F-products at the lambda level

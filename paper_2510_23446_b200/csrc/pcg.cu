@@ -120,6 +120,11 @@ struct StepArgs {
   double* Pcs;                   // coarse solution by primal group
   double* cf_pb;                 // backward chunk partial sums (64 per chunk)
   unsigned int* cf_cnt;          // backward chunk arrival counters (monotone)
+  const int4* cf_node;           // per node: parent, #fw items, #bw items, #children's fw items
+  const int2* cf_bwdep;          // per node: nearest ancestor with bw items and their count, or (-1, #own fw items)
+  unsigned int* cf_dflow;        // [0, nn): children's fw items done; [nn, 2nn): own fw; [2nn, 3nn): own bw
+  int cf_nn;
+  int cf_sync;                   // 1: level-synchronous (grid barrier per level) instead of dataflow
   unsigned long long* tstamp;  // optional phase timestamps (rank 0 block 0)
   double rtol;
   int max_iter;
@@ -1050,19 +1055,61 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     if (A.tstamp && me == 0 && bl == 0 && threadIdx.x == 0 && cstamp_call < 8 && k < 64)
       A.tstamp[528 + 8 * 4096 + cstamp_call * 64 + k] = gtimer();
   };
+  // Dataflow (default): no grid barrier between levels. A forward item of node x waits until
+  // all forward items of x's children are done (their B rows are x's input); a backward item
+  // waits for the parent's backward items (x_B lives in ancestors, all solved before the
+  // parent's) or, at the root, for the root's own forward items. Every block runs its items
+  // level by level, dependencies point to earlier levels, and all blocks are co-resident, so
+  // the waits always end. Counters are monotone within a launch (zeroed before it): target =
+  // solves so far x item count.
+  unsigned int cuse = 0;  // coarse solves in this launch (uniform)
+  auto cwait = [&](const unsigned int* c, unsigned int target) {
+    if (threadIdx.x == 0) {
+      const unsigned long long t0 = gtimer();
+      while ((int)(ld_acquire_u32(c, 0) - target) < 0)
+        if (gtimer() - t0 > kBarrierTimeoutNs) __trap();
+    }
+    __syncthreads();
+  };
   auto coarse_sparse = [&](auto gsrc) {
     cstamp(0);
+    ++cuse;
+    const int nn = A.cf_nn;
+    unsigned int* kd = A.cf_dflow;
+    unsigned int* fd = A.cf_dflow + nn;
+    unsigned int* bd = A.cf_dflow + 2 * nn;
     for (int lv = 0; lv < A.cf_levels; ++lv) {
       const int b = A.cf_fw_off[lv * A.nbr + bl], e = A.cf_fw_off[lv * A.nbr + bl + 1];
-      for (int j = b; j < e; ++j) fwc_item(A.cf_fw[j], A.FR, A.cf_prog, A.cf_kw, gsrc, A.CW, A.cf_pb, A.cf_cnt, smw);
-      bar(-1, false, 0.0);
+      for (int j = b; j < e; ++j) {
+        const ItemDesc& it = A.cf_fw[j];
+        const int4 nd = A.cf_node[it.s];
+        if (!A.cf_sync && nd.w > 0) cwait(kd + it.s, cuse * (unsigned int)nd.w);
+        fwc_item(it, A.FR, A.cf_prog, A.cf_kw, gsrc, A.CW, A.cf_pb, A.cf_cnt, smw);
+        if (!A.cf_sync && threadIdx.x == 0) {  // fwc_item ended with __syncthreads
+          __threadfence();
+          if (nd.x >= 0) atomicAdd(kd + nd.x, 1u);
+          atomicAdd(fd + it.s, 1u);
+        }
+      }
+      if (A.cf_sync) bar(-1, false, 0.0);
       cstamp(1 + lv);
     }
     for (int lv = A.cf_levels - 1; lv >= 0; --lv) {
       const int b = A.cf_bw_off[lv * A.nbr + bl], e = A.cf_bw_off[lv * A.nbr + bl + 1];
-      for (int j = b; j < e; ++j)
-        bwc_item(A.cf_bw[j], A.FR, A.CW, A.cf_vl, A.cf_bl, A.Pcs, A.cf_pb, A.cf_cnt, smw, A.scratch / TS - 9);
-      if (lv > 0) bar(-1, false, 0.0);
+      for (int j = b; j < e; ++j) {
+        const ItemDesc& it = A.cf_bw[j];
+        if (!A.cf_sync) {  // x_B from the ancestors, y_V from x's own forward rows
+          const int2 dp = A.cf_bwdep[it.s];
+          if (dp.x >= 0) cwait(bd + dp.x, cuse * (unsigned int)dp.y);
+          cwait(fd + it.s, cuse * (unsigned int)A.cf_node[it.s].y);
+        }
+        bwc_item(it, A.FR, A.CW, A.cf_vl, A.cf_bl, A.Pcs, A.cf_pb, A.cf_cnt, smw, A.scratch / TS - 9);
+        if (!A.cf_sync && threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(bd + it.s, 1u);
+        }
+      }
+      if (A.cf_sync && lv > 0) bar(-1, false, 0.0);
       cstamp(2 * A.cf_levels - lv);
     }
     ++cstamp_call;
