@@ -196,6 +196,8 @@ struct tcg_ctx {
   std::vector<std::vector<void*>> peer_bufs;  // [rank][buffer] device pointers (own or peer)
   double* sync_tok = nullptr;
   unsigned long long* tstamp = nullptr;
+  double* itime = nullptr;
+  int itime_stride = 0;
   double* dbgA = nullptr;
   double* dbgC = nullptr;
   std::vector<int64_t> h_a_off, h_vec_off, h_sbb_off;
@@ -1587,7 +1589,13 @@ static tcg_status do_setup(tcg_ctx* h) {
     }
     if (!h->h_st) CK(cudaMallocHost(&h->h_st, sizeof(PcgState)));
   }
-  if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) TRY(dzero(h, &h->tstamp, 8 * 64 + 16 + 8 * 4096 + 8 * 64));
+  if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) {
+    TRY(dzero(h, &h->tstamp, 8 * 64 + 16 + 8 * 4096 + 8 * 64));
+    int mx = 1;
+    for (int ph = 0; ph < NCACHE; ++ph) mx = std::max(mx, (int)h->h_items[ph].size());
+    h->itime_stride = mx;
+    TRY(dzero(h, &h->itime, (size_t)NCACHE * mx));
+  }
   if (getenv("TCG_DEBUG_KEEP") && atoi(getenv("TCG_DEBUG_KEEP")) != 0) {
     TRY(dalloc(h, &h->dbgA, h->rd[0].A ? (size_t)oa[h->rd[0].r] : 1));
     TRY(dalloc(h, &h->dbgC, (size_t)tri_tiles(Tc) * TSZ));
@@ -1735,6 +1743,8 @@ static StepArgs step_args(tcg_ctx* h) {
     A.cf_sync = getenv("TCG_CF_LEVELSYNC") && atoi(getenv("TCG_CF_LEVELSYNC")) != 0;
   }
   A.tstamp = h->tstamp;
+  A.itime = h->itime;
+  A.itime_stride = h->itime_stride;
   A.rtol = h->rtol;
   A.max_iter = h->max_iter;
   A.nranks = h->nranks;
@@ -2281,6 +2291,28 @@ tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t 
       tmp.push_back((double)n.B.size());
       tmp.push_back(n.TV);
       tmp.push_back(n.TB);
+    }
+    if (tmp.empty()) tmp.push_back(0);
+  } else if (what == 10 || what == 11) {
+    // 10: per-item durations (ns) of phase idx, 11: the items of phase idx as rows
+    // (block, s, I, part & 15, gather code, Tb, Tp, nb, np) -- phase-timing builds only
+    const int ph = idx;
+    if (ph < 0 || ph >= NCACHE) return TCG_EINVAL;
+    const auto& items = h->h_items[ph];
+    if (what == 10) {
+      if (!h->itime) return fail(h, TCG_ESTATE, "TCG_PHASE_TIMING not set");
+      std::vector<double> t((size_t)h->itime_stride);
+      CK(cudaMemcpy(t.data(), h->itime + (size_t)ph * h->itime_stride, t.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      tmp.assign(t.begin(), t.begin() + items.size());
+    } else {
+      const auto& bo = h->h_boff[ph];
+      for (size_t b = 0; b + 1 < bo.size(); ++b)
+        for (int j = bo[b]; j < bo[b + 1]; ++j) {
+          const ItemDesc& d = items[j];
+          for (double v : {(double)b, (double)d.s, (double)d.I, (double)(d.part & 15), (double)((d.part >> 4) & 3),
+                           (double)d.Tb, (double)d.Tp, (double)d.nb, (double)d.np})
+            tmp.push_back(v);
+        }
     }
     if (tmp.empty()) tmp.push_back(0);
   } else if (what == 7) {

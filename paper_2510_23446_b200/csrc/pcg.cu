@@ -126,6 +126,8 @@ struct StepArgs {
   int cf_nn;
   int cf_sync;                   // 1: level-synchronous (grid barrier per level) instead of dataflow
   unsigned long long* tstamp;  // optional phase timestamps (rank 0 block 0)
+  double* itime;               // optional per-item durations (ns), [phase * itime_stride + item]
+  int itime_stride;
   double rtol;
   int max_iter;
   // ranks
@@ -845,6 +847,11 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
 // step-level stamps of step 0 (slots 512..527): R1..R5 ends, loop end, E1..E3 ends
 #define SSTAMP(slot) \
   if (A.tstamp && me == 0 && bl == 0 && threadIdx.x == 0 && step == 0) A.tstamp[512 + (slot)] = gtimer()
+// per-item durations of PCG iteration 2 of step 0 (phase-timing builds): itime[ph][global item]
+#define ITIME_BEGIN unsigned long long it_t0 = 0; if (A.itime && step == 0 && it == 2 && threadIdx.x == 0) it_t0 = gtimer();
+#define ITIME_END(ph, j)                                                                                   \
+  if (A.itime && step == 0 && it == 2 && threadIdx.x == 0)                                                \
+    A.itime[(ph) * A.itime_stride + A.boff[ph][gb] + (j)] = (double)(gtimer() - it_t0);
 // per-block work-end stamps of PCG iteration 2 of step 0 (slots 528 + 8*block + phase)
 #define WSTAMP(slot)                                                                   \
   if (A.tstamp && step == 0 && it == 2) {                                              \
@@ -900,6 +907,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   const int64_t k0 = min(m, gb * A.lam_chunk), k1 = min(m, k0 + A.lam_chunk);
   const int nk = (int)(k1 - k0);
   unsigned int round = A.round0;
+  if (A.tstamp && threadIdx.x == 0 && gb < 4096) {  // phase-timing builds: the block's SM (slot 4)
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    A.tstamp[528 + gb * 8 + 4] = smid;
+  }
   const double* Xr = D.Ar[me];
   const double* Sr = D.Sbbr[me];
   // ---- per-launch setup: item lists (and lambda-chunk index data) into shared memory ----
@@ -1346,7 +1358,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           return q.aown * ldcg(A.PW[me] + own_idx(iw, pos)) + q.apart * ldcg(A.PW[pown(ppatch(bb))] + q.part) +
                  q.sign * beta * ldcg(pprev[lown(q.k)] + q.k);
         };
-        FOR_ITEMS(PH_P1, w) p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
+        FOR_ITEMS(PH_P1, w) {
+          ITIME_BEGIN
+          p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
+          ITIME_END(PH_P1, j_w)
+        }
         if (kq < k1) pcur[kq] = pv;
         for (int64_t k = kq + blockDim.x; k < k1; k += blockDim.x)
           pcur[k] = lw_p(k) * ldcg(A.PW[pown(lpat_p(k))] + lidx_p(k)) -
@@ -1365,7 +1381,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       double pq;
       {
         double loc = 0.0;
-        FOR_ITEMS(PH_P5, w)
+        FOR_ITEMS(PH_P5, w) {
+          ITIME_BEGIN
           loc += p5_item(w, Xr, A.XW[me], D.p_grp, pcf,
                          [&](const ItemDesc& iw, int64_t bb, int pos) {
                            const BPos q = bget(iw, bb, pos);
@@ -1374,6 +1391,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                          A.Y[me], A.Y2[me], smw, red,
                          (A.tstamp && step == 0 && it == 2 && gb < 4096) ? A.tstamp + 528 + gb * 8 + 4 : nullptr,
                          PF0(j_w), GAT(PH_P5, w));
+          ITIME_END(PH_P5, j_w)
+        }
         WSTAMP(2);
         pq = bar(PH_SY, true, loc);
       }
@@ -1398,7 +1417,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           yd = yv(pown(lpat_p(kq)), lidx_p(kq)) - yv(pown(lpat_m(kq)), lidx_m(kq));
         }
         double loc = 0.0;
-        FOR_ITEMS(PH_SY, w) loc += symv_item(w, Sr, A.PW[me], unew, smw, red, PF0(j_w), GAT(PH_SY, w));
+        FOR_ITEMS(PH_SY, w) {
+          ITIME_BEGIN
+          loc += symv_item(w, Sr, A.PW[me], unew, smw, red, PF0(j_w), GAT(PH_SY, w));
+          ITIME_END(PH_SY, j_w)
+        }
         if (kq < k1) {
           A.lam[me][kq] = lv + alpha * pv;
           rn[kq] = rv - alpha * yd;
