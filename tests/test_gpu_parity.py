@@ -403,3 +403,23 @@ def test_warm_start_matches_oracle(tcg, name, steps, vranks, k):
         itc = c.history()[0]
         c.close()
         assert sum(it[1:]) < sum(itc[1:]), (list(it), list(itc))
+
+
+def test_sparse_coarse_dataflow_equals_level_sync(tcg, sparse_coarse, monkeypatch):
+    """The dataflow ordering of the sparse coarse levels (per-node counters) changes only the
+    synchronisation, not the arithmetic: bit-identical to one grid barrier per level."""
+    pr = workloads.cfg2()
+    out = {}
+    for sync in ("0", "1"):
+        monkeypatch.setenv("TCG_CF_LEVELSYNC", sync)
+        a1, a0, it, hist, inf = run_gpu(tcg, pr, 3)
+        out[sync] = (a1, list(it), hist)
+    assert np.array_equal(out["0"][0], out["1"][0]) and out["0"][1] == out["1"][1]
+    assert np.array_equal(out["0"][2], out["1"][2])
+
+
+def test_warm_start_with_sparse_coarse(tcg, sparse_coarse):
+    """Warm start (R20) on the sparse coarse path against the oracle's warm PCG."""
+    pr = copy.deepcopy(workloads.cfg2())
+    pr.warm_start = 4
+    compare(tcg, pr, steps=5)
