@@ -617,19 +617,8 @@ static tcg_status deal_items(tcg_ctx* h, ItemLists& L, int ph, int overhead, boo
   };
   std::vector<ItemDesc> all;
   std::vector<int> boff(1, 0);
-  const char* fe = getenv("TCG_STEP_FLAGS");
-  const int flags = fe ? atoi(fe) : 0;
   for (auto& v : L.per_rank) {
     std::stable_sort(v.begin(), v.end(), bycost);
-    if (flags & 2) {  // experiment: round-robin dealing of the cost-sorted items
-      std::vector<std::vector<ItemDesc>> blk(nbr);
-      for (size_t i = 0; i < v.size(); ++i) blk[i % nbr].push_back(v[i].second);
-      for (int b = 0; b < nbr; ++b) {
-        all.insert(all.end(), blk[b].begin(), blk[b].end());
-        boff.push_back((int)all.size());
-      }
-      continue;
-    }
     std::vector<std::vector<ItemDesc>> blk(nbr);
     std::vector<std::pair<int64_t, int>> heap;  // (load, block) min-heap
     for (int b = 0; b < nbr; ++b) heap.push_back({0, b});
