@@ -1358,7 +1358,9 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(deal_items(h, bw, PH_BW, 2));
     TRY(deal_items(h, bwc, PH_BWC, 2));
     TRY(deal_items(h, rhs, PH_RHS, 0));
+    hm.mark("deal");
     if (h->sparse) TRY(setup_sparse_coarse(h, owner, cidx, cpat));
+    hm.mark("sparse-coarse");
   }
   // shared-memory caches of the per-iteration item lists and the lambda chunk, if they fit
   // next to the scratch at `per` blocks per SM
@@ -1559,11 +1561,18 @@ static tcg_status do_setup(tcg_ctx* h) {
   // readout maps: glued edge -> (patch*nloc + local) of its lowest-id owner; gathered a
   {
     std::vector<int64_t> src(pl.nedges, -1);
-    for (int s = 0; s < P; ++s)
-      for (int a = 0; a < pl.nloc; ++a) {
-        int64_t g = pl.local_to_global(s, a);
-        if (src[g] < 0) src[g] = (int64_t)s * pl.nloc + a;
-      }
+    for (int s = 0; s < P; ++s) {  // local DOF a -> glued edge, in local order (no divisions)
+      const int sx = s % pl.P[0], sy = (s / pl.P[0]) % pl.P[1], sz = s / (pl.P[0] * pl.P[1]);
+      const int64_t o0 = (int64_t)sx * (pl.n[0] - 1), o1 = (int64_t)sy * (pl.n[1] - 1), o2 = (int64_t)sz * (pl.n[2] - 1);
+      int a = 0;
+      for (int c = 0; c < 3; ++c)
+        for (int k = 0; k < pl.comp_dim(c, 2); ++k)
+          for (int j = 0; j < pl.comp_dim(c, 1); ++j)
+            for (int i = 0; i < pl.comp_dim(c, 0); ++i, ++a) {
+              const int64_t g = pl.edge_id(c, o0 + i, o1 + j, o2 + k);
+              if (src[g] < 0) src[g] = (int64_t)s * pl.nloc + a;
+            }
+    }
     TRY(dupload(h, &h->d_glued_src, src));
     TRY(dalloc(h, &h->glued, pl.nedges));
     TRY(dalloc(h, &h->a_all, (size_t)P * pl.nloc));

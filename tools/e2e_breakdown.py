@@ -5,7 +5,7 @@ sys.path.insert(0, os.getcwd())
 import torch, workloads, paper_2510_23446_b200 as tcg
 for name in sys.argv[1:] or ["cfg2"]:
     prob = workloads.get(name)
-    for rep in range(4):
+    for rep in range(int(os.environ.get("E2E_REPS", "4"))):
         torch.cuda.synchronize()
         t = [time.perf_counter()]
         u = tcg.Solver(device=0); t.append(time.perf_counter())
