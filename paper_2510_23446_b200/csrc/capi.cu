@@ -14,6 +14,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <chrono>
@@ -473,7 +474,7 @@ static tcg_status check_err(tcg_ctx* h) {
   return TCG_OK;
 }
 
-static tcg_status do_numeric(tcg_ctx* h) {
+static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid = nullptr) {
   Plan& pl = h->plan;
   const int Tc = h->Tc;
   const double dt = h->T / h->n_steps;
@@ -569,6 +570,7 @@ static tcg_status do_numeric(tcg_ctx* h) {
       CKL();
     }
   }
+  if (mid) TRY(mid());  // host work overlapped with the kernels above (first setup only)
   // insulator precompute: XJ = [X_rr j_S,r ; j_S,p - Phi^T j_S,r] for owned patches
   for (auto& R : h->rd) {
     const int b0 = h->h_boff[PH_FWA][R.r * h->nbr], n = h->h_boff[PH_FWA][(R.r + 1) * h->nbr] - b0;
@@ -1277,181 +1279,193 @@ static tcg_status do_setup(tcg_ctx* h) {
   std::vector<int> crow_owner(std::max(Tc, 1));
   for (int I = 0; I < Tc; ++I) crow_owner[I] = (int)((int64_t)I * NR / Tc);
   TRY(dupload(h, &h->d_crow_owner, crow_owner));
-  {
-    auto desc = [&](int s, int I) {
-      ItemDesc d{};
-      d.s = s;
-      d.I = I;
-      d.Ti = Ti[s]; d.Tb = Tb[s]; d.Tp = Tp[s]; d.T = T[s];
-      d.nb = nb[s]; d.np = np[s];
-      d.a_off = a_off[s]; d.vec_off = vec_off[s]; d.b_off = b_off[s]; d.p_off = p_off[s]; d.sbb_off = sbb_off[s];
-      return d;
-    };
-    ItemLists p1(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR);
-    for (int s = 0; s < P; ++s) {
-      const int r = owner[s];
-      const int Trs = Ti[s] + Tb[s];
-      for (int I = 0; I < T[s]; ++I) {
-        const int cost = I < Trs ? I + 1 : Trs;
-        if (pl.sigma[s] > 0) fw.per_rank[r].push_back({cost, desc(s, I)});
-        fwa.per_rank[r].push_back({cost, desc(s, I)});
+  // The stepper's work items and shared-memory caches are built on the host while the
+  // assembly / factorisation / coarse kernels run (do_numeric calls this after launching
+  // them, before the insulator precompute that needs the items).
+  auto deal_phase = [&]() -> tcg_status {
+    {
+      auto desc = [&](int s, int I) {
+        ItemDesc d{};
+        d.s = s;
+        d.I = I;
+        d.Ti = Ti[s]; d.Tb = Tb[s]; d.Tp = Tp[s]; d.T = T[s];
+        d.nb = nb[s]; d.np = np[s];
+        d.a_off = a_off[s]; d.vec_off = vec_off[s]; d.b_off = b_off[s]; d.p_off = p_off[s]; d.sbb_off = sbb_off[s];
+        return d;
+      };
+      ItemLists p1(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR);
+      for (int s = 0; s < P; ++s) {
+        const int r = owner[s];
+        const int Trs = Ti[s] + Tb[s];
+        for (int I = 0; I < T[s]; ++I) {
+          const int cost = I < Trs ? I + 1 : Trs;
+          if (pl.sigma[s] > 0) fw.per_rank[r].push_back({cost, desc(s, I)});
+          fwa.per_rank[r].push_back({cost, desc(s, I)});
+        }
+        for (int J = 0; J < std::max(Trs, 1); ++J) {
+          bw.per_rank[r].push_back({T[s] - J, desc(s, J)});
+          if (pl.sigma[s] > 0) bwc.per_rank[r].push_back({T[s] - J, desc(s, J)});
+        }
+        if (pl.sigma[s] > 0)
+          for (int c = 0; c < 3; ++c) rhs.per_rank[r].push_back({pl.nloc / 3, desc(s, c)});
+        else
+          rhs.per_rank[r].push_back({T[s] * TS / 8, desc(s, -1)});
+        for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
+        for (int J = 0; J < Tb[s]; ++J) {
+          p5.per_rank[r].push_back({Tb[s] - J, desc(s, J)});
+          if (np[s] > 0) {
+            ItemDesc d = desc(s, J);
+            d.part = 1;
+            p5.per_rank[r].push_back({Tp[s], d});
+          }
+        }
+        for (int I = 0; I < Tb[s]; ++I) sy.per_rank[r].push_back({Tb[s], desc(s, I)});
       }
-      for (int J = 0; J < std::max(Trs, 1); ++J) {
-        bw.per_rank[r].push_back({T[s] - J, desc(s, J)});
-        if (pl.sigma[s] > 0) bwc.per_rank[r].push_back({T[s] - J, desc(s, J)});
+      const int ch = h->coarse_ch;
+      // PC gather programs (one per column chunk; shared by the chunk's row-block items)
+      std::vector<int64_t> prog;
+      std::vector<int64_t> prog_off(h->coarse_maxch), prog_len(h->coarse_maxch);
+      for (int c = 0; c < h->coarse_maxch; ++c) {
+        const int J0 = c * ch, J1 = std::min(Tc, J0 + ch);
+        const int nE = (J1 - J0) * TS;
+        prog_off[c] = (int64_t)prog.size();
+        std::vector<int64_t> offs(nE + 1, 0), ent;
+        for (int e = 0; e < nE; ++e) {
+          const int64_t g = (int64_t)J0 * TS + e;
+          if (g < pl.nc)
+            for (int k = pl.coarse_ptr[g]; k < pl.coarse_ptr[g + 1]; ++k)
+              ent.push_back(cidx[k] | ((int64_t)owner[cpat[k]] << 56));
+          offs[e + 1] = (int64_t)ent.size();
+        }
+        prog.insert(prog.end(), offs.begin(), offs.end());
+        prog.insert(prog.end(), ent.begin(), ent.end());
+        prog_len[c] = (int64_t)prog.size() - prog_off[c];
       }
-      if (pl.sigma[s] > 0)
-        for (int c = 0; c < 3; ++c) rhs.per_rank[r].push_back({pl.nloc / 3, desc(s, c)});
-      else
-        rhs.per_rank[r].push_back({T[s] * TS / 8, desc(s, -1)});
-      for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
-      for (int J = 0; J < Tb[s]; ++J) {
-        p5.per_rank[r].push_back({Tb[s] - J, desc(s, J)});
-        if (np[s] > 0) {
-          ItemDesc d = desc(s, J);
-          d.part = 1;
-          p5.per_rank[r].push_back({Tp[s], d});
+      if (prog.empty()) prog.push_back(0);
+      TRY(dupload(h, &h->d_pcprog, prog));
+      for (int I = 0; I < (h->sparse ? 0 : Tc); ++I)
+        for (int c = 0; c < h->coarse_maxch; ++c) {
+          ItemDesc d{};
+          d.s = I;
+          d.I = c;
+          d.vec_off = prog_off[c];
+          d.b_off = prog_len[c];
+          pcv.per_rank[crow_owner[I]].push_back({std::min(Tc, (c + 1) * ch) - c * ch, d});
+        }
+      // fixed per-item overhead (tile units) of the latency-bound item phases
+      // whole-patch dealing when there are many patches per block (cfg5: 2048 patches)
+      const bool grp = (int64_t)P >= 2 * (int64_t)NR * h->nbr && !(getenv("TCG_NO_GROUP") && atoi(getenv("TCG_NO_GROUP")));
+      TRY(deal_items(h, p1, PH_P1, 2, grp));
+      TRY(deal_items(h, pcv, PH_PC, 2));
+      TRY(deal_items(h, p5, PH_P5, 2, grp));
+      TRY(deal_items(h, sy, PH_SY, 2));  // (grouping the S_bb rows of a patch measured slower)
+      TRY(deal_items(h, fw, PH_FW, 2));
+      TRY(deal_items(h, fwa, PH_FWA, 2));
+      TRY(deal_items(h, bw, PH_BW, 2));
+      TRY(deal_items(h, bwc, PH_BWC, 2));
+      TRY(deal_items(h, rhs, PH_RHS, 0));
+      hm.mark("deal");
+    }
+    // shared-memory caches of the per-iteration item lists and the lambda chunk, if they fit
+    // next to the scratch at `per` blocks per SM
+    {
+      int max_items = 0;
+      for (int gb = 0; gb < NR * h->nbr; ++gb) {
+        int n = 0;
+        for (int ph = 0; ph < NCACHE; ++ph) n += h->h_boff[ph][gb + 1] - h->h_boff[ph][gb];
+        max_items = std::max(max_items, n);
+      }
+      const size_t items_b = (size_t)max_items * sizeof(ItemDesc);
+      int64_t max_prog = 0;
+      {
+        const std::vector<ItemDesc>& hp = h->h_items[PH_PC];
+        for (int gb = 0; gb < NR * h->nbr; ++gb) {
+          int64_t n = 0;
+          for (int j = h->h_boff[PH_PC][gb]; j < h->h_boff[PH_PC][gb + 1]; ++j) n += hp[j].b_off;
+          max_prog = std::max<int64_t>(max_prog, (n + 1) & ~(int64_t)1);
         }
       }
-      for (int I = 0; I < Tb[s]; ++I) sy.per_rank[r].push_back({Tb[s], desc(s, I)});
-    }
-    const int ch = h->coarse_ch;
-    // PC gather programs (one per column chunk; shared by the chunk's row-block items)
-    std::vector<int64_t> prog;
-    std::vector<int64_t> prog_off(h->coarse_maxch), prog_len(h->coarse_maxch);
-    for (int c = 0; c < h->coarse_maxch; ++c) {
-      const int J0 = c * ch, J1 = std::min(Tc, J0 + ch);
-      const int nE = (J1 - J0) * TS;
-      prog_off[c] = (int64_t)prog.size();
-      std::vector<int64_t> offs(nE + 1, 0), ent;
-      for (int e = 0; e < nE; ++e) {
-        const int64_t g = (int64_t)J0 * TS + e;
-        if (g < pl.nc)
-          for (int k = pl.coarse_ptr[g]; k < pl.coarse_ptr[g + 1]; ++k)
-            ent.push_back(cidx[k] | ((int64_t)owner[cpat[k]] << 56));
-        offs[e + 1] = (int64_t)ent.size();
+      const size_t prog_b = (size_t)max_prog * sizeof(int64_t);
+      const size_t lam_b = (size_t)h->lam_chunk * sizeof(LamC);
+      int smem_sm = 0, reserved = 0;
+      CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
+      CK(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, h->device));
+      cudaFuncAttributes fa;
+      CK(cudaFuncGetAttributes(&fa, k_steps<true, true>));
+      int64_t budget = (int64_t)smem_sm / per - reserved - (int64_t)fa.sharedSizeBytes - 256;
+      // tile prefetch buffer first (bulk copies of the next phase's first tiles during barriers)
+      {
+        const char* ne = getenv("TCG_NPF");
+        int npf = ne ? std::max(0, std::min(2, atoi(ne))) : 1;  // 2 tiles shrink L1 too much on the HBM-bound configs
+        while (npf > 0 && (int64_t)(h->smem_pcg + (size_t)npf * TSZ * sizeof(double)) > budget) --npf;
+        h->npf = npf;
+        budget -= (int64_t)npf * TSZ * sizeof(double);
       }
-      prog.insert(prog.end(), offs.begin(), offs.end());
-      prog.insert(prog.end(), ent.begin(), ent.end());
-      prog_len[c] = (int64_t)prog.size() - prog_off[c];
-    }
-    if (prog.empty()) prog.push_back(0);
-    TRY(dupload(h, &h->d_pcprog, prog));
-    for (int I = 0; I < (h->sparse ? 0 : Tc); ++I)
-      for (int c = 0; c < h->coarse_maxch; ++c) {
-        ItemDesc d{};
-        d.s = I;
-        d.I = c;
-        d.vec_off = prog_off[c];
-        d.b_off = prog_len[c];
-        pcv.per_rank[crow_owner[I]].push_back({std::min(Tc, (c + 1) * ch) - c * ch, d});
-      }
-    // fixed per-item overhead (tile units) of the latency-bound item phases
-    // whole-patch dealing when there are many patches per block (cfg5: 2048 patches)
-    const bool grp = (int64_t)P >= 2 * (int64_t)NR * h->nbr && !(getenv("TCG_NO_GROUP") && atoi(getenv("TCG_NO_GROUP")));
-    TRY(deal_items(h, p1, PH_P1, 2, grp));
-    TRY(deal_items(h, pcv, PH_PC, 2));
-    TRY(deal_items(h, p5, PH_P5, 2, grp));
-    TRY(deal_items(h, sy, PH_SY, 2));  // (grouping the S_bb rows of a patch measured slower)
-    TRY(deal_items(h, fw, PH_FW, 2));
-    TRY(deal_items(h, fwa, PH_FWA, 2));
-    TRY(deal_items(h, bw, PH_BW, 2));
-    TRY(deal_items(h, bwc, PH_BWC, 2));
-    TRY(deal_items(h, rhs, PH_RHS, 0));
-    hm.mark("deal");
-    if (h->sparse) TRY(setup_sparse_coarse(h, owner, cidx, cpat));
-    hm.mark("sparse-coarse");
-  }
-  // shared-memory caches of the per-iteration item lists and the lambda chunk, if they fit
-  // next to the scratch at `per` blocks per SM
-  {
-    int max_items = 0;
-    for (int gb = 0; gb < NR * h->nbr; ++gb) {
-      int n = 0;
-      for (int ph = 0; ph < NCACHE; ++ph) n += h->h_boff[ph][gb + 1] - h->h_boff[ph][gb];
-      max_items = std::max(max_items, n);
-    }
-    const size_t items_b = (size_t)max_items * sizeof(ItemDesc);
-    int64_t max_prog = 0;
-    {
-      const std::vector<ItemDesc>& hp = h->h_items[PH_PC];
+      const char* ev = getenv("TCG_NO_SMEM_CACHE");
+      const bool allow = !(ev && atoi(ev) != 0);
+      h->cache_items = allow && (int64_t)(h->smem_pcg + items_b) <= budget && items_b <= 48 * 1024;
+      h->cache_pcprog = allow && h->cache_items && (int64_t)(h->smem_pcg + items_b + prog_b) <= budget && prog_b <= 32 * 1024;
+      const size_t used = h->smem_pcg + (h->cache_items ? items_b : 0) + (h->cache_pcprog ? prog_b : 0);
+      h->cache_lam = allow && (int64_t)(used + lam_b) <= budget && lam_b <= 32 * 1024;
+      size_t used2 = used + (h->cache_lam ? lam_b : 0);
+      // b-position records of the patches of each block's P1 / P5 / SY items
+      std::vector<int> bpl, bploff(1, 0);
+      size_t max_bp = 0;
       for (int gb = 0; gb < NR * h->nbr; ++gb) {
-        int64_t n = 0;
-        for (int j = h->h_boff[PH_PC][gb]; j < h->h_boff[PH_PC][gb + 1]; ++j) n += hp[j].b_off;
-        max_prog = std::max<int64_t>(max_prog, (n + 1) & ~(int64_t)1);
+        std::vector<int> pats;
+        for (int ph : {PH_P1, PH_P5, PH_SY})
+          for (int j = h->h_boff[ph][gb]; j < h->h_boff[ph][gb + 1]; ++j) pats.push_back(h->h_items[ph][j].s);
+        std::sort(pats.begin(), pats.end());
+        pats.erase(std::unique(pats.begin(), pats.end()), pats.end());
+        int off = 0;
+        for (int sp : pats) {
+          bpl.push_back(sp);
+          bpl.push_back(off);
+          off += nb[sp];
+        }
+        bploff.push_back((int)(bpl.size() / 2));
+        max_bp = std::max(max_bp, (size_t)off * sizeof(BPos));
       }
-    }
-    const size_t prog_b = (size_t)max_prog * sizeof(int64_t);
-    const size_t lam_b = (size_t)h->lam_chunk * sizeof(LamC);
-    int smem_sm = 0, reserved = 0;
-    CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device));
-    CK(cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, h->device));
-    cudaFuncAttributes fa;
-    CK(cudaFuncGetAttributes(&fa, k_steps<true, true>));
-    int64_t budget = (int64_t)smem_sm / per - reserved - (int64_t)fa.sharedSizeBytes - 256;
-    // tile prefetch buffer first (bulk copies of the next phase's first tiles during barriers)
-    {
-      const char* ne = getenv("TCG_NPF");
-      int npf = ne ? std::max(0, std::min(2, atoi(ne))) : 1;  // 2 tiles shrink L1 too much on the HBM-bound configs
-      while (npf > 0 && (int64_t)(h->smem_pcg + (size_t)npf * TSZ * sizeof(double)) > budget) --npf;
-      h->npf = npf;
-      budget -= (int64_t)npf * TSZ * sizeof(double);
-    }
-    const char* ev = getenv("TCG_NO_SMEM_CACHE");
-    const bool allow = !(ev && atoi(ev) != 0);
-    h->cache_items = allow && (int64_t)(h->smem_pcg + items_b) <= budget && items_b <= 48 * 1024;
-    h->cache_pcprog = allow && h->cache_items && (int64_t)(h->smem_pcg + items_b + prog_b) <= budget && prog_b <= 32 * 1024;
-    const size_t used = h->smem_pcg + (h->cache_items ? items_b : 0) + (h->cache_pcprog ? prog_b : 0);
-    h->cache_lam = allow && (int64_t)(used + lam_b) <= budget && lam_b <= 32 * 1024;
-    size_t used2 = used + (h->cache_lam ? lam_b : 0);
-    // b-position records of the patches of each block's P1 / P5 / SY items
-    std::vector<int> bpl, bploff(1, 0);
-    size_t max_bp = 0;
-    for (int gb = 0; gb < NR * h->nbr; ++gb) {
-      std::vector<int> pats;
-      for (int ph : {PH_P1, PH_P5, PH_SY})
-        for (int j = h->h_boff[ph][gb]; j < h->h_boff[ph][gb + 1]; ++j) pats.push_back(h->h_items[ph][j].s);
-      std::sort(pats.begin(), pats.end());
-      pats.erase(std::unique(pats.begin(), pats.end()), pats.end());
-      int off = 0;
-      for (int sp : pats) {
-        bpl.push_back(sp);
-        bpl.push_back(off);
-        off += nb[sp];
+      h->cache_bpos = allow && h->cache_items && (int64_t)(used2 + max_bp) <= budget && max_bp <= 48 * 1024;
+      if (h->cache_bpos) {
+        used2 += max_bp;
+        for (int ph : {PH_P1, PH_P5, PH_SY})
+          for (int gb = 0; gb < NR * h->nbr; ++gb)
+            for (int j = h->h_boff[ph][gb]; j < h->h_boff[ph][gb + 1]; ++j) {
+              ItemDesc& d = h->h_items[ph][j];
+              for (int q = bploff[gb]; q < bploff[gb + 1]; ++q)
+                if (bpl[2 * q] == d.s) d.bc = bpl[2 * q + 1];
+            }
       }
-      bploff.push_back((int)(bpl.size() / 2));
-      max_bp = std::max(max_bp, (size_t)off * sizeof(BPos));
+      if (bpl.empty()) bpl.assign(2, 0);
+      TRY(dupload(h, &h->d_bpl, bpl));
+      TRY(dupload(h, &h->d_bploff, bploff));
+      for (int ph = 0; ph < NPH; ++ph) {
+        std::vector<ItemDesc> all = h->h_items[ph];
+        if (all.empty()) all.push_back(ItemDesc{});
+        TRY(dupload(h, &h->d_items[ph], all));
+        TRY(dupload(h, &h->d_boff[ph], h->h_boff[ph]));
+      }
+      h->smem_steps = used2 + (size_t)h->npf * TSZ * sizeof(double);
+      for (const void* f : {(const void*)k_steps<false, false>, (const void*)k_steps<true, false>,
+                            (const void*)k_steps<false, true>, (const void*)k_steps<true, true>})
+        TRY(set_smem(h, f, h->smem_steps));
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps<true, true>, NTHR, h->smem_steps));
+      if (occ < per) return fail(h, TCG_ECUDA, "persistent stepper: shared-memory caches broke occupancy");
     }
-    h->cache_bpos = allow && h->cache_items && (int64_t)(used2 + max_bp) <= budget && max_bp <= 48 * 1024;
-    if (h->cache_bpos) {
-      used2 += max_bp;
-      for (int ph : {PH_P1, PH_P5, PH_SY})
-        for (int gb = 0; gb < NR * h->nbr; ++gb)
-          for (int j = h->h_boff[ph][gb]; j < h->h_boff[ph][gb + 1]; ++j) {
-            ItemDesc& d = h->h_items[ph][j];
-            for (int q = bploff[gb]; q < bploff[gb + 1]; ++q)
-              if (bpl[2 * q] == d.s) d.bc = bpl[2 * q + 1];
-          }
+    if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) {
+      TRY(dzero(h, &h->tstamp, 8 * 64 + 16 + 8 * 4096 + 8 * 64));
+      int mx = 1;
+      for (int ph = 0; ph < NCACHE; ++ph) mx = std::max(mx, (int)h->h_items[ph].size());
+      h->itime_stride = mx;
+      TRY(dzero(h, &h->itime, (size_t)NCACHE * mx));
     }
-    if (bpl.empty()) bpl.assign(2, 0);
-    TRY(dupload(h, &h->d_bpl, bpl));
-    TRY(dupload(h, &h->d_bploff, bploff));
-    for (int ph = 0; ph < NPH; ++ph) {
-      std::vector<ItemDesc> all = h->h_items[ph];
-      if (all.empty()) all.push_back(ItemDesc{});
-      TRY(dupload(h, &h->d_items[ph], all));
-      TRY(dupload(h, &h->d_boff[ph], h->h_boff[ph]));
-    }
-    h->smem_steps = used2 + (size_t)h->npf * TSZ * sizeof(double);
-    for (const void* f : {(const void*)k_steps<false, false>, (const void*)k_steps<true, false>,
-                          (const void*)k_steps<false, true>, (const void*)k_steps<true, true>})
-      TRY(set_smem(h, f, h->smem_steps));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_steps<true, true>, NTHR, h->smem_steps));
-    if (occ < per) return fail(h, TCG_ECUDA, "persistent stepper: shared-memory caches broke occupancy");
-  }
-
-  hm.mark("items+caches");
+    hm.mark("items+caches (overlapped)");
+    return TCG_OK;
+  };
+  if (h->sparse) TRY(setup_sparse_coarse(h, owner, cidx, cpat));
+  hm.mark("sparse-coarse");
   // ---- per-rank allocations ----
   std::vector<int> local_ranks;
   if (h->world > 1) local_ranks.push_back(h->rank);
@@ -1587,13 +1601,6 @@ static tcg_status do_setup(tcg_ctx* h) {
     }
     if (!h->h_st) CK(cudaMallocHost(&h->h_st, sizeof(PcgState)));
   }
-  if (getenv("TCG_PHASE_TIMING") && atoi(getenv("TCG_PHASE_TIMING")) != 0) {
-    TRY(dzero(h, &h->tstamp, 8 * 64 + 16 + 8 * 4096 + 8 * 64));
-    int mx = 1;
-    for (int ph = 0; ph < NCACHE; ++ph) mx = std::max(mx, (int)h->h_items[ph].size());
-    h->itime_stride = mx;
-    TRY(dzero(h, &h->itime, (size_t)NCACHE * mx));
-  }
   if (getenv("TCG_DEBUG_KEEP") && atoi(getenv("TCG_DEBUG_KEEP")) != 0) {
     TRY(dalloc(h, &h->dbgA, h->rd[0].A ? (size_t)oa[h->rd[0].r] : 1));
     TRY(dalloc(h, &h->dbgC, (size_t)tri_tiles(Tc) * TSZ));
@@ -1601,7 +1608,7 @@ static tcg_status do_setup(tcg_ctx* h) {
   h->bar_round = 0;
   TRY(sync_ranks(h));
   hm.mark("tables+state");
-  TRY(do_numeric(h));
+  TRY(do_numeric(h, deal_phase));
   hm.mark("numeric");
   h->setup_done = true;
   return TCG_OK;
