@@ -686,12 +686,34 @@ static tcg_status deal_items(tcg_ctx* h, ItemLists& L, int ph, int overhead, boo
 // Sparse coarse problem: nested-dissection symbolic analysis (coarse_nd.h), node
 // storage, assembly maps, per-level factorisation descriptors, the forward gather programs and
 // the stepper's per-level work items (single-rank handles; requires h->nbr).
+// host-side timeline of do_setup (TCG_HOST_TIMING=1: one line on stderr per setup)
+struct HostMarks {
+  bool on = getenv("TCG_HOST_TIMING") && atoi(getenv("TCG_HOST_TIMING")) != 0;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  std::string line;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    char b[96];
+    snprintf(b, sizeof b, " %s %.3f", what, std::chrono::duration<double, std::milli>(t - last).count());
+    line += b;
+    last = t;
+  }
+  ~HostMarks() {
+    if (on) fprintf(stderr, "[tcg host ms]%s total %.3f\n", line.c_str(),
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+
 static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner, const std::vector<int64_t>& cidx,
                                       const std::vector<int>& cpat) {
   Plan& pl = h->plan;
   CoarseND& nd = h->nd;
+  HostMarks hm;
+  hm.line = " [sparse coarse]";
   nd = CoarseND();
   nd.build(pl);
+  hm.mark("nd-build");
   const auto& N = nd.nd;
   const int nn = (int)N.size();
   auto& g = h->ndd;
@@ -770,31 +792,62 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
     for (int x : g.lvl[lv])
       if (N[x].child.size() > 2) return fail(h, TCG_EINVAL, "nested dissection: more than 2 children");
   }
+  hm.mark("levels");
   // S^s -> frontal scatter maps (one entry per (a, b) of each patch, -1 = counted elsewhere)
   {
-    std::vector<int64_t> moff(pl.npatch + 1, 0), map;
+    std::vector<int64_t> moff(pl.npatch + 1, 0);
+    for (int s2 = 0; s2 < pl.npatch; ++s2) {
+      const int np2 = (int)pl.pp[s2].p_grp.size();
+      moff[s2 + 1] = moff[s2] + (int64_t)np2 * np2;
+    }
+    std::vector<int64_t> map(std::max<int64_t>(moff[pl.npatch], 1), -1);
+    // entries bucketed by the front that receives them (the node eliminating the first of the
+    // two groups), then resolved per node through a dense group -> frontal position table
+    std::vector<int64_t> boffs(nn + 1, 0);
     for (int s2 = 0; s2 < pl.npatch; ++s2) {
       const auto& grp = pl.pp[s2].p_grp;
-      const int np2 = (int)grp.size();
-      moff[s2 + 1] = moff[s2] + (int64_t)np2 * np2;
-      for (int a = 0; a < np2; ++a)
-        for (int b = 0; b < np2; ++b) {
-          const int ga = grp[a], gb = grp[b];
-          if (ga < gb) {
-            map.push_back(-1);
-            continue;
-          }
-          const int x = std::min(nd.node_of[ga], nd.node_of[gb]);  // postorder: descendant first
-          const int fa2 = nd.fpos(x, ga), fb2 = nd.fpos(x, gb);
-          if (fa2 < 0 || fb2 < 0) return fail(h, TCG_EINVAL, "nested dissection: coupled pair outside a front");
-          const int r = std::max(fa2, fb2), c = std::min(fa2, fb2);
-          map.push_back(aoff[x] + tri_off(r >> 6, c >> 6) + (int64_t)(r & 63) * TS + (c & 63));
-        }
+      for (int ga : grp)
+        for (int gb : grp)
+          if (ga >= gb) ++boffs[std::min(nd.node_of[ga], nd.node_of[gb]) + 1];
     }
-    if (map.empty()) map.push_back(-1);
+    for (int x = 0; x < nn; ++x) boffs[x + 1] += boffs[x];
+    struct Ent {
+      int64_t e;
+      int ga, gb;
+    };
+    std::vector<Ent> ents(std::max<int64_t>(boffs[nn], 1));
+    {
+      std::vector<int64_t> fill(boffs.begin(), boffs.end() - 1);
+      for (int s2 = 0; s2 < pl.npatch; ++s2) {
+        const auto& grp = pl.pp[s2].p_grp;
+        const int np2 = (int)grp.size();
+        for (int a = 0; a < np2; ++a)
+          for (int b = 0; b < np2; ++b) {
+            const int ga = grp[a], gb = grp[b];
+            if (ga < gb) continue;
+            const int x = std::min(nd.node_of[ga], nd.node_of[gb]);  // postorder: descendant first
+            ents[fill[x]++] = Ent{moff[s2] + (int64_t)a * np2 + b, ga, gb};
+          }
+      }
+    }
+    std::vector<int> pos(std::max<int64_t>(pl.nc, 1), -1);
+    for (int x = 0; x < nn; ++x) {
+      if (boffs[x] == boffs[x + 1]) continue;
+      for (size_t i = 0; i < N[x].V.size(); ++i) pos[N[x].V[i]] = (int)i;
+      for (size_t i = 0; i < N[x].B.size(); ++i) pos[N[x].B[i]] = 64 * N[x].TV + (int)i;
+      for (int64_t q = boffs[x]; q < boffs[x + 1]; ++q) {
+        const int fa2 = pos[ents[q].ga], fb2 = pos[ents[q].gb];
+        if (fa2 < 0 || fb2 < 0) return fail(h, TCG_EINVAL, "nested dissection: coupled pair outside a front");
+        const int r = std::max(fa2, fb2), c = std::min(fa2, fb2);
+        map[ents[q].e] = aoff[x] + tri_off(r >> 6, c >> 6) + (int64_t)(r & 63) * TS + (c & 63);
+      }
+      for (int g2 : N[x].V) pos[g2] = -1;
+      for (int g2 : N[x].B) pos[g2] = -1;
+    }
     TRY(dupload(h, &g.moff, moff));
     TRY(dupload(h, &g.map, map));
   }
+  hm.mark("scatter-maps");
   // extend-add maps and forward gather programs
   std::vector<int64_t> xo(nn + 1, 0);
   std::vector<int> ext;
@@ -844,6 +897,7 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
   TRY(dupload(h, &g.prog, prog));
   TRY(dupload(h, &g.vl, vl));
   TRY(dupload(h, &g.bl, bl));
+  hm.mark("extend+programs");
   // stepper items: forward rows (x, I < T) and backward V columns (x, J < TV), per level, LPT
   const int nb2 = h->nbr;
   int64_t npb = 0;
@@ -975,25 +1029,6 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
 }
 
 static tcg_status open_peer_tables(tcg_ctx* h, std::vector<std::vector<void*>>& bufs_by_rank);
-
-// host-side timeline of do_setup (TCG_HOST_TIMING=1: one line on stderr per setup)
-struct HostMarks {
-  bool on = getenv("TCG_HOST_TIMING") && atoi(getenv("TCG_HOST_TIMING")) != 0;
-  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
-  std::string line;
-  void mark(const char* what) {
-    if (!on) return;
-    const auto t = std::chrono::steady_clock::now();
-    char b[96];
-    snprintf(b, sizeof b, " %s %.3f", what, std::chrono::duration<double, std::milli>(t - last).count());
-    line += b;
-    last = t;
-  }
-  ~HostMarks() {
-    if (on) fprintf(stderr, "[tcg host ms]%s total %.3f\n", line.c_str(),
-                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-  }
-};
 
 static tcg_status do_setup(tcg_ctx* h) {
   HostMarks hm;
