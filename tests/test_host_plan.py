@@ -53,6 +53,12 @@ def test_argument_validation(tcg):
     with pytest.raises(tcg.TcgError) as e:
         s.plan()                                   # materials/time missing
     assert e.value.status == tcg.TCG_ESTATE
+    for k in (-1, 5):                              # warm-start subspace 0..4 (R20)
+        with pytest.raises(tcg.TcgError) as e:
+            s.set_warm_start(k)
+        assert e.value.status == tcg.TCG_EINVAL
+    s.set_warm_start(4)
+    s.set_warm_start(0)
     s.set_materials([1.0, 0.0], [1.0, 1.0])
     s.set_time(1.0, 4)
     s.plan()
