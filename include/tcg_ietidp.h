@@ -153,8 +153,9 @@ tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, 
  * iteration). The stopping reference stays sqrt(d^T M^-1 d) (the cold r0^T z0), so warm and
  * cold runs stop at one absolute residual; a step whose start already meets it takes 0
  * iterations; d = 0 gives lambda = 0. tcg_refactor restarts the history (step 0 is cold).
- * Takes effect from the next tcg_step; device memory (2k+1 lambda-length vectors per rank)
- * is allocated then. EINVAL unless 0 <= k <= 4. */
+ * Takes effect from the next tcg_step; changing k restarts the history (the next step is
+ * cold), as does tcg_refactor. Device memory (2k+1 lambda-length vectors per rank) is
+ * allocated at the first warm step. EINVAL unless 0 <= k <= 4. */
 tcg_status tcg_set_warm_start(tcg_handle h, int k);
 
 /* Host-only planning (no CUDA): topology, ranked-Kruskal tree, e/p/r partition,

@@ -187,6 +187,7 @@ struct tcg_ctx {
   int cache_items = 0, cache_lam = 0, cache_pcprog = 0;
   int npf = 0;  // prefetched tiles per phase (stepper)
   int warm = 0;  // warm-start subspace dimension k (tcg_set_warm_start), 0 = off
+  int64_t warm_base = 0;  // first step of the current warm-start history (k changed / refactor)
   int64_t* d_pcprog = nullptr;
   size_t smem_steps = 0;  // dynamic shared memory of k_steps: item scratch + caches
   int coarse_ch = 1, coarse_maxch = 1;
@@ -592,6 +593,7 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
   cudaEventDestroy(e2);
   cudaEventDestroy(e3);
   h->steps_done = 0;
+  h->warm_base = 0;  // refactor / setup: the time integration restarts, so does the warm history
   h->hist_len = 0;
   h->total_iters = 0;
   h->iters.clear();
@@ -1751,6 +1753,7 @@ static StepArgs step_args(tcg_ctx* h) {
   A.scratch = (int)(h->smem_pcg / sizeof(double));
   A.npf = h->npf;
   A.warm = h->warm;
+  A.warm_base = (int)h->warm_base;
   for (auto& R : h->rd) {
     A.Wr[R.r] = R.Wr;
     A.FWr[R.r] = R.FWr;
@@ -1979,6 +1982,7 @@ tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, 
 tcg_status tcg_set_warm_start(tcg_handle h, int on) {
   if (!h) return TCG_EINVAL;
   if (on < 0 || on > KW) return fail(h, TCG_EINVAL, "warm start subspace dimension must be in [0, " + std::to_string(KW) + "]");
+  if (on != h->warm) h->warm_base = h->steps_done;  // a new subspace size restarts the history
   h->warm = on;
   return TCG_OK;
 }

@@ -100,6 +100,7 @@ struct StepArgs {
   int mode;         // 0: nsteps implicit-Euler steps; 1: nsteps applications q = F p (p = pk[0], q -> r[1])
   int dbg_stop;     // debug: 1 = return after the first step's R3 coarse solve
   int warm;         // k > 0: PCG starts from the Galerkin projection on the previous k solutions (f2)
+  int warm_base;        // warm start: history starts at this step (set when k changes; refactor: 0)
   double* Wr[MAXR];     // warm start: ring of the previous k solutions (slot = global step % k), own rank
   double* FWr[MAXR];    // and of d_j - r_j (= F W_j up to the tolerance)
   double* dsave[MAXR];  // this step's d (lambda level)
@@ -1181,7 +1182,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
     // (warm start: rho0 = d^T M^-1 d stays the reference of the stopping rule, so warm and
     // cold runs share one absolute target)
-    const int nW = A.warm ? min(A.step0 + step, A.warm) : 0;
+    const int nW = A.warm ? max(0, min(A.step0 + step - A.warm_base, A.warm)) : 0;
     double rho0;
     {
       double loc = 0.0;

@@ -423,3 +423,25 @@ def test_warm_start_with_sparse_coarse(tcg, sparse_coarse):
     pr = copy.deepcopy(workloads.cfg2())
     pr.warm_start = 4
     compare(tcg, pr, steps=5)
+
+
+def test_warm_start_k_change_restarts_history(tcg):
+    """Changing the warm-start subspace mid-run restarts the history: the next step starts
+    cold (its iteration count equals a cold step's), and the run still matches the oracle's
+    cold solution to the tolerance."""
+    pr = copy.deepcopy(workloads.cfg1())
+    o = Oracle(copy.deepcopy(pr))
+    o.run(6)
+    s = tcg.Solver().configure(pr)
+    s.setup()
+    s.set_warm_start(4)
+    s.step(3)
+    s.set_warm_start(2)
+    s.step(3)
+    it = list(s.history()[0])
+    a1 = s.coefficients(1)
+    s.close()
+    assert abs(it[3] - o.iters[3]) <= 1, (it, o.iters)  # step 3 is cold again
+    assert it[4] < o.iters[4] or it[5] < o.iters[5], (it, o.iters)
+    ref = o.coefficients(1)
+    assert np.linalg.norm(a1 - ref) / np.linalg.norm(ref) <= TOL
