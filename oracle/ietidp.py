@@ -76,17 +76,68 @@ def chol_skip_solve(G, b, tol=1e-12):
     return c
 
 
+def patch_box(prob, s):
+    """Axis-aligned box of patch s = ix + Px (iy + Py iz) in the uniform patch grid."""
+    ix = s % prob.npatch[0]
+    iy = (s // prob.npatch[0]) % prob.npatch[1]
+    iz = s // (prob.npatch[0] * prob.npatch[1])
+    idx = (ix, iy, iz)
+    lo = [prob.lo[d] + (prob.hi[d] - prob.lo[d]) * idx[d] / prob.npatch[d] for d in range(3)]
+    hi = [prob.lo[d] + (prob.hi[d] - prob.lo[d]) * (idx[d] + 1) / prob.npatch[d] for d in range(3)]
+    return lo, hi
+
+
+def local_operators(prob, s, r, pl, ni, dt, lean=False):
+    """Per-patch setup (P:L83-87 assembly, P:L133 W^ = K + M/dt, P:L154 local Schur
+    complement): element-loop K, M, j_S of patch s; W^ = nu K + (sigma/dt) M restricted to
+    r = [i; b] (local ids `r`) and to the primal DOFs `pl`; Cholesky of W_rr and W_ii;
+    Phi = W_rr^-1 W_rp; S^s = W_pp - W_pr Phi. lean=True keeps only what the time stepping
+    needs (no K / full W; the blocks of W that are only multiplied with, and M, in sparse
+    storage; M dropped for insulators, where it is zero) -- storage only, same operators.
+    Module-level so that a process pool can run it patch by patch."""
+    lo, hi = patch_box(prob, s)
+    sp = assembly.PatchSpace(prob.p, prob.elems, lo, hi)
+    K, M, jS = assembly.assemble_patch(sp, prob.nu[s], prob.sigma[s], prob.source)
+    W = K + M / dt
+    Wrr = W[np.ix_(r, r)]
+    cf = _chol(Wrr, f"W_rr patch {s}")
+    Wrp = W[np.ix_(r, pl)]
+    Wpp = W[np.ix_(pl, pl)]
+    Phi = _solve(cf, Wrp) if cf is not None else np.zeros_like(Wrp)
+    Ss = Wpp - Wrp.T @ Phi
+    Wii_cf = _chol(Wrr[:ni, :ni], f"W_ii patch {s}")
+    out = dict(Wrr_cf=cf, Wii_cf=Wii_cf, Wrp=Wrp, Wpp=Wpp, Phi=Phi, Ss=Ss, Wbb=Wrr[ni:, ni:], Wbi=Wrr[ni:, :ni],
+               Wdiag=np.diag(W).copy(), jS=jS, K=K, M=M, Wfull=W)
+    if lean:
+        import scipy.sparse as sps
+        out.update(K=None, Wfull=None, Wpp=None, M=sps.csr_matrix(M) if prob.sigma[s] > 0 else None,
+                   Wrp=sps.csr_matrix(Wrp), Wbb=sps.csr_matrix(out["Wbb"]), Wbi=sps.csr_matrix(out["Wbi"]))
+    return out
+
+
+def _local_job(args):
+    return local_operators(*args)
+
+
 class Oracle:
-    def __init__(self, prob, assemble=True):
+    """workers > 1 runs the per-patch work (assembly + local factorisations in a process
+    pool, the local solves of every F / preconditioner / step in a thread pool; LAPACK
+    releases the GIL) and lean=True drops storage the stepping never reads (see
+    local_operators). Neither changes the operators; sums over patches keep patch order."""
+
+    def __init__(self, prob, assemble=True, workers=1, lean=False):
         self.prob = prob
         P = prob.n_patches
+        self.workers = max(1, int(workers))
+        self.lean = lean
+        self._tp = None
         self.topo = topology.Topology(prob.npatch, prob.p, prob.elems, prob.sigma)
         self.tree = gauge.build_tree(self.topo, prob.tree_order)
         self.part = gauge.Partition(self.topo, self.tree)
         self.dt = prob.T / prob.n_steps
+        self._index_tables()
         if assemble:
-            self._assemble()
-            self._factor()
+            self._setup_locals()
         self.a = [np.zeros(self.topo.l2g.shape[1]) for _ in range(P)]
         self.ell = 0
         self.iters = []
@@ -95,60 +146,67 @@ class Oracle:
 
     # ---- setup -------------------------------------------------------------------
     def patch_box(self, s):
-        pr = self.prob
-        ix = s % pr.npatch[0]
-        iy = (s // pr.npatch[0]) % pr.npatch[1]
-        iz = s // (pr.npatch[0] * pr.npatch[1])
-        idx = (ix, iy, iz)
-        lo = [pr.lo[d] + (pr.hi[d] - pr.lo[d]) * idx[d] / pr.npatch[d] for d in range(3)]
-        hi = [pr.lo[d] + (pr.hi[d] - pr.lo[d]) * (idx[d] + 1) / pr.npatch[d] for d in range(3)]
-        return lo, hi
+        return patch_box(self.prob, s)
 
-    def _assemble(self):
-        pr = self.prob
-        self.K, self.M, self.jS = [], [], []
-        for s in range(pr.n_patches):
-            lo, hi = self.patch_box(s)
-            sp = assembly.PatchSpace(pr.p, pr.elems, lo, hi)
-            K, M, jS = assembly.assemble_patch(sp, pr.nu[s], pr.sigma[s], pr.source)
-            self.K.append(K)
-            self.M.append(M)
-            self.jS.append(jS)
+    def _map(self, fn, items):
+        """[fn(x) for x in items], on the thread pool when workers > 1 (results in order)."""
+        if self.workers == 1:
+            return [fn(x) for x in items]
+        if self._tp is None:
+            from concurrent.futures import ThreadPoolExecutor
+            self._tp = ThreadPoolExecutor(self.workers)
+        return list(self._tp.map(fn, items))
 
-    def W(self, s):
-        """W^_s = nu_s K_s + (sigma_s/dt) M_s (K, M carry nu, sigma)."""
-        return self.K[s] + self.M[s] / self.dt
-
-    def _factor(self):
+    def _index_tables(self):
+        """Flat positions of the two local copies of every multiplier (B_s entries)
+        in the concatenation of the patches' r vectors."""
         pt = self.part
         P = self.prob.n_patches
-        self.Wrr_cf, self.Wii_cf, self.Wrp, self.Wpp, self.Phi, self.Wbb, self.Wbi, self.Wfull = [], [], [], [], [], [], [], []
+        self.r_off = np.zeros(P + 1, dtype=np.int64)
+        for s in range(P):
+            self.r_off[s + 1] = self.r_off[s] + len(pt.r_i[s]) + len(pt.r_b[s])
+        if pt.m:
+            self.pos_plus = self.r_off[pt.lam_plus[:, 0]] + pt.lam_plus[:, 1]
+            self.pos_minus = self.r_off[pt.lam_minus[:, 0]] + pt.lam_minus[:, 1]
+        else:
+            self.pos_plus = self.pos_minus = np.zeros(0, dtype=np.int64)
+
+    def _setup_locals(self):
+        pr = self.prob
+        pt = self.part
+        P = pr.n_patches
+        jobs = [(pr, s, pt.r_order(s), pt.p_loc[s], len(pt.r_i[s]), self.dt, self.lean) for s in range(P)]
+        names = ("Wrr_cf", "Wii_cf", "Wrp", "Wpp", "Phi", "Wbb", "Wbi", "Wdiag", "jS", "K", "M", "Wfull")
+        for n in names:
+            setattr(self, n, [])
         nc = pt.nc
         Spp = np.zeros((nc, nc))
-        for s in range(P):
-            W = self.W(s)
-            r = pt.r_order(s)
-            pl = pt.p_loc[s]
-            Wrr = W[np.ix_(r, r)]
-            cf = _chol(Wrr, f"W_rr patch {s}")
-            Wrp = W[np.ix_(r, pl)]
-            Wpp = W[np.ix_(pl, pl)]
-            Phi = _solve(cf, Wrp) if cf is not None else np.zeros_like(Wrp)
-            Ss = Wpp - Wrp.T @ Phi
+        if self.workers == 1:
+            results = map(_local_job, jobs)
+            pool = None
+        else:
+            import multiprocessing as mp
+            from threadpoolctl import threadpool_limits
+            self._limits = threadpool_limits(1)   # one BLAS thread per pool worker
+            pool = mp.get_context("fork").Pool(self.workers)
+            results = pool.imap(_local_job, jobs, chunksize=1)
+        for s, loc in enumerate(results):       # patch order: the S_pp sums are ordered
             g = pt.p_grp[s]
-            Spp[np.ix_(g, g)] += Ss
-            ni = len(pt.r_i[s])
-            Wii = Wrr[:ni, :ni]
-            self.Wii_cf.append(_chol(Wii, f"W_ii patch {s}"))
-            self.Wbb.append(Wrr[ni:, ni:])
-            self.Wbi.append(Wrr[ni:, :ni])
-            self.Wrr_cf.append(cf)
-            self.Wrp.append(Wrp)
-            self.Wpp.append(Wpp)
-            self.Phi.append(Phi)
-            self.Wfull.append(W)
+            Spp[np.ix_(g, g)] += loc["Ss"]
+            for n in names:
+                getattr(self, n).append(loc[n])
+        if pool is not None:
+            pool.close()
+            pool.join()
         self.Spp = Spp
-        self.Spp_cf = _chol(Spp, "coarse S_pp")
+        if self.workers > 1:
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(self.workers):
+                self.Spp_cf = _chol(Spp, "coarse S_pp")
+        else:
+            self.Spp_cf = _chol(Spp, "coarse S_pp")
+        if self.lean:
+            self.Spp = None
         # rho-scaling weights (DESIGN.md R5): rho_s = W^_s diagonal at the b-DOF
         m = pt.m
         self.wplus = np.ones(m)
@@ -159,35 +217,38 @@ class Oracle:
                 sm, am = pt.lam_minus[k]
                 lp = pt.r_order(sp)[ap]
                 lm = pt.r_order(sm)[am]
-                rp = self.Wfull[sp][lp, lp]
-                rm = self.Wfull[sm][lm, lm]
+                rp = self.Wdiag[sp][lp]
+                rm = self.Wdiag[sm][lm]
                 self.wplus[k] = rm / (rp + rm)
                 self.wminus[k] = rp / (rp + rm)
+
+    def W(self, s):
+        """W^_s = nu_s K_s + (sigma_s/dt) M_s (K, M carry nu, sigma)."""
+        return self.K[s] + self.M[s] / self.dt
+
+    def Ma(self, s, a):
+        """M_s a (zero for an insulator whose M is not stored, lean mode)."""
+        M = self.M[s]
+        return np.zeros_like(a) if M is None else M @ a
 
     # ---- operators ---------------------------------------------------------------
     def nr(self, s):
         return len(self.part.r_i[s]) + len(self.part.r_b[s])
 
     def Bt(self, lam, wp=None, wm=None):
-        """Per-patch v_s = B_s^T lam (optionally weighted: B_D^(s)T)."""
-        pt = self.part
-        v = [np.zeros(self.nr(s)) for s in range(self.prob.n_patches)]
-        for k in range(pt.m):
-            sp, ap = pt.lam_plus[k]
-            sm, am = pt.lam_minus[k]
-            v[sp][ap] += lam[k] * (1.0 if wp is None else wp[k])
-            v[sm][am] -= lam[k] * (1.0 if wm is None else wm[k])
-        return v
+        """Per-patch v_s = B_s^T lam (optionally weighted: B_D^(s)T): the multiplier k adds
+        +lam_k at its lower patch's copy and -lam_k at the other (R4)."""
+        flat = np.zeros(self.r_off[-1])
+        np.add.at(flat, self.pos_plus, lam * (1.0 if wp is None else wp))
+        np.add.at(flat, self.pos_minus, -(lam * (1.0 if wm is None else wm)))
+        return [flat[self.r_off[s]:self.r_off[s + 1]] for s in range(self.prob.n_patches)]
 
     def Bj(self, y, wp=None, wm=None):
         """(B y)_k = y_{s+}[a+] - y_{s-}[a-] (optionally weighted)."""
-        pt = self.part
-        out = np.zeros(pt.m)
-        for k in range(pt.m):
-            sp, ap = pt.lam_plus[k]
-            sm, am = pt.lam_minus[k]
-            out[k] = y[sp][ap] * (1.0 if wp is None else wp[k]) - y[sm][am] * (1.0 if wm is None else wm[k])
-        return out
+        if self.part.m == 0:
+            return np.zeros(0)
+        flat = np.concatenate(y)
+        return flat[self.pos_plus] * (1.0 if wp is None else wp) - flat[self.pos_minus] * (1.0 if wm is None else wm)
 
     def NT(self, vecs):
         """sum_s N_s^T v_s (v_s indexed by the patch's primal DOFs)."""
@@ -200,7 +261,7 @@ class Oracle:
         """F lam = B W_rr^-1 B^T lam + B Phi N S_pp^-1 N^T Phi^T B^T lam."""
         P = self.prob.n_patches
         v = self.Bt(lam)
-        u = [_solve(self.Wrr_cf[s], v[s]) for s in range(P)]
+        u = self._map(lambda s: _solve(self.Wrr_cf[s], v[s]), range(P))
         g = self.NT([self.Phi[s].T @ v[s] for s in range(P)])
         pc = _solve(self.Spp_cf, g)
         y = [u[s] + self.Phi[s] @ pc[self.part.p_grp[s]] for s in range(P)]
@@ -218,12 +279,13 @@ class Oracle:
         pt = self.part
         P = self.prob.n_patches
         v = self.Bt(r, self.wplus, self.wminus)
-        w = []
-        for s in range(P):
+
+        def one(s):
             ni = len(pt.r_i[s])
             ws = np.zeros(self.nr(s))
             ws[ni:] = self.Sbb_apply(s, v[s][ni:])
-            w.append(ws)
+            return ws
+        w = self._map(one, range(P))
         return self.Bj(w, self.wplus, self.wminus)
 
     # ---- time step ---------------------------------------------------------------
@@ -293,10 +355,10 @@ class Oracle:
         f = []
         for s in range(P):
             js = load[s] if load is not None else self.source_factor(s, t) * self.jS[s]
-            f.append(self.M[s] @ self.a[s] / self.dt + js)
+            f.append(self.Ma(s, self.a[s]) / self.dt + js)
         fr = [f[s][pt.r_order(s)] for s in range(P)]
         fp = [f[s][pt.p_loc[s]] for s in range(P)]
-        x1 = [_solve(self.Wrr_cf[s], fr[s]) for s in range(P)]
+        x1 = self._map(lambda s: _solve(self.Wrr_cf[s], fr[s]), range(P))
         h = [self.Wrp[s].T @ x1[s] for s in range(P)]
         fpg = self.NT(fp)
         p0 = _solve(self.Spp_cf, fpg - self.NT(h))
@@ -310,12 +372,13 @@ class Oracle:
             self.warm_FW = (self.warm_FW + [d - r])[-kw:]
         v = self.Bt(lam)
         pc = _solve(self.Spp_cf, fpg - self.NT([h[s] - self.Phi[s].T @ v[s] for s in range(P)]))
-        for s in range(P):
+        def recover(s):
             ar = _solve(self.Wrr_cf[s], fr[s] - v[s] - self.Wrp[s] @ pc[pt.p_grp[s]])
             a = np.zeros(self.topo.l2g.shape[1])
             a[pt.r_order(s)] = ar
             a[pt.p_loc[s]] = pc[pt.p_grp[s]]
-            self.a[s] = a
+            return a
+        self.a = self._map(recover, range(P))
         self.lam = lam
         self.pc = pc
         self.ell += 1

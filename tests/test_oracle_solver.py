@@ -5,6 +5,7 @@ same discrete system), the block 3x3 Euler system residual (P12), gauge invarian
 of curl-related quantities (P13), closed-form degenerate cases (P14), a manufactured
 exact discrete solution (P15) and manufactured-solution convergence rates of the
 paper's error measures (P16)."""
+import copy
 import math
 
 import numpy as np
@@ -291,3 +292,70 @@ def test_mms_time_rate():
         errs.append(math.sqrt(tot))
     rates = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
     assert all(abs(r - 1.0) <= 0.15 for r in rates), (errs, rates)
+
+
+# ---- rho-scaling pins (R5 / SURVEY Q5; the paper's preconditioner P:L170, scaling as
+# outlook P:L550). Textbook property of the coefficient-scaled Dirichlet preconditioner: the
+# weight of side s at a multiplier joining s and t is rho_t / (rho_s + rho_t) (the OTHER side's
+# coefficient), which makes kappa(M^-1 F) robust to coefficient jumps; unscaled (or swapped)
+# weights let it grow with the contrast.
+
+def _kappa(o):
+    ev = np.real(sla.eigvals(o.dense_precond() @ o.dense_F()))
+    assert ev.min() > 0
+    return ev.max() / ev.min()
+
+
+def test_rho_scaling_robust_to_contrast():
+    """Pin of the rho weights: on the contrast case (sigma 1e6 / nu 1e-3 jumps) the scaled
+    kappa is <= 10 while the unscaled one is >= 1e3 times larger; swapping w+ and w- (a
+    plausible index mistake) gives kappa ~ 3e7 and fails the first bar."""
+    pr = next(p for p in SMALL if p.name == "contrast")
+    k_rho = _kappa(_o(copy.deepcopy(pr), scaling=1))
+    k_none = _kappa(_o(copy.deepcopy(pr), scaling=0))
+    assert k_rho <= 10.0, k_rho
+    assert k_none >= 1e3 * k_rho, (k_none, k_rho)
+    # swapped weights, to show the pin discriminates
+    o = _o(copy.deepcopy(pr), scaling=1)
+    o.wplus, o.wminus = o.wminus.copy(), o.wplus.copy()
+    assert _kappa(o) > 1e3
+
+
+def test_rho_scaling_kappa_flat_in_contrast():
+    """Growing the conductor's sigma by 1e4 leaves the rho-scaled kappa within a factor 2."""
+    ks = []
+    for sig in (1e2, 1e6):
+        pr = workloads.custom((2, 2, 1), 3, (2, 2, 2), [sig, 0, sig, 0], [1e-3, 1, 1, 1e-2], name="contrast")
+        ks.append(_kappa(_o(pr, scaling=1)))
+    assert max(ks) <= 2.0 * min(ks), ks
+
+
+def test_rho_scaling_equal_coefficients_is_quarter_of_unscaled():
+    """with the same coefficient on both sides of every multiplier the rho weights
+    are 1/2, so M^-1 (rho) = M^-1 (none) / 4 and PCG, invariant to scaling the
+    preconditioner, produces the same iterates and iteration counts."""
+    pr = workloads.custom((2, 2, 2), 2, (2, 2, 2), [0.0] * 8, [1.0] * 8, n_steps=3, name="uniform")
+    o1 = _o(copy.deepcopy(pr), scaling=1)
+    o0 = _o(copy.deepcopy(pr), scaling=0)
+    assert np.allclose(o1.wplus, 0.5, rtol=1e-14, atol=0) and np.allclose(o1.wminus, 0.5, rtol=1e-14, atol=0)
+    M1, M0 = o1.dense_precond(), o0.dense_precond()
+    assert np.max(np.abs(M1 - 0.25 * M0)) <= 1e-14 * np.max(np.abs(M0))
+    o1.run(3)
+    o0.run(3)
+    assert o1.iters == o0.iters
+    a1, a0 = o1.coefficients(1), o0.coefficients(1)
+    assert np.linalg.norm(a1 - a0) <= 1e-12 * np.linalg.norm(a0)
+
+
+def test_lean_parallel_oracle_equals_plain():
+    """tools/make_golden.py runs Oracle(workers=N, lean=True): the same operators with the
+    per-patch work on a pool and sparse storage of the blocks that are only multiplied with;
+    only the rounding order of those products differs."""
+    for pr, tol in ((workloads.cfg1(), 1e-10), (SMALL[4], 1e-9)):
+        pr = copy.deepcopy(pr)
+        pr.n_steps = min(pr.n_steps, 4)
+        a = Oracle(copy.deepcopy(pr)).run()
+        b = Oracle(copy.deepcopy(pr), workers=3, lean=True).run()
+        x, y = a.coefficients(1), b.coefficients(1)
+        assert np.linalg.norm(x - y) <= tol * np.linalg.norm(x)
+        assert a.iters == b.iters
