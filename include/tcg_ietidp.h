@@ -105,7 +105,9 @@ typedef struct tcg_info {
   double coarse_factor_bytes; /* bytes of the coarse inverse factors read per coarse solve   */
 } tcg_info;
 
-/* Create a handle. device: CUDA ordinal used by setup; rank/world: this process's place
+/* Create a handle (the solver object of BASELINE.json north_star "build patches, materials
+ * and source; setup and factorise; step(n); read coefficients A and residual history";
+ * SURVEY §8(b)). device: CUDA ordinal used by setup; rank/world: this process's place
  * in the job (world=1 for one GPU, world <= 8); nccl_id: 128-byte ncclUniqueId when world > 1
  * (NULL iff world == 1), used only to bootstrap (CUDA IPC handles of every rank's buffers are
  * all-gathered; the solve itself reads/writes peer memory over NVLink inside one persistent
@@ -123,27 +125,48 @@ tcg_status tcg_nccl_unique_id(unsigned char* out);
  * two-level barrier as a multi-GPU job). Requires world == 1; call before tcg_plan. */
 tcg_status tcg_set_virtual_ranks(tcg_handle h, int vranks);
 
-/* Uniform box grid of npatch[0] x npatch[1] x npatch[2] patches on [lo,hi], spline degree
- * p >= 1 and elems[d] >= 1 elements per patch per direction. */
+/* Multipatch domain (P:L56-60 Omega = union of patches Omega^(i), each the image of the unit
+ * cube; P:L74-77 spline edge spaces of degrees (p-1,p,p) cyclic on each patch): a uniform box
+ * grid of npatch[0] x npatch[1] x npatch[2] axis-aligned patches on [lo,hi] (identity
+ * geometry maps), spline degree p >= 1, elems[d] >= 1 elements per patch per direction
+ * (S:L124-152). Errors: TCG_EINVAL (null, p < 1, counts < 1, lo >= hi), TCG_ESTATE (after
+ * plan/setup). Arrays are read during the call only. */
 tcg_status tcg_set_patches(tcg_handle h, const int npatch[3], const double lo[3], const double hi[3],
                            int degree_p, const int elems[3]);
 
-/* Per-patch conductivity sigma >= 0 (0 = insulator) and reluctivity nu > 0, n = #patches
- * (sigma = 0 in Omega_I, nu bounded away from 0). */
+/* Materials (Omega = Omega_C u Omega_I with sigma > 0 in the conductor and sigma = 0
+ * in the insulator; nu > 0 bounded, piecewise constant; here constant per patch):
+ * sigma[n] >= 0, nu[n] > 0, finite, n = #patches in patch-id order (copied during the call).
+ * Errors: TCG_EINVAL (length, range), TCG_ESTATE (before set_patches, after plan/setup). */
 tcg_status tcg_set_materials(tcg_handle h, const double* sigma, const double* nu, size_t n);
 
-/* Source kind (TCG_SOURCE_*). Default TCG_SOURCE_CURL_PSI. */
-tcg_status tcg_set_source(tcg_handle h, int kind);
+/* Source current density J of the eddy-current problem (P:L42 right-hand side of eq.
+ * formA*; its Galerkin load j_i = <J_i, w_j>): J(x,t) = amp * phi_s(t) * S(x) with
+ * kind (TCG_SOURCE_*) and params[nparams] (NULL/0 = defaults, copied during the call):
+ *   TCG_SOURCE_CURL_PSI  params {amp = 1, freq = 1}: phi = sin(2 pi freq t)
+ *   TCG_SOURCE_MMS       params {amp = 1}
+ *   TCG_SOURCE_NONE      no params (J = 0)
+ * Default: TCG_SOURCE_CURL_PSI with amp = freq = 1 (the BASELINE.json configs).
+ * Errors: TCG_EINVAL (unknown kind, too many params, non-finite), TCG_ESTATE (after setup). */
+tcg_status tcg_set_source(tcg_handle h, int kind, const double* params, size_t nparams);
 
-/* Time interval (0,T], n_steps implicit-Euler steps, dt = T/n_steps, A(0) = 0. */
+/* Time grid of the implicit Euler method (eq. euler: W a^(l+1) = f^(l+1) with
+ * W = M + dt K, f^(l+1) = M a^(l) + dt j^(l+1)): interval (0,T], n_steps uniform steps,
+ * dt = T/n_steps, A(0) = 0. Errors: TCG_EINVAL (T <= 0, n_steps < 1), TCG_ESTATE (after setup). */
 tcg_status tcg_set_time(tcg_handle h, double T, int n_steps);
 
-/* PCG stopping rule sqrt(r^T z) <= rtol sqrt(r0^T z0), max_iter (ENOCONV beyond);
- * scaling TCG_SCALING_*; tree_order 0: ascending edge ids within a Kruskal rank,
- * 1: descending (gauge-invariance test). Defaults 1e-10, 5000, RHO, 0. */
+/* Solver parameters: PCG on the multipliers with the Dirichlet preconditioner (P:L170,
+ * "PCG tolerance" P:L544); stopping rule sqrt(r^T z) <= rtol sqrt(r0^T z0) (R6),
+ * max_iter (a step that reaches it fails the call with TCG_ENOCONV); scaling TCG_SCALING_*
+ * (P:L170 none, R5 rho); tree_order of the tree-cotree gauge (0: ascending
+ * edge ids within a Kruskal rank, 1: descending, the gauge-invariance test; R2).
+ * Defaults 1e-10, 5000, RHO, 0. Errors: TCG_EINVAL (rtol <= 0, max_iter < 1, unknown
+ * scaling/order), TCG_ESTATE (after plan/setup). */
 tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, int tree_order);
 
-/* Warm start (the paper's outlook P:L550 on cheaper PCG; R20).
+/* Collective on world > 1 handles: every rank must make the same calls at the same step (each
+ * tcg_step checks the agreement over NCCL and fails with TCG_EINVAL otherwise).
+ * Warm start (the paper's outlook P:L550 on cheaper PCG; R20).
  * k = 0 (default): the paper's lambda0 = 0. k in 1..4: from step 1 on the PCG starts from the
  * Galerkin projection of the step's solution on the span of the previous k solutions W_j:
  * lambda0 = sum_j c_j W_j, G c = W^T d, G_ij = (W_i^T FW_j + W_j^T FW_i)/2 with FW_j = d_j - r_j
@@ -154,8 +177,8 @@ tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, 
  * cold runs stop at one absolute residual; a step whose start already meets it takes 0
  * iterations; d = 0 gives lambda = 0. tcg_refactor restarts the history (step 0 is cold).
  * Takes effect from the next tcg_step; changing k restarts the history (the next step is
- * cold), as does tcg_refactor. Device memory (2k+1 lambda-length vectors per rank) is
- * allocated at the first warm step. EINVAL unless 0 <= k <= 4. */
+ * cold), as does tcg_refactor. Device memory (2*4+1 = 9 lambda-length vectors per rank,
+ * sized for the largest k) is allocated at the first warm step. EINVAL unless 0 <= k <= 4. */
 tcg_status tcg_set_warm_start(tcg_handle h, int k);
 
 /* Host-only planning (no CUDA): topology, ranked-Kruskal tree, e/p/r partition,
@@ -165,29 +188,45 @@ tcg_status tcg_plan(tcg_handle h);
 /* Copy a plan array (TCG_PLAN_*) into out[len] (int64). Requires tcg_plan. */
 tcg_status tcg_get_plan(tcg_handle h, int what, int64_t* out, size_t len);
 
-/* Collective: plan (if needed), device assembly of W^_s = nu_s K_s + sigma_s/dt M_s,
- * batched FP64 Cholesky, coarse problem assembly and factorisation. */
+/* Collective: plan (if needed), device assembly of W^_s = nu_s K_s + sigma_s/dt M_s
+ * (P:L83-87 K_i, M_C, j_i; P:L133 W), batched FP64 Cholesky of the gauged local matrices
+ * ("two sequential Schur complements"; the gauge makes them SPD), coarse problem
+ * S_pp = sum_s N_s^T S^s N_s (P:L138 N) assembly and factorisation.
+ * Errors: TCG_ENOTSPD (a pivot <= 0: patch id or "coarse", pivot index and value in
+ * tcg_last_error; a gauging bug; the handle then accepts only get_* / destroy),
+ * TCG_ENOMEM, TCG_ECUDA (no sm_100 device, launch failure), TCG_ENCCL, TCG_ESTATE. */
 tcg_status tcg_setup(tcg_handle h);
 
-/* Re-run the numeric setup (assembly, batched Cholesky, coarse factorisation) on the
- * existing allocations and reset the time stepping to t = 0, A = 0 (one "pass over one
- * batch of input" for benchmarking; the plan and device memory are reused). */
+/* Re-run the numeric setup of tcg_setup on the existing
+ * allocations and reset the time stepping to t = 0, A = 0 (one "pass over one batch of input"
+ * for benchmarking; the plan and device memory are reused). Collective. Errors as tcg_setup. */
 tcg_status tcg_refactor(tcg_handle h);
 
-/* Collective: n implicit-Euler steps (each: rhs, PCG on lambda, recovery). */
+/* Collective: n implicit-Euler steps (P:L133 eq. euler; each step: right-hand side
+ * f = M a^(l)/dt + j^(l+1), the 3x3 block system of P:L139-153 reduced to F lam = d and solved by
+ * PCG from lam0 = 0, recovery of a = (a_e = 0, a_p = N p, a_r)). One persistent
+ * kernel launch per call. Errors: TCG_EINVAL (n < 0, more steps than set_time allows),
+ * TCG_ENOCONV (PCG reached max_iter: step, iterations and relres in tcg_last_error; the
+ * handle then accepts only get_* / destroy), TCG_ESTATE (before setup / failed handle). */
 tcg_status tcg_step(tcg_handle h, int n);
 
-/* Coefficients of A after the last step. layout 0: per-patch local vectors concatenated
+/* Coefficients of A (the spline coefficient vector a of P:L88-121 / P:L133) after the last
+ * step, written to the caller's out[len] (len too short: TCG_EINVAL with the needed length).
+ * layout 0: per-patch local vectors concatenated
  * (n_patches * n_local; eliminated DOFs 0); layout 1: one value per glued edge taken
  * from the lowest-id owning patch (n_edges). */
 tcg_status tcg_get_coefficients(tcg_handle h, int layout, double* out, size_t len);
 
-/* Per-step PCG iteration counts iters[nsteps] and final relative residuals
+/* Residual history of the PCG of P:L170 (iteration counts are the paper's scalability
+ * indicator): per-step PCG iteration counts iters[nsteps] and final relative residuals
  * final_relres[nsteps] (either may be NULL); if relres_hist != NULL, the concatenated
  * per-step histories sqrt(r_k^T z_k / r_0^T z_0), k = 0..iters (sum(iters+1) values). */
 tcg_status tcg_get_history(tcg_handle h, int* iters, double* final_relres, size_t nsteps,
                            double* relres_hist, size_t hist_len);
 
+/* Counts of the plan (#multipliers m, #primal groups n_c, gauge and Dirichlet
+ * DOFs), algorithmic byte and flop counts, timings and profiling results.
+ * Valid in any state (zeros before tcg_plan). */
 tcg_status tcg_get_info(tcg_handle h, tcg_info* out);
 
 /* The dual operator of the IETI-DP system ("two sequential Schur complements";
@@ -211,7 +250,9 @@ tcg_status tcg_bench_fapply(tcg_handle h, int n, double* ms);
  * Resets the accumulators. */
 tcg_status tcg_set_profile(tcg_handle h, int kernel_id);
 
+/* Message of the last failed call on h (owned by the handle, valid until the next call). */
 const char* tcg_last_error(tcg_handle h);
+/* Release every device allocation, stream and communicator of h (NULL is a no-op). */
 void tcg_destroy(tcg_handle h);
 
 #ifdef __cplusplus

@@ -84,14 +84,17 @@ def sinpi(x: float) -> float:
     return sign * math.sin(math.pi * r)
 
 
-def source_time_factor(kind: int, t: float, nu: float, sigma: float) -> float:
-    """phi_s(t) with J = phi_s(t) S(x) on patch s.
-    kind 1: sin(2 pi t) (evaluated as sinpi(2t)).  kind 2: 2 pi^2 nu (1-e^-t) + sigma e^-t
-    (curl curl S = 2 pi^2 S)."""
+def source_time_factor(kind: int, t: float, nu: float, sigma: float, params=()) -> float:
+    """phi_s(t) with J = phi_s(t) S(x) on patch s (params: an amplitude, and for kind 1 a
+    frequency; defaults 1).
+    kind 1: amp sin(2 pi freq t) (evaluated as sinpi(2 freq t)).
+    kind 2: amp [2 pi^2 nu (1-e^-t) + sigma e^-t] (curl curl S = 2 pi^2 S)."""
+    amp = params[0] if len(params) >= 1 else 1.0
     if kind == 1:
-        return sinpi(2.0 * t)
+        freq = params[1] if len(params) >= 2 else 1.0
+        return amp * sinpi(2.0 * freq * t)
     if kind == 2:
-        return 2.0 * math.pi ** 2 * nu * (1.0 - math.exp(-t)) + sigma * math.exp(-t)
+        return amp * (2.0 * math.pi ** 2 * nu * (1.0 - math.exp(-t)) + sigma * math.exp(-t))
     return 0.0
 
 

@@ -291,7 +291,7 @@ class Oracle:
     # ---- time step ---------------------------------------------------------------
     def source_factor(self, s, t):
         pr = self.prob
-        return assembly.source_time_factor(pr.source, t, pr.nu[s], pr.sigma[s])
+        return assembly.source_time_factor(pr.source, t, pr.nu[s], pr.sigma[s], getattr(pr, "source_params", ()))
 
     def pcg(self, d, W=None, FW=None):
         """Classical Hestenes-Stiefel PCG from lam0 = 0 (R6), or, warm start

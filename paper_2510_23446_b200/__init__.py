@@ -62,7 +62,7 @@ def lib():
     L.tcg_create.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, C.c_char_p, vp]
     L.tcg_set_patches.argtypes = [vp, ip, dp, dp, C.c_int, ip]
     L.tcg_set_materials.argtypes = [vp, dp, dp, C.c_size_t]
-    L.tcg_set_source.argtypes = [vp, C.c_int]
+    L.tcg_set_source.argtypes = [vp, C.c_int, dp, C.c_size_t]
     L.tcg_set_time.argtypes = [vp, C.c_double, C.c_int]
     L.tcg_set_solver.argtypes = [vp, C.c_double, C.c_int, C.c_int, C.c_int]
     L.tcg_set_warm_start.argtypes = [vp, C.c_int]
@@ -127,8 +127,10 @@ class Solver:
         n = np.ascontiguousarray(nu, dtype=np.float64)
         self._ck(self.L.tcg_set_materials(self.h, _dptr(s), _dptr(n), len(s)))
 
-    def set_source(self, kind):
-        self._ck(self.L.tcg_set_source(self.h, int(kind)))
+    def set_source(self, kind, params=()):
+        """J = amp * phi(t) * S(x): kind 1 params (amp, freq), kind 2 (amp,), kind 0 ()."""
+        p = np.ascontiguousarray(params, dtype=np.float64)
+        self._ck(self.L.tcg_set_source(self.h, int(kind), _dptr(p) if p.size else None, p.size))
 
     def set_time(self, T, n_steps):
         self._ck(self.L.tcg_set_time(self.h, float(T), int(n_steps)))
@@ -146,7 +148,7 @@ class Solver:
         """Set everything from a problem description with the fields of workloads.Problem."""
         self.set_patches(prob.npatch, prob.lo, prob.hi, prob.p, prob.elems)
         self.set_materials(prob.sigma, prob.nu)
-        self.set_source(prob.source)
+        self.set_source(prob.source, getattr(prob, "source_params", ()))
         self.set_time(prob.T, prob.n_steps)
         self.set_solver(prob.rtol, prob.max_iter, prob.scaling, prob.tree_order)
         self.set_warm_start(getattr(prob, "warm_start", 0))

@@ -45,7 +45,7 @@ typedef struct {
 } ncclUniqueId;
 typedef int ncclResult_t;
 enum { ncclInt8 = 0, ncclChar = 0, ncclFloat64 = 8 };
-enum { ncclSum = 0 };
+enum { ncclSum = 0, ncclMax = 2 };
 struct NcclApi {
   void* lib = nullptr;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
@@ -115,6 +115,7 @@ struct tcg_ctx {
   bool have_patches = false, have_materials = false, have_time = false;
   bool planned = false, setup_done = false, broken = false;
   int source = TCG_SOURCE_CURL_PSI;
+  double src_amp = 1.0, src_freq = 1.0;  // tcg_set_source params
   double T = 1.0;
   int n_steps = 0;
   double rtol = 1e-10;
@@ -128,7 +129,9 @@ struct tcg_ctx {
 
   // device state
   std::vector<void*> allocs;       // cudaMalloc (multi-GPU: IPC-exportable)
-  std::vector<void*> pool_allocs;  // cudaMallocAsync from the retained default pool
+  std::vector<void*> pool_allocs;  // cudaMallocFromPoolAsync from the library's own pool
+  bool pool_user = false;          // counted in the device's live-handle count of that pool
+  double* agree_buf = nullptr;     // world > 1: per-launch agreement of the warm-start state
   std::vector<void*> ipc_opened;
   int64_t device_bytes = 0;
   int nranks = 1;  // ranks of the job: world (real) or vranks (virtual)
@@ -220,6 +223,35 @@ struct tcg_ctx {
   double ms_plan = 0, ms_assembly = 0, ms_factor = 0, ms_coarse = 0, ms_steps = 0;
 
   ~tcg_ctx() { release(); }
+  // The library's own stream-ordered memory pool per device (never the device's default
+  // pool): freed memory is kept while handles live on the device (re-creating a handle costs
+  // no driver allocations) and trimmed to zero when the last handle of the device is released.
+  struct PoolReg {
+    std::mutex mu;
+    cudaMemPool_t pool[64] = {};
+    int live[64] = {};
+  };
+  static PoolReg& pools() {
+    static PoolReg r;
+    return r;
+  }
+  static cudaMemPool_t lib_pool(int device) {
+    PoolReg& R = pools();
+    std::lock_guard<std::mutex> lk(R.mu);
+    if (device < 0 || device >= 64) return nullptr;
+    if (!R.pool[device]) {
+      cudaMemPoolProps pp{};
+      pp.allocType = cudaMemAllocationTypePinned;
+      pp.location.type = cudaMemLocationTypeDevice;
+      pp.location.id = device;
+      cudaMemPool_t mp = nullptr;
+      if (cudaMemPoolCreate(&mp, &pp) != cudaSuccess) return nullptr;
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+      R.pool[device] = mp;
+    }
+    return R.pool[device];
+  }
   // pinned PcgState buffers are recycled across handles (cudaMallocHost costs ~ms)
   static std::vector<PcgState*>& pinned_free() {
     static std::vector<PcgState*> v;
@@ -236,6 +268,12 @@ struct tcg_ctx {
     for (void* p : pool_allocs) cudaFreeAsync(p, stream);
     pool_allocs.clear();
     if (stream) cudaStreamSynchronize(stream);
+    if (pool_user) {  // last handle on this device: hand the pool's memory back to the driver
+      PoolReg& R = pools();
+      std::lock_guard<std::mutex> lk(R.mu);
+      if (--R.live[device] == 0 && R.pool[device]) cudaMemPoolTrimTo(R.pool[device], 0);
+      pool_user = false;
+    }
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
     if (h_st) {
@@ -285,19 +323,9 @@ tcg_status fail(tcg_ctx* h, tcg_status s, const std::string& msg) {
     if (s_ != TCG_OK) return s_; \
   } while (0)
 
-// Device allocations: single-process handles use the device's stream-ordered memory pool,
-// configured to keep freed memory (so re-creating a handle costs no driver allocations);
-// multi-GPU handles use cudaMalloc (their buffers are exported with CUDA IPC).
-void retain_pool(int device) {
-  static bool done[64] = {false};
-  if (device < 0 || device >= 64 || done[device]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done[device] = true;
-}
+// Device allocations: single-process handles use the library's own stream-ordered pool
+// (tcg_ctx::lib_pool; trimmed when the device's last handle is released); multi-GPU handles
+// use cudaMalloc (their buffers are exported with CUDA IPC).
 
 template <class T>
 tcg_status dalloc(tcg_ctx* h, T** out, size_t n) {
@@ -305,8 +333,14 @@ tcg_status dalloc(tcg_ctx* h, T** out, size_t n) {
   void* p = nullptr;
   cudaError_t e;
   if (h->world == 1) {
-    retain_pool(h->device);
-    e = cudaMallocAsync(&p, bytes, h->stream);
+    cudaMemPool_t mp = tcg_ctx::lib_pool(h->device);
+    if (!mp) return fail(h, TCG_ECUDA, "cudaMemPoolCreate failed");
+    if (!h->pool_user) {
+      std::lock_guard<std::mutex> lk(tcg_ctx::pools().mu);
+      ++tcg_ctx::pools().live[h->device];
+      h->pool_user = true;
+    }
+    e = cudaMallocFromPoolAsync(&p, bytes, mp, h->stream);
     if (e == cudaSuccess) h->pool_allocs.push_back(p);
   } else {
     e = cudaMalloc(&p, bytes);
@@ -479,11 +513,16 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
   Plan& pl = h->plan;
   const int Tc = h->Tc;
   const double dt = h->T / h->n_steps;
-  cudaEvent_t e0, e1, e2, e3;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventCreate(&e2);
-  cudaEventCreate(&e3);
+  struct Events {  // destroyed on every return path
+    cudaEvent_t e[4];
+    Events() {
+      for (auto& x : e) cudaEventCreate(&x);
+    }
+    ~Events() {
+      for (auto& x : e) cudaEventDestroy(x);
+    }
+  } ev;
+  cudaEvent_t e0 = ev.e[0], e1 = ev.e[1], e2 = ev.e[2], e3 = ev.e[3];
   CK(cudaEventRecord(e0, h->stream));
   k_tables1d<<<3, 256, h->smem_tables, h->stream>>>(h->tb, pl.p);
   ++h->nlaunch;
@@ -501,6 +540,15 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
       ++h->nlaunch;
       CKL();
     }
+  }
+  if (const char* ns = getenv("TCG_DEBUG_NOTSPD")) {  // test hook: first pivot of patch s := -1
+    const int sbad = atoi(ns);
+    for (auto& R : h->rd)
+      if (sbad >= 0 && sbad < pl.npatch && pl.rank_of_patch[sbad] == R.r) {
+        const double neg = -1.0;
+        CK(cudaMemcpyAsync(R.A + h->h_a_off[sbad], &neg, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+      }
   }
   TRY(sync_ranks(h));  // every rank's W^ assembled (rho weights read both interface sides)
   for (auto& R : h->rd) {
@@ -588,10 +636,6 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
   h->ms_assembly = elapsed_ms(e0, e1);
   h->ms_factor = elapsed_ms(e1, e2);
   h->ms_coarse = elapsed_ms(e2, e3);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(e2);
-  cudaEventDestroy(e3);
   h->steps_done = 0;
   h->warm_base = 0;  // refactor / setup: the time integration restarts, so does the warm history
   h->hist_len = 0;
@@ -1796,6 +1840,8 @@ static StepArgs step_args(tcg_ctx* h) {
   A.sys_scope = (h->world > 1) ? 1 : 0;
   A.lam_chunk = h->lam_chunk;
   A.source = h->source;
+  A.src_amp = h->src_amp;
+  A.src_freq = h->src_freq;
   A.dt = h->T / h->n_steps;
   A.step0 = (int)h->steps_done;
   A.nsteps = 0;
@@ -1804,6 +1850,23 @@ static StepArgs step_args(tcg_ctx* h) {
   A.tb = h->tb;
   A.G = h->G;
   return A;
+}
+
+// The warm-start state (k, first step of the history) decides which barriers a launch runs;
+// every rank must agree or the monotone barrier counters would pair different rounds. One
+// NCCL max-allreduce of (k, base, -k, -base) per tcg_step on world > 1 handles.
+static tcg_status agree_warm(tcg_ctx* h) {
+  if (!h->agree_buf) TRY(dzero(h, &h->agree_buf, 4));
+  const double v[4] = {(double)h->warm, (double)h->warm_base, -(double)h->warm, -(double)h->warm_base};
+  CK(cudaMemcpyAsync(h->agree_buf, v, sizeof v, cudaMemcpyHostToDevice, h->stream));
+  ncclResult_t r = g_nccl.allReduce(h->agree_buf, h->agree_buf, 4, ncclFloat64, ncclMax, h->comm, h->stream);
+  if (r != 0) return fail(h, TCG_ENCCL, "ncclAllReduce (warm-start agreement) failed");
+  double w[4];
+  CK(cudaMemcpyAsync(w, h->agree_buf, sizeof w, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  if (w[0] != -w[2] || w[1] != -w[3])
+    return fail(h, TCG_EINVAL, "tcg_set_warm_start is collective: ranks disagree on k or on the step it was set at");
+  return TCG_OK;
 }
 
 // n implicit-Euler steps in ONE persistent cooperative launch (k_steps) over all local ranks
@@ -1821,6 +1884,7 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
         TRY(dzero(h, &R.dsave, m));
         TRY(dzero(h, &R.wpart, (size_t)2 * h->nbr * KW_NV));
       }
+  if (h->world > 1) TRY(agree_warm(h));
   StepArgs A = step_args(h);
   A.nsteps = n;
   DevPlan D = h->D;
@@ -1949,11 +2013,20 @@ tcg_status tcg_set_materials(tcg_handle h, const double* sigma, const double* nu
   return TCG_OK;
 }
 
-tcg_status tcg_set_source(tcg_handle h, int kind) {
+tcg_status tcg_set_source(tcg_handle h, int kind, const double* params, size_t nparams) {
   if (!h) return TCG_EINVAL;
   if (h->setup_done) return fail(h, TCG_ESTATE, "set_source after setup");
   if (kind < 0 || kind > 2) return fail(h, TCG_EINVAL, "unknown source kind");
+  const size_t maxp = kind == 1 ? 2 : (kind == 2 ? 1 : 0);
+  if (nparams > maxp || (nparams > 0 && !params))
+    return fail(h, TCG_EINVAL, "source kind " + std::to_string(kind) + " takes at most " + std::to_string(maxp) + " parameters");
+  double amp = 1.0, freq = 1.0;
+  if (nparams >= 1) amp = params[0];
+  if (nparams >= 2) freq = params[1];
+  if (!std::isfinite(amp) || !std::isfinite(freq)) return fail(h, TCG_EINVAL, "source parameters must be finite");
   h->source = kind;
+  h->src_amp = amp;
+  h->src_freq = freq;
   return TCG_OK;
 }
 
@@ -2036,7 +2109,7 @@ tcg_status tcg_setup(tcg_handle h) {
   if (h->setup_done) return fail(h, TCG_ESTATE, "setup already done");
   if (h->broken) return fail(h, TCG_ESTATE, "handle is in a failed state");
   tcg_status s = do_setup(h);
-  if (s != TCG_OK && s != TCG_ENOTSPD) h->broken = true;
+  if (s != TCG_OK) h->broken = true;  // ENOTSPD included: only get_* / destroy afterwards
   return s;
 }
 
@@ -2044,7 +2117,9 @@ tcg_status tcg_refactor(tcg_handle h) {
   if (!h) return TCG_EINVAL;
   if (!h->setup_done || h->broken) return fail(h, TCG_ESTATE, "setup first (or handle failed)");
   cudaSetDevice(h->device);
-  return do_numeric(h);
+  tcg_status s = do_numeric(h);
+  if (s != TCG_OK) h->broken = true;
+  return s;
 }
 
 tcg_status tcg_step(tcg_handle h, int n) {

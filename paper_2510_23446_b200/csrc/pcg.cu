@@ -139,6 +139,7 @@ struct StepArgs {
   int64_t lam_chunk;  // lambda entries per (rank, block): owner of k = (k / lam_chunk) / nbr
   // time stepping
   int source;
+  double src_amp, src_freq;  // J = src_amp * phi(t; src_freq) * S(x) (tcg_set_source params)
   double dt;
   int step0;    // steps done before this launch
   int nsteps;   // steps to run
@@ -792,8 +793,8 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
   const int s = it.s, c = it.I;
   const double sig = D.sigma[s], nu = D.nu[s];
   double phi = 0.0;
-  if (A.source == 1) phi = sinpi(2.0 * t);
-  else if (A.source == 2) phi = 2.0 * M_PI * M_PI * nu * (1.0 - exp(-t)) + sig * exp(-t);
+  if (A.source == 1) phi = A.src_amp * sinpi(2.0 * A.src_freq * t);
+  else if (A.source == 2) phi = A.src_amp * (2.0 * M_PI * M_PI * nu * (1.0 - exp(-t)) + sig * exp(-t));
   const int64_t vo = it.vec_off;
   if (c < 0) {
     const int R = it.T * TS;

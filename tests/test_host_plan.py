@@ -80,9 +80,14 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("pr", CASES, ids=lambda p: p.name)
-@pytest.mark.parametrize("order", [0, 1])
-def test_plan_matches_oracle(tcg, pr, order):
+# BASELINE.json configs[2..4] at full size (tree order 0, the one every run uses)
+BIG = [(workloads.cfg3, 0), (workloads.cfg4, 0), (workloads.cfg5, 0)]
+
+
+@pytest.mark.parametrize("make,order", [(lambda p=p: p, o) for p in CASES for o in (0, 1)] + BIG,
+                         ids=[f"{p.name}-{o}" for p in CASES for o in (0, 1)] + ["cfg3-0", "cfg4-0", "cfg5-0"])
+def test_plan_matches_oracle(tcg, make, order):
+    pr = make()
     pr.tree_order = order
     topo = topology.Topology(pr.npatch, pr.p, pr.elems, pr.sigma)
     tree = gauge.build_tree(topo, order)

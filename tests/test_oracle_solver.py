@@ -359,3 +359,18 @@ def test_lean_parallel_oracle_equals_plain():
         x, y = a.coefficients(1), b.coefficients(1)
         assert np.linalg.norm(x - y) <= tol * np.linalg.norm(x)
         assert a.iters == b.iters
+
+
+def test_source_params_amplitude_and_frequency():
+    """phi_s(t) = amp sin(2 pi freq t): amp scales the solution linearly (the system is
+    linear in J), freq = 1 is the default source, and freq = 2 puts the source's
+    zeros at t = k/4 (exact argument reduction, R19)."""
+    base = workloads.cfg1()
+    base.n_steps = 4
+    a0 = Oracle(copy.deepcopy(base)).run().coefficients(1)
+    q = copy.deepcopy(base)
+    q.source_params = (2.0, 1.0)
+    a2 = Oracle(q).run().coefficients(1)
+    assert np.linalg.norm(a2 - 2.0 * a0) <= 1e-9 * np.linalg.norm(a0)
+    assert assembly.source_time_factor(1, 0.25, 1.0, 0.0, (1.0, 2.0)) == 0.0
+    assert assembly.source_time_factor(1, 0.125, 1.0, 0.0, (3.0, 2.0)) == 3.0

@@ -37,6 +37,7 @@ class Problem:
     T: float = 1.0
     n_steps: int = 10
     source: int = SOURCE_CURL_PSI
+    source_params: tuple = ()            # kind 1: (amp, freq) default (1, 1); kind 2: (amp,) default (1,)
     rtol: float = 1e-10
     max_iter: int = 5000
     scaling: int = 1                     # 0 = none (paper P:L170), 1 = rho (BJ.ns "scaled")
