@@ -56,7 +56,9 @@ def local_dof_table(n) -> np.ndarray:
 def source_field(kind: int, x, y, z):
     """Spatial part S(x) of J = phi(t) S(x).
     kind 1: S = curl(0,0,psi), psi = sin(pi x) sin(pi y) sin(pi z)   (BJ configs)
-    kind 2: S = (sin pi y sin pi z, sin pi x sin pi z, sin pi x sin pi y)  (MMS)"""
+    kind 2: S = (sin pi y sin pi z, sin pi x sin pi z, sin pi x sin pi y)  (MMS)
+    kind 3: S = (sin x cos y cos z, -2 cos x sin y cos z, cos x cos y sin z)  (the paper's
+            prescribed solution A = e^-t S; oracle/paper_mms.py)"""
     pi = math.pi
     if kind == 1:
         return (pi * np.sin(pi * x) * np.cos(pi * y) * np.sin(pi * z),
@@ -64,6 +66,9 @@ def source_field(kind: int, x, y, z):
                 0.0 * x)
     if kind == 2:
         return (np.sin(pi * y) * np.sin(pi * z), np.sin(pi * x) * np.sin(pi * z), np.sin(pi * x) * np.sin(pi * y))
+    if kind == 3:
+        return (np.sin(x) * np.cos(y) * np.cos(z), -2.0 * np.cos(x) * np.sin(y) * np.cos(z),
+                np.cos(x) * np.cos(y) * np.sin(z))
     return (0.0 * x, 0.0 * x, 0.0 * x)
 
 
@@ -88,13 +93,17 @@ def source_time_factor(kind: int, t: float, nu: float, sigma: float, params=()) 
     """phi_s(t) with J = phi_s(t) S(x) on patch s (params: an amplitude, and for kind 1 a
     frequency; defaults 1).
     kind 1: amp sin(2 pi freq t) (evaluated as sinpi(2 freq t)).
-    kind 2: amp [2 pi^2 nu (1-e^-t) + sigma e^-t] (curl curl S = 2 pi^2 S)."""
+    kind 2: amp [2 pi^2 nu (1-e^-t) + sigma e^-t] (curl curl S = 2 pi^2 S).
+    kind 3: amp e^-t (3 nu - sigma): J = nu curl curl A + sigma dA/dt for A = e^-t S,
+            curl curl S = 3 S."""
     amp = params[0] if len(params) >= 1 else 1.0
     if kind == 1:
         freq = params[1] if len(params) >= 2 else 1.0
         return amp * sinpi(2.0 * freq * t)
     if kind == 2:
         return amp * (2.0 * math.pi ** 2 * nu * (1.0 - math.exp(-t)) + sigma * math.exp(-t))
+    if kind == 3:
+        return amp * math.exp(-t) * (3.0 * nu - sigma)
     return 0.0
 
 

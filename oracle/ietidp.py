@@ -20,10 +20,12 @@ W_bb - W_bi W_ii^-1 W_ib (interior solves), not by any condensed factor.
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import scipy.linalg as sla
 
-from . import assembly, topology, gauge
+from . import assembly, topology, gauge, paper_mms
 
 
 class NotSPD(RuntimeError):
@@ -87,7 +89,7 @@ def patch_box(prob, s):
     return lo, hi
 
 
-def local_operators(prob, s, r, pl, ni, dt, lean=False):
+def local_operators(prob, s, r, pl, ni, dt, lean=False, dl=None):
     """Per-patch setup (P:L83-87 assembly, P:L133 W^ = K + M/dt, P:L154 local Schur
     complement): element-loop K, M, j_S of patch s; W^ = nu K + (sigma/dt) M restricted to
     r = [i; b] (local ids `r`) and to the primal DOFs `pl`; Cholesky of W_rr and W_ii;
@@ -107,7 +109,13 @@ def local_operators(prob, s, r, pl, ni, dt, lean=False):
     Ss = Wpp - Wrp.T @ Phi
     Wii_cf = _chol(Wrr[:ni, :ni], f"W_ii patch {s}")
     out = dict(Wrr_cf=cf, Wii_cf=Wii_cf, Wrp=Wrp, Wpp=Wpp, Phi=Phi, Ss=Ss, Wbb=Wrr[ni:, ni:], Wbi=Wrr[ni:, :ni],
-               Wdiag=np.diag(W).copy(), jS=jS, K=K, M=M, Wfull=W)
+               Wdiag=np.diag(W).copy(), jS=jS, K=K, M=M, Wfull=W, Pi=None, hr=None, hp=None)
+    if prob.source == paper_mms.SOURCE_PAPER:
+        # the paper's experiment: a(0) = Pi_h S and the Dirichlet lifting
+        # a_D(t) = e^-t (Pi_h S)_D (R21); its right-hand-side terms W_rD a_D, W_pD a_D
+        Pi = paper_mms.commuting_projection(sp, paper_mms.S)
+        dl = np.zeros(0, dtype=np.int64) if dl is None else dl
+        out.update(Pi=Pi, hr=W[np.ix_(r, dl)] @ Pi[dl], hp=W[np.ix_(pl, dl)] @ Pi[dl])
     if lean:
         import scipy.sparse as sps
         out.update(K=None, Wfull=None, Wpp=None, M=sps.csr_matrix(M) if prob.sigma[s] > 0 else None,
@@ -136,9 +144,16 @@ class Oracle:
         self.part = gauge.Partition(self.topo, self.tree)
         self.dt = prob.T / prob.n_steps
         self._index_tables()
+        # local Dirichlet DOFs (class D edges) of every patch
+        self.d_loc = [np.array([a for a in self.part.e_loc[s] if self.part.part[self.topo.l2g[s][a]] == gauge.CLS_D],
+                               dtype=np.int64) for s in range(P)]
+        self.lifting = prob.source == paper_mms.SOURCE_PAPER
         if assemble:
             self._setup_locals()
         self.a = [np.zeros(self.topo.l2g.shape[1]) for _ in range(P)]
+        if self.lifting and assemble:  # A(0) = Pi_h A_0 (R21)
+            self.a = [self.Pi[s].copy() for s in range(P)]
+        self.errors = paper_mms.ErrorTracker(self) if (self.lifting and getattr(prob, "track_errors", False)) else None
         self.ell = 0
         self.iters = []
         self.hist = []
@@ -175,8 +190,8 @@ class Oracle:
         pr = self.prob
         pt = self.part
         P = pr.n_patches
-        jobs = [(pr, s, pt.r_order(s), pt.p_loc[s], len(pt.r_i[s]), self.dt, self.lean) for s in range(P)]
-        names = ("Wrr_cf", "Wii_cf", "Wrp", "Wpp", "Phi", "Wbb", "Wbi", "Wdiag", "jS", "K", "M", "Wfull")
+        jobs = [(pr, s, pt.r_order(s), pt.p_loc[s], len(pt.r_i[s]), self.dt, self.lean, self.d_loc[s]) for s in range(P)]
+        names = ("Wrr_cf", "Wii_cf", "Wrp", "Wpp", "Phi", "Wbb", "Wbi", "Wdiag", "jS", "K", "M", "Wfull", "Pi", "hr", "hp")
         for n in names:
             setattr(self, n, [])
         nc = pt.nc
@@ -358,6 +373,11 @@ class Oracle:
             f.append(self.Ma(s, self.a[s]) / self.dt + js)
         fr = [f[s][pt.r_order(s)] for s in range(P)]
         fp = [f[s][pt.p_loc[s]] for s in range(P)]
+        if self.lifting:  # f_r - W_rD a_D(t), f_p - W_pD a_D(t), a_D(t) = e^-t (Pi_h S)_D
+            eD = math.exp(-t)
+            fr = [fr[s] - eD * self.hr[s] for s in range(P)]
+            fp = [fp[s] - eD * self.hp[s] for s in range(P)]
+        a_old = self.a
         x1 = self._map(lambda s: _solve(self.Wrr_cf[s], fr[s]), range(P))
         h = [self.Wrp[s].T @ x1[s] for s in range(P)]
         fpg = self.NT(fp)
@@ -377,6 +397,9 @@ class Oracle:
             a = np.zeros(self.topo.l2g.shape[1])
             a[pt.r_order(s)] = ar
             a[pt.p_loc[s]] = pc[pt.p_grp[s]]
+            if self.lifting:
+                dl = self.d_loc[s]
+                a[dl] = math.exp(-t) * self.Pi[s][dl]
             return a
         self.a = self._map(recover, range(P))
         self.lam = lam
@@ -384,6 +407,8 @@ class Oracle:
         self.ell += 1
         self.iters.append(k)
         self.hist.append(hist)
+        if self.errors is not None:
+            self.errors.after_step(a_old)
         return k
 
     def run(self, n=None):

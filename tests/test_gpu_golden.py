@@ -100,3 +100,37 @@ def test_full_size_matches_oracle_golden(tcg, path):
     assert e_patch <= PATCH_TOL, (e_patch, s_worst)
     d_it = np.abs(np.asarray(it, dtype=np.int64) - g["iters"].astype(np.int64))
     assert np.all(d_it <= 1), (list(it), list(g["iters"]))
+
+
+def _golden(name):
+    hits = [p for p in GOLDEN if os.path.basename(p).startswith(name + "_s")]
+    if not hits:
+        pytest.skip(f"no golden file for {name}")
+    g = np.load(hits[0])
+    return g, json.loads(str(g["meta"]))
+
+
+@pytest.mark.parametrize("name,vranks", [("cfg2", 2), ("cfg2", 3), ("cfg2", 4), ("cfg4", 2), ("cfg4", 4)])
+def test_virtual_ranks_sparse_coarse_match_golden(tcg, monkeypatch, name, vranks):
+    """Sharded solve (virtual ranks: x-slab patch ownership, peer-table dataflow, two-level
+    barrier) with the sparse coarse solver (every rank runs the replicated
+    nested-dissection solve, gathering the primal rows of other ranks' patches through the
+    peer tables) against the oracle's golden file."""
+    monkeypatch.setenv("TCG_COARSE", "sparse")
+    g, meta = _golden(name)
+    pr = workloads.get(name)
+    steps = int(meta["steps"])
+    s = tcg.Solver()
+    s.set_virtual_ranks(vranks)
+    s.configure(pr)
+    s.setup()
+    s.step(steps)
+    a = s.coefficients(1)
+    it = s.history()[0]
+    inf = s.info()
+    s.close()
+    assert inf["coarse_sparse"] == 1 and inf["world"] == vranks
+    ref = g["a1"]
+    err = float(np.linalg.norm(a - ref) / np.linalg.norm(ref))
+    assert err <= TOL, err
+    assert np.all(np.abs(np.asarray(it, dtype=np.int64) - g["iters"].astype(np.int64)) <= 1), (list(it), list(g["iters"]))

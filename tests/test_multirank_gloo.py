@@ -6,7 +6,12 @@
    by ranks as I*NR/Tc, lambda entries gathered from both interface sides) reproduces the
    un-sharded dual operator and preconditioner: each rank applies the oracle's local operators
    to its own patches only, and the values the GPU kernels read from peers are exchanged with
-   gloo all_reduce. The result must equal the oracle's F(lambda) and M^-1(r)."""
+   gloo all_reduce. The result must equal the oracle's F(lambda) and M^-1(r).
+3. Two coarse ownerships: "rows" (dense S_pp^-1, coarse row block I owned by rank I*NR/Tc,
+   every rank reads the solution rows from their owners) and "replicated" (the sparse coarse
+   solver on several ranks: every rank gathers the primal rows -g_s of all patches through
+   the peer tables and runs the whole coarse solve itself; the solutions must be identical
+   on every rank, bit for bit, and no coarse exchange follows)."""
 import os
 import socket
 
@@ -35,7 +40,7 @@ def _allreduce(x):
     return t.numpy()
 
 
-def _worker(rank, world, port, name, out_q):
+def _worker(rank, world, port, name, coarse, out_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -74,11 +79,17 @@ def _worker(rank, world, port, name, out_q):
         g = _allreduce(g_part)                         # PC reads -g_s of every patch
         Tc = (pt.nc + 63) // 64
         pc_full = oi._solve(o.Spp_cf, g)
-        pc_part = np.zeros(pt.nc)                      # coarse rows owned as I*NR/Tc
-        for I in range(Tc):
-            if (I * world) // Tc == rank:
-                pc_part[I * 64:(I + 1) * 64] = pc_full[I * 64:(I + 1) * 64]
-        pc = _allreduce(pc_part)                       # P5 reads Pc from the row owners
+        if coarse == "rows":
+            pc_part = np.zeros(pt.nc)                  # coarse rows owned as I*NR/Tc
+            for I in range(Tc):
+                if (I * world) // Tc == rank:
+                    pc_part[I * 64:(I + 1) * 64] = pc_full[I * 64:(I + 1) * 64]
+            pc = _allreduce(pc_part)                   # P5 reads Pc from the row owners
+        else:
+            pc = pc_full                               # replicated: every rank solved it whole
+            allpc = [None] * world
+            dist.all_gather_object(allpc, pc.tobytes())
+            assert all(x == allpc[0] for x in allpc), "replicated coarse solutions differ across ranks"
         y = {p: u[p] + o.Phi[p] @ pc[pt.p_grp[p]] for p in mine}
         q_part = np.zeros(pt.m)                        # jump: both sides, possibly remote
         for k in range(pt.m):
@@ -121,14 +132,15 @@ def _worker(rank, world, port, name, out_q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("coarse", ["rows", "replicated"])
 @pytest.mark.parametrize("name", ["cfg1", "aniso"])
-def test_sharded_dataflow_gloo(name):
+def test_sharded_dataflow_gloo(name, coarse):
     from paper_2510_23446_b200 import build
     build.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, coarse, q)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]

@@ -22,6 +22,7 @@ import numpy as np
 SOURCE_NONE = 0
 SOURCE_CURL_PSI = 1   # J = curl(0,0,sin(pi x)sin(pi y)sin(pi z)) * sin(2 pi t)   (BJ configs)
 SOURCE_MMS = 2        # J = [2 pi^2 nu (1-e^-t) + sigma e^-t] S(x), S=(sy sz, sx sz, sx sy)
+SOURCE_PAPER = 3      # the paper's A = e^-t (sx cy cz, -2 cx sy cz, cx cy sz), inhomogeneous Dirichlet
 
 
 @dataclass
@@ -43,6 +44,7 @@ class Problem:
     scaling: int = 1                     # 0 = none (paper P:L170), 1 = rho (BJ.ns "scaled")
     tree_order: int = 0                  # 0 ascending ids within a rank, 1 descending
     warm_start: int = 0                  # 0: lambda0 = 0 (paper); k: projection on the last k solutions
+    track_errors: bool = False           # source 3: accumulate eps_B, eps_E every step
     extra: dict = field(default_factory=dict)
 
     @property
@@ -183,6 +185,20 @@ def cfg5() -> Problem:
     sig = np.array([1e6 if iz <= 3 else 0.0 for (_, _, iz) in _grid(npatch)])
     nu = np.array([1e-3 if (6 <= ix <= 9 and 6 <= iy <= 9) else 1.0 for (ix, iy, _) in _grid(npatch)])
     return Problem("cfg5", npatch, (0, 0, 0), (2, 2, 1), 3, (6, 6, 6), sig, nu, 1.0, 100)
+
+
+def paper(p: int, divs: int, n_steps: int, T: float = 1.0) -> Problem:
+    """The paper's experiment: Omega = (0,1)^3 split at x = 1/2 into two patches,
+    conductor x < 1/2 (sigma = 1) and insulator (sigma = 0), nu = 1 in both; `divs` elements per
+    direction over the whole cube (divs/2 along x per patch); A = e^-t S prescribed (source 3,
+    inhomogeneous Dirichlet lifting, A(0) from the same projection); PCG "without scaling"
+     and tolerance 1e-6."""
+    if divs % 2:
+        raise ValueError("divs must be even (two patches along x)")
+    pr = Problem(f"paper-p{p}-d{divs}-nt{n_steps}", (2, 1, 1), (0, 0, 0), (1, 1, 1), p, (divs // 2, divs, divs),
+                 np.array([1.0, 0.0]), np.array([1.0, 1.0]), T, n_steps, SOURCE_PAPER, rtol=1e-6, scaling=0)
+    pr.track_errors = True
+    return pr
 
 
 CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
