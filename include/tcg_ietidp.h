@@ -62,6 +62,10 @@ typedef enum {
 #define TCG_SOURCE_CURL_PSI 1 /* S = curl(0,0,sin(pi x)sin(pi y)sin(pi z)), phi = sin(2 pi t)  (BASELINE.json configs) */
 #define TCG_SOURCE_MMS 2      /* S = (sin pi y sin pi z, sin pi x sin pi z, sin pi x sin pi y),
                                  phi_s = 2 pi^2 nu_s (1-e^-t) + sigma_s e^-t  (manufactured, R16) */
+#define TCG_SOURCE_PAPER 3    /* the paper's experiment: A = e^-t (sin x cos y cos z, -2 cos x sin y cos z,
+                                 cos x cos y sin z), J = e^-t (3 nu_s - sigma_s) S; inhomogeneous Dirichlet data
+                                 a_D(t) = e^-t (Pi_h S)_D and A(0) = Pi_h S by the commuting spline projection
+                                 (R21); requires elements + p <= 72 per patch and direction */
 
 /* preconditioner scaling (P:L170 uses none; BASELINE.json north_star says "scaled") */
 #define TCG_SCALING_NONE 0
@@ -145,6 +149,7 @@ tcg_status tcg_set_materials(tcg_handle h, const double* sigma, const double* nu
  * kind (TCG_SOURCE_*) and params[nparams] (NULL/0 = defaults, copied during the call):
  *   TCG_SOURCE_CURL_PSI  params {amp = 1, freq = 1}: phi = sin(2 pi freq t)
  *   TCG_SOURCE_MMS       params {amp = 1}
+ *   TCG_SOURCE_PAPER     params {amp = 1}: A = amp e^-t S (boundary data and A(0) scale with amp)
  *   TCG_SOURCE_NONE      no params (J = 0)
  * Default: TCG_SOURCE_CURL_PSI with amp = freq = 1 (the BASELINE.json configs).
  * Errors: TCG_EINVAL (unknown kind, too many params, non-finite), TCG_ESTATE (after setup). */
@@ -180,6 +185,20 @@ tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, 
  * cold), as does tcg_refactor. Device memory (2*4+1 = 9 lambda-length vectors per rank,
  * sized for the largest k) is allocated at the first warm step. EINVAL unless 0 <= k <= 4. */
 tcg_status tcg_set_warm_start(tcg_handle h, int k);
+
+/* Error norms of the paper's experiment: with on = 1 (source TCG_SOURCE_PAPER,
+ * single-process handle, before the first step) every tcg_step runs one step per launch and
+ * accumulates on the device, by (p+1)-point Gauss quadrature per element,
+ *   e_B(t_l) = ||B(t_l) - curl A_h(t_l)||^2_{L2(Omega)},
+ *   e_E(t_l) = ||E_C(t_l) + (A_h(t_l) - A_h(t_{l-1}))/dt||^2_{L2(Omega_C)},
+ *   eps_B = sqrt(max_l e_B + dt sum_l e_B),  eps_E = sqrt(dt sum_l e_E)   (reset by tcg_refactor).
+ * Errors: TCG_EINVAL (other source, world > 1), TCG_ESTATE (steps already done). */
+tcg_status tcg_set_error_tracking(tcg_handle h, int on);
+
+/* eps_B, eps_E after the steps done so far (either pointer may be NULL) and, if per_step !=
+ * NULL, the per-step (e_B, e_E) pairs of the first nsteps steps (2*nsteps doubles, caller-owned).
+ * Errors: TCG_ESTATE (tracking off), TCG_EINVAL (nsteps > steps done). */
+tcg_status tcg_get_errors(tcg_handle h, double* eps_B, double* eps_E, double* per_step, size_t nsteps);
 
 /* Host-only planning (no CUDA): topology, ranked-Kruskal tree, e/p/r partition,
  * multiplier and primal numbering, patch->rank sharding. Idempotent. */

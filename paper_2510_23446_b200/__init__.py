@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIBPATH = os.path.join(HERE, "libtcg_ietidp.so")
+LIBPATH = os.environ.get("TCG_LIBPATH") or os.path.join(HERE, "libtcg_ietidp.so")  # (env: A/B experiments only)
 
 TCG_OK, TCG_EINVAL, TCG_ESTATE, TCG_ENOTSPD, TCG_ENOCONV, TCG_ECUDA, TCG_ENCCL, TCG_ENOMEM = 0, -1, -2, -3, -4, -5, -6, -7
 STATUS_NAMES = {0: "TCG_OK", -1: "TCG_EINVAL", -2: "TCG_ESTATE", -3: "TCG_ENOTSPD", -4: "TCG_ENOCONV",
@@ -23,7 +23,7 @@ PLAN_EDGE_CLASS, PLAN_EDGE_REGION, PLAN_TREE, PLAN_PART, PLAN_PATCH_COUNTS, PLAN
 EXPORTS = ["tcg_create", "tcg_set_patches", "tcg_set_materials", "tcg_set_source", "tcg_set_time", "tcg_set_solver", "tcg_set_warm_start",
            "tcg_plan", "tcg_get_plan", "tcg_setup", "tcg_refactor", "tcg_step", "tcg_get_coefficients", "tcg_get_history",
            "tcg_get_info", "tcg_fapply", "tcg_bench_fapply", "tcg_set_profile", "tcg_set_virtual_ranks", "tcg_nccl_unique_id", "tcg_last_error",
-           "tcg_destroy"]
+           "tcg_destroy", "tcg_set_error_tracking", "tcg_get_errors"]
 
 
 class TcgInfo(C.Structure):
@@ -81,10 +81,13 @@ def lib():
     L.tcg_nccl_unique_id.argtypes = [C.c_char_p]
     L.tcg_last_error.argtypes = [vp]
     L.tcg_last_error.restype = C.c_char_p
+    if hasattr(L, "tcg_get_errors") or not os.environ.get("TCG_LIBPATH"):  # (older A/B builds lack them)
+        L.tcg_set_error_tracking.argtypes = [vp, C.c_int]
+        L.tcg_get_errors.argtypes = [vp, dp, dp, dp, C.c_size_t]
     L.tcg_destroy.argtypes = [vp]
     L.tcg_destroy.restype = None
     for n in EXPORTS:
-        if n not in ("tcg_last_error", "tcg_destroy"):
+        if n not in ("tcg_last_error", "tcg_destroy") and (hasattr(L, n) or not os.environ.get("TCG_LIBPATH")):
             getattr(L, n).restype = C.c_int
     _LIB = L
     return L
@@ -144,6 +147,19 @@ class Solver:
         self._ck(self.L.tcg_set_warm_start(self.h, int(k)))
         return self
 
+    def set_error_tracking(self, on=True):
+        """Accumulate the paper's eps_B, eps_E every step (source 3 only)."""
+        self._ck(self.L.tcg_set_error_tracking(self.h, int(bool(on))))
+        return self
+
+    def errors(self, per_step=False):
+        """(eps_B, eps_E) and, with per_step, the (e_B, e_E) pairs of every step done."""
+        eb, ee = C.c_double(), C.c_double()
+        ns = self.info()["steps_done"] if per_step else 0
+        ps = np.zeros(2 * max(ns, 1))
+        self._ck(self.L.tcg_get_errors(self.h, C.byref(eb), C.byref(ee), _dptr(ps) if per_step else None, ns))
+        return (eb.value, ee.value, ps[:2 * ns].reshape(-1, 2)) if per_step else (eb.value, ee.value)
+
     def configure(self, prob):
         """Set everything from a problem description with the fields of workloads.Problem."""
         self.set_patches(prob.npatch, prob.lo, prob.hi, prob.p, prob.elems)
@@ -152,6 +168,8 @@ class Solver:
         self.set_time(prob.T, prob.n_steps)
         self.set_solver(prob.rtol, prob.max_iter, prob.scaling, prob.tree_order)
         self.set_warm_start(getattr(prob, "warm_start", 0))
+        if getattr(prob, "track_errors", False):
+            self.set_error_tracking(True)
         return self
 
     def plan(self):

@@ -72,8 +72,9 @@ __device__ void bsplines_at(int p, int el, double h, int deg, double x, double* 
 }
 
 // One block per direction d. Writes Mb, Md, Kb, C, oneD and per-patch-index source
-// integrals sD, cB, sB (see device.h Tables1D for the layout).
-__global__ void k_tables1d(Tables1D tb, int p) {
+// integrals sD, cB, sB of sin(omega x), cos(omega x) (omega = pi for the BASELINE source and
+// the homogeneous MMS, 1 for the paper's solution; see device.h Tables1D for the layout).
+__global__ void k_tables1d(Tables1D tb, int p, double omega) {
   const int d = blockIdx.x;
   const int el = tb.el[d], n = el + p, q = p + 1;
   const double h = tb.h[d];
@@ -151,7 +152,7 @@ __global__ void k_tables1d(Tables1D tb, int p) {
     double ssD = 0, scB = 0, ssB = 0;
     for (int eg = 0; eg < ne; ++eg) {
       double x = x0 + Xp[eg];
-      double sx = sin(M_PI * x), cx = cos(M_PI * x);
+      double sx = sin(omega * x), cx = cos(omega * x);
       if (i < n - 1) ssD += Wp[eg] * sx * Dv[eg * (n - 1) + i];
       scB += Wp[eg] * cx * Bv[eg * n + i];
       ssB += Wp[eg] * sx * Bv[eg * n + i];
@@ -312,7 +313,7 @@ __global__ void k_btables(DevPlan D, int64_t nbtot) {
 
 // Spatial load j_S,s = <S, w> in aug order (r and p positions; padding 0), from the
 // separable 1D source integrals. kind 1: S = (pi sx cy sz, -pi cx sy sz, 0);
-// kind 2: S = (sy sz, sx sz, sx sy).
+// kind 2: S = (sy sz, sx sz, sx sy); kind 3 (tables with omega = 1): S = (sx cy cz, -2 cx sy cz, cx cy sz).
 __device__ double load_entry(const Tables1D& tb, const Geom& G, int kind, int pidx[3], const LocalDof& A) {
   if (kind == 0) return 0.0;
   const int* i = A.i;
@@ -324,6 +325,11 @@ __device__ double load_entry(const Tables1D& tb, const Geom& G, int kind, int pi
     if (A.c == 0) return M_PI * sD(0, i[0]) * cB(1, i[1]) * sB(2, i[2]);
     if (A.c == 1) return -M_PI * cB(0, i[0]) * sD(1, i[1]) * sB(2, i[2]);
     return 0.0;
+  }
+  if (kind == 3) {
+    if (A.c == 0) return sD(0, i[0]) * cB(1, i[1]) * cB(2, i[2]);
+    if (A.c == 1) return -2.0 * cB(0, i[0]) * sD(1, i[1]) * cB(2, i[2]);
+    return cB(0, i[0]) * cB(1, i[1]) * sD(2, i[2]);
   }
   if (A.c == 0) return oD(0, i[0]) * sB(1, i[1]) * sB(2, i[2]);
   if (A.c == 1) return sB(0, i[0]) * oD(1, i[1]) * sB(2, i[2]);

@@ -33,6 +33,7 @@
 #include "solve.cu"
 #include "pcg.cu"
 #include "nd.cu"
+#include "mms.cu"
 #include "coarse_nd.h"
 
 using namespace tcg;
@@ -115,6 +116,18 @@ struct tcg_ctx {
   bool have_patches = false, have_materials = false, have_time = false;
   bool planned = false, setup_done = false, broken = false;
   int source = TCG_SOURCE_CURL_PSI;
+  // the paper's experiment (TCG_SOURCE_PAPER, mms.cu): 1D projections, Dirichlet DOF list and
+  // template values; error tracking state
+  double* proj = nullptr;
+  ProjTables ptab{};
+  int64_t *d_dlist = nullptr, *d_doff = nullptr;
+  int64_t* d_poff = nullptr;
+  double* aD0 = nullptr;
+  int64_t ndir = 0;  // Dirichlet DOFs (patch-local copies) of the paper's experiment
+  bool track = false;
+  std::vector<double*> a_prev;     // per local rank: a_loc before the step
+  double *err_part = nullptr, *err_acc = nullptr, *err_step = nullptr;
+  int err_blocks = 0;
   double src_amp = 1.0, src_freq = 1.0;  // tcg_set_source params
   double T = 1.0;
   int n_steps = 0;
@@ -155,7 +168,10 @@ struct tcg_ctx {
   int sparse = 0;
   CoarseND nd;
   struct NDDev {
-    double *FR = nullptr, *FDinv = nullptr, *Fscr = nullptr, *CW = nullptr, *Pcs = nullptr;
+    double *FR = nullptr, *FDinv = nullptr, *Fscr = nullptr;
+    // solve state per local rank (each rank runs the replicated coarse solve on its blocks)
+    std::vector<double*> CW, Pcs, pb;
+    std::vector<unsigned int*> cnt, dflow;
     int64_t fr_size = 0;
     std::vector<std::vector<int>> lvl;            // node ids per height
     std::vector<CholDesc*> ldesc;                 // per level
@@ -172,11 +188,8 @@ struct tcg_ctx {
     ItemDesc *fw = nullptr, *bw = nullptr;
     int *fw_off = nullptr, *bw_off = nullptr;     // [(level) * (nblocks + 1) + block]
     int kw = 1;                                    // forward gather sources per position
-    double* pb = nullptr;                          // backward chunk partials
-    unsigned int* cnt = nullptr;                   // backward chunk counters
     int4* node = nullptr;                          // per node: parent, #fw items, #bw items, #children's fw items
     int2* bwdep = nullptr;                         // per node: backward dependency (ancestor or -1), its item count
-    unsigned int* dflow = nullptr;                 // 3 x nodes dataflow counters (zeroed per launch)
     int nn = 0;
   } ndd;
   // stepper work items per phase: ItemDesc lists ordered by (rank, block), per-block offsets
@@ -524,9 +537,21 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
   } ev;
   cudaEvent_t e0 = ev.e[0], e1 = ev.e[1], e2 = ev.e[2], e3 = ev.e[3];
   CK(cudaEventRecord(e0, h->stream));
-  k_tables1d<<<3, 256, h->smem_tables, h->stream>>>(h->tb, pl.p);
+  k_tables1d<<<3, 256, h->smem_tables, h->stream>>>(h->tb, pl.p, h->source == TCG_SOURCE_PAPER ? 1.0 : M_PI);
   ++h->nlaunch;
   CKL();
+  if (h->source == TCG_SOURCE_PAPER) {
+    const int maxP = std::max(pl.P[0], std::max(pl.P[1], pl.P[2]));
+    int maxn = 0;
+    for (int d = 0; d < 3; ++d) maxn = std::max(maxn, pl.el[d] + pl.p);
+    k_proj1d<<<dim3(maxP, 3), 32, sizeof(double) * ((size_t)maxn * maxn + maxn), h->stream>>>(h->tb, pl.p, h->d_poff,
+                                                                                               h->d_poff + 3, h->proj);
+    ++h->nlaunch;
+    CKL();
+    if (h->track) {
+      CK(cudaMemsetAsync(h->err_acc, 0, 8 * sizeof(double), h->stream));
+    }
+  }
   for (auto& R : h->rd) {
     CK(cudaMemsetAsync(R.derr, 0, sizeof(DevError), h->stream));
     if (R.ntiles > 0) {
@@ -535,7 +560,16 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
       ++h->nlaunch;
       CKL();
     }
-    if (!R.plist.empty()) {
+    if (!R.plist.empty() && h->source == TCG_SOURCE_PAPER) {
+      // a(0) = amp Pi_h S, Dirichlet template, load template with the lifting folded in (mms.cu)
+      k_mms_init<<<(unsigned)R.plist.size(), 256, 0, h->stream>>>(R.D, h->G, h->ptab, h->src_amp, R.d_plist, R.a_loc,
+                                                                   h->d_dlist, h->d_doff, h->aD0);
+      ++h->nlaunch;
+      k_mms_load<<<(unsigned)R.plist.size(), 256, 0, h->stream>>>(R.D, h->tb, h->G, 1.0 / dt, R.d_plist, h->d_dlist,
+                                                                   h->d_doff, h->aD0, R.JS);
+      ++h->nlaunch;
+      CKL();
+    } else if (!R.plist.empty()) {
       k_load_vector<<<(unsigned)R.plist.size(), 256, 0, h->stream>>>(R.D, h->tb, h->G, h->source, R.JS, R.d_plist);
       ++h->nlaunch;
       CKL();
@@ -628,7 +662,8 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
       ++h->nlaunch;
       CKL();
     }
-    CK(cudaMemsetAsync(R.a_loc, 0, sizeof(double) * (size_t)pl.npatch * pl.nloc, h->stream));
+    if (h->source != TCG_SOURCE_PAPER)  // (the paper's experiment starts from a(0) = amp Pi_h S, set above)
+      CK(cudaMemsetAsync(R.a_loc, 0, sizeof(double) * (size_t)pl.npatch * pl.nloc, h->stream));
   }
   CK(cudaEventRecord(e3, h->stream));
   TRY(check_err(h));
@@ -777,8 +812,16 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
   TRY(dalloc(h, &g.FR, std::max<int64_t>(fa, 1)));
   TRY(dalloc(h, &g.FDinv, std::max<int64_t>(fd, 1)));
   TRY(dalloc(h, &g.Fscr, std::max<int64_t>(fd, 1)));
-  TRY(dzero(h, &g.CW, std::max<int64_t>(fv, 1)));
-  TRY(dzero(h, &g.Pcs, std::max<int64_t>(pl.nc, 1)));
+  const int nlocal = (h->world > 1) ? 1 : h->vranks;  // local ranks (same order as h->rd)
+  g.CW.assign(nlocal, nullptr);
+  g.Pcs.assign(nlocal, nullptr);
+  g.pb.assign(nlocal, nullptr);
+  g.cnt.assign(nlocal, nullptr);
+  g.dflow.assign(nlocal, nullptr);
+  for (int li = 0; li < nlocal; ++li) {
+    TRY(dzero(h, &g.CW[li], std::max<int64_t>(fv, 1)));
+    TRY(dzero(h, &g.Pcs[li], std::max<int64_t>(pl.nc, 1)));
+  }
   std::vector<int> tv(nn), tt(nn), nvv(nn), nbv(nn), par(nn), zero(nn, 0);
   for (int x = 0; x < nn; ++x) {
     tv[x] = N[x].TV;
@@ -1062,15 +1105,15 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
     }
     TRY(dupload(h, &g.node, nodev));
     TRY(dupload(h, &g.bwdep, dep));
-    TRY(dzero(h, &g.dflow, (size_t)3 * std::max(nn, 1)));
+    for (auto& df : g.dflow) TRY(dzero(h, &df, (size_t)3 * std::max(nn, 1)));
     g.nn = nn;
   }
   TRY(dupload(h, &g.fw, fwi));
   TRY(dupload(h, &g.bw, bwi));
   TRY(dupload(h, &g.fw_off, fwo));
   TRY(dupload(h, &g.bw_off, bwo));
-  TRY(dzero(h, &g.pb, std::max<int64_t>(npb, 1) * TS));
-  TRY(dzero(h, &g.cnt, std::max(ncnt, 1)));
+  for (auto& q : g.pb) TRY(dzero(h, &q, std::max<int64_t>(npb, 1) * TS));
+  for (auto& q : g.cnt) TRY(dzero(h, &q, std::max(ncnt, 1)));
   return TCG_OK;
 }
 
@@ -1297,6 +1340,36 @@ static tcg_status do_setup(tcg_ctx* h) {
     h->smem_tables = sizeof(double) * (2 * (pl.p + 1) + (size_t)maxel * (pl.p + 1) * (3 * maxn + 2));
   }
 
+  if (h->source == TCG_SOURCE_PAPER) {
+    // 1D projection tables (cos: n per patch index, sin: n-1), Dirichlet DOF list per patch
+    std::vector<int64_t> poff(6);
+    int64_t o = 0;
+    for (int d = 0; d < 3; ++d) {
+      const int n = pl.el[d] + pl.p;
+      if (n > kProjMaxN) return fail(h, TCG_EINVAL, "source 3: elements + p per patch and direction must be <= 72");
+      poff[d] = o;
+      o += (int64_t)pl.P[d] * n;
+      poff[3 + d] = o;
+      o += (int64_t)pl.P[d] * (n - 1);
+      h->ptab.off_cos[d] = poff[d];
+      h->ptab.off_sin[d] = poff[3 + d];
+      h->ptab.n[d] = n;
+    }
+    TRY(dalloc(h, &h->proj, o));
+    TRY(dupload(h, &h->d_poff, poff));
+    h->ptab.base = h->proj;
+    std::vector<int64_t> dl, doff(1, 0);
+    for (int s2 = 0; s2 < P; ++s2) {
+      for (int a = 0; a < pl.nloc; ++a)
+        if (pl.part[pl.local_to_global(s2, a)] == PART_DIR) dl.push_back((int64_t)s2 * pl.nloc + a);
+      doff.push_back((int64_t)dl.size());
+    }
+    h->ndir = (int64_t)dl.size();
+    if (dl.empty()) dl.push_back(0);
+    TRY(dupload(h, &h->d_dlist, dl));
+    TRY(dupload(h, &h->d_doff, doff));
+    TRY(dzero(h, &h->aD0, dl.size()));
+  }
   hm.mark("tables");
   // ---- shared memory and persistent grid ----
   int dev_sms = 148;
@@ -1354,7 +1427,7 @@ static tcg_status do_setup(tcg_ctx* h) {
   {
     const char* ce = getenv("TCG_COARSE");  // "dense", "sparse", default auto
     const bool want = ce ? (std::strcmp(ce, "sparse") == 0) : (pl.nc > 8192);
-    h->sparse = (want && NR == 1 && pl.nc > 0) ? 1 : 0;
+    h->sparse = (want && pl.nc > 0) ? 1 : 0;  // several ranks: every rank runs the whole solve
   }
   // ---- work items per rank, dealt to the rank's persistent blocks (LPT) ----
   std::vector<int> crow_owner(std::max(Tc, 1));
@@ -1371,6 +1444,7 @@ static tcg_status do_setup(tcg_ctx* h) {
         d.I = I;
         d.Ti = Ti[s]; d.Tb = Tb[s]; d.Tp = Tp[s]; d.T = T[s];
         d.nb = nb[s]; d.np = np[s];
+        d.ni = pl.pp[s].ni;
         d.a_off = a_off[s]; d.vec_off = vec_off[s]; d.b_off = b_off[s]; d.p_off = p_off[s]; d.sbb_off = sbb_off[s];
         return d;
       };
@@ -1477,7 +1551,8 @@ static tcg_status do_setup(tcg_ctx* h) {
       // tile prefetch buffer first (bulk copies of the next phase's first tiles during barriers)
       {
         const char* ne = getenv("TCG_NPF");
-        int npf = ne ? std::max(0, std::min(2, atoi(ne))) : 1;  // 2 tiles shrink L1 too much on the HBM-bound configs
+        // RS tiles: the tile ring of the P1/P5/SY GEMVs (pcg.cu); fewer: first-tile prefetch only
+        int npf = ne ? std::max(0, std::min(RS, atoi(ne))) : RS;
         while (npf > 0 && (int64_t)(h->smem_pcg + (size_t)npf * TSZ * sizeof(double)) > budget) --npf;
         h->npf = npf;
         budget -= (int64_t)npf * TSZ * sizeof(double);
@@ -1796,6 +1871,10 @@ static StepArgs step_args(tcg_ctx* h) {
   A.cache_lam = h->cache_lam;
   A.scratch = (int)(h->smem_pcg / sizeof(double));
   A.npf = h->npf;
+  {
+    const char* e = getenv("TCG_L2PF");
+    A.l2pf = e ? std::max(0, atoi(e)) : 6;
+  }
   A.warm = h->warm;
   A.warm_base = (int)h->warm_base;
   for (auto& R : h->rd) {
@@ -1819,13 +1898,16 @@ static StepArgs step_args(tcg_ctx* h) {
     A.cf_kw = g.kw;
     A.cf_vl = g.vl;
     A.cf_bl = g.bl;
-    A.CW = g.CW;
-    A.Pcs = g.Pcs;
-    A.cf_pb = g.pb;
-    A.cf_cnt = g.cnt;
+    for (size_t li = 0; li < h->rd.size(); ++li) {
+      const int r = h->rd[li].r;
+      A.CW[r] = g.CW[li];
+      A.Pcs[r] = g.Pcs[li];
+      A.cf_pb[r] = g.pb[li];
+      A.cf_cnt[r] = g.cnt[li];
+      A.cf_dflow[r] = g.dflow[li];
+    }
     A.cf_node = g.node;
     A.cf_bwdep = g.bwdep;
-    A.cf_dflow = g.dflow;
     A.cf_nn = g.nn;
     A.cf_sync = getenv("TCG_CF_LEVELSYNC") && atoi(getenv("TCG_CF_LEVELSYNC")) != 0;
   }
@@ -1840,6 +1922,9 @@ static StepArgs step_args(tcg_ctx* h) {
   A.sys_scope = (h->world > 1) ? 1 : 0;
   A.lam_chunk = h->lam_chunk;
   A.source = h->source;
+  A.dlist = h->d_dlist;
+  A.aD0 = h->aD0;
+  A.nd = (h->source == TCG_SOURCE_PAPER) ? h->ndir : 0;
   A.src_amp = h->src_amp;
   A.src_freq = h->src_freq;
   A.dt = h->T / h->n_steps;
@@ -1874,7 +1959,8 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   if (n <= 0) return TCG_OK;
   if (h->steps_done + n > h->n_steps) return fail(h, TCG_EINVAL, "more steps than set_time allows (n_steps)");
   for (auto& R : h->rd) CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), h->stream));
-  if (h->sparse) CK(cudaMemsetAsync(h->ndd.dflow, 0, 3 * sizeof(unsigned int) * std::max(h->ndd.nn, 1), h->stream));
+  if (h->sparse)
+    for (auto* df : h->ndd.dflow) CK(cudaMemsetAsync(df, 0, 3 * sizeof(unsigned int) * std::max(h->ndd.nn, 1), h->stream));
   if (h->warm)
     for (auto& R : h->rd)
       if (!R.Wr) {  // warm-start rings: k solutions and k F-products at the lambda level
@@ -2016,8 +2102,8 @@ tcg_status tcg_set_materials(tcg_handle h, const double* sigma, const double* nu
 tcg_status tcg_set_source(tcg_handle h, int kind, const double* params, size_t nparams) {
   if (!h) return TCG_EINVAL;
   if (h->setup_done) return fail(h, TCG_ESTATE, "set_source after setup");
-  if (kind < 0 || kind > 2) return fail(h, TCG_EINVAL, "unknown source kind");
-  const size_t maxp = kind == 1 ? 2 : (kind == 2 ? 1 : 0);
+  if (kind < 0 || kind > 3) return fail(h, TCG_EINVAL, "unknown source kind");
+  const size_t maxp = kind == 1 ? 2 : (kind >= 2 ? 1 : 0);
   if (nparams > maxp || (nparams > 0 && !params))
     return fail(h, TCG_EINVAL, "source kind " + std::to_string(kind) + " takes at most " + std::to_string(maxp) + " parameters");
   double amp = 1.0, freq = 1.0;
@@ -2057,6 +2143,39 @@ tcg_status tcg_set_warm_start(tcg_handle h, int on) {
   if (on < 0 || on > KW) return fail(h, TCG_EINVAL, "warm start subspace dimension must be in [0, " + std::to_string(KW) + "]");
   if (on != h->warm) h->warm_base = h->steps_done;  // a new subspace size restarts the history
   h->warm = on;
+  return TCG_OK;
+}
+
+tcg_status tcg_set_error_tracking(tcg_handle h, int on) {
+  if (!h) return TCG_EINVAL;
+  if (on && h->source != TCG_SOURCE_PAPER) return fail(h, TCG_EINVAL, "error tracking needs TCG_SOURCE_PAPER (the exact solution)");
+  if (on && h->world > 1) return fail(h, TCG_EINVAL, "error tracking needs a single-process handle");
+  if (h->setup_done && h->steps_done > 0) return fail(h, TCG_ESTATE, "enable error tracking before the first step");
+  if (on && !h->err_acc) {
+    cudaSetDevice(h->device);
+    if (!h->stream) {
+      CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      h->own_stream = true;
+    }
+    TRY(dzero(h, &h->err_acc, 8));
+  }
+  h->track = on != 0;
+  return TCG_OK;
+}
+
+tcg_status tcg_get_errors(tcg_handle h, double* eps_B, double* eps_E, double* per_step, size_t nsteps) {
+  if (!h) return TCG_EINVAL;
+  if (!h->track || !h->err_acc) return fail(h, TCG_ESTATE, "error tracking is off");
+  if (nsteps > (size_t)h->steps_done) return fail(h, TCG_EINVAL, "only " + std::to_string(h->steps_done) + " steps done");
+  cudaSetDevice(h->device);
+  double acc[8];
+  CK(cudaMemcpyAsync(acc, h->err_acc, sizeof acc, cudaMemcpyDeviceToHost, h->stream));
+  if (per_step && nsteps > 0)
+    CK(cudaMemcpyAsync(per_step, h->err_step, 2 * nsteps * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  h->d2h_bytes += (int64_t)(sizeof acc + (per_step ? 2 * nsteps * sizeof(double) : 0));
+  if (eps_B) *eps_B = h->steps_done ? acc[3] : 0.0;
+  if (eps_E) *eps_E = h->steps_done ? acc[4] : 0.0;
   return TCG_OK;
 }
 
@@ -2131,7 +2250,47 @@ tcg_status tcg_step(tcg_handle h, int n) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, h->stream);
-  tcg_status s = do_steps(h, n);
+  tcg_status s = TCG_OK;
+  if (h->track) {
+    // the paper's error norms (mms.cu): one step per launch (so every patch's
+    // coefficients, insulators included, are recovered), then the error kernels
+    const Plan& pl = h->plan;
+    const size_t nall = (size_t)pl.npatch * pl.nloc;
+    if (h->a_prev.empty()) {
+      h->a_prev.assign(h->rd.size(), nullptr);
+      for (auto& q : h->a_prev) {
+        s = dalloc(h, &q, nall);
+        if (s != TCG_OK) return s;
+      }
+      int nbk = 0;
+      for (auto& R : h->rd) nbk += (int)R.plist.size() * pl.el[2];
+      h->err_blocks = nbk;
+      if ((s = dalloc(h, &h->err_part, 2 * (size_t)std::max(nbk, 1))) != TCG_OK) return s;
+      if ((s = dalloc(h, &h->err_step, 2 * (size_t)h->n_steps)) != TCG_OK) return s;
+    }
+    const double dt = h->T / h->n_steps;
+    for (int i = 0; i < n && s == TCG_OK; ++i) {
+      for (size_t li = 0; li < h->rd.size(); ++li)
+        CK(cudaMemcpyAsync(h->a_prev[li], h->rd[li].a_loc, nall * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+      s = do_steps(h, 1);
+      if (s != TCG_OK) break;
+      int64_t boff = 0;
+      for (size_t li = 0; li < h->rd.size(); ++li) {
+        RankDev& R = h->rd[li];
+        if (R.plist.empty()) continue;
+        k_mms_errors<<<dim3((unsigned)R.plist.size(), pl.el[2]), 256, 0, h->stream>>>(
+            R.D, h->G, h->tb, h->steps_done * dt, dt, h->src_amp, R.d_plist, R.a_loc, h->a_prev[li], h->err_part + 2 * boff);
+        ++h->nlaunch;
+        boff += (int64_t)R.plist.size() * pl.el[2];
+      }
+      k_mms_accumulate<<<1, 32, 0, h->stream>>>(h->err_part, h->err_blocks, dt, h->err_acc, h->err_step,
+                                                 (int)h->steps_done - 1);
+      ++h->nlaunch;
+      CKL();
+    }
+  } else {
+    s = do_steps(h, n);
+  }
   if (s == TCG_OK) {
     cudaEventRecord(e1, h->stream);
     cudaEventSynchronize(e1);
@@ -2294,7 +2453,8 @@ static tcg_status run_fapply(tcg_ctx* h, int n, double* ms) {
   if (h->world > 1) return fail(h, TCG_EINVAL, "F-apply hooks need a single-process handle");
   CK(cudaSetDevice(h->device));
   for (auto& R : h->rd) CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), h->stream));
-  if (h->sparse) CK(cudaMemsetAsync(h->ndd.dflow, 0, 3 * sizeof(unsigned int) * std::max(h->ndd.nn, 1), h->stream));
+  if (h->sparse)
+    for (auto* df : h->ndd.dflow) CK(cudaMemsetAsync(df, 0, 3 * sizeof(unsigned int) * std::max(h->ndd.nn, 1), h->stream));
   if (h->warm)
     for (auto& R : h->rd)
       if (!R.Wr) {  // warm-start rings: k solutions and k F-products at the lambda level
@@ -2401,7 +2561,7 @@ tcg_status tcg_debug_array(tcg_handle h, int what, int idx, double* out, size_t 
   } else if (what == 8) {  // sparse coarse solution (by primal group) and forward vectors
     if (!h->sparse) return fail(h, TCG_ESTATE, "dense coarse");
     std::vector<double> a((size_t)h->plan.nc);
-    CK(cudaMemcpy(a.data(), h->ndd.Pcs, sizeof(double) * a.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(a.data(), h->ndd.Pcs[0], sizeof(double) * a.size(), cudaMemcpyDeviceToHost));
     tmp = a;
   } else if (what == 9) {  // sparse coarse tree: per node (height, n_V, n_B, T_V, T_B)
     for (const auto& n : h->nd.nd) {

@@ -1,0 +1,17 @@
+#!/bin/bash
+# A/B of stepper variants inside ONE box call (box-to-box variation is ~15 %):
+# round-1 library (ab_base/libtcg_round1.so), padding-predicated loads (TCG_NPF=1), tile ring (default)
+mkdir -p gpurun_out
+for rep in 1 2; do
+for v in "TCG_LIBPATH=$PWD/ab_base/libtcg_round1.so" "TCG_NPF=1" "TCG_NPF=2"; do
+  for c in ${AB_CFGS:-cfg5 cfg3 cfg4}; do
+    echo "== $v $c rep $rep" >> gpurun_out/ab.txt
+    env $v timeout 300 python bench.py --config $c --no-cpu-baseline --no-extras --e2e-steps 0 --steps 3 --warmup 3 2>/dev/null | python -c "
+import json,sys
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print('value', round(d['value'],2), 'roof', round(d['roofline']['frac'],4), 'fapply_us', round(d['fapply']['us_per_apply'],1), 'clk', d['clocks']['sm_mhz'], d['clocks']['reasons'])
+" >> gpurun_out/ab.txt
+  done
+done
+done
