@@ -1449,6 +1449,9 @@ static tcg_status do_setup(tcg_ctx* h) {
         return d;
       };
       ItemLists p1(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR);
+      // whole-patch dealing when there are many patches per block (cfg5: 2048 patches)
+      const bool grp = (int64_t)P >= 2 * (int64_t)NR * h->nbr && !(getenv("TCG_NO_GROUP") && atoi(getenv("TCG_NO_GROUP")));
+      const bool grp5 = grp && !(getenv("TCG_P5_SPLIT") && atoi(getenv("TCG_P5_SPLIT")));
       for (int s = 0; s < P; ++s) {
         const int r = owner[s];
         const int Trs = Ti[s] + Tb[s];
@@ -1467,6 +1470,12 @@ static tcg_status do_setup(tcg_ctx* h) {
           rhs.per_rank[r].push_back({T[s] * TS / 8, desc(s, -1)});
         for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
         for (int J = 0; J < Tb[s]; ++J) {
+          if (grp5 && np[s] > 0) {  // whole-patch dealing: one item per column (fewer item starts)
+            ItemDesc d = desc(s, J);
+            d.part = 2;
+            p5.per_rank[r].push_back({Tb[s] - J + Tp[s], d});
+            continue;
+          }
           p5.per_rank[r].push_back({Tb[s] - J, desc(s, J)});
           if (np[s] > 0) {
             ItemDesc d = desc(s, J);
@@ -1508,8 +1517,6 @@ static tcg_status do_setup(tcg_ctx* h) {
           pcv.per_rank[crow_owner[I]].push_back({std::min(Tc, (c + 1) * ch) - c * ch, d});
         }
       // fixed per-item overhead (tile units) of the latency-bound item phases
-      // whole-patch dealing when there are many patches per block (cfg5: 2048 patches)
-      const bool grp = (int64_t)P >= 2 * (int64_t)NR * h->nbr && !(getenv("TCG_NO_GROUP") && atoi(getenv("TCG_NO_GROUP")));
       TRY(deal_items(h, p1, PH_P1, 2, grp));
       TRY(deal_items(h, pcv, PH_PC, 2));
       TRY(deal_items(h, p5, PH_P5, 2, grp));
@@ -1551,8 +1558,9 @@ static tcg_status do_setup(tcg_ctx* h) {
       // tile prefetch buffer first (bulk copies of the next phase's first tiles during barriers)
       {
         const char* ne = getenv("TCG_NPF");
-        // RS tiles: the tile ring of the P1/P5/SY GEMVs (pcg.cu); fewer: first-tile prefetch only
-        int npf = ne ? std::max(0, std::min(RS, atoi(ne))) : RS;
+        // 1: the first tile of each phase during the barrier (default); RS: the tile ring of the
+        // P1/P5/SY GEMVs (pcg.cu; measured slower on cfg3-cfg5, profiles/round2_notes.md)
+        int npf = ne ? std::max(0, std::min(RS, atoi(ne))) : 1;
         while (npf > 0 && (int64_t)(h->smem_pcg + (size_t)npf * TSZ * sizeof(double)) > budget) --npf;
         h->npf = npf;
         budget -= (int64_t)npf * TSZ * sizeof(double);
@@ -1873,7 +1881,7 @@ static StepArgs step_args(tcg_ctx* h) {
   A.npf = h->npf;
   {
     const char* e = getenv("TCG_L2PF");
-    A.l2pf = e ? std::max(0, atoi(e)) : 6;
+    A.l2pf = e ? std::max(0, atoi(e)) : 0;
   }
   A.warm = h->warm;
   A.warm_base = (int)h->warm_base;

@@ -487,7 +487,8 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
                                           int npf = 0, int gat = 1, bool ring = false, RG rg = RG(), RR rr = RR()) {
   const int J = it.I, Ti = it.Ti, Tb = it.Tb, np = it.np, nb = it.nb;
   const bool ppart = (it.part & 1) != 0;
-  const int I0 = ppart ? Tb : J, I1 = ppart ? Tb + it.Tp : Tb;
+  const bool merged = (it.part & 2) != 0;  // whole column J: X_bb^T tiles then Phi_b tiles (-> Y)
+  const int I0 = ppart ? Tb : J, I1 = (ppart || merged) ? Tb + it.Tp : Tb;
   // the whole b (part 0) or p (part 1) input of the patch, reused by the next item of the
   // same patch and part (gat = false)
   const int G0 = ppart ? Tb : 0;
@@ -506,7 +507,8 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
     if (gat)
       for (int e = (gat == 2 ? 0 : (I0 - G0) * TS) + threadIdx.x; e < (I1 - G0) * TS; e += blockDim.x) {
         double val;
-        if (!ppart) val = ldcg(W + vo + e);
+        if (merged) val = (e < Tb * TS) ? ldcg(W + vo + e) : ((e - Tb * TS < np) ? -pc(grp[e - Tb * TS]) : 0.0);
+        else if (!ppart) val = ldcg(W + vo + e);
         else val = (e < np) ? -pc(grp[e]) : 0.0;
         sfull[e] = val;
       }
@@ -525,9 +527,7 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
     contrib = vj * acc;
   }
   SUBSTAMP(2);
-  const double bsum = block_sum(contrib, red);
-  SUBSTAMP(3);
-  return bsum;
+  return contrib;  // this thread's share of v_J . y_J; the caller block-sums once per phase
 }
 
 // ---- P7 / R5: symmetric S_bb apply, one row block I of one patch --------------------------
@@ -603,7 +603,7 @@ __device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr
     PW[it.vec_off + (int64_t)(Ti + I) * TS + threadIdx.x] = v;
     contrib = u[I * TS + threadIdx.x] * v;
   }
-  return block_sum(contrib, red);
+  return contrib;  // this thread's share of u^T S_bb u; the caller block-sums once per phase
 }
 
 // ---- R2: forward item (conductor patch s, aug row block I): Z_I = X_IJ f_J / f_p - Phi^T f_r --
@@ -1004,6 +1004,10 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
 #define FOR_ITEMS(ph, var)                                  \
   for (int j_##var = 0; j_##var < s_icnt[ph]; ++j_##var)    \
     if (const ItemDesc& var = s_ip[ph][j_##var]; true)
+// the same for the per-iteration GEMV phases, with the L2 prefetch of coming tiles (pf_hook)
+#define FOR_ITEMS_PF(ph, var)                               \
+  for (int j_##var = 0; j_##var < s_icnt[ph]; ++j_##var)    \
+    if (const ItemDesc& var = s_ip[ph][j_##var]; pf_hook(ph, j_##var))
 
 // =======================================================================================
 // Persistent cooperative time stepper: A.nsteps implicit-Euler steps in one launch, over
@@ -1149,7 +1153,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         n = min(J1 - J0, A.npf);
         for (int q = 0; q < n; ++q) src[q] = A.Sinv[me] + ((int64_t)w.s * D.Tc + J0 + q) * TSZ;
       } else if (ph == PH_P5) {
-        const int I0 = (w.part & 1) ? w.Tb : w.I, I1 = (w.part & 1) ? w.Tb + w.Tp : w.Tb;
+        const int I0 = (w.part & 1) ? w.Tb : w.I, I1 = (w.part & 3) ? w.Tb + w.Tp : w.Tb;
         n = min(I1 - I0, A.npf);
         for (int q = 0; q < n; ++q) src[q] = Xr + w.a_off + tri_off(w.Ti + I0 + q, w.Ti + w.I);
       } else if (ph == PH_SY) {
@@ -1187,7 +1191,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     }
     if (ph == PH_P5) {
       const bool pp5 = (w.part & 1) != 0;
-      const int I = (pp5 ? w.Tb : w.I) + k, I1 = pp5 ? w.Tb + w.Tp : w.Tb;
+      const int I = (pp5 ? w.Tb : w.I) + k, I1 = (w.part & 3) ? w.Tb + w.Tp : w.Tb;
       if (I >= I1) return nullptr;
       const int rv = I < w.Tb ? min(TS, w.nb - I * TS) : min(TS, w.np - (I - w.Tb) * TS);
       bytes = (uint32_t)rv * TS * sizeof(double);
@@ -1254,6 +1258,42 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     if (threadIdx.x == 0) ring_produce(rcons);
   };
   auto is_ring_ph = [&](int ph) { return ring_on && (ph == PH_P1 || ph == PH_P5 || ph == PH_SY); };
+  // (experiment, TCG_L2PF > 0: thread 0 bulk-prefetches tiles into L2; measured slower)
+  auto pf_l2_item = [&](int ph, int j, int k0, int k1) {
+    if (j >= s_icnt[ph]) return;
+    const ItemDesc& w = s_ip[ph][j];
+    for (int k = k0; k < k1; ++k) {
+      uint32_t bytes = 0;
+      const double* src = ring_tile(ph, w, k, bytes);
+      if (!src) break;
+      prefetch_l2_bulk(src, bytes);
+    }
+  };
+  // At the start of item j every thread prefetches into L2 its own rows of the first tiles of
+  // item j + 1, so their HBM latency overlaps item j instead of opening item j + 1 (a block
+  // streams its items one after the other; ~1 us of first-tile latency per item otherwise).
+  const int pf_next = (c_step_flags & 8) ? 2 : 0;  // opt-in (TCG_STEP_FLAGS bit 3): measured slower
+  const int warp_ = threadIdx.x >> 5, lane_ = threadIdx.x & 31;
+  auto pf_hook = [&](int ph, int j) {
+    if (A.l2pf > 0 && !ring_on && threadIdx.x == 0) {
+      pf_l2_item(ph, j, 2, 1 << 20);
+      pf_l2_item(ph, j + 1, 0, A.l2pf);
+    }
+    if (pf_next > 0 && !ring_on && j + 1 < s_icnt[ph]) {
+      const ItemDesc& w = s_ip[ph][j + 1];
+      for (int k = 0; k < pf_next; ++k) {
+        uint32_t bytes = 0;
+        const double* src = ring_tile(ph, w, k, bytes);
+        if (!src) break;
+        const int rows = (int)(bytes / (TS * sizeof(double)));
+        const double* t = src + warp_ * 8 * TS + 2 * lane_;
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (warp_ * 8 + r < rows && (lane_ & 3) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(t + r * TS));
+      }
+    }
+    return true;
+  };
   auto hook = [&](int ph) { return [&, ph]() { pf_issue(ph); }; };
   int64_t hoff = A.hist_off;
   int total_status = 0;
@@ -1266,8 +1306,15 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     // overwrite that thread 0 issues after the barrier's __syncthreads (WAR across proxies)
     if (A.npf > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     const double r = grid_barrier(A, me, bl, round, reduce, v, bcast, [&]() {
-      if (is_ring_ph(ph_next)) ring_start(ph_next);
-      else pf_issue(ph_next);
+      if (is_ring_ph(ph_next)) {
+        ring_start(ph_next);
+      } else {
+        pf_issue(ph_next);
+        if (A.l2pf > 0 && (ph_next == PH_P1 || ph_next == PH_P5 || ph_next == PH_SY)) {
+          pf_l2_item(ph_next, 0, 1, A.l2pf + 2);
+          pf_l2_item(ph_next, 1, 0, A.l2pf);
+        }
+      }
     });
     npf_cur = pf_wait();
     return r;
@@ -1356,7 +1403,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     const int step = -1, it = -1;  // no stamps
     (void)step;
     (void)it;
-    FOR_ITEMS(PH_P1, w)
+    FOR_ITEMS_PF(PH_P1, w)
       p1_item(w, Xr,
               [&](const ItemDesc& iw, int64_t bb, int pos) {
                 const BPos q = bget(iw, bb, pos);
@@ -1366,7 +1413,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     bar(PH_PC, false, 0.0);
     COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
     bar(PH_P5, false, 0.0);
-    FOR_ITEMS(PH_P5, w)
+    FOR_ITEMS_PF(PH_P5, w)
       p5_item(w, Xr, A.XW[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
               red, nullptr, PF0(j_w), GAT(PH_P5, w), ring_on, rget, rrel);
     bar(-1, false, 0.0);
@@ -1392,7 +1439,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     if (A.dbg_stop == 1) break;
     SSTAMP(3);
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
-    FOR_ITEMS(PH_P5, w)
+    FOR_ITEMS_PF(PH_P5, w)
       p5_item(w, Xr, A.Z[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
               red, nullptr, PF0(j_w), GAT(PH_P5, w), ring_on, rget, rrel);
     bar(PH_SY, false, 0.0);
@@ -1404,7 +1451,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     double rho0;
     {
       double loc = 0.0;
-      FOR_ITEMS(PH_SY, w)
+      FOR_ITEMS_PF(PH_SY, w)
         loc += symv_item(w, Sr, A.PW[me],
                          [&](const ItemDesc& iw, int64_t bb, int pos) {
                            const BPos q = bget(iw, bb, pos);
@@ -1418,6 +1465,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         A.lam[me][k] = 0.0;
         if (A.warm) A.dsave[me][k] = dk;
       }
+      loc = block_sum(loc, red);
       rho0 = bar(nW > 0 ? -1 : PH_P1, true, loc);  // W1 runs first on a warm step
     }
     SSTAMP(5);
@@ -1549,13 +1597,14 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       bar(PH_SY, false, 0.0);
       // ---- W2: z0 = M^-1 r0, rho = r0^T z0 ----
       double loc = 0.0;
-      FOR_ITEMS(PH_SY, w)
+      FOR_ITEMS_PF(PH_SY, w)
         loc += symv_item(w, Sr, A.PW[me],
                          [&](const ItemDesc& iw, int64_t bb, int pos) {
                            const BPos q = bget(iw, bb, pos);
                            return q.aown * q.sign * ldcg(A.r[1][lown(q.k)] + q.k);
                          },
                          smw, red, PF0(j_w), GAT(PH_SY, w), ring_on, rget, rrel);
+      loc = block_sum(loc, red);
       rz = bar(PH_P1, true, loc);
       rho = rz;
       rp = 1;
@@ -1581,7 +1630,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           return q.aown * ldcg(A.PW[me] + own_idx(iw, pos)) + q.apart * ldcg(A.PW[pown(ppatch(bb))] + q.part) +
                  q.sign * beta * ldcg(pprev[lown(q.k)] + q.k);
         };
-        FOR_ITEMS(PH_P1, w) {
+        FOR_ITEMS_PF(PH_P1, w) {
           ITIME_BEGIN
           p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w), ring_on, rget, rrel);
           ITIME_END(PH_P1, j_w)
@@ -1604,7 +1653,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       double pq;
       {
         double loc = 0.0;
-        FOR_ITEMS(PH_P5, w) {
+        FOR_ITEMS_PF(PH_P5, w) {
           ITIME_BEGIN
           loc += p5_item(w, Xr, A.XW[me], D.p_grp, pcf,
                          [&](const ItemDesc& iw, int64_t bb, int pos) {
@@ -1617,6 +1666,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           ITIME_END(PH_P5, j_w)
         }
         WSTAMP(2);
+        loc = block_sum(loc, red);
         pq = bar(PH_SY, true, loc);
       }
       TSTAMP(3);
@@ -1640,7 +1690,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           yd = yv(pown(lpat_p(kq)), lidx_p(kq)) - yv(pown(lpat_m(kq)), lidx_m(kq));
         }
         double loc = 0.0;
-        FOR_ITEMS(PH_SY, w) {
+        FOR_ITEMS_PF(PH_SY, w) {
           ITIME_BEGIN
           loc += symv_item(w, Sr, A.PW[me], unew, smw, red, PF0(j_w), GAT(PH_SY, w), ring_on, rget, rrel);
           ITIME_END(PH_SY, j_w)
@@ -1654,6 +1704,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           rn[k] = ldcg(rc[me] + k) - alpha * (yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k)));
         }
         WSTAMP(3);
+        loc = block_sum(loc, red);
         rz = bar(PH_P1, true, loc);
       }
       TSTAMP(4);
@@ -1693,7 +1744,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     }
     SSTAMP(6);
     // ---- E1 v = B^T lambda ; w, -Phi^T v ----
-    FOR_ITEMS(PH_P1, w)
+    FOR_ITEMS_PF(PH_P1, w)
       p1_item(w, Xr,
               [&](const ItemDesc& iw, int64_t bb, int pos) {
                 const BPos q = bget(iw, bb, pos);
