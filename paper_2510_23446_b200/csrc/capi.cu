@@ -793,7 +793,11 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
   HostMarks hm;
   hm.line = " [sparse coarse]";
   nd = CoarseND();
-  nd.build(pl);
+  {
+    // leaf boxes of up to 32 patches (TCG_ND_LEAF): measured on cfg4 / cfg5, profiles/round2_notes.md
+    const char* e = getenv("TCG_ND_LEAF");
+    nd.build(pl, e ? std::max(1, atoi(e)) : 32);
+  }
   hm.mark("nd-build");
   const auto& N = nd.nd;
   const int nn = (int)N.size();
@@ -1520,7 +1524,10 @@ static tcg_status do_setup(tcg_ctx* h) {
       TRY(deal_items(h, p1, PH_P1, 2, grp));
       TRY(deal_items(h, pcv, PH_PC, 2));
       TRY(deal_items(h, p5, PH_P5, 2, grp));
-      TRY(deal_items(h, sy, PH_SY, 2));  // (grouping the S_bb rows of a patch measured slower)
+      // S_bb rows are dealt one by one: whole-patch groups (one u gather per patch,
+      // TCG_SY_GROUP=1) measured slower on cfg5 (patch-granular imbalance; round2_notes.md)
+      const bool grp_sy = grp && getenv("TCG_SY_GROUP") && atoi(getenv("TCG_SY_GROUP")) != 0;
+      TRY(deal_items(h, sy, PH_SY, 2, grp_sy));
       TRY(deal_items(h, fw, PH_FW, 2));
       TRY(deal_items(h, fwa, PH_FWA, 2));
       TRY(deal_items(h, bw, PH_BW, 2));

@@ -20,19 +20,37 @@ namespace tcg {
 // -------------------------------------------------------------------------------------
 // 64x64 tile GEMM on DMMA: C = A B^T (mode 0) or C -= A B^T (mode 1). 128 threads.
 // -------------------------------------------------------------------------------------
-__device__ __forceinline__ void stage_tile(const double* __restrict__ g, double* s) {
-  for (int e = threadIdx.x; e < TSZ / 2; e += blockDim.x) {
-    int r = e / 32, c2 = e % 32;
-    double2 v = reinterpret_cast<const double2*>(g)[e];
-    s[r * SPAD + 2 * c2] = v.x;
-    s[r * SPAD + 2 * c2 + 1] = v.y;
+
+// ---- cp.async-staged DMMA tile products (two-stage pipeline over a K loop of tiles) -------
+// Tiles are copied untransposed (row-major, row stride SPAD, 16-byte cp.async chunks); the
+// fragment loads pick the operand orientation: A as [m][k] (AT = false) or as the transpose
+// of a [k][m] tile (AT = true); B as [k][n] (BT = false) or as the transpose of [n][k]
+// (BT = true). SPAD = 68: every orientation reads conflict-free half-warps.
+__device__ __forceinline__ uint32_t cvta_s(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(cvta_s(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void stage_async(const double* __restrict__ g, double* s) {
+  for (int c = threadIdx.x; c < TS * (TS / 2); c += blockDim.x) {
+    const int r = c >> 5, q = c & 31;
+    cp_async16(s + r * SPAD + 2 * q, g + r * TS + 2 * q);
   }
 }
-
 __device__ void tile_gemm_nt(const double* A, const double* B, double* C, double* sA, double* sB, int mode) {
-  stage_tile(A, sA);
-  if (B != A) stage_tile(B, sB);
+  // operands staged with cp.async (no register round trip); the C tile of an update is
+  // pulled into L2 meanwhile, so its read-modify-write after the products hits L2
+  stage_async(A, sA);
+  if (B != A) stage_async(B, sB);
+  cp_commit();
+  if (mode == 1)
+    for (int e = threadIdx.x; e < TSZ / 16; e += blockDim.x) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + 16 * e));
   const double* sBB = (B != A) ? sB : sA;
+  cp_wait<0>();
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -388,26 +406,6 @@ __device__ __forceinline__ void acc_to_smemT(double* sB, const double (&acc)[4][
     }
 }
 
-// ---- cp.async-staged DMMA tile products (two-stage pipeline over a K loop of tiles) -------
-// Tiles are copied untransposed (row-major, row stride SPAD, 16-byte cp.async chunks); the
-// fragment loads pick the operand orientation: A as [m][k] (AT = false) or as the transpose
-// of a [k][m] tile (AT = true); B as [k][n] (BT = false) or as the transpose of [n][k]
-// (BT = true). SPAD = 68: every orientation reads conflict-free half-warps.
-__device__ __forceinline__ uint32_t cvta_s(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void cp_async16(void* s, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(cvta_s(s)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void stage_async(const double* __restrict__ g, double* s) {
-  for (int c = threadIdx.x; c < TS * (TS / 2); c += blockDim.x) {
-    const int r = c >> 5, q = c & 31;
-    cp_async16(s + r * SPAD + 2 * q, g + r * TS + 2 * q);
-  }
-}
 template <bool AT, bool BT>
 __device__ __forceinline__ void mma_acc2(const double* sA, const double* sB, double (&acc)[4][4][2]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

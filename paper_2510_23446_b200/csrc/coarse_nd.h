@@ -47,7 +47,9 @@ struct CoarseND {
   // B is ordered by (node of the group, group id): ancestors nearest first
   int64_t key(int g) const { return ((int64_t)node_of[g] << 32) | (uint32_t)g; }
 
-  void build(const Plan& pl) {
+  // leaf_max: boxes of at most this many patches are not dissected further (one leaf front
+  // eliminates all their groups): fewer levels = a shorter dependent chain per coarse solve
+  void build(const Plan& pl, int leaf_max = 1) {
     const int64_t nc = pl.nc;
     node_of.assign(nc, -1);
     pos_in_V.assign(nc, -1);
@@ -98,7 +100,8 @@ struct CoarseND {
       int d = 0;
       for (int e = 1; e < 3; ++e)
         if (j.hi[e] - j.lo[e] > j.hi[d] - j.lo[d]) d = e;
-      if (j.hi[d] - j.lo[d] <= 1) {
+      const int64_t vol = (int64_t)(j.hi[0] - j.lo[0]) * (j.hi[1] - j.lo[1]) * (j.hi[2] - j.lo[2]);
+      if (j.hi[d] - j.lo[d] <= 1 || vol <= leaf_max) {
         t[me].V = j.groups;
         continue;
       }
