@@ -1448,7 +1448,6 @@ static tcg_status do_setup(tcg_ctx* h) {
         d.I = I;
         d.Ti = Ti[s]; d.Tb = Tb[s]; d.Tp = Tp[s]; d.T = T[s];
         d.nb = nb[s]; d.np = np[s];
-        d.ni = pl.pp[s].ni;
         d.a_off = a_off[s]; d.vec_off = vec_off[s]; d.b_off = b_off[s]; d.p_off = p_off[s]; d.sbb_off = sbb_off[s];
         return d;
       };
@@ -1565,9 +1564,7 @@ static tcg_status do_setup(tcg_ctx* h) {
       // tile prefetch buffer first (bulk copies of the next phase's first tiles during barriers)
       {
         const char* ne = getenv("TCG_NPF");
-        // 1: the first tile of each phase during the barrier (default); RS: the tile ring of the
-        // P1/P5/SY GEMVs (pcg.cu; measured slower on cfg3-cfg5, profiles/round2_notes.md)
-        int npf = ne ? std::max(0, std::min(RS, atoi(ne))) : 1;
+        int npf = ne ? std::max(0, std::min(2, atoi(ne))) : 1;  // 2 tiles shrink L1 too much on the HBM-bound configs
         while (npf > 0 && (int64_t)(h->smem_pcg + (size_t)npf * TSZ * sizeof(double)) > budget) --npf;
         h->npf = npf;
         budget -= (int64_t)npf * TSZ * sizeof(double);
@@ -1886,10 +1883,6 @@ static StepArgs step_args(tcg_ctx* h) {
   A.cache_lam = h->cache_lam;
   A.scratch = (int)(h->smem_pcg / sizeof(double));
   A.npf = h->npf;
-  {
-    const char* e = getenv("TCG_L2PF");
-    A.l2pf = e ? std::max(0, atoi(e)) : 0;
-  }
   A.warm = h->warm;
   A.warm_base = (int)h->warm_base;
   for (auto& R : h->rd) {

@@ -41,7 +41,6 @@ struct __align__(16) ItemDesc {
   int s, I;
   int Ti, Tb, Tp, T;
   int nb, np;
-  int ni, pad_;  // ni: interior r-DOFs (the full-factor items skip the padding of each block)
   int64_t a_off, vec_off, b_off, p_off, sbb_off;
   int part;  // P5: bit 0: 0 = X_bb^T tiles (-> Y), 1 = Phi_b tiles (-> Y2); bits 4-5: gather code
              // (pcg.cu GAT); coarse items: chunk index

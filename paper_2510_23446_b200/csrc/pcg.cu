@@ -97,7 +97,6 @@ struct StepArgs {
   int cache_lam;    // 1: the block's lambda-chunk index data are copied to shared memory
   int scratch;      // doubles of item scratch (after the prefetch tiles) in dynamic shared memory (even)
   int npf;          // tiles of the next phase's first item bulk-copied to shared memory during a barrier
-  int l2pf;         // tiles bulk-prefetched into L2 ahead of the tile ring (0: off)
   int mode;         // 0: nsteps implicit-Euler steps; 1: nsteps applications q = F p (p = pk[0], q -> r[1])
   int dbg_stop;     // debug: 1 = return after the first step's R3 coarse solve
   int warm;         // k > 0: PCG starts from the Galerkin projection on the previous k solutions (f2)
@@ -180,9 +179,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(mb))
                : "memory");
 }
-__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(unsigned long long* mb, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
@@ -252,17 +248,9 @@ __device__ __forceinline__ void prefetch_tiles(TileF tile, int J0, int J1) {
 // row:  part[r] += sum_{J=J0}^{J1-1} tile(J)[row0+r][:] . x[(J-J0)*64 : ]
 // The first npf tiles were copied to shared memory (pft) by a bulk copy issued during the
 // preceding grid barrier; the rest stream from global memory.
-// Padding is not read from HBM: rows >= rv of the row block, columns >= cvf(J) of tile J
-// and, in tile jd, the zero upper triangle (columns > row) are skipped per lane (a lane's
-// two columns share one 16-byte load, so skipping is exact at sector granularity); the
-// skipped entries are zeros or meet zero inputs, so every sum is bit-identical.
-struct AllCols {
-  __device__ int operator()(int) const { return TS; }
-};
-template <class TileF, class Gather, class ColsF = AllCols>
+template <class TileF, class Gather>
 __device__ __forceinline__ void gemv_row_g(TileF tile, int J0, int J1, const double* x, Gather gather,
-                                           double (&part)[8], const double* pft = nullptr, int npf = 0,
-                                           int rv = TS, ColsF cvf = AllCols(), int jd = -1) {
+                                           double (&part)[8], const double* pft = nullptr, int npf = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
   const int off = row0 * TS + 2 * lane;
   if (!(c_step_flags & 1)) prefetch_tiles(tile, J0 + npf, J1);
@@ -282,27 +270,17 @@ __device__ __forceinline__ void gemv_row_g(TileF tile, int J0, int J1, const dou
   for (int J = J0 + npf; J < J1; ++J) {
     const double* t = tile(J) + off;
     const double2 xv = *reinterpret_cast<const double2*>(x + (J - J0) * TS + 2 * lane);
-    const bool cok = 2 * lane < cvf(J);
-    const int rmax = min(rv - row0, 8);                       // valid rows of this warp
-    const int rdiag = (J == jd) ? 2 * lane - row0 : -1 << 30;  // rows r < rdiag are above the diagonal
     double2 a[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      a[r] = (cok && r < rmax && r >= rdiag) ? ldg2(t + r * TS) : make_double2(0.0, 0.0);
+    for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
 #pragma unroll
     for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
   }
 }
 // col:  c[0..1] += sum_{I=I0}^{I1-1} tile(I)[row0+r][2*lane..] * x[(I-I0)*64 + row0 + r]
-// Padding is skipped as in gemv_row_g: rows >= rvf(I) of tile I, columns >= ncv of the
-// column block, and in tile id the zero upper triangle.
-struct AllRows {
-  __device__ int operator()(int) const { return TS; }
-};
-template <class TileF, class Gather, class RowsF = AllRows>
+template <class TileF, class Gather>
 __device__ __forceinline__ void gemv_col_g(TileF tile, int I0, int I1, const double* x, Gather gather, double& c0,
-                                           double& c1, const double* pft = nullptr, int npf = 0,
-                                           RowsF rvf = AllRows(), int ncv = 1 << 30, int id = -1) {
+                                           double& c1, const double* pft = nullptr, int npf = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
   const int off = row0 * TS + 2 * lane;
   if (!(c_step_flags & 1)) prefetch_tiles(tile, I0 + npf, I1);
@@ -320,16 +298,12 @@ __device__ __forceinline__ void gemv_col_g(TileF tile, int I0, int I1, const dou
       c1 += a[r].y * xr;
     }
   }
-  const bool cok = 2 * lane < ncv;
 #pragma unroll 2
   for (int I = I0 + npf; I < I1; ++I) {
     const double* t = tile(I) + off;
-    const int rmax = min(rvf(I) - row0, 8);
-    const int rdiag = (I == id) ? 2 * lane - row0 : -1 << 30;
     double2 a[8];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-      a[r] = (cok && r < rmax && r >= rdiag) ? ldg2(t + r * TS) : make_double2(0.0, 0.0);
+    for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const double xr = x[(I - I0) * TS + row0 + r];
@@ -352,87 +326,27 @@ __device__ __forceinline__ double col_finish(double c0, double c1, double* cr) {
   return acc;
 }
 
-// ---- tile ring (TMA engine): GEMVs over tiles that a bulk-copy producer streams into a ring of
-// RS shared-memory slots (k_steps: ring_start / ring_produce). get() waits for the next tile of
-// the block's sequence and returns its slot; rel() releases it (block-wide) and lets thread 0
-// refill the slot with the next tile of the phase, across item boundaries, so the HBM stream
-// continues through every gather, reduction and barrier. Only the valid rows of a tile are
-// copied (rows >= rv of the slot hold stale data and are skipped).
-constexpr int RS = 2;  // ring slots (32 KiB tiles) per block
-struct NoRingGet {
-  __device__ const double* operator()() const { return nullptr; }
-};
-struct NoRingRel {
-  __device__ void operator()() const {}
-};
-template <class Get, class Rel, class Gather>
-__device__ __forceinline__ void gemv_row_ring(Get get, Rel rel, int J0, int J1, const double* x, Gather gather,
-                                              double (&part)[8], int rv) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
-  const int off = row0 * TS + 2 * lane;
-  const int rmax = min(rv - row0, 8);
-  gather();
-  __syncthreads();
-  for (int J = J0; J < J1; ++J) {
-    const double* t = get() + off;
-    const double2 xv = *reinterpret_cast<const double2*>(x + (J - J0) * TS + 2 * lane);
-    double2 a[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) a[r] = (r < rmax) ? lds2(t + r * TS) : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
-    rel();
-  }
-}
-template <class Get, class Rel, class Gather, class RowsF>
-__device__ __forceinline__ void gemv_col_ring(Get get, Rel rel, int I0, int I1, const double* x, Gather gather, double& c0,
-                                              double& c1, RowsF rvf) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
-  const int off = row0 * TS + 2 * lane;
-  gather();
-  __syncthreads();
-  for (int I = I0; I < I1; ++I) {
-    const double* t = get() + off;
-    const int rmax = min(rvf(I) - row0, 8);
-    double2 a[8];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) a[r] = (r < rmax) ? lds2(t + r * TS) : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const double xr = x[(I - I0) * TS + row0 + r];
-      c0 += a[r].x * xr;
-      c1 += a[r].y * xr;
-    }
-    rel();
-  }
-}
-
 // ---- P1 / E1: [X_bb; Phi_b^T] v, v = B_s^T p gathered per b position ---------------------
 // vsrc(it, b, pos) returns (B_s^T p)_pos, b = b_off + pos. Output XW: +w (b rows), -g (p rows).
 // Xr = the rank's inverse-factor store.
 // gat = false: sv still holds this patch's v from the previous item of the same patch
-template <class Src, class RG = NoRingGet, class RR = NoRingRel>
+template <class Src>
 __device__ __forceinline__ void p1_item(const ItemDesc& it, const double* Xr, Src vsrc, double* XW, double* sv,
-                                        const double* pft = nullptr, int npf = 0, int gat = 1, bool ring = false,
-                                        RG rg = RG(), RR rr = RR()) {
+                                        const double* pft = nullptr, int npf = 0, int gat = 1) {
   const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   const int Jn = (I < Tb) ? I + 1 : Tb;
   const double* X = Xr + it.a_off;
   double part[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) part[r] = 0.0;
-  auto gather = [&] {
-    if (gat) {
-      const int ne = (gat == 2) ? Tb * TS : Jn * TS;  // the full vector only if reused
-      for (int e = threadIdx.x; e < ne; e += blockDim.x) sv[e] = (e < nb) ? vsrc(it, it.b_off + e, e) : 0.0;
-    }
-  };
-  const int rv = (I < Tb) ? nb - I * TS : it.np - (I - Tb) * TS;
-  if (ring)
-    gemv_row_ring(rg, rr, Ti, Ti + Jn, sv, gather, part, rv);
-  else
-    gemv_row_g([&](int J) { return X + tri_off(Ti + I, J); }, Ti, Ti + Jn, sv, gather, part, pft, npf, rv,
-               [&](int J) { return nb - (J - Ti) * TS; }, (I < Tb) ? Ti + I : -1);
+  gemv_row_g([&](int J) { return X + tri_off(Ti + I, J); }, Ti, Ti + Jn, sv,
+             [&] {
+               if (gat) {
+                 const int ne = (gat == 2) ? Tb * TS : Jn * TS;  // the full vector only if reused
+                 for (int e = threadIdx.x; e < ne; e += blockDim.x) sv[e] = (e < nb) ? vsrc(it, it.b_off + e, e) : 0.0;
+               }
+             },
+             part, pft, npf);
   const double sum = warp_reduce8(part);
   const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
   if ((lane & 3) == 0) XW[it.vec_off + (int64_t)(Ti + I) * TS + row0 + warp_reduce8_row()] = (I < Tb) ? sum : -sum;
@@ -480,11 +394,11 @@ __device__ __forceinline__ void pc_item(const DevPlan& D, const StepArgs& A, con
 // Split in two items so no single item streams more than max(Tb, Tp) tiles: part 0 the X_bb^T
 // tiles (-> Y), part 1 the Phi_b tiles (-> Y2); consumers read y = Y + Y2. Returns this item's
 // share of v_J . y_J (vsrc gives (B_s^T p)_pos; pass zero for R4).
-template <class PcF, class Src, class RG = NoRingGet, class RR = NoRingRel>
+template <class PcF, class Src>
 __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, const double* W, const int* p_grp,
                                           PcF pc, Src vsrc, double* Y, double* Y2, double* sm, double* red,
                                           unsigned long long* sub = nullptr, const double* pft = nullptr,
-                                          int npf = 0, int gat = 1, bool ring = false, RG rg = RG(), RR rr = RR()) {
+                                          int npf = 0, int gat = 1) {
   const int J = it.I, Ti = it.Ti, Tb = it.Tb, np = it.np, nb = it.nb;
   const bool ppart = (it.part & 1) != 0;
   const bool merged = (it.part & 2) != 0;  // whole column J: X_bb^T tiles then Phi_b tiles (-> Y)
@@ -503,22 +417,18 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
   if (threadIdx.x < TS && J * TS + (int)threadIdx.x < nb)
     vj = vsrc(it, it.b_off + J * TS + threadIdx.x, J * TS + threadIdx.x);
   double c0 = 0.0, c1 = 0.0;
-  auto gather = [&] {
-    if (gat)
-      for (int e = (gat == 2 ? 0 : (I0 - G0) * TS) + threadIdx.x; e < (I1 - G0) * TS; e += blockDim.x) {
-        double val;
-        if (merged) val = (e < Tb * TS) ? ldcg(W + vo + e) : ((e - Tb * TS < np) ? -pc(grp[e - Tb * TS]) : 0.0);
-        else if (!ppart) val = ldcg(W + vo + e);
-        else val = (e < np) ? -pc(grp[e]) : 0.0;
-        sfull[e] = val;
-      }
-  };
-  auto rvf = [&](int I) { return I < Tb ? nb - I * TS : np - (I - Tb) * TS; };
-  if (ring)
-    gemv_col_ring(rg, rr, I0, I1, sw, gather, c0, c1, rvf);
-  else
-    gemv_col_g([&](int I) { return X + tri_off(Ti + I, Ti + J); }, I0, I1, sw, gather, c0, c1, pft, npf, rvf,
-               nb - J * TS, ppart ? -1 : J);
+  gemv_col_g([&](int I) { return X + tri_off(Ti + I, Ti + J); }, I0, I1, sw,
+             [&] {
+               if (gat)
+                 for (int e = (gat == 2 ? 0 : (I0 - G0) * TS) + threadIdx.x; e < (I1 - G0) * TS; e += blockDim.x) {
+                   double val;
+                   if (merged) val = (e < Tb * TS) ? ldcg(W + vo + e) : ((e - Tb * TS < np) ? -pc(grp[e - Tb * TS]) : 0.0);
+                   else if (!ppart) val = ldcg(W + vo + e);
+                   else val = (e < np) ? -pc(grp[e]) : 0.0;
+                   sfull[e] = val;
+                 }
+             },
+             c0, c1, pft, npf);
   SUBSTAMP(1);
   const double acc = col_finish(c0, c1, cr);
   double contrib = 0.0;
@@ -532,10 +442,9 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
 
 // ---- P7 / R5: symmetric S_bb apply, one row block I of one patch --------------------------
 // usrc(it, b, pos) returns (B_D^(s)T r)_pos. Returns this item's share of u^T S_bb u.
-template <class Src, class RG = NoRingGet, class RR = NoRingRel>
+template <class Src>
 __device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm,
-                                            double* red, const double* pft = nullptr, int npf = 0, bool gat = true,
-                                            bool ring = false, RG rg = RG(), RR rr = RR()) {
+                                            double* red, const double* pft = nullptr, int npf = 0, bool gat = true) {
   const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   double* u = sm;            // Tb*64
   double* cr = u + Tb * TS;  // 9 * 64
@@ -545,45 +454,25 @@ __device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr
 #pragma unroll
   for (int q = 0; q < 8; ++q) part[q] = 0.0;
   // row part: S_IJ u_J (J <= I), the u gather overlapped with the first tile's loads
-  auto gather = [&] {
-    if (gat)
-      for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) u[i] = (i < nb) ? usrc(it, it.b_off + i, i) : 0.0;
-  };
+  gemv_row_g([&](int J) { return S + tri_off(I, J); }, 0, I + 1, u,
+             [&] {
+               if (gat)
+                 for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) u[i] = (i < nb) ? usrc(it, it.b_off + i, i) : 0.0;
+             },
+             part, pft, npf);
   double c0 = 0.0, c1 = 0.0;
-  if (ring) {
-    gemv_row_ring(rg, rr, 0, I + 1, u, gather, part, nb - I * TS);
-    for (int J = I + 1; J < Tb; ++J) {  // column part: S_JI^T u_J, tiles (J, I) from the ring
-      const double* t = rg() + row0 * TS + 2 * lane;
-      const int rmax = min(nb - J * TS - row0, 8);
-      double2 a[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) a[q] = (q < rmax) ? lds2(t + q * TS) : make_double2(0.0, 0.0);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double xr = u[J * TS + row0 + q];
-        c0 += a[q].x * xr;
-        c1 += a[q].y * xr;
-      }
-      rr();
-    }
-  } else {
-  gemv_row_g([&](int J) { return S + tri_off(I, J); }, 0, I + 1, u, gather, part, pft, npf, nb - I * TS,
-             [&](int J) { return nb - J * TS; });
-  const bool cok = 2 * lane < nb - I * TS;
 #pragma unroll 2
   for (int J = I + 1; J < Tb; ++J) {  // column part: S_JI^T u_J
     const double* t = S + tri_off(J, I) + row0 * TS + 2 * lane;
-    const int rmax = min(nb - J * TS - row0, 8);
     double2 a[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = (cok && q < rmax) ? ldg2(t + q * TS) : make_double2(0.0, 0.0);
+    for (int q = 0; q < 8; ++q) a[q] = ldg2(t + q * TS);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const double xr = u[J * TS + row0 + q];
       c0 += a[q].x * xr;
       c1 += a[q].y * xr;
     }
-  }
   }
   cr[warp * TS + 2 * lane] = c0;
   cr[warp * TS + 2 * lane + 1] = c1;
@@ -615,13 +504,11 @@ __device__ __forceinline__ void fw_item(const ItemDesc& it, const double* Xr, co
   double part[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) part[r] = 0.0;
-  const int Ti = it.Ti, ni = it.ni, nb = it.nb;
-  auto nvalid = [&](int K) { return K < Ti ? ni - K * TS : (K < Tr ? nb - (K - Ti) * TS : it.np - (K - Tr) * TS); };
   gemv_row_g([&](int J) { return X + tri_off(I, J); }, 0, Jn, sm,
              [&] {
                for (int e = threadIdx.x; e < Jn * TS; e += blockDim.x) sm[e] = ldcg(Fv + vo + e);
              },
-             part, nullptr, 0, nvalid(I), nvalid, (I < Tr) ? I : -1);
+             part);
   const double sum = warp_reduce8(part);
   const int lane = threadIdx.x & 31, row0 = (threadIdx.x >> 5) * 8;
   if ((lane & 3) == 0) {
@@ -657,9 +544,7 @@ __device__ __forceinline__ void bw_item(const DevPlan& D, const ItemDesc& it, co
                  sx[e] = val;
                }
              },
-             c0, c1, nullptr, 0,
-             [&](int I) { return I < Ti ? it.ni - I * TS : (I < Tr ? it.nb - (I - Ti) * TS : np - (I - Tr) * TS); },
-             J < Ti ? it.ni - J * TS : it.nb - (J - Ti) * TS, J);
+             c0, c1);
   const double acc = col_finish(c0, c1, cr);
   double* as = a_loc + (int64_t)s * nloc;
   if (threadIdx.x < TS) {
@@ -714,8 +599,7 @@ __device__ __forceinline__ void fwc_item(const ItemDesc& it, const double* FR, c
              [&] {
                for (int e = threadIdx.x; e < (J1 - J0) * TS; e += blockDim.x) sm[e] = fval(J0 * TS + e);
              },
-             part, nullptr, 0, (I < TV) ? it.np - I * TS : it.nb - (I - TV) * TS, [&](int J) { return it.np - J * TS; },
-             (I < TV) ? I : -1);
+             part);
   const double sum = warp_reduce8(part);
   const double mine = (I < TV) ? sum : frow - sum;  // this chunk's share of the output
   if (nch == 1) {
@@ -771,7 +655,7 @@ __device__ __forceinline__ void bwc_item(const ItemDesc& it, const double* FR, c
                    sx[e] = val;
                  }
                },
-               c0, c1, nullptr, 0, [&](int I) { return I < TV ? nV - I * TS : nB - (I - TV) * TS; }, nV - J * TS, J);
+               c0, c1);
     __syncthreads();  // sx reused by the next chunk
   }
   const double acc = col_finish(c0, c1, cr);
@@ -1004,10 +888,6 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
 #define FOR_ITEMS(ph, var)                                  \
   for (int j_##var = 0; j_##var < s_icnt[ph]; ++j_##var)    \
     if (const ItemDesc& var = s_ip[ph][j_##var]; true)
-// the same for the per-iteration GEMV phases, with the L2 prefetch of coming tiles (pf_hook)
-#define FOR_ITEMS_PF(ph, var)                               \
-  for (int j_##var = 0; j_##var < s_icnt[ph]; ++j_##var)    \
-    if (const ItemDesc& var = s_ip[ph][j_##var]; pf_hook(ph, j_##var))
 
 // =======================================================================================
 // Persistent cooperative time stepper: A.nsteps implicit-Euler steps in one launch, over
@@ -1026,10 +906,6 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   __shared__ const BPos* s_bp;
   __shared__ __align__(8) unsigned long long s_mb;  // mbarrier of the tile prefetch
   __shared__ int s_pfn;                            // tiles prefetched for the coming phase
-  __shared__ __align__(8) unsigned long long s_full[RS];  // tile ring: one mbarrier per slot
-  __shared__ unsigned int s_rp, s_rj, s_rk;        // ring producer: tiles issued, item / tile cursor
-  __shared__ unsigned int s_qp, s_qj, s_qk;        // L2 prefetch cursor (runs A.l2pf tiles ahead)
-  __shared__ int s_rph;                            // ring producer: phase
   double* const tbuf = sm;                         // A.npf prefetched tiles
   double* const smw = sm + (size_t)A.npf * TSZ;    // item scratch
   // MULTI = false: one rank, every owner lookup folds to rank 0 at compile time
@@ -1054,8 +930,6 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     if (threadIdx.x == 0) {
       mbar_init(&s_mb);
       s_pfn = 0;
-      for (int q = 0; q < RS; ++q) mbar_init(&s_full[q]);
-      s_rp = 0;
     }
 #pragma unroll
     for (int ph = 0; ph < NPH; ++ph)  // constant indices: no local copy of the parameter block
@@ -1177,123 +1051,6 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     }
     return n;
   };
-  // ---- tile ring of the per-iteration GEMV phases (P1, P5, SY): RS slots of tbuf ----
-  const bool ring_on = A.npf >= RS;
-  unsigned int rcons = 0;  // tiles consumed by this block (uniform over its threads)
-  // tile k of item w of phase ph: global address and the bytes of its valid rows (nullptr: done)
-  auto ring_tile = [&](int ph, const ItemDesc& w, int k, uint32_t& bytes) -> const double* {
-    if (ph == PH_P1) {
-      const int Jn = (w.I < w.Tb) ? w.I + 1 : w.Tb;
-      if (k >= Jn) return nullptr;
-      const int rv = (w.I < w.Tb) ? min(TS, w.nb - w.I * TS) : min(TS, w.np - (w.I - w.Tb) * TS);
-      bytes = (uint32_t)rv * TS * sizeof(double);
-      return Xr + w.a_off + tri_off(w.Ti + w.I, w.Ti + k);
-    }
-    if (ph == PH_P5) {
-      const bool pp5 = (w.part & 1) != 0;
-      const int I = (pp5 ? w.Tb : w.I) + k, I1 = (w.part & 3) ? w.Tb + w.Tp : w.Tb;
-      if (I >= I1) return nullptr;
-      const int rv = I < w.Tb ? min(TS, w.nb - I * TS) : min(TS, w.np - (I - w.Tb) * TS);
-      bytes = (uint32_t)rv * TS * sizeof(double);
-      return Xr + w.a_off + tri_off(w.Ti + I, w.Ti + w.I);
-    }
-    if (k >= w.Tb) return nullptr;  // PH_SY: row part (I, k <= I), then column part (k > I, I)
-    const int rb = (k <= w.I) ? w.I : k;
-    bytes = (uint32_t)min(TS, w.nb - rb * TS) * TS * sizeof(double);
-    return Sr + w.sbb_off + ((k <= w.I) ? tri_off(w.I, k) : tri_off(k, w.I));
-  };
-  // thread 0: issue the phase's next tiles into the free slots
-  auto ring_produce = [&](unsigned int cons) {
-    const int ph = s_rph;
-    // HBM latency (~2 us under load) dominates a tile, so the tiles A.l2pf ahead of the ring
-    // are pulled into L2 first (bulk prefetch: no shared memory, no registers)
-    while (s_qp < s_rp + (unsigned)A.l2pf && (int)s_qj < s_icnt[ph]) {
-      uint32_t bytes = 0;
-      const double* src = ring_tile(ph, s_ip[ph][s_qj], (int)s_qk, bytes);
-      if (!src) {
-        ++s_qj;
-        s_qk = 0;
-        continue;
-      }
-      prefetch_l2_bulk(src, bytes);
-      ++s_qp;
-      ++s_qk;
-    }
-    while (s_rp - cons < (unsigned)RS && (int)s_rj < s_icnt[ph]) {
-      uint32_t bytes = 0;
-      const double* src = ring_tile(ph, s_ip[ph][s_rj], (int)s_rk, bytes);
-      if (!src) {
-        ++s_rj;
-        s_rk = 0;
-        continue;
-      }
-      const int slot = (int)(s_rp % RS);
-      mbar_expect_tx(&s_full[slot], bytes);
-      bulk_g2s(tbuf + (size_t)slot * TSZ, src, bytes, &s_full[slot]);
-      ++s_rp;
-      ++s_rk;
-    }
-  };
-  // thread 0, inside the grid barrier before phase ph: the first RS tiles start streaming
-  auto ring_start = [&](int ph) {
-    s_rph = ph;
-    s_rj = 0;
-    s_rk = 0;
-    s_qj = 0;
-    s_qk = 0;
-    s_qp = s_rp;
-    s_pfn = 0;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    ring_produce(rcons);
-  };
-  auto rget = [&]() -> const double* {
-    const unsigned int c = rcons;
-    mbar_wait(&s_full[c % RS], (c / RS) & 1u);
-    return tbuf + (size_t)(c % RS) * TSZ;
-  };
-  auto rrel = [&]() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
-    __syncthreads();
-    ++rcons;
-    if (threadIdx.x == 0) ring_produce(rcons);
-  };
-  auto is_ring_ph = [&](int ph) { return ring_on && (ph == PH_P1 || ph == PH_P5 || ph == PH_SY); };
-  // (experiment, TCG_L2PF > 0: thread 0 bulk-prefetches tiles into L2; measured slower)
-  auto pf_l2_item = [&](int ph, int j, int k0, int k1) {
-    if (j >= s_icnt[ph]) return;
-    const ItemDesc& w = s_ip[ph][j];
-    for (int k = k0; k < k1; ++k) {
-      uint32_t bytes = 0;
-      const double* src = ring_tile(ph, w, k, bytes);
-      if (!src) break;
-      prefetch_l2_bulk(src, bytes);
-    }
-  };
-  // At the start of item j every thread prefetches into L2 its own rows of the first tiles of
-  // item j + 1, so their HBM latency overlaps item j instead of opening item j + 1 (a block
-  // streams its items one after the other; ~1 us of first-tile latency per item otherwise).
-  const int pf_next = (c_step_flags & 8) ? 2 : 0;  // opt-in (TCG_STEP_FLAGS bit 3): measured slower
-  const int warp_ = threadIdx.x >> 5, lane_ = threadIdx.x & 31;
-  auto pf_hook = [&](int ph, int j) {
-    if (A.l2pf > 0 && !ring_on && threadIdx.x == 0) {
-      pf_l2_item(ph, j, 2, 1 << 20);
-      pf_l2_item(ph, j + 1, 0, A.l2pf);
-    }
-    if (pf_next > 0 && !ring_on && j + 1 < s_icnt[ph]) {
-      const ItemDesc& w = s_ip[ph][j + 1];
-      for (int k = 0; k < pf_next; ++k) {
-        uint32_t bytes = 0;
-        const double* src = ring_tile(ph, w, k, bytes);
-        if (!src) break;
-        const int rows = (int)(bytes / (TS * sizeof(double)));
-        const double* t = src + warp_ * 8 * TS + 2 * lane_;
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-          if (warp_ * 8 + r < rows && (lane_ & 3) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(t + r * TS));
-      }
-    }
-    return true;
-  };
   auto hook = [&](int ph) { return [&, ph]() { pf_issue(ph); }; };
   int64_t hoff = A.hist_off;
   int total_status = 0;
@@ -1305,17 +1062,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     // every thread orders its generic-proxy reads of tbuf before the async-proxy (bulk copy)
     // overwrite that thread 0 issues after the barrier's __syncthreads (WAR across proxies)
     if (A.npf > 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    const double r = grid_barrier(A, me, bl, round, reduce, v, bcast, [&]() {
-      if (is_ring_ph(ph_next)) {
-        ring_start(ph_next);
-      } else {
-        pf_issue(ph_next);
-        if (A.l2pf > 0 && (ph_next == PH_P1 || ph_next == PH_P5 || ph_next == PH_SY)) {
-          pf_l2_item(ph_next, 0, 1, A.l2pf + 2);
-          pf_l2_item(ph_next, 1, 0, A.l2pf);
-        }
-      }
-    });
+    const double r = grid_barrier(A, me, bl, round, reduce, v, bcast, [&]() { pf_issue(ph_next); });
     npf_cur = pf_wait();
     return r;
   };
@@ -1395,27 +1142,23 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     PC_PHASE(GS);                 \
   }
   // ---- mode 1: the dual operator alone, q = F p, A.nsteps times (F-apply benchmark / test) ----
-  if (A.mode == 1 && A.nsteps > 0 && ring_on) {
-    if (threadIdx.x == 0) ring_start(PH_P1);
-    __syncthreads();
-  }
   for (int rep = 0; A.mode == 1 && rep < A.nsteps; ++rep) {
     const int step = -1, it = -1;  // no stamps
     (void)step;
     (void)it;
-    FOR_ITEMS_PF(PH_P1, w)
+    FOR_ITEMS(PH_P1, w)
       p1_item(w, Xr,
               [&](const ItemDesc& iw, int64_t bb, int pos) {
                 const BPos q = bget(iw, bb, pos);
                 return q.sign * ldcg(A.pk[0][lown(q.k)] + q.k);
               },
-              A.XW[me], smw, PF0(j_w), GAT(PH_P1, w), ring_on, rget, rrel);
+              A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
     bar(PH_PC, false, 0.0);
     COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
     bar(PH_P5, false, 0.0);
-    FOR_ITEMS_PF(PH_P5, w)
+    FOR_ITEMS(PH_P5, w)
       p5_item(w, Xr, A.XW[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
-              red, nullptr, PF0(j_w), GAT(PH_P5, w), ring_on, rget, rrel);
+              red, nullptr, PF0(j_w), GAT(PH_P5, w));
     bar(-1, false, 0.0);
     for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
       A.r[1][me][k] = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
@@ -1439,9 +1182,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     if (A.dbg_stop == 1) break;
     SSTAMP(3);
     // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
-    FOR_ITEMS_PF(PH_P5, w)
+    FOR_ITEMS(PH_P5, w)
       p5_item(w, Xr, A.Z[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
-              red, nullptr, PF0(j_w), GAT(PH_P5, w), ring_on, rget, rrel);
+              red, nullptr, PF0(j_w), GAT(PH_P5, w));
     bar(PH_SY, false, 0.0);
     SSTAMP(4);
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
@@ -1451,13 +1194,13 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     double rho0;
     {
       double loc = 0.0;
-      FOR_ITEMS_PF(PH_SY, w)
+      FOR_ITEMS(PH_SY, w)
         loc += symv_item(w, Sr, A.PW[me],
                          [&](const ItemDesc& iw, int64_t bb, int pos) {
                            const BPos q = bget(iw, bb, pos);
                            return q.aown * (yv(me, own_idx(iw, pos)) - yv(pown(ppatch(bb)), q.part));
                          },
-                         smw, red, PF0(j_w), GAT(PH_SY, w), ring_on, rget, rrel);
+                         smw, red, PF0(j_w), GAT(PH_SY, w));
       for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
         const double dk = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
         A.r[0][me][k] = dk;
@@ -1466,7 +1209,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         if (A.warm) A.dsave[me][k] = dk;
       }
       loc = block_sum(loc, red);
-      rho0 = bar(nW > 0 ? -1 : PH_P1, true, loc);  // W1 runs first on a warm step
+      rho0 = bar(PH_P1, true, loc);
     }
     SSTAMP(5);
     int status = 0;  // 0 running, 1 converged, 2 failed
@@ -1476,10 +1219,6 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     double rho = rho0, beta = 0.0;
     int rp = 0, pp = 0;
     double rel0 = 1.0;
-    if (nW > 0 && status != 0 && ring_on) {  // no W1 after all: start the P1 tiles here
-      if (threadIdx.x == 0) ring_start(PH_P1);
-      __syncthreads();
-    }
     if (nW > 0 && status == 0) {
       // ---- W1: Galerkin start on span{W_j} (oracle Oracle.pcg, R20): dot products
       // b_j = W_j.d, G_ij = (W_i.FW_j + W_j.FW_i)/2 over the block's lambda chunk ----
@@ -1597,13 +1336,13 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       bar(PH_SY, false, 0.0);
       // ---- W2: z0 = M^-1 r0, rho = r0^T z0 ----
       double loc = 0.0;
-      FOR_ITEMS_PF(PH_SY, w)
+      FOR_ITEMS(PH_SY, w)
         loc += symv_item(w, Sr, A.PW[me],
                          [&](const ItemDesc& iw, int64_t bb, int pos) {
                            const BPos q = bget(iw, bb, pos);
                            return q.aown * q.sign * ldcg(A.r[1][lown(q.k)] + q.k);
                          },
-                         smw, red, PF0(j_w), GAT(PH_SY, w), ring_on, rget, rrel);
+                         smw, red, PF0(j_w), GAT(PH_SY, w));
       loc = block_sum(loc, red);
       rz = bar(PH_P1, true, loc);
       rho = rz;
@@ -1630,9 +1369,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           return q.aown * ldcg(A.PW[me] + own_idx(iw, pos)) + q.apart * ldcg(A.PW[pown(ppatch(bb))] + q.part) +
                  q.sign * beta * ldcg(pprev[lown(q.k)] + q.k);
         };
-        FOR_ITEMS_PF(PH_P1, w) {
+        FOR_ITEMS(PH_P1, w) {
           ITIME_BEGIN
-          p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w), ring_on, rget, rrel);
+          p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
           ITIME_END(PH_P1, j_w)
         }
         if (kq < k1) pcur[kq] = pv;
@@ -1653,7 +1392,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       double pq;
       {
         double loc = 0.0;
-        FOR_ITEMS_PF(PH_P5, w) {
+        FOR_ITEMS(PH_P5, w) {
           ITIME_BEGIN
           loc += p5_item(w, Xr, A.XW[me], D.p_grp, pcf,
                          [&](const ItemDesc& iw, int64_t bb, int pos) {
@@ -1662,7 +1401,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
                          },
                          A.Y[me], A.Y2[me], smw, red,
                          (A.tstamp && step == 0 && it == 2 && gb < 4096) ? A.tstamp + 528 + gb * 8 + 4 : nullptr,
-                         PF0(j_w), GAT(PH_P5, w), ring_on, rget, rrel);
+                         PF0(j_w), GAT(PH_P5, w));
           ITIME_END(PH_P5, j_w)
         }
         WSTAMP(2);
@@ -1690,9 +1429,9 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
           yd = yv(pown(lpat_p(kq)), lidx_p(kq)) - yv(pown(lpat_m(kq)), lidx_m(kq));
         }
         double loc = 0.0;
-        FOR_ITEMS_PF(PH_SY, w) {
+        FOR_ITEMS(PH_SY, w) {
           ITIME_BEGIN
-          loc += symv_item(w, Sr, A.PW[me], unew, smw, red, PF0(j_w), GAT(PH_SY, w), ring_on, rget, rrel);
+          loc += symv_item(w, Sr, A.PW[me], unew, smw, red, PF0(j_w), GAT(PH_SY, w));
           ITIME_END(PH_SY, j_w)
         }
         if (kq < k1) {
@@ -1744,13 +1483,13 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     }
     SSTAMP(6);
     // ---- E1 v = B^T lambda ; w, -Phi^T v ----
-    FOR_ITEMS_PF(PH_P1, w)
+    FOR_ITEMS(PH_P1, w)
       p1_item(w, Xr,
               [&](const ItemDesc& iw, int64_t bb, int pos) {
                 const BPos q = bget(iw, bb, pos);
                 return q.sign * ldcg(A.lam[lown(q.k)] + q.k);
               },
-              A.XW[me], smw, PF0(j_w), GAT(PH_P1, w), ring_on, rget, rrel);
+              A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
     bar(PH_PC, false, 0.0);
     SSTAMP(7);
     // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
@@ -1776,15 +1515,6 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     }
     bar(-1, false, 0.0);
     SSTAMP(9);
-  }
-  // drain the tile ring: a phase started in the last barrier may still have tiles in flight
-  __syncthreads();
-  {
-    const unsigned int issued = s_rp;
-    while (rcons < issued) {
-      mbar_wait(&s_full[rcons % RS], (rcons / RS) & 1u);
-      ++rcons;
-    }
   }
   if (bl == 0 && threadIdx.x == 0) {
     A.st[me]->done = 1;
