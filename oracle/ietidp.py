@@ -89,17 +89,20 @@ def patch_box(prob, s):
     return lo, hi
 
 
-def local_operators(prob, s, r, pl, ni, dt, lean=False, dl=None):
+def local_operators(prob, s, r, pl, ni, dt, lean=False, dl=None, K_override=None):
     """Per-patch setup (P:L83-87 assembly, P:L133 W^ = K + M/dt, P:L154 local Schur
     complement): element-loop K, M, j_S of patch s; W^ = nu K + (sigma/dt) M restricted to
     r = [i; b] (local ids `r`) and to the primal DOFs `pl`; Cholesky of W_rr and W_ii;
     Phi = W_rr^-1 W_rp; S^s = W_pp - W_pr Phi. lean=True keeps only what the time stepping
     needs (no K / full W; the blocks of W that are only multiplied with, and M, in sparse
     storage; M dropped for insulators, where it is zero) -- storage only, same operators.
+    K_override replaces nu K (the Newton step of oracle/nonlinear.py: the tangent matrix).
     Module-level so that a process pool can run it patch by patch."""
     lo, hi = patch_box(prob, s)
     sp = assembly.PatchSpace(prob.p, prob.elems, lo, hi)
     K, M, jS = assembly.assemble_patch(sp, prob.nu[s], prob.sigma[s], prob.source)
+    if K_override is not None:
+        K = K_override
     W = K + M / dt
     Wrr = W[np.ix_(r, r)]
     cf = _chol(Wrr, f"W_rr patch {s}")
@@ -186,16 +189,18 @@ class Oracle:
         else:
             self.pos_plus = self.pos_minus = np.zeros(0, dtype=np.int64)
 
+    _local_names = ("Wrr_cf", "Wii_cf", "Wrp", "Wpp", "Phi", "Wbb", "Wbi", "Wdiag", "jS", "K", "M", "Wfull", "Pi",
+                    "hr", "hp")
+
     def _setup_locals(self):
         pr = self.prob
         pt = self.part
         P = pr.n_patches
         jobs = [(pr, s, pt.r_order(s), pt.p_loc[s], len(pt.r_i[s]), self.dt, self.lean, self.d_loc[s]) for s in range(P)]
-        names = ("Wrr_cf", "Wii_cf", "Wrp", "Wpp", "Phi", "Wbb", "Wbi", "Wdiag", "jS", "K", "M", "Wfull", "Pi", "hr", "hp")
+        names = self._local_names
         for n in names:
             setattr(self, n, [])
-        nc = pt.nc
-        Spp = np.zeros((nc, nc))
+        self.Ss = []
         if self.workers == 1:
             results = map(_local_job, jobs)
             pool = None
@@ -205,14 +210,24 @@ class Oracle:
             self._limits = threadpool_limits(1)   # one BLAS thread per pool worker
             pool = mp.get_context("fork").Pool(self.workers)
             results = pool.imap(_local_job, jobs, chunksize=1)
-        for s, loc in enumerate(results):       # patch order: the S_pp sums are ordered
-            g = pt.p_grp[s]
-            Spp[np.ix_(g, g)] += loc["Ss"]
+        for s, loc in enumerate(results):
+            self.Ss.append(loc["Ss"])
             for n in names:
                 getattr(self, n).append(loc[n])
         if pool is not None:
             pool.close()
             pool.join()
+        self._coarse_and_weights()
+
+    def _coarse_and_weights(self):
+        """S_pp = sum_s N_s^T S^s N_s (patch order: the sums are ordered), its Cholesky factor,
+        and the rho-scaling weights from the local matrices' diagonals."""
+        pt = self.part
+        nc = pt.nc
+        Spp = np.zeros((nc, nc))
+        for s in range(self.prob.n_patches):
+            g = pt.p_grp[s]
+            Spp[np.ix_(g, g)] += self.Ss[s]
         self.Spp = Spp
         if self.workers > 1:
             from threadpoolctl import threadpool_limits
@@ -222,6 +237,7 @@ class Oracle:
             self.Spp_cf = _chol(Spp, "coarse S_pp")
         if self.lean:
             self.Spp = None
+            self.Ss = [None] * len(self.Ss)
         # rho-scaling weights (R5): rho_s = W^_s diagonal at the b-DOF
         m = pt.m
         self.wplus = np.ones(m)
@@ -364,20 +380,33 @@ class Oracle:
     def step(self, load=None):
         """One implicit-Euler step l -> l+1 (t = (l+1) dt). `load`, if given, is a list
         of per-patch load vectors j^(l+1) replacing phi_s(t) jS_s (pin P15)."""
-        pt = self.part
         P = self.prob.n_patches
         t = (self.ell + 1) * self.dt
         f = []
         for s in range(P):
             js = load[s] if load is not None else self.source_factor(s, t) * self.jS[s]
             f.append(self.Ma(s, self.a[s]) / self.dt + js)
+        a_old = self.a
+        self.a, k, hist = self.solve_rhs(f, t)
+        self.ell += 1
+        self.iters.append(k)
+        self.hist.append(hist)
+        if self.errors is not None:
+            self.errors.after_step(a_old)
+        return k
+
+    def solve_rhs(self, f, t):
+        """The 3x3 block system of P:L139-153 for the per-patch (torn) right-hand sides f_s at
+        time t: dual rhs d, PCG for lambda, recovery of a = (a_e = 0, a_p = N p, a_r).
+        Returns (per-patch local vectors, PCG iterations, relres history)."""
+        pt = self.part
+        P = self.prob.n_patches
         fr = [f[s][pt.r_order(s)] for s in range(P)]
         fp = [f[s][pt.p_loc[s]] for s in range(P)]
         if self.lifting:  # f_r - W_rD a_D(t), f_p - W_pD a_D(t) (P:L150), a_D(t) = e^-t (Pi_h S)_D
             eD = math.exp(-t)
             fr = [fr[s] - eD * self.hr[s] for s in range(P)]
             fp = [fp[s] - eD * self.hp[s] for s in range(P)]
-        a_old = self.a
         x1 = self._map(lambda s: _solve(self.Wrr_cf[s], fr[s]), range(P))
         h = [self.Wrp[s].T @ x1[s] for s in range(P)]
         fpg = self.NT(fp)
@@ -392,6 +421,7 @@ class Oracle:
             self.warm_FW = (self.warm_FW + [d - r])[-kw:]
         v = self.Bt(lam)
         pc = _solve(self.Spp_cf, fpg - self.NT([h[s] - self.Phi[s].T @ v[s] for s in range(P)]))
+
         def recover(s):
             ar = _solve(self.Wrr_cf[s], fr[s] - v[s] - self.Wrp[s] @ pc[pt.p_grp[s]])
             a = np.zeros(self.topo.l2g.shape[1])
@@ -401,15 +431,10 @@ class Oracle:
                 dl = self.d_loc[s]
                 a[dl] = math.exp(-t) * self.Pi[s][dl]
             return a
-        self.a = self._map(recover, range(P))
+        a_new = self._map(recover, range(P))
         self.lam = lam
         self.pc = pc
-        self.ell += 1
-        self.iters.append(k)
-        self.hist.append(hist)
-        if self.errors is not None:
-            self.errors.after_step(a_old)
-        return k
+        return a_new, k, hist
 
     def run(self, n=None):
         n = self.prob.n_steps - self.ell if n is None else n

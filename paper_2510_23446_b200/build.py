@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtcg_ietidp.so")
 SOURCES = ["capi.cu", "plan.cpp"]
-DEPS = ["capi.cu", "plan.cpp", "plan.h", "assembly.cu", "chol.cu", "solve.cu", "pcg.cu", "nd.cu", "coarse_nd.h", "common.cuh", "device.h"]
+DEPS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h", ".cpp")))
 
 
 def nvcc() -> str:

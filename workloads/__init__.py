@@ -45,6 +45,10 @@ class Problem:
     tree_order: int = 0                  # 0 ascending ids within a rank, 1 descending
     warm_start: int = 0                  # 0: lambda0 = 0 (paper); k: projection on the last k solutions
     track_errors: bool = False           # source 3: accumulate eps_B, eps_E every step
+    nl: np.ndarray = None                # (P, 3) Brauer parameters (k1, k2, k3) per patch, nu = k1 exp(k2 |B|^2) + k3;
+                                         # all-zero rows (or None) = linear patch with nu_s (R25)
+    newton_tol: float = 1e-8             # Newton stop: ||a_{k+1} - a_k|| <= newton_tol ||a_{k+1}|| (per-patch vectors)
+    newton_max: int = 20
     extra: dict = field(default_factory=dict)
 
     @property
@@ -59,6 +63,7 @@ class Problem:
         d = asdict(self)
         d["sigma"] = [float(x) for x in self.sigma]
         d["nu"] = [float(x) for x in self.nu]
+        d["nl"] = None if self.nl is None else [[float(v) for v in row] for row in self.nl]
         return d
 
 
@@ -201,7 +206,41 @@ def paper(p: int, divs: int, n_steps: int, T: float = 1.0) -> Problem:
     return pr
 
 
-CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
+# Brauer parameters of the nonlinear workloads (R25): nu(0) = k1 + k3 = 1, nu grows
+# to ~2.7 at |B| = 0.5 and ~55 at |B| = 1 (the unit-amplitude BJ source gives |B| up to ~0.5)
+NL_SOFT = (0.1, 4.0, 0.9)
+
+
+def nonlinear(base: Problem, patches, k=NL_SOFT, amp: float = 1.0, name: str | None = None, **kw) -> Problem:
+    """`base` with Brauer reluctivity k on the listed patches, source
+    amplitude amp (kind 1 params (amp, 1)); other fields of `base` kept."""
+    P = base.n_patches
+    nl = np.zeros((P, 3))
+    for s in patches:
+        nl[s] = k
+    base.nl = nl
+    base.source_params = (float(amp), 1.0)
+    base.name = name or f"{base.name}-nl"
+    for key, v in kw.items():
+        setattr(base, key, v)
+    return base
+
+
+def nl1() -> Problem:
+    """cfg1 with its 4 conductor patches nonlinear (NL_SOFT), source amplitude 3."""
+    b = cfg1()
+    return nonlinear(b, [s for s in range(b.n_patches) if b.sigma[s] > 0], amp=3.0, name="nl1")
+
+
+def nl2() -> Problem:
+    """cfg2 with the conductor block and the ring of insulator patches around it in x,y
+    nonlinear (NL_SOFT), source amplitude 3, 50 steps."""
+    b = cfg2()
+    sel = [s for s, (ix, iy, iz) in enumerate(_grid(b.npatch)) if iz in (1, 2)]
+    return nonlinear(b, sel, amp=3.0, name="nl2")
+
+
+CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5, "nl1": nl1, "nl2": nl2}
 
 
 def get(name: str) -> Problem:
