@@ -107,6 +107,11 @@ typedef struct tcg_info {
   int64_t coarse_nodes;   /* separator-tree nodes of the sparse coarse (0 if dense)          */
   int64_t coarse_levels;  /* tree height + 1: forward + backward phases per coarse solve     */
   double coarse_factor_bytes; /* bytes of the coarse inverse factors read per coarse solve   */
+  int64_t n_nonlinear;    /* patches with a nonlinear reluctivity (tcg_set_nonlinear)          */
+  int64_t newton_iters;   /* Newton iterations over all steps done (= linear solves)           */
+  int64_t linear_solves;  /* IETI-DP linear solves done (one per step without nonlinear patches) */
+  int64_t hist_len;       /* entries of the concatenated relres history (tcg_get_history)      */
+  double ms_newton_numeric; /* device time of the Newton re-assemblies and factorisations      */
 } tcg_info;
 
 /* Create a handle (the solver object of BASELINE.json north_star "build patches, materials
@@ -186,6 +191,30 @@ tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, 
  * sized for the largest k) is allocated at the first warm step. EINVAL unless 0 <= k <= 4. */
 tcg_status tcg_set_warm_start(tcg_handle h, int k);
 
+/* Nonlinear reluctivity (the paper: "nonlinear behavior can be modeled as a
+ * simple extension"; law and linearisation are DESIGN.md R25). k[3n] holds per patch the
+ * Brauer parameters (k1, k2, k3) of nu(|B|) = k1 exp(k2 |B|^2) + k3 (k1, k2 >= 0, k3 > 0; an all-zero
+ * triple keeps the linear patch and its nu_s; n = 0 / k = NULL: no nonlinear patch). Every
+ * tcg_step then runs Newton's method per implicit-Euler step from a_0 = a^(l): iterate k
+ * re-assembles the nonlinear patches' tangent matrices J = Kt(a_k) + sigma/dt M,
+ * Kt_jk = <(nu I + 2 dnu/d|B|^2 B B^T) curl w_k, curl w_j> by (p+1)-point Gauss quadrature,
+ * re-factorises (local Cholesky, inverse factors, coarse problem) and solves
+ * J a_{k+1} = (Kt - K)(a_k) a_k + sigma/dt M a^(l) + j^(l+1) with the IETI-DP PCG; it stops when
+ * ||a_{k+1} - a_k||_2 <= newton_tol ||a_{k+1}||_2 over all patches' local vectors, and fails the
+ * call with TCG_ENOCONV after newton_max iterations. Defaults: no nonlinear patch, 1e-8, 20.
+ * tcg_get_history then reports per step the PCG iterations summed over its Newton solves, the
+ * last solve's final relres, and every solve's relres history (tcg_info.hist_len entries).
+ * Requires p <= 7, a source of kind 0-2, no warm start and no error tracking.
+ * Errors: TCG_EINVAL (length, parameter range), TCG_ESTATE (before set_patches, after plan/setup). */
+tcg_status tcg_set_nonlinear(tcg_handle h, const double* k, size_t n, double newton_tol, int newton_max);
+
+/* Newton statistics after the steps done: newton_iters[nsteps] (Newton iterations per step) and,
+ * per linear solve in order, solve_iters[nsolves] (PCG iterations) and increments[nsolves]
+ * (||a_{k+1} - a_k|| / ||a_{k+1}||); any pointer may be NULL. Without nonlinear patches nothing is
+ * recorded. Errors: TCG_EINVAL (more steps / solves than recorded). */
+tcg_status tcg_get_newton(tcg_handle h, int* newton_iters, size_t nsteps, int* solve_iters, double* increments,
+                          size_t nsolves);
+
 /* Error norms of the paper's experiment: with on = 1 (source TCG_SOURCE_PAPER,
  * single-process handle, before the first step) every tcg_step runs one step per launch and
  * accumulates on the device, by (p+1)-point Gauss quadrature per element,
@@ -239,7 +268,8 @@ tcg_status tcg_get_coefficients(tcg_handle h, int layout, double* out, size_t le
 /* Residual history of the PCG of P:L170 (iteration counts are the paper's scalability
  * indicator): per-step PCG iteration counts iters[nsteps] and final relative residuals
  * final_relres[nsteps] (either may be NULL); if relres_hist != NULL, the concatenated
- * per-step histories sqrt(r_k^T z_k / r_0^T z_0), k = 0..iters (sum(iters+1) values). */
+ * per-step histories sqrt(r_k^T z_k / r_0^T z_0), k = 0..iters (sum(iters+1) values; with
+ * nonlinear patches every Newton solve's history, tcg_info.hist_len values in all). */
 tcg_status tcg_get_history(tcg_handle h, int* iters, double* final_relres, size_t nsteps,
                            double* relres_hist, size_t hist_len);
 

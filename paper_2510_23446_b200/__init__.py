@@ -23,7 +23,7 @@ PLAN_EDGE_CLASS, PLAN_EDGE_REGION, PLAN_TREE, PLAN_PART, PLAN_PATCH_COUNTS, PLAN
 EXPORTS = ["tcg_create", "tcg_set_patches", "tcg_set_materials", "tcg_set_source", "tcg_set_time", "tcg_set_solver", "tcg_set_warm_start",
            "tcg_plan", "tcg_get_plan", "tcg_setup", "tcg_refactor", "tcg_step", "tcg_get_coefficients", "tcg_get_history",
            "tcg_get_info", "tcg_fapply", "tcg_bench_fapply", "tcg_set_profile", "tcg_set_virtual_ranks", "tcg_nccl_unique_id", "tcg_last_error",
-           "tcg_destroy", "tcg_set_error_tracking", "tcg_get_errors"]
+           "tcg_destroy", "tcg_set_error_tracking", "tcg_get_errors", "tcg_set_nonlinear", "tcg_get_newton"]
 
 
 class TcgInfo(C.Structure):
@@ -34,7 +34,9 @@ class TcgInfo(C.Structure):
         "bytes_fapply", "bytes_precond", "bytes_step_fixed", "flops_factor", "ms_plan", "ms_assembly", "ms_factor",
         "ms_coarse", "ms_steps", "ms_pcg_last_step", "prof_ms")] + [("prof_launches", C.c_int64),
         ("prof_bytes_per_launch", C.c_double), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("rank", C.c_int32), ("world", C.c_int32), ("pad_", C.c_int32),
-        ("coarse_sparse", C.c_int32), ("coarse_nodes", C.c_int64), ("coarse_levels", C.c_int64), ("coarse_factor_bytes", C.c_double)]
+        ("coarse_sparse", C.c_int32), ("coarse_nodes", C.c_int64), ("coarse_levels", C.c_int64), ("coarse_factor_bytes", C.c_double),
+        ("n_nonlinear", C.c_int64), ("newton_iters", C.c_int64), ("linear_solves", C.c_int64), ("hist_len", C.c_int64),
+        ("ms_newton_numeric", C.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_ if n != "pad_"}
@@ -84,6 +86,9 @@ def lib():
     if hasattr(L, "tcg_get_errors") or not os.environ.get("TCG_LIBPATH"):  # (older A/B builds lack them)
         L.tcg_set_error_tracking.argtypes = [vp, C.c_int]
         L.tcg_get_errors.argtypes = [vp, dp, dp, dp, C.c_size_t]
+    if hasattr(L, "tcg_set_nonlinear") or not os.environ.get("TCG_LIBPATH"):
+        L.tcg_set_nonlinear.argtypes = [vp, dp, C.c_size_t, C.c_double, C.c_int]
+        L.tcg_get_newton.argtypes = [vp, ip, C.c_size_t, ip, dp, C.c_size_t]
     L.tcg_destroy.argtypes = [vp]
     L.tcg_destroy.restype = None
     for n in EXPORTS:
@@ -160,6 +165,25 @@ class Solver:
         self._ck(self.L.tcg_get_errors(self.h, C.byref(eb), C.byref(ee), _dptr(ps) if per_step else None, ns))
         return (eb.value, ee.value, ps[:2 * ns].reshape(-1, 2)) if per_step else (eb.value, ee.value)
 
+    def set_nonlinear(self, k, newton_tol=1e-8, newton_max=20):
+        """Brauer reluctivity nu = k1 exp(k2 |B|^2) + k3 per patch (k: (P, 3); zero rows linear)
+        with Newton's method per step (R25)."""
+        k = np.ascontiguousarray(k, dtype=np.float64).reshape(-1)
+        self._ck(self.L.tcg_set_nonlinear(self.h, _dptr(k) if k.size else None, k.size // 3, float(newton_tol),
+                                          int(newton_max)))
+        return self
+
+    def newton(self):
+        """(Newton iterations per step, PCG iterations per linear solve, increments per solve)."""
+        inf = self.info()
+        ns, nv = inf["steps_done"] if inf["n_nonlinear"] else 0, inf["linear_solves"]
+        ni = np.zeros(max(ns, 1), dtype=np.int32)
+        si = np.zeros(max(nv, 1), dtype=np.int32)
+        inc = np.zeros(max(nv, 1))
+        self._ck(self.L.tcg_get_newton(self.h, ni.ctypes.data_as(C.POINTER(C.c_int)), ns,
+                                       si.ctypes.data_as(C.POINTER(C.c_int)), _dptr(inc), nv))
+        return ni[:ns], si[:nv], inc[:nv]
+
     def configure(self, prob):
         """Set everything from a problem description with the fields of workloads.Problem."""
         self.set_patches(prob.npatch, prob.lo, prob.hi, prob.p, prob.elems)
@@ -168,6 +192,8 @@ class Solver:
         self.set_time(prob.T, prob.n_steps)
         self.set_solver(prob.rtol, prob.max_iter, prob.scaling, prob.tree_order)
         self.set_warm_start(getattr(prob, "warm_start", 0))
+        if getattr(prob, "nl", None) is not None:
+            self.set_nonlinear(prob.nl, getattr(prob, "newton_tol", 1e-8), getattr(prob, "newton_max", 20))
         if getattr(prob, "track_errors", False):
             self.set_error_tracking(True)
         return self
@@ -208,7 +234,7 @@ class Solver:
         it = np.zeros(ns, dtype=np.int32)
         fr = np.zeros(ns)
         self._ck(self.L.tcg_get_history(self.h, it.ctypes.data_as(C.POINTER(C.c_int)), _dptr(fr), ns, None, 0))
-        hl = int(np.sum(it + 1))
+        hl = int(inf["hist_len"])
         hist = np.zeros(max(hl, 1))
         self._ck(self.L.tcg_get_history(self.h, None, None, ns, _dptr(hist), hl))
         return it, fr, hist[:hl]

@@ -34,6 +34,7 @@
 #include "pcg.cu"
 #include "nd.cu"
 #include "mms.cu"
+#include "nonlinear.cu"
 #include "coarse_nd.h"
 
 using namespace tcg;
@@ -102,6 +103,13 @@ struct RankDev {
   BarMem* bar = nullptr;
   PcgState* st = nullptr;
   DevError* derr = nullptr;
+  // nonlinear patches (nonlinear.cu): owned list, tile prefix, Gauss-point
+  // coefficients Q, Newton right-hand-side vector g (aug layout), a^l and the iterate a_k
+  std::vector<int> nlist;
+  int* d_nlist = nullptr;
+  int64_t* d_ntstart = nullptr;
+  int64_t nl_ntiles = 0;
+  double *Q = nullptr, *gnl = nullptr, *a_old = nullptr, *a_k = nullptr, *nl_part = nullptr;
   // replicated coarse problem (computed by the first local rank, aliased by other local ranks)
   double *C = nullptr, *Cinv = nullptr, *CX = nullptr, *Sinv = nullptr;
   DevPlan D{};  // DevPlan with me / A / Dinv / Sbb of this rank
@@ -129,6 +137,21 @@ struct tcg_ctx {
   double *err_part = nullptr, *err_acc = nullptr, *err_step = nullptr;
   int err_blocks = 0;
   double src_amp = 1.0, src_freq = 1.0;  // tcg_set_source params
+  // nonlinear reluctivity (tcg_set_nonlinear): Brauer (k1,k2,k3) per patch
+  std::vector<double> nlk;
+  int n_nl = 0;
+  double newton_tol = 1e-8;
+  int newton_max = 20;
+  double* d_nlk = nullptr;
+  double* nltab = nullptr;
+  NlTab ntab{};
+  size_t nl_smem = 0;
+  std::vector<int> newton_its, solve_its;
+  std::vector<double> solve_inc;
+  double ms_newton_numeric = 0.0;  // device time of the Newton re-assemblies + factorisations
+  bool is_nl(int s) const { return n_nl > 0 && (nlk[3 * s] != 0.0 || nlk[3 * s + 1] != 0.0 || nlk[3 * s + 2] != 0.0); }
+  // patches whose right-hand side is recomputed every step (mass term or Newton vector)
+  bool dyn(int s) const { return plan.sigma[s] > 0 || is_nl(s); }
   double T = 1.0;
   int n_steps = 0;
   double rtol = 1e-10;
@@ -225,6 +248,7 @@ struct tcg_ctx {
   int64_t steps_done = 0, total_iters = 0, hist_len = 0;
   std::vector<int> iters;
   std::vector<double> final_rel, hist_all;
+  std::vector<int64_t> hist_per_step;  // relres-history entries of each step (Newton: all its solves)
   int64_t nlaunch = 0;
   int64_t h2d_bytes = 0, d2h_bytes = 0;
   int prof_id = 0;
@@ -522,7 +546,10 @@ static tcg_status check_err(tcg_ctx* h) {
   return TCG_OK;
 }
 
-static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid = nullptr) {
+// newton = true: one Newton iterate's re-assembly and factorisation (nonlinear.cu, tcg_step):
+// the nonlinear patches' tangent matrices at the current coefficients a_loc, the Newton
+// right-hand-side vector g; the time-stepping state (a, steps, histories) is kept.
+static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid = nullptr, bool newton = false) {
   Plan& pl = h->plan;
   const int Tc = h->Tc;
   const double dt = h->T / h->n_steps;
@@ -572,6 +599,28 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
     } else if (!R.plist.empty()) {
       k_load_vector<<<(unsigned)R.plist.size(), 256, 0, h->stream>>>(R.D, h->tb, h->G, h->source, R.JS, R.d_plist);
       ++h->nlaunch;
+      CKL();
+    }
+  }
+  if (h->n_nl > 0) {
+    // nonlinear patches (nonlinear.cu): Gauss-point B, nu, nu' from the current coefficients
+    // (zero at setup / refactor: the time stepping restarts from A = 0), the tangent matrix
+    // J = Kt + (sigma/dt) M over k_assemble's tiles, and g = (Kt - K) a
+    k_nl_tab1d<<<3, 128, 0, h->stream>>>(h->nltab, h->ntab, h->tb, pl.p);
+    ++h->nlaunch;
+    CKL();
+    const int64_t nqp = (int64_t)h->ntab.nq[0] * h->ntab.nq[1] * h->ntab.nq[2];
+    for (auto& R : h->rd) {
+      if (!newton) CK(cudaMemsetAsync(R.a_loc, 0, sizeof(double) * (size_t)pl.npatch * pl.nloc, h->stream));
+      const unsigned nn = (unsigned)R.nlist.size();
+      if (nn == 0) continue;
+      k_nl_quad<<<dim3(nn, (unsigned)std::min<int64_t>(64, (nqp + 255) / 256)), 256, 0, h->stream>>>(
+          h->G, h->ntab, R.d_nlist, R.a_loc, h->d_nlk, R.Q);
+      k_nl_assemble<<<(unsigned)R.nl_ntiles, 256, h->nl_smem, h->stream>>>(R.D, h->tb, h->G, h->ntab, 1.0 / dt, R.d_nlist,
+                                                                           R.d_ntstart, (int)nn, R.Q);
+      k_nl_g<<<dim3(nn, (unsigned)((pl.nloc + 255) / 256)), 256, h->nl_smem, h->stream>>>(R.D, h->G, h->ntab, R.d_nlist,
+                                                                                        R.Q, R.gnl);
+      h->nlaunch += 3;
       CKL();
     }
   }
@@ -662,7 +711,7 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
       ++h->nlaunch;
       CKL();
     }
-    if (h->source != TCG_SOURCE_PAPER)  // (the paper's experiment starts from a(0) = amp Pi_h S, set above)
+    if (h->source != TCG_SOURCE_PAPER && !newton)  // (the paper's experiment starts from a(0) = amp Pi_h S, set above)
       CK(cudaMemsetAsync(R.a_loc, 0, sizeof(double) * (size_t)pl.npatch * pl.nloc, h->stream));
   }
   CK(cudaEventRecord(e3, h->stream));
@@ -671,11 +720,20 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
   h->ms_assembly = elapsed_ms(e0, e1);
   h->ms_factor = elapsed_ms(e1, e2);
   h->ms_coarse = elapsed_ms(e2, e3);
+  if (newton) {
+    h->ms_newton_numeric += elapsed_ms(e0, e3);
+    return TCG_OK;
+  }
+  h->newton_its.clear();
+  h->solve_its.clear();
+  h->solve_inc.clear();
+  h->ms_newton_numeric = 0.0;
   h->steps_done = 0;
   h->warm_base = 0;  // refactor / setup: the time integration restarts, so does the warm history
   h->hist_len = 0;
   h->total_iters = 0;
   h->iters.clear();
+  h->hist_per_step.clear();
   h->final_rel.clear();
   h->hist_all.clear();
   return TCG_OK;
@@ -1335,6 +1393,23 @@ static tcg_status do_setup(tcg_ctx* h) {
     if (pl.el[d] + 2 * pl.p > 160) return fail(h, TCG_EINVAL, "elements + 2p must be <= 160");
   }
   TRY(dalloc(h, &tb.base, toff));
+  if (h->n_nl > 0) {  // nonlinear patches (nonlinear.cu): Gauss-point tables, Brauer parameters
+    NlTab& NT = h->ntab;
+    NT.stride = 1 + 3 * (pl.p + 1);
+    int64_t o = 0;
+    for (int d = 0; d < 3; ++d) {
+      NT.nq[d] = pl.el[d] * (pl.p + 1);
+      NT.off[d] = o;
+      o += (int64_t)NT.nq[d] * NT.stride;
+    }
+    TRY(dalloc(h, &h->nltab, (size_t)o));
+    NT.base = h->nltab;
+    h->nl_smem = sizeof(double) * (size_t)o;
+    if (h->nl_smem > 200 * 1024) return fail(h, TCG_EINVAL, "nonlinear patches: Gauss-point tables exceed shared memory");
+    TRY(set_smem(h, (const void*)k_nl_g, h->nl_smem));
+    TRY(set_smem(h, (const void*)k_nl_assemble, h->nl_smem));
+    TRY(dupload(h, &h->d_nlk, h->nlk));
+  }
   {
     int maxn = 0, maxel = 0;
     for (int d = 0; d < 3; ++d) {
@@ -1460,14 +1535,14 @@ static tcg_status do_setup(tcg_ctx* h) {
         const int Trs = Ti[s] + Tb[s];
         for (int I = 0; I < T[s]; ++I) {
           const int cost = I < Trs ? I + 1 : Trs;
-          if (pl.sigma[s] > 0) fw.per_rank[r].push_back({cost, desc(s, I)});
+          if (h->dyn(s)) fw.per_rank[r].push_back({cost, desc(s, I)});
           fwa.per_rank[r].push_back({cost, desc(s, I)});
         }
         for (int J = 0; J < std::max(Trs, 1); ++J) {
           bw.per_rank[r].push_back({T[s] - J, desc(s, J)});
-          if (pl.sigma[s] > 0) bwc.per_rank[r].push_back({T[s] - J, desc(s, J)});
+          if (h->dyn(s)) bwc.per_rank[r].push_back({T[s] - J, desc(s, J)});
         }
-        if (pl.sigma[s] > 0)
+        if (h->dyn(s))
           for (int c = 0; c < 3; ++c) rhs.per_rank[r].push_back({pl.nloc / 3, desc(s, c)});
         else
           rhs.per_rank[r].push_back({T[s] * TS / 8, desc(s, -1)});
@@ -1686,6 +1761,23 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dzero(h, &R.bar, 1));
     TRY(dzero(h, &R.st, 1));
     TRY(dzero(h, &R.derr, 1));
+    for (int s : R.plist)
+      if (h->is_nl(s)) R.nlist.push_back(s);
+    if (!R.nlist.empty()) {
+      std::vector<int64_t> nts(1, 0);
+      for (int s : R.nlist) nts.push_back(nts.back() + tri_tiles(T[s]));
+      R.nl_ntiles = nts.back();
+      TRY(dupload(h, &R.d_nlist, R.nlist));
+      TRY(dupload(h, &R.d_ntstart, nts));
+      const int64_t nqp = (int64_t)h->ntab.nq[0] * h->ntab.nq[1] * h->ntab.nq[2];
+      TRY(dalloc(h, &R.Q, (size_t)R.nlist.size() * 9 * nqp));
+    }
+    if (h->n_nl > 0) {  // every rank joins the Newton loop (right-hand side vector, iterates, norms)
+      TRY(dzero(h, &R.gnl, ov));
+      TRY(dzero(h, &R.a_old, (size_t)P * pl.nloc));
+      TRY(dzero(h, &R.a_k, (size_t)P * pl.nloc));
+      TRY(dzero(h, &R.nl_part, 2 * (size_t)NL_NORM_BLOCKS));
+    }
     if (li == 0) {
       const int Tcd = h->sparse ? 1 : Tc;  // the sparse coarse keeps no dense factor / inverse
       TRY(dalloc(h, &R.C, (size_t)tri_tiles(Tcd) * TSZ));
@@ -1962,8 +2054,11 @@ static tcg_status agree_warm(tcg_ctx* h) {
   return TCG_OK;
 }
 
-// n implicit-Euler steps in ONE persistent cooperative launch (k_steps) over all local ranks
-static tcg_status do_steps(tcg_ctx* h, int n) {
+// n implicit-Euler steps in ONE persistent cooperative launch (k_steps) over all local ranks.
+// newton_it != nullptr: one linear solve of a Newton iterate of step steps_done (n = 1; the
+// mass term reads a_old, the right-hand side adds gnl); its PCG iterations and final relres go
+// to *newton_it / *newton_rel and its history is appended, but the step is not counted.
+static tcg_status do_steps(tcg_ctx* h, int n, int* newton_it = nullptr, double* newton_rel = nullptr) {
   if (n <= 0) return TCG_OK;
   if (h->steps_done + n > h->n_steps) return fail(h, TCG_EINVAL, "more steps than set_time allows (n_steps)");
   for (auto& R : h->rd) CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), h->stream));
@@ -1981,6 +2076,13 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   if (h->world > 1) TRY(agree_warm(h));
   StepArgs A = step_args(h);
   A.nsteps = n;
+  if (newton_it) {
+    for (auto& R : h->rd) {
+      A.a_old[R.r] = R.a_old;
+      A.gnl[R.r] = R.gnl;
+    }
+    A.hist_off = 0;  // each solve's history starts at the buffer's head (copied out below)
+  }
   DevPlan D = h->D;
   void* args[] = {(void*)&D, (void*)&A};
   const int grid = h->nbr * (int)h->rd.size();
@@ -2004,7 +2106,8 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   std::vector<double> hh(std::max<int64_t>(hl, 1));
   // histories are written by rank 0 (block 0); on other ranks use the local iteration counts
   const bool have_hist = (h->world == 1 || h->rank == 0);
-  if (have_hist && hl > 0) CK(cudaMemcpy(hh.data(), R0.hist + h->hist_len, sizeof(double) * hl, cudaMemcpyDeviceToHost));
+  if (have_hist && hl > 0)
+    CK(cudaMemcpy(hh.data(), R0.hist + (newton_it ? 0 : h->hist_len), sizeof(double) * hl, cudaMemcpyDeviceToHost));
   h->d2h_bytes += (int64_t)(sizeof(int) * n + sizeof(double) * hl);
   if (hs.failed) {
     std::ostringstream o;
@@ -2013,9 +2116,18 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
     h->broken = true;
     return fail(h, TCG_ENOCONV, o.str());
   }
+  if (newton_it) {
+    *newton_it = it[0];
+    *newton_rel = have_hist ? hh[it[0]] : 0.0;
+    if (have_hist) h->hist_all.insert(h->hist_all.end(), hh.begin(), hh.begin() + hl);
+    else h->hist_all.insert(h->hist_all.end(), (size_t)hl, 0.0);
+    h->hist_len += hl;
+    return TCG_OK;
+  }
   int64_t off = 0;
   for (int i = 0; i < n; ++i) {
     h->iters.push_back(it[i]);
+    h->hist_per_step.push_back(it[i] + 1);
     h->final_rel.push_back(have_hist ? hh[off + it[i]] : 0.0);
     off += it[i] + 1;
     h->total_iters += it[i];
@@ -2024,6 +2136,66 @@ static tcg_status do_steps(tcg_ctx* h, int n) {
   else h->hist_all.insert(h->hist_all.end(), (size_t)hl, 0.0);
   h->hist_len += hl;
   h->steps_done += n;
+  return TCG_OK;
+}
+
+// One implicit-Euler step with nonlinear patches (R25): Newton from
+// a_0 = a^l; iterate k re-assembles and factorises at a_k (do_numeric newton mode: the
+// nonlinear patches' tangent matrices and g = (Kt - K) a_k), then one linear IETI-DP solve of
+// J(a_k) a_{k+1} = g + (sigma/dt) M a^l + j^(l+1) in the persistent stepper. Stops when
+// ||a_{k+1} - a_k|| <= newton_tol ||a_{k+1}|| (all patches' local vectors; fixed-order sums
+// of per-block partials in rank order, NCCL sum across processes).
+static tcg_status do_newton_step(tcg_ctx* h) {
+  const Plan& pl = h->plan;
+  const int64_t nall = (int64_t)pl.npatch * pl.nloc;
+  const size_t nb = sizeof(double) * (size_t)nall;
+  for (auto& R : h->rd) CK(cudaMemcpyAsync(R.a_old, R.a_loc, nb, cudaMemcpyDeviceToDevice, h->stream));
+  int total = 0, it = 0;
+  double rel = 0.0, inc = 0.0;
+  std::vector<double> part(2 * NL_NORM_BLOCKS);
+  for (it = 1;; ++it) {
+    for (auto& R : h->rd) CK(cudaMemcpyAsync(R.a_k, R.a_loc, nb, cudaMemcpyDeviceToDevice, h->stream));
+    TRY(do_numeric(h, nullptr, true));
+    int its = 0;
+    TRY(do_steps(h, 1, &its, &rel));
+    total += its;
+    double sums[2] = {0.0, 0.0};
+    for (auto& R : h->rd) {
+      k_nl_norms<<<NL_NORM_BLOCKS, 256, 0, h->stream>>>(R.a_loc, R.a_k, h->D.owner, R.r, pl.nloc, nall, R.nl_part);
+      ++h->nlaunch;
+      CKL();
+      CK(cudaMemcpyAsync(part.data(), R.nl_part, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      for (int b = 0; b < NL_NORM_BLOCKS; ++b) {
+        sums[0] += part[2 * b];
+        sums[1] += part[2 * b + 1];
+      }
+    }
+    if (h->world > 1) {
+      if (!h->agree_buf) TRY(dzero(h, &h->agree_buf, 4));
+      CK(cudaMemcpyAsync(h->agree_buf, sums, sizeof sums, cudaMemcpyHostToDevice, h->stream));
+      ncclResult_t r = g_nccl.allReduce(h->agree_buf, h->agree_buf, 2, ncclFloat64, ncclSum, h->comm, h->stream);
+      if (r != 0) return fail(h, TCG_ENCCL, "ncclAllReduce (Newton increment) failed");
+      CK(cudaMemcpyAsync(sums, h->agree_buf, sizeof sums, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    }
+    inc = sums[1] > 0.0 ? std::sqrt(sums[0] / sums[1]) : 0.0;
+    h->solve_its.push_back(its);
+    h->solve_inc.push_back(inc);
+    if (inc <= h->newton_tol) break;
+    if (it >= h->newton_max) {
+      h->broken = true;
+      std::ostringstream o;
+      o << "Newton did not converge: step " << h->steps_done + 1 << ", " << it << " iterations, increment " << inc;
+      return fail(h, TCG_ENOCONV, o.str());
+    }
+  }
+  h->newton_its.push_back(it);
+  h->hist_per_step.push_back(total + it);
+  h->iters.push_back(total);
+  h->final_rel.push_back(rel);
+  h->total_iters += total;
+  h->steps_done += 1;
   return TCG_OK;
 }
 
@@ -2124,6 +2296,49 @@ tcg_status tcg_set_source(tcg_handle h, int kind, const double* params, size_t n
   return TCG_OK;
 }
 
+tcg_status tcg_set_nonlinear(tcg_handle h, const double* k, size_t n, double newton_tol, int newton_max) {
+  if (!h) return TCG_EINVAL;
+  if (h->planned || h->setup_done) return fail(h, TCG_ESTATE, "set_nonlinear after plan/setup");
+  if (!h->have_patches) return fail(h, TCG_ESTATE, "set_patches first");
+  const size_t P = (size_t)h->plan.P[0] * h->plan.P[1] * h->plan.P[2];
+  if (n != 0 && (!k || n != P)) return fail(h, TCG_EINVAL, "one (k1, k2, k3) triple per patch (" + std::to_string(P) + ")");
+  if (!(newton_tol > 0) || !std::isfinite(newton_tol) || newton_max < 1)
+    return fail(h, TCG_EINVAL, "newton_tol > 0 and newton_max >= 1 required");
+  int cnt = 0;
+  for (size_t s = 0; s < n; ++s) {
+    const double k1 = k[3 * s], k2 = k[3 * s + 1], k3 = k[3 * s + 2];
+    if (!std::isfinite(k1) || !std::isfinite(k2) || !std::isfinite(k3))
+      return fail(h, TCG_EINVAL, "Brauer parameters must be finite");
+    if (k1 == 0.0 && k2 == 0.0 && k3 == 0.0) continue;
+    if (!(k1 >= 0.0) || !(k2 >= 0.0) || !(k3 > 0.0))
+      return fail(h, TCG_EINVAL, "Brauer parameters need k1 >= 0, k2 >= 0, k3 > 0 (patch " + std::to_string(s) + ")");
+    ++cnt;
+  }
+  if (cnt > 0 && h->plan.p > NL_MAXP) return fail(h, TCG_EINVAL, "nonlinear patches need p <= " + std::to_string(NL_MAXP));
+  if (cnt > 0 && h->warm) return fail(h, TCG_EINVAL, "warm start is not available with nonlinear patches");
+  h->nlk.assign(k ? k : nullptr, k ? k + 3 * n : nullptr);
+  h->n_nl = cnt;
+  h->newton_tol = newton_tol;
+  h->newton_max = newton_max;
+  return TCG_OK;
+}
+
+tcg_status tcg_get_newton(tcg_handle h, int* newton_iters, size_t nsteps, int* solve_iters, double* increments,
+                          size_t nsolves) {
+  if (!h) return TCG_EINVAL;
+  if (nsteps > h->newton_its.size())
+    return fail(h, TCG_EINVAL, "only " + std::to_string(h->newton_its.size()) + " Newton steps recorded");
+  if (nsolves > h->solve_its.size())
+    return fail(h, TCG_EINVAL, "only " + std::to_string(h->solve_its.size()) + " linear solves recorded");
+  for (size_t i = 0; i < nsteps; ++i)
+    if (newton_iters) newton_iters[i] = h->newton_its[i];
+  for (size_t i = 0; i < nsolves; ++i) {
+    if (solve_iters) solve_iters[i] = h->solve_its[i];
+    if (increments) increments[i] = h->solve_inc[i];
+  }
+  return TCG_OK;
+}
+
 tcg_status tcg_set_time(tcg_handle h, double T, int n_steps) {
   if (!h) return TCG_EINVAL;
   if (h->setup_done) return fail(h, TCG_ESTATE, "set_time after setup");
@@ -2148,6 +2363,7 @@ tcg_status tcg_set_solver(tcg_handle h, double rtol, int max_iter, int scaling, 
 
 tcg_status tcg_set_warm_start(tcg_handle h, int on) {
   if (!h) return TCG_EINVAL;
+  if (on && h->n_nl > 0) return fail(h, TCG_EINVAL, "warm start is not available with nonlinear patches");
   if (on < 0 || on > KW) return fail(h, TCG_EINVAL, "warm start subspace dimension must be in [0, " + std::to_string(KW) + "]");
   if (on != h->warm) h->warm_base = h->steps_done;  // a new subspace size restarts the history
   h->warm = on;
@@ -2156,6 +2372,7 @@ tcg_status tcg_set_warm_start(tcg_handle h, int on) {
 
 tcg_status tcg_set_error_tracking(tcg_handle h, int on) {
   if (!h) return TCG_EINVAL;
+  if (on && h->n_nl > 0) return fail(h, TCG_EINVAL, "error tracking is not available with nonlinear patches");
   if (on && h->source != TCG_SOURCE_PAPER) return fail(h, TCG_EINVAL, "error tracking needs TCG_SOURCE_PAPER (the exact solution)");
   if (on && h->world > 1) return fail(h, TCG_EINVAL, "error tracking needs a single-process handle");
   if (h->setup_done && h->steps_done > 0) return fail(h, TCG_ESTATE, "enable error tracking before the first step");
@@ -2235,6 +2452,9 @@ tcg_status tcg_setup(tcg_handle h) {
   if (!h) return TCG_EINVAL;
   if (h->setup_done) return fail(h, TCG_ESTATE, "setup already done");
   if (h->broken) return fail(h, TCG_ESTATE, "handle is in a failed state");
+  if (h->n_nl > 0 && h->source == TCG_SOURCE_PAPER)
+    return fail(h, TCG_EINVAL, "nonlinear patches need a source without Dirichlet lifting (kinds 0-2)");
+  if (h->n_nl > 0 && h->track) return fail(h, TCG_EINVAL, "error tracking is not available with nonlinear patches");
   tcg_status s = do_setup(h);
   if (s != TCG_OK) h->broken = true;  // ENOTSPD included: only get_* / destroy afterwards
   return s;
@@ -2296,6 +2516,9 @@ tcg_status tcg_step(tcg_handle h, int n) {
       ++h->nlaunch;
       CKL();
     }
+  } else if (h->n_nl > 0) {
+    if (h->steps_done + n > h->n_steps) s = fail(h, TCG_EINVAL, "more steps than set_time allows (n_steps)");
+    for (int i = 0; i < n && s == TCG_OK; ++i) s = do_newton_step(h);
   } else {
     s = do_steps(h, n);
   }
@@ -2352,7 +2575,7 @@ tcg_status tcg_get_history(tcg_handle h, int* iters, double* final_relres, size_
   }
   if (relres_hist) {
     size_t need = 0;
-    for (size_t i = 0; i < nsteps; ++i) need += h->iters[i] + 1;
+    for (size_t i = 0; i < nsteps; ++i) need += h->hist_per_step[i];
     if (hist_len < need) return fail(h, TCG_EINVAL, "history buffer too short: need " + std::to_string(need));
     std::copy(h->hist_all.begin(), h->hist_all.begin() + need, relres_hist);
   }
@@ -2392,7 +2615,7 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
     bm += 4.0 * q.nb * (q.nb + 1);
     const double nrp = (double)nr;
     // per step outside PCG: conductors read [X_rr; Phi^T] twice (R2 forward, E3 backward)
-    if (p.sigma[s] > 0) bs += 2.0 * 8.0 * (nrp * (nrp + 1) / 2 + nrp * q.np);
+    if (h->dyn(s)) bs += 2.0 * 8.0 * (nrp * (nrp + 1) / 2 + nrp * q.np);
     // Cholesky + p-row TRSM + S^s update, then the inverse factors X_rr = L_rr^-1 (nr^3/3) and
     // X_pr = L_pr X_rr (np nr^2)
     fl += nrp * nrp * nrp / 3.0 + 2.0 * nrp * nrp * q.np + 2.0 * nrp * q.np * q.np;
@@ -2451,6 +2674,13 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
   out->prof_bytes_per_launch = 0.0;  // per-launch bytes of the stepper depend on iterations (bench.py)
   out->h2d_bytes = h->h2d_bytes;
   out->d2h_bytes = h->d2h_bytes;
+  out->n_nonlinear = h->n_nl;
+  out->newton_iters = 0;
+  for (int v : h->newton_its) out->newton_iters += v;
+  out->linear_solves = (int64_t)h->solve_its.size();
+  out->hist_len = 0;
+  for (int64_t v : h->hist_per_step) out->hist_len += v;
+  out->ms_newton_numeric = h->ms_newton_numeric;
   return TCG_OK;
 }
 

@@ -73,6 +73,10 @@ struct StepArgs {
   double* Y2[MAXR];    // P5/R4 output: b part y, -Phi_b N Pc part
   double* PW[MAXR];    // S_bb apply output: b part
   double* a_loc[MAXR]; // local coefficient vectors (npatch x nloc)
+  // Newton iterate of a nonlinear step (nonlinear.cu; null otherwise): R1's mass term reads
+  // a^l from a_old instead of a_loc, and the right-hand side gains gnl (aug order)
+  double* a_old[MAXR];
+  double* gnl[MAXR];
   // coarse
   const double* Sinv[MAXR];  // full symmetric S_pp^-1 (replicated), Tc x Tc row-major tiles
   double* Ppart[MAXR];       // Tc x maxch x 64 chunk partials of Pc (rows of the owning rank)
@@ -815,7 +819,8 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
   const int nn = nx * ny * nz;
   int off = 0;
   for (int cc = 0; cc < c; ++cc) off += G.cdim[cc][0] * G.cdim[cc][1] * G.cdim[cc][2];
-  const double* as = A.a_loc[me] + (int64_t)s * G.nloc + off;
+  const double* as = (A.a_old[me] ? A.a_old[me] : A.a_loc[me]) + (int64_t)s * G.nloc + off;
+  const double* gn = A.gnl[me];
   double* u0 = sm;
   double* u1 = sm + nn;
   const int n0 = tb.el[0] + p, n1 = tb.el[1] + p, n2 = tb.el[2] + p;
@@ -845,7 +850,7 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
     const int ij = e % (nx * ny), k = e / (nx * ny);
     double v = 0.0;
     for (int q = max(0, k - p); q <= min(nz - 1, k + p); ++q) v += Fz[k * ldz + q] * u1[ij + nx * ny * q];
-    A.F[me][vo + pos] = scale * v + phi * A.JS[me][vo + pos];
+    A.F[me][vo + pos] = scale * v + phi * A.JS[me][vo + pos] + (gn ? gn[vo + pos] : 0.0);
   }
   __syncthreads();
 }

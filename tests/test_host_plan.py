@@ -59,6 +59,26 @@ def test_argument_validation(tcg):
         assert e.value.status == tcg.TCG_EINVAL
     s.set_warm_start(4)
     s.set_warm_start(0)
+    # nonlinear reluctivity (R25): one Brauer triple per patch
+    for bad in ([[0.1, 4.0, 0.9]], [[0.1, 4.0, 0.0], [0, 0, 0]], [[-0.1, 4.0, 0.9], [0, 0, 0]],
+                [[0.1, -1.0, 0.9], [0, 0, 0]], [[np.nan, 1.0, 1.0], [0, 0, 0]]):
+        with pytest.raises(tcg.TcgError) as e:
+            s.set_nonlinear(np.array(bad, dtype=float))
+        assert e.value.status == tcg.TCG_EINVAL
+    for tol, mx in ((0.0, 20), (1e-8, 0)):
+        with pytest.raises(tcg.TcgError) as e:
+            s.set_nonlinear(np.array([[0.1, 4.0, 0.9], [0, 0, 0]]), tol, mx)
+        assert e.value.status == tcg.TCG_EINVAL
+    s.set_nonlinear(np.array([[0.1, 4.0, 0.9], [0, 0, 0]]))
+    with pytest.raises(tcg.TcgError) as e:
+        s.set_warm_start(2)                        # not with nonlinear patches
+    assert e.value.status == tcg.TCG_EINVAL
+    s.set_nonlinear(np.zeros((2, 3)))              # all-zero triples: linear again
+    s.set_warm_start(2)
+    with pytest.raises(tcg.TcgError) as e:
+        s.set_nonlinear(np.array([[0.1, 4.0, 0.9], [0, 0, 0]]))
+    assert e.value.status == tcg.TCG_EINVAL        # ... nor with a warm start set
+    s.set_warm_start(0)
     s.set_materials([1.0, 0.0], [1.0, 1.0])
     s.set_time(1.0, 4)
     s.plan()
