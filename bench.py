@@ -432,6 +432,48 @@ def measure_extra(tcg, name, stream, flush, peak, passes):
     return out
 
 
+def measure_nonlinear(tcg, name, stream, flush, passes):
+    """the nonlinear workload's pass (refactor + n_t steps, each
+    step Newton's method: per iterate re-assembly of the nonlinear patches' tangent matrices,
+    their re-factorisation + coarse, one stepper launch), event-timed like the headline."""
+    import torch
+    prob = workloads.get(name)
+    s = tcg.Solver(stream=stream.cuda_stream).configure(prob)
+    s.setup()
+    n_t = prob.n_steps
+
+    def one_pass():
+        s.refactor()
+        s.step(n_t)
+
+    one_pass()
+    tot = 0.0
+    num0 = 0.0
+    for _ in range(passes):
+        with torch.cuda.stream(stream):
+            flush.fill_(1.0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        one_pass()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+        num0 += s.info()["ms_newton_numeric"]
+    inf = s.info()
+    ni, si, _ = s.newton()
+    value = n_t * passes / (tot / 1000.0)
+    out = {"workload": config_desc(prob) + f", {int(inf['n_nonlinear'])} nonlinear patches (Brauer {tuple(prob.nl[prob.nl.any(1)][0])}), "
+                                           f"source amplitude {prob.source_params[0]}",
+           "steps_per_s": value, "newton_iters_per_step": float(np.mean(ni)), "pcg_iters_per_solve": float(np.mean(si)),
+           "linear_solves_per_s": value * float(np.mean(ni)), "ms_per_pass": tot / passes, "passes": passes,
+           "newton_numeric_share": num0 / tot,
+           "note": "per Newton iterate: k_nl_quad + k_nl_assemble + k_nl_g, re-factorisation of the nonlinear patches "
+                   "and the coarse problem (newton_numeric_share of the pass), one k_steps launch; host loop per iterate"}
+    s.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -444,6 +486,7 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip cfg1-cfg4 beside the headline config")
     ap.add_argument("--extra-configs", default="cfg1,cfg2,cfg3,cfg4")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--nonlinear", default="nl2", help="nonlinear workload beside the headline (SURVEY f4); '' = none")
     args = ap.parse_args()
     t_start = time.perf_counter()
     if args.warmup < 3:
@@ -605,6 +648,10 @@ def main():
         for name in [c for c in args.extra_configs.split(",") if c and c != args.config]:
             extras[name] = measure_extra(tcg, name, stream, flush, peak, passes=3 if name != "cfg4" else 2)
 
+    nonlin = None
+    if world == 1 and not args.no_extras and args.nonlinear:
+        nonlin = measure_nonlinear(tcg, args.nonlinear, stream, flush, passes=2)
+
     # ---- cpu baseline (oracle, rank 0, N=1 only) ----
     cpu = None
     if not args.no_cpu_baseline and world == 1 and rank == 0:
@@ -628,7 +675,7 @@ def main():
             "pcg_iters_per_step": iters_per_step,
             "setup_ms": inf["ms_assembly"] + inf["ms_factor"] + inf["ms_coarse"],
             "roofline": roof, "fapply": fap, "factorisation": fac, "warm_start": warm, "kernel_shares": shares,
-            "configs": extras, "cpu_baseline": cpu, "e2e": e2e,
+            "configs": extras, "nonlinear": nonlin, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "wall_s": time.perf_counter() - t_start,
         }
         print(json.dumps(line), flush=True)

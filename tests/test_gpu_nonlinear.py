@@ -140,3 +140,23 @@ def test_refactor_restarts_newton(tcg):
     s.step(2)
     assert np.array_equal(a, s.coefficients(1)) and list(s.newton()[0]) == ni
     s.close()
+
+
+def test_nl2_golden(tcg):
+    """cfg2-size nonlinear workload (workloads.nl2: 32 nonlinear patches), first 5 steps, against
+    the oracle's golden file (tools/make_golden.py nl2 --steps 5, oracle only), in the bench's
+    launch configuration (library defaults)."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "nl2_s5.npz")
+    gd = np.load(path)
+    meta = json.loads(str(gd["meta"]))
+    pr = workloads.nl2()
+    g = run_gpu(tcg, pr, meta["steps"])
+    ref = gd["a1"]
+    err = np.linalg.norm(g["a1"] - ref) / np.linalg.norm(ref)
+    assert err <= TOL, err
+    assert np.max(np.abs(g["a1"] - ref)) <= TOL * np.max(np.abs(ref))
+    ni, si, inc = g["newton"]
+    assert list(ni) == list(gd["newton_iters"]), (list(ni), list(gd["newton_iters"]))
+    assert np.all(np.abs(si - gd["solve_iters"]) <= 1), (list(si), list(gd["solve_iters"]))

@@ -13,6 +13,8 @@ tests/golden/<cfg>_s<steps>.npz holds
   iters      PCG iterations of every step
   relres     final relative residual of every step
   meta       JSON: config, steps, rtol, scaling, counts, host cores, wall times
+  nonlinear workloads (prob.nl set, oracle/nonlinear.py NewtonOracle) add newton_iters (per
+  step), solve_iters and increments (per linear solve); relres is then per linear solve
 """
 from __future__ import annotations
 
@@ -29,6 +31,7 @@ import numpy as np  # noqa: E402
 
 import workloads  # noqa: E402
 from oracle.ietidp import Oracle  # noqa: E402
+from oracle.nonlinear import NewtonOracle  # noqa: E402
 
 
 def main():
@@ -40,7 +43,10 @@ def main():
     args = ap.parse_args()
     prob = workloads.get(args.config)
     t0 = time.perf_counter()
-    o = Oracle(prob, workers=args.workers, lean=True)
+    if prob.nl is not None:  # nonlinear workloads: Newton oracle, full storage
+        o = NewtonOracle(prob, workers=args.workers)
+    else:
+        o = Oracle(prob, workers=args.workers, lean=True)
     t_setup = time.perf_counter() - t0
     print(f"{args.config}: setup {t_setup:.1f} s (m={o.part.m}, n_c={o.part.nc})", flush=True)
     t_steps = []
@@ -57,8 +63,12 @@ def main():
             "step_s": t_steps, "writer": "tools/make_golden.py (oracle only)"}
     os.makedirs(args.out, exist_ok=True)
     path = os.path.join(args.out, f"{args.config}_s{args.steps}.npz")
+    extra = {}
+    if prob.nl is not None:
+        extra = dict(newton_iters=np.array(o.newton_iters, dtype=np.int32),
+                     solve_iters=np.array(o.solve_iters, dtype=np.int32), increments=np.array(o.increments))
     np.savez_compressed(path, a1=a1, iters=np.array(o.iters, dtype=np.int32),
-                        relres=np.array([h[-1] for h in o.hist]), meta=np.array(json.dumps(meta)))
+                        relres=np.array([h[-1] for h in o.hist]), meta=np.array(json.dumps(meta)), **extra)
     print(f"wrote {path} ({os.path.getsize(path) / 1e6:.1f} MB)", flush=True)
 
 
