@@ -281,7 +281,22 @@ __global__ void __launch_bounds__(256) k_assemble(DevPlan D, Tables1D tb, Geom G
 
 // rho-scaling weights (R5): for multiplier k joining s+ and s-,
 // w+ = rho(s-)/(rho(s+)+rho(s-)), w- = rho(s+)/(rho(s+)+rho(s-)), rho = diagonal of W^.
-__global__ void k_rho_weights(DevPlan D, int scaling) {
+// k_rho_capture copies the two diagonal entries from the assembled tiles into rho[2k], rho[2k+1]
+// (only the sides whose patch has only[s] != 0, if only is given: the Newton re-assembly of the
+// nonlinear patches, nonlinear.cu); k_rho_weights forms the weights from them.
+__global__ void k_rho_capture(DevPlan D, double* rho, const unsigned char* only) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= D.m) return;
+  for (int side = 0; side < 2; ++side) {
+    int s = side == 0 ? D.lam_patch_p[k] : D.lam_patch_m[k];
+    if (only && !only[s]) continue;
+    int pos = D.Ti[s] * TS + (side == 0 ? D.lam_pos_p[k] : D.lam_pos_m[k]);
+    int Itile = pos / TS, rr = pos % TS;
+    rho[2 * k + side] = D.Ar[D.owner[s]][D.a_off[s] + tri_off(Itile, Itile) + rr * TS + rr];
+  }
+}
+
+__global__ void k_rho_weights(DevPlan D, int scaling, const double* rho) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= D.m) return;
   if (scaling == 0) {
@@ -289,15 +304,9 @@ __global__ void k_rho_weights(DevPlan D, int scaling) {
     D.wminus[k] = 1.0;
     return;
   }
-  double rho[2];
-  for (int side = 0; side < 2; ++side) {
-    int s = side == 0 ? D.lam_patch_p[k] : D.lam_patch_m[k];
-    int pos = D.Ti[s] * TS + (side == 0 ? D.lam_pos_p[k] : D.lam_pos_m[k]);
-    int Itile = pos / TS, rr = pos % TS;
-    rho[side] = D.Ar[D.owner[s]][D.a_off[s] + tri_off(Itile, Itile) + rr * TS + rr];
-  }
-  D.wplus[k] = rho[1] / (rho[0] + rho[1]);
-  D.wminus[k] = rho[0] / (rho[0] + rho[1]);
+  const double rp = rho[2 * k], rm = rho[2 * k + 1];
+  D.wplus[k] = rm / (rp + rm);
+  D.wminus[k] = rp / (rp + rm);
 }
 
 // Per b position: a_own = weight of this side, a_part = -(weight of the other side), so that

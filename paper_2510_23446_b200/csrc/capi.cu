@@ -107,6 +107,8 @@ struct RankDev {
   // coefficients Q, Newton right-hand-side vector g (aug layout), a^l and the iterate a_k
   std::vector<int> nlist;
   int* d_nlist = nullptr;
+  CholDesc* d_nldesc = nullptr;
+  int nl_maxT = 0, nl_maxTr = 0, nl_maxTb = 0;
   int64_t* d_ntstart = nullptr;
   int64_t nl_ntiles = 0;
   double *Q = nullptr, *gnl = nullptr, *a_old = nullptr, *a_k = nullptr, *nl_part = nullptr;
@@ -143,6 +145,9 @@ struct tcg_ctx {
   double newton_tol = 1e-8;
   int newton_max = 20;
   double* d_nlk = nullptr;
+  unsigned char* d_nlflag = nullptr;  // per patch: 1 = nonlinear
+  double* rho_diag = nullptr;         // per multiplier: W^ diagonal at its + and - copies
+  bool err_nl = false;                // the last factorisation ran over the nonlinear lists
   double* nltab = nullptr;
   NlTab ntab{};
   size_t nl_smem = 0;
@@ -537,7 +542,7 @@ static tcg_status check_err(tcg_ctx* h) {
     if (herr.flag) {
       h->broken = true;
       std::ostringstream o;
-      if (herr.matrix >= 0) o << "local Cholesky: patch " << R.plist[herr.matrix];
+      if (herr.matrix >= 0) o << "local Cholesky: patch " << (h->err_nl ? R.nlist : R.plist)[herr.matrix];
       else o << "coarse Cholesky";
       o << " pivot " << herr.index << " value " << herr.value;
       return fail(h, TCG_ENOTSPD, o.str());
@@ -564,9 +569,13 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
   } ev;
   cudaEvent_t e0 = ev.e[0], e1 = ev.e[1], e2 = ev.e[2], e3 = ev.e[3];
   CK(cudaEventRecord(e0, h->stream));
-  k_tables1d<<<3, 256, h->smem_tables, h->stream>>>(h->tb, pl.p, h->source == TCG_SOURCE_PAPER ? 1.0 : M_PI);
-  ++h->nlaunch;
-  CKL();
+  // Newton iterates re-assemble and re-factorise the nonlinear patches only: the linear
+  // patches' factors, S_bb, inverse factors, S^s and load vectors are unchanged
+  if (!newton) {
+    k_tables1d<<<3, 256, h->smem_tables, h->stream>>>(h->tb, pl.p, h->source == TCG_SOURCE_PAPER ? 1.0 : M_PI);
+    ++h->nlaunch;
+    CKL();
+  }
   if (h->source == TCG_SOURCE_PAPER) {
     const int maxP = std::max(pl.P[0], std::max(pl.P[1], pl.P[2]));
     int maxn = 0;
@@ -579,8 +588,10 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
       CK(cudaMemsetAsync(h->err_acc, 0, 8 * sizeof(double), h->stream));
     }
   }
+  h->err_nl = newton;
   for (auto& R : h->rd) {
     CK(cudaMemsetAsync(R.derr, 0, sizeof(DevError), h->stream));
+    if (newton) continue;
     if (R.ntiles > 0) {
       k_assemble<<<(unsigned)R.ntiles, 256, 0, h->stream>>>(R.D, h->tb, h->G, 1.0 / dt, R.d_plist, R.d_tstart,
                                                            (int)R.plist.size());
@@ -606,9 +617,11 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
     // nonlinear patches (nonlinear.cu): Gauss-point B, nu, nu' from the current coefficients
     // (zero at setup / refactor: the time stepping restarts from A = 0), the tangent matrix
     // J = Kt + (sigma/dt) M over k_assemble's tiles, and g = (Kt - K) a
-    k_nl_tab1d<<<3, 128, 0, h->stream>>>(h->nltab, h->ntab, h->tb, pl.p);
-    ++h->nlaunch;
-    CKL();
+    if (!newton) {
+      k_nl_tab1d<<<3, 128, 0, h->stream>>>(h->nltab, h->ntab, h->tb, pl.p);
+      ++h->nlaunch;
+      CKL();
+    }
     const int64_t nqp = (int64_t)h->ntab.nq[0] * h->ntab.nq[1] * h->ntab.nq[2];
     for (auto& R : h->rd) {
       if (!newton) CK(cudaMemsetAsync(R.a_loc, 0, sizeof(double) * (size_t)pl.npatch * pl.nloc, h->stream));
@@ -624,7 +637,7 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
       CKL();
     }
   }
-  if (const char* ns = getenv("TCG_DEBUG_NOTSPD")) {  // test hook: first pivot of patch s := -1
+  if (const char* ns = newton ? nullptr : getenv("TCG_DEBUG_NOTSPD")) {  // test hook: first pivot of patch s := -1
     const int sbad = atoi(ns);
     for (auto& R : h->rd)
       if (sbad >= 0 && sbad < pl.npatch && pl.rank_of_patch[sbad] == R.r) {
@@ -636,7 +649,11 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
   TRY(sync_ranks(h));  // every rank's W^ assembled (rho weights read both interface sides)
   for (auto& R : h->rd) {
     if (pl.m > 0) {
-      k_rho_weights<<<(unsigned)((pl.m + 255) / 256), 256, 0, h->stream>>>(R.D, h->scaling);
+      // diagonal of W^ at both sides of every multiplier, captured from the freshly assembled
+      // tiles (Newton: the nonlinear patches' sides only; the rest keep the linear values)
+      k_rho_capture<<<(unsigned)((pl.m + 255) / 256), 256, 0, h->stream>>>(R.D, h->rho_diag, newton ? h->d_nlflag : nullptr);
+      ++h->nlaunch;
+      k_rho_weights<<<(unsigned)((pl.m + 255) / 256), 256, 0, h->stream>>>(R.D, h->scaling, h->rho_diag);
       ++h->nlaunch;
       CKL();
     }
@@ -652,15 +669,18 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
   if (h->dbgA && h->rd.size() == 1)
     CK(cudaMemcpyAsync(h->dbgA, h->rd[0].A, sizeof(double) * h->h_a_off.back(), cudaMemcpyDeviceToDevice, h->stream));
   for (auto& R : h->rd) {
-    if (R.ndesc == 0) continue;
-    TRY(run_cholesky(h, R.d_desc, R.ndesc, R.maxT, R.maxTr, R.maxTb, R.A, R.Dinv, R.Sbb, R.derr, 0));
+    const int nmat = newton ? (int)R.nlist.size() : R.ndesc;
+    if (nmat == 0) continue;
+    const int mT = newton ? R.nl_maxT : R.maxT, mTr = newton ? R.nl_maxTr : R.maxTr, mTb = newton ? R.nl_maxTb : R.maxTb;
+    const int* lst = newton ? R.d_nlist : R.d_plist;
+    TRY(run_cholesky(h, newton ? R.d_nldesc : R.d_desc, nmat, mT, mTr, mTb, R.A, R.Dinv, R.Sbb, R.derr, 0));
     // in-place inverse of the augmented factor: Xaug = [L_rr^-1 ; W_pr W_rr^-1]
     const int64_t* scr_off = h->D.dinv_off;  // scratch rows share the Dinv layout (Tr tiles)
-    for (int I = 0; I < R.maxT; ++I) {
-      dim3 g(std::min(I + 1, R.maxTr), (unsigned)R.plist.size());
-      k_xinv_row<<<g, 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(R.D, I, R.xscr, scr_off, R.d_plist);
+    for (int I = 0; I < mT; ++I) {
+      dim3 g(std::min(I + 1, mTr), (unsigned)nmat);
+      k_xinv_row<<<g, 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(R.D, I, R.xscr, scr_off, lst);
       ++h->nlaunch;
-      k_xrow_copy<<<g, 256, 0, h->stream>>>(R.D, I, R.xscr, scr_off, R.d_plist);
+      k_xrow_copy<<<g, 256, 0, h->stream>>>(R.D, I, R.xscr, scr_off, lst);
       ++h->nlaunch;
       CKL();
     }
@@ -703,8 +723,10 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
     }
   }
   if (mid) TRY(mid());  // host work overlapped with the kernels above (first setup only)
-  // insulator precompute: XJ = [X_rr j_S,r ; j_S,p - Phi^T j_S,r] for owned patches
+  // insulator precompute: XJ = [X_rr j_S,r ; j_S,p - Phi^T j_S,r] for owned patches (the
+  // nonlinear patches never use it: their rhs is recomputed every step)
   for (auto& R : h->rd) {
+    if (newton) break;
     const int b0 = h->h_boff[PH_FWA][R.r * h->nbr], n = h->h_boff[PH_FWA][(R.r + 1) * h->nbr] - b0;
     if (n > 0) {
       k_fw<<<n, NTHR, h->smem_pcg, h->stream>>>(R.D, h->d_items[PH_FWA] + b0, n, R.JS, R.XJ);
@@ -1409,7 +1431,11 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(set_smem(h, (const void*)k_nl_g, h->nl_smem));
     TRY(set_smem(h, (const void*)k_nl_assemble, h->nl_smem));
     TRY(dupload(h, &h->d_nlk, h->nlk));
+    std::vector<unsigned char> fl(pl.npatch);
+    for (int s = 0; s < pl.npatch; ++s) fl[s] = h->is_nl(s) ? 1 : 0;
+    TRY(dupload(h, &h->d_nlflag, fl));
   }
+  TRY(dzero(h, &h->rho_diag, 2 * (size_t)std::max<int64_t>(pl.m, 1)));
   {
     int maxn = 0, maxel = 0;
     for (int d = 0; d < 3; ++d) {
@@ -1461,6 +1487,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     size_t p5 = (size_t)(h->maxTb + h->maxTp) * TS + 8 * TS;
     size_t pcs = (size_t)h->coarse_ch * TS;
     size_t syv = (size_t)h->maxTb * TS + 9 * TS;
+    syv = std::max(syv, (size_t)2 * h->maxTb * TS + 16 * TS);  // whole-patch S_bb apply (symv_patch)
     size_t fwb = (size_t)h->maxT * TS + 8 * TS;
     size_t maxcomp = 0;
     for (int c = 0; c < 3; ++c) maxcomp = std::max(maxcomp, (size_t)pl.comp_dim(c, 0) * pl.comp_dim(c, 1) * pl.comp_dim(c, 2));
@@ -1528,8 +1555,11 @@ static tcg_status do_setup(tcg_ctx* h) {
       };
       ItemLists p1(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR);
       // whole-patch dealing when there are many patches per block (cfg5: 2048 patches)
-      const bool grp = (int64_t)P >= 2 * (int64_t)NR * h->nbr && !(getenv("TCG_NO_GROUP") && atoi(getenv("TCG_NO_GROUP")));
+      // (TCG_GROUP=1 forces it: the parity tests exercise the whole-patch items on small configs)
+      const bool grp = ((int64_t)P >= 2 * (int64_t)NR * h->nbr || (getenv("TCG_GROUP") && atoi(getenv("TCG_GROUP")))) &&
+                       !(getenv("TCG_NO_GROUP") && atoi(getenv("TCG_NO_GROUP")));
       const bool grp5 = grp && !(getenv("TCG_P5_SPLIT") && atoi(getenv("TCG_P5_SPLIT")));
+      const bool grp_syp = grp && !(getenv("TCG_SY_SPLIT") && atoi(getenv("TCG_SY_SPLIT")));
       for (int s = 0; s < P; ++s) {
         const int r = owner[s];
         const int Trs = Ti[s] + Tb[s];
@@ -1561,7 +1591,13 @@ static tcg_status do_setup(tcg_ctx* h) {
             p5.per_rank[r].push_back({Tp[s], d});
           }
         }
-        for (int I = 0; I < Tb[s]; ++I) sy.per_rank[r].push_back({Tb[s], desc(s, I)});
+        if (grp_syp) {  // whole-patch S_bb apply: every stored tile read once (pcg.cu symv_patch)
+          ItemDesc d = desc(s, 0);
+          d.part = 2;
+          if (Tb[s] > 0) sy.per_rank[r].push_back({Tb[s] * (Tb[s] + 1) / 2, d});
+        } else {
+          for (int I = 0; I < Tb[s]; ++I) sy.per_rank[r].push_back({Tb[s], desc(s, I)});
+        }
       }
       const int ch = h->coarse_ch;
       // PC gather programs (one per column chunk; shared by the chunk's row-block items)
@@ -1765,7 +1801,15 @@ static tcg_status do_setup(tcg_ctx* h) {
       if (h->is_nl(s)) R.nlist.push_back(s);
     if (!R.nlist.empty()) {
       std::vector<int64_t> nts(1, 0);
-      for (int s : R.nlist) nts.push_back(nts.back() + tri_tiles(T[s]));
+      std::vector<CholDesc> nd;
+      for (int s : R.nlist) {
+        nts.push_back(nts.back() + tri_tiles(T[s]));
+        nd.push_back(CholDesc{a_off[s], dinv_off[s], sbb_off[s], T[s], Ti[s] + Tb[s], Ti[s], Tb[s]});
+        R.nl_maxT = std::max(R.nl_maxT, T[s]);
+        R.nl_maxTr = std::max(R.nl_maxTr, Ti[s] + Tb[s]);
+        R.nl_maxTb = std::max(R.nl_maxTb, Tb[s]);
+      }
+      TRY(dupload(h, &R.d_nldesc, nd));
       R.nl_ntiles = nts.back();
       TRY(dupload(h, &R.d_nlist, R.nlist));
       TRY(dupload(h, &R.d_ntstart, nts));

@@ -444,11 +444,81 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
   return contrib;  // this thread's share of v_J . y_J; the caller block-sums once per phase
 }
 
+// ---- P7 / R5, whole-patch dealing (ItemDesc part 2): the S_bb apply of one patch with every
+// stored tile read once. Tile (I,J), I > J, gives its row contribution S_IJ u_J to y_I and its
+// column contribution S_IJ^T u_I to y_J from the same registers; column blocks J run outer and
+// row blocks I >= J inner, so y_J is complete when column block J ends (its row contributions
+// come from tiles (J, J' <= J)). Warp w owns rows 8w..8w+7 of each tile (row sums by
+// warp_reduce8 into y, exclusive per warp), lane l columns 2l, 2l+1 (column sums in registers
+// over the column block, then over the 8 warps in warp order): deterministic. One
+// __syncthreads per column block (double-buffered warp partials).
+template <class Src>
+__device__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm,
+                             const double* pft, int npf) {
+  const int Ti = it.Ti, Tb = it.Tb, nb = it.nb;
+  double* u = sm;             // Tb*64 input
+  double* y = u + Tb * TS;    // Tb*64 row contributions
+  double* cw = y + Tb * TS;   // 2 x 8 warps x 64 column partials
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
+  const int off = row0 * TS + 2 * lane;
+  const double* S = Sr + it.sbb_off;
+  if (!(c_step_flags & 1)) prefetch_tiles([&](int I) { return S + tri_off(I, 0); }, npf > 0 ? 1 : 0, Tb);
+  for (int i = threadIdx.x; i < Tb * TS; i += blockDim.x) {
+    u[i] = (i < nb) ? usrc(it, it.b_off + i, i) : 0.0;
+    y[i] = 0.0;
+  }
+  __syncthreads();
+  double contrib = 0.0;
+  for (int J = 0; J < Tb; ++J) {
+    const double2 uJ = *reinterpret_cast<const double2*>(u + J * TS + 2 * lane);
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll 2
+    for (int I = J; I < Tb; ++I) {
+      double2 a[8];
+      if (I == 0 && npf > 0) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) a[r] = lds2(pft + off + r * TS);
+      } else {
+        const double* t = S + tri_off(I, J) + off;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
+      }
+      double part[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) part[r] = a[r].x * uJ.x + a[r].y * uJ.y;
+      if (I > J) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const double xr = u[I * TS + row0 + r];
+          c0 += a[r].x * xr;
+          c1 += a[r].y * xr;
+        }
+      }
+      const double rs = warp_reduce8(part);
+      if ((lane & 3) == 0) y[I * TS + row0 + warp_reduce8_row()] += rs;
+    }
+    double* cb = cw + (J & 1) * 8 * TS;
+    cb[warp * TS + 2 * lane] = c0;
+    cb[warp * TS + 2 * lane + 1] = c1;
+    __syncthreads();
+    if (threadIdx.x < TS) {
+      double v = y[J * TS + threadIdx.x];
+#pragma unroll
+      for (int w = 0; w < NTHR / 32; ++w) v += cb[w * TS + threadIdx.x];
+      PW[it.vec_off + (int64_t)(Ti + J) * TS + threadIdx.x] = v;
+      contrib += u[J * TS + threadIdx.x] * v;
+    }
+  }
+  __syncthreads();  // the next item overwrites u / y
+  return contrib;
+}
+
 // ---- P7 / R5: symmetric S_bb apply, one row block I of one patch --------------------------
 // usrc(it, b, pos) returns (B_D^(s)T r)_pos. Returns this item's share of u^T S_bb u.
 template <class Src>
 __device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm,
                                             double* red, const double* pft = nullptr, int npf = 0, bool gat = true) {
+  if ((it.part & 15) == 2) return symv_patch(it, Sr, PW, usrc, sm, pft, npf);
   const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   double* u = sm;            // Tb*64
   double* cr = u + Tb * TS;  // 9 * 64

@@ -134,3 +134,26 @@ def test_virtual_ranks_sparse_coarse_match_golden(tcg, monkeypatch, name, vranks
     err = float(np.linalg.norm(a - ref) / np.linalg.norm(ref))
     assert err <= TOL, err
     assert np.all(np.abs(np.asarray(it, dtype=np.int64) - g["iters"].astype(np.int64)) <= 1), (list(it), list(g["iters"]))
+
+
+@pytest.mark.parametrize("vranks", [1, 2])
+def test_whole_patch_items_cfg2_match_golden(tcg, monkeypatch, vranks):
+    """Whole-patch dealing (the item kinds cfg5 runs: one P5 item per column, one S_bb item per
+    patch reading every stored tile once, pcg.cu symv_patch), forced on cfg2 (TCG_GROUP=1),
+    all 50 steps against the oracle's golden file."""
+    monkeypatch.setenv("TCG_GROUP", "1")
+    g, meta = _golden("cfg2")
+    pr = workloads.get("cfg2")
+    s = tcg.Solver()
+    if vranks > 1:
+        s.set_virtual_ranks(vranks)
+    s.configure(pr)
+    s.setup()
+    s.step(int(meta["steps"]))
+    a = s.coefficients(1)
+    it = s.history()[0]
+    s.close()
+    ref = g["a1"]
+    err = float(np.linalg.norm(a - ref) / np.linalg.norm(ref))
+    assert err <= TOL, err
+    assert np.all(np.abs(np.asarray(it, dtype=np.int64) - g["iters"].astype(np.int64)) <= 1), (list(it), list(g["iters"]))
