@@ -92,6 +92,7 @@ struct RankDev {
   int64_t* d_tstart = nullptr;
   int64_t ntiles = 0;
   double *A = nullptr, *Dinv = nullptr, *Sbb = nullptr, *xscr = nullptr;
+  double* SI = nullptr;  // explicit S_bb^-1 (S_bb layout) when the iteration applies it (sbbinv)
   double *Wr = nullptr, *FWr = nullptr, *dsave = nullptr, *wpart = nullptr;  // warm start (lazy)
   CholDesc* d_desc = nullptr;
   int ndesc = 0, maxT = 0, maxTr = 0, maxTb = 0;
@@ -230,6 +231,9 @@ struct tcg_ctx {
   int cache_bpos = 0;
   int cache_items = 0, cache_lam = 0, cache_pcprog = 0;
   int npf = 0;  // prefetched tiles per phase (stepper)
+  // the PCG iteration applies W_rr^-1 restricted to b as the explicit S_bb^-1 = X_bb^T X_bb
+  // (one symmetric read) instead of X_bb^T (X_bb v) (two reads); TCG_SBBINV=0 restores the latter
+  bool sbbinv = true;
   int warm = 0;  // warm-start subspace dimension k (tcg_set_warm_start), 0 = off
   int64_t warm_base = 0;  // first step of the current warm-start history (k changed / refactor)
   int64_t* d_pcprog = nullptr;
@@ -681,6 +685,12 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
       k_xinv_row<<<g, 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(R.D, I, R.xscr, scr_off, lst);
       ++h->nlaunch;
       k_xrow_copy<<<g, 256, 0, h->stream>>>(R.D, I, R.xscr, scr_off, lst);
+      ++h->nlaunch;
+      CKL();
+    }
+    if (h->sbbinv && mTb > 0) {  // S_bb^-1 = X_bb^T X_bb for the PCG iteration
+      k_sbbinv<<<dim3((unsigned)tri_tiles(mTb), (unsigned)nmat), 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(
+          R.D, lst, R.SI);
       ++h->nlaunch;
       CKL();
     }
@@ -1233,6 +1243,8 @@ static tcg_status do_setup(tcg_ctx* h) {
   {
     const char* ev = getenv("TCG_STABLE");
     if (ev) h->stable_mask = atoi(ev);
+    const char* si = getenv("TCG_SBBINV");
+    h->sbbinv = !(si && atoi(si) == 0);
   }
   const int P = pl.npatch;
   const int NR = h->nranks;
@@ -1498,6 +1510,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(set_smem(h, (const void*)k_fw, h->smem_pcg));
     TRY(set_smem(h, (const void*)k_xinv_row, 4 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_sinv, 4 * TS * SPAD * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_sbbinv, 4 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_trinv_row, 4 * TS * SPAD * sizeof(double)));
     TRY(set_smem(h, (const void*)k_tables1d, h->smem_tables));
     TRY(set_smem(h, (const void*)k_potrf, 2 * TS * PS * sizeof(double)));
@@ -1553,7 +1566,8 @@ static tcg_status do_setup(tcg_ctx* h) {
         d.a_off = a_off[s]; d.vec_off = vec_off[s]; d.b_off = b_off[s]; d.p_off = p_off[s]; d.sbb_off = sbb_off[s];
         return d;
       };
-      ItemLists p1(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR);
+      ItemLists p1(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR), e1(NR), e5(NR);
+      const bool si = h->sbbinv;
       // whole-patch dealing when there are many patches per block (cfg5: 2048 patches)
       // (TCG_GROUP=1 forces it: the parity tests exercise the whole-patch items on small configs)
       const bool grp = ((int64_t)P >= 2 * (int64_t)NR * h->nbr || (getenv("TCG_GROUP") && atoi(getenv("TCG_GROUP")))) &&
@@ -1576,19 +1590,40 @@ static tcg_status do_setup(tcg_ctx* h) {
           for (int c = 0; c < 3; ++c) rhs.per_rank[r].push_back({pl.nloc / 3, desc(s, c)});
         else
           rhs.per_rank[r].push_back({T[s] * TS / 8, desc(s, -1)});
-        for (int I = 0; I < Tb[s] + Tp[s]; ++I) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
+        // E1 / E5 (per-step uses of the F-apply halves, X_bb form); with sbbinv, E5 keeps the
+        // split items (X_bb^T -> Y, Phi_b -> Y2) because the iteration writes Y2 every time
+        for (int I = 0; I < Tb[s] + Tp[s]; ++I) {
+          e1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
+          if (!si || I >= Tb[s]) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
+        }
         for (int J = 0; J < Tb[s]; ++J) {
-          if (grp5 && np[s] > 0) {  // whole-patch dealing: one item per column (fewer item starts)
+          if (grp5 && np[s] > 0 && !si) {  // whole-patch dealing: one item per column (fewer item starts)
             ItemDesc d = desc(s, J);
             d.part = 2;
+            e5.per_rank[r].push_back({Tb[s] - J + Tp[s], d});
             p5.per_rank[r].push_back({Tb[s] - J + Tp[s], d});
             continue;
           }
-          p5.per_rank[r].push_back({Tb[s] - J, desc(s, J)});
+          e5.per_rank[r].push_back({Tb[s] - J, desc(s, J)});
+          if (!si) p5.per_rank[r].push_back({Tb[s] - J, desc(s, J)});
           if (np[s] > 0) {
             ItemDesc d = desc(s, J);
             d.part = 1;
+            e5.per_rank[r].push_back({Tp[s], d});
             p5.per_rank[r].push_back({Tp[s], d});
+          }
+        }
+        if (si && Tb[s] > 0) {  // the iteration's local half: y1 = S_bb^-1 v (ItemDesc part bit 3)
+          if (grp_syp) {
+            ItemDesc d = desc(s, 0);
+            d.part = 8 | 2;
+            p1.per_rank[r].push_back({Tb[s] * (Tb[s] + 1) / 2, d});
+          } else {
+            for (int I = 0; I < Tb[s]; ++I) {
+              ItemDesc d = desc(s, I);
+              d.part = 8;
+              p1.per_rank[r].push_back({Tb[s], d});
+            }
           }
         }
         if (grp_syp) {  // whole-patch S_bb apply: every stored tile read once (pcg.cu symv_patch)
@@ -1632,6 +1667,8 @@ static tcg_status do_setup(tcg_ctx* h) {
         }
       // fixed per-item overhead (tile units) of the latency-bound item phases
       TRY(deal_items(h, p1, PH_P1, 2, grp));
+      TRY(deal_items(h, e1, PH_E1, 2, grp));
+      TRY(deal_items(h, e5, PH_E5, 2, grp));
       TRY(deal_items(h, pcv, PH_PC, 2));
       TRY(deal_items(h, p5, PH_P5, 2, grp));
       // S_bb rows are dealt one by one: whole-patch groups (one u gather per patch,
@@ -1774,6 +1811,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     TRY(dalloc(h, &R.Dinv, od[R.r]));
     TRY(dalloc(h, &R.xscr, od[R.r]));
     TRY(dalloc(h, &R.Sbb, os[R.r]));
+    if (h->sbbinv) TRY(dalloc(h, &R.SI, os[R.r]));
     TRY(dzero(h, &R.F, ov));
     TRY(dzero(h, &R.Z, ov));
     TRY(dzero(h, &R.XJ, ov));
@@ -1847,6 +1885,7 @@ static tcg_status do_setup(tcg_ctx* h) {
       D.Sbbr[r] = (double*)bufs[r][1];
     }
     h->D.me = 0;
+    for (auto& R : h->rd) D.SIr[R.r] = R.SI;  // own patches only (items run on the owner)
     for (auto& R : h->rd) {
       R.D = D;
       R.D.me = R.r;
@@ -2642,7 +2681,7 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
   out->n_gauge = p.n_gauge;
   out->n_dirichlet = p.n_dir;
   out->nr_min = out->nb_min = out->np_min = INT64_MAX;
-  double bf = 0, bm = 0, bs = 0, fl = 0;
+  double bf = 0, bm = 0, bs = 0, fl = 0, bsi = 0;
   for (int s = 0; s < p.npatch; ++s) {
     const PatchPlan& q = p.pp[s];
     int64_t nr = q.ni + q.nb;
@@ -2657,6 +2696,9 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
     // per preconditioner apply packed S_bb read once
     bf += 8.0 * q.nb * (q.nb + 1) + 16.0 * q.nb * q.np;
     bm += 4.0 * q.nb * (q.nb + 1);
+    // sbbinv: the iteration's F-apply reads the packed S_bb^-1 once instead of X_bb twice
+    bsi += 4.0 * q.nb * (q.nb + 1) + 16.0 * q.nb * q.np;
+    if (h->sbbinv) fl += (double)q.nb * q.nb * q.nb / 3.0;
     const double nrp = (double)nr;
     // per step outside PCG: conductors read [X_rr; Phi^T] twice (R2 forward, E3 backward)
     if (h->dyn(s)) bs += 2.0 * 8.0 * (nrp * (nrp + 1) / 2 + nrp * q.np);
@@ -2673,8 +2715,14 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
       bf += 2.0 * 8.0 * (v * (v + 1) / 2 + v * b);
     }
     bf += 40.0 * p.m;
+    for (const auto& n : h->nd.nd) {
+      const double v = (double)n.V.size(), b = (double)n.B.size();
+      bsi += 2.0 * 8.0 * (v * (v + 1) / 2 + v * b);
+    }
+    bsi += 40.0 * p.m;
   } else {
     bf += 8.0 * nc * (nc + 1) + 40.0 * p.m;  // dense S_pp^-1 read once = two triangular passes
+    bsi += 8.0 * nc * (nc + 1) + 40.0 * p.m;
   }
   bm += 40.0 * p.m;
   bs += bf + bm;  // R3/R4/E1/E2 (one F-apply worth) and the z0 preconditioner apply (R5)
@@ -2700,7 +2748,7 @@ tcg_status tcg_get_info(tcg_handle h, tcg_info* out) {
       cb = 8.0 * nc * nc;
     out->coarse_factor_bytes = cb;
   }
-  out->bytes_fapply = bf;
+  out->bytes_fapply = h->sbbinv ? bsi : bf;  // (bytes_step_fixed keeps the X_bb form of R4 / E1)
   out->bytes_precond = bm;
   out->bytes_step_fixed = bs;
   out->flops_factor = fl;

@@ -522,6 +522,39 @@ __global__ void __launch_bounds__(128) k_sinv(const double* __restrict__ X, doub
   acc_store(Sinv + ((int64_t)I * Tc + J) * TSZ, acc, 1.0);
 }
 
+// Explicit S_bb^-1 = X_bb^T X_bb (X_bb = L_bb^-1, the trailing (b,b) block of L_rr^-1 in the
+// inverse-factor store) per patch, tile-packed lower in the S_bb layout: tile (I,J), I >= J,
+// = sum_{K >= I} X_KI^T X_KJ. Diagonal tiles are written full and exactly symmetric (lower
+// triangle mirrored). grid (tri_tiles(maxTb), #patches), 128 threads.
+__global__ void __launch_bounds__(128) k_sbbinv(DevPlan D, const int* plist, double* SI) {
+  const int s = plist[blockIdx.y];
+  const int Tb = D.Tb[s], Ti = D.Ti[s];
+  const int64_t y = blockIdx.x;
+  if (y >= (int64_t)Tb * (Tb + 1) / 2) return;
+  int I = (int)((sqrt(8.0 * (double)y + 1.0) - 1.0) * 0.5);
+  while ((int64_t)I * (I + 1) / 2 > y) --I;
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= y) ++I;
+  const int J = (int)(y - (int64_t)I * (I + 1) / 2);
+  extern __shared__ __align__(16) double smem[];
+  const double* X = D.A + D.a_off[s];
+  double acc[4][4][2];
+  acc_zero(acc);
+  mma_stream<true, false>([&](int q) { return X + tri_off(Ti + I + q, Ti + I); },
+                          [&](int q) { return X + tri_off(Ti + I + q, Ti + J); }, Tb - I, smem, acc);
+  double* out = SI + D.sbb_off[s] + tri_off(I, J);
+  if (I != J) {
+    acc_store(out, acc, 1.0);
+    return;
+  }
+  double* st = smem;  // (the pipeline's buffers are free again)
+  acc_to_smem(st, acc);
+  __syncthreads();
+  for (int e = threadIdx.x; e < TSZ; e += blockDim.x) {
+    const int r = e / TS, c = e % TS;
+    out[e] = (c <= r) ? st[r * SPAD + c] : st[c * SPAD + r];
+  }
+}
+
 }  // namespace tcg
 
 namespace tcg {

@@ -40,6 +40,7 @@ struct DevPlan {
   const int* owner;         // per patch: owning rank
   double* Ar[MAXR];         // per rank: augmented factors / inverse factors
   double* Sbbr[MAXR];       // per rank: S_bb stores
+  double* SIr[MAXR];        // per rank: explicit S_bb^-1 = X_bb^T X_bb stores (S_bb layout; null if unused)
   int64_t m, nc;
   // per patch
   const int* Ti;

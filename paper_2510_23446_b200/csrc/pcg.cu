@@ -518,7 +518,7 @@ __device__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, S
 template <class Src>
 __device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm,
                                             double* red, const double* pft = nullptr, int npf = 0, bool gat = true) {
-  if ((it.part & 15) == 2) return symv_patch(it, Sr, PW, usrc, sm, pft, npf);
+  if ((it.part & 7) == 2) return symv_patch(it, Sr, PW, usrc, sm, pft, npf);
   const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   double* u = sm;            // Tb*64
   double* cr = u + Tb * TS;  // 9 * 64
@@ -998,6 +998,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   }
   const double* Xr = D.Ar[me];
   const double* Sr = D.Sbbr[me];
+  const double* SIr = D.SIr[me];
   // ---- per-launch setup: item lists (and lambda-chunk index data) into shared memory ----
   {
     ItemDesc* ic = reinterpret_cast<ItemDesc*>(smw + A.scratch);
@@ -1093,7 +1094,10 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     const double* src[2] = {nullptr, nullptr};
     if (A.npf > 0 && ph >= 0 && ph < NCACHE && !((c_step_flags >> (4 + ph)) & 1) && s_icnt[ph] > 0) {
       const ItemDesc& w = s_ip[ph][0];
-      if (ph == PH_P1) {
+      if (ph == PH_P1 && (w.part & 8)) {  // explicit S_bb^-1 apply (row block I, or patch from I = 0)
+        n = min(w.I + 1, A.npf);
+        for (int q = 0; q < n; ++q) src[q] = SIr + w.sbb_off + tri_off(w.I, q);
+      } else if (ph == PH_P1) {
         const int Jn = (w.I < w.Tb) ? w.I + 1 : w.Tb;
         n = min(Jn, A.npf);
         for (int q = 0; q < n; ++q) src[q] = Xr + w.a_off + tri_off(w.Ti + w.I, w.Ti + q);
@@ -1221,13 +1225,16 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     const int step = -1, it = -1;  // no stamps
     (void)step;
     (void)it;
-    FOR_ITEMS(PH_P1, w)
-      p1_item(w, Xr,
-              [&](const ItemDesc& iw, int64_t bb, int pos) {
-                const BPos q = bget(iw, bb, pos);
-                return q.sign * ldcg(A.pk[0][lown(q.k)] + q.k);
-              },
-              A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
+    {
+      auto vsrc = [&](const ItemDesc& iw, int64_t bb, int pos) {
+        const BPos q = bget(iw, bb, pos);
+        return q.sign * ldcg(A.pk[0][lown(q.k)] + q.k);
+      };
+      FOR_ITEMS(PH_P1, w) {
+        if (w.part & 8) symv_item(w, SIr, A.Y[me], vsrc, smw, red, PF0(j_w), GAT(PH_P1, w));
+        else p1_item(w, Xr, vsrc, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
+      }
+    }
     bar(PH_PC, false, 0.0);
     COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
     bar(PH_P5, false, 0.0);
@@ -1256,10 +1263,10 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     bar(PH_P5, false, 0.0);
     if (A.dbg_stop == 1) break;
     SSTAMP(3);
-    // ---- R4 y = X_bb^T Z_b - Phi_b N p0 ----
-    FOR_ITEMS(PH_P5, w)
+    // ---- R4 y = X_bb^T Z_b - Phi_b N p0 (the X_bb form of the F-apply's second half) ----
+    FOR_ITEMS(PH_E5, w)
       p5_item(w, Xr, A.Z[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
-              red, nullptr, PF0(j_w), GAT(PH_P5, w));
+              red, nullptr, nullptr, 0, GAT(PH_E5, w));
     bar(PH_SY, false, 0.0);
     SSTAMP(4);
     // ---- R5 d = B y; r0 = d, lambda = 0; z0 = M^-1 d, rho0 ----
@@ -1432,6 +1439,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       double* const* pprev = A.pk[pp];
       double* pcur = A.pk[pp ^ 1][me];
       // P1: p = z + beta p_prev on the fly; v = B^T p; w = X_bb v, -g = -Phi^T v; owners store p
+      // (sbbinv: y1 = S_bb^-1 v -> Y instead of w, and its share v . y1 of p^T F p -> loc1)
+      double loc1 = 0.0;
       {
         // the block's own lambda chunk first (independent loads in flight before the items)
         double pv = 0.0;
@@ -1446,7 +1455,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         };
         FOR_ITEMS(PH_P1, w) {
           ITIME_BEGIN
-          p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
+          if (w.part & 8) loc1 += symv_item(w, SIr, A.Y[me], vnew, smw, red, PF0(j_w), GAT(PH_P1, w));
+          else p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
           ITIME_END(PH_P1, j_w)
         }
         if (kq < k1) pcur[kq] = pv;
@@ -1466,7 +1476,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       double* const* pcurt = A.pk[pp ^ 1];
       double pq;
       {
-        double loc = 0.0;
+        double loc = loc1;
         FOR_ITEMS(PH_P5, w) {
           ITIME_BEGIN
           loc += p5_item(w, Xr, A.XW[me], D.p_grp, pcf,
@@ -1557,14 +1567,14 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       }
     }
     SSTAMP(6);
-    // ---- E1 v = B^T lambda ; w, -Phi^T v ----
-    FOR_ITEMS(PH_P1, w)
+    // ---- E1 v = B^T lambda ; w, -Phi^T v (the X_bb form of the F-apply's first half) ----
+    FOR_ITEMS(PH_E1, w)
       p1_item(w, Xr,
               [&](const ItemDesc& iw, int64_t bb, int pos) {
                 const BPos q = bget(iw, bb, pos);
                 return q.sign * ldcg(A.lam[lown(q.k)] + q.k);
               },
-              A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
+              A.XW[me], smw, nullptr, 0, GAT(PH_E1, w));
     bar(PH_PC, false, 0.0);
     SSTAMP(7);
     // ---- E2 p = S_pp^-1 sum N^T (Z_p - XW_p) ----
