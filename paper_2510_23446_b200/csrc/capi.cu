@@ -633,8 +633,8 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
       if (nn == 0) continue;
       k_nl_quad<<<dim3(nn, (unsigned)std::min<int64_t>(64, (nqp + 255) / 256)), 256, 0, h->stream>>>(
           h->G, h->ntab, R.d_nlist, R.a_loc, h->d_nlk, R.Q);
-      k_nl_assemble<<<(unsigned)R.nl_ntiles, 256, h->nl_smem, h->stream>>>(R.D, h->tb, h->G, h->ntab, 1.0 / dt, R.d_nlist,
-                                                                           R.d_ntstart, (int)nn, R.Q);
+      launch_nl_assemble(pl.p, (unsigned)R.nl_ntiles, h->nl_smem, h->stream, R.D, h->tb, h->G, h->ntab, 1.0 / dt,
+                         R.d_nlist, R.d_ntstart, (int)nn, R.Q);
       k_nl_g<<<dim3(nn, (unsigned)((pl.nloc + 255) / 256)), 256, h->nl_smem, h->stream>>>(R.D, h->G, h->ntab, R.d_nlist,
                                                                                         R.Q, R.gnl);
       h->nlaunch += 3;
@@ -1441,7 +1441,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     h->nl_smem = sizeof(double) * (size_t)o;
     if (h->nl_smem > 200 * 1024) return fail(h, TCG_EINVAL, "nonlinear patches: Gauss-point tables exceed shared memory");
     TRY(set_smem(h, (const void*)k_nl_g, h->nl_smem));
-    TRY(set_smem(h, (const void*)k_nl_assemble, h->nl_smem));
+    CK(nl_assemble_smem(h->nl_smem));
     TRY(dupload(h, &h->d_nlk, h->nlk));
     std::vector<unsigned char> fl(pl.npatch);
     for (int s = 0; s < pl.npatch; ++s) fl[s] = h->is_nl(s) ? 1 : 0;
@@ -1498,6 +1498,7 @@ static tcg_status do_setup(tcg_ctx* h) {
     size_t p1 = (size_t)h->maxTb * TS;
     size_t p5 = (size_t)(h->maxTb + h->maxTp) * TS + 8 * TS;
     size_t pcs = (size_t)h->coarse_ch * TS;
+    p5 = std::max(p5, (size_t)h->maxTp * TS + 16 * TS);  // whole-patch Phi_b item (p5_phi_patch)
     size_t syv = (size_t)h->maxTb * TS + 9 * TS;
     syv = std::max(syv, (size_t)2 * h->maxTb * TS + 16 * TS);  // whole-patch S_bb apply (symv_patch)
     size_t fwb = (size_t)h->maxT * TS + 8 * TS;
@@ -1574,6 +1575,9 @@ static tcg_status do_setup(tcg_ctx* h) {
                        !(getenv("TCG_NO_GROUP") && atoi(getenv("TCG_NO_GROUP")));
       const bool grp5 = grp && !(getenv("TCG_P5_SPLIT") && atoi(getenv("TCG_P5_SPLIT")));
       const bool grp_syp = grp && !(getenv("TCG_SY_SPLIT") && atoi(getenv("TCG_SY_SPLIT")));
+      // with sbbinv: the Phi_b^T rows join the whole-patch S_bb^-1 item, one whole-patch Phi_b item
+      // per patch in P5 (TCG_SI_MERGE=0: separate row / column items)
+      const bool simerge = grp_syp && !(getenv("TCG_SI_MERGE") && atoi(getenv("TCG_SI_MERGE")) == 0);
       for (int s = 0; s < P; ++s) {
         const int r = owner[s];
         const int Trs = Ti[s] + Tb[s];
@@ -1594,7 +1598,7 @@ static tcg_status do_setup(tcg_ctx* h) {
         // split items (X_bb^T -> Y, Phi_b -> Y2) because the iteration writes Y2 every time
         for (int I = 0; I < Tb[s] + Tp[s]; ++I) {
           e1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
-          if (!si || I >= Tb[s]) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
+          if (!si || (I >= Tb[s] && !(simerge && Tb[s] > 0))) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
         }
         for (int J = 0; J < Tb[s]; ++J) {
           if (grp5 && np[s] > 0 && !si) {  // whole-patch dealing: one item per column (fewer item starts)
@@ -1610,14 +1614,19 @@ static tcg_status do_setup(tcg_ctx* h) {
             ItemDesc d = desc(s, J);
             d.part = 1;
             e5.per_rank[r].push_back({Tp[s], d});
-            p5.per_rank[r].push_back({Tp[s], d});
+            if (!(si && simerge)) p5.per_rank[r].push_back({Tp[s], d});
           }
         }
+        if (si && simerge && np[s] > 0 && Tb[s] > 0) {  // whole-patch Phi_b item (pcg.cu p5_phi_patch)
+          ItemDesc d = desc(s, 0);
+          d.part = 3;
+          p5.per_rank[r].push_back({Tp[s] * Tb[s], d});
+        }
         if (si && Tb[s] > 0) {  // the iteration's local half: y1 = S_bb^-1 v (ItemDesc part bit 3)
-          if (grp_syp) {
+          if (grp_syp) {  // + the Phi_b^T rows on the same gathered input (part bit 2)
             ItemDesc d = desc(s, 0);
-            d.part = 8 | 2;
-            p1.per_rank[r].push_back({Tb[s] * (Tb[s] + 1) / 2, d});
+            d.part = simerge ? (8 | 4 | 2) : (8 | 2);
+            p1.per_rank[r].push_back({Tb[s] * (Tb[s] + 1) / 2 + (simerge ? Tp[s] * Tb[s] : 0), d});
           } else {
             for (int I = 0; I < Tb[s]; ++I) {
               ItemDesc d = desc(s, I);

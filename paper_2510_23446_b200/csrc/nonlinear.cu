@@ -202,11 +202,15 @@ __global__ void __launch_bounds__(256) k_nl_g(DevPlan D, Geom G, NlTab T, const 
 
 // One CTA per 64x64 tile of the nonlinear patches' tile-packed J = Kt + (sigma/dt) M (the
 // rank's nonlinear list nlist, tile prefix tstart over it); same layout and padding as
-// k_assemble. Kt entry: sum over the common support's Gauss points of
-// curl w_a^T Nw curl w_b (4 products of the two functions' nonzero curl components).
+// k_assemble. Kt entry (a, b): sum over the Gauss points of the elements both functions are
+// active on of curl w_a^T Nw curl w_b (each curl has two nonzero components, each a product
+// of three 1D factors). Loops run element by element (the active-function offset i - e is
+// fixed per element, no division or support test per point), Q = p + 1 points unrolled.
+template <int P>
 __global__ void __launch_bounds__(256) k_nl_assemble(DevPlan D, Tables1D tb, Geom G, NlTab T, double inv_dt,
                                                      const int* nlist, const int64_t* tstart, int nnl,
                                                      const double* __restrict__ Q) {
+  constexpr int NQ = P + 1;
   extern __shared__ double tabs[];
   const int64_t tile = blockIdx.x;
   const int li = find_patch(tstart, nnl, tile);
@@ -228,9 +232,9 @@ __global__ void __launch_bounds__(256) k_nl_assemble(DevPlan D, Tables1D tb, Geo
   const int64_t tsz = T.off[2] + (int64_t)T.nq[2] * T.stride;
   for (int64_t i = threadIdx.x; i < tsz; i += blockDim.x) tabs[i] = T.base[i];
   __syncthreads();
-  const int p = G.p;
   const int nqx = T.nq[0], nqy = T.nq[1];
   const int64_t nqp = (int64_t)nqx * nqy * T.nq[2];
+  const int st = T.stride;
   const double* Qs = Q + (int64_t)li * 9 * nqp;
   const double sg = D.sigma[s] * inv_dt;
   const int* aug = D.aug + D.aug_off[s];
@@ -245,48 +249,95 @@ __global__ void __launch_bounds__(256) k_nl_assemble(DevPlan D, Tables1D tb, Geo
       const LocalDof A = decode_local(G, ga), B = decode_local(G, gb);
       double Kl, M;
       kron_entry(t1, A, B, Kl, M);
-      int lo[3], hi[3];
+      int e0[3], e1[3];
       bool empty = false;
       for (int d = 0; d < 3; ++d) {
-        int la, ha, lb, hb;
-        nl_support(A.i[d], d == A.c, p, G.el[d], la, ha);
-        nl_support(B.i[d], d == B.c, p, G.el[d], lb, hb);
-        lo[d] = max(la, lb);
-        hi[d] = min(ha, hb);
-        empty |= lo[d] >= hi[d];
+        const int a0 = max(0, A.i[d] - (d == A.c ? P - 1 : P)), b0 = max(0, B.i[d] - (d == B.c ? P - 1 : P));
+        e0[d] = max(a0, b0);
+        e1[d] = min(min(A.i[d], B.i[d]), G.el[d] - 1);
+        empty |= e0[d] > e1[d];
       }
       double K = 0.0;
       if (!empty) {
         const CurlTerms CA = curl_terms(A.c), CB = curl_terms(B.c);
-        int nidx[2][2];
+        const double* Nq[2][2];
         for (int t = 0; t < 2; ++t)
-          for (int u = 0; u < 2; ++u) nidx[t][u] = sym6(CA.r[t], CB.r[u]);
-        for (int qz = lo[2]; qz < hi[2]; ++qz)
-          for (int qy = lo[1]; qy < hi[1]; ++qy) {
-            double ya[2], yb[2];
+          for (int u = 0; u < 2; ++u) Nq[t][u] = Qs + sym6(CA.r[t], CB.r[u]) * nqp;
+        // table column of each term's factor along d: 1 + kind * NQ (+ active offset per element)
+        int ka[2][3], kb[2][3];
+        for (int t = 0; t < 2; ++t)
+          for (int d = 0; d < 3; ++d) {
+            ka[t][d] = 1 + CA.kd[t][d] * NQ;
+            kb[t][d] = 1 + CB.kd[t][d] * NQ;
+          }
+        for (int ez = e0[2]; ez <= e1[2]; ++ez) {
+          const int oaz = A.i[2] - ez, obz = B.i[2] - ez;
+#pragma unroll
+          for (int gz = 0; gz < NQ; ++gz) {
+            const int qz = ez * NQ + gz;
+            const double* rz = tabs + T.off[2] + (int64_t)qz * st;
+            double za[2], zb[2];
             for (int t = 0; t < 2; ++t) {
-              ya[t] = CA.sg[t] * nl_f1(tabs, T, 1, CA.kd[t][1], A.i[1], qy, p) *
-                      nl_f1(tabs, T, 2, CA.kd[t][2], A.i[2], qz, p);
-              yb[t] = CB.sg[t] * nl_f1(tabs, T, 1, CB.kd[t][1], B.i[1], qy, p) *
-                      nl_f1(tabs, T, 2, CB.kd[t][2], B.i[2], qz, p);
+              za[t] = CA.sg[t] * rz[ka[t][2] + oaz];
+              zb[t] = CB.sg[t] * rz[kb[t][2] + obz];
             }
-            const int64_t wrow = (int64_t)nqx * (qy + (int64_t)nqy * qz);
-            for (int qx = lo[0]; qx < hi[0]; ++qx) {
-              double fa[2], fb[2];
-              for (int t = 0; t < 2; ++t) {
-                fa[t] = ya[t] * nl_f1(tabs, T, 0, CA.kd[t][0], A.i[0], qx, p);
-                fb[t] = yb[t] * nl_f1(tabs, T, 0, CB.kd[t][0], B.i[0], qx, p);
+            for (int ey = e0[1]; ey <= e1[1]; ++ey) {
+              const int oay = A.i[1] - ey, oby = B.i[1] - ey;
+#pragma unroll
+              for (int gy = 0; gy < NQ; ++gy) {
+                const int qy = ey * NQ + gy;
+                const double* ry = tabs + T.off[1] + (int64_t)qy * st;
+                double ya[2], yb[2];
+                for (int t = 0; t < 2; ++t) {
+                  ya[t] = za[t] * ry[ka[t][1] + oay];
+                  yb[t] = zb[t] * ry[kb[t][1] + oby];
+                }
+                const int64_t wrow = (int64_t)nqx * (qy + (int64_t)nqy * qz);
+                for (int ex = e0[0]; ex <= e1[0]; ++ex) {
+                  const int oax = A.i[0] - ex, obx = B.i[0] - ex;
+#pragma unroll
+                  for (int gx = 0; gx < NQ; ++gx) {
+                    const int qx = ex * NQ + gx;
+                    const double* rx = tabs + T.off[0] + (int64_t)qx * st;
+                    const double fa0 = ya[0] * rx[ka[0][0] + oax], fa1 = ya[1] * rx[ka[1][0] + oax];
+                    const double fb0 = yb[0] * rx[kb[0][0] + obx], fb1 = yb[1] * rx[kb[1][0] + obx];
+                    const int64_t w = wrow + qx;
+                    K += fa0 * (__ldg(Nq[0][0] + w) * fb0 + __ldg(Nq[0][1] + w) * fb1) +
+                         fa1 * (__ldg(Nq[1][0] + w) * fb0 + __ldg(Nq[1][1] + w) * fb1);
+                  }
+                }
               }
-              const int64_t w = wrow + qx;
-              for (int t = 0; t < 2; ++t)
-                for (int u = 0; u < 2; ++u) K += fa[t] * __ldg(Qs + nidx[t][u] * nqp + w) * fb[u];
             }
           }
+        }
       }
       v = K + sg * M;
     }
     out[e] = v;
   }
+}
+
+// host-side dispatch on the spline degree (the Gauss-point loops unroll)
+inline void launch_nl_assemble(int p, unsigned grid, size_t smem, cudaStream_t st, const DevPlan& D, const Tables1D& tb,
+                               const Geom& G, const NlTab& T, double inv_dt, const int* nlist, const int64_t* tstart,
+                               int nnl, const double* Q) {
+  switch (p) {
+#define NLA(PP) \
+  case PP: k_nl_assemble<PP><<<grid, 256, smem, st>>>(D, tb, G, T, inv_dt, nlist, tstart, nnl, Q); break;
+    NLA(1) NLA(2) NLA(3) NLA(4) NLA(5) NLA(6) NLA(7)
+#undef NLA
+    default: break;
+  }
+}
+inline cudaError_t nl_assemble_smem(size_t smem) {
+  const void* fs[7] = {(const void*)k_nl_assemble<1>, (const void*)k_nl_assemble<2>, (const void*)k_nl_assemble<3>,
+                       (const void*)k_nl_assemble<4>, (const void*)k_nl_assemble<5>, (const void*)k_nl_assemble<6>,
+                       (const void*)k_nl_assemble<7>};
+  for (const void* f : fs) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // per-block partial sums (fixed order) of |a - a_k|^2 and |a|^2 over the owned patches'

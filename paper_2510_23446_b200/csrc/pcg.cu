@@ -454,7 +454,7 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
 // __syncthreads per column block (double-buffered warp partials).
 template <class Src>
 __device__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm,
-                             const double* pft, int npf) {
+                             const double* pft, int npf, const double* Xr = nullptr, double* XW = nullptr) {
   const int Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   double* u = sm;             // Tb*64 input
   double* y = u + Tb * TS;    // Tb*64 row contributions
@@ -509,7 +509,80 @@ __device__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, S
       contrib += u[J * TS + threadIdx.x] * v;
     }
   }
+  if (it.part & 4) {
+    // the F-apply's Phi_b^T rows on the same input (P1 with sbbinv): -g_I = -sum_J PhiT_IJ v_J,
+    // rows Tb..Tb+Tp-1 of the inverse-factor store, into XW (as p1_item's p rows)
+    const double* X = Xr + it.a_off;
+    for (int I = Tb; I < Tb + it.Tp; ++I) {
+      double part[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) part[r] = 0.0;
+#pragma unroll 2
+      for (int J = 0; J < Tb; ++J) {
+        const double* t = X + tri_off(Ti + I, Ti + J) + off;
+        const double2 xv = *reinterpret_cast<const double2*>(u + J * TS + 2 * lane);
+        double2 a[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
+      }
+      const double sum = warp_reduce8(part);
+      if ((lane & 3) == 0) XW[it.vec_off + (int64_t)(Ti + I) * TS + row0 + warp_reduce8_row()] = -sum;
+    }
+  }
   __syncthreads();  // the next item overwrites u / y
+  return contrib;
+}
+
+// ---- P5 with sbbinv, whole-patch dealing (ItemDesc part 3): y2_J = -sum_I PhiT_IJ^T (N Pc)_I
+// for every column block J of the patch, N Pc gathered once; column sums over the 8 warps in
+// warp order (double-buffered partials, one __syncthreads per column). Returns this thread's
+// share of v . y2 (vsrc gives v = (B_s^T p)_pos).
+template <class PcF, class Src>
+__device__ double p5_phi_patch(const ItemDesc& it, const double* Xr, const int* p_grp, PcF pc, Src vsrc, double* Y2,
+                               double* sm) {
+  const int Ti = it.Ti, Tb = it.Tb, Tp = it.Tp, np = it.np, nb = it.nb;
+  double* g = sm;               // Tp*64: -(N Pc) on the patch's primal rows
+  double* cw = g + Tp * TS;     // 2 x 8 warps x 64
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
+  const int off = row0 * TS + 2 * lane;
+  const int* grp = p_grp + it.p_off;
+  const double* X = Xr + it.a_off;
+  const int64_t vo = it.vec_off + (int64_t)Ti * TS;
+  for (int e = threadIdx.x; e < Tp * TS; e += blockDim.x) g[e] = (e < np) ? -pc(grp[e]) : 0.0;
+  __syncthreads();
+  double contrib = 0.0;
+  for (int J = 0; J < Tb; ++J) {
+    double vj = 0.0;
+    if (threadIdx.x < TS && J * TS + (int)threadIdx.x < nb) vj = vsrc(it, it.b_off + J * TS + threadIdx.x, J * TS + threadIdx.x);
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll 2
+    for (int I = 0; I < Tp; ++I) {
+      const double* t = X + tri_off(Ti + Tb + I, Ti + J) + off;
+      double2 a[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const double xr = g[I * TS + row0 + r];
+        c0 += a[r].x * xr;
+        c1 += a[r].y * xr;
+      }
+    }
+    double* cb = cw + (J & 1) * 8 * TS;
+    cb[warp * TS + 2 * lane] = c0;
+    cb[warp * TS + 2 * lane + 1] = c1;
+    __syncthreads();
+    if (threadIdx.x < TS) {
+      double acc = 0.0;
+#pragma unroll
+      for (int w = 0; w < NTHR / 32; ++w) acc += cb[w * TS + threadIdx.x];
+      Y2[vo + (int64_t)J * TS + threadIdx.x] = acc;
+      contrib += vj * acc;
+    }
+  }
+  __syncthreads();
   return contrib;
 }
 
@@ -518,7 +591,7 @@ __device__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, S
 template <class Src>
 __device__ __forceinline__ double symv_item(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm,
                                             double* red, const double* pft = nullptr, int npf = 0, bool gat = true) {
-  if ((it.part & 7) == 2) return symv_patch(it, Sr, PW, usrc, sm, pft, npf);
+  if (it.part & 2) return symv_patch(it, Sr, PW, usrc, sm, pft, npf);
   const int I = it.I, Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   double* u = sm;            // Tb*64
   double* cr = u + Tb * TS;  // 9 * 64
@@ -1231,16 +1304,19 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         return q.sign * ldcg(A.pk[0][lown(q.k)] + q.k);
       };
       FOR_ITEMS(PH_P1, w) {
-        if (w.part & 8) symv_item(w, SIr, A.Y[me], vsrc, smw, red, PF0(j_w), GAT(PH_P1, w));
+        if ((w.part & 10) == 10) symv_patch(w, SIr, A.Y[me], vsrc, smw, PF0(j_w), Xr, A.XW[me]);
+        else if (w.part & 8) symv_item(w, SIr, A.Y[me], vsrc, smw, red, PF0(j_w), GAT(PH_P1, w));
         else p1_item(w, Xr, vsrc, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
       }
     }
     bar(PH_PC, false, 0.0);
     COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
     bar(PH_P5, false, 0.0);
-    FOR_ITEMS(PH_P5, w)
-      p5_item(w, Xr, A.XW[me], D.p_grp, pcf, [&](const ItemDesc&, int64_t, int) { return 0.0; }, A.Y[me], A.Y2[me], smw,
-              red, nullptr, PF0(j_w), GAT(PH_P5, w));
+    FOR_ITEMS(PH_P5, w) {
+      auto zero = [&](const ItemDesc&, int64_t, int) { return 0.0; };
+      if ((w.part & 3) == 3) p5_phi_patch(w, Xr, D.p_grp, pcf, zero, A.Y2[me], smw);
+      else p5_item(w, Xr, A.XW[me], D.p_grp, pcf, zero, A.Y[me], A.Y2[me], smw, red, nullptr, PF0(j_w), GAT(PH_P5, w));
+    }
     bar(-1, false, 0.0);
     for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x)
       A.r[1][me][k] = yv(pown(lpat_p(k)), lidx_p(k)) - yv(pown(lpat_m(k)), lidx_m(k));
@@ -1455,7 +1531,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         };
         FOR_ITEMS(PH_P1, w) {
           ITIME_BEGIN
-          if (w.part & 8) loc1 += symv_item(w, SIr, A.Y[me], vnew, smw, red, PF0(j_w), GAT(PH_P1, w));
+          if ((w.part & 10) == 10) loc1 += symv_patch(w, SIr, A.Y[me], vnew, smw, PF0(j_w), Xr, A.XW[me]);
+          else if (w.part & 8) loc1 += symv_item(w, SIr, A.Y[me], vnew, smw, red, PF0(j_w), GAT(PH_P1, w));
           else p1_item(w, Xr, vnew, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
           ITIME_END(PH_P1, j_w)
         }
@@ -1477,13 +1554,15 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       double pq;
       {
         double loc = loc1;
+        auto vcur = [&](const ItemDesc& iw, int64_t bb, int pos) {
+          const BPos q = bget(iw, bb, pos);
+          return q.sign * ldcg(pcurt[lown(q.k)] + q.k);
+        };
         FOR_ITEMS(PH_P5, w) {
           ITIME_BEGIN
-          loc += p5_item(w, Xr, A.XW[me], D.p_grp, pcf,
-                         [&](const ItemDesc& iw, int64_t bb, int pos) {
-                           const BPos q = bget(iw, bb, pos);
-                           return q.sign * ldcg(pcurt[lown(q.k)] + q.k);
-                         },
+          if ((w.part & 3) == 3) loc += p5_phi_patch(w, Xr, D.p_grp, pcf, vcur, A.Y2[me], smw);
+          else
+          loc += p5_item(w, Xr, A.XW[me], D.p_grp, pcf, vcur,
                          A.Y[me], A.Y2[me], smw, red,
                          (A.tstamp && step == 0 && it == 2 && gb < 4096) ? A.tstamp + 528 + gb * 8 + 4 : nullptr,
                          PF0(j_w), GAT(PH_P5, w));
