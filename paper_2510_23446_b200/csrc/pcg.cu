@@ -536,53 +536,43 @@ __device__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, S
 }
 
 // ---- P5 with sbbinv, whole-patch dealing (ItemDesc part 3): y2_J = -sum_I PhiT_IJ^T (N Pc)_I
-// for every column block J of the patch, N Pc gathered once; column sums over the 8 warps in
-// warp order (double-buffered partials, one __syncthreads per column). Returns this thread's
-// share of v . y2 (vsrc gives v = (B_s^T p)_pos).
+// for every column block J of the patch, N Pc gathered once. Warp w owns column blocks
+// J = w, w + 8, ...; lane l columns 2l, 2l+1 of them, streaming the Tp tiles of the column
+// row by row (coalesced 512-byte rows) with the sums in registers: no cross-warp reduction and
+// no block barrier per column (fixed row order: deterministic). Returns this thread's share of
+// v . y2 (vsrc gives v = (B_s^T p)_pos).
 template <class PcF, class Src>
 __device__ double p5_phi_patch(const ItemDesc& it, const double* Xr, const int* p_grp, PcF pc, Src vsrc, double* Y2,
                                double* sm) {
   const int Ti = it.Ti, Tb = it.Tb, Tp = it.Tp, np = it.np, nb = it.nb;
-  double* g = sm;               // Tp*64: -(N Pc) on the patch's primal rows
-  double* cw = g + Tp * TS;     // 2 x 8 warps x 64
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, row0 = warp * 8;
-  const int off = row0 * TS + 2 * lane;
+  double* g = sm;  // Tp*64: -(N Pc) on the patch's primal rows
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int* grp = p_grp + it.p_off;
   const double* X = Xr + it.a_off;
   const int64_t vo = it.vec_off + (int64_t)Ti * TS;
   for (int e = threadIdx.x; e < Tp * TS; e += blockDim.x) g[e] = (e < np) ? -pc(grp[e]) : 0.0;
   __syncthreads();
   double contrib = 0.0;
-  for (int J = 0; J < Tb; ++J) {
-    double vj = 0.0;
-    if (threadIdx.x < TS && J * TS + (int)threadIdx.x < nb) vj = vsrc(it, it.b_off + J * TS + threadIdx.x, J * TS + threadIdx.x);
+  for (int J = warp; J < Tb; J += NTHR / 32) {
+    const int c = J * TS + 2 * lane;
+    const double v0 = (c < nb) ? vsrc(it, it.b_off + c, c) : 0.0;
+    const double v1 = (c + 1 < nb) ? vsrc(it, it.b_off + c + 1, c + 1) : 0.0;
     double c0 = 0.0, c1 = 0.0;
-#pragma unroll 2
     for (int I = 0; I < Tp; ++I) {
-      const double* t = X + tri_off(Ti + Tb + I, Ti + J) + off;
-      double2 a[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const double xr = g[I * TS + row0 + r];
-        c0 += a[r].x * xr;
-        c1 += a[r].y * xr;
+      const double* t = X + tri_off(Ti + Tb + I, Ti + J) + 2 * lane;
+      const double* gi = g + I * TS;
+#pragma unroll 8
+      for (int r = 0; r < TS; ++r) {
+        const double2 a = ldg2(t + r * TS);
+        const double gr = gi[r];
+        c0 += a.x * gr;
+        c1 += a.y * gr;
       }
     }
-    double* cb = cw + (J & 1) * 8 * TS;
-    cb[warp * TS + 2 * lane] = c0;
-    cb[warp * TS + 2 * lane + 1] = c1;
-    __syncthreads();
-    if (threadIdx.x < TS) {
-      double acc = 0.0;
-#pragma unroll
-      for (int w = 0; w < NTHR / 32; ++w) acc += cb[w * TS + threadIdx.x];
-      Y2[vo + (int64_t)J * TS + threadIdx.x] = acc;
-      contrib += vj * acc;
-    }
+    *reinterpret_cast<double2*>(Y2 + vo + c) = make_double2(c0, c1);
+    contrib += v0 * c0 + v1 * c1;
   }
-  __syncthreads();
+  __syncthreads();  // the next item overwrites g
   return contrib;
 }
 
