@@ -424,25 +424,69 @@ __device__ __forceinline__ void mma_acc2(const double* sA, const double* sB, dou
       for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
   }
 }
-// acc += sum_{q < nk} op(A_q) op(B_q); sm holds 4 tiles (2 stages x {A, B})
+// ---- deep-K tile stream: acc += sum_{q < nk} op(A_q) op(B_q), K split into 32-wide halves,
+// 3-stage cp.async pipeline (one __syncthreads pair per half). A stage holds the two operand
+// halves in compact layouts: K along the stored tile's rows -> [32][SPAD] (all 64 columns);
+// K along its columns -> [64][HPAD]. Fragment reads are conflict-free per half-warp in both
+// (row strides 68 and 36 doubles are 4 mod 16 banks). 110.6 KB per CTA: 2 CTAs (8 warps) per
+// SM, where the 2-stage full-tile pipeline (139 KB) allowed one.
+constexpr int HPAD = 36;
+constexpr int HSZ = TS * HPAD;  // >= 32 * SPAD
+constexpr int MMA_STG = 2 * HSZ;
+constexpr int MMA_SMEM_DOUBLES = 3 * MMA_STG;  // also >= 2 full SPAD tiles (mul_left_store, mirrors)
+static_assert(MMA_SMEM_DOUBLES >= 2 * TS * SPAD, "stream buffer must hold two full tiles");
+template <bool KROWS>
+__device__ __forceinline__ void stage_half(const double* __restrict__ g, double* s, int kh) {
+  if (KROWS) {
+    for (int c = threadIdx.x; c < 32 * (TS / 2); c += blockDim.x) {
+      const int r = c >> 5, q = c & 31;
+      cp_async16(s + r * SPAD + 2 * q, g + (kh * 32 + r) * TS + 2 * q);
+    }
+  } else {
+    for (int c = threadIdx.x; c < TS * 16; c += blockDim.x) {
+      const int r = c >> 4, q = c & 15;
+      cp_async16(s + r * HPAD + 2 * q, g + r * TS + kh * 32 + 2 * q);
+    }
+  }
+}
+template <bool AT, bool BT>
+__device__ __forceinline__ void mma_acc_h(const double* sA, const double* sB, double (&acc)[4][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+#pragma unroll 4
+  for (int k0 = 0; k0 < 32; k0 += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = AT ? sA[(k0 + t) * SPAD + wm + i * 8 + g] : sA[(wm + i * 8 + g) * HPAD + k0 + t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = BT ? sB[(wn + j * 8 + g) * HPAD + k0 + t] : sB[(k0 + t) * SPAD + wn + j * 8 + g];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+}
 template <bool AT, bool BT, class AF, class BF>
 __device__ __forceinline__ void mma_stream(AF atile, BF btile, int nk, double* sm, double (&acc)[4][4][2]) {
   if (nk <= 0) return;
-  constexpr int STG = 2 * TS * SPAD;  // one stage = {A, B}
-  stage_async(atile(0), sm);
-  stage_async(btile(0), sm + TS * SPAD);
+  const int ns = 2 * nk;
+  auto issue = [&](int s) {
+    double* b = sm + (s % 3) * MMA_STG;
+    stage_half<AT>(atile(s >> 1), b, s & 1);
+    stage_half<!BT>(btile(s >> 1), b + HSZ, s & 1);
+  };
+  issue(0);
   cp_commit();
-  for (int q = 0; q < nk; ++q) {
-    if (q + 1 < nk) {
-      double* nx = sm + ((q + 1) & 1) * STG;
-      stage_async(atile(q + 1), nx);
-      stage_async(btile(q + 1), nx + TS * SPAD);
-    }
+  issue(1);
+  cp_commit();
+  for (int s = 0; s < ns; ++s) {
+    if (s + 2 < ns) issue(s + 2);
     cp_commit();
-    cp_wait<1>();
+    cp_wait<2>();
     __syncthreads();
-    const double* cu = sm + (q & 1) * STG;
-    mma_acc2<AT, BT>(cu, cu + TS * SPAD, acc);
+    const double* cu = sm + (s % 3) * MMA_STG;
+    mma_acc_h<AT, BT>(cu, cu + HSZ, acc);
     __syncthreads();
   }
 }
@@ -553,6 +597,69 @@ __global__ void __launch_bounds__(128) k_sbbinv(DevPlan D, const int* plist, dou
     const int r = e / TS, c = e % TS;
     out[e] = (c <= r) ? st[r * SPAD + c] : st[c * SPAD + r];
   }
+}
+
+// ---- left-looking factorisation (DESIGN.md §5 "Factorisation"): column J of every matrix is
+// brought up to date in one pass, A_IJ = W_IJ - sum_{K<J} L_IK L_JK^T for all I >= J, as one
+// deep-K DMMA stream per tile (operands read once per column, the tile written once) instead
+// of J rank-64 read-modify-writes; potrf + trsm of column J follow. In the b block
+// (Ti <= J <= I < Tfact) the partial sum over the i columns gives the interface Schur
+// complement S_bb_IJ = W_IJ - sum_{K<Ti} L_IK L_JK^T, written before the stream continues.
+// grid (maxT - J, nmat), 128 threads, MMA_SMEM_DOUBLES shared.
+__device__ __forceinline__ void acc_sub_store(const double* W, double* out, const double (&acc)[4][4][2]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int o = (wm + i * 8 + g) * TS + wn + j * 8 + 2 * t;
+      const double2 w = *reinterpret_cast<const double2*>(W + o);
+      *reinterpret_cast<double2*>(out + o) = make_double2(w.x - acc[i][j][0], w.y - acc[i][j][1]);
+    }
+}
+__global__ void __launch_bounds__(128) k_colupd(const CholDesc* __restrict__ ds, int J, double* base, double* sbb) {
+  const CholDesc d = ds[blockIdx.y];
+  const int I = J + blockIdx.x;
+  if (J >= d.Tfact || I >= d.T) return;
+  const bool cap = sbb && d.sbb_off >= 0 && J >= d.Ti && I < d.Tfact;
+  if (J == 0 && !cap) return;
+  extern __shared__ __align__(16) double smem[];
+  double* L = base + d.a_off;
+  double* C = L + tri_off(I, J);
+  double acc[4][4][2];
+  acc_zero(acc);
+  const int K1 = cap ? d.Ti : J;
+  mma_stream<false, true>([&](int q) { return L + tri_off(I, q); }, [&](int q) { return L + tri_off(J, q); }, K1, smem, acc);
+  if (cap) {
+    acc_sub_store(C, sbb + d.sbb_off + tri_off(I - d.Ti, J - d.Ti), acc);
+    mma_stream<false, true>([&](int q) { return L + tri_off(I, d.Ti + q); }, [&](int q) { return L + tri_off(J, d.Ti + q); },
+                            J - d.Ti, smem, acc);
+  }
+  acc_sub_store(C, C, acc);
+}
+// after the Tfact columns: the trailing tiles (I, J), Tfact <= J <= I < T (the local coarse
+// contribution S^s, or a front's update matrix), A_IJ -= sum_{K<Tfact} L_IK L_JK^T.
+// grid (tri_tiles(max T - Tfact), nmat).
+__global__ void __launch_bounds__(128) k_tailupd(const CholDesc* __restrict__ ds, double* base) {
+  const CholDesc d = ds[blockIdx.y];
+  const int Tt = d.T - d.Tfact;
+  const int64_t y = blockIdx.x;
+  if (y >= (int64_t)Tt * (Tt + 1) / 2 || d.Tfact == 0) return;
+  int Ip = (int)((sqrt(8.0 * (double)y + 1.0) - 1.0) * 0.5);
+  while ((int64_t)Ip * (Ip + 1) / 2 > y) --Ip;
+  while ((int64_t)(Ip + 1) * (Ip + 2) / 2 <= y) ++Ip;
+  const int Jp = (int)(y - (int64_t)Ip * (Ip + 1) / 2);
+  const int I = d.Tfact + Ip, J = d.Tfact + Jp;
+  extern __shared__ __align__(16) double smem[];
+  double* L = base + d.a_off;
+  double* C = L + tri_off(I, J);
+  double acc[4][4][2];
+  acc_zero(acc);
+  mma_stream<false, true>([&](int q) { return L + tri_off(I, q); }, [&](int q) { return L + tri_off(J, q); }, d.Tfact,
+                          smem, acc);
+  acc_sub_store(C, C, acc);
 }
 
 }  // namespace tcg

@@ -136,18 +136,39 @@ def test_virtual_ranks_sparse_coarse_match_golden(tcg, monkeypatch, name, vranks
     assert np.all(np.abs(np.asarray(it, dtype=np.int64) - g["iters"].astype(np.int64)) <= 1), (list(it), list(g["iters"]))
 
 
-@pytest.mark.parametrize("vranks", [1, 2])
-def test_whole_patch_items_cfg2_match_golden(tcg, monkeypatch, vranks):
-    """Whole-patch dealing (the item kinds cfg5 runs: one P5 item per column, one S_bb item per
-    patch reading every stored tile once, pcg.cu symv_patch), forced on cfg2 (TCG_GROUP=1),
-    all 50 steps against the oracle's golden file."""
+@pytest.mark.parametrize("vranks,sbbinv", [(1, 1), (2, 1), (1, 0), (3, 0)])
+def test_whole_patch_items_cfg2_match_golden(tcg, monkeypatch, vranks, sbbinv):
+    """Whole-patch dealing (the item kinds cfg5 runs: one S_bb / S_bb^-1 item per patch reading
+    every stored tile once, pcg.cu symv_patch, with the Phi_b^T rows; one Phi_b item per patch
+    in P5, p5_phi_patch; or, without the explicit S_bb^-1, one P5 item per column), forced on
+    cfg2 (TCG_GROUP=1, TCG_SBBINV), all 50 steps against the oracle's golden file."""
     monkeypatch.setenv("TCG_GROUP", "1")
+    monkeypatch.setenv("TCG_SBBINV", str(sbbinv))
     g, meta = _golden("cfg2")
     pr = workloads.get("cfg2")
     s = tcg.Solver()
     if vranks > 1:
         s.set_virtual_ranks(vranks)
     s.configure(pr)
+    s.setup()
+    s.step(int(meta["steps"]))
+    a = s.coefficients(1)
+    it = s.history()[0]
+    s.close()
+    ref = g["a1"]
+    err = float(np.linalg.norm(a - ref) / np.linalg.norm(ref))
+    assert err <= TOL, err
+    assert np.all(np.abs(np.asarray(it, dtype=np.int64) - g["iters"].astype(np.int64)) <= 1), (list(it), list(g["iters"]))
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_sbbinv_off_and_on_match_golden(tcg, monkeypatch, name):
+    """The PCG iteration with the explicit S_bb^-1 forced on (cfg2, where the default is the
+    X_bb form) or off (cfg3, where the default is S_bb^-1), all steps of the golden file."""
+    monkeypatch.setenv("TCG_SBBINV", "1" if name == "cfg2" else "0")
+    g, meta = _golden(name)
+    pr = workloads.get(name)
+    s = tcg.Solver().configure(pr)
     s.setup()
     s.step(int(meta["steps"]))
     a = s.coefficients(1)

@@ -98,6 +98,15 @@ def test_nonlinear_virtual_ranks(tcg):
     compare(tcg, small(), 3, vranks=2)
 
 
+@pytest.mark.parametrize("group", [0, 1])
+def test_nonlinear_with_explicit_sbb_inverse(tcg, monkeypatch, group):
+    """Newton iterates re-form S_bb^-1 for the nonlinear patches (k_sbbinv over their list);
+    forced on for the small case, with row items and with whole-patch items."""
+    monkeypatch.setenv("TCG_SBBINV", "1")
+    monkeypatch.setenv("TCG_GROUP", str(group))
+    compare(tcg, workloads.nl1(), 4)
+
+
 def test_constant_law_equals_linear(tcg):
     """k2 = 0: nu = k1 + k3 everywhere on the patch; the first Newton solve is the linear
     step and the second confirms it."""
