@@ -234,6 +234,9 @@ struct tcg_ctx {
   // the PCG iteration applies W_rr^-1 restricted to b as the explicit S_bb^-1 = X_bb^T X_bb
   // (one symmetric read) instead of X_bb^T (X_bb v) (two reads); TCG_SBBINV=0 restores the latter
   bool sbbinv = true;
+  // local factorisation order: left-looking (deep-K column updates, default) or right-looking
+  // (TCG_CHOL=right)
+  bool chol_left = true;
   int warm = 0;  // warm-start subspace dimension k (tcg_set_warm_start), 0 = off
   int64_t warm_base = 0;  // first step of the current warm-start history (k changed / refactor)
   int64_t* d_pcprog = nullptr;
@@ -465,9 +468,31 @@ static tcg_status do_plan(tcg_ctx* h) {
 // =========================================================================================
 // numeric setup (assembly, batched Cholesky, inverse factors, coarse)
 // =========================================================================================
+// maxTtail > 0: left-looking (k_colupd per column, k_tailupd for the trailing block of at
+// most maxTtail tiles); 0: right-looking (k_capture_sbb / k_update per column)
 static tcg_status run_cholesky(tcg_ctx* h, const CholDesc* d_desc, int nmat, int maxT, int maxTf, int maxTb,
-                               double* base, double* dinv, double* sbb, DevError* derr, int coarse) {
+                               double* base, double* dinv, double* sbb, DevError* derr, int coarse, int maxTtail = 0) {
   const int subst = (h->stable_mask & 4) ? 1 : 0;
+  if (maxTtail > 0) {
+    for (int J = 0; J < maxTf; ++J) {
+      k_colupd<<<dim3((unsigned)(maxT - J), (unsigned)nmat), 128, MMA_SMEM_DOUBLES * sizeof(double), h->stream>>>(
+          d_desc, J, base, sbb);
+      k_potrf<<<nmat, 256, 2 * TS * PS * sizeof(double), h->stream>>>(d_desc, J, base, dinv, derr, coarse);
+      h->nlaunch += 2;
+      CKL();
+      const int rows = maxT - J - 1;
+      if (rows > 0) {
+        k_trsm<<<dim3(rows, nmat), 128, 2 * TS * SPAD * sizeof(double), h->stream>>>(d_desc, J, base, dinv, subst);
+        ++h->nlaunch;
+        CKL();
+      }
+    }
+    k_tailupd<<<dim3((unsigned)tri_tiles(maxTtail), (unsigned)nmat), 128, MMA_SMEM_DOUBLES * sizeof(double), h->stream>>>(
+        d_desc, base);
+    ++h->nlaunch;
+    CKL();
+    return TCG_OK;
+  }
   for (int k = 0; k < maxTf; ++k) {
     if (sbb && maxTb > 0) {
       dim3 gc((unsigned)tri_tiles(maxTb), nmat);
@@ -528,7 +553,7 @@ static tcg_status numeric_sparse_coarse(tcg_ctx* h) {
     TRY(run_cholesky(h, g.ldesc[lv], nlv, g.lmaxT[lv], g.lmaxTV[lv], 0, g.FR, g.FDinv, nullptr, R.derr, 1));
     for (int I = 0; I < g.lmaxT[lv]; ++I) {
       dim3 gr(std::max(1, std::min(I + 1, g.lmaxTV[lv])), (unsigned)nlv);
-      k_xinv_row<<<gr, 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(g.Dn, I, g.Fscr, g.Dn.dinv_off, g.lplist[lv]);
+      k_xinv_row<<<gr, 128, MMA_SMEM_DOUBLES * sizeof(double), h->stream>>>(g.Dn, I, g.Fscr, g.Dn.dinv_off, g.lplist[lv]);
       ++h->nlaunch;
       k_xrow_copy<<<gr, 256, 0, h->stream>>>(g.Dn, I, g.Fscr, g.Dn.dinv_off, g.lplist[lv]);
       ++h->nlaunch;
@@ -677,19 +702,20 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
     if (nmat == 0) continue;
     const int mT = newton ? R.nl_maxT : R.maxT, mTr = newton ? R.nl_maxTr : R.maxTr, mTb = newton ? R.nl_maxTb : R.maxTb;
     const int* lst = newton ? R.d_nlist : R.d_plist;
-    TRY(run_cholesky(h, newton ? R.d_nldesc : R.d_desc, nmat, mT, mTr, mTb, R.A, R.Dinv, R.Sbb, R.derr, 0));
+    TRY(run_cholesky(h, newton ? R.d_nldesc : R.d_desc, nmat, mT, mTr, mTb, R.A, R.Dinv, R.Sbb, R.derr, 0,
+                     h->chol_left ? std::max(1, h->maxTp) : 0));
     // in-place inverse of the augmented factor: Xaug = [L_rr^-1 ; W_pr W_rr^-1]
     const int64_t* scr_off = h->D.dinv_off;  // scratch rows share the Dinv layout (Tr tiles)
     for (int I = 0; I < mT; ++I) {
       dim3 g(std::min(I + 1, mTr), (unsigned)nmat);
-      k_xinv_row<<<g, 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(R.D, I, R.xscr, scr_off, lst);
+      k_xinv_row<<<g, 128, MMA_SMEM_DOUBLES * sizeof(double), h->stream>>>(R.D, I, R.xscr, scr_off, lst);
       ++h->nlaunch;
       k_xrow_copy<<<g, 256, 0, h->stream>>>(R.D, I, R.xscr, scr_off, lst);
       ++h->nlaunch;
       CKL();
     }
     if (h->sbbinv && mTb > 0) {  // S_bb^-1 = X_bb^T X_bb for the PCG iteration
-      k_sbbinv<<<dim3((unsigned)tri_tiles(mTb), (unsigned)nmat), 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(
+      k_sbbinv<<<dim3((unsigned)tri_tiles(mTb), (unsigned)nmat), 128, MMA_SMEM_DOUBLES * sizeof(double), h->stream>>>(
           R.D, lst, R.SI);
       ++h->nlaunch;
       CKL();
@@ -723,11 +749,11 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
       TRY(run_cholesky(h, h->d_cdesc, 1, Tc, Tc, 0, R.C, R.Cinv, nullptr, R.derr, 1));
       for (int I = 0; I < Tc; ++I) {
         dim3 g(I + 1, 1);
-        k_trinv_row<<<g, 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(h->d_cinv, I, R.C, R.CX, R.Cinv);
+        k_trinv_row<<<g, 128, MMA_SMEM_DOUBLES * sizeof(double), h->stream>>>(h->d_cinv, I, R.C, R.CX, R.Cinv);
         ++h->nlaunch;
         CKL();
       }
-      k_sinv<<<dim3(Tc, Tc), 128, 4 * TS * SPAD * sizeof(double), h->stream>>>(R.CX, R.Sinv, Tc);
+      k_sinv<<<dim3(Tc, Tc), 128, MMA_SMEM_DOUBLES * sizeof(double), h->stream>>>(R.CX, R.Sinv, Tc);
       ++h->nlaunch;
       CKL();
     }
@@ -1243,8 +1269,15 @@ static tcg_status do_setup(tcg_ctx* h) {
   {
     const char* ev = getenv("TCG_STABLE");
     if (ev) h->stable_mask = atoi(ev);
+    // explicit S_bb^-1 in the iteration when the local factors stream from HBM (packed X_bb
+    // beyond 16 MB: cfg3-cfg5); on L2-resident working sets (cfg1, cfg2) the two row/column
+    // GEMVs of X_bb are 3-5 % faster than the symmetric product (profiles/round2_notes.md)
+    const char* cl = getenv("TCG_CHOL");
+    h->chol_left = !(cl && std::string(cl) == "right");
     const char* si = getenv("TCG_SBBINV");
-    h->sbbinv = !(si && atoi(si) == 0);
+    double xbb = 0.0;
+    for (const auto& q : h->plan.pp) xbb += 4.0 * q.nb * (q.nb + 1.0);
+    h->sbbinv = si ? atoi(si) != 0 : xbb > 16e6;
   }
   const int P = pl.npatch;
   const int NR = h->nranks;
@@ -1509,10 +1542,12 @@ static tcg_status do_setup(tcg_ctx* h) {
     scratch = (scratch + 1) & ~(size_t)1;  // keep the item cache 16-byte aligned
     h->smem_pcg = sizeof(double) * scratch;
     TRY(set_smem(h, (const void*)k_fw, h->smem_pcg));
-    TRY(set_smem(h, (const void*)k_xinv_row, 4 * TS * SPAD * sizeof(double)));
-    TRY(set_smem(h, (const void*)k_sinv, 4 * TS * SPAD * sizeof(double)));
-    TRY(set_smem(h, (const void*)k_sbbinv, 4 * TS * SPAD * sizeof(double)));
-    TRY(set_smem(h, (const void*)k_trinv_row, 4 * TS * SPAD * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_xinv_row, MMA_SMEM_DOUBLES * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_sinv, MMA_SMEM_DOUBLES * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_sbbinv, MMA_SMEM_DOUBLES * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_colupd, MMA_SMEM_DOUBLES * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_tailupd, MMA_SMEM_DOUBLES * sizeof(double)));
+    TRY(set_smem(h, (const void*)k_trinv_row, MMA_SMEM_DOUBLES * sizeof(double)));
     TRY(set_smem(h, (const void*)k_tables1d, h->smem_tables));
     TRY(set_smem(h, (const void*)k_potrf, 2 * TS * PS * sizeof(double)));
     TRY(set_smem(h, (const void*)k_trsm, 2 * TS * SPAD * sizeof(double)));
