@@ -475,23 +475,45 @@ __device__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, S
 #pragma unroll 2
     for (int I = J; I < Tb; ++I) {
       double2 a[8];
+      // diagonal tiles: only the lower triangle is used (row part c <= r, column part c < r);
+      // rows / columns at or beyond nb (padding) are not loaded: the product is the same and
+      // the DRAM sectors of the skipped entries are never fetched
+      const bool edge = (I == J) || ((I == Tb - 1) && (nb & (TS - 1)));
       if (I == 0 && npf > 0) {
 #pragma unroll
         for (int r = 0; r < 8; ++r) a[r] = lds2(pft + off + r * TS);
-      } else {
+      } else if (!edge) {
         const double* t = S + tri_off(I, J) + off;
 #pragma unroll
         for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
+      } else {
+        const double* t = S + tri_off(I, J) + off;
+        const int rlim = nb - I * TS - row0, cl = 2 * lane;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const bool ok = r < rlim && J * TS + cl < nb && (I != J || cl <= row0 + r);
+          a[r] = ok ? ldg2(t + r * TS) : make_double2(0.0, 0.0);
+        }
+      }
+      if (I == J) {  // mask the strict upper triangle (the .y of a pair straddling the diagonal)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          if (2 * lane > row0 + r) a[r].x = 0.0;
+          if (2 * lane + 1 > row0 + r) a[r].y = 0.0;
+        }
       }
       double part[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) part[r] = a[r].x * uJ.x + a[r].y * uJ.y;
-      if (I > J) {
+      {
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const double xr = u[I * TS + row0 + r];
-          c0 += a[r].x * xr;
-          c1 += a[r].y * xr;
+          // column part of the strict lower triangle: diagonal entries only in the row part
+          const double ax = (I == J && 2 * lane == row0 + r) ? 0.0 : a[r].x;
+          const double ay = (I == J && 2 * lane + 1 == row0 + r) ? 0.0 : a[r].y;
+          c0 += ax * xr;
+          c1 += ay * xr;
         }
       }
       const double rs = warp_reduce8(part);
@@ -517,13 +539,15 @@ __device__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, S
       double part[8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) part[r] = 0.0;
+      const int rlim = it.np - (I - Tb) * TS - row0;  // primal rows of this block (padding skipped)
 #pragma unroll 2
       for (int J = 0; J < Tb; ++J) {
         const double* t = X + tri_off(Ti + I, Ti + J) + off;
         const double2 xv = *reinterpret_cast<const double2*>(u + J * TS + 2 * lane);
+        const bool cok = J * TS + 2 * lane < nb;
         double2 a[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) a[r] = ldg2(t + r * TS);
+        for (int r = 0; r < 8; ++r) a[r] = (r < rlim && cok) ? ldg2(t + r * TS) : make_double2(0.0, 0.0);
 #pragma unroll
         for (int r = 0; r < 8; ++r) part[r] += a[r].x * xv.x + a[r].y * xv.y;
       }
@@ -558,12 +582,14 @@ __device__ double p5_phi_patch(const ItemDesc& it, const double* Xr, const int* 
     const double v0 = (c < nb) ? vsrc(it, it.b_off + c, c) : 0.0;
     const double v1 = (c + 1 < nb) ? vsrc(it, it.b_off + c + 1, c + 1) : 0.0;
     double c0 = 0.0, c1 = 0.0;
+    const bool cok = c < nb;  // padded columns and rows are not loaded
     for (int I = 0; I < Tp; ++I) {
       const double* t = X + tri_off(Ti + Tb + I, Ti + J) + 2 * lane;
       const double* gi = g + I * TS;
+      const int rn = min(TS, np - I * TS);
 #pragma unroll 8
-      for (int r = 0; r < TS; ++r) {
-        const double2 a = ldg2(t + r * TS);
+      for (int r = 0; r < rn; ++r) {
+        const double2 a = cok ? ldg2(t + r * TS) : make_double2(0.0, 0.0);
         const double gr = gi[r];
         c0 += a.x * gr;
         c1 += a.y * gr;
