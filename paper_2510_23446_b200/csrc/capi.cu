@@ -320,7 +320,8 @@ struct tcg_ctx {
     if (pool_user) {  // last handle on this device: hand the pool's memory back to the driver
       PoolReg& R = pools();
       std::lock_guard<std::mutex> lk(R.mu);
-      if (--R.live[device] == 0 && R.pool[device]) cudaMemPoolTrimTo(R.pool[device], 0);
+      const char* keep = getenv("TCG_POOL_RETAIN");  // experiment: keep the freed memory cached
+      if (--R.live[device] == 0 && R.pool[device] && !(keep && atoi(keep))) cudaMemPoolTrimTo(R.pool[device], 0);
       pool_user = false;
     }
     for (void* p : allocs) cudaFree(p);

@@ -577,26 +577,42 @@ __device__ double p5_phi_patch(const ItemDesc& it, const double* Xr, const int* 
   for (int e = threadIdx.x; e < Tp * TS; e += blockDim.x) g[e] = (e < np) ? -pc(grp[e]) : 0.0;
   __syncthreads();
   double contrib = 0.0;
-  for (int J = warp; J < Tb; J += NTHR / 32) {
-    const int c = J * TS + 2 * lane;
-    const double v0 = (c < nb) ? vsrc(it, it.b_off + c, c) : 0.0;
-    const double v1 = (c + 1 < nb) ? vsrc(it, it.b_off + c + 1, c + 1) : 0.0;
-    double c0 = 0.0, c1 = 0.0;
-    const bool cok = c < nb;  // padded columns and rows are not loaded
+  // column blocks J and J + 8 of a warp are streamed together (twice the loads in flight; with
+  // Tb <= 16 every warp has at most these two)
+  for (int J0 = warp; J0 < Tb; J0 += 2 * (NTHR / 32)) {
+    const int J1 = J0 + NTHR / 32;
+    const bool two = J1 < Tb;
+    const int ca = J0 * TS + 2 * lane, cb = J1 * TS + 2 * lane;
+    const bool oka = ca < nb, okb = two && cb < nb;  // padded columns and rows are not loaded
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
     for (int I = 0; I < Tp; ++I) {
-      const double* t = X + tri_off(Ti + Tb + I, Ti + J) + 2 * lane;
+      const double* ta = X + tri_off(Ti + Tb + I, Ti + J0) + 2 * lane;
+      const double* tb = two ? X + tri_off(Ti + Tb + I, Ti + J1) + 2 * lane : ta;
       const double* gi = g + I * TS;
       const int rn = min(TS, np - I * TS);
 #pragma unroll 8
       for (int r = 0; r < rn; ++r) {
-        const double2 a = cok ? ldg2(t + r * TS) : make_double2(0.0, 0.0);
+        const double2 x = oka ? ldg2(ta + r * TS) : make_double2(0.0, 0.0);
+        const double2 z = okb ? ldg2(tb + r * TS) : make_double2(0.0, 0.0);
         const double gr = gi[r];
-        c0 += a.x * gr;
-        c1 += a.y * gr;
+        a0 += x.x * gr;
+        a1 += x.y * gr;
+        b0 += z.x * gr;
+        b1 += z.y * gr;
       }
     }
-    *reinterpret_cast<double2*>(Y2 + vo + c) = make_double2(c0, c1);
-    contrib += v0 * c0 + v1 * c1;
+    *reinterpret_cast<double2*>(Y2 + vo + ca) = make_double2(a0, a1);
+    double va0 = 0.0, va1 = 0.0;
+    if (ca < nb) va0 = vsrc(it, it.b_off + ca, ca);
+    if (ca + 1 < nb) va1 = vsrc(it, it.b_off + ca + 1, ca + 1);
+    contrib += va0 * a0 + va1 * a1;
+    if (two) {
+      *reinterpret_cast<double2*>(Y2 + vo + cb) = make_double2(b0, b1);
+      double vb0 = 0.0, vb1 = 0.0;
+      if (cb < nb) vb0 = vsrc(it, it.b_off + cb, cb);
+      if (cb + 1 < nb) vb1 = vsrc(it, it.b_off + cb + 1, cb + 1);
+      contrib += vb0 * b0 + vb1 * b1;
+    }
   }
   __syncthreads();  // the next item overwrites g
   return contrib;
