@@ -361,14 +361,20 @@ def test_back_to_back_reductions_no_race(tcg, monkeypatch):
             assert np.linalg.norm(a1 - ref) / np.linalg.norm(ref) <= TOL
 
 
-@pytest.mark.parametrize("name,steps,vranks,k", [("cfg1", 10, 1, 4), ("cfg1", 10, 1, 1), ("contrast", 6, 1, 4),
-                                                 ("cfg2", 8, 1, 4), ("cfg2", 6, 3, 4), ("insulators", 7, 1, 3)])
-def test_warm_start_matches_oracle(tcg, name, steps, vranks, k):
+@pytest.mark.parametrize("name,steps,vranks,k,knobs", [("cfg1", 10, 1, 4, ""), ("cfg1", 10, 1, 1, ""),
+                                                       ("contrast", 6, 1, 4, ""), ("cfg2", 8, 1, 4, ""),
+                                                       ("cfg2", 6, 3, 4, ""), ("insulators", 7, 1, 3, ""),
+                                                       ("cfg2", 8, 1, 4, "si-group")])
+def test_warm_start_matches_oracle(tcg, monkeypatch, name, steps, vranks, k, knobs):
     """Warm start (R20): the GPU's Galerkin projection on the
     previous k solutions (ring buffers, d - r products, skip-Cholesky in thread 0) against
     the oracle's warm PCG, every step; on cfg2 it saves PCG iterations against the cold start.
     'insulators' has exact starts (0 iterations after step 0), a d = 0 step (t = 1/2) and a
-    rank-1 subspace; it stops at t = 7/8 (at t = 1 the solution is exactly 0)."""
+    rank-1 subspace; it stops at t = 7/8 (at t = 1 the solution is exactly 0). 'si-group'
+    runs the item kinds of cfg5 (explicit S_bb^-1, whole-patch items) on cfg2."""
+    if knobs == "si-group":
+        monkeypatch.setenv("TCG_SBBINV", "1")
+        monkeypatch.setenv("TCG_GROUP", "1")
     if name == "insulators":
         pr = workloads.custom((2, 2, 1), 1, (2, 2, 2), [0.0] * 4, [1.0, 2.0, 1.0, 3.0], name="insulators")
         pr.n_steps = 8
