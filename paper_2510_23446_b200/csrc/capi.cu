@@ -17,6 +17,8 @@
 #include <functional>
 #include <map>
 #include <mutex>
+#include <thread>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -112,7 +114,7 @@ struct RankDev {
   int nl_maxT = 0, nl_maxTr = 0, nl_maxTb = 0;
   int64_t* d_ntstart = nullptr;
   int64_t nl_ntiles = 0;
-  double *Q = nullptr, *gnl = nullptr, *a_old = nullptr, *a_k = nullptr, *nl_part = nullptr;
+  double *Q = nullptr, *gnl = nullptr, *a_old = nullptr, *a_k = nullptr, *nl_part = nullptr, *Kel = nullptr;
   // replicated coarse problem (computed by the first local rank, aliased by other local ranks)
   double *C = nullptr, *Cinv = nullptr, *CX = nullptr, *Sinv = nullptr;
   DevPlan D{};  // DevPlan with me / A / Dinv / Sbb of this rank
@@ -660,7 +662,7 @@ static tcg_status do_numeric(tcg_ctx* h, const std::function<tcg_status()>& mid 
       k_nl_quad<<<dim3(nn, (unsigned)std::min<int64_t>(64, (nqp + 255) / 256)), 256, 0, h->stream>>>(
           h->G, h->ntab, R.d_nlist, R.a_loc, h->d_nlk, R.Q);
       launch_nl_assemble(pl.p, (unsigned)R.nl_ntiles, h->nl_smem, h->stream, R.D, h->tb, h->G, h->ntab, 1.0 / dt,
-                         R.d_nlist, R.d_ntstart, (int)nn, R.Q);
+                         R.d_nlist, R.d_ntstart, (int)nn, R.Q, R.Kel);
       k_nl_g<<<dim3(nn, (unsigned)((pl.nloc + 255) / 256)), 256, h->nl_smem, h->stream>>>(R.D, h->G, h->ntab, R.d_nlist,
                                                                                         R.Q, R.gnl);
       h->nlaunch += 3;
@@ -1011,24 +1013,12 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
       moff[s2 + 1] = moff[s2] + (int64_t)np2 * np2;
     }
     std::vector<int64_t> map(std::max<int64_t>(moff[pl.npatch], 1), -1);
-    // entries bucketed by the front that receives them (the node eliminating the first of the
-    // two groups), then resolved per node through a dense group -> frontal position table
-    std::vector<int64_t> boffs(nn + 1, 0);
-    for (int s2 = 0; s2 < pl.npatch; ++s2) {
-      const auto& grp = pl.pp[s2].p_grp;
-      for (int ga : grp)
-        for (int gb : grp)
-          if (ga >= gb) ++boffs[std::min(nd.node_of[ga], nd.node_of[gb]) + 1];
-    }
-    for (int x = 0; x < nn; ++x) boffs[x + 1] += boffs[x];
-    struct Ent {
-      int64_t e;
-      int ga, gb;
-    };
-    std::vector<Ent> ents(std::max<int64_t>(boffs[nn], 1));
-    {
-      std::vector<int64_t> fill(boffs.begin(), boffs.end() - 1);
-      for (int s2 = 0; s2 < pl.npatch; ++s2) {
+    // each entry (ga >= gb) goes to the front of the node eliminating the first of the two
+    // groups, at the groups' frontal positions (CoarseND::fpos); patches are independent, so
+    // host threads split them (the map is a pure function of the plan)
+    std::atomic<int> bad{0};
+    auto work = [&](int t0, int nt) {
+      for (int s2 = t0; s2 < pl.npatch; s2 += nt) {
         const auto& grp = pl.pp[s2].p_grp;
         const int np2 = (int)grp.size();
         for (int a = 0; a < np2; ++a)
@@ -1036,24 +1026,24 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
             const int ga = grp[a], gb = grp[b];
             if (ga < gb) continue;
             const int x = std::min(nd.node_of[ga], nd.node_of[gb]);  // postorder: descendant first
-            ents[fill[x]++] = Ent{moff[s2] + (int64_t)a * np2 + b, ga, gb};
+            const int fa2 = nd.fpos(x, ga), fb2 = nd.fpos(x, gb);
+            if (fa2 < 0 || fb2 < 0) {
+              bad = 1;
+              continue;
+            }
+            const int r = std::max(fa2, fb2), cc = std::min(fa2, fb2);
+            map[moff[s2] + (int64_t)a * np2 + b] = aoff[x] + tri_off(r >> 6, cc >> 6) + (int64_t)(r & 63) * TS + (cc & 63);
           }
       }
+    };
+    {
+      const int nt = std::max(1, std::min(16, (int)std::thread::hardware_concurrency()));
+      std::vector<std::thread> th;
+      for (int t0 = 1; t0 < nt; ++t0) th.emplace_back(work, t0, nt);
+      work(0, nt);
+      for (auto& x : th) x.join();
     }
-    std::vector<int> pos(std::max<int64_t>(pl.nc, 1), -1);
-    for (int x = 0; x < nn; ++x) {
-      if (boffs[x] == boffs[x + 1]) continue;
-      for (size_t i = 0; i < N[x].V.size(); ++i) pos[N[x].V[i]] = (int)i;
-      for (size_t i = 0; i < N[x].B.size(); ++i) pos[N[x].B[i]] = 64 * N[x].TV + (int)i;
-      for (int64_t q = boffs[x]; q < boffs[x + 1]; ++q) {
-        const int fa2 = pos[ents[q].ga], fb2 = pos[ents[q].gb];
-        if (fa2 < 0 || fb2 < 0) return fail(h, TCG_EINVAL, "nested dissection: coupled pair outside a front");
-        const int r = std::max(fa2, fb2), c = std::min(fa2, fb2);
-        map[ents[q].e] = aoff[x] + tri_off(r >> 6, c >> 6) + (int64_t)(r & 63) * TS + (c & 63);
-      }
-      for (int g2 : N[x].V) pos[g2] = -1;
-      for (int g2 : N[x].B) pos[g2] = -1;
-    }
+    if (bad) return fail(h, TCG_EINVAL, "nested dissection: coupled pair outside a front");
     TRY(dupload(h, &g.moff, moff));
     TRY(dupload(h, &g.map, map));
   }
@@ -1898,6 +1888,10 @@ static tcg_status do_setup(tcg_ctx* h) {
       TRY(dupload(h, &R.d_ntstart, nts));
       const int64_t nqp = (int64_t)h->ntab.nq[0] * h->ntab.nq[1] * h->ntab.nq[2];
       TRY(dalloc(h, &R.Q, (size_t)R.nlist.size() * 9 * nqp));
+      // element tangent matrices (p <= 3; TCG_NL_ELEM=0: the per-entry Gauss-point kernel)
+      const size_t ke = nl_elem_doubles(pl.p, pl.el[0] * pl.el[1] * pl.el[2]);
+      const char* ne = getenv("TCG_NL_ELEM");
+      if (ke > 0 && !(ne && atoi(ne) == 0)) TRY(dalloc(h, &R.Kel, R.nlist.size() * ke));
     }
     if (h->n_nl > 0) {  // every rank joins the Newton loop (right-hand side vector, iterates, norms)
       TRY(dzero(h, &R.gnl, ov));

@@ -317,10 +317,166 @@ __global__ void __launch_bounds__(256) k_nl_assemble(DevPlan D, Tables1D tb, Geo
   }
 }
 
+// ---- element matrices (p <= 3): one CTA per element of a nonlinear patch computes the
+// element tangent matrix Ke[a][b] = sum_q curl w_a^T Nw curl w_b over the element's (p+1)^3
+// Gauss points with the functions' curl values and Nw staged in shared memory (lower triangle,
+// local function order: component-major, then kk, jj, ii of the active functions); the tile
+// kernel then sums Ke over the elements of each entry's common support (fixed element order).
+template <int P>
+struct NlElem {
+  static constexpr int NQ = P + 1, NQ3 = NQ * NQ * NQ;
+  static constexpr int NF1 = P * (P + 1) * (P + 1), NF = 3 * NF1;
+  static constexpr size_t smem = sizeof(double) * ((size_t)NF * NQ3 * 2 + 6 * NQ3);
+  // local index of a function (component c, element offsets oi, oj, ok along x, y, z)
+  __device__ static int loc(int c, int oi, int oj, int ok) {
+    const int n0 = (c == 0) ? P : P + 1, n1 = (c == 1) ? P : P + 1;
+    return c * NF1 + oi + n0 * (oj + n1 * ok);
+  }
+};
+template <int P>
+__global__ void __launch_bounds__(256) k_nl_elem(Geom G, NlTab T, const int* nlist, const double* __restrict__ Q,
+                                                 double* Kel) {
+  using E = NlElem<P>;
+  constexpr int NQ = E::NQ, NQ3 = E::NQ3, NF1 = E::NF1, NF = E::NF;
+  extern __shared__ double sm[];
+  double* Cv = sm;               // [NF][NQ3][2]: the two nonzero curl terms (signs included)
+  double* Ns = sm + NF * NQ3 * 2;  // [6][NQ3]
+  const int li = blockIdx.y;
+  const int e = blockIdx.x, ne = G.el[0] * G.el[1] * G.el[2];
+  const int ex = e % G.el[0], ey = (e / G.el[0]) % G.el[1], ez = e / (G.el[0] * G.el[1]);
+  const int nqx = T.nq[0], nqy = T.nq[1];
+  const int64_t nqp = (int64_t)nqx * nqy * T.nq[2];
+  const double* Qs = Q + (int64_t)li * 9 * nqp;
+  for (int i = threadIdx.x; i < 6 * NQ3; i += blockDim.x) {
+    const int comp = i / NQ3, q = i % NQ3;
+    const int gx = q % NQ, gy = (q / NQ) % NQ, gz = q / (NQ * NQ);
+    const int64_t w = (ex * NQ + gx) + (int64_t)nqx * ((ey * NQ + gy) + (int64_t)nqy * (ez * NQ + gz));
+    Ns[i] = Qs[comp * nqp + w];
+  }
+  for (int i = threadIdx.x; i < NF * NQ3; i += blockDim.x) {
+    const int f = i / NQ3, q = i % NQ3;
+    const int c = f / NF1, lf = f % NF1;
+    const int n0 = (c == 0) ? P : P + 1, n1 = (c == 1) ? P : P + 1;
+    const int oi = lf % n0, oj = (lf / n0) % n1, ok = lf / (n0 * n1);
+    const int gx = q % NQ, gy = (q / NQ) % NQ, gz = q / (NQ * NQ);
+    const double* rx = T.base + T.off[0] + (int64_t)(ex * NQ + gx) * T.stride + 1;
+    const double* ry = T.base + T.off[1] + (int64_t)(ey * NQ + gy) * T.stride + 1;
+    const double* rz = T.base + T.off[2] + (int64_t)(ez * NQ + gz) * T.stride + 1;
+    const CurlTerms C = curl_terms(c);
+    for (int t = 0; t < 2; ++t)
+      Cv[(f * NQ3 + q) * 2 + t] = C.sg[t] * rx[C.kd[t][0] * NQ + oi] * ry[C.kd[t][1] * NQ + oj] * rz[C.kd[t][2] * NQ + ok];
+  }
+  __syncthreads();
+  double* K = Kel + ((int64_t)li * ne + e) * NF * NF;
+  for (int idx = threadIdx.x; idx < NF * NF; idx += blockDim.x) {
+    const int a = idx / NF, b = idx % NF;
+    if (b > a) continue;
+    const CurlTerms CA = curl_terms(a / NF1), CB = curl_terms(b / NF1);
+    const double* n00 = Ns + sym6(CA.r[0], CB.r[0]) * NQ3;
+    const double* n01 = Ns + sym6(CA.r[0], CB.r[1]) * NQ3;
+    const double* n10 = Ns + sym6(CA.r[1], CB.r[0]) * NQ3;
+    const double* n11 = Ns + sym6(CA.r[1], CB.r[1]) * NQ3;
+    const double* ca = Cv + a * NQ3 * 2;
+    const double* cb = Cv + b * NQ3 * 2;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int q = 0; q < NQ3; ++q) {
+      const double a0 = ca[2 * q], a1 = ca[2 * q + 1], b0 = cb[2 * q], b1 = cb[2 * q + 1];
+      acc += a0 * (n00[q] * b0 + n01[q] * b1) + a1 * (n10[q] * b0 + n11[q] * b1);
+    }
+    K[a * NF + b] = acc;
+  }
+}
+
+// the tile-packed J of the nonlinear patches from the element matrices: entry (a, b) = sum over
+// the elements both functions are active on (z, y, x order) of Ke + (sigma/dt) M_ab
+template <int P>
+__global__ void __launch_bounds__(256) k_nl_gather(DevPlan D, Tables1D tb, Geom G, double inv_dt, const int* nlist,
+                                                   const int64_t* tstart, int nnl, const double* __restrict__ Kel) {
+  using E = NlElem<P>;
+  constexpr int NF = E::NF;
+  const int64_t tile = blockIdx.x;
+  const int li = find_patch(tstart, nnl, tile);
+  const int s = nlist[li];
+  const int64_t tl = tile - tstart[li];
+  int I = (int)((sqrt(8.0 * (double)tl + 1.0) - 1.0) * 0.5);
+  while ((int64_t)I * (I + 1) / 2 > tl) --I;
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= tl) ++I;
+  const int J = (int)(tl - (int64_t)I * (I + 1) / 2);
+  __shared__ T1 t1[3];
+  if (threadIdx.x < 3) {
+    const int d = threadIdx.x;
+    t1[d].Mb = tb.base + tb.off_Mb[d];
+    t1[d].Md = tb.base + tb.off_Md[d];
+    t1[d].Kb = tb.base + tb.off_Kb[d];
+    t1[d].C = tb.base + tb.off_C[d];
+    t1[d].n = tb.el[d] + G.p;
+  }
+  __syncthreads();
+  const int ne = G.el[0] * G.el[1] * G.el[2];
+  const double* Ks = Kel + (int64_t)li * ne * NF * NF;
+  const double sg = D.sigma[s] * inv_dt;
+  const int* aug = D.aug + D.aug_off[s];
+  double* out = D.A + D.a_off[s] + tri_off(I, J);
+  for (int e = threadIdx.x; e < TSZ; e += blockDim.x) {
+    const int r = e / TS, c = e % TS;
+    const int ga = aug[I * TS + r], gb = aug[J * TS + c];
+    double v;
+    if (ga < 0 || gb < 0) {
+      v = (I == J && r == c) ? 1.0 : 0.0;
+    } else {
+      const LocalDof A = decode_local(G, ga), B = decode_local(G, gb);
+      double Kl, M;
+      kron_entry(t1, A, B, Kl, M);
+      int e0[3], e1[3];
+      bool empty = false;
+      for (int d = 0; d < 3; ++d) {
+        const int a0 = max(0, A.i[d] - (d == A.c ? P - 1 : P)), b0 = max(0, B.i[d] - (d == B.c ? P - 1 : P));
+        e0[d] = max(a0, b0);
+        e1[d] = min(min(A.i[d], B.i[d]), G.el[d] - 1);
+        empty |= e0[d] > e1[d];
+      }
+      double K = 0.0;
+      if (!empty)
+        for (int ez = e0[2]; ez <= e1[2]; ++ez)
+          for (int ey = e0[1]; ey <= e1[1]; ++ey)
+            for (int ex = e0[0]; ex <= e1[0]; ++ex) {
+              const int la = E::loc(A.c, A.i[0] - ex, A.i[1] - ey, A.i[2] - ez);
+              const int lb = E::loc(B.c, B.i[0] - ex, B.i[1] - ey, B.i[2] - ez);
+              const int el = ex + G.el[0] * (ey + G.el[1] * ez);
+              K += __ldg(Ks + (int64_t)el * NF * NF + (int64_t)max(la, lb) * NF + min(la, lb));
+            }
+      v = K + sg * M;
+    }
+    out[e] = v;
+  }
+}
+
 // host-side dispatch on the spline degree (the Gauss-point loops unroll)
+// p <= 3: element matrices (Kel: nnl x elements x NF^2 doubles) then the tile gather; else the
+// per-entry Gauss-point kernel
+inline size_t nl_elem_doubles(int p, int nel) {
+  if (p < 1 || p > 3) return 0;
+  const size_t nf = 3 * (size_t)p * (p + 1) * (p + 1);
+  return (size_t)nel * nf * nf;
+}
 inline void launch_nl_assemble(int p, unsigned grid, size_t smem, cudaStream_t st, const DevPlan& D, const Tables1D& tb,
                                const Geom& G, const NlTab& T, double inv_dt, const int* nlist, const int64_t* tstart,
-                               int nnl, const double* Q) {
+                               int nnl, const double* Q, double* Kel = nullptr) {
+  if (Kel && p >= 1 && p <= 3) {
+    const unsigned ne = (unsigned)(G.el[0] * G.el[1] * G.el[2]);
+    switch (p) {
+#define NLE(PP)                                                                                  \
+  case PP:                                                                                       \
+    k_nl_elem<PP><<<dim3(ne, (unsigned)nnl), 256, NlElem<PP>::smem, st>>>(G, T, nlist, Q, Kel);  \
+    k_nl_gather<PP><<<grid, 256, 0, st>>>(D, tb, G, inv_dt, nlist, tstart, nnl, Kel);            \
+    break;
+      NLE(1) NLE(2) NLE(3)
+#undef NLE
+      default: break;
+    }
+    return;
+  }
   switch (p) {
 #define NLA(PP) \
   case PP: k_nl_assemble<PP><<<grid, 256, smem, st>>>(D, tb, G, T, inv_dt, nlist, tstart, nnl, Q); break;
@@ -335,6 +491,12 @@ inline cudaError_t nl_assemble_smem(size_t smem) {
                        (const void*)k_nl_assemble<7>};
   for (const void* f : fs) {
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const void* ef[3] = {(const void*)k_nl_elem<1>, (const void*)k_nl_elem<2>, (const void*)k_nl_elem<3>};
+  const size_t es[3] = {NlElem<1>::smem, NlElem<2>::smem, NlElem<3>::smem};
+  for (int i = 0; i < 3; ++i) {
+    cudaError_t e = cudaFuncSetAttribute(ef[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)es[i]);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
