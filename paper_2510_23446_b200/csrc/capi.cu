@@ -1593,7 +1593,7 @@ static tcg_status do_setup(tcg_ctx* h) {
         d.a_off = a_off[s]; d.vec_off = vec_off[s]; d.b_off = b_off[s]; d.p_off = p_off[s]; d.sbb_off = sbb_off[s];
         return d;
       };
-      ItemLists p1(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR), e1(NR), e5(NR);
+      ItemLists p1(NR), p1b(NR), p5(NR), sy(NR), pcv(NR), fw(NR), fwa(NR), bw(NR), bwc(NR), rhs(NR), e1(NR), e5(NR);
       const bool si = h->sbbinv;
       // whole-patch dealing when there are many patches per block (cfg5: 2048 patches)
       // (TCG_GROUP=1 forces it: the parity tests exercise the whole-patch items on small configs)
@@ -1604,6 +1604,11 @@ static tcg_status do_setup(tcg_ctx* h) {
       // with sbbinv: the Phi_b^T rows join the whole-patch S_bb^-1 item, one whole-patch Phi_b item
       // per patch in P5 (TCG_SI_MERGE=0: separate row / column items)
       const bool simerge = grp_syp && !(getenv("TCG_SI_MERGE") && atoi(getenv("TCG_SI_MERGE")) == 0);
+      // TCG_OVERLAP: the S_bb^-1 items leave P1 for their own list (PH_P1B) and run while their
+      // block waits for dependencies of the sparse coarse solve, which needs only P1's Phi_b^T
+      // rows (default: on where the coarse chain is latency-bound, i.e. without whole-patch dealing)
+      const bool ovl = si && h->sparse && (getenv("TCG_OVERLAP") ? atoi(getenv("TCG_OVERLAP")) != 0 : !grp);
+      const bool p1merge = simerge && !ovl;
       for (int s = 0; s < P; ++s) {
         const int r = owner[s];
         const int Trs = Ti[s] + Tb[s];
@@ -1624,7 +1629,7 @@ static tcg_status do_setup(tcg_ctx* h) {
         // split items (X_bb^T -> Y, Phi_b -> Y2) because the iteration writes Y2 every time
         for (int I = 0; I < Tb[s] + Tp[s]; ++I) {
           e1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
-          if (!si || (I >= Tb[s] && !(simerge && Tb[s] > 0))) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
+          if (!si || (I >= Tb[s] && !(p1merge && Tb[s] > 0))) p1.per_rank[r].push_back({I < Tb[s] ? I + 1 : Tb[s], desc(s, I)});
         }
         for (int J = 0; J < Tb[s]; ++J) {
           if (grp5 && np[s] > 0 && !si) {  // whole-patch dealing: one item per column (fewer item starts)
@@ -1651,13 +1656,13 @@ static tcg_status do_setup(tcg_ctx* h) {
         if (si && Tb[s] > 0) {  // the iteration's local half: y1 = S_bb^-1 v (ItemDesc part bit 3)
           if (grp_syp) {  // + the Phi_b^T rows on the same gathered input (part bit 2)
             ItemDesc d = desc(s, 0);
-            d.part = simerge ? (8 | 4 | 2) : (8 | 2);
-            p1.per_rank[r].push_back({Tb[s] * (Tb[s] + 1) / 2 + (simerge ? Tp[s] * Tb[s] : 0), d});
+            d.part = p1merge ? (8 | 4 | 2) : (8 | 2);
+            (ovl ? p1b : p1).per_rank[r].push_back({Tb[s] * (Tb[s] + 1) / 2 + (p1merge ? Tp[s] * Tb[s] : 0), d});
           } else {
             for (int I = 0; I < Tb[s]; ++I) {
               ItemDesc d = desc(s, I);
               d.part = 8;
-              p1.per_rank[r].push_back({Tb[s], d});
+              (ovl ? p1b : p1).per_rank[r].push_back({Tb[s], d});
             }
           }
         }
@@ -1702,6 +1707,7 @@ static tcg_status do_setup(tcg_ctx* h) {
         }
       // fixed per-item overhead (tile units) of the latency-bound item phases
       TRY(deal_items(h, p1, PH_P1, 2, grp));
+      TRY(deal_items(h, p1b, PH_P1B, 2, grp));
       TRY(deal_items(h, e1, PH_E1, 2, grp));
       TRY(deal_items(h, e5, PH_E5, 2, grp));
       TRY(deal_items(h, pcv, PH_PC, 2));
@@ -1764,7 +1770,7 @@ static tcg_status do_setup(tcg_ctx* h) {
       size_t max_bp = 0;
       for (int gb = 0; gb < NR * h->nbr; ++gb) {
         std::vector<int> pats;
-        for (int ph : {PH_P1, PH_P5, PH_SY})
+        for (int ph : {PH_P1, PH_P1B, PH_P5, PH_SY})
           for (int j = h->h_boff[ph][gb]; j < h->h_boff[ph][gb + 1]; ++j) pats.push_back(h->h_items[ph][j].s);
         std::sort(pats.begin(), pats.end());
         pats.erase(std::unique(pats.begin(), pats.end()), pats.end());
@@ -1780,7 +1786,7 @@ static tcg_status do_setup(tcg_ctx* h) {
       h->cache_bpos = allow && h->cache_items && (int64_t)(used2 + max_bp) <= budget && max_bp <= 48 * 1024;
       if (h->cache_bpos) {
         used2 += max_bp;
-        for (int ph : {PH_P1, PH_P5, PH_SY})
+        for (int ph : {PH_P1, PH_P1B, PH_P5, PH_SY})
           for (int gb = 0; gb < NR * h->nbr; ++gb)
             for (int j = h->h_boff[ph][gb]; j < h->h_boff[ph][gb + 1]; ++j) {
               ItemDesc& d = h->h_items[ph][j];

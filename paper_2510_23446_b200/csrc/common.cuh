@@ -56,9 +56,10 @@ struct BPos {
 // item phases of the stepper; the first NCACHE are the per-iteration ones (shared-memory cache)
 // PH_P1 / PH_P5 are the per-iteration F-apply halves; PH_E1 / PH_E5 the same halves in their
 // X_bb form for the per-step uses (R4 dual rhs, E1 recovery), which differ from PH_P1 / PH_P5
-// when the iteration applies the explicit S_bb^-1 (ItemDesc part bit 3, pcg.cu)
-enum { PH_P1 = 0, PH_PC, PH_P5, PH_SY, PH_FW, PH_FWA, PH_BW, PH_BWC, PH_RHS, PH_E1, PH_E5, NPH };
-constexpr int NCACHE = 4;
+// when the iteration applies the explicit S_bb^-1 (ItemDesc part bit 3, pcg.cu). PH_P1B holds the
+// S_bb^-1 items when they run under the sparse coarse solve's dependency waits (TCG_OVERLAP)
+enum { PH_P1 = 0, PH_PC, PH_P5, PH_SY, PH_P1B, PH_FW, PH_FWA, PH_BW, PH_BWC, PH_RHS, PH_E1, PH_E5, NPH };
+constexpr int NCACHE = 5;
 
 // Per-matrix descriptor for the batched tiled Cholesky (patches and the coarse matrix).
 struct CholDesc {

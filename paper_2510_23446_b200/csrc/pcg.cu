@@ -1069,6 +1069,37 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
   for (int j_##var = 0; j_##var < s_icnt[ph]; ++j_##var)    \
     if (const ItemDesc& var = s_ip[ph][j_##var]; true)
 
+// Side work of the F-apply's sparse coarse solve (TCG_OVERLAP): this block's PH_P1B items
+// (y1 = S_bb^-1 v into Y, src = P1's input v) run while the block waits for a coarse dependency;
+// *sum collects this thread's share of v . y1 in list order. An item that reuses the patch vector
+// gathered by the previous one (GAT 0) gathers again when a coarse item ran in between (the
+// scratch is shared).
+struct NoSide {
+  __device__ bool left() const { return false; }
+  __device__ void run() {}
+  __device__ void clobber() {}
+};
+template <class Src>
+struct SideWork {
+  Src src;
+  double* sum;
+  int j, n;
+  bool clob;
+  const ItemDesc* items;
+  const double* SI;
+  double* Y;
+  double* smw;
+  double* red;
+  __device__ bool left() const { return j < n; }
+  __device__ void clobber() { clob = true; }
+  __device__ void run() {
+    const ItemDesc& w = items[j++];
+    if ((w.part & 10) == 10) *sum += symv_patch(w, SI, Y, src, smw, nullptr, 0);
+    else *sum += symv_item(w, SI, Y, src, smw, red, nullptr, 0, clob || GAT(PH_P1B, w));
+    clob = false;
+  }
+};
+
 // =======================================================================================
 // Persistent cooperative time stepper: A.nsteps implicit-Euler steps in one launch, over
 // all ranks of the job. Control flow depends only on values every block of every rank
@@ -1268,7 +1299,15 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
   // the waits always end. Counters are monotone within a launch (zeroed before it): target =
   // solves so far x item count.
   unsigned int cuse = 0;  // coarse solves in this launch (uniform)
-  auto cwait = [&](const unsigned int* c, unsigned int target) {
+  // (side: work of this block that does not depend on the coarse solve, the S_bb^-1 items of
+  // PH_P1B. While the awaited counter is short of its target the block runs one side item and
+  // polls again; with none left it spins as before. Item order within the side list is fixed, so
+  // the sums they return do not depend on the interleaving.)
+  auto cwait = [&](const unsigned int* c, unsigned int target, auto& side) {
+    while (side.left()) {
+      if (__syncthreads_or(threadIdx.x == 0 && (int)(ld_acquire_u32(c, 0) - target) >= 0)) return;
+      side.run();
+    }
     if (threadIdx.x == 0) {
       const unsigned long long t0 = gtimer();
       while ((int)(ld_acquire_u32(c, 0) - target) < 0)
@@ -1276,7 +1315,7 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
     }
     __syncthreads();
   };
-  auto coarse_sparse = [&](auto gsrc) {
+  auto coarse_sparse = [&](auto gsrc, auto& side) {
     cstamp(0);
     ++cuse;
     const int nn = A.cf_nn;
@@ -1288,7 +1327,8 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       for (int j = b; j < e; ++j) {
         const ItemDesc& it = A.cf_fw[j];
         const int4 nd = A.cf_node[it.s];
-        if (!A.cf_sync && nd.w > 0) cwait(kd + it.s, cuse * (unsigned int)nd.w);
+        if (!A.cf_sync && nd.w > 0) cwait(kd + it.s, cuse * (unsigned int)nd.w, side);
+        side.clobber();
         fwc_item(it, A.FR, A.cf_prog, A.cf_kw, gsrc, A.CW[me], A.cf_pb[me], A.cf_cnt[me], smw);
         if (!A.cf_sync && threadIdx.x == 0) {  // fwc_item ended with __syncthreads
           __threadfence();
@@ -1305,9 +1345,10 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         const ItemDesc& it = A.cf_bw[j];
         if (!A.cf_sync) {  // x_B from the ancestors, y_V from x's own forward rows
           const int2 dp = A.cf_bwdep[it.s];
-          if (dp.x >= 0) cwait(bd + dp.x, cuse * (unsigned int)dp.y);
-          cwait(fd + it.s, cuse * (unsigned int)A.cf_node[it.s].y);
+          if (dp.x >= 0) cwait(bd + dp.x, cuse * (unsigned int)dp.y, side);
+          cwait(fd + it.s, cuse * (unsigned int)A.cf_node[it.s].y, side);
         }
+        side.clobber();
         bwc_item(it, A.FR, A.CW[me], A.cf_vl, A.cf_bl, A.Pcs[me], A.cf_pb[me], A.cf_cnt[me], smw, A.scratch / TS - 9);
         if (!A.cf_sync && threadIdx.x == 0) {
           __threadfence();
@@ -1318,13 +1359,22 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       cstamp(2 * A.cf_levels - lv);
     }
     ++cstamp_call;
+    if (side.left()) {  // the rest of the side items (the last coarse item may still read smw)
+      __syncthreads();
+      while (side.left()) side.run();
+    }
   };
-#define COARSE(GS)                \
+  NoSide no_side;
+  auto make_side = [&](auto vsrc, double* sum) {
+    return SideWork<decltype(vsrc)>{vsrc, sum, 0, s_icnt[PH_P1B], true, s_ip[PH_P1B], SIr, A.Y[me], smw, red};
+  };
+#define COARSE2(GS, SIDE)         \
   if (A.sparse) {                 \
-    coarse_sparse(GS);            \
+    coarse_sparse(GS, SIDE);      \
   } else {                        \
     PC_PHASE(GS);                 \
   }
+#define COARSE(GS) COARSE2(GS, no_side)
   // ---- mode 1: the dual operator alone, q = F p, A.nsteps times (F-apply benchmark / test) ----
   for (int rep = 0; A.mode == 1 && rep < A.nsteps; ++rep) {
     const int step = -1, it = -1;  // no stamps
@@ -1340,9 +1390,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         else if (w.part & 8) symv_item(w, SIr, A.Y[me], vsrc, smw, red, PF0(j_w), GAT(PH_P1, w));
         else p1_item(w, Xr, vsrc, A.XW[me], smw, PF0(j_w), GAT(PH_P1, w));
       }
+      bar(PH_PC, false, 0.0);
+      double unused = 0.0;
+      auto side = make_side(vsrc, &unused);
+      COARSE2(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }), side);
     }
-    bar(PH_PC, false, 0.0);
-    COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
     bar(PH_P5, false, 0.0);
     FOR_ITEMS(PH_P5, w) {
       auto zero = [&](const ItemDesc&, int64_t, int) { return 0.0; };
@@ -1549,6 +1601,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       // P1: p = z + beta p_prev on the fly; v = B^T p; w = X_bb v, -g = -Phi^T v; owners store p
       // (sbbinv: y1 = S_bb^-1 v -> Y instead of w, and its share v . y1 of p^T F p -> loc1)
       double loc1 = 0.0;
+      auto vnew = [&](const ItemDesc& iw, int64_t bb, int pos) {
+        const BPos q = bget(iw, bb, pos);
+        return q.aown * ldcg(A.PW[me] + own_idx(iw, pos)) + q.apart * ldcg(A.PW[pown(ppatch(bb))] + q.part) +
+               q.sign * beta * ldcg(pprev[lown(q.k)] + q.k);
+      };
       {
         // the block's own lambda chunk first (independent loads in flight before the items)
         double pv = 0.0;
@@ -1556,11 +1613,6 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
         if (kq < k1)
           pv = lw_p(kq) * ldcg(A.PW[pown(lpat_p(kq))] + lidx_p(kq)) -
                lw_m(kq) * ldcg(A.PW[pown(lpat_m(kq))] + lidx_m(kq)) + beta * ldcg(pprev[me] + kq);
-        auto vnew = [&](const ItemDesc& iw, int64_t bb, int pos) {
-          const BPos q = bget(iw, bb, pos);
-          return q.aown * ldcg(A.PW[me] + own_idx(iw, pos)) + q.apart * ldcg(A.PW[pown(ppatch(bb))] + q.part) +
-                 q.sign * beta * ldcg(pprev[lown(q.k)] + q.k);
-        };
         FOR_ITEMS(PH_P1, w) {
           ITIME_BEGIN
           if ((w.part & 10) == 10) loc1 += symv_patch(w, SIr, A.Y[me], vnew, smw, PF0(j_w), Xr, A.XW[me]);
@@ -1576,8 +1628,11 @@ __global__ void __launch_bounds__(NTHR, 2) k_steps(DevPlan D, StepArgs A) {
       WSTAMP(0);
       bar(PH_PC, false, 0.0);
       TSTAMP(1);
-      // PC
-      COARSE(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }));
+      // PC (the PH_P1B items, if any, run under its dependency waits)
+      {
+        auto side = make_side(vnew, &loc1);
+        COARSE2(([&](int64_t i, int o) { return ldcg(A.XW[MULTI ? o : 0] + i); }), side);
+      }
       WSTAMP(1);
       bar(PH_P5, false, 0.0);
       TSTAMP(2);

@@ -161,6 +161,35 @@ def test_whole_patch_items_cfg2_match_golden(tcg, monkeypatch, vranks, sbbinv):
     assert np.all(np.abs(np.asarray(it, dtype=np.int64) - g["iters"].astype(np.int64)) <= 1), (list(it), list(g["iters"]))
 
 
+@pytest.mark.parametrize("vranks,group,overlap", [(1, 0, 1), (1, 1, 1), (2, 0, 1), (3, 1, 1), (1, 0, 0)])
+def test_overlap_items_cfg2_match_golden(tcg, monkeypatch, vranks, group, overlap):
+    """S_bb^-1 items run under the sparse coarse solve's dependency waits (PH_P1B side work,
+    TCG_OVERLAP; the default of cfg4), forced on cfg2 with the sparse coarse and the explicit
+    S_bb^-1, row items or whole-patch items, all 50 steps against the oracle's golden file;
+    overlap = 0 is the same configuration with the items back in P1."""
+    monkeypatch.setenv("TCG_COARSE", "sparse")
+    monkeypatch.setenv("TCG_SBBINV", "1")
+    monkeypatch.setenv("TCG_OVERLAP", str(overlap))
+    monkeypatch.setenv("TCG_GROUP", str(group))
+    g, meta = _golden("cfg2")
+    pr = workloads.get("cfg2")
+    s = tcg.Solver()
+    if vranks > 1:
+        s.set_virtual_ranks(vranks)
+    s.configure(pr)
+    s.setup()
+    s.step(int(meta["steps"]))
+    a = s.coefficients(1)
+    it = s.history()[0]
+    inf = s.info()
+    s.close()
+    assert inf["coarse_sparse"] == 1
+    ref = g["a1"]
+    err = float(np.linalg.norm(a - ref) / np.linalg.norm(ref))
+    assert err <= TOL, err
+    assert np.all(np.abs(np.asarray(it, dtype=np.int64) - g["iters"].astype(np.int64)) <= 1), (list(it), list(g["iters"]))
+
+
 @pytest.mark.parametrize("name", ["cfg2", "cfg3"])
 def test_sbbinv_off_and_on_match_golden(tcg, monkeypatch, name):
     """The PCG iteration with the explicit S_bb^-1 forced on (cfg2, where the default is the

@@ -326,6 +326,28 @@ def test_sparse_coarse_cfg2_steps_and_F(tcg, sparse_coarse):
     assert np.linalg.norm(q - ref) / np.linalg.norm(ref) <= 1e-11
 
 
+@pytest.mark.parametrize("group", [0, 1])
+def test_overlap_side_items_small_cases_and_F(tcg, sparse_coarse, monkeypatch, group):
+    """The S_bb^-1 items as side work of the sparse coarse solve (PH_P1B, TCG_OVERLAP=1) with the
+    explicit S_bb^-1 forced on: small cases end to end and the isolated F-apply against the oracle."""
+    monkeypatch.setenv("TCG_SBBINV", "1")
+    monkeypatch.setenv("TCG_OVERLAP", "1")
+    monkeypatch.setenv("TCG_GROUP", str(group))
+    compare(tcg, workloads.cfg1())
+    for name in ("contrast", "p3-ragged-tiles"):
+        compare(tcg, next(p for p in SMALL if p.name == name))
+    o = Oracle(workloads.cfg2())
+    lam = np.random.default_rng(5).standard_normal(o.part.m)
+    s = tcg.Solver().configure(workloads.cfg2())
+    s.setup()
+    q = s.apply_F(lam)
+    q2 = s.apply_F(lam)
+    s.close()
+    ref = o.F(lam)
+    assert np.linalg.norm(q - ref) / np.linalg.norm(ref) <= 1e-11
+    assert np.array_equal(q, q2)
+
+
 def test_sparse_vs_dense_coarse_cfg4(tcg, monkeypatch):
     """cfg4 (n_c ~ 15.7k, sparse by default) against the dense S_pp^-1 path, first 2 steps."""
     pr = workloads.cfg4()
