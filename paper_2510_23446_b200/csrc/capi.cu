@@ -236,6 +236,8 @@ struct tcg_ctx {
   // the PCG iteration applies W_rr^-1 restricted to b as the explicit S_bb^-1 = X_bb^T X_bb
   // (one symmetric read) instead of X_bb^T (X_bb v) (two reads); TCG_SBBINV=0 restores the latter
   bool sbbinv = true;
+  bool ovl = false;     // S_bb^-1 items as side work of the sparse coarse solve (TCG_OVERLAP)
+  int ovl_chain = 0;    // blocks that run the coarse levels above the leaves and take no side items
   // local factorisation order: left-looking (deep-K column updates, default) or right-looking
   // (TCG_CHOL=right)
   bool chol_left = true;
@@ -811,7 +813,7 @@ struct ItemLists {
   explicit ItemLists(int nr) : per_rank(nr) {}
 };
 
-static tcg_status deal_items(tcg_ctx* h, ItemLists& L, int ph, int overhead, bool group = false) {
+static tcg_status deal_items(tcg_ctx* h, ItemLists& L, int ph, int overhead, bool group = false, int skip_first = 0) {
   const int nbr = h->nbr;
   auto bycost = [](const std::pair<int, ItemDesc>& x, const std::pair<int, ItemDesc>& y) {
     return x.first != y.first ? x.first > y.first
@@ -823,7 +825,7 @@ static tcg_status deal_items(tcg_ctx* h, ItemLists& L, int ph, int overhead, boo
     std::stable_sort(v.begin(), v.end(), bycost);
     std::vector<std::vector<ItemDesc>> blk(nbr);
     std::vector<std::pair<int64_t, int>> heap;  // (load, block) min-heap
-    for (int b = 0; b < nbr; ++b) heap.push_back({0, b});
+    for (int b = 0; b < nbr; ++b) heap.push_back({b < skip_first ? ((int64_t)1 << 50) : 0, b});  // the first skip_first blocks get nothing
     auto cmp = [](const std::pair<int64_t, int>& x, const std::pair<int64_t, int>& y) { return x > y; };
     std::make_heap(heap.begin(), heap.end(), cmp);
     if (group) {
@@ -1116,7 +1118,9 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
           for (int J = 0; J < N[x].TV; ++J) lvl_tiles += N[x].T - J;
         }
       }
-      const int cw = (int)std::max<int64_t>(4, std::min<int64_t>(64, (lvl_tiles + nb2 - 1) / nb2));
+      // (overlap with chain blocks: the levels above the leaves go to the first ovl_chain blocks)
+      const int nbl = (lv > 0 && h->ovl_chain > 0) ? h->ovl_chain : nb2;
+      const int cw = (int)std::max<int64_t>(4, std::min<int64_t>(64, (lvl_tiles + nbl - 1) / nbl));
       std::vector<std::pair<int, ItemDesc>> items;
       for (int x : g.lvl[lv]) {
         ItemDesc d{};
@@ -1170,7 +1174,7 @@ static tcg_status setup_sparse_coarse(tcg_ctx* h, const std::vector<int>& owner,
       });
       std::vector<std::vector<ItemDesc>> blk(nb2);
       std::vector<std::pair<int64_t, int>> heap;
-      for (int b = 0; b < nb2; ++b) heap.push_back({0, b});
+      for (int b = 0; b < nbl; ++b) heap.push_back({0, b});
       auto cmp = [](const std::pair<int64_t, int>& a, const std::pair<int64_t, int>& b) { return a > b; };
       std::make_heap(heap.begin(), heap.end(), cmp);
       for (auto& e : items) {
@@ -1574,6 +1578,22 @@ static tcg_status do_setup(tcg_ctx* h) {
     const char* ce = getenv("TCG_COARSE");  // "dense", "sparse", default auto
     const bool want = ce ? (std::strcmp(ce, "sparse") == 0) : (pl.nc > 8192);
     h->sparse = (want && pl.nc > 0) ? 1 : 0;  // several ranks: every rank runs the whole solve
+    // TCG_OVERLAP: the S_bb^-1 items leave P1 for their own list (PH_P1B) and run while their
+    // block waits for dependencies of the sparse coarse solve, which needs only P1's Phi_b^T
+    // rows (default: on where the coarse chain is latency-bound, i.e. without whole-patch dealing).
+    // TCG_OVL_CHAIN=k: the levels above the leaves are dealt to the first k blocks of a rank,
+    // which take no side items, so the dependent chain is not delayed by them.
+    {
+      const bool grp0 = ((int64_t)P >= 2 * (int64_t)NR * h->nbr || (getenv("TCG_GROUP") && atoi(getenv("TCG_GROUP")))) &&
+                        !(getenv("TCG_NO_GROUP") && atoi(getenv("TCG_NO_GROUP")));
+      h->ovl = h->sbbinv && h->sparse && (getenv("TCG_OVERLAP") ? atoi(getenv("TCG_OVERLAP")) != 0 : !grp0);
+      const char* ce2 = getenv("TCG_OVL_CHAIN");
+      // default with row items: 0.54 of the blocks (cfg4 sweep over k = 0 .. 280 of 296 blocks:
+      // 89.8, 64.6 (24), 79.1 (48), 91.4 (96), 95.1 (160), 89.6 (192), 80.0 (224) steps/s;
+      // profiles/round2_ab_overlap.txt); whole-patch side items (forced overlap): none
+      const int kdef = grp0 ? 0 : (int)(0.54 * h->nbr + 0.5);
+      h->ovl_chain = h->ovl ? std::max(0, std::min(h->nbr - 1, ce2 ? atoi(ce2) : kdef)) : 0;
+    }
   }
   // ---- work items per rank, dealt to the rank's persistent blocks (LPT) ----
   std::vector<int> crow_owner(std::max(Tc, 1));
@@ -1604,10 +1624,8 @@ static tcg_status do_setup(tcg_ctx* h) {
       // with sbbinv: the Phi_b^T rows join the whole-patch S_bb^-1 item, one whole-patch Phi_b item
       // per patch in P5 (TCG_SI_MERGE=0: separate row / column items)
       const bool simerge = grp_syp && !(getenv("TCG_SI_MERGE") && atoi(getenv("TCG_SI_MERGE")) == 0);
-      // TCG_OVERLAP: the S_bb^-1 items leave P1 for their own list (PH_P1B) and run while their
-      // block waits for dependencies of the sparse coarse solve, which needs only P1's Phi_b^T
-      // rows (default: on where the coarse chain is latency-bound, i.e. without whole-patch dealing)
-      const bool ovl = si && h->sparse && (getenv("TCG_OVERLAP") ? atoi(getenv("TCG_OVERLAP")) != 0 : !grp);
+      // (h->ovl: the S_bb^-1 items go to PH_P1B, side work of the sparse coarse solve)
+      const bool ovl = h->ovl;
       const bool p1merge = simerge && !ovl;
       for (int s = 0; s < P; ++s) {
         const int r = owner[s];
@@ -1707,7 +1725,7 @@ static tcg_status do_setup(tcg_ctx* h) {
         }
       // fixed per-item overhead (tile units) of the latency-bound item phases
       TRY(deal_items(h, p1, PH_P1, 2, grp));
-      TRY(deal_items(h, p1b, PH_P1B, 2, grp));
+      TRY(deal_items(h, p1b, PH_P1B, 2, grp, h->ovl_chain));
       TRY(deal_items(h, e1, PH_E1, 2, grp));
       TRY(deal_items(h, e5, PH_E5, 2, grp));
       TRY(deal_items(h, pcv, PH_PC, 2));

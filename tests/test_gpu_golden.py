@@ -161,12 +161,16 @@ def test_whole_patch_items_cfg2_match_golden(tcg, monkeypatch, vranks, sbbinv):
     assert np.all(np.abs(np.asarray(it, dtype=np.int64) - g["iters"].astype(np.int64)) <= 1), (list(it), list(g["iters"]))
 
 
-@pytest.mark.parametrize("vranks,group,overlap", [(1, 0, 1), (1, 1, 1), (2, 0, 1), (3, 1, 1), (1, 0, 0)])
-def test_overlap_items_cfg2_match_golden(tcg, monkeypatch, vranks, group, overlap):
+@pytest.mark.parametrize("vranks,group,overlap,chain", [(1, 0, 1, 0), (1, 1, 1, 0), (2, 0, 1, 0), (3, 1, 1, 0), (1, 0, 0, 0),
+                                                        (1, 0, 1, 24), (2, 1, 1, 16)])
+def test_overlap_items_cfg2_match_golden(tcg, monkeypatch, vranks, group, overlap, chain):
     """S_bb^-1 items run under the sparse coarse solve's dependency waits (PH_P1B side work,
     TCG_OVERLAP; the default of cfg4), forced on cfg2 with the sparse coarse and the explicit
     S_bb^-1, row items or whole-patch items, all 50 steps against the oracle's golden file;
-    overlap = 0 is the same configuration with the items back in P1."""
+    overlap = 0 is the same configuration with the items back in P1; chain > 0 deals the coarse
+    levels above the leaves to the first `chain` blocks of a rank, which take no side items
+    (TCG_OVL_CHAIN)."""
+    monkeypatch.setenv("TCG_OVL_CHAIN", str(chain))
     monkeypatch.setenv("TCG_COARSE", "sparse")
     monkeypatch.setenv("TCG_SBBINV", "1")
     monkeypatch.setenv("TCG_OVERLAP", str(overlap))

@@ -1,0 +1,18 @@
+#!/bin/bash
+# second sweep of TCG_OVL_CHAIN on cfg4 (and cfg3-size check that nothing else moved)
+mkdir -p gpurun_out
+rm -f gpurun_out/ab_ovl3.txt
+run() {  # config, env...
+  c=$1; shift
+  echo "== $* $c" >> gpurun_out/ab_ovl3.txt
+  env "$@" timeout 300 python bench.py --config $c --no-cpu-baseline --no-extras --e2e-steps 0 --steps 3 --warmup 3 2>/dev/null | python -c "
+import json,sys
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print('value', round(d['value'],2), 'iters/step', d['pcg_iters_per_step'], 'fapply_us', round(d['fapply']['us_per_apply'],1), 'k_steps_frac', round(d['roofline']['frac'],3), 'clk', d['clocks']['sm_mhz'])
+" >> gpurun_out/ab_ovl3.txt
+}
+for rep in 1 2; do
+  run cfg4 TCG_OVERLAP=0
+  for k in 160 192 224 256 280; do run cfg4 TCG_OVERLAP=1 TCG_OVL_CHAIN=$k; done
+done
