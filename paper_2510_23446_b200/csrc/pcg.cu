@@ -453,7 +453,7 @@ __device__ __forceinline__ double p5_item(const ItemDesc& it, const double* Xr, 
 // over the column block, then over the 8 warps in warp order): deterministic. One
 // __syncthreads per column block (double-buffered warp partials).
 template <class Src>
-__device__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm,
+__device__ __forceinline__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, Src usrc, double* sm,
                              const double* pft, int npf, const double* Xr = nullptr, double* XW = nullptr) {
   const int Ti = it.Ti, Tb = it.Tb, nb = it.nb;
   double* u = sm;             // Tb*64 input
@@ -566,7 +566,7 @@ __device__ double symv_patch(const ItemDesc& it, const double* Sr, double* PW, S
 // no block barrier per column (fixed row order: deterministic). Returns this thread's share of
 // v . y2 (vsrc gives v = (B_s^T p)_pos).
 template <class PcF, class Src>
-__device__ double p5_phi_patch(const ItemDesc& it, const double* Xr, const int* p_grp, PcF pc, Src vsrc, double* Y2,
+__device__ __forceinline__ double p5_phi_patch(const ItemDesc& it, const double* Xr, const int* p_grp, PcF pc, Src vsrc, double* Y2,
                                double* sm) {
   const int Ti = it.Ti, Tb = it.Tb, Tp = it.Tp, np = it.np, nb = it.nb;
   double* g = sm;  // Tp*64: -(N Pc) on the patch's primal rows
@@ -897,7 +897,7 @@ struct NoHook {
 // hook(): run by thread 0 right after this block's arrival, before it waits (used to issue the
 // bulk copies of the next phase's first tiles so they stream in during the wait)
 template <class Hook = NoHook>
-__device__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& round, bool reduce, double value,
+__device__ __forceinline__ double grid_barrier(const StepArgs& A, int me, int bl, unsigned int& round, bool reduce, double value,
                                double* bcast, Hook hook = Hook()) {
   __shared__ int s_leader;
   __syncthreads();
@@ -1075,9 +1075,9 @@ __device__ __forceinline__ void rhs_item(const DevPlan& D, const StepArgs& A, in
 // gathered by the previous one (GAT 0) gathers again when a coarse item ran in between (the
 // scratch is shared).
 struct NoSide {
-  __device__ bool left() const { return false; }
-  __device__ void run() {}
-  __device__ void clobber() {}
+  __device__ __forceinline__ bool left() const { return false; }
+  __device__ __forceinline__ void run() {}
+  __device__ __forceinline__ void clobber() {}
 };
 template <class Src>
 struct SideWork {
@@ -1090,9 +1090,11 @@ struct SideWork {
   double* Y;
   double* smw;
   double* red;
-  __device__ bool left() const { return j < n; }
-  __device__ void clobber() { clob = true; }
-  __device__ void run() {
+  // (force-inlined with symv_patch: an out-of-line call would take the address of the kernel's
+  // parameter block through src's captures and cost a 3.6 KB local copy per thread)
+  __device__ __forceinline__ bool left() const { return j < n; }
+  __device__ __forceinline__ void clobber() { clob = true; }
+  __device__ __forceinline__ void run() {
     const ItemDesc& w = items[j++];
     if ((w.part & 10) == 10) *sum += symv_patch(w, SI, Y, src, smw, nullptr, 0);
     else *sum += symv_item(w, SI, Y, src, smw, red, nullptr, 0, clob || GAT(PH_P1B, w));
